@@ -1,0 +1,146 @@
+/*
+ * fedsim_b200.h -- C ABI of the B200 (sm_100a) central-iteration kernels.
+ *
+ * One shared library, libfedsim_b200.so, loaded by the Python host side
+ * with ctypes (paper_2404_06430_b200/native.py).  Every entry point is a
+ * batched-cohort replacement for a per-user reference function; the
+ * reference function each one replaces is cited beside it
+ * (paths relative to /root/reference/pkg/src/).
+ *
+ * Conventions
+ *   - Every pointer argument is a caller-owned, contiguous DEVICE buffer
+ *     (fp32 unless the type says otherwise) except where marked [host].
+ *   - Every call is asynchronous on the given stream (a cudaStream_t passed
+ *     as void*; NULL = legacy default stream) and never synchronises.
+ *   - No hidden allocations: scratch comes from the caller, sized with the
+ *     matching *_workspace_bytes query.
+ *   - Return 0 (FB_OK) or a negative FB_ERR_* code; fb_last_error() returns
+ *     a thread-local message describing the last failure on this thread.
+ *   - Parameter vectors are flat in the model's entry order
+ *     (paper_2404_06430_b200/models.py), the payload order of the
+ *     reference's Statistics (fedsim/core/statistics.py:97-101).
+ *   - A cohort is described by per-client arrays over a packed dataset:
+ *       row_start[c] (int64)  first row of client c in X / y
+ *       num_rows[c]  (int32)  n_c >= 1
+ *       perm_off[c]  (int64)  first entry of client c in perms
+ *       perms        (int32)  epochs * n_c local row indices per client,
+ *                             epoch-major: batch j of epoch e is
+ *                             perms[perm_off[c] + e*n_c + j*B ...]
+ *                             (fedsim/models/kernels.py:46-50)
+ *   - Local SGD writes delta_out[c*ld + i] = theta_t[i] - theta_c[i]
+ *     (unweighted; fedsim/models/params.py:32-45 before weighting).
+ */
+#ifndef FEDSIM_B200_H
+#define FEDSIM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FB_OK 0
+#define FB_ERR_ARG (-1)         /* invalid argument (reference: ValueError)   */
+#define FB_ERR_CUDA (-2)        /* CUDA runtime / launch failure              */
+#define FB_ERR_UNSUPPORTED (-3) /* shape outside what the kernels implement   */
+
+#define FB_ABI_VERSION 1
+
+int fb_abi_version(void);
+const char* fb_last_error(void);
+/* [host] writes the device's SM count and L2 bytes; 0 on success. */
+int fb_device_info(int device, int* sm_count, int64_t* l2_bytes);
+
+/* ---------------------------------------------------------------- a4 eval
+ * Per-client summed cross-entropy and correct count at the shared theta,
+ * over all of the client's rows.  Replaces fedsim/models/kernels.py:70-83
+ * (_logistic_eval) and :123-136 (_mlp_eval) via evaluate_model
+ * (fedsim/models/models.py:275-296), batched over the cohort.
+ * loss_sum[c] += ..., correct[c] += ... are OVERWRITTEN (not accumulated).
+ * Argmax takes the first maximal logit (numpy.argmax).                     */
+int fb_eval_linear_f32(const float* theta, int dim, int num_classes,
+                       const float* X, const int32_t* y,
+                       const int64_t* row_start, const int32_t* num_rows, int num_clients,
+                       double* loss_sum, int32_t* correct, void* stream);
+int fb_eval_mlp_f32(const float* theta, int dim, int hidden, int num_classes,
+                    const float* X, const int32_t* y,
+                    const int64_t* row_start, const int32_t* num_rows, int num_clients,
+                    double* loss_sum, int32_t* correct, void* stream);
+
+/* --------------------------------------------------------- a5 local SGD
+ * E epochs of minibatch SGD from theta_t for every client at once; batch
+ * gradients are means over the ACTUAL batch size (tail batch kept), update
+ * theta <- theta - lr*(g + prox_mu*(theta - theta_t) + control).
+ * control may be NULL (zero) or [num_clients, ld_control] (ld 0 = one
+ * vector shared by all clients).  nonfinite[c] is set to 1 if client c's
+ * delta contains a non-finite value, else 0.
+ * Replaces fedsim/models/kernels.py:38-67 (_logistic_fit) and :86-120
+ * (_mlp_fit) driven by local_train_sgd (fedsim/models/models.py:231-264).  */
+int fb_local_sgd_linear_f32(const float* theta_t, int dim, int num_classes,
+                            const float* X, const int32_t* y,
+                            const int64_t* row_start, const int32_t* num_rows,
+                            const int32_t* perms, const int64_t* perm_off, int num_clients,
+                            int epochs, int batch_size, float lr, float prox_mu,
+                            const float* control, int64_t ld_control,
+                            float* delta_out, int64_t ld_delta, int32_t* nonfinite,
+                            void* stream);
+int fb_local_sgd_mlp_f32(const float* theta_t, int dim, int hidden, int num_classes,
+                         const float* X, const int32_t* y,
+                         const int64_t* row_start, const int32_t* num_rows,
+                         const int32_t* perms, const int64_t* perm_off, int num_clients,
+                         int epochs, int batch_size, float lr, float prox_mu,
+                         const float* control, int64_t ld_control,
+                         float* delta_out, int64_t ld_delta, int32_t* nonfinite,
+                         void* stream);
+
+/* ------------------------------------------------- a6 + a7 (kernel K2)
+ * For every client c: norm[c] = || w[c] * delta[c, :D] ||_2 (fp64
+ * accumulation), clipped[c] = norm[c] > bound (strict), coef[c] =
+ * w[c] * (clipped ? bound / norm : 1), nonfinite[c] = !isfinite(norm).
+ * Replaces model_update_delta -> weighted (fedsim/models/params.py:32-45,
+ * fedsim/core/statistics.py:124-136) followed by clip_norm
+ * (fedsim/privacy/clipping.py:37-56) over the payload entries.
+ * bound <= 0 disables clipping (coef = w, clipped = 0).                   */
+int64_t fb_clip_workspace_bytes(int num_clients, int64_t D);
+int fb_delta_norm_clip_f32(const float* delta, int64_t ld_delta, int num_clients, int64_t D,
+                           const float* w, double bound,
+                           double* norm, float* coef, int32_t* clipped, int32_t* nonfinite,
+                           void* workspace, int64_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------- a8 (kernel K3)
+ * agg[i] (+)= sum_c coef[c] * delta[c*ld + i], fp64 accumulation per
+ * element; accumulate = 0 overwrites agg, 1 adds into it.
+ * Replaces SumAggregator.accumulate (fedsim/engine/aggregator.py:39-44,
+ * fedsim/core/statistics.py:96-102) over a worker's queue.                 */
+int64_t fb_weighted_sum_workspace_bytes(int num_clients, int64_t D);
+int fb_weighted_sum_f32(const float* delta, int64_t ld_delta, int num_clients, int64_t D,
+                        const float* coef, float* agg, int accumulate,
+                        void* workspace, int64_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------- a10 helpers (K4 SNR)
+ * out[0] = sum_i x[i]^2 in fp64 (OVERWRITTEN).  workspace >= 8 KiB.         */
+int fb_sumsq_f32(const float* x, int64_t n, double* out, void* workspace,
+                 int64_t workspace_bytes, void* stream);
+
+/* Counter-based Gaussian: out[i] (+)= std * N(0,1) from Philox4x32-10 keyed
+ * by seed, counter = offset + i.  accumulate = 0 overwrites.               */
+int fb_gaussian_f32(float* out, int64_t n, double std, uint64_t seed, uint64_t offset,
+                    int accumulate, void* stream);
+
+/* ------------------------------------------ a10 + a12 (kernels K4 + K5)
+ * theta[i] -= lr * inv_weight * (agg[i] + noise_i) where noise_i is
+ *   injected[i]                          if injected != NULL (parity runs),
+ *   noise_std * Philox-normal(seed, i)   otherwise (0 if noise_std == 0).
+ * Replaces _add_noise (fedsim/privacy/mechanisms.py:58-75) + average
+ * (fedsim/core/statistics.py:105-113) + SGDOptimizer.step / apply_delta
+ * (fedsim/models/optimizers.py:13-21, fedsim/models/params.py:48-53).
+ * If agg_out != NULL the noised aggregate is also written there.           */
+int fb_noise_avg_sgd_f32(float* theta, const float* agg, int64_t D,
+                         double noise_std, uint64_t seed, const float* injected,
+                         double inv_weight, double lr, float* agg_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FEDSIM_B200_H */

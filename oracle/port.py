@@ -1,0 +1,424 @@
+"""Float64 numpy restatement of the reference central iteration.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  Every function cites
+the reference code it restates; paths are relative to
+/root/reference/pkg/src/.  Self-contained: numpy + hashlib only, so it can
+check the product without sharing its code.
+"""
+
+from __future__ import annotations
+
+import hashlib
+from dataclasses import dataclass, field
+
+import numpy as np
+
+# ------------------------------------------------------------------ seeds
+# fedsim/core/seeds.py:18-42
+
+
+def derive_seed(*parts) -> int:
+    h = hashlib.sha256()
+    for p in parts:
+        h.update(repr(p).encode())
+        h.update(b"\x1f")
+    return int.from_bytes(h.digest()[:8], "little") & ((1 << 63) - 1)
+
+
+def user_seed(ctx_seed: int, uid: str) -> int:
+    return derive_seed(ctx_seed, "user", uid)
+
+
+def cohort_seed(run_seed: int, t: int, pop: str) -> int:
+    return derive_seed(run_seed, "cohort", t, pop)
+
+
+def noise_seed(base: int, t: int, pop: str) -> int:
+    return derive_seed(base, "noise", t, pop)
+
+
+# --------------------------------------------------------------- sampling
+# fedsim/feddata/sampling.py:25-34 (fixed mode)
+
+
+def sample_cohort(user_ids, cohort_size: int, seed: int) -> tuple:
+    picks = np.random.default_rng(seed).choice(len(user_ids), size=cohort_size, replace=False)
+    return tuple(user_ids[i] for i in picks)
+
+
+# fedsim/engine/scheduling.py:34-78
+
+
+def lower_median(ws) -> float:
+    s = sorted(ws)
+    return float(s[(len(s) - 1) // 2])
+
+
+def lpt_queues(weights: dict, m: int, base: float):
+    order = sorted(weights.items(), key=lambda kv: (-kv[1], kv[0]))
+    queues = [[] for _ in range(m)]
+    loads = [0.0] * m
+    for uid, w in order:
+        k = min(range(m), key=loads.__getitem__)
+        queues[k].append(uid)
+        loads[k] += w + base
+    return [tuple(q) for q in queues], loads
+
+
+# fedsim/models/models.py:231-264
+
+
+def user_perms(ctx_seed: int, uid: str, n: int, epochs: int) -> np.ndarray:
+    rng = np.random.default_rng(user_seed(ctx_seed, uid))
+    return np.stack([rng.permutation(n) for _ in range(epochs)]).astype(np.int64)
+
+
+# ---------------------------------------------------------------- models
+
+
+def _xent(logits: np.ndarray, y: np.ndarray):
+    """Mean CE and d(mean CE)/dlogits (fedsim/models/models.py:115-124)."""
+    n = logits.shape[0]
+    z = logits - logits.max(axis=1, keepdims=True)
+    p = np.exp(z)
+    p /= p.sum(axis=1, keepdims=True)
+    loss = -np.mean(np.log(p[np.arange(n), y]))
+    p[np.arange(n), y] -= 1.0
+    return float(loss), p / n
+
+
+def _eval_rows(logits: np.ndarray, y: np.ndarray):
+    """Summed CE and first-argmax hits (fedsim/models/kernels.py:70-83)."""
+    m = logits.max(axis=1, keepdims=True)
+    lse = np.log(np.exp(logits - m).sum(axis=1))
+    loss = -(logits[np.arange(len(y)), y] - m[:, 0] - lse)
+    return float(loss.sum()), int((np.argmax(logits, axis=1) == y).sum())
+
+
+@dataclass(frozen=True)
+class Linear:
+    dim: int
+    k: int
+
+    @property
+    def dims(self):
+        return {"weights": self.dim * self.k, "bias": self.k}
+
+    def init(self, seed):
+        return {n: np.zeros(s) for n, s in self.dims.items()}
+
+    def loss_and_grad(self, p, X, y):  # fedsim/models/models.py:110-124
+        W = p["weights"].reshape(self.dim, self.k)
+        loss, dl = _xent(X @ W + p["bias"], y)
+        return loss, {"weights": (X.T @ dl).ravel(), "bias": dl.sum(axis=0)}
+
+    def eval_counts(self, p, X, y):
+        W = p["weights"].reshape(self.dim, self.k)
+        return _eval_rows(X @ W + p["bias"], y)
+
+
+@dataclass(frozen=True)
+class Mlp:
+    dim: int
+    h: int
+    k: int
+
+    @property
+    def dims(self):
+        return {"layer1/weights": self.dim * self.h, "layer1/bias": self.h,
+                "layer2/weights": self.h * self.k, "layer2/bias": self.k}
+
+    def init(self, seed):  # fedsim/models/models.py:162-175
+        rng = np.random.default_rng(seed)
+        b1, b2 = 1.0 / np.sqrt(self.dim), 1.0 / np.sqrt(self.h)
+        return {"layer1/weights": rng.uniform(-b1, b1, self.dim * self.h),
+                "layer1/bias": rng.uniform(-b1, b1, self.h),
+                "layer2/weights": rng.uniform(-b2, b2, self.h * self.k),
+                "layer2/bias": rng.uniform(-b2, b2, self.k)}
+
+    def loss_and_grad(self, p, X, y):  # fedsim/models/models.py:185-205
+        W1 = p["layer1/weights"].reshape(self.dim, self.h)
+        W2 = p["layer2/weights"].reshape(self.h, self.k)
+        z1 = X @ W1 + p["layer1/bias"]
+        h = np.maximum(z1, 0.0)
+        loss, dl = _xent(h @ W2 + p["layer2/bias"], y)
+        dz1 = (dl @ W2.T) * (z1 > 0.0)
+        return loss, {"layer1/weights": (X.T @ dz1).ravel(), "layer1/bias": dz1.sum(axis=0),
+                      "layer2/weights": (h.T @ dl).ravel(), "layer2/bias": dl.sum(axis=0)}
+
+    def eval_counts(self, p, X, y):
+        W1 = p["layer1/weights"].reshape(self.dim, self.h)
+        W2 = p["layer2/weights"].reshape(self.h, self.k)
+        h = np.maximum(X @ W1 + p["layer1/bias"], 0.0)
+        return _eval_rows(h @ W2 + p["layer2/bias"], y)
+
+
+def _im2col3(x: np.ndarray) -> np.ndarray:
+    """[N, C, H, W] -> [N, (H-2)*(W-2), C*9] with (c, kh, kw) column order."""
+    win = np.lib.stride_tricks.sliding_window_view(x, (3, 3), axis=(2, 3))  # N,C,Ho,Wo,3,3
+    n, c, ho, wo = win.shape[:4]
+    return win.transpose(0, 2, 3, 1, 4, 5).reshape(n, ho * wo, c * 9)
+
+
+def _col2im3(cols: np.ndarray, c: int, h: int, w: int) -> np.ndarray:
+    """Adjoint of _im2col3: [N, Ho*Wo, C*9] -> [N, C, H, W]."""
+    n = cols.shape[0]
+    ho, wo = h - 2, w - 2
+    k = cols.reshape(n, ho, wo, c, 3, 3)
+    out = np.zeros((n, c, h, w))
+    for a in range(3):
+        for b in range(3):
+            out[:, :, a:a + ho, b:b + wo] += k[:, :, :, :, a, b].transpose(0, 3, 1, 2)
+    return out
+
+
+@dataclass(frozen=True)
+class Cnn:
+    """conv3x3(3->32)+ReLU, conv3x3(32->64)+ReLU, maxpool2, fc 12544->128
+    +ReLU, fc 128->10; valid convs, CHW inputs, OIHW conv weights, [in,out]
+    fc weights (paper_2404_06430_b200/models.py).  No reference
+    implementation exists (SURVEY.md section 8 "Assumed CNN")."""
+
+    c0: int = 3
+    s: int = 32
+    c1: int = 32
+    c2: int = 64
+    hid: int = 128
+    k: int = 10
+
+    @property
+    def flat(self):
+        return self.c2 * ((self.s - 4) // 2) ** 2
+
+    @property
+    def dims(self):
+        return {"conv1/weights": self.c1 * self.c0 * 9, "conv1/bias": self.c1,
+                "conv2/weights": self.c2 * self.c1 * 9, "conv2/bias": self.c2,
+                "fc1/weights": self.flat * self.hid, "fc1/bias": self.hid,
+                "fc2/weights": self.hid * self.k, "fc2/bias": self.k}
+
+    def init(self, seed):
+        fan = {"conv1": self.c0 * 9, "conv2": self.c1 * 9, "fc1": self.flat, "fc2": self.hid}
+        rng = np.random.default_rng(seed)
+        out = {}
+        for name, n in self.dims.items():
+            b = 1.0 / np.sqrt(fan[name.split("/")[0]])
+            out[name] = rng.uniform(-b, b, n)
+        return out
+
+    def _forward(self, p, X):
+        N, s = X.shape[0], self.s
+        x = X.reshape(N, self.c0, s, s)
+        cols1 = _im2col3(x)
+        z1 = cols1 @ p["conv1/weights"].reshape(self.c1, -1).T + p["conv1/bias"]  # N, s1*s1, c1
+        s1 = s - 2
+        a1 = np.maximum(z1, 0.0).transpose(0, 2, 1).reshape(N, self.c1, s1, s1)
+        cols2 = _im2col3(a1)
+        z2 = cols2 @ p["conv2/weights"].reshape(self.c2, -1).T + p["conv2/bias"]  # N, s2*s2, c2
+        s2 = s1 - 2
+        a2 = np.maximum(z2, 0.0).transpose(0, 2, 1).reshape(N, self.c2, s2, s2)
+        sp = s2 // 2
+        win = a2.reshape(N, self.c2, sp, 2, sp, 2).transpose(0, 1, 2, 4, 3, 5).reshape(N, self.c2, sp, sp, 4)
+        arg = win.argmax(axis=4)  # first maximum in (0,0),(0,1),(1,0),(1,1) order
+        pooled = np.take_along_axis(win, arg[..., None], axis=4)[..., 0]
+        flat = pooled.reshape(N, -1)
+        z3 = flat @ p["fc1/weights"].reshape(self.flat, self.hid) + p["fc1/bias"]
+        a3 = np.maximum(z3, 0.0)
+        logits = a3 @ p["fc2/weights"].reshape(self.hid, self.k) + p["fc2/bias"]
+        return dict(cols1=cols1, z1=z1, cols2=cols2, z2=z2, arg=arg, flat=flat, z3=z3, a3=a3), logits
+
+    def loss_and_grad(self, p, X, y):
+        N = X.shape[0]
+        c, logits = self._forward(p, X)
+        loss, dl = _xent(logits, y)
+        Wf2 = p["fc2/weights"].reshape(self.hid, self.k)
+        Wf1 = p["fc1/weights"].reshape(self.flat, self.hid)
+        g = {"fc2/weights": (c["a3"].T @ dl).ravel(), "fc2/bias": dl.sum(axis=0)}
+        dz3 = (dl @ Wf2.T) * (c["z3"] > 0.0)
+        g["fc1/weights"] = (c["flat"].T @ dz3).ravel()
+        g["fc1/bias"] = dz3.sum(axis=0)
+        sp = (self.s - 4) // 2
+        dpool = (dz3 @ Wf1.T).reshape(N, self.c2, sp, sp)
+        dwin = np.zeros((N, self.c2, sp, sp, 4))
+        np.put_along_axis(dwin, c["arg"][..., None], dpool[..., None], axis=4)
+        s2 = 2 * sp
+        da2 = dwin.reshape(N, self.c2, sp, sp, 2, 2).transpose(0, 1, 2, 4, 3, 5).reshape(N, self.c2, s2, s2)
+        dz2 = da2.reshape(N, self.c2, s2 * s2).transpose(0, 2, 1) * (c["z2"] > 0.0)  # N, s2*s2, c2
+        W2 = p["conv2/weights"].reshape(self.c2, -1)
+        g["conv2/weights"] = np.einsum("npo,npk->ok", dz2, c["cols2"]).ravel()
+        g["conv2/bias"] = dz2.sum(axis=(0, 1))
+        s1 = s2 + 2
+        da1 = _col2im3(dz2 @ W2, self.c1, s1, s1)  # N, c1, s1, s1
+        dz1 = da1.reshape(N, self.c1, s1 * s1).transpose(0, 2, 1) * (c["z1"] > 0.0)
+        g["conv1/weights"] = np.einsum("npo,npk->ok", dz1, c["cols1"]).ravel()
+        g["conv1/bias"] = dz1.sum(axis=(0, 1))
+        return loss, {n: g[n] for n in self.dims}
+
+    def eval_counts(self, p, X, y):
+        _, logits = self._forward(p, X)
+        return _eval_rows(logits, y)
+
+
+# ------------------------------------------------------------ local work
+
+
+def fit_local(model, params, X, y, perms, lr, batch_size, mu=0.0, control=None):
+    """Generic Model.fit_local (fedsim/models/models.py:53-79): batches in
+    perms order, tail batch kept, all entries updated after the gradient."""
+    p = {n: v.copy() for n, v in params.items()}
+    E, n = perms.shape
+    for e in range(E):
+        for s in range(0, n, batch_size):
+            idx = perms[e, s:s + batch_size]
+            _, g = model.loss_and_grad(p, X[idx], y[idx])
+            for name in p:
+                step = g[name]
+                if mu != 0.0:
+                    step = step + mu * (p[name] - params[name])
+                if control is not None:
+                    step = step + control[name]
+                p[name] = p[name] - lr * step
+    return p
+
+
+def flat(params, dims) -> np.ndarray:
+    return np.concatenate([np.asarray(params[n], dtype=np.float64).ravel() for n in dims])
+
+
+@dataclass
+class ContextResult:
+    cohort: tuple
+    queue: tuple
+    loss_sum: np.ndarray          # per queue user
+    correct: np.ndarray
+    n: np.ndarray
+    delta: np.ndarray | None = None   # [C, D] weighted (w_u * (theta_t - theta_u))
+    norm: np.ndarray | None = None
+    clipped: np.ndarray | None = None
+    aggregate: np.ndarray | None = None   # clipped sum, before noise
+    weight: float = 0.0
+    noise: np.ndarray | None = None
+    metrics: dict = field(default_factory=dict)
+
+
+def run_context(model, theta: dict, users: dict, cohort_size: int, ctx_seed: int, *, train=None,
+                weighting="datapoints", bound=None, sigma=0.0, r=1.0, noise_base=0, t=0, pop="train",
+                world=1, rank=0, base_policy="median", noise=True):
+    """One context of SimulationEngine._run_context (fedsim/engine/runtime.py:106-171)
+    with FedAvg users (fedsim/algorithms/fedavg.py:127-180), ClippingPostprocessor
+    (fedsim/privacy/clipping.py:105-146) and GaussianCentralMechanism
+    (fedsim/privacy/mechanisms.py:146-193).  ``train`` = (lr, epochs, batch)."""
+    ids = tuple(users)
+    cohort = sample_cohort(ids, cohort_size, ctx_seed)
+    w_all = {u: float(users[u][0].shape[0]) for u in cohort}
+    base = lower_median(list(w_all.values())) if base_policy == "median" else 0.0
+    queue = lpt_queues(w_all, world, base)[0][rank]
+    dims = model.dims
+    res = ContextResult(cohort, queue, np.zeros(len(queue)), np.zeros(len(queue), dtype=np.int64),
+                        np.array([users[u][0].shape[0] for u in queue], dtype=np.int64))
+    deltas, norms, clips = [], [], []
+    for i, uid in enumerate(queue):
+        X, y = users[uid]
+        res.loss_sum[i], res.correct[i] = model.eval_counts(theta, X, y)
+        if train is None:
+            continue
+        lr, E, B = train
+        after = fit_local(model, theta, X, y, user_perms(ctx_seed, uid, X.shape[0], E), lr, B) if E else theta
+        w = float(X.shape[0]) if weighting == "datapoints" else 1.0
+        d = w * (flat(theta, dims) - flat(after, dims))       # fedsim/models/params.py:32-45
+        nrm = float(np.linalg.norm(d))
+        c = bound is not None and nrm > bound                 # fedsim/privacy/clipping.py:49
+        if c:
+            d = d * (bound / nrm)
+        deltas.append(d)
+        norms.append(nrm)
+        clips.append(c)
+        res.weight += w
+    n = res.n.astype(np.float64)
+    res.metrics = {"loss": (res.loss_sum.sum(), n.sum()), "accuracy": (float(res.correct.sum()), n.sum()),
+                   "per_user_accuracy": ((res.correct / n).sum(), float(len(queue)))}
+    if train is None:
+        return res
+    res.delta = np.array(deltas)
+    res.norm = np.array(norms)
+    res.clipped = np.array(clips)
+    res.aggregate = res.delta.sum(axis=0)
+    if bound is not None:
+        std = r * sigma * bound
+        res.metrics.update({"clip_fraction": (float(res.clipped.sum()), float(len(queue))),
+                            "update_norm": (float(res.norm.sum()), float(len(queue))),
+                            "clipping_bound": (bound, 1.0), "noise_std": (std, 1.0)})
+        sig = float(np.linalg.norm(res.aggregate))
+        if std > 0:
+            res.metrics["snr"] = (sig / np.sqrt(res.aggregate.size * std**2), 1.0)
+        if std > 0 and noise:
+            rng = np.random.default_rng(noise_seed(noise_base, t, pop))
+            res.noise = np.concatenate([rng.normal(0.0, std, k) for k in dims.values()])
+    return res
+
+
+def central_sgd(theta_flat: np.ndarray, aggregate: np.ndarray, weight: float, lr: float, noise=None):
+    """average -> SGD (fedsim/core/statistics.py:105-113, fedsim/models/optimizers.py:13-21);
+    noise is added to the SUM first."""
+    agg = aggregate if noise is None else aggregate + noise
+    return theta_flat - lr * (agg * (1.0 / weight))
+
+
+def run_fedavg(model, train_users: dict, val_users: dict, *, iterations, cohort, eval_cohort, eval_every,
+               lr, epochs, batch, clr, weighting, bound, sigma, r, noise_base, run_seed, init_seed, world=1):
+    """run_simulation (fedsim/engine/loop.py:45-88) over FedAvg contexts
+    (fedsim/algorithms/fedavg.py:97-125,183-198).  Returns per-iteration
+    flat thetas, metric rows sorted by (population, name), cohort digest."""
+    dims = model.dims
+    theta = model.init(init_seed)
+    thetas, rows = [], []
+    digest = hashlib.sha256()
+    for t in range(iterations):
+        metrics = {}
+        cohorts = []
+        ctxs = [("train", train_users, cohort, True)]
+        if t % eval_every == 0:
+            ctxs.append(("val", val_users, eval_cohort, False))
+        agg_state = None
+        for pop, users, csize, train in ctxs:
+            parts = [run_context(model, theta, users, csize, cohort_seed(run_seed, t, pop),
+                                 train=(lr, epochs, batch) if train else None, weighting=weighting,
+                                 bound=bound, sigma=sigma, r=r, noise_base=noise_base, t=t, pop=pop,
+                                 world=world, rank=k) for k in range(world)]
+            cohorts.append((pop, parts[0].cohort))
+            for k, v in _merge_parts(parts).items():
+                metrics[(pop, k)] = v
+            if train:
+                agg = sum(p.aggregate for p in parts if len(p.queue))
+                weight = sum(p.weight for p in parts)
+                agg_state = (agg, weight, parts[0].noise)  # one draw per context (rank-independent)
+        if agg_state is not None:
+            agg, weight, nz = agg_state
+            new = central_sgd(flat(theta, dims), agg, weight, clr, nz)
+            off = np.cumsum([0] + list(dims.values()))
+            theta = {n: new[off[i]:off[i + 1]] for i, n in enumerate(dims)}
+        thetas.append(flat(theta, dims))
+        for pop, c in cohorts:
+            digest.update(repr((t, pop, c)).encode())
+        rows.extend((t, pop, name, num / den, den) for (pop, name), (num, den) in sorted(metrics.items()))
+    return np.array(thetas), rows, digest.hexdigest()
+
+
+def _merge_parts(parts):
+    """Sum per-rank metric (num, den) pairs; snr / noise_std / bound are
+    computed once on the reduced aggregate."""
+    out = {}
+    for p in parts:
+        for k, (num, den) in p.metrics.items():
+            if k in ("snr", "noise_std", "clipping_bound"):
+                continue
+            a = out.get(k, (0.0, 0.0))
+            out[k] = (a[0] + num, a[1] + den)
+    ref = parts[0].metrics
+    for k in ("noise_std", "clipping_bound"):
+        if k in ref:
+            out[k] = ref[k]
+    if "noise_std" in ref and ref["noise_std"][0] > 0:
+        agg = sum(p.aggregate for p in parts if len(p.queue))
+        out["snr"] = (float(np.linalg.norm(agg)) / np.sqrt(agg.size * ref["noise_std"][0] ** 2), 1.0)
+    return out

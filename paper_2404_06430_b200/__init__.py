@@ -1,0 +1,78 @@
+"""B200-native central-iteration engine for private federated learning
+simulation (pfl-research, arXiv 2404.06430, as restated by fedsim).
+
+Public surface mirrors the reference's names (FedAvg, ClippingPostprocessor,
+GaussianCentralMechanism, SumAggregator, run_simulation, ...) and adds
+``GpuSimulationEngine``, the drop-in for fedsim's SimulationEngine whose
+cohort work runs in hand-written sm_100a kernels (libfedsim_b200.so).
+"""
+
+from .aggregator import Aggregator, SumAggregator, worker_reduce_sum
+from .algorithms import AlgorithmState, CohortPlan, FederatedAlgorithm, FedAvg, FedProx, UserResult
+from .core import (
+    CentralContext,
+    Constant,
+    EvalParams,
+    HyperParam,
+    LinearWarmup,
+    LocalTrainParams,
+    MetricKind,
+    MetricValue,
+    PiecewiseConstant,
+    Population,
+    Statistics,
+    accumulate,
+    average,
+    cohort_seed,
+    derive_seed,
+    global_norm,
+    make_rng,
+    merge_metrics,
+    metric_aggregate,
+    noise_seed,
+    resolve,
+    scale_entries,
+    user_seed,
+    weighted,
+)
+from .device import DeviceParams, DevicePopulation, DeviceStatistics
+from .engine import GpuSimulationEngine, IterationResult, client_permutations
+from .errors import (
+    CohortTooLarge,
+    DataError,
+    EmptyCohort,
+    EngineError,
+    FedsimError,
+    IncompatibleShapes,
+    NativeError,
+    NativeUnavailable,
+    NotClippedUpstream,
+    TooFewPoints,
+    ZeroWeight,
+)
+from .feddata import (
+    FederatedDataset,
+    UserDataset,
+    load_partition,
+    make_synthetic_classification,
+    partition_iid,
+    sample_cohort,
+    save_partition,
+)
+from .loop import MetricsRow, SimulationResult, run_simulation
+from .models import CNN, MLP, LogisticRegression, Model, SGDOptimizer, central_step, count_local_steps
+from .privacy import (
+    AdaptiveClipConfig,
+    ClippingPostprocessor,
+    GaussianCentralMechanism,
+    adaptive_clip_update,
+    payload_names,
+    snr,
+    validate_pipeline,
+)
+from .scheduling import WorkerAssignment, compute_base_weight, round_robin_schedule, schedule_users
+
+# SimulationEngine is the name the reference's loop and runner use
+SimulationEngine = GpuSimulationEngine
+
+__version__ = "0.1.0"

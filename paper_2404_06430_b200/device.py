@@ -1,0 +1,260 @@
+"""Device-resident forms of the path's value types.
+
+* :class:`DeviceParams` -- model parameters as ONE flat fp32 HBM vector in
+  entry order (the reference's ``ModelParams`` dict, fedsim/models/params.py:17).
+* :class:`DeviceStatistics` -- the reduced cohort aggregate: the payload as a
+  flat fp32 HBM vector, the ``_clip/*`` bookkeeping sums as host scalars,
+  the total weight, and any *pending* central noise / averaging, which the
+  central SGD step applies in one fused kernel (fb_noise_avg_sgd_f32).
+* :class:`DevicePopulation` -- a FederatedDataset packed once into HBM:
+  features fp32 [rows, dim] (users contiguous, dataset order), labels int32.
+* :class:`Workspace` -- grow-only scratch buffers keyed by purpose (the C
+  ABI never allocates).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field, replace
+from typing import Iterator, Mapping
+
+import numpy as np
+
+from . import native
+from .core import Statistics
+from .errors import IncompatibleShapes, ZeroWeight
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+class Workspace:
+    """Named, grow-only device scratch (one per engine / device)."""
+
+    def __init__(self, device):
+        self.device = device
+        self._bufs: dict[str, object] = {}
+
+    def get(self, name: str, nbytes: int):
+        torch = _torch()
+        nbytes = max(int(nbytes), 16)
+        buf = self._bufs.get(name)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            self._bufs[name] = buf
+        return buf
+
+    def tensor(self, name: str, shape, dtype):
+        torch = _torch()
+        n = int(np.prod(shape)) if len(shape) else 1
+        esize = torch.empty((), dtype=dtype).element_size()
+        return self.get(name, n * esize)[: n * esize].view(dtype).view(*shape)
+
+
+def _offsets(dims: Mapping[str, int]) -> dict[str, tuple[int, int]]:
+    out, o = {}, 0
+    for n, k in dims.items():
+        out[n] = (o, o + int(k))
+        o += int(k)
+    return out
+
+
+class DeviceParams(Mapping):
+    """Flat fp32 parameter vector with named views (entry order = dims order)."""
+
+    def __init__(self, flat, dims: Mapping[str, int]):
+        self.flat = flat
+        self.dims = dict(dims)
+        self._off = _offsets(self.dims)
+        if flat.numel() != sum(self.dims.values()):
+            raise IncompatibleShapes(f"flat has {flat.numel()} values, layout needs {sum(self.dims.values())}")
+
+    @classmethod
+    def from_host(cls, params: Mapping[str, np.ndarray], device) -> "DeviceParams":
+        torch = _torch()
+        dims = {n: int(np.asarray(v).size) for n, v in params.items()}
+        host = np.concatenate([np.asarray(v, dtype=np.float64).ravel() for v in params.values()])
+        return cls(torch.from_numpy(host.astype(np.float32)).to(device), dims)
+
+    def __getitem__(self, name: str):
+        lo, hi = self._off[name]
+        return self.flat[lo:hi]
+
+    def __iter__(self) -> Iterator[str]:
+        return iter(self.dims)
+
+    def __len__(self) -> int:
+        return len(self.dims)
+
+    @property
+    def num_params(self) -> int:
+        return self.flat.numel()
+
+    def to_host(self) -> dict[str, np.ndarray]:
+        host = self.flat.detach().to("cpu", dtype=_torch().float64).numpy()
+        return {n: host[lo:hi].copy() for n, (lo, hi) in self._off.items()}
+
+    def flat_host(self) -> np.ndarray:
+        return self.flat.detach().to("cpu", dtype=_torch().float64).numpy()
+
+    def clone(self) -> "DeviceParams":
+        return DeviceParams(self.flat.clone(), self.dims)
+
+
+@dataclass
+class PendingNoise:
+    std: float
+    seed: int                      # Philox key (the reference's noise_seed value)
+    injected: object | None = None  # device fp32 [D]: the reference's own draws (parity)
+
+
+@dataclass
+class Comm:
+    """How the central epilogue is distributed (set by the engine)."""
+
+    rank: int = 0
+    world_size: int = 1
+    group: object | None = None
+    epilogue: str = "rank0"   # "rank0": step on rank 0 + broadcast; "replicated"
+
+
+@dataclass
+class DeviceStatistics:
+    """Reduced aggregate.  ``flat`` holds the payload sum (un-averaged,
+    un-noised); averaging and noise are recorded and applied lazily."""
+
+    flat: object
+    dims: dict[str, int]
+    weight: float
+    bookkeeping: dict[str, np.ndarray] = field(default_factory=dict)
+    noise: PendingNoise | None = None
+    scale: float = 1.0
+    workspace: Workspace | None = None
+    comm: Comm = field(default_factory=Comm)
+
+    # ---- reference-compatible surface (fedsim/core/statistics.py:21-80)
+    @property
+    def entries(self) -> dict:
+        out = {}
+        for n, (lo, hi) in _offsets(self.dims).items():
+            out[n] = self.flat[lo:hi]
+        out.update(self.bookkeeping)
+        return out
+
+    @property
+    def names(self) -> tuple[str, ...]:
+        return tuple(self.dims) + tuple(self.bookkeeping)
+
+    @property
+    def payload_names(self) -> tuple[str, ...]:
+        return tuple(self.dims)
+
+    @property
+    def num_dims(self) -> int:
+        return self.flat.numel() + sum(int(v.size) for v in self.bookkeeping.values())
+
+    # ---- device operations
+    def device_norm(self, order: float, names) -> float:
+        """L2 norm of the selected payload entries of the (un-noised, unscaled)
+        aggregate, fp64 accumulation on the device."""
+        if order != 2.0:
+            raise ValueError("device aggregates support the L2 norm only")
+        names = tuple(names)
+        if names != tuple(self.dims):
+            raise ValueError("device norm is defined over the whole payload")
+        torch = _torch()
+        ws = self.workspace or Workspace(self.flat.device)
+        out = ws.tensor("sumsq_out", (1,), torch.float64)
+        scratch = ws.get("sumsq_ws", 8192)
+        native.call("fb_sumsq_f32", native.ptr(self.flat), self.flat.numel(), native.ptr(out),
+                    native.ptr(scratch), scratch.numel(), native.stream_handle())
+        return float(np.sqrt(out.item())) * abs(self.scale)
+
+    def with_noise(self, std: float, seed: int, injected=None) -> "DeviceStatistics":
+        if self.noise is not None:
+            raise ValueError("aggregate already carries pending noise")
+        return replace(self, noise=PendingNoise(float(std), int(seed), injected))
+
+    def without_bookkeeping(self) -> "DeviceStatistics":
+        return replace(self, bookkeeping={})
+
+    def averaged(self) -> "DeviceStatistics":
+        if self.weight == 0.0:
+            raise ZeroWeight("cannot average statistics with zero total weight")
+        return replace(self, scale=self.scale / self.weight, weight=1.0)
+
+    def apply_sgd(self, params: DeviceParams, lr: float) -> DeviceParams:
+        """theta_{t+1} = theta_t - lr * scale * (sum + noise): K4+K5 in one kernel.
+
+        With a multi-rank engine the step runs on rank 0 and theta is
+        broadcast (``epilogue="rank0"``), or identically on every rank from
+        the counter-based noise (``"replicated"``)."""
+        if params.num_params != self.flat.numel():
+            raise IncompatibleShapes("aggregate and parameters differ in size")
+        torch = _torch()
+        out = params.flat.clone()
+        comm = self.comm
+        run_here = comm.world_size == 1 or comm.epilogue == "replicated" or comm.rank == 0
+        if run_here:
+            nz = self.noise
+            native.call(
+                "fb_noise_avg_sgd_f32", native.ptr(out), native.ptr(self.flat), self.flat.numel(),
+                nz.std if nz else 0.0, nz.seed if nz else 0,
+                native.ptr(nz.injected) if nz is not None and nz.injected is not None else None,
+                float(self.scale), float(lr), None, native.stream_handle(),
+            )
+        if comm.world_size > 1 and comm.epilogue == "rank0":
+            torch.distributed.broadcast(out, src=0, group=comm.group)
+        return DeviceParams(out, params.dims)
+
+    def materialize(self):
+        """Device fp32 payload with pending noise and scale applied."""
+        torch = _torch()
+        x = self.flat.clone()
+        nz = self.noise
+        if nz is not None:
+            if nz.injected is not None:
+                x += nz.injected
+            elif nz.std != 0.0:
+                native.call("fb_gaussian_f32", native.ptr(x), x.numel(), nz.std, nz.seed, 0, 1,
+                            native.stream_handle())
+        if self.scale != 1.0:
+            x = (x.double() * self.scale).float()
+        return x
+
+    def to_host(self) -> Statistics:
+        host = self.materialize().to("cpu", dtype=_torch().float64).numpy()
+        entries = {n: host[lo:hi].copy() for n, (lo, hi) in _offsets(self.dims).items()}
+        entries.update({n: np.array(v, dtype=np.float64) for n, v in self.bookkeeping.items()})
+        return Statistics(entries=entries, weight=self.weight)
+
+
+class DevicePopulation:
+    """A FederatedDataset packed once into HBM (features fp32, labels int32)."""
+
+    def __init__(self, dataset, device):
+        torch = _torch()
+        users = list(dataset.users.values())
+        if not users:
+            raise ValueError("cannot pack an empty dataset")
+        dims = {u.features.shape[1] for u in users}
+        if len(dims) != 1:
+            raise ValueError(f"users disagree on feature dim: {sorted(dims)}")
+        self.dim = dims.pop()
+        counts = np.array([u.num_points for u in users], dtype=np.int64)
+        starts = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.int64)
+        self.index = {u.user_id: i for i, u in enumerate(users)}
+        self.row_start = starts
+        self.num_rows = counts.astype(np.int32)
+        total = int(counts.sum())
+        X = np.empty((total, self.dim), dtype=np.float32)
+        y = np.empty(total, dtype=np.int32)
+        for u, s in zip(users, starts):
+            X[s:s + u.num_points] = u.features
+            y[s:s + u.num_points] = u.labels
+        self.X = torch.from_numpy(X).to(device)
+        self.y = torch.from_numpy(y).to(device)
+        self.total_rows = total
+        self.max_label = int(y.max()) if total else 0

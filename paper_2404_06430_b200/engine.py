@@ -1,0 +1,374 @@
+"""GpuSimulationEngine -- drop-in for fedsim's SimulationEngine.
+
+Same constructor keywords and the same ``run_iteration(algorithm, state,
+contexts) -> IterationResult`` as fedsim/engine/runtime.py:36-104 (the only
+call the outer loop makes, fedsim/engine/loop.py:62).  Per context:
+
+  host  sample_cohort -> compute_base_weight -> schedule_users(world)   bit-exact
+        per-user seeds -> minibatch permutations (this rank's queue)     bit-exact
+  H2D   one packed copy of the cohort descriptor
+  GPU   eval at theta_t (K0) -> local SGD (K1) -> delta/norm/clip (K2)
+        -> weighted sum (K3)                               [one stream]
+  NCCL  all-reduce of the flat payload + fp64 all-reduce of the sums (N>1)
+  D2H   per-client loss/correct/norm/clipped/non-finite flags (one copy)
+  host  metrics, provenance errors, server postprocessors (reversed order)
+
+The central step (noise + /W + SGD, K4+K5) runs when the algorithm folds
+the aggregate back (``FedAvg.process_aggregated_statistics_all_contexts``)
+because the returned DeviceStatistics carries the pending noise.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Any, Mapping, Sequence
+
+import numpy as np
+
+from . import native
+from .aggregator import SumAggregator
+from .core import CentralContext, MetricKind, MetricValue, Population, merge_metrics, user_seed
+from .device import Comm, DeviceParams, DevicePopulation, DeviceStatistics, Workspace
+from .errors import EngineError
+from .feddata import FederatedDataset, sample_cohort
+from .models import CNN, MLP, LogisticRegression
+from .privacy import (
+    CLIPPED_KEY,
+    COUNT_KEY,
+    NORM_KEY,
+    ClippingPostprocessor,
+    GaussianCentralMechanism,
+    validate_pipeline,
+)
+from .scheduling import compute_base_weight, schedule_users
+
+
+@dataclass
+class IterationResult:
+    aggregates: tuple
+    metrics: dict[tuple[str, str], MetricValue]
+    user_updates: list = field(default_factory=list)
+    cohorts: tuple[tuple[str, tuple[str, ...]], ...] = ()
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def client_permutations(ctx_seed: int, user_ids: Sequence[str], sizes: Sequence[int], epochs: int) -> list[np.ndarray]:
+    """Per-user epoch shuffles: default_rng(user_seed(ctx, uid)).permutation(n)
+    per epoch (fedsim/models/models.py:252-255 with fedsim/core/seeds.py:31)."""
+    out = []
+    for uid, n in zip(user_ids, sizes):
+        rng = np.random.default_rng(user_seed(ctx_seed, uid))
+        out.append(np.concatenate([rng.permutation(n) for _ in range(epochs)]) if epochs else
+                   np.zeros(0, dtype=np.int64))
+    return out
+
+
+class _Staging:
+    """Packs host arrays into one pinned buffer, one H2D copy, device views."""
+
+    def __init__(self, device):
+        self.device = device
+        self._host = None
+        self._dev = None
+
+    def upload(self, arrays: Sequence[np.ndarray]):
+        torch = _torch()
+        offs, total = [], 0
+        for a in arrays:
+            offs.append(total)
+            total += (a.nbytes + 15) & ~15
+        total = max(total, 16)
+        if self._host is None or self._host.numel() < total:
+            self._host = torch.empty(total * 2, dtype=torch.uint8, pin_memory=True)
+            self._dev = torch.empty(total * 2, dtype=torch.uint8, device=self.device)
+        hv = self._host.numpy()
+        for a, o in zip(arrays, offs):
+            hv[o:o + a.nbytes] = np.ascontiguousarray(a).view(np.uint8).ravel()
+        self._dev[:total].copy_(self._host[:total], non_blocking=True)
+        views = []
+        for a, o in zip(arrays, offs):
+            dt = {np.dtype(np.int64): torch.int64, np.dtype(np.int32): torch.int32,
+                  np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float64}[a.dtype]
+            views.append(self._dev[o:o + a.nbytes].view(dt))
+        return views
+
+
+class _ModelRunner:
+    """Dispatches eval / local SGD to the model's fb_* entry points."""
+
+    def __init__(self, model, ws: Workspace):
+        self.model = model
+        self.ws = ws
+        if isinstance(model, MLP):
+            self.kind, self.dims = "mlp", (model.dim, model.hidden_units, model.num_classes)
+        elif isinstance(model, LogisticRegression):
+            self.kind, self.dims = "linear", (model.dim, model.num_classes)
+        elif isinstance(model, CNN):
+            self.kind, self.dims = "cnn", ()
+        else:
+            raise ValueError(f"GpuSimulationEngine: unsupported model {type(model).__name__}")
+        self.D = model.num_params
+        self.ld = (self.D + 3) & ~3  # 16-byte aligned client rows
+
+    def eval(self, theta, pop: DevicePopulation, row_start, num_rows, C, loss, correct, stream):
+        if self.kind == "cnn":
+            from . import cnn
+
+            return cnn.eval_cohort(self, theta, pop, row_start, num_rows, C, loss, correct, stream)
+        fn = f"fb_eval_{self.kind}_f32"
+        native.call(fn, native.ptr(theta), *self.dims, native.ptr(pop.X), native.ptr(pop.y),
+                    native.ptr(row_start), native.ptr(num_rows), C, native.ptr(loss), native.ptr(correct),
+                    stream)
+
+    def local_sgd(self, theta, pop, row_start, num_rows, perms, perm_off, C, tp, prox_mu, delta, nonfinite, stream):
+        if self.kind == "cnn":
+            from . import cnn
+
+            return cnn.local_sgd_cohort(self, theta, pop, row_start, num_rows, perms, perm_off, C, tp,
+                                        prox_mu, delta, nonfinite, stream)
+        fn = f"fb_local_sgd_{self.kind}_f32"
+        native.call(fn, native.ptr(theta), *self.dims, native.ptr(pop.X), native.ptr(pop.y),
+                    native.ptr(row_start), native.ptr(num_rows), native.ptr(perms), native.ptr(perm_off), C,
+                    tp.num_epochs, tp.batch_size, float(tp.learning_rate), float(prox_mu), None, 0,
+                    native.ptr(delta), self.ld, native.ptr(nonfinite), stream)
+
+
+class GpuSimulationEngine:
+    """Runs central iterations with the whole cohort batched on B200(s).
+
+    Multi-GPU: one process per GPU (torchrun); if ``torch.distributed`` is
+    initialised, the cohort is sharded with the reference's LPT scheduler
+    over ``world_size`` workers and rank r simulates ``queues[r]``.
+    ``central_epilogue``: "rank0" (noise + step on rank 0, broadcast theta)
+    or "replicated" (every rank applies the same counter-based noise).
+    """
+
+    def __init__(
+        self,
+        datasets: Mapping[Population, FederatedDataset],
+        *,
+        num_workers: int = 1,
+        postprocessors: Sequence = (),
+        aggregator=None,
+        base_policy: str = "median",
+        base_value: float = 0.0,
+        cohort_mode: str = "fixed",
+        poisson_rate: float | None = None,
+        device=None,
+        process_group=None,
+        central_epilogue: str = "rank0",
+    ):
+        if num_workers < 1:
+            raise ValueError("num_workers must be >= 1")
+        validate_pipeline(postprocessors)
+        for p in postprocessors:
+            if isinstance(p, ClippingPostprocessor):
+                if p.norm_order != 2.0:
+                    raise ValueError("GpuSimulationEngine supports L2 clipping only")
+            elif isinstance(p, GaussianCentralMechanism):
+                if p.privatize_bookkeeping:
+                    raise ValueError("privatize_bookkeeping is not supported on the GPU path")
+            else:
+                raise ValueError(f"GpuSimulationEngine: unsupported postprocessor {type(p).__name__}")
+        if sum(isinstance(p, ClippingPostprocessor) for p in postprocessors) > 1:
+            raise ValueError("GpuSimulationEngine supports at most one clipping postprocessor")
+        if aggregator is not None and not isinstance(aggregator, SumAggregator):
+            raise ValueError(f"GpuSimulationEngine: unsupported aggregator {type(aggregator).__name__}")
+        if central_epilogue not in ("rank0", "replicated"):
+            raise ValueError("central_epilogue must be 'rank0' or 'replicated'")
+        torch = _torch()
+        native.lib()  # fail loudly: no CUDA device / no library => no engine
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        dist = torch.distributed
+        if dist.is_available() and dist.is_initialized():
+            self.rank = dist.get_rank(process_group)
+            self.world_size = dist.get_world_size(process_group)
+        else:
+            self.rank, self.world_size = 0, 1
+        self.group = process_group
+        self._comm = Comm(self.rank, self.world_size, process_group, central_epilogue)
+        self._datasets = dict(datasets)
+        self._num_workers = int(num_workers)
+        self._postprocessors = tuple(postprocessors)
+        self._clip = next((p for p in postprocessors if isinstance(p, ClippingPostprocessor)), None)
+        self._aggregator = aggregator if aggregator is not None else SumAggregator()
+        self._base_policy = base_policy
+        self._base_value = float(base_value)
+        self._cohort_mode = cohort_mode
+        self._poisson_rate = poisson_rate
+        self.ws = Workspace(self.device)
+        self._staging = _Staging(self.device)
+        self._pops: dict[Population, DevicePopulation] = {}
+        self._runners: dict[int, _ModelRunner] = {}
+        self.stream = torch.cuda.current_stream(self.device)
+        self.last_timings: dict[str, float] = {}
+
+    @property
+    def num_workers(self) -> int:
+        return self._num_workers
+
+    @property
+    def postprocessors(self) -> tuple:
+        return self._postprocessors
+
+    def population(self, pop: Population) -> DevicePopulation:
+        if pop not in self._pops:
+            self._pops[pop] = DevicePopulation(self._datasets[pop], self.device)
+        return self._pops[pop]
+
+    def _runner(self, model) -> _ModelRunner:
+        key = id(model)
+        if key not in self._runners:
+            self._runners[key] = _ModelRunner(model, self.ws)
+        return self._runners[key]
+
+    # ------------------------------------------------------------------ API
+    def run_iteration(self, algorithm, state, contexts: Sequence[CentralContext]) -> IterationResult:
+        if not hasattr(algorithm, "cohort_plan"):
+            raise ValueError(f"GpuSimulationEngine: unsupported algorithm {type(algorithm).__name__}")
+        if not isinstance(state.params, DeviceParams):
+            state.params = DeviceParams.from_host(state.params, self.device)
+        aggregates, metrics, cohorts = [], {}, []
+        for ctx in contexts:
+            agg, ctx_metrics, cohort = self._run_context(algorithm, state, ctx)
+            aggregates.append(agg)
+            pop = ctx.population.value
+            for name, val in ctx_metrics.items():
+                key = (pop, name)
+                metrics[key] = metrics[key] + val if key in metrics else val
+            cohorts.append((pop, cohort))
+        return IterationResult(tuple(aggregates), metrics, [], tuple(cohorts))
+
+    # ------------------------------------------------------------ internals
+    def _run_context(self, algorithm, state, ctx: CentralContext):
+        torch = _torch()
+        pop_key = ctx.population
+        dataset = self._datasets.get(pop_key)
+        if dataset is None:
+            raise EngineError(f"iteration {ctx.iteration}: no dataset for population {pop_key.value!r}")
+        cohort = sample_cohort(dataset, ctx.cohort_size, ctx.seed, mode=self._cohort_mode,
+                               poisson_rate=self._poisson_rate)
+        if not cohort:
+            return None, {}, cohort
+        users = dataset.users
+        weights = {uid: float(users[uid].weight) for uid in cohort}
+        base = compute_base_weight(list(weights.values()), self._base_policy, self._base_value)
+        queue = schedule_users(weights, self.world_size, base).queues[self.rank]
+
+        plan = algorithm.cohort_plan(state, ctx)
+        runner = self._runner(plan.model)
+        pop = self.population(pop_key)
+        if pop.dim != plan.model.input_dim:
+            raise ValueError(f"dataset dim {pop.dim} != model input dim {plan.model.input_dim}")
+        theta: DeviceParams = state.params
+        C = len(queue)
+        stream = native.stream_handle(self.stream)
+        idx = np.fromiter((pop.index[u] for u in queue), dtype=np.int64, count=C)
+        row_start = pop.row_start[idx]
+        num_rows = pop.num_rows[idx]
+        train = plan.train is not None
+        host = [row_start, num_rows]
+        if train:
+            tp = plan.train
+            perms = client_permutations(ctx.seed, queue, num_rows.tolist(), tp.num_epochs)
+            perm_flat = (np.concatenate(perms) if perms else np.zeros(0)).astype(np.int32)
+            perm_off = np.zeros(C, dtype=np.int64)
+            if C > 1:
+                perm_off[1:] = np.cumsum(num_rows[:-1].astype(np.int64) * tp.num_epochs)
+            w = (num_rows.astype(np.float32) if plan.weighting == "datapoints"
+                 else np.ones(C, dtype=np.float32))
+            host += [perm_flat, perm_off, w]
+        dev = self._staging.upload(host)
+        d_row_start, d_num_rows = dev[0], dev[1]
+
+        # per-client result block: loss f64, norm f64 | correct, clipped, nonfinite i32
+        Cp = max(C, 1)
+        res = self.ws.get("client_results", 8 * Cp * 2 + 4 * Cp * 3)
+        loss = res[: 8 * Cp].view(torch.float64)
+        norm = res[8 * Cp: 16 * Cp].view(torch.float64)
+        ints = res[16 * Cp: 16 * Cp + 12 * Cp].view(torch.int32)
+        correct, clipped, nonfinite = ints[:Cp], ints[Cp:2 * Cp], ints[2 * Cp:3 * Cp]
+        if C:
+            runner.eval(theta.flat, pop, d_row_start, d_num_rows, C, loss, correct, stream)
+
+        agg_flat = None
+        if train:
+            d_perms, d_perm_off, d_w = dev[2], dev[3], dev[4]
+            agg_flat = torch.empty(runner.D, dtype=torch.float32, device=self.device)
+            if C:
+                delta = self.ws.tensor("delta", (C, runner.ld), torch.float32)
+                runner.local_sgd(theta.flat, pop, d_row_start, d_num_rows, d_perms, d_perm_off, C, plan.train,
+                                 plan.prox_mu, delta, nonfinite, stream)
+                coef = self.ws.tensor("coef", (Cp,), torch.float32)
+                bound = self._clip.current_bound if self._clip is not None else 0.0
+                wsb = native.call("fb_clip_workspace_bytes", C, runner.D)
+                kws = self.ws.get("clip_ws", wsb)
+                nf2 = self.ws.tensor("nonfinite2", (Cp,), torch.int32)
+                native.call("fb_delta_norm_clip_f32", native.ptr(delta), runner.ld, C, runner.D, native.ptr(d_w),
+                            float(bound), native.ptr(norm), native.ptr(coef), native.ptr(clipped),
+                            native.ptr(nf2), native.ptr(kws), kws.numel(), stream)
+                torch.bitwise_or(nonfinite[:C], nf2[:C], out=nonfinite[:C])
+                wsb = native.call("fb_weighted_sum_workspace_bytes", C, runner.D)
+                sws = self.ws.get("sum_ws", wsb)
+                native.call("fb_weighted_sum_f32", native.ptr(delta), runner.ld, C, runner.D, native.ptr(coef),
+                            native.ptr(agg_flat), 0, native.ptr(sws), sws.numel(), stream)
+            else:
+                agg_flat.zero_()
+
+        # one D2H copy of the per-client results
+        host_res = res[: 16 * Cp + 12 * Cp].to("cpu", non_blocking=False)
+        h_loss = host_res[: 8 * Cp].view(torch.float64).numpy()[:C]
+        h_norm = host_res[8 * Cp: 16 * Cp].view(torch.float64).numpy()[:C]
+        h_ints = host_res[16 * Cp:].view(torch.int32).numpy()
+        h_correct, h_clipped, h_bad = h_ints[:C], h_ints[Cp:Cp + C], h_ints[2 * Cp:2 * Cp + C]
+
+        if train and C and h_bad.any():
+            uid = queue[int(np.flatnonzero(h_bad)[0])]
+            raise EngineError(
+                f"iteration {ctx.iteration}, population {pop_key.value!r}, user {uid!r}: "
+                "entry contains non-finite values"
+            )
+        n_f = num_rows.astype(np.float64)
+        sums = np.array([
+            h_loss.sum(), float(h_correct.sum()), n_f.sum(), (h_correct / n_f).sum() if C else 0.0, float(C),
+            float(h_clipped.sum()) if train else 0.0, float(C) if train else 0.0,
+            float(h_norm.sum()) if train else 0.0,
+            float((n_f if plan.weighting == "datapoints" else np.ones(C)).sum()) if train else 0.0,
+        ], dtype=np.float64)
+        if self.world_size > 1:
+            t = torch.from_numpy(sums).to(self.device)
+            torch.distributed.all_reduce(t, group=self.group)
+            if agg_flat is not None:
+                torch.distributed.all_reduce(agg_flat, group=self.group)
+            sums = t.cpu().numpy()
+        metrics: dict[str, MetricValue] = {}
+        if sums[4] > 0:
+            metrics = {
+                "loss": MetricValue(MetricKind.CENTRAL, float(sums[0]), float(sums[2])),
+                "accuracy": MetricValue(MetricKind.CENTRAL, float(sums[1]), float(sums[2])),
+                "per_user_accuracy": MetricValue(MetricKind.PER_USER, float(sums[3]), float(sums[4])),
+            }
+        if not train:
+            return None, metrics, cohort
+
+        book = {}
+        if self._clip is not None:
+            book = {CLIPPED_KEY: np.array([sums[5]]), COUNT_KEY: np.array([sums[6]]),
+                    NORM_KEY: np.array([sums[7]])}
+        aggregate = DeviceStatistics(flat=agg_flat, dims=dict(plan.model.param_dims), weight=float(sums[8]),
+                                     bookkeeping=book, workspace=self.ws, comm=self._comm)
+        for proc in reversed(self._postprocessors):
+            try:
+                aggregate, server_metrics = proc.postprocess_server(aggregate, ctx)
+            except Exception as exc:
+                raise EngineError(
+                    f"iteration {ctx.iteration}, population {pop_key.value!r}: server postprocessor "
+                    f"{type(proc).__name__} failed: {exc}"
+                ) from exc
+            metrics = merge_metrics(metrics, server_metrics)
+        return aggregate, metrics, cohort

@@ -1,0 +1,208 @@
+"""Model layouts and central optimizers for the GPU path.
+
+A model here is a *layout*: ordered parameter entries (the payload order
+of every flat device buffer), an initialiser that replays the reference's
+numpy draws, and the geometry the sm_100a kernels need.  The arithmetic
+lives in ``csrc/`` -- there is no host forward/backward (no CPU fallback).
+
+* ``LogisticRegression`` -- fedsim/models/models.py:88-142 (zeros init).
+* ``MLP``                -- fedsim/models/models.py:145-228
+                            (U(+-1/sqrt(fan_in)) in entry order).
+* ``CNN``                -- the BASELINE "small CIFAR-10 CNN", absent from
+  the reference ("Assumed CNN"): conv3x3(3->32)+ReLU,
+  conv3x3(32->64)+ReLU, maxpool 2x2, flatten(12544), fc128+ReLU, fc10,
+  valid convolutions, no dropout.  D = 1,626,442.  Conv weights are
+  [out][in][kh][kw], fc weights [in][out] (the reference's ``X @ W``
+  convention); inputs are CHW rows of 3*32*32.  Initialised like the
+  reference MLP: U(+-1/sqrt(fan_in)) drawn in entry order.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Mapping
+
+import numpy as np
+
+from .core import HyperParam, make_rng, resolve
+
+
+class Model:
+    """Layout contract shared by every model (fedsim/models/models.py:21-51)."""
+
+    kind: str = ""
+
+    @property
+    def param_dims(self) -> dict[str, int]:
+        raise NotImplementedError
+
+    @property
+    def num_params(self) -> int:
+        return sum(self.param_dims.values())
+
+    def init_params(self, seed: int) -> dict[str, np.ndarray]:
+        raise NotImplementedError
+
+    def _uniform_init(self, seed: int, fan_in: Mapping[str, int]) -> dict[str, np.ndarray]:
+        rng = make_rng(seed)
+        out = {}
+        for name, n in self.param_dims.items():
+            bound = 1.0 / np.sqrt(fan_in[name])
+            out[name] = rng.uniform(-bound, bound, n)
+        return out
+
+
+@dataclass(frozen=True)
+class LogisticRegression(Model):
+    dim: int
+    num_classes: int
+    kind = "linear"
+
+    @property
+    def param_dims(self) -> dict[str, int]:
+        return {"weights": self.dim * self.num_classes, "bias": self.num_classes}
+
+    def init_params(self, seed: int) -> dict[str, np.ndarray]:
+        return {n: np.zeros(k) for n, k in self.param_dims.items()}
+
+    @property
+    def input_dim(self) -> int:
+        return self.dim
+
+
+@dataclass(frozen=True)
+class MLP(Model):
+    dim: int
+    hidden_units: int
+    num_classes: int
+    kind = "mlp"
+
+    @property
+    def param_dims(self) -> dict[str, int]:
+        return {
+            "layer1/weights": self.dim * self.hidden_units,
+            "layer1/bias": self.hidden_units,
+            "layer2/weights": self.hidden_units * self.num_classes,
+            "layer2/bias": self.num_classes,
+        }
+
+    def init_params(self, seed: int) -> dict[str, np.ndarray]:
+        # entries are drawn W1, b1, W2, b2 from one stream
+        # (fedsim/models/models.py:162-175)
+        d, h = self.dim, self.hidden_units
+        return self._uniform_init(
+            seed, {"layer1/weights": d, "layer1/bias": d, "layer2/weights": h, "layer2/bias": h}
+        )
+
+    @property
+    def input_dim(self) -> int:
+        return self.dim
+
+
+@dataclass(frozen=True)
+class CNN(Model):
+    in_channels: int = 3
+    image_size: int = 32
+    conv1_channels: int = 32
+    conv2_channels: int = 64
+    hidden_units: int = 128
+    num_classes: int = 10
+    kind = "cnn"
+
+    @property
+    def conv1_out(self) -> int:  # spatial side after conv1 (valid 3x3)
+        return self.image_size - 2
+
+    @property
+    def conv2_out(self) -> int:
+        return self.image_size - 4
+
+    @property
+    def pool_out(self) -> int:
+        return self.conv2_out // 2
+
+    @property
+    def flat_dim(self) -> int:
+        return self.conv2_channels * self.pool_out * self.pool_out
+
+    @property
+    def input_dim(self) -> int:
+        return self.in_channels * self.image_size * self.image_size
+
+    @property
+    def param_dims(self) -> dict[str, int]:
+        c0, c1, c2 = self.in_channels, self.conv1_channels, self.conv2_channels
+        return {
+            "conv1/weights": c1 * c0 * 9,
+            "conv1/bias": c1,
+            "conv2/weights": c2 * c1 * 9,
+            "conv2/bias": c2,
+            "fc1/weights": self.flat_dim * self.hidden_units,
+            "fc1/bias": self.hidden_units,
+            "fc2/weights": self.hidden_units * self.num_classes,
+            "fc2/bias": self.num_classes,
+        }
+
+    def init_params(self, seed: int) -> dict[str, np.ndarray]:
+        c0, c1 = self.in_channels, self.conv1_channels
+        fan = {
+            "conv1/weights": c0 * 9, "conv1/bias": c0 * 9,
+            "conv2/weights": c1 * 9, "conv2/bias": c1 * 9,
+            "fc1/weights": self.flat_dim, "fc1/bias": self.flat_dim,
+            "fc2/weights": self.hidden_units, "fc2/bias": self.hidden_units,
+        }
+        return self._uniform_init(seed, fan)
+
+    def forward_flops_per_sample(self) -> int:
+        """2 x MACs of one forward pass (33.67 MFLOP)."""
+        s1, s2 = self.conv1_out, self.conv2_out
+        macs = (
+            s1 * s1 * self.conv1_channels * self.in_channels * 9
+            + s2 * s2 * self.conv2_channels * self.conv1_channels * 9
+            + self.flat_dim * self.hidden_units
+            + self.hidden_units * self.num_classes
+        )
+        return 2 * macs
+
+
+def count_local_steps(num_points: int, local_params) -> int:
+    """E * ceil(n / B) (fedsim/models/models.py:267-272)."""
+    if num_points == 0:
+        return 0
+    return local_params.num_epochs * (-(-num_points // local_params.batch_size))
+
+
+# --------------------------------------------------------------------------
+# central optimizers (fedsim/models/optimizers.py:13-87)
+
+
+class SGDOptimizer:
+    """theta <- theta - lr * averaged_delta (fedsim/models/optimizers.py:13-21).
+
+    On the GPU path the step is one fused kernel that also adds the
+    pending central DP noise and divides by the total weight."""
+
+    def __init__(self, learning_rate: "float | HyperParam"):
+        self.learning_rate = learning_rate
+
+    def step(self, params, direction, iteration: int):
+        lr = resolve(self.learning_rate, iteration)
+        if hasattr(direction, "apply_sgd"):
+            return direction.apply_sgd(params, lr)
+        return {n: params[n] - lr * direction[n] for n in params}
+
+
+CentralOptimizer = SGDOptimizer
+
+
+def central_step(optimizer, params, averaged_delta, iteration: int):
+    """Apply one central update from an averaged delta (weight 1)
+    (fedsim/models/optimizers.py:74-87)."""
+    if averaged_delta.weight != 1.0:
+        raise ValueError(
+            "central_step expects an averaged delta (weight 1), "
+            f"got weight {averaged_delta.weight}"
+        )
+    if hasattr(averaged_delta, "apply_sgd"):
+        return optimizer.step(params, averaged_delta, iteration)
+    return optimizer.step(params, averaged_delta.entries, iteration)

@@ -1,0 +1,82 @@
+"""Build the golden-fixture configurations with the product (host mirror)
+and with the oracle, from tests/golden/configs.py."""
+
+from __future__ import annotations
+
+import numpy as np
+
+import paper_2404_06430_b200 as fb
+from oracle import port
+from tests.golden.configs import CONFIGS
+
+
+def product_datasets(cfg):
+    ppu = cfg["ppu"]
+    ntr, nva = cfg["users"] * ppu, cfg["val_users"] * ppu
+    X, y = fb.make_synthetic_classification(ntr + nva, dim=cfg["dim"], num_classes=cfg["classes"],
+                                            margin=cfg["margin"], seed=fb.derive_seed(cfg["data_seed"], "pool"))
+    train = fb.partition_iid(X[:ntr], y[:ntr], ppu, seed=fb.derive_seed(cfg["data_seed"], "train", "split"),
+                             population=fb.Population.TRAIN, id_prefix="train")
+    val = fb.partition_iid(X[ntr:], y[ntr:], ppu, seed=fb.derive_seed(cfg["data_seed"], "val", "split"),
+                           population=fb.Population.VAL, id_prefix="val")
+    return {fb.Population.TRAIN: train, fb.Population.VAL: val}
+
+
+def product_model(cfg):
+    if cfg["model"] == "mlp":
+        return fb.MLP(cfg["dim"], cfg["hidden"], cfg["classes"])
+    if cfg["model"] == "logistic":
+        return fb.LogisticRegression(cfg["dim"], cfg["classes"])
+    return fb.CNN()
+
+
+def oracle_model(cfg):
+    if cfg["model"] == "mlp":
+        return port.Mlp(cfg["dim"], cfg["hidden"], cfg["classes"])
+    if cfg["model"] == "logistic":
+        return port.Linear(cfg["dim"], cfg["classes"])
+    return port.Cnn()
+
+
+def noise_base(cfg) -> int:
+    return fb.derive_seed(cfg["run_seed"], "noise-stream", cfg["noise_seed"])
+
+
+def product_run_parts(cfg, noise_source="numpy", sigma=None):
+    """(algorithm, postprocessors) built with the product's mirror API."""
+    alg = fb.FedAvg(product_model(cfg), fb.SGDOptimizer(cfg["clr"]), total_iterations=cfg["iterations"],
+                    cohort_size=cfg["cohort"], local_learning_rate=cfg["lr"], local_num_epochs=cfg["epochs"],
+                    local_batch_size=cfg["batch"], eval_frequency=cfg["eval_every"],
+                    eval_cohort_size=cfg["eval_cohort"], weighting=cfg["weighting"], run_seed=cfg["run_seed"],
+                    init_seed=cfg["init_seed"])
+    post = []
+    if cfg["bound"] is not None:
+        clip = fb.ClippingPostprocessor(cfg["bound"])
+        post = [clip, fb.GaussianCentralMechanism(clip, sigma=cfg["sigma"] if sigma is None else sigma,
+                                                  r=cfg["r"], noise_base_seed=noise_base(cfg),
+                                                  noise_source=noise_source)]
+    return alg, post
+
+
+def users_of(ds) -> dict:
+    return {u.user_id: (u.features, u.labels) for u in ds.users.values()}
+
+
+def oracle_run(cfg, world=None):
+    ds = product_datasets(cfg)
+    return port.run_fedavg(
+        oracle_model(cfg), users_of(ds[fb.Population.TRAIN]), users_of(ds[fb.Population.VAL]),
+        iterations=cfg["iterations"], cohort=cfg["cohort"], eval_cohort=cfg["eval_cohort"],
+        eval_every=cfg["eval_every"], lr=cfg["lr"], epochs=cfg["epochs"], batch=cfg["batch"], clr=cfg["clr"],
+        weighting=cfg["weighting"], bound=cfg["bound"], sigma=cfg["sigma"], r=cfg["r"],
+        noise_base=noise_base(cfg), run_seed=cfg["run_seed"], init_seed=cfg["init_seed"],
+        world=cfg["workers"] if world is None else world)
+
+
+def golden_rows(g):
+    return [(int(t), str(p), str(n), float(v), float(w))
+            for t, p, n, v, w in zip(g["row_t"], g["row_pop"], g["row_name"], g["row_value"], g["row_weight"])]
+
+
+__all__ = ["CONFIGS", "product_datasets", "product_model", "oracle_model", "product_run_parts", "oracle_run",
+           "golden_rows", "users_of", "noise_base"]
