@@ -94,6 +94,32 @@ int fb_local_sgd_mlp_f32(const float* theta_t, int dim, int hidden, int num_clas
                          float* delta_out, int64_t ld_delta, int32_t* nonfinite,
                          void* stream);
 
+/* ----------------------------------------------------------------- CNN
+ * The BASELINE "small CIFAR-10 CNN" (paper_2404_06430_b200/models.py:CNN):
+ * conv3x3(3->32)+ReLU, conv3x3(32->64)+ReLU, maxpool2, fc(12544->128)+ReLU,
+ * fc(128->10), valid convolutions, CHW input rows of 3072, D = 1,626,442.
+ * The reference has no CNN; these replace the generic Model.fit_local loop
+ * (fedsim/models/models.py:53-79) and evaluate_model (:275-296) for a Model
+ * with that layout, batched over the cohort (one SGD step of every client
+ * per sequence of layer kernels).
+ * max_slots = samples processed per layer launch (>= batch_size; clients
+ * are trained in waves of max_slots / batch_size); the workspace for a
+ * given max_slots and client count comes from fb_cnn_workspace_bytes.
+ * max_steps = max over clients of epochs * ceil(n_c / batch_size).
+ * batch_size <= 16.  nonfinite[] is zeroed (non-finite deltas are caught by
+ * fb_delta_norm_clip_f32).                                                 */
+int64_t fb_cnn_workspace_bytes(int max_slots, int max_clients);
+int fb_eval_cnn_f32(const float* theta, const float* X, const int32_t* y,
+                    const int64_t* row_start, const int32_t* num_rows, int num_clients,
+                    int64_t total_rows, double* loss_sum, int32_t* correct,
+                    int max_slots, void* workspace, int64_t workspace_bytes, void* stream);
+int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
+                         const int64_t* row_start, const int32_t* num_rows,
+                         const int32_t* perms, const int64_t* perm_off, int num_clients,
+                         int epochs, int batch_size, int max_steps, float lr, float prox_mu,
+                         float* delta_out, int64_t ld_delta, int32_t* nonfinite,
+                         int max_slots, void* workspace, int64_t workspace_bytes, void* stream);
+
 /* ------------------------------------------------- a6 + a7 (kernel K2)
  * For every client c: norm[c] = || w[c] * delta[c, :D] ||_2 (fp64
  * accumulation), clipped[c] = norm[c] > bound (strict), coef[c] =

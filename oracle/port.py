@@ -153,6 +153,23 @@ class Mlp:
         return _eval_rows(h @ W2 + p["layer2/bias"], y)
 
 
+# Decision margins of the last CNN forwards (test instrumentation): fp32 vs
+# float64 can only disagree on a ReLU sign or a max-pool winner when the
+# float64 value sits within ~1e-6 (relative) of that decision boundary.
+MARGINS: list[float] = []
+TRACK_MARGINS = False
+
+
+def _record_margin(*vals):
+    if TRACK_MARGINS:
+        MARGINS.append(min(vals))
+
+
+def _relu_margin(z: np.ndarray) -> float:
+    scale = float(np.sqrt(np.mean(z * z))) or 1.0
+    return float(np.abs(z).min()) / scale
+
+
 def _im2col3(x: np.ndarray) -> np.ndarray:
     """[N, C, H, W] -> [N, (H-2)*(W-2), C*9] with (c, kh, kw) column order."""
     win = np.lib.stride_tricks.sliding_window_view(x, (3, 3), axis=(2, 3))  # N,C,Ho,Wo,3,3
@@ -221,9 +238,17 @@ class Cnn:
         win = a2.reshape(N, self.c2, sp, 2, sp, 2).transpose(0, 1, 2, 4, 3, 5).reshape(N, self.c2, sp, sp, 4)
         arg = win.argmax(axis=4)  # first maximum in (0,0),(0,1),(1,0),(1,1) order
         pooled = np.take_along_axis(win, arg[..., None], axis=4)[..., 0]
+        if TRACK_MARGINS:
+            srt = np.sort(win, axis=4)
+            live = srt[..., 3] > 0
+            gap = (srt[..., 3] - srt[..., 2])[live]
+            scale = float(np.sqrt(np.mean(z2 * z2))) or 1.0
+            pool_gap = float(gap.min()) / scale if gap.size else np.inf
+            _record_margin(_relu_margin(z1), _relu_margin(z2), pool_gap)
         flat = pooled.reshape(N, -1)
         z3 = flat @ p["fc1/weights"].reshape(self.flat, self.hid) + p["fc1/bias"]
         a3 = np.maximum(z3, 0.0)
+        _record_margin(_relu_margin(z3))
         logits = a3 @ p["fc2/weights"].reshape(self.hid, self.k) + p["fc2/bias"]
         return dict(cols1=cols1, z1=z1, cols2=cols2, z2=z2, arg=arg, flat=flat, z3=z3, a3=a3), logits
 

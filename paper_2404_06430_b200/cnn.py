@@ -1,0 +1,49 @@
+"""Host glue for the CNN entry points (fb_eval_cnn_f32 / fb_local_sgd_cnn_f32).
+
+Chooses the slot count per layer launch (every client's step-s minibatch in
+one wave when it fits the memory budget) and sizes the workspace.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import native
+
+# samples per layer launch; ~0.35 MB of activations per slot -> <= ~6 GB
+MAX_SLOTS = 16384
+EVAL_GROUP = 16
+
+
+def _slots(C: int, B: int) -> int:
+    per_wave = max(1, min(C, MAX_SLOTS // B))
+    return per_wave * B
+
+
+def _eval_slots(total_rows: int) -> int:
+    n = min(MAX_SLOTS, max(EVAL_GROUP, int(total_rows)))
+    return (n + EVAL_GROUP - 1) // EVAL_GROUP * EVAL_GROUP
+
+
+def eval_cohort(runner, theta, pop, row_start, num_rows, C, loss, correct, stream, h_num_rows):
+    total = int(np.asarray(h_num_rows, dtype=np.int64).sum())
+    slots = _eval_slots(total)
+    nbytes = native.call("fb_cnn_workspace_bytes", slots, C)
+    ws = runner.ws.get("cnn_ws", nbytes)
+    native.call("fb_eval_cnn_f32", native.ptr(theta), native.ptr(pop.X), native.ptr(pop.y), native.ptr(row_start),
+                native.ptr(num_rows), C, total, native.ptr(loss), native.ptr(correct), slots, native.ptr(ws),
+                ws.numel(), stream)
+
+
+def local_sgd_cohort(runner, theta, pop, row_start, num_rows, perms, perm_off, C, tp, prox_mu, delta, nonfinite,
+                     stream, h_num_rows):
+    B = tp.batch_size
+    n = np.asarray(h_num_rows, dtype=np.int64)
+    max_steps = int((tp.num_epochs * ((n + B - 1) // B)).max()) if len(n) else 0
+    slots = _slots(C, B)
+    nbytes = native.call("fb_cnn_workspace_bytes", slots, slots // B)
+    ws = runner.ws.get("cnn_ws", nbytes)
+    native.call("fb_local_sgd_cnn_f32", native.ptr(theta), native.ptr(pop.X), native.ptr(pop.y),
+                native.ptr(row_start), native.ptr(num_rows), native.ptr(perms), native.ptr(perm_off), C,
+                tp.num_epochs, B, max_steps, float(tp.learning_rate), float(prox_mu), native.ptr(delta),
+                runner.ld, native.ptr(nonfinite), slots, native.ptr(ws), ws.numel(), stream)

@@ -1,0 +1,775 @@
+// Cohort-batched local SGD and evaluation for the BASELINE CIFAR-10 CNN:
+//   conv3x3(3->32)+ReLU -> conv3x3(32->64)+ReLU -> maxpool2 -> fc(12544->128)+ReLU -> fc(128->10)
+// (valid convolutions; paper_2404_06430_b200/models.py:CNN).  The reference
+// has no CNN; the update rule is the generic Model.fit_local loop
+// (fedsim/models/models.py:53-79) -- every gradient of a step is formed at
+// the step's starting weights, then theta <- theta - lr*(g + mu*(theta-theta_t)).
+//
+// Execution model: one SGD step of the WHOLE cohort per sequence of layer
+// kernels ("slots" = the <= B samples of every client in this step, slot
+// n = c*B + j).  Every client's current weights are theta_t - delta_c, read
+// on the fly (theta_t is shared and L2-resident; delta_c is the client's row
+// of the [C, ld] delta matrix the clip/aggregate kernels consume).  Layer
+// kernels, per step:
+//   slots        perms -> dataset row per slot
+//   conv1_fwd    gather x, conv1+ReLU            -> a1   [N,30,30,32] NHWC
+//   conv2_fwd    conv2+ReLU+maxpool (argmax kept) -> pooled [N,12544] CHW, code
+//   fc1_fwd      split-K, per-client weights     -> partial z3
+//   head         fc1 bias/ReLU, fc2, softmax-CE, dz3, fc2 + fc1-bias updates
+//   fc1_bwd      dp = dz3 W^T (old W), delta_fc1 += lr * p^T dz3
+//   conv2_bwd_x  dz1 = (unpool(dp) * relu') conv^T W2 * relu'(a1)
+//   conv2_bwd_w  dW2 over the client's slots (max-pool sparsity), update
+//   conv1_bwd_w  dW1 over the client's slots, update
+// Evaluation runs the forward kernels at theta_t over all cohort rows in
+// chunks of N slots and reduces loss / hits per client.
+
+#include "fb_common.cuh"
+
+namespace fb {
+namespace cnn {
+
+constexpr int C0 = 3, S0 = 32, C1 = 32, S1 = 30, C2 = 64, S2 = 28, SP = 14;
+constexpr int NPOOL = SP * SP;         // 196
+constexpr int FLAT = C2 * NPOOL;       // 12544
+constexpr int HID = 128, NCLS = 10;
+constexpr int IMG = C0 * S0 * S0;      // 3072
+constexpr int A1 = S1 * S1 * C1;       // 28800
+constexpr int A1P = 33;                // padded channel stride of a1 in smem
+
+// flat parameter offsets (entry order of models.CNN.param_dims)
+constexpr int64_t O_W1 = 0, O_B1 = O_W1 + C1 * C0 * 9, O_W2 = O_B1 + C1, O_B2 = O_W2 + C2 * C1 * 9,
+                  O_F1 = O_B2 + C2, O_BF1 = O_F1 + (int64_t)FLAT * HID, O_F2 = O_BF1 + HID,
+                  O_BF2 = O_F2 + HID * NCLS, D = O_BF2 + NCLS;
+static_assert(D == 1626442, "CNN parameter count");
+
+constexpr int GMAX = 16;       // max samples per weight group (batch size limit)
+constexpr int KSPLIT = 14;     // fc1 split-K factor (12544 = 14 * 896)
+constexpr int KCHUNK = FLAT / KSPLIT;
+constexpr int FC1F_SMEM = GMAX * KCHUNK * 4;
+static_assert(FLAT % KSPLIT == 0, "fc1 split");
+
+struct Step {
+  float lr, mu;
+};
+
+// weight of the client owning `dc` (nullptr = shared theta_t)
+__device__ __forceinline__ float wt(const float* __restrict__ th, const float* __restrict__ dc, int64_t i) {
+  return dc ? th[i] - dc[i] : th[i];
+}
+
+// ---------------------------------------------------------------- slots
+// training step `step`: slot (c, j) -> dataset row (or -1), client batch size
+__global__ void train_slots_kernel(int step, const int64_t* __restrict__ row_start,
+                                   const int32_t* __restrict__ num_rows, const int32_t* __restrict__ perms,
+                                   const int64_t* __restrict__ perm_off, int C, int E, int B,
+                                   int64_t* __restrict__ slot_row, int32_t* __restrict__ client_nb) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= C * B) return;
+  const int c = t / B, j = t - c * B;
+  const int n = num_rows[c];
+  const int spe = (n + B - 1) / B;
+  int nb = 0;
+  int64_t row = -1;
+  if (step < E * spe) {
+    const int e = step / spe, b = step - e * spe;
+    nb = min(B, n - b * B);
+    if (j < nb) row = row_start[c] + perms[perm_off[c] + (int64_t)e * n + (int64_t)b * B + j];
+  }
+  slot_row[t] = row;
+  if (j == 0) client_nb[c] = nb;
+}
+
+// evaluation chunk: cohort rows [r0, r0+N) -> (dataset row, client)
+__global__ void eval_slots_kernel(int64_t r0, int N, int64_t total, const int64_t* __restrict__ prefix, int C,
+                                  const int64_t* __restrict__ row_start, int64_t* __restrict__ slot_row,
+                                  int32_t* __restrict__ slot_client) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  const int64_t r = r0 + n;
+  if (r >= total) {
+    slot_row[n] = -1;
+    slot_client[n] = -1;
+    return;
+  }
+  int lo = 0, hi = C;  // largest c with prefix[c] <= r
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (prefix[mid] <= r) lo = mid; else hi = mid;
+  }
+  slot_row[n] = row_start[lo] + (r - prefix[lo]);
+  slot_client[n] = lo;
+}
+
+__global__ void prefix_kernel(const int32_t* __restrict__ num_rows, int C, int64_t* __restrict__ prefix) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    int64_t s = 0;
+    for (int c = 0; c < C; ++c) {
+      prefix[c] = s;
+      s += num_rows[c];
+    }
+    prefix[C] = s;
+  }
+}
+
+// ------------------------------------------------------------ conv1 fwd
+// one CTA per slot; thread per output position, all 32 channels
+__global__ void __launch_bounds__(256) conv1_fwd_kernel(const float* __restrict__ X,
+                                                        const int64_t* __restrict__ slot_row,
+                                                        const float* __restrict__ theta,
+                                                        const float* __restrict__ delta, int64_t ld, int B,
+                                                        float* __restrict__ a1) {
+  __shared__ float img[IMG];
+  __shared__ float w[27 * C1 + C1];  // [tap27][o] then bias
+  const int n = blockIdx.x;
+  const int64_t row = slot_row[n];
+  if (row < 0) return;
+  const float* dc = delta ? delta + (int64_t)(n / B) * ld : nullptr;
+  for (int i = threadIdx.x; i < IMG; i += blockDim.x) img[i] = X[row * IMG + i];
+  for (int i = threadIdx.x; i < 27 * C1; i += blockDim.x) {
+    const int o = i / 27, r = i - o * 27;  // OIHW source, [ci*9+ky*3+kx]
+    w[r * C1 + o] = wt(theta, dc, O_W1 + i);
+  }
+  for (int o = threadIdx.x; o < C1; o += blockDim.x) w[27 * C1 + o] = wt(theta, dc, O_B1 + o);
+  __syncthreads();
+  float* out = a1 + (int64_t)n * A1;
+  for (int p = threadIdx.x; p < S1 * S1; p += blockDim.x) {
+    const int y = p / S1, x = p - y * S1;
+    float acc[C1];
+#pragma unroll
+    for (int o = 0; o < C1; ++o) acc[o] = w[27 * C1 + o];
+#pragma unroll 1
+    for (int ci = 0; ci < C0; ++ci)
+#pragma unroll
+      for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+        for (int kx = 0; kx < 3; ++kx) {
+          const float v = img[ci * S0 * S0 + (y + ky) * S0 + x + kx];
+          const float* wr = w + (ci * 9 + ky * 3 + kx) * C1;
+#pragma unroll
+          for (int o = 0; o < C1; ++o) acc[o] = fmaf(v, wr[o], acc[o]);
+        }
+    float4* dst = reinterpret_cast<float4*>(out + (int64_t)p * C1);
+#pragma unroll
+    for (int q = 0; q < C1 / 4; ++q)
+      dst[q] = make_float4(fmaxf(acc[4 * q], 0.f), fmaxf(acc[4 * q + 1], 0.f), fmaxf(acc[4 * q + 2], 0.f),
+                           fmaxf(acc[4 * q + 3], 0.f));
+  }
+}
+
+// ------------------------------------------------- conv2 fwd + ReLU + pool
+// one CTA per slot; a1 of the slot staged in smem (channel stride padded to
+// 33 floats: conflict-free reads across positions); work item = one pooled
+// position x 16 output channels (4 window positions x 16 accumulators)
+constexpr int C2F_SMEM = (S1 * S1 * A1P + 9 * C1 * C2 + C2) * 4;
+
+__global__ void __launch_bounds__(256) conv2_fwd_pool_kernel(const float* __restrict__ a1,
+                                                             const int64_t* __restrict__ slot_row,
+                                                             const float* __restrict__ theta,
+                                                             const float* __restrict__ delta, int64_t ld,
+                                                             int B, float* __restrict__ pooled,
+                                                             uint8_t* __restrict__ code) {
+  extern __shared__ float sm[];
+  float* as = sm;                          // [900][33]
+  float* ws = as + S1 * S1 * A1P;          // [tap9][ci32][o64]
+  float* bs = ws + 9 * C1 * C2;            // [64]
+  const int n = blockIdx.x;
+  if (slot_row[n] < 0) return;
+  const float* dc = delta ? delta + (int64_t)(n / B) * ld : nullptr;
+  const float* src = a1 + (int64_t)n * A1;
+  for (int i = threadIdx.x; i < A1; i += blockDim.x) as[(i >> 5) * A1P + (i & 31)] = src[i];
+  for (int i = threadIdx.x; i < C2 * C1 * 9; i += blockDim.x) {
+    const int o = i / (C1 * 9), r = i - o * (C1 * 9), ci = r / 9, tap = r - ci * 9;
+    ws[(tap * C1 + ci) * C2 + o] = wt(theta, dc, O_W2 + i);
+  }
+  for (int o = threadIdx.x; o < C2; o += blockDim.x) bs[o] = wt(theta, dc, O_B2 + o);
+  __syncthreads();
+  float* pout = pooled + (int64_t)n * FLAT;
+  uint8_t* cout = code + (int64_t)n * FLAT;
+  for (int item = threadIdx.x; item < NPOOL * 4; item += blockDim.x) {
+    const int og = item / NPOOL, pp = item - og * NPOOL;  // consecutive threads: consecutive positions
+    const int py = pp / SP, px = pp - py * SP;
+    float acc[4][16];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int o = 0; o < 16; ++o) acc[q][o] = 0.f;
+#pragma unroll 1
+    for (int tap = 0; tap < 9; ++tap) {
+      const int ky = tap / 3, kx = tap - ky * 3;
+      const float* a00 = as + ((2 * py + ky) * S1 + 2 * px + kx) * A1P;
+      const float* wr = ws + tap * C1 * C2 + og * 16;
+#pragma unroll 4
+      for (int ci = 0; ci < C1; ++ci) {
+        const float v0 = a00[ci], v1 = a00[A1P + ci], v2 = a00[S1 * A1P + ci], v3 = a00[(S1 + 1) * A1P + ci];
+        const float4* w4 = reinterpret_cast<const float4*>(wr + ci * C2);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 wv = w4[q];
+          const float wq[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            acc[0][4 * q + e] = fmaf(v0, wq[e], acc[0][4 * q + e]);
+            acc[1][4 * q + e] = fmaf(v1, wq[e], acc[1][4 * q + e]);
+            acc[2][4 * q + e] = fmaf(v2, wq[e], acc[2][4 * q + e]);
+            acc[3][4 * q + e] = fmaf(v3, wq[e], acc[3][4 * q + e]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < 16; ++o) {
+      const int oc = og * 16 + o;
+      const float b = bs[oc];
+      float best = fmaxf(acc[0][o] + b, 0.f);
+      int arg = 0;
+#pragma unroll
+      for (int q = 1; q < 4; ++q) {
+        const float v = fmaxf(acc[q][o] + b, 0.f);
+        if (v > best) { best = v; arg = q; }  // first maximum in (0,0),(0,1),(1,0),(1,1) order
+      }
+      pout[oc * NPOOL + pp] = best;
+      cout[oc * NPOOL + pp] = (uint8_t)arg;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- fc1 fwd
+// grid (groups, KSPLIT): group = G consecutive slots sharing weights (a client
+// in training, G = B; a chunk of rows at theta_t in evaluation, G = GMAX);
+// thread j = output unit; part[split][n][j]
+__global__ void __launch_bounds__(HID) fc1_fwd_kernel(const float* __restrict__ pooled,
+                                                      const int64_t* __restrict__ slot_row, int N, int G,
+                                                      const float* __restrict__ theta,
+                                                      const float* __restrict__ delta, int64_t ld,
+                                                      float* __restrict__ part) {
+  extern __shared__ float ps_flat[];  // [GMAX][KCHUNK], rows >= G zero
+  auto ps = reinterpret_cast<float(*)[KCHUNK]>(ps_flat);
+  const int g = blockIdx.x, split = blockIdx.y, j = threadIdx.x;
+  const int n0 = g * G;
+  const int k0 = split * KCHUNK;
+  const float* dc = delta ? delta + (int64_t)g * ld : nullptr;
+  int live = 0;
+  for (int b = 0; b < G && n0 + b < N; ++b) live += slot_row[n0 + b] >= 0;
+  if (!live) return;
+  for (int i = threadIdx.x; i < GMAX * KCHUNK; i += blockDim.x) {
+    const int b = i / KCHUNK, k = i - b * KCHUNK;
+    const int n = n0 + b;
+    ps[b][k] = (b < G && n < N && slot_row[n] >= 0) ? pooled[(int64_t)n * FLAT + k0 + k] : 0.f;
+  }
+  __syncthreads();
+  float acc[GMAX];
+#pragma unroll
+  for (int b = 0; b < GMAX; ++b) acc[b] = 0.f;
+  const float* th = theta + O_F1 + (int64_t)k0 * HID + j;
+  const float* dd = dc ? dc + O_F1 + (int64_t)k0 * HID + j : nullptr;
+#pragma unroll 4
+  for (int k = 0; k < KCHUNK; ++k) {
+    const float w = dd ? th[(int64_t)k * HID] - dd[(int64_t)k * HID] : th[(int64_t)k * HID];
+#pragma unroll
+    for (int b = 0; b < GMAX; ++b) acc[b] = fmaf(ps[b][k], w, acc[b]);
+  }
+#pragma unroll
+  for (int b = 0; b < GMAX; ++b)
+    if (b < G && n0 + b < N) part[((int64_t)split * N + n0 + b) * HID + j] = acc[b];
+}
+
+// ------------------------------------------------------------------ head
+// one CTA per group.  Eval: per-slot loss / hit.  Train: softmax-CE grad of
+// the mean batch loss, dz3, and the fc2 + fc1-bias updates of the client.
+__global__ void __launch_bounds__(HID) head_kernel(const float* __restrict__ part,
+                                                   const int64_t* __restrict__ slot_row, int N, int G,
+                                                   const int32_t* __restrict__ yl,
+                                                   const float* __restrict__ theta, float* __restrict__ delta,
+                                                   int64_t ld, const int32_t* __restrict__ client_nb, Step st,
+                                                   float* __restrict__ dz3, double* __restrict__ slot_loss,
+                                                   int32_t* __restrict__ slot_hit) {
+  __shared__ float z3[GMAX][HID];
+  __shared__ float lg[GMAX][NCLS];
+  __shared__ float w2[HID * NCLS + NCLS];
+  __shared__ int lab[GMAX];
+  const int g = blockIdx.x, j = threadIdx.x;
+  const int n0 = g * G;
+  const bool train = delta != nullptr;
+  float* dc = train ? delta + (int64_t)g * ld : nullptr;
+  const int nb = train ? client_nb[g] : 0;
+  if (train && nb == 0) return;
+  for (int i = j; i < HID * NCLS + NCLS; i += blockDim.x) w2[i] = wt(theta, dc, O_F2 + i);
+  const float bf1 = wt(theta, dc, O_BF1 + j);
+  for (int b = 0; b < G; ++b) {
+    const int n = n0 + b;
+    float z = 0.f;
+    if (n < N && slot_row[n] >= 0) {
+      z = bf1;
+      for (int s = 0; s < KSPLIT; ++s) z += part[((int64_t)s * N + n) * HID + j];
+    }
+    z3[b][j] = z;
+  }
+  if (j < G) {
+    const int n = n0 + j;
+    lab[j] = (n < N && slot_row[n] >= 0) ? yl[slot_row[n]] : -1;
+  }
+  __syncthreads();
+  for (int t = j; t < G * NCLS; t += blockDim.x) {
+    const int b = t / NCLS, q = t - b * NCLS;
+    float v = w2[HID * NCLS + q];
+    for (int h = 0; h < HID; ++h) v = fmaf(fmaxf(z3[b][h], 0.f), w2[h * NCLS + q], v);
+    lg[b][q] = v;
+  }
+  __syncthreads();
+  if (j < G && lab[j] >= 0) {
+    float* row = lg[j];
+    float mx = row[0];
+    int arg = 0;
+    for (int q = 1; q < NCLS; ++q)
+      if (row[q] > mx) { mx = row[q]; arg = q; }
+    float s = 0.f;
+    for (int q = 0; q < NCLS; ++q) s += expf(row[q] - mx);
+    if (!train) {
+      slot_loss[n0 + j] = -((double)row[lab[j]] - (double)mx - (double)logf(s));
+      slot_hit[n0 + j] = arg == lab[j];
+    } else {
+      for (int q = 0; q < NCLS; ++q) {
+        float p = expf(row[q] - mx) / s;
+        if (q == lab[j]) p -= 1.f;
+        row[q] = p / (float)nb;
+      }
+    }
+  }
+  if (!train) return;
+  __syncthreads();
+  // dz3 (old fc2 weights), fc1 bias grad
+  float gb = 0.f;
+  for (int b = 0; b < nb; ++b) {
+    float d = 0.f;
+#pragma unroll
+    for (int q = 0; q < NCLS; ++q) d = fmaf(lg[b][q], w2[j * NCLS + q], d);
+    d = z3[b][j] > 0.f ? d : 0.f;
+    dz3[(int64_t)(n0 + b) * HID + j] = d;
+    gb += d;
+  }
+  // updates: theta <- theta - lr*(g + mu*(theta - theta_t)) == delta += lr*(g - mu*delta)
+  {
+    float& dl = dc[O_BF1 + j];
+    dl += st.lr * (gb - st.mu * dl);
+  }
+  for (int t = j; t < HID * NCLS; t += blockDim.x) {
+    const int h = t / NCLS, q = t - h * NCLS;
+    float gw = 0.f;
+    for (int b = 0; b < nb; ++b) gw = fmaf(fmaxf(z3[b][h], 0.f), lg[b][q], gw);
+    float& dl = dc[O_F2 + t];
+    dl += st.lr * (gw - st.mu * dl);
+  }
+  if (j < NCLS) {
+    float gw = 0.f;
+    for (int b = 0; b < nb; ++b) gw += lg[b][j];
+    float& dl = dc[O_BF2 + j];
+    dl += st.lr * (gw - st.mu * dl);
+  }
+}
+
+// ------------------------------------------------------- fc1 bwd + update
+// grid (C, KSPLIT); tiles of 32 rows x 128 units: dp = dz3 W^T at the old W,
+// then delta += lr * (p^T dz3 - mu * delta)
+__global__ void __launch_bounds__(HID) fc1_bwd_kernel(const float* __restrict__ pooled,
+                                                      const float* __restrict__ dz3, int B,
+                                                      const int32_t* __restrict__ client_nb,
+                                                      const float* __restrict__ theta, float* __restrict__ delta,
+                                                      int64_t ld, Step st, float* __restrict__ dp) {
+  constexpr int TR = 32;
+  __shared__ float wtile[TR][HID + 1];
+  __shared__ float dz[GMAX][HID];
+  __shared__ float pv[GMAX][TR];
+  const int c = blockIdx.x, split = blockIdx.y, j = threadIdx.x;
+  const int nb = client_nb[c];
+  if (nb == 0) return;
+  const int n0 = c * B;
+  float* dc = delta + (int64_t)c * ld;
+  for (int b = 0; b < nb; ++b) dz[b][j] = dz3[(int64_t)(n0 + b) * HID + j];
+  for (int k0 = split * KCHUNK; k0 < (split + 1) * KCHUNK; k0 += TR) {
+    __syncthreads();
+    for (int i = j; i < nb * TR; i += blockDim.x) {
+      const int b = i / TR, r = i - b * TR;
+      pv[b][r] = pooled[(int64_t)(n0 + b) * FLAT + k0 + r];
+    }
+    float dl[TR];
+#pragma unroll
+    for (int r = 0; r < TR; ++r) {
+      const int64_t idx = O_F1 + (int64_t)(k0 + r) * HID + j;
+      dl[r] = dc[idx];
+      wtile[r][j] = theta[idx] - dl[r];
+    }
+    __syncthreads();
+    // dp[b][k0+r] = sum_j dz[b][j] * w[r][j]: thread handles (b, r) pairs
+    for (int t = j; t < nb * TR; t += blockDim.x) {
+      const int b = t / TR, r = t - b * TR;
+      float s = 0.f;
+#pragma unroll 8
+      for (int h = 0; h < HID; ++h) s = fmaf(dz[b][h], wtile[r][h], s);
+      dp[(int64_t)(n0 + b) * FLAT + k0 + r] = s;
+    }
+#pragma unroll
+    for (int r = 0; r < TR; ++r) {
+      float gw = 0.f;
+      for (int b = 0; b < nb; ++b) gw = fmaf(pv[b][r], dz[b][j], gw);
+      dc[O_F1 + (int64_t)(k0 + r) * HID + j] = dl[r] + st.lr * (gw - st.mu * dl[r]);
+    }
+  }
+}
+
+// --------------------------------------------- conv2 backward (data) -> dz1
+// one CTA per active slot; g = dp * relu'(at argmax) kept sparse with its
+// window code; thread per a1 position, 32 input-channel accumulators
+constexpr int C2X_SMEM = (9 * C2 * C1 + C2 * NPOOL) * 4 + C2 * NPOOL;
+
+__global__ void __launch_bounds__(256) conv2_bwd_x_kernel(const float* __restrict__ dp,
+                                                          const float* __restrict__ pooled,
+                                                          const uint8_t* __restrict__ code,
+                                                          const float* __restrict__ a1,
+                                                          const int64_t* __restrict__ slot_row, int B,
+                                                          const float* __restrict__ theta,
+                                                          const float* __restrict__ delta, int64_t ld,
+                                                          float* __restrict__ dz1) {
+  extern __shared__ float sm[];
+  float* ws = sm;                      // [tap9][o64][ci32]
+  float* gs = ws + 9 * C2 * C1;        // [o64][196]
+  uint8_t* cs = reinterpret_cast<uint8_t*>(gs + C2 * NPOOL);
+  const int n = blockIdx.x;
+  if (slot_row[n] < 0) return;
+  const float* dc = delta + (int64_t)(n / B) * ld;
+  for (int i = threadIdx.x; i < C2 * C1 * 9; i += blockDim.x) {
+    const int o = i / (C1 * 9), r = i - o * (C1 * 9), ci = r / 9, tap = r - ci * 9;
+    ws[(tap * C2 + o) * C1 + ci] = theta[O_W2 + i] - dc[O_W2 + i];
+  }
+  for (int i = threadIdx.x; i < FLAT; i += blockDim.x) {
+    const int64_t s = (int64_t)n * FLAT + i;
+    gs[i] = pooled[s] > 0.f ? dp[s] : 0.f;
+    cs[i] = code[s];
+  }
+  __syncthreads();
+  const float* a1n = a1 + (int64_t)n * A1;
+  float* out = dz1 + (int64_t)n * A1;
+  for (int p = threadIdx.x; p < S1 * S1; p += blockDim.x) {
+    const int y = p / S1, x = p - y * S1;
+    float acc[C1];
+#pragma unroll
+    for (int ci = 0; ci < C1; ++ci) acc[ci] = 0.f;
+#pragma unroll 1
+    for (int tap = 0; tap < 9; ++tap) {
+      const int ky = tap / 3, kx = tap - ky * 3;
+      const int zy = y - ky, zx = x - kx;
+      if (zy < 0 || zx < 0 || zy >= S2 || zx >= S2) continue;
+      const int pp = (zy >> 1) * SP + (zx >> 1);
+      const int sub = ((zy & 1) << 1) | (zx & 1);
+      const float* wr = ws + tap * C2 * C1;
+#pragma unroll 2
+      for (int o = 0; o < C2; ++o) {
+        const float gv = cs[o * NPOOL + pp] == sub ? gs[o * NPOOL + pp] : 0.f;
+        if (gv == 0.f) continue;
+        const float4* w4 = reinterpret_cast<const float4*>(wr + o * C1);
+#pragma unroll
+        for (int q = 0; q < C1 / 4; ++q) {
+          const float4 wv = w4[q];
+          acc[4 * q] = fmaf(gv, wv.x, acc[4 * q]);
+          acc[4 * q + 1] = fmaf(gv, wv.y, acc[4 * q + 1]);
+          acc[4 * q + 2] = fmaf(gv, wv.z, acc[4 * q + 2]);
+          acc[4 * q + 3] = fmaf(gv, wv.w, acc[4 * q + 3]);
+        }
+      }
+    }
+    const float4* am = reinterpret_cast<const float4*>(a1n + (int64_t)p * C1);
+    float4* dst = reinterpret_cast<float4*>(out + (int64_t)p * C1);
+#pragma unroll
+    for (int q = 0; q < C1 / 4; ++q) {
+      const float4 m = am[q];
+      dst[q] = make_float4(m.x > 0.f ? acc[4 * q] : 0.f, m.y > 0.f ? acc[4 * q + 1] : 0.f,
+                           m.z > 0.f ? acc[4 * q + 2] : 0.f, m.w > 0.f ? acc[4 * q + 3] : 0.f);
+    }
+  }
+}
+
+// ------------------------------------------- conv2 backward (weights) + update
+// one CTA per client: dW2[o][tap][ci] = sum over slots and pooled positions
+// of g * a1(window argmax + tap); thread = (o, quarter of the 288 (tap,ci))
+constexpr int C2W_SMEM = (S1 * S1 * A1P + C2 * NPOOL) * 4 + C2 * NPOOL;
+
+__global__ void __launch_bounds__(256) conv2_bwd_w_kernel(const float* __restrict__ dp,
+                                                          const float* __restrict__ pooled,
+                                                          const uint8_t* __restrict__ code,
+                                                          const float* __restrict__ a1, int B,
+                                                          const int32_t* __restrict__ client_nb,
+                                                          float* __restrict__ delta, int64_t ld, Step st) {
+  extern __shared__ float sm[];
+  float* as = sm;                      // [900][33]
+  float* gs = as + S1 * S1 * A1P;      // [64][196]
+  uint8_t* cs = reinterpret_cast<uint8_t*>(gs + C2 * NPOOL);
+  const int c = blockIdx.x;
+  const int nb = client_nb[c];
+  if (nb == 0) return;
+  const int o = threadIdx.x >> 2, quarter = threadIdx.x & 3;  // 72 (tap,ci) per thread
+  float acc[72];
+#pragma unroll
+  for (int i = 0; i < 72; ++i) acc[i] = 0.f;
+  float gbias = 0.f;
+  for (int b = 0; b < nb; ++b) {
+    const int64_t n = (int64_t)c * B + b;
+    __syncthreads();
+    for (int i = threadIdx.x; i < A1; i += blockDim.x) as[(i >> 5) * A1P + (i & 31)] = a1[n * A1 + i];
+    for (int i = threadIdx.x; i < FLAT; i += blockDim.x) {
+      gs[i] = pooled[n * FLAT + i] > 0.f ? dp[n * FLAT + i] : 0.f;
+      cs[i] = code[n * FLAT + i];
+    }
+    __syncthreads();
+    for (int pp = 0; pp < NPOOL; ++pp) {
+      const float gv = gs[o * NPOOL + pp];
+      if (gv == 0.f) continue;
+      gbias += gv;
+      const int sub = cs[o * NPOOL + pp];
+      const int y = 2 * (pp / SP) + (sub >> 1), x = 2 * (pp % SP) + (sub & 1);
+#pragma unroll
+      for (int i = 0; i < 72; ++i) {
+        const int k = quarter * 72 + i, tap = k >> 5, ci = k & 31;
+        const int ky = tap / 3, kx = tap - ky * 3;
+        acc[i] = fmaf(gv, as[((y + ky) * S1 + x + kx) * A1P + ci], acc[i]);
+      }
+    }
+  }
+  float* dc = delta + (int64_t)c * ld;
+#pragma unroll
+  for (int i = 0; i < 72; ++i) {
+    const int k = quarter * 72 + i, tap = k >> 5, ci = k & 31;
+    float& dl = dc[O_W2 + (int64_t)o * C1 * 9 + ci * 9 + tap];
+    dl += st.lr * (acc[i] - st.mu * dl);
+  }
+  // bias: the four threads of channel o hold identical sums; one writes
+  if (quarter == 0) {
+    float& dl = dc[O_B2 + o];
+    dl += st.lr * (gbias - st.mu * dl);
+  }
+}
+
+// ------------------------------------------- conv1 backward (weights) + update
+// one CTA per client; thread t < 864 owns dW1[o][ci][ky][kx], t in [864, 896) a bias
+__global__ void __launch_bounds__(C1 * 28) conv1_bwd_w_kernel(const float* __restrict__ X,
+                                                             const int64_t* __restrict__ slot_row,
+                                                             const float* __restrict__ dz1, int B,
+                                                             const int32_t* __restrict__ client_nb,
+                                                             float* __restrict__ delta, int64_t ld, Step st) {
+  extern __shared__ float sm[];
+  float* img = sm;                    // [3][32][32]
+  float* dz = img + IMG;              // [900][33]
+  const int c = blockIdx.x;
+  const int nb = client_nb[c];
+  if (nb == 0) return;
+  const int t = threadIdx.x;
+  const bool is_w = t < C1 * 27;
+  const int o = is_w ? t / 27 : t - C1 * 27;
+  const int r = is_w ? t - o * 27 : 0, ci = r / 9, ky = (r % 9) / 3, kx = r % 3;
+  float acc = 0.f;
+  for (int b = 0; b < nb; ++b) {
+    const int64_t n = (int64_t)c * B + b;
+    const int64_t row = slot_row[n];
+    __syncthreads();
+    for (int i = t; i < IMG; i += blockDim.x) img[i] = X[row * IMG + i];
+    for (int i = t; i < A1; i += blockDim.x) dz[(i >> 5) * A1P + (i & 31)] = dz1[n * A1 + i];
+    __syncthreads();
+    if (is_w) {
+      const float* im = img + ci * S0 * S0 + ky * S0 + kx;
+      for (int y = 0; y < S1; ++y)
+        for (int x = 0; x < S1; ++x) acc = fmaf(dz[(y * S1 + x) * A1P + o], im[y * S0 + x], acc);
+    } else if (o < C1) {
+      for (int p = 0; p < S1 * S1; ++p) acc += dz[p * A1P + o];
+    }
+  }
+  float* dc = delta + (int64_t)c * ld;
+  if (is_w) {
+    float& dl = dc[O_W1 + t];
+    dl += st.lr * (acc - st.mu * dl);
+  } else if (o < C1) {
+    float& dl = dc[O_B1 + o];
+    dl += st.lr * (acc - st.mu * dl);
+  }
+}
+
+__global__ void eval_reduce_kernel(const double* __restrict__ slot_loss, const int32_t* __restrict__ slot_hit,
+                                   const int32_t* __restrict__ slot_client, int N, int64_t r0,
+                                   const int64_t* __restrict__ prefix, int C, double* __restrict__ loss_sum,
+                                   int32_t* __restrict__ correct) {
+  // clients overlapping the chunk [r0, r0+N): sum their slots in row order
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const int64_t lo = max(prefix[c], r0), hi = min(prefix[c + 1], r0 + N);
+  if (lo >= hi) return;
+  double s = 0.0;
+  int h = 0;
+  for (int64_t r = lo; r < hi; ++r) {
+    s += slot_loss[r - r0];
+    h += slot_hit[r - r0];
+  }
+  loss_sum[c] += s;
+  correct[c] += h;
+}
+
+__global__ void zero_delta_kernel(float* __restrict__ delta, int64_t ld, int C) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < (int64_t)C * ld) delta[i] = 0.f;
+}
+
+// ------------------------------------------------------------- workspace
+struct Work {
+  int64_t* slot_row;
+  int32_t* slot_client;
+  int32_t* client_nb;
+  int64_t* prefix;
+  double* slot_loss;
+  int32_t* slot_hit;
+  float *a1, *pooled, *part, *dz3, *dp, *dz1;
+  uint8_t* code;
+};
+
+inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
+
+// layout for N slots and up to Cmax clients
+inline int64_t carve(void* base, int N, int Cmax, Work* w) {
+  int64_t off = 0;
+  auto take = [&](int64_t bytes) {
+    const int64_t o = off;
+    off += align256(bytes);
+    return o;
+  };
+  const int64_t o_row = take(8LL * N), o_cl = take(4LL * N), o_nb = take(4LL * (Cmax + 1)),
+                o_pre = take(8LL * (Cmax + 1)), o_loss = take(8LL * N), o_hit = take(4LL * N),
+                o_a1 = take(4LL * N * A1), o_pool = take(4LL * N * FLAT), o_code = take((int64_t)N * FLAT),
+                o_part = take(4LL * KSPLIT * N * HID), o_dz3 = take(4LL * N * HID), o_dp = take(4LL * N * FLAT),
+                o_dz1 = take(4LL * N * A1);
+  if (w && base) {
+    char* b = static_cast<char*>(base);
+    w->slot_row = reinterpret_cast<int64_t*>(b + o_row);
+    w->slot_client = reinterpret_cast<int32_t*>(b + o_cl);
+    w->client_nb = reinterpret_cast<int32_t*>(b + o_nb);
+    w->prefix = reinterpret_cast<int64_t*>(b + o_pre);
+    w->slot_loss = reinterpret_cast<double*>(b + o_loss);
+    w->slot_hit = reinterpret_cast<int32_t*>(b + o_hit);
+    w->a1 = reinterpret_cast<float*>(b + o_a1);
+    w->pooled = reinterpret_cast<float*>(b + o_pool);
+    w->code = reinterpret_cast<uint8_t*>(b + o_code);
+    w->part = reinterpret_cast<float*>(b + o_part);
+    w->dz3 = reinterpret_cast<float*>(b + o_dz3);
+    w->dp = reinterpret_cast<float*>(b + o_dp);
+    w->dz1 = reinterpret_cast<float*>(b + o_dz1);
+  }
+  return off;
+}
+
+int set_smem_limits() {
+  static bool done = false;
+  if (done) return FB_OK;
+  cudaFuncSetAttribute(conv2_fwd_pool_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C2F_SMEM);
+  cudaFuncSetAttribute(conv2_bwd_x_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C2X_SMEM);
+  cudaFuncSetAttribute(conv2_bwd_w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C2W_SMEM);
+  cudaFuncSetAttribute(fc1_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FC1F_SMEM);
+  cudaFuncSetAttribute(conv1_bwd_w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (IMG + S1 * S1 * A1P) * 4);
+  done = true;
+  return launch_status("cnn: cudaFuncSetAttribute");
+}
+
+// forward of N slots (shared weights when delta == nullptr) up to the head
+int forward(const float* X, const float* theta, const float* delta, int64_t ld, int B, int N, int G,
+            const Work& w, cudaStream_t s) {
+  conv1_fwd_kernel<<<N, 256, 0, s>>>(X, w.slot_row, theta, delta, ld, B, w.a1);
+  conv2_fwd_pool_kernel<<<N, 256, C2F_SMEM, s>>>(w.a1, w.slot_row, theta, delta, ld, B, w.pooled, w.code);
+  fc1_fwd_kernel<<<dim3((N + G - 1) / G, KSPLIT), HID, FC1F_SMEM, s>>>(w.pooled, w.slot_row, N, G, theta, delta, ld,
+                                                               w.part);
+  return launch_status("cnn forward");
+}
+
+}  // namespace cnn
+}  // namespace fb
+
+using namespace fb::cnn;
+
+extern "C" {
+
+int64_t fb_cnn_workspace_bytes(int max_slots, int max_clients) {
+  return carve(nullptr, max_slots, max_clients, nullptr);
+}
+
+int fb_eval_cnn_f32(const float* theta, const float* X, const int32_t* y, const int64_t* row_start,
+                    const int32_t* num_rows, int num_clients, int64_t total_rows, double* loss_sum,
+                    int32_t* correct, int max_slots, void* workspace, int64_t workspace_bytes, void* stream) {
+  FB_REQUIRE(num_clients >= 0 && total_rows >= 0 && max_slots >= GMAX, "eval_cnn: bad arguments");
+  FB_REQUIRE(workspace_bytes >= carve(nullptr, max_slots, num_clients, nullptr), "eval_cnn: workspace too small");
+  if (num_clients == 0) return FB_OK;
+  int st = set_smem_limits();
+  if (st) return st;
+  cudaStream_t s = fb::as_stream(stream);
+  Work w;
+  carve(workspace, max_slots, num_clients, &w);
+  const int N = (max_slots / GMAX) * GMAX;
+  cudaMemsetAsync(loss_sum, 0, sizeof(double) * num_clients, s);
+  cudaMemsetAsync(correct, 0, sizeof(int32_t) * num_clients, s);
+  prefix_kernel<<<1, 1, 0, s>>>(num_rows, num_clients, w.prefix);
+  for (int64_t r0 = 0; r0 < total_rows; r0 += N) {
+    eval_slots_kernel<<<(N + 255) / 256, 256, 0, s>>>(r0, N, total_rows, w.prefix, num_clients, row_start,
+                                                      w.slot_row, w.slot_client);
+    st = forward(X, theta, nullptr, 0, 1, N, GMAX, w, s);
+    if (st) return st;
+    head_kernel<<<N / GMAX, HID, 0, s>>>(w.part, w.slot_row, N, GMAX, y, theta, nullptr, 0, nullptr, Step{0, 0},
+                                         nullptr, w.slot_loss, w.slot_hit);
+    eval_reduce_kernel<<<(num_clients + 127) / 128, 128, 0, s>>>(w.slot_loss, w.slot_hit, w.slot_client, N, r0,
+                                                                 w.prefix, num_clients, loss_sum, correct);
+    st = fb::launch_status("eval_cnn");
+    if (st) return st;
+  }
+  return FB_OK;
+}
+
+int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y, const int64_t* row_start,
+                         const int32_t* num_rows, const int32_t* perms, const int64_t* perm_off, int num_clients,
+                         int epochs, int batch_size, int max_steps, float lr, float prox_mu, float* delta_out,
+                         int64_t ld_delta, int32_t* nonfinite, int max_slots, void* workspace,
+                         int64_t workspace_bytes, void* stream) {
+  FB_REQUIRE(num_clients >= 0 && epochs >= 0 && batch_size >= 1 && max_steps >= 0, "local_sgd_cnn: bad arguments");
+  FB_UNSUPPORTED(batch_size <= GMAX, "local_sgd_cnn: batch_size %d > %d", batch_size, GMAX);
+  FB_REQUIRE(ld_delta >= D && (ld_delta & 3) == 0, "local_sgd_cnn: ld_delta must be >= D and a multiple of 4");
+  FB_REQUIRE(max_slots >= batch_size, "local_sgd_cnn: max_slots < batch_size");
+  const int per = max_slots / batch_size;  // clients per wave
+  FB_REQUIRE(workspace_bytes >= carve(nullptr, max_slots, per, nullptr), "local_sgd_cnn: workspace too small");
+  if (num_clients == 0) return FB_OK;
+  int st = set_smem_limits();
+  if (st) return st;
+  cudaStream_t s = fb::as_stream(stream);
+  Work w;
+  carve(workspace, max_slots, per, &w);
+  const int64_t tot = (int64_t)num_clients * ld_delta;
+  zero_delta_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(delta_out, ld_delta, num_clients);
+  cudaMemsetAsync(nonfinite, 0, sizeof(int32_t) * num_clients, s);
+  const Step sp{lr, prox_mu};
+  const int B = batch_size;
+  for (int c0 = 0; c0 < num_clients; c0 += per) {
+    const int Cw = min(per, num_clients - c0);
+    const int N = Cw * B;
+    float* dlt = delta_out + (int64_t)c0 * ld_delta;
+    for (int step = 0; step < max_steps; ++step) {
+      train_slots_kernel<<<(N + 255) / 256, 256, 0, s>>>(step, row_start + c0, num_rows + c0, perms, perm_off + c0,
+                                                        Cw, epochs, B, w.slot_row, w.client_nb);
+      st = forward(X, theta_t, dlt, ld_delta, B, N, B, w, s);
+      if (st) return st;
+      head_kernel<<<Cw, HID, 0, s>>>(w.part, w.slot_row, N, B, y, theta_t, dlt, ld_delta, w.client_nb, sp, w.dz3,
+                                     nullptr, nullptr);
+      fc1_bwd_kernel<<<dim3(Cw, KSPLIT), HID, 0, s>>>(w.pooled, w.dz3, B, w.client_nb, theta_t, dlt, ld_delta, sp,
+                                                      w.dp);
+      conv2_bwd_x_kernel<<<N, 256, C2X_SMEM, s>>>(w.dp, w.pooled, w.code, w.a1, w.slot_row, B, theta_t, dlt,
+                                                  ld_delta, w.dz1);
+      conv2_bwd_w_kernel<<<Cw, 256, C2W_SMEM, s>>>(w.dp, w.pooled, w.code, w.a1, B, w.client_nb, dlt, ld_delta,
+                                                   sp);
+      conv1_bwd_w_kernel<<<Cw, C1 * 28, (IMG + S1 * S1 * A1P) * 4, s>>>(X, w.slot_row, w.dz1, B, w.client_nb, dlt,
+                                                                       ld_delta, sp);
+      st = fb::launch_status("local_sgd_cnn step");
+      if (st) return st;
+    }
+  }
+  return FB_OK;
+}
+
+}  // extern "C"

@@ -25,7 +25,7 @@ from typing import Any, Mapping, Sequence
 
 import numpy as np
 
-from . import native
+from . import cnn, native
 from .aggregator import SumAggregator
 from .core import CentralContext, MetricKind, MetricValue, Population, merge_metrics, user_seed
 from .device import Comm, DeviceParams, DevicePopulation, DeviceStatistics, Workspace
@@ -115,22 +115,19 @@ class _ModelRunner:
         self.D = model.num_params
         self.ld = (self.D + 3) & ~3  # 16-byte aligned client rows
 
-    def eval(self, theta, pop: DevicePopulation, row_start, num_rows, C, loss, correct, stream):
+    def eval(self, theta, pop: DevicePopulation, row_start, num_rows, C, loss, correct, stream, h_num_rows):
         if self.kind == "cnn":
-            from . import cnn
-
-            return cnn.eval_cohort(self, theta, pop, row_start, num_rows, C, loss, correct, stream)
+            return cnn.eval_cohort(self, theta, pop, row_start, num_rows, C, loss, correct, stream, h_num_rows)
         fn = f"fb_eval_{self.kind}_f32"
         native.call(fn, native.ptr(theta), *self.dims, native.ptr(pop.X), native.ptr(pop.y),
                     native.ptr(row_start), native.ptr(num_rows), C, native.ptr(loss), native.ptr(correct),
                     stream)
 
-    def local_sgd(self, theta, pop, row_start, num_rows, perms, perm_off, C, tp, prox_mu, delta, nonfinite, stream):
+    def local_sgd(self, theta, pop, row_start, num_rows, perms, perm_off, C, tp, prox_mu, delta, nonfinite, stream,
+                  h_num_rows):
         if self.kind == "cnn":
-            from . import cnn
-
             return cnn.local_sgd_cohort(self, theta, pop, row_start, num_rows, perms, perm_off, C, tp,
-                                        prox_mu, delta, nonfinite, stream)
+                                        prox_mu, delta, nonfinite, stream, h_num_rows)
         fn = f"fb_local_sgd_{self.kind}_f32"
         native.call(fn, native.ptr(theta), *self.dims, native.ptr(pop.X), native.ptr(pop.y),
                     native.ptr(row_start), native.ptr(num_rows), native.ptr(perms), native.ptr(perm_off), C,
@@ -294,7 +291,7 @@ class GpuSimulationEngine:
         ints = res[16 * Cp: 16 * Cp + 12 * Cp].view(torch.int32)
         correct, clipped, nonfinite = ints[:Cp], ints[Cp:2 * Cp], ints[2 * Cp:3 * Cp]
         if C:
-            runner.eval(theta.flat, pop, d_row_start, d_num_rows, C, loss, correct, stream)
+            runner.eval(theta.flat, pop, d_row_start, d_num_rows, C, loss, correct, stream, num_rows)
 
         agg_flat = None
         if train:
@@ -303,7 +300,7 @@ class GpuSimulationEngine:
             if C:
                 delta = self.ws.tensor("delta", (C, runner.ld), torch.float32)
                 runner.local_sgd(theta.flat, pop, d_row_start, d_num_rows, d_perms, d_perm_off, C, plan.train,
-                                 plan.prox_mu, delta, nonfinite, stream)
+                                 plan.prox_mu, delta, nonfinite, stream, num_rows)
                 coef = self.ws.tensor("coef", (Cp,), torch.float32)
                 bound = self._clip.current_bound if self._clip is not None else 0.0
                 wsb = native.call("fb_clip_workspace_bytes", C, runner.D)
