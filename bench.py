@@ -1,0 +1,393 @@
+#!/usr/bin/env python
+"""Central-iteration throughput of the B200 engine (BASELINE.json metric:
+central iterations/sec and clients/sec at cohort N) and the CPU reference arm.
+
+Default workload (BASELINE configs[1], single-GPU form): FedAvg + central
+Gaussian DP (L2 clip 1.0), the CIFAR-10 CNN, cohort 1000 of 1000 users x 50
+synthetic CIFAR-shaped points (3x32x32), 1 local epoch, batch 10, local lr
+0.1, central SGD lr 1.0, uniform weighting, sigma 0.8025 (the reference's
+calibration for eps=2, delta=1e-6, q=0.001, T=1500), r = C / C~ = 1,
+validation context (100 users) every 10 iterations.
+
+A step = one central iteration (host sampling + LPT shard + permutations,
+eval + local SGD + clip + aggregate on the GPU, all-reduce for N>1, noise +
+average + central SGD).  ``value`` has the dataset resident in HBM; ``e2e``
+keeps it in pinned host memory and moves each iteration's cohort rows to the
+device inside the timed region (plus the per-client results back).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "central iterations/sec and clients/sec at cohort N, 1/2/4/8 B200 vs host-CPU ref"
+SIGMA_T1500 = 0.802516171110736  # reference calibrate_sigma(2.0, 1e-6, 0.001, 1500)
+
+WORKLOADS = {
+    "cnn": dict(model="cnn", dim=3072, users=1000, val_users=100, ppu=50, cohort=1000, eval_cohort=100,
+                epochs=1, batch=10, lr=0.1, clr=1.0, bound=1.0, sigma=SIGMA_T1500, noise_cohort=1000,
+                eval_every=10, name="cifar10-cnn fedavg+gaussian-dp cohort1000 (BASELINE configs[1])"),
+    "mlp": dict(model="mlp", dim=32, hidden=64, users=1000, val_users=100, ppu=50, cohort=1000, eval_cohort=100,
+                epochs=1, batch=10, lr=0.1, clr=1.0, bound=1.0, sigma=SIGMA_T1500, noise_cohort=1000,
+                eval_every=10, name="mlp(64) fedavg+gaussian-dp cohort1000 (reference-native shape)"),
+    "logistic": dict(model="logistic", dim=32, users=1000, val_users=100, ppu=50, cohort=1000, eval_cohort=100,
+                     epochs=1, batch=10, lr=0.1, clr=1.0, bound=1.0, sigma=SIGMA_T1500, noise_cohort=1000,
+                     eval_every=10, name="logistic fedavg+gaussian-dp cohort1000 (reference-native shape)"),
+}
+
+# algorithmic FLOPs per processed sample for the CNN kernels (2 x MACs of the
+# dense operation the kernel implements)
+CNN_MACS = {"conv1": 30 * 30 * 32 * 27, "conv2": 28 * 28 * 64 * 288, "fc1": 12544 * 128, "fc2": 128 * 10}
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+# ------------------------------------------------------------------ setup
+
+
+def build(wl: dict):
+    import paper_2404_06430_b200 as fb
+
+    ppu = wl["ppu"]
+    ntr, nva = wl["users"] * ppu, wl["val_users"] * ppu
+    X, y = fb.make_synthetic_classification(ntr + nva, dim=wl["dim"], num_classes=10, margin=6.0,
+                                            seed=fb.derive_seed(0, "pool"))
+    X = X.astype(np.float32)  # features are cast to fp32 once and fed to both sides
+    train = fb.partition_iid(X[:ntr], y[:ntr], ppu, seed=fb.derive_seed(0, "train", "split"),
+                             population=fb.Population.TRAIN, id_prefix="train")
+    val = fb.partition_iid(X[ntr:], y[ntr:], ppu, seed=fb.derive_seed(0, "val", "split"),
+                           population=fb.Population.VAL, id_prefix="val")
+    return {fb.Population.TRAIN: train, fb.Population.VAL: val}
+
+
+def make_model(wl):
+    import paper_2404_06430_b200 as fb
+
+    if wl["model"] == "cnn":
+        return fb.CNN()
+    if wl["model"] == "mlp":
+        return fb.MLP(wl["dim"], wl["hidden"], 10)
+    return fb.LogisticRegression(wl["dim"], 10)
+
+
+def make_algorithm(wl, iterations):
+    import paper_2404_06430_b200 as fb
+
+    alg = fb.FedAvg(make_model(wl), fb.SGDOptimizer(wl["clr"]), total_iterations=iterations,
+                    cohort_size=wl["cohort"], local_learning_rate=wl["lr"], local_num_epochs=wl["epochs"],
+                    local_batch_size=wl["batch"], eval_frequency=wl["eval_every"],
+                    eval_cohort_size=wl["eval_cohort"], weighting="uniform", run_seed=0, init_seed=0)
+    clip = fb.ClippingPostprocessor(wl["bound"])
+    r = wl["cohort"] / wl["noise_cohort"]
+    mech = fb.GaussianCentralMechanism(clip, sigma=wl["sigma"], r=r,
+                                       noise_base_seed=fb.derive_seed(0, "noise-stream", 0))
+    return alg, [clip, mech]
+
+
+# ----------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = Path(tempfile.mkstemp(suffix=".csv")[1])
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=self.path.open("w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait(timeout=10)
+
+    def summary(self) -> dict:
+        rows = []
+        for line in self.path.read_text().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) == 6 and f[0].isdigit():
+                rows.append(f)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(float(r[0]) for r in rows), "sm_max_mhz": float(rows[0][1]),
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------- GPU arm
+
+
+def run_iterations(engine, alg, state, t0, k):
+    for t in range(t0, t0 + k):
+        ctxs = alg.get_next_central_contexts(state, t)
+        res = engine.run_iteration(alg, state, ctxs)
+        state = alg.process_aggregated_statistics_all_contexts(state, ctxs, res.aggregates, res.metrics,
+                                                               res.user_updates)
+    return state
+
+
+def timed(engine, alg, state, t0, k, dist, world):
+    """K iterations bracketed by barrier + synchronize; CUDA-event device time,
+    max over ranks."""
+    torch = _torch()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    ev0.record(engine.stream)
+    state = run_iterations(engine, alg, state, t0, k)
+    ev1.record(engine.stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    wall = time.perf_counter() - w0
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device=engine.device, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return state, ms, wall
+
+
+def roofline(report: dict, wl: dict, samples: dict, peaks: dict) -> dict:
+    """Dominant kernel's achieved throughput vs the measured peak."""
+    if not report:
+        return {}
+    name, (ms, launches) = max(report.items(), key=lambda kv: kv[1][0])
+    per_sample = {
+        "conv2_fwd_pool_kernel": ("tensor", 2 * CNN_MACS["conv2"], "fwd"),
+        "conv2_bwd_x_kernel": ("tensor", 2 * CNN_MACS["conv2"], "train"),
+        "conv2_bwd_w_kernel": ("tensor", 2 * CNN_MACS["conv2"], "train"),
+        "conv1_fwd_kernel": ("tensor", 2 * CNN_MACS["conv1"], "fwd"),
+        "conv1_bwd_w_kernel": ("tensor", 2 * CNN_MACS["conv1"], "train"),
+    }
+    out = {"kernel": name, "share_of_gpu_time": None}
+    total = sum(v[0] for v in report.values())
+    out["share_of_gpu_time"] = ms / total if total else None
+    if name in per_sample:
+        bound, flops, which = per_sample[name]
+        n = samples["fwd"] if which == "fwd" else samples["train"]
+        achieved = flops * n / (ms * 1e-3) / 1e12
+        peak = peaks.get("bf16_tflops", 1590.0)
+        out.update(bound=bound, achieved=achieved, peak=peak, unit="TFLOP/s", frac=achieved / peak,
+                   traffic=None, peak_source="MEASURED_PEAKS.json bf16_tflops (dense tensor); kernel runs FP32 FFMA",
+                   algorithmic=f"{flops} FLOP/sample x {n} samples over {launches} launches")
+    else:
+        out.update(bound="hbm", achieved=None, peak=peaks.get("hbm_gbs", 6650.0), unit="GB/s", frac=None,
+                   traffic=None)
+    return out
+
+
+def gpu_arm(args, wl):
+    torch = _torch()
+    import paper_2404_06430_b200 as fb
+    from paper_2404_06430_b200 import native
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = torch.distributed
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+
+    ds = build(wl)
+    K, W = args.steps, args.warmup
+    alg, post = make_algorithm(wl, W + K + args.e2e_warmup + args.e2e_steps + 1)
+    engine = fb.GpuSimulationEngine(ds, postprocessors=post)
+    state = alg.initial_state()
+    state = run_iterations(engine, alg, state, 0, W)
+    n0 = native.lib().fb_launch_count()
+    native.lib().fb_timing_enable(1)
+    with ClockSampler(local) as clk:
+        state, ms, wall = timed(engine, alg, state, W, K, dist, world)
+    report = native.timing_report()
+    native.lib().fb_timing_enable(0)
+    launches = native.lib().fb_launch_count() - n0
+    clocks = clk.summary()
+
+    # samples processed by the forward / training kernels in the timed window (this rank)
+    C = wl["cohort"]
+    per_rank = C / world
+    val_iters = sum(1 for t in range(W, W + K) if t % wl["eval_every"] == 0)
+    steps = wl["epochs"] * -(-wl["ppu"] // wl["batch"])
+    train_samples = per_rank * wl["ppu"] * wl["epochs"] * K
+    fwd_samples = train_samples + per_rank * wl["ppu"] * K + val_iters * (wl["eval_cohort"] / world) * wl["ppu"]
+    samples = {"train": train_samples, "fwd": fwd_samples}
+
+    # end-to-end: dataset in pinned host memory, cohort rows moved every iteration
+    e2e = None
+    if args.e2e_steps > 0:
+        eng2 = fb.GpuSimulationEngine(ds, postprocessors=post, data_residency="host")
+        t0 = W + K
+        state = run_iterations(eng2, alg, state, t0, args.e2e_warmup)
+        eng2.io_bytes = {"h2d": 0, "d2h": 0}
+        state, ms2, wall2 = timed(eng2, alg, state, t0 + args.e2e_warmup, args.e2e_steps, dist, world)
+        e2e = {"value": args.e2e_steps / (ms2 / 1e3), "unit": "iterations/s",
+               "clients_per_sec": C * args.e2e_steps / (ms2 / 1e3),
+               "h2d_bytes_per_step": int(eng2.io_bytes["h2d"] / args.e2e_steps),
+               "d2h_bytes_per_step": int(eng2.io_bytes["d2h"] / args.e2e_steps),
+               "data": "dataset in pinned host memory; cohort rows gathered to HBM each iteration"}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(wl, ds, args.cpu_clients)
+
+    if rank == 0:
+        ips = K / (ms / 1e3)
+        line = {
+            "metric": METRIC, "value": ips, "unit": "iterations/s", "clients_per_sec": ips * C,
+            "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": wl["name"], "model": wl["model"], "cohort": C, "users": wl["users"],
+                       "points_per_user": wl["ppu"], "local_epochs": wl["epochs"], "batch": wl["batch"],
+                       "local_steps_per_client": steps, "sigma": wl["sigma"], "clip_bound": wl["bound"],
+                       "eval_every": wl["eval_every"], "parallelism": f"cohort-dp{world}",
+                       "l2": "inputs larger than L2 (dataset 614 MB + per-iteration working set of GBs)"},
+            "wall_s": wall, "clocks": clocks, "gpu_launches": int(launches), "e2e": e2e,
+            "roofline": roofline(report, wl, samples, peaks) if wl["model"] == "cnn" else {},
+            "kernels_ms": {k: round(v[0], 3) for k, v in sorted(report.items(), key=lambda kv: -kv[1][0])},
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------- CPU arms
+
+
+def _cores() -> int:
+    try:
+        from threadpoolctl import threadpool_info
+
+        n = max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
+        return int(n)
+    except Exception:
+        return len(os.sched_getaffinity(0))
+
+
+def cpu_iteration_seconds(wl, ds, n_clients: int, t: int = 0) -> tuple[float, str]:
+    """Time the oracle port (the reference algorithm, numpy float64) on a
+    bounded sample of the train cohort and extrapolate one central
+    iteration: C x per-client time + amortised validation eval."""
+    import paper_2404_06430_b200 as fb
+    from oracle import port
+
+    model = {"cnn": lambda: port.Cnn(), "mlp": lambda: port.Mlp(wl["dim"], wl["hidden"], 10),
+             "logistic": lambda: port.Linear(wl["dim"], 10)}[wl["model"]]()
+    theta = model.init(0)
+    train = ds[fb.Population.TRAIN]
+    ctx = port.cohort_seed(0, t, "train")
+    cohort = port.sample_cohort(train.user_ids, wl["cohort"], ctx)[:n_clients]
+    users = {u: (train.users[u].features.astype(np.float64), train.users[u].labels) for u in cohort}
+    t0 = time.perf_counter()
+    port.run_context(model, theta, users, len(cohort), ctx, train=(wl["lr"], wl["epochs"], wl["batch"]),
+                     weighting="uniform", bound=wl["bound"], sigma=wl["sigma"], r=1.0, noise=False)
+    per_client = (time.perf_counter() - t0) / len(cohort)
+    val = ds[fb.Population.VAL]
+    vu = val.user_ids[:max(1, n_clients // 4)]
+    t1 = time.perf_counter()
+    for u in vu:
+        model.eval_counts(theta, val.users[u].features, val.users[u].labels)
+    per_val = (time.perf_counter() - t1) / len(vu)
+    it = wl["cohort"] * per_client + wl["eval_cohort"] * per_val / wl["eval_every"]
+    sample = (f"{len(cohort)} train clients (eval + {wl['epochs']} epoch local SGD + clip) and {len(vu)} val users "
+              f"of iteration {t}, extrapolated to cohort {wl['cohort']} + validation every {wl['eval_every']}")
+    return it, sample
+
+
+def cpu_baseline(wl, ds, n_clients):
+    it, sample = cpu_iteration_seconds(wl, ds, n_clients)
+    return {"value": 1.0 / it, "unit": "iterations/s", "cores": _cores(), "kind": "port", "sample": sample,
+            "seconds_per_iteration": it}
+
+
+def reference_arm(args, wl):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    ds = build(wl)
+    cpu_iteration_seconds(wl, ds, 1)  # warm-up (BLAS thread pools, page-in)
+    its = []
+    for k in range(args.steps):
+        it, sample = cpu_iteration_seconds(wl, ds, args.ref_clients, t=k)
+        its.append(it)
+    value = 1.0 / float(np.mean(its))
+    C = wl["cohort"]
+    line = {
+        "metric": METRIC, "impl": "reference", "value": value, "unit": "iterations/s", "clients_per_sec": value * C,
+        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": wl["name"], "model": wl["model"], "cohort": C, "parallelism": "host-cpu"},
+        "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": _cores(), "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cnn")
+    ap.add_argument("--cohort", type=int, default=None)
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-warmup", type=int, default=2)
+    ap.add_argument("--cpu-clients", type=int, default=16)
+    ap.add_argument("--ref-clients", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args(argv)
+    if args.warmup < 3 and args.impl == "ours":
+        ap.error("--warmup must be >= 3")
+    wl = dict(WORKLOADS[args.workload])
+    if args.cohort:
+        wl["cohort"] = args.cohort
+        wl["name"] += f" (cohort {args.cohort})"
+    if args.impl == "reference":
+        reference_arm(args, wl)
+    else:
+        gpu_arm(args, wl)
+
+
+if __name__ == "__main__":
+    main()

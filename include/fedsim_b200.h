@@ -52,6 +52,16 @@ const char* fb_last_error(void);
 /* [host] writes the device's SM count and L2 bytes; 0 on success. */
 int fb_device_info(int device, int* sm_count, int64_t* l2_bytes);
 
+/* [host] Launch accounting (bench/profiling).  fb_launch_count: kernels
+ * launched by this library since load.  fb_timing_enable(1) clears and starts
+ * bracketing every launch with CUDA events on its own stream;
+ * fb_timing_report synchronises on them and writes, per kernel name,
+ * the summed device milliseconds and launch count (names '\n'-separated);
+ * returns the number of entries (or < 0 on error).                          */
+int64_t fb_launch_count(void);
+void fb_timing_enable(int on);
+int fb_timing_report(char* names, int names_len, double* ms, int64_t* counts, int max_entries);
+
 /* ---------------------------------------------------------------- a4 eval
  * Per-client summed cross-entropy and correct count at the shared theta,
  * over all of the client's rows.  Replaces fedsim/models/kernels.py:70-83
@@ -119,6 +129,17 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
                          int epochs, int batch_size, int max_steps, float lr, float prox_mu,
                          float* delta_out, int64_t ld_delta, int32_t* nonfinite,
                          int max_slots, void* workspace, int64_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------- data movement
+ * Copy each cohort client's contiguous rows (num_rows[c] rows of row_bytes
+ * starting at row row_start[c] of src) to row dst_start[c] of dst.  src may
+ * be device memory or pinned host memory (UVA); one launch per context.
+ * max_rows_per_client sizes the grid.  Used by the host-resident-dataset
+ * (end-to-end) path in place of per-user host arrays
+ * (fedsim/feddata/datasets.py:12-40).                                     */
+int fb_gather_rows(const void* src, int64_t row_bytes, const int64_t* row_start,
+                   const int32_t* num_rows, int num_clients, const int64_t* dst_start,
+                   void* dst, int64_t max_rows_per_client, void* stream);
 
 /* ------------------------------------------------- a6 + a7 (kernel K2)
  * For every client c: norm[c] = || w[c] * delta[c, :D] ||_2 (fp64

@@ -171,22 +171,11 @@ def _relu_margin(z: np.ndarray) -> float:
 
 
 def _im2col3(x: np.ndarray) -> np.ndarray:
-    """[N, C, H, W] -> [N, (H-2)*(W-2), C*9] with (c, kh, kw) column order."""
-    win = np.lib.stride_tricks.sliding_window_view(x, (3, 3), axis=(2, 3))  # N,C,Ho,Wo,3,3
-    n, c, ho, wo = win.shape[:4]
-    return win.transpose(0, 2, 3, 1, 4, 5).reshape(n, ho * wo, c * 9)
-
-
-def _col2im3(cols: np.ndarray, c: int, h: int, w: int) -> np.ndarray:
-    """Adjoint of _im2col3: [N, Ho*Wo, C*9] -> [N, C, H, W]."""
-    n = cols.shape[0]
-    ho, wo = h - 2, w - 2
-    k = cols.reshape(n, ho, wo, c, 3, 3)
-    out = np.zeros((n, c, h, w))
-    for a in range(3):
-        for b in range(3):
-            out[:, :, a:a + ho, b:b + wo] += k[:, :, :, :, a, b].transpose(0, 3, 1, 2)
-    return out
+    """NHWC [N, H, W, C] -> [N*(H-2)*(W-2), C*9] with (c, kh, kw) column order
+    (the OIHW weight flattening)."""
+    win = np.lib.stride_tricks.sliding_window_view(x, (3, 3), axis=(1, 2))  # N,Ho,Wo,C,3,3
+    n, ho, wo, c = win.shape[:4]
+    return win.reshape(n * ho * wo, c * 9)
 
 
 @dataclass(frozen=True)
@@ -225,17 +214,15 @@ class Cnn:
 
     def _forward(self, p, X):
         N, s = X.shape[0], self.s
-        x = X.reshape(N, self.c0, s, s)
-        cols1 = _im2col3(x)
-        z1 = cols1 @ p["conv1/weights"].reshape(self.c1, -1).T + p["conv1/bias"]  # N, s1*s1, c1
-        s1 = s - 2
-        a1 = np.maximum(z1, 0.0).transpose(0, 2, 1).reshape(N, self.c1, s1, s1)
-        cols2 = _im2col3(a1)
-        z2 = cols2 @ p["conv2/weights"].reshape(self.c2, -1).T + p["conv2/bias"]  # N, s2*s2, c2
-        s2 = s1 - 2
-        a2 = np.maximum(z2, 0.0).transpose(0, 2, 1).reshape(N, self.c2, s2, s2)
-        sp = s2 // 2
-        win = a2.reshape(N, self.c2, sp, 2, sp, 2).transpose(0, 1, 2, 4, 3, 5).reshape(N, self.c2, sp, sp, 4)
+        s1, s2, sp = s - 2, s - 4, (s - 4) // 2
+        x = X.reshape(N, self.c0, s, s).transpose(0, 2, 3, 1)             # NHWC
+        cols1 = _im2col3(x)                                                # N*s1*s1, c0*9
+        z1 = cols1 @ p["conv1/weights"].reshape(self.c1, -1).T + p["conv1/bias"]
+        a1 = np.maximum(z1, 0.0).reshape(N, s1, s1, self.c1)
+        cols2 = _im2col3(a1)                                               # N*s2*s2, c1*9
+        z2 = cols2 @ p["conv2/weights"].reshape(self.c2, -1).T + p["conv2/bias"]
+        a2 = np.maximum(z2, 0.0).reshape(N, sp, 2, sp, 2, self.c2)
+        win = a2.transpose(0, 5, 1, 3, 2, 4).reshape(N, self.c2, sp, sp, 4)  # (dy, dx) window order
         arg = win.argmax(axis=4)  # first maximum in (0,0),(0,1),(1,0),(1,1) order
         pooled = np.take_along_axis(win, arg[..., None], axis=4)[..., 0]
         if TRACK_MARGINS:
@@ -245,7 +232,7 @@ class Cnn:
             scale = float(np.sqrt(np.mean(z2 * z2))) or 1.0
             pool_gap = float(gap.min()) / scale if gap.size else np.inf
             _record_margin(_relu_margin(z1), _relu_margin(z2), pool_gap)
-        flat = pooled.reshape(N, -1)
+        flat = pooled.reshape(N, -1)                                       # CHW flatten order
         z3 = flat @ p["fc1/weights"].reshape(self.flat, self.hid) + p["fc1/bias"]
         a3 = np.maximum(z3, 0.0)
         _record_margin(_relu_margin(z3))
@@ -254,6 +241,7 @@ class Cnn:
 
     def loss_and_grad(self, p, X, y):
         N = X.shape[0]
+        s1, s2, sp = self.s - 2, self.s - 4, (self.s - 4) // 2
         c, logits = self._forward(p, X)
         loss, dl = _xent(logits, y)
         Wf2 = p["fc2/weights"].reshape(self.hid, self.k)
@@ -262,21 +250,24 @@ class Cnn:
         dz3 = (dl @ Wf2.T) * (c["z3"] > 0.0)
         g["fc1/weights"] = (c["flat"].T @ dz3).ravel()
         g["fc1/bias"] = dz3.sum(axis=0)
-        sp = (self.s - 4) // 2
         dpool = (dz3 @ Wf1.T).reshape(N, self.c2, sp, sp)
         dwin = np.zeros((N, self.c2, sp, sp, 4))
         np.put_along_axis(dwin, c["arg"][..., None], dpool[..., None], axis=4)
-        s2 = 2 * sp
-        da2 = dwin.reshape(N, self.c2, sp, sp, 2, 2).transpose(0, 1, 2, 4, 3, 5).reshape(N, self.c2, s2, s2)
-        dz2 = da2.reshape(N, self.c2, s2 * s2).transpose(0, 2, 1) * (c["z2"] > 0.0)  # N, s2*s2, c2
-        W2 = p["conv2/weights"].reshape(self.c2, -1)
-        g["conv2/weights"] = np.einsum("npo,npk->ok", dz2, c["cols2"]).ravel()
-        g["conv2/bias"] = dz2.sum(axis=(0, 1))
-        s1 = s2 + 2
-        da1 = _col2im3(dz2 @ W2, self.c1, s1, s1)  # N, c1, s1, s1
-        dz1 = da1.reshape(N, self.c1, s1 * s1).transpose(0, 2, 1) * (c["z1"] > 0.0)
-        g["conv1/weights"] = np.einsum("npo,npk->ok", dz1, c["cols1"]).ravel()
-        g["conv1/bias"] = dz1.sum(axis=(0, 1))
+        da2 = dwin.reshape(N, self.c2, sp, sp, 2, 2).transpose(0, 2, 4, 3, 5, 1).reshape(N * s2 * s2, self.c2)
+        dz2 = da2 * (c["z2"] > 0.0)                                        # N*s2*s2, c2
+        g["conv2/weights"] = (dz2.T @ c["cols2"]).ravel()
+        g["conv2/bias"] = dz2.sum(axis=0)
+        # conv-transpose per tap: da1[y+a, x+b, :] += dz2[y, x, :] @ W2[:, :, a, b]
+        W2t = p["conv2/weights"].reshape(self.c2, self.c1, 3, 3)
+        dzi = dz2.reshape(N, s2, s2, self.c2)
+        da1 = np.zeros((N, s1, s1, self.c1))
+        for a in range(3):
+            for b in range(3):
+                da1[:, a:a + s2, b:b + s2, :] += dzi @ W2t[:, :, a, b]
+        da1 = da1.reshape(N * s1 * s1, self.c1)
+        dz1 = da1 * (c["z1"] > 0.0)
+        g["conv1/weights"] = (dz1.T @ c["cols1"]).ravel()
+        g["conv1/bias"] = dz1.sum(axis=0)
         return loss, {n: g[n] for n in self.dims}
 
     def eval_counts(self, p, X, y):

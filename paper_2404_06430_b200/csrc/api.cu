@@ -1,6 +1,12 @@
 // Library-level entry points: ABI version, thread-local error text, device info.
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
 
 #include "fb_common.cuh"
 
@@ -24,9 +30,90 @@ int launch_status(const char* what) {
   return FB_OK;
 }
 
+// ------------------------------------------------------- launch accounting
+static std::atomic<long long> g_launches{0};
+static std::atomic<bool> g_timing{false};
+static std::mutex g_mu;
+struct Rec {
+  std::string name;
+  cudaEvent_t start, stop;
+};
+static std::vector<Rec> g_recs;
+static std::vector<cudaEvent_t> g_free;
+
+static cudaEvent_t take_event() {
+  if (!g_free.empty()) {
+    cudaEvent_t e = g_free.back();
+    g_free.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+LaunchScope::LaunchScope(const char* n, cudaStream_t s) : name(n), stream(s), slot(-1) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (!g_timing.load(std::memory_order_relaxed)) return;
+  std::lock_guard<std::mutex> lk(g_mu);
+  Rec r{n, take_event(), take_event()};
+  cudaEventRecord(r.start, s);
+  g_recs.push_back(r);
+  slot = (int)g_recs.size() - 1;
+}
+
+LaunchScope::~LaunchScope() {
+  if (slot < 0) return;
+  std::lock_guard<std::mutex> lk(g_mu);
+  cudaEventRecord(g_recs[slot].stop, stream);
+}
+
 }  // namespace fb
 
 extern "C" {
+
+int64_t fb_launch_count(void) { return fb::g_launches.load(); }
+
+void fb_timing_enable(int on) {
+  std::lock_guard<std::mutex> lk(fb::g_mu);
+  for (auto& r : fb::g_recs) {
+    fb::g_free.push_back(r.start);
+    fb::g_free.push_back(r.stop);
+  }
+  fb::g_recs.clear();
+  fb::g_timing.store(on != 0);
+}
+
+int fb_timing_report(char* names, int names_len, double* ms, int64_t* counts, int max_entries) {
+  std::lock_guard<std::mutex> lk(fb::g_mu);
+  std::map<std::string, std::pair<double, int64_t>> agg;
+  for (auto& r : fb::g_recs) {
+    if (cudaEventSynchronize(r.stop) != cudaSuccess) {
+      fb::set_error("fb_timing_report: %s", cudaGetErrorString(cudaGetLastError()));
+      return FB_ERR_CUDA;
+    }
+    float t = 0.f;
+    cudaEventElapsedTime(&t, r.start, r.stop);
+    auto& a = agg[r.name];
+    a.first += t;
+    a.second += 1;
+  }
+  int k = 0;
+  std::string all;
+  for (auto& kv : agg) {
+    if (k >= max_entries) break;
+    ms[k] = kv.second.first;
+    counts[k] = kv.second.second;
+    all += kv.first;
+    all += '\n';
+    ++k;
+  }
+  if (names && names_len > 0) {
+    strncpy(names, all.c_str(), names_len - 1);
+    names[names_len - 1] = 0;
+  }
+  return k;
+}
 
 int fb_abi_version(void) { return FB_ABI_VERSION; }
 

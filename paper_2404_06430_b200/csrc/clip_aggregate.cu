@@ -220,12 +220,12 @@ int fb_delta_norm_clip_f32(const float* delta, int64_t ld_delta, int num_clients
   const int64_t chunk = ((D + chunks - 1) / chunks + 3) & ~int64_t(3);
   double* partial = static_cast<double*>(workspace);
   cudaStream_t s = fb::as_stream(stream);
-  fb::row_sumsq_partial_kernel<<<dim3(chunks, num_clients), fb::kThreads, 0, s>>>(
-      delta, ld_delta, D, chunks, chunk, partial);
+  FB_LAUNCH("row_sumsq_partial_kernel", s, fb::row_sumsq_partial_kernel<<<dim3(chunks, num_clients), fb::kThreads, 0, s>>>(
+      delta, ld_delta, D, chunks, chunk, partial));
   int st = fb::launch_status("row_sumsq_partial_kernel");
   if (st) return st;
-  fb::clip_finalize_kernel<<<(num_clients + 127) / 128, 128, 0, s>>>(
-      partial, chunks, num_clients, w, bound, norm, coef, clipped, nonfinite);
+  FB_LAUNCH("clip_finalize_kernel", s, fb::clip_finalize_kernel<<<(num_clients + 127) / 128, 128, 0, s>>>(
+      partial, chunks, num_clients, w, bound, norm, coef, clipped, nonfinite));
   return fb::launch_status("clip_finalize_kernel");
 }
 
@@ -248,18 +248,18 @@ int fb_weighted_sum_f32(const float* delta, int64_t ld_delta, int num_clients, i
   const int64_t quads = (D + 3) >> 2;
   const unsigned bx = (unsigned)((quads + fb::kThreads - 1) / fb::kThreads);
   if (S == 1) {
-    fb::weighted_sum_kernel<float><<<dim3(bx, 1), fb::kThreads, 0, s>>>(
-        delta, ld_delta, D, coef, num_clients, num_clients, agg, 0, accumulate);
+    FB_LAUNCH("weighted_sum_kernel", s, fb::weighted_sum_kernel<float><<<dim3(bx, 1), fb::kThreads, 0, s>>>(
+        delta, ld_delta, D, coef, num_clients, num_clients, agg, 0, accumulate));
     return fb::launch_status("weighted_sum_kernel");
   }
   FB_REQUIRE(workspace_bytes >= (int64_t)sizeof(double) * S * D, "weighted_sum: workspace too small");
   const int per = (num_clients + S - 1) / S;
   double* part = static_cast<double*>(workspace);
-  fb::weighted_sum_kernel<double><<<dim3(bx, S), fb::kThreads, 0, s>>>(
-      delta, ld_delta, D, coef, num_clients, per, part, D, 0);
+  FB_LAUNCH("weighted_sum_kernel", s, fb::weighted_sum_kernel<double><<<dim3(bx, S), fb::kThreads, 0, s>>>(
+      delta, ld_delta, D, coef, num_clients, per, part, D, 0));
   int st = fb::launch_status("weighted_sum_kernel(sliced)");
   if (st) return st;
-  fb::slice_reduce_kernel<<<(unsigned)((D + 255) / 256), 256, 0, s>>>(part, S, D, agg, accumulate);
+  FB_LAUNCH("slice_reduce_kernel", s, fb::slice_reduce_kernel<<<(unsigned)((D + 255) / 256), 256, 0, s>>>(part, S, D, agg, accumulate));
   return fb::launch_status("slice_reduce_kernel");
 }
 
@@ -272,10 +272,10 @@ int fb_sumsq_f32(const float* x, int64_t n, double* out, void* workspace, int64_
   if (nb < 1) nb = 1;
   if (nb > 1024) nb = 1024;
   double* part = static_cast<double*>(workspace);
-  fb::sumsq_partial_kernel<<<(unsigned)nb, fb::kThreads, 0, s>>>(x, n, part);
+  FB_LAUNCH("sumsq_partial_kernel", s, fb::sumsq_partial_kernel<<<(unsigned)nb, fb::kThreads, 0, s>>>(x, n, part));
   int st = fb::launch_status("sumsq_partial_kernel");
   if (st) return st;
-  fb::sumsq_final_kernel<<<1, 256, 0, s>>>(part, (int)nb, out);
+  FB_LAUNCH("sumsq_final_kernel", s, fb::sumsq_final_kernel<<<1, 256, 0, s>>>(part, (int)nb, out));
   return fb::launch_status("sumsq_final_kernel");
 }
 

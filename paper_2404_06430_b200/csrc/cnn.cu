@@ -676,10 +676,10 @@ int set_smem_limits() {
 // forward of N slots (shared weights when delta == nullptr) up to the head
 int forward(const float* X, const float* theta, const float* delta, int64_t ld, int B, int N, int G,
             const Work& w, cudaStream_t s) {
-  conv1_fwd_kernel<<<N, 256, 0, s>>>(X, w.slot_row, theta, delta, ld, B, w.a1);
-  conv2_fwd_pool_kernel<<<N, 256, C2F_SMEM, s>>>(w.a1, w.slot_row, theta, delta, ld, B, w.pooled, w.code);
-  fc1_fwd_kernel<<<dim3((N + G - 1) / G, KSPLIT), HID, FC1F_SMEM, s>>>(w.pooled, w.slot_row, N, G, theta, delta, ld,
-                                                               w.part);
+  FB_LAUNCH("conv1_fwd_kernel", s, conv1_fwd_kernel<<<N, 256, 0, s>>>(X, w.slot_row, theta, delta, ld, B, w.a1));
+  FB_LAUNCH("conv2_fwd_pool_kernel", s, conv2_fwd_pool_kernel<<<N, 256, C2F_SMEM, s>>>(w.a1, w.slot_row, theta, delta, ld, B, w.pooled, w.code));
+  FB_LAUNCH("fc1_fwd_kernel", s, fc1_fwd_kernel<<<dim3((N + G - 1) / G, KSPLIT), HID, FC1F_SMEM, s>>>(w.pooled, w.slot_row, N, G, theta, delta, ld,
+                                                               w.part));
   return launch_status("cnn forward");
 }
 
@@ -708,16 +708,16 @@ int fb_eval_cnn_f32(const float* theta, const float* X, const int32_t* y, const 
   const int N = (max_slots / GMAX) * GMAX;
   cudaMemsetAsync(loss_sum, 0, sizeof(double) * num_clients, s);
   cudaMemsetAsync(correct, 0, sizeof(int32_t) * num_clients, s);
-  prefix_kernel<<<1, 1, 0, s>>>(num_rows, num_clients, w.prefix);
+  FB_LAUNCH("prefix_kernel", s, prefix_kernel<<<1, 1, 0, s>>>(num_rows, num_clients, w.prefix));
   for (int64_t r0 = 0; r0 < total_rows; r0 += N) {
-    eval_slots_kernel<<<(N + 255) / 256, 256, 0, s>>>(r0, N, total_rows, w.prefix, num_clients, row_start,
-                                                      w.slot_row, w.slot_client);
+    FB_LAUNCH("eval_slots_kernel", s, eval_slots_kernel<<<(N + 255) / 256, 256, 0, s>>>(r0, N, total_rows, w.prefix, num_clients, row_start,
+                                                      w.slot_row, w.slot_client));
     st = forward(X, theta, nullptr, 0, 1, N, GMAX, w, s);
     if (st) return st;
-    head_kernel<<<N / GMAX, HID, 0, s>>>(w.part, w.slot_row, N, GMAX, y, theta, nullptr, 0, nullptr, Step{0, 0},
-                                         nullptr, w.slot_loss, w.slot_hit);
-    eval_reduce_kernel<<<(num_clients + 127) / 128, 128, 0, s>>>(w.slot_loss, w.slot_hit, w.slot_client, N, r0,
-                                                                 w.prefix, num_clients, loss_sum, correct);
+    FB_LAUNCH("head_kernel", s, head_kernel<<<N / GMAX, HID, 0, s>>>(w.part, w.slot_row, N, GMAX, y, theta, nullptr, 0, nullptr, Step{0, 0},
+                                         nullptr, w.slot_loss, w.slot_hit));
+    FB_LAUNCH("eval_reduce_kernel", s, eval_reduce_kernel<<<(num_clients + 127) / 128, 128, 0, s>>>(w.slot_loss, w.slot_hit, w.slot_client, N, r0,
+                                                                 w.prefix, num_clients, loss_sum, correct));
     st = fb::launch_status("eval_cnn");
     if (st) return st;
   }
@@ -742,7 +742,7 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
   Work w;
   carve(workspace, max_slots, per, &w);
   const int64_t tot = (int64_t)num_clients * ld_delta;
-  zero_delta_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(delta_out, ld_delta, num_clients);
+  FB_LAUNCH("zero_delta_kernel", s, zero_delta_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(delta_out, ld_delta, num_clients));
   cudaMemsetAsync(nonfinite, 0, sizeof(int32_t) * num_clients, s);
   const Step sp{lr, prox_mu};
   const int B = batch_size;
@@ -751,20 +751,20 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
     const int N = Cw * B;
     float* dlt = delta_out + (int64_t)c0 * ld_delta;
     for (int step = 0; step < max_steps; ++step) {
-      train_slots_kernel<<<(N + 255) / 256, 256, 0, s>>>(step, row_start + c0, num_rows + c0, perms, perm_off + c0,
-                                                        Cw, epochs, B, w.slot_row, w.client_nb);
+      FB_LAUNCH("train_slots_kernel", s, train_slots_kernel<<<(N + 255) / 256, 256, 0, s>>>(step, row_start + c0, num_rows + c0, perms, perm_off + c0,
+                                                        Cw, epochs, B, w.slot_row, w.client_nb));
       st = forward(X, theta_t, dlt, ld_delta, B, N, B, w, s);
       if (st) return st;
-      head_kernel<<<Cw, HID, 0, s>>>(w.part, w.slot_row, N, B, y, theta_t, dlt, ld_delta, w.client_nb, sp, w.dz3,
-                                     nullptr, nullptr);
-      fc1_bwd_kernel<<<dim3(Cw, KSPLIT), HID, 0, s>>>(w.pooled, w.dz3, B, w.client_nb, theta_t, dlt, ld_delta, sp,
-                                                      w.dp);
-      conv2_bwd_x_kernel<<<N, 256, C2X_SMEM, s>>>(w.dp, w.pooled, w.code, w.a1, w.slot_row, B, theta_t, dlt,
-                                                  ld_delta, w.dz1);
-      conv2_bwd_w_kernel<<<Cw, 256, C2W_SMEM, s>>>(w.dp, w.pooled, w.code, w.a1, B, w.client_nb, dlt, ld_delta,
-                                                   sp);
-      conv1_bwd_w_kernel<<<Cw, C1 * 28, (IMG + S1 * S1 * A1P) * 4, s>>>(X, w.slot_row, w.dz1, B, w.client_nb, dlt,
-                                                                       ld_delta, sp);
+      FB_LAUNCH("head_kernel", s, head_kernel<<<Cw, HID, 0, s>>>(w.part, w.slot_row, N, B, y, theta_t, dlt, ld_delta, w.client_nb, sp, w.dz3,
+                                     nullptr, nullptr));
+      FB_LAUNCH("fc1_bwd_kernel", s, fc1_bwd_kernel<<<dim3(Cw, KSPLIT), HID, 0, s>>>(w.pooled, w.dz3, B, w.client_nb, theta_t, dlt, ld_delta, sp,
+                                                      w.dp));
+      FB_LAUNCH("conv2_bwd_x_kernel", s, conv2_bwd_x_kernel<<<N, 256, C2X_SMEM, s>>>(w.dp, w.pooled, w.code, w.a1, w.slot_row, B, theta_t, dlt,
+                                                  ld_delta, w.dz1));
+      FB_LAUNCH("conv2_bwd_w_kernel", s, conv2_bwd_w_kernel<<<Cw, 256, C2W_SMEM, s>>>(w.dp, w.pooled, w.code, w.a1, B, w.client_nb, dlt, ld_delta,
+                                                   sp));
+      FB_LAUNCH("conv1_bwd_w_kernel", s, conv1_bwd_w_kernel<<<Cw, C1 * 28, (IMG + S1 * S1 * A1P) * 4, s>>>(X, w.slot_row, w.dz1, B, w.client_nb, dlt,
+                                                                       ld_delta, sp));
       st = fb::launch_status("local_sgd_cnn step");
       if (st) return st;
     }

@@ -15,6 +15,17 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 
 int launch_status(const char* what);
 
+// Launch accounting: every kernel launch of the library goes through
+// FB_LAUNCH, which counts it and -- when timing is enabled
+// (fb_timing_enable) -- brackets it with CUDA events on its own stream.
+struct LaunchScope {
+  LaunchScope(const char* name, cudaStream_t s);
+  ~LaunchScope();
+  const char* name;
+  cudaStream_t stream;
+  int slot;
+};
+
 constexpr int kWarp = 32;
 
 __device__ __forceinline__ float warp_sum(float v) {
@@ -47,6 +58,12 @@ __device__ __forceinline__ double block_sum(double v, double* scratch) {
 }
 
 }  // namespace fb
+
+#define FB_LAUNCH(name, stream, ...)             \
+  do {                                           \
+    ::fb::LaunchScope fb_launch_scope_(name, stream); \
+    __VA_ARGS__;                                 \
+  } while (0)
 
 #define FB_REQUIRE(cond, ...)            \
   do {                                   \

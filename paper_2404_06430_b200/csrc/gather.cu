@@ -1,0 +1,61 @@
+// Cohort row gather: copy every cohort client's contiguous block of dataset
+// rows into a packed device buffer.  The source may be device memory or
+// pinned host memory (UVA-mapped, read over PCIe/C2C by the kernel itself --
+// one launch per context instead of one memcpy per client).  This is the
+// "host-resident dataset" data path of the end-to-end measurement; the
+// reference keeps every user's rows as a host numpy array
+// (fedsim/feddata/datasets.py:12-40).
+
+#include "fb_common.cuh"
+
+namespace fb {
+namespace {
+
+constexpr int kThreads = 256;
+
+// grid (chunks, C): block x of client c copies its share of the client's bytes
+__global__ void __launch_bounds__(kThreads) gather_rows_kernel(const uint8_t* __restrict__ src, int64_t row_bytes,
+                                                               const int64_t* __restrict__ row_start,
+                                                               const int32_t* __restrict__ num_rows,
+                                                               const int64_t* __restrict__ dst_start,
+                                                               uint8_t* __restrict__ dst) {
+  const int c = blockIdx.y;
+  const int64_t bytes = (int64_t)num_rows[c] * row_bytes;
+  const uint8_t* s = src + row_start[c] * row_bytes;
+  uint8_t* d = dst + dst_start[c] * row_bytes;
+  const bool vec = ((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(d) | (uintptr_t)bytes) & 15u) == 0;
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  if (vec) {
+    const int64_t n16 = bytes >> 4;
+    const uint4* s4 = reinterpret_cast<const uint4*>(s);
+    uint4* d4 = reinterpret_cast<uint4*>(d);
+    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n16; i += stride) d4[i] = s4[i];
+  } else {
+    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < bytes; i += stride) d[i] = s[i];
+  }
+}
+
+}  // namespace
+}  // namespace fb
+
+extern "C" {
+
+int fb_gather_rows(const void* src, int64_t row_bytes, const int64_t* row_start, const int32_t* num_rows,
+                   int num_clients, const int64_t* dst_start, void* dst, int64_t max_rows_per_client,
+                   void* stream) {
+  FB_REQUIRE(row_bytes > 0 && num_clients >= 0 && num_clients <= 65535 && max_rows_per_client >= 0,
+             "gather_rows: bad arguments");
+  if (num_clients == 0 || max_rows_per_client == 0) return FB_OK;
+  const int64_t bytes = max_rows_per_client * row_bytes;
+  int64_t chunks = (bytes / 16 + fb::kThreads * 4 - 1) / (fb::kThreads * 4);
+  if (chunks < 1) chunks = 1;
+  if (chunks > 64) chunks = 64;
+  cudaStream_t s = fb::as_stream(stream);
+  FB_LAUNCH("gather_rows_kernel", s,
+            fb::gather_rows_kernel<<<dim3((unsigned)chunks, num_clients), fb::kThreads, 0, s>>>(
+                static_cast<const uint8_t*>(src), row_bytes, row_start, num_rows, dst_start,
+                static_cast<uint8_t*>(dst)));
+  return fb::launch_status("gather_rows_kernel");
+}
+
+}  // extern "C"

@@ -118,8 +118,8 @@ int fb_gaussian_f32(float* out, int64_t n, double std, uint64_t seed, uint64_t o
   FB_REQUIRE((offset & 3) == 0, "gaussian: offset must be a multiple of 4");
   if (n == 0) return FB_OK;
   const int64_t groups = (n + 3) >> 2;
-  fb::gaussian_kernel<<<(unsigned)((groups + fb::kThreads - 1) / fb::kThreads), fb::kThreads, 0,
-                        fb::as_stream(stream)>>>(out, n, (float)std, seed, offset, accumulate);
+  FB_LAUNCH("gaussian_kernel", fb::as_stream(stream), fb::gaussian_kernel<<<(unsigned)((groups + fb::kThreads - 1) / fb::kThreads), fb::kThreads, 0,
+                        fb::as_stream(stream)>>>(out, n, (float)std, seed, offset, accumulate));
   return fb::launch_status("gaussian_kernel");
 }
 
@@ -130,9 +130,9 @@ int fb_noise_avg_sgd_f32(float* theta, const float* agg, int64_t D, double noise
   FB_REQUIRE(inv_weight >= 0.0 && isfinite(inv_weight), "noise_avg_sgd: bad inverse weight");
   if (D == 0) return FB_OK;
   const int64_t groups = (D + 3) >> 2;
-  fb::noise_avg_sgd_kernel<<<(unsigned)((groups + fb::kThreads - 1) / fb::kThreads), fb::kThreads, 0,
+  FB_LAUNCH("noise_avg_sgd_kernel", fb::as_stream(stream), fb::noise_avg_sgd_kernel<<<(unsigned)((groups + fb::kThreads - 1) / fb::kThreads), fb::kThreads, 0,
                              fb::as_stream(stream)>>>(theta, agg, D, (float)noise_std, seed, injected,
-                                                      (float)(lr * inv_weight), agg_out);
+                                                      (float)(lr * inv_weight), agg_out));
   return fb::launch_status("noise_avg_sgd_kernel");
 }
 

@@ -257,9 +257,9 @@ int launch_local_sgd(const float* theta_t, Dims m, const float* X, const int32_t
   FB_UNSUPPORTED(smem <= 227 * 1024, "local_sgd: model needs %zu bytes of shared memory", smem);
   auto kern = local_sgd_small_kernel<kHidden>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<C, kThreads, smem, as_stream(stream)>>>(theta_t, m, X, y, row_start, num_rows, perms,
+  FB_LAUNCH(kHidden ? "local_sgd_mlp_kernel" : "local_sgd_linear_kernel", as_stream(stream), kern<<<C, kThreads, smem, as_stream(stream)>>>(theta_t, m, X, y, row_start, num_rows, perms,
                                                  perm_off, epochs, B, lr, mu, control, ld_control,
-                                                 delta_out, ld_delta, nonfinite);
+                                                 delta_out, ld_delta, nonfinite));
   return launch_status("local_sgd_small_kernel");
 }
 
@@ -274,7 +274,7 @@ int launch_eval(const float* theta, Dims m, const float* X, const int32_t* y,
   FB_UNSUPPORTED(smem <= 227 * 1024, "eval: model needs %zu bytes of shared memory", smem);
   auto kern = eval_small_kernel<kHidden>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<C, kThreads, smem, as_stream(stream)>>>(theta, m, X, y, row_start, num_rows, loss_sum, correct);
+  FB_LAUNCH(kHidden ? "eval_mlp_kernel" : "eval_linear_kernel", as_stream(stream), kern<<<C, kThreads, smem, as_stream(stream)>>>(theta, m, X, y, row_start, num_rows, loss_sum, correct));
   return launch_status("eval_small_kernel");
 }
 

@@ -232,9 +232,17 @@ class DeviceStatistics:
 
 
 class DevicePopulation:
-    """A FederatedDataset packed once into HBM (features fp32, labels int32)."""
+    """A FederatedDataset packed once (features fp32, labels int32).
 
-    def __init__(self, dataset, device):
+    ``residency="device"`` keeps the packed arrays in HBM; ``"host"`` keeps
+    them in pinned host memory and the engine gathers each context's cohort
+    rows to the device (one fb_gather_rows launch reading host memory), the
+    end-to-end data path."""
+
+    def __init__(self, dataset, device, residency: str = "device"):
+        if residency not in ("device", "host"):
+            raise ValueError("residency must be 'device' or 'host'")
+        self.residency = residency
         torch = _torch()
         users = list(dataset.users.values())
         if not users:
@@ -254,7 +262,11 @@ class DevicePopulation:
         for u, s in zip(users, starts):
             X[s:s + u.num_points] = u.features
             y[s:s + u.num_points] = u.labels
-        self.X = torch.from_numpy(X).to(device)
-        self.y = torch.from_numpy(y).to(device)
+        if residency == "device":
+            self.X = torch.from_numpy(X).to(device)
+            self.y = torch.from_numpy(y).to(device)
+        else:
+            self.X = torch.from_numpy(X).pin_memory()
+            self.y = torch.from_numpy(y).pin_memory()
         self.total_rows = total
         self.max_label = int(y.max()) if total else 0

@@ -98,6 +98,15 @@ class _Staging:
         return views
 
 
+@dataclass
+class _GatheredPopulation:
+    """This context's cohort rows, gathered to the device in cohort order."""
+
+    X: Any
+    y: Any
+    dim: int
+
+
 class _ModelRunner:
     """Dispatches eval / local SGD to the model's fb_* entry points."""
 
@@ -159,6 +168,7 @@ class GpuSimulationEngine:
         device=None,
         process_group=None,
         central_epilogue: str = "rank0",
+        data_residency: str = "device",
     ):
         if num_workers < 1:
             raise ValueError("num_workers must be >= 1")
@@ -178,6 +188,9 @@ class GpuSimulationEngine:
             raise ValueError(f"GpuSimulationEngine: unsupported aggregator {type(aggregator).__name__}")
         if central_epilogue not in ("rank0", "replicated"):
             raise ValueError("central_epilogue must be 'rank0' or 'replicated'")
+        if data_residency not in ("device", "host"):
+            raise ValueError("data_residency must be 'device' or 'host'")
+        self.data_residency = data_residency
         torch = _torch()
         native.lib()  # fail loudly: no CUDA device / no library => no engine
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -203,7 +216,7 @@ class GpuSimulationEngine:
         self._pops: dict[Population, DevicePopulation] = {}
         self._runners: dict[int, _ModelRunner] = {}
         self.stream = torch.cuda.current_stream(self.device)
-        self.last_timings: dict[str, float] = {}
+        self.io_bytes = {"h2d": 0, "d2h": 0}  # cumulative host<->device traffic of run_iteration
 
     @property
     def num_workers(self) -> int:
@@ -215,7 +228,7 @@ class GpuSimulationEngine:
 
     def population(self, pop: Population) -> DevicePopulation:
         if pop not in self._pops:
-            self._pops[pop] = DevicePopulation(self._datasets[pop], self.device)
+            self._pops[pop] = DevicePopulation(self._datasets[pop], self.device, self.data_residency)
         return self._pops[pop]
 
     def _runner(self, model) -> _ModelRunner:
@@ -269,6 +282,12 @@ class GpuSimulationEngine:
         row_start = pop.row_start[idx]
         num_rows = pop.num_rows[idx]
         train = plan.train is not None
+        gathered = pop.residency == "host"
+        if gathered:  # kernels see the cohort's rows packed in cohort order
+            src_start = row_start
+            row_start = np.zeros(C, dtype=np.int64)
+            if C > 1:
+                row_start[1:] = np.cumsum(num_rows[:-1].astype(np.int64))
         host = [row_start, num_rows]
         if train:
             tp = plan.train
@@ -280,8 +299,22 @@ class GpuSimulationEngine:
             w = (num_rows.astype(np.float32) if plan.weighting == "datapoints"
                  else np.ones(C, dtype=np.float32))
             host += [perm_flat, perm_off, w]
+        if gathered:
+            host.append(src_start)
         dev = self._staging.upload(host)
+        self.io_bytes["h2d"] += sum(int(a.nbytes) for a in host)
         d_row_start, d_num_rows = dev[0], dev[1]
+        if gathered:
+            rows = int(num_rows.sum())
+            gX = self.ws.tensor("gather_X", (max(rows, 1), pop.dim), torch.float32)
+            gy = self.ws.tensor("gather_y", (max(rows, 1),), torch.int32)
+            mx = int(num_rows.max()) if C else 0
+            native.call("fb_gather_rows", native.ptr(pop.X), 4 * pop.dim, native.ptr(dev[-1]), native.ptr(d_num_rows),
+                        C, native.ptr(d_row_start), native.ptr(gX), mx, stream)
+            native.call("fb_gather_rows", native.ptr(pop.y), 4, native.ptr(dev[-1]), native.ptr(d_num_rows), C,
+                        native.ptr(d_row_start), native.ptr(gy), mx, stream)
+            self.io_bytes["h2d"] += rows * (4 * pop.dim + 4)
+            pop = _GatheredPopulation(gX, gy, pop.dim)
 
         # per-client result block: loss f64, norm f64 | correct, clipped, nonfinite i32
         Cp = max(C, 1)
@@ -319,6 +352,7 @@ class GpuSimulationEngine:
 
         # one D2H copy of the per-client results
         host_res = res[: 16 * Cp + 12 * Cp].to("cpu", non_blocking=False)
+        self.io_bytes["d2h"] += int(host_res.numel())
         h_loss = host_res[: 8 * Cp].view(torch.float64).numpy()[:C]
         h_norm = host_res[8 * Cp: 16 * Cp].view(torch.float64).numpy()[:C]
         h_ints = host_res[16 * Cp:].view(torch.int32).numpy()

@@ -30,6 +30,9 @@ SIGNATURES: dict[str, tuple] = {
     "fb_abi_version": (_i32, []),
     "fb_last_error": (C.c_char_p, []),
     "fb_device_info": (_i32, [_i32, C.POINTER(_i32), C.POINTER(_i64)]),
+    "fb_launch_count": (_i64, []),
+    "fb_timing_enable": (None, [_i32]),
+    "fb_timing_report": (_i32, [C.c_char_p, _i32, C.POINTER(_f64), C.POINTER(_i64), _i32]),
     "fb_eval_linear_f32": (_i32, [_p, _i32, _i32, _p, _p, _p, _p, _i32, _p, _p, _p]),
     "fb_eval_mlp_f32": (_i32, [_p, _i32, _i32, _i32, _p, _p, _p, _p, _i32, _p, _p, _p]),
     "fb_local_sgd_linear_f32": (
@@ -40,6 +43,7 @@ SIGNATURES: dict[str, tuple] = {
         _i32,
         [_p, _i32, _i32, _i32, _p, _p, _p, _p, _p, _p, _i32, _i32, _i32, _f32, _f32, _p, _i64, _p, _i64, _p, _p],
     ),
+    "fb_gather_rows": (_i32, [_p, _i64, _p, _p, _i32, _p, _p, _i64, _p]),
     "fb_cnn_workspace_bytes": (_i64, [_i32, _i32]),
     "fb_eval_cnn_f32": (_i32, [_p, _p, _p, _p, _p, _i32, _i64, _p, _p, _i32, _p, _i64, _p]),
     "fb_local_sgd_cnn_f32": (
@@ -100,9 +104,21 @@ def call(name: str, *args) -> int:
     """Invoke an fb_* entry point; raise on a non-zero status."""
     fn = getattr(lib(), name)
     rc = fn(*args)
-    if SIGNATURES[name][0] is _i32 and name not in ("fb_abi_version",):
+    if SIGNATURES[name][0] is _i32 and name not in ("fb_abi_version", "fb_timing_report"):
         check(rc, name)
     return rc
+
+
+def timing_report(max_entries: int = 256) -> dict[str, tuple[float, int]]:
+    """{kernel name: (summed device ms, launches)} since fb_timing_enable(1)."""
+    L = lib()
+    names = C.create_string_buffer(64 * max_entries)
+    ms = (_f64 * max_entries)()
+    cnt = (_i64 * max_entries)()
+    k = L.fb_timing_report(names, len(names), ms, cnt, max_entries)
+    check(0 if k >= 0 else k, "fb_timing_report")
+    keys = names.value.decode().split("\n")[:k]
+    return {n: (ms[i], cnt[i]) for i, n in enumerate(keys)}
 
 
 def ptr(t) -> int | None:

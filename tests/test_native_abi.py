@@ -18,7 +18,7 @@ def _declared() -> dict[str, int]:
     names = {}
     for h in (ROOT / "include").glob("*.h"):
         text = re.sub(r"/\*.*?\*/", "", h.read_text(), flags=re.S)
-        for m in re.finditer(r"\b(?:int|int64_t|const char\*)\s+(fb_\w+)\s*\(([^)]*)\)\s*;", text):
+        for m in re.finditer(r"\b(?:void|int|int64_t|const char\*)\s+(fb_\w+)\s*\(([^)]*)\)\s*;", text):
             args = [a for a in m.group(2).split(",") if a.strip() and a.strip() != "void"]
             names[m.group(1)] = len(args)
     return names
