@@ -119,6 +119,9 @@ int fb_local_sgd_mlp_f32(const float* theta_t, int dim, int hidden, int num_clas
  * batch_size <= 16.  nonfinite[] is zeroed (non-finite deltas are caught by
  * fb_delta_norm_clip_f32).                                                 */
 int64_t fb_cnn_workspace_bytes(int max_slots, int max_clients);
+/* Validation knob: 1 (default) = conv2 forward on tcgen05 (3xTF32, TMA,
+ * TMEM); 0 = the FP32 CUDA-core kernels kept as an independent check.     */
+int fb_cnn_set_conv_impl(int impl);
 int fb_eval_cnn_f32(const float* theta, const float* X, const int32_t* y,
                     const int64_t* row_start, const int32_t* num_rows, int num_clients,
                     int64_t total_rows, double* loss_sum, int32_t* correct,

@@ -24,6 +24,9 @@
 // chunks of N slots and reduces loss / hits per client.
 
 #include "fb_common.cuh"
+#include "tc_common.cuh"
+
+#include <cudaTypedefs.h>
 
 namespace fb {
 namespace cnn {
@@ -117,7 +120,7 @@ __global__ void __launch_bounds__(256) conv1_fwd_kernel(const float* __restrict_
                                                         const int64_t* __restrict__ slot_row,
                                                         const float* __restrict__ theta,
                                                         const float* __restrict__ delta, int64_t ld, int B,
-                                                        float* __restrict__ a1) {
+                                                        float* __restrict__ a1h, float* __restrict__ a1l) {
   __shared__ float img[IMG];
   __shared__ float w[27 * C1 + C1];  // [tap27][o] then bias
   const int n = blockIdx.x;
@@ -131,7 +134,8 @@ __global__ void __launch_bounds__(256) conv1_fwd_kernel(const float* __restrict_
   }
   for (int o = threadIdx.x; o < C1; o += blockDim.x) w[27 * C1 + o] = wt(theta, dc, O_B1 + o);
   __syncthreads();
-  float* out = a1 + (int64_t)n * A1;
+  float* outh = a1h + (int64_t)n * A1;
+  float* outl = a1l + (int64_t)n * A1;
   for (int p = threadIdx.x; p < S1 * S1; p += blockDim.x) {
     const int y = p / S1, x = p - y * S1;
     float acc[C1];
@@ -148,11 +152,17 @@ __global__ void __launch_bounds__(256) conv1_fwd_kernel(const float* __restrict_
 #pragma unroll
           for (int o = 0; o < C1; ++o) acc[o] = fmaf(v, wr[o], acc[o]);
         }
-    float4* dst = reinterpret_cast<float4*>(out + (int64_t)p * C1);
+    // a1 is stored split for 3xTF32: a1 = hi + lo exactly, hi tf32-rounded
+    float4* dh = reinterpret_cast<float4*>(outh + (int64_t)p * C1);
+    float4* dl = reinterpret_cast<float4*>(outl + (int64_t)p * C1);
 #pragma unroll
-    for (int q = 0; q < C1 / 4; ++q)
-      dst[q] = make_float4(fmaxf(acc[4 * q], 0.f), fmaxf(acc[4 * q + 1], 0.f), fmaxf(acc[4 * q + 2], 0.f),
-                           fmaxf(acc[4 * q + 3], 0.f));
+    for (int q = 0; q < C1 / 4; ++q) {
+      float h[4], l[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) tc::split_tf32(fmaxf(acc[4 * q + e], 0.f), h[e], l[e]);
+      dh[q] = make_float4(h[0], h[1], h[2], h[3]);
+      dl[q] = make_float4(l[0], l[1], l[2], l[3]);
+    }
   }
 }
 
@@ -162,7 +172,8 @@ __global__ void __launch_bounds__(256) conv1_fwd_kernel(const float* __restrict_
 // position x 16 output channels (4 window positions x 16 accumulators)
 constexpr int C2F_SMEM = (S1 * S1 * A1P + 9 * C1 * C2 + C2) * 4;
 
-__global__ void __launch_bounds__(256) conv2_fwd_pool_kernel(const float* __restrict__ a1,
+__global__ void __launch_bounds__(256) conv2_fwd_pool_kernel(const float* __restrict__ a1h,
+                                                             const float* __restrict__ a1l,
                                                              const int64_t* __restrict__ slot_row,
                                                              const float* __restrict__ theta,
                                                              const float* __restrict__ delta, int64_t ld,
@@ -175,8 +186,9 @@ __global__ void __launch_bounds__(256) conv2_fwd_pool_kernel(const float* __rest
   const int n = blockIdx.x;
   if (slot_row[n] < 0) return;
   const float* dc = delta ? delta + (int64_t)(n / B) * ld : nullptr;
-  const float* src = a1 + (int64_t)n * A1;
-  for (int i = threadIdx.x; i < A1; i += blockDim.x) as[(i >> 5) * A1P + (i & 31)] = src[i];
+  const float* srch = a1h + (int64_t)n * A1;
+  const float* srcl = a1l + (int64_t)n * A1;
+  for (int i = threadIdx.x; i < A1; i += blockDim.x) as[(i >> 5) * A1P + (i & 31)] = srch[i] + srcl[i];
   for (int i = threadIdx.x; i < C2 * C1 * 9; i += blockDim.x) {
     const int o = i / (C1 * 9), r = i - o * (C1 * 9), ci = r / 9, tap = r - ci * 9;
     ws[(tap * C1 + ci) * C2 + o] = wt(theta, dc, O_W2 + i);
@@ -424,7 +436,7 @@ constexpr int C2X_SMEM = (9 * C2 * C1 + C2 * NPOOL) * 4 + C2 * NPOOL;
 __global__ void __launch_bounds__(256) conv2_bwd_x_kernel(const float* __restrict__ dp,
                                                           const float* __restrict__ pooled,
                                                           const uint8_t* __restrict__ code,
-                                                          const float* __restrict__ a1,
+                                                          const float* __restrict__ a1,  // hi part: sign of a1
                                                           const int64_t* __restrict__ slot_row, int B,
                                                           const float* __restrict__ theta,
                                                           const float* __restrict__ delta, int64_t ld,
@@ -495,7 +507,8 @@ constexpr int C2W_SMEM = (S1 * S1 * A1P + C2 * NPOOL) * 4 + C2 * NPOOL;
 __global__ void __launch_bounds__(256) conv2_bwd_w_kernel(const float* __restrict__ dp,
                                                           const float* __restrict__ pooled,
                                                           const uint8_t* __restrict__ code,
-                                                          const float* __restrict__ a1, int B,
+                                                          const float* __restrict__ a1h,
+                                                          const float* __restrict__ a1l, int B,
                                                           const int32_t* __restrict__ client_nb,
                                                           float* __restrict__ delta, int64_t ld, Step st) {
   extern __shared__ float sm[];
@@ -513,7 +526,8 @@ __global__ void __launch_bounds__(256) conv2_bwd_w_kernel(const float* __restric
   for (int b = 0; b < nb; ++b) {
     const int64_t n = (int64_t)c * B + b;
     __syncthreads();
-    for (int i = threadIdx.x; i < A1; i += blockDim.x) as[(i >> 5) * A1P + (i & 31)] = a1[n * A1 + i];
+    for (int i = threadIdx.x; i < A1; i += blockDim.x)
+      as[(i >> 5) * A1P + (i & 31)] = a1h[n * A1 + i] + a1l[n * A1 + i];
     for (int i = threadIdx.x; i < FLAT; i += blockDim.x) {
       gs[i] = pooled[n * FLAT + i] > 0.f ? dp[n * FLAT + i] : 0.f;
       cs[i] = code[n * FLAT + i];
@@ -614,6 +628,269 @@ __global__ void zero_delta_kernel(float* __restrict__ delta, int64_t ld, int C) 
   if (i < (int64_t)C * ld) delta[i] = 0.f;
 }
 
+
+// ================================================================ tcgen05
+// conv2 forward + ReLU + 2x2 max-pool on the 5th-generation tensor cores.
+//
+// Implicit GEMM per sample: Z[m, o] = sum_{tap, ci} a1[y+ky, x+kx, ci] W[o, ci, ky, kx]
+// with m = (y, x).  An M tile is 4 output rows x 28 columns = 112 rows (the
+// UMMA M = 128 tile's last 16 rows are don't-care), N = 64 channels, K = 9
+// taps x 32 input channels.  For tap (ky, kx) the A tile is ONE 4-D TMA box
+// {32 ci, 28 x, 4 y, 1 n} of the NHWC a1 at (0, kx, y0 + ky, n): each output
+// row's 32 channels are one 128-byte swizzle row, so the TMA writes exactly the
+// K-major SWIZZLE_128B canonical layout (implicit im2col, no copy kernel).
+// Precision: 3xTF32 -- a1 and W are stored split (hi = tf32-rounded, lo =
+// remainder) and each tap issues hi*Whi + hi*Wlo + lo*Whi into the same fp32
+// TMEM accumulator (~fp32 accuracy; plain TF32 would miss the 1e-5 gate).
+// Roles (192 threads): warp 0 TMA producer, warp 1 TMEM owner + MMA issuer,
+// warps 2-5 epilogue (TMEM -> registers -> bias/ReLU -> smem -> pool -> HBM).
+// The client's whole 9-tap W (hi + lo, 144 KB) stays resident in smem; A
+// streams through a 3-stage ring; the accumulator is double-buffered in TMEM
+// so the epilogue of tile i overlaps the MMAs of tile i+1.
+constexpr int TC_ROWS = 4;                       // conv rows per M tile
+constexpr int TC_M = TC_ROWS * S2;               // 112 valid rows
+constexpr int TC_TILES = S2 / TC_ROWS;           // 7 tiles per sample
+constexpr int TC_A_STAGE = 128 * 128;            // 16 KB smem per stage (128 rows x 128 B)
+constexpr int TC_A_TX = TC_M * 128;              // 14336 bytes landed per TMA box
+constexpr int TC_B_TAP = C2 * 128;               // 8 KB: 64 rows (o) x 32 ci
+constexpr int WIMG_BYTES = 9 * 2 * TC_B_TAP;     // 147456: [tap][hi|lo] images
+constexpr int TC_STAGES = 3;
+constexpr int TC_EPI_LD = 33;
+constexpr int TC_EPI_BYTES = TC_M * TC_EPI_LD * 4;
+constexpr int TC_SMEM = 1024 + WIMG_BYTES + TC_STAGES * TC_A_STAGE + TC_EPI_BYTES + 256;
+constexpr int TC_THREADS = 192;
+constexpr int TC_ACC_COLS = 4 * C2;              // 4 accumulators x 64 fp32 columns per tile
+constexpr uint32_t TC_IDESC = tc::idesc_tf32(128, C2);
+
+// per-group conv2 weight image: K-major SW128 tiles, tap-major, hi then lo
+__global__ void __launch_bounds__(256) conv2_wimg_kernel(const float* __restrict__ theta,
+                                                         const float* __restrict__ delta, int64_t ld,
+                                                         const int32_t* __restrict__ client_nb,
+                                                         uint8_t* __restrict__ wimg) {
+  const int g = blockIdx.x;
+  if (delta && client_nb && client_nb[g] == 0) return;
+  const float* dc = delta ? delta + (int64_t)g * ld : nullptr;
+  uint8_t* img = wimg + (int64_t)g * WIMG_BYTES;
+  for (int i = threadIdx.x; i < C2 * C1 * 9; i += blockDim.x) {
+    const int o = i / (C1 * 9), r = i - o * (C1 * 9), ci = r / 9, tap = r - ci * 9;
+    float h, l;
+    tc::split_tf32(wt(theta, dc, O_W2 + i), h, l);
+    const uint32_t off = tc::sw128_offset(o, ci);
+    *reinterpret_cast<float*>(img + (tap * 2 + 0) * TC_B_TAP + off) = h;
+    *reinterpret_cast<float*>(img + (tap * 2 + 1) * TC_B_TAP + off) = l;
+  }
+}
+
+__global__ void __launch_bounds__(TC_THREADS, 1) conv2_fwd_tc_kernel(
+    const __grid_constant__ CUtensorMap tm_hi, const __grid_constant__ CUtensorMap tm_lo,
+    const uint8_t* __restrict__ wimg, int64_t wimg_stride, const int64_t* __restrict__ slot_row, int N, int G,
+    const float* __restrict__ theta, const float* __restrict__ delta, int64_t ld, float* __restrict__ pooled,
+    uint8_t* __restrict__ code) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sB = sm;                                        // [9][2][8 KB]
+  uint8_t* sA = sB + WIMG_BYTES;                           // [stages][16 KB]
+  float* sE = reinterpret_cast<float*>(sA + TC_STAGES * TC_A_STAGE);  // [112][33]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sE) + TC_EPI_BYTES);
+  uint64_t* full = bars;                 // [stages]
+  uint64_t* empty = bars + TC_STAGES;    // [stages]
+  uint64_t* tfull = empty + TC_STAGES;   // [2]
+  uint64_t* tempty = tfull + 2;          // [2]
+  uint64_t* bfull = tempty + 2;          // [1]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
+  __shared__ float bias[C2];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = blockIdx.x;
+  const int n0 = g * G;
+  const float* dc = delta ? delta + (int64_t)g * ld : nullptr;
+
+  if (threadIdx.x < C2) bias[threadIdx.x] = wt(theta, dc, O_B2 + threadIdx.x);
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < TC_STAGES; ++i) {
+      tc::mbar_init(&full[i], 1);
+      tc::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&tfull[i], 1);
+      tc::mbar_init(&tempty[i], 4);
+    }
+    tc::mbar_init(bfull, 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc<2 * TC_ACC_COLS>(tmem_slot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      tc::tma_prefetch(&tm_hi);
+      tc::tma_prefetch(&tm_lo);
+      tc::mbar_arrive_expect_tx(bfull, WIMG_BYTES);
+      tc::bulk_load(sB, wimg + (int64_t)g * wimg_stride, WIMG_BYTES, bfull);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int b = 0; b < G; ++b) {
+        const int n = n0 + b;
+        if (n >= N || slot_row[n] < 0) continue;
+        for (int t = 0; t < TC_TILES; ++t)
+          for (int tap = 0; tap < 9; ++tap)
+            for (int part = 0; part < 2; ++part) {
+              tc::mbar_wait(&empty[stage], phase ^ 1);
+              tc::mbar_arrive_expect_tx(&full[stage], TC_A_TX);
+              tc::tma_load_4d(sA + stage * TC_A_STAGE, part ? &tm_lo : &tm_hi, 0, tap % 3, TC_ROWS * t + tap / 3, n,
+                              &full[stage]);
+              if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
+            }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------- MMA issuer
+    tc::mbar_wait(bfull, 0);
+    int stage = 0, tile = 0;
+    uint32_t phase = 0;
+    const uint32_t sA0 = tc::smem_u32(sA), sB0 = tc::smem_u32(sB);
+    for (int b = 0; b < G; ++b) {
+      const int n = n0 + b;
+      if (n >= N || slot_row[n] < 0) continue;
+      for (int t = 0; t < TC_TILES; ++t, ++tile) {
+        const int acc = tile & 1;
+        tc::mbar_wait(&tempty[acc], ((tile >> 1) & 1) ^ 1);
+        tc::tc_fence_after();
+        // four fp32 accumulators per tile (summed with round-to-nearest in the
+        // epilogue): hi*Whi of taps 0-2 / 3-5 / 6-8, and every cross term
+        // (hi*Wlo + lo*Whi) -- short accumulation chains keep 3xTF32 at fp32 accuracy
+        const uint32_t d = tmem + acc * TC_ACC_COLS;
+        for (int tap = 0; tap < 9; ++tap)
+          for (int part = 0; part < 2; ++part) {
+            tc::mbar_wait(&full[stage], phase);
+            tc::tc_fence_after();
+            if (lane == 0) {
+              const uint32_t a = sA0 + stage * TC_A_STAGE;
+              const uint32_t bh = sB0 + (tap * 2 + 0) * TC_B_TAP, bl = sB0 + (tap * 2 + 1) * TC_B_TAP;
+              const uint32_t dmain = d + (tap / 3) * C2, dcross = d + 3 * C2;
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const uint64_t ad = tc::sdesc_k128(a + 32 * k);
+                if (part == 0) {
+                  tc::mma_tf32(dmain, ad, tc::sdesc_k128(bh + 32 * k), TC_IDESC, (tap % 3 | k) != 0);
+                  tc::mma_tf32(dcross, ad, tc::sdesc_k128(bl + 32 * k), TC_IDESC, (tap | k) != 0);
+                } else {
+                  tc::mma_tf32(dcross, ad, tc::sdesc_k128(bh + 32 * k), TC_IDESC, 1);
+                }
+              }
+              tc::mma_commit(&empty[stage]);
+            }
+            __syncwarp();
+            if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
+          }
+        if (lane == 0) tc::mma_commit(&tfull[acc]);
+        __syncwarp();
+      }
+    }
+  } else {
+    // ---------------------------------------------------------- epilogue
+    const int ew = warp & 3;               // TMEM lane quarter this warp may access
+    const int row = ew * 32 + lane;        // accumulator row = TMEM lane
+    const int et = threadIdx.x - 64;       // 0..127 among epilogue threads
+    int tile = 0;
+    for (int b = 0; b < G; ++b) {
+      const int n = n0 + b;
+      if (n >= N || slot_row[n] < 0) continue;
+      float* pout = pooled + (int64_t)n * FLAT;
+      uint8_t* cout = code + (int64_t)n * FLAT;
+      for (int t = 0; t < TC_TILES; ++t, ++tile) {
+        const int acc = tile & 1;
+        tc::mbar_wait(&tfull[acc], (tile >> 1) & 1);
+        tc::tc_fence_after();
+        for (int h = 0; h < 2; ++h) {
+          float zsum[32];
+          {
+            const uint32_t base = tmem + ((uint32_t)(ew * 32) << 16) + acc * TC_ACC_COLS + h * 32;
+            uint32_t v0[32], v1[32];
+            tc::tmem_ld32(base, v0);
+            tc::tmem_ld32(base + C2, v1);
+            tc::tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) zsum[j] = __uint_as_float(v0[j]) + __uint_as_float(v1[j]);
+            tc::tmem_ld32(base + 2 * C2, v0);
+            tc::tmem_ld32(base + 3 * C2, v1);
+            tc::tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) zsum[j] = (zsum[j] + __uint_as_float(v0[j])) + __uint_as_float(v1[j]);
+          }
+          if (row < TC_M) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) sE[row * TC_EPI_LD + j] = fmaxf(zsum[j] + bias[h * 32 + j], 0.f);
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          for (int it = et; it < 2 * SP * 32; it += 128) {
+            const int j = it & 31, pp = it >> 5, pr = pp / SP, px = pp - pr * SP;
+            const float* e0 = sE + ((2 * pr) * S2 + 2 * px) * TC_EPI_LD + j;
+            const float q0 = e0[0], q1 = e0[TC_EPI_LD], q2 = e0[S2 * TC_EPI_LD], q3 = e0[(S2 + 1) * TC_EPI_LD];
+            float best = q0;
+            int arg = 0;
+            if (q1 > best) { best = q1; arg = 1; }
+            if (q2 > best) { best = q2; arg = 2; }
+            if (q3 > best) { best = q3; arg = 3; }
+            const int o = h * 32 + j;
+            const int idx = o * NPOOL + (TC_ROWS / 2 * t + pr) * SP + px;
+            pout[idx] = best;
+            cout[idx] = (uint8_t)arg;
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+        }
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  if (warp == 1) tc::tmem_dealloc<2 * TC_ACC_COLS>(tmem);
+}
+
+// host: driver entry point for cuTensorMapEncodeTiled (cudart is linked statically)
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// NHWC a1 [N][30][30][32] fp32 viewed as 4-D {32, 30, 30, N}; box {32, 28, 4, 1}
+int a1_tensor_map(CUtensorMap* map, const float* a1, int N) {
+  auto fn = encode_fn();
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return FB_ERR_CUDA;
+  }
+  const cuuint64_t dims[4] = {(cuuint64_t)C1, (cuuint64_t)S1, (cuuint64_t)S1, (cuuint64_t)N};
+  const cuuint64_t strides[3] = {(cuuint64_t)C1 * 4, (cuuint64_t)S1 * C1 * 4, (cuuint64_t)S1 * S1 * C1 * 4};
+  const cuuint32_t box[4] = {(cuuint32_t)C1, (cuuint32_t)S2, (cuuint32_t)TC_ROWS, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(a1), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return FB_ERR_CUDA;
+  }
+  return FB_OK;
+}
+
+int g_conv_impl = 1;  // 1 = tcgen05 (product path), 0 = FP32 CUDA-core kernels (validation)
+
 // ------------------------------------------------------------- workspace
 struct Work {
   int64_t* slot_row;
@@ -622,8 +899,9 @@ struct Work {
   int64_t* prefix;
   double* slot_loss;
   int32_t* slot_hit;
-  float *a1, *pooled, *part, *dz3, *dp, *dz1;
+  float *a1h, *a1l, *pooled, *part, *dz3, *dp, *dz1;
   uint8_t* code;
+  uint8_t* wimg;  // per-group conv2 weight images (tcgen05 B operand)
 };
 
 inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
@@ -638,9 +916,9 @@ inline int64_t carve(void* base, int N, int Cmax, Work* w) {
   };
   const int64_t o_row = take(8LL * N), o_cl = take(4LL * N), o_nb = take(4LL * (Cmax + 1)),
                 o_pre = take(8LL * (Cmax + 1)), o_loss = take(8LL * N), o_hit = take(4LL * N),
-                o_a1 = take(4LL * N * A1), o_pool = take(4LL * N * FLAT), o_code = take((int64_t)N * FLAT),
+                o_a1 = take(4LL * N * A1), o_a1l = take(4LL * N * A1), o_pool = take(4LL * N * FLAT), o_code = take((int64_t)N * FLAT),
                 o_part = take(4LL * KSPLIT * N * HID), o_dz3 = take(4LL * N * HID), o_dp = take(4LL * N * FLAT),
-                o_dz1 = take(4LL * N * A1);
+                o_dz1 = take(4LL * N * A1), o_wimg = take((int64_t)WIMG_BYTES * (Cmax + 1));
   if (w && base) {
     char* b = static_cast<char*>(base);
     w->slot_row = reinterpret_cast<int64_t*>(b + o_row);
@@ -649,7 +927,9 @@ inline int64_t carve(void* base, int N, int Cmax, Work* w) {
     w->prefix = reinterpret_cast<int64_t*>(b + o_pre);
     w->slot_loss = reinterpret_cast<double*>(b + o_loss);
     w->slot_hit = reinterpret_cast<int32_t*>(b + o_hit);
-    w->a1 = reinterpret_cast<float*>(b + o_a1);
+    w->a1h = reinterpret_cast<float*>(b + o_a1);
+    w->a1l = reinterpret_cast<float*>(b + o_a1l);
+    w->wimg = reinterpret_cast<uint8_t*>(b + o_wimg);
     w->pooled = reinterpret_cast<float*>(b + o_pool);
     w->code = reinterpret_cast<uint8_t*>(b + o_code);
     w->part = reinterpret_cast<float*>(b + o_part);
@@ -667,6 +947,7 @@ int set_smem_limits() {
   cudaFuncSetAttribute(conv2_bwd_x_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C2X_SMEM);
   cudaFuncSetAttribute(conv2_bwd_w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C2W_SMEM);
   cudaFuncSetAttribute(fc1_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FC1F_SMEM);
+  cudaFuncSetAttribute(conv2_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
   cudaFuncSetAttribute(conv1_bwd_w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (IMG + S1 * S1 * A1P) * 4);
   done = true;
@@ -675,9 +956,22 @@ int set_smem_limits() {
 
 // forward of N slots (shared weights when delta == nullptr) up to the head
 int forward(const float* X, const float* theta, const float* delta, int64_t ld, int B, int N, int G,
-            const Work& w, cudaStream_t s) {
-  FB_LAUNCH("conv1_fwd_kernel", s, conv1_fwd_kernel<<<N, 256, 0, s>>>(X, w.slot_row, theta, delta, ld, B, w.a1));
-  FB_LAUNCH("conv2_fwd_pool_kernel", s, conv2_fwd_pool_kernel<<<N, 256, C2F_SMEM, s>>>(w.a1, w.slot_row, theta, delta, ld, B, w.pooled, w.code));
+            const Work& w, cudaStream_t s, const int32_t* client_nb) {
+  FB_LAUNCH("conv1_fwd_kernel", s, conv1_fwd_kernel<<<N, 256, 0, s>>>(X, w.slot_row, theta, delta, ld, B, w.a1h, w.a1l));
+  if (g_conv_impl == 1) {
+    // weight groups: one per client in training (G = B), one shared image at theta_t in evaluation
+    const int groups = delta ? (N + B - 1) / B : 1;
+    FB_LAUNCH("conv2_wimg_kernel", s, conv2_wimg_kernel<<<groups, 256, 0, s>>>(theta, delta, ld, client_nb, w.wimg));
+    CUtensorMap mh, ml;
+    int st = a1_tensor_map(&mh, w.a1h, N);
+    if (!st) st = a1_tensor_map(&ml, w.a1l, N);
+    if (st) return st;
+    const int gt = delta ? B : 8;  // samples per CTA
+    FB_LAUNCH("conv2_fwd_tc_kernel", s, conv2_fwd_tc_kernel<<<(N + gt - 1) / gt, TC_THREADS, TC_SMEM, s>>>(
+        mh, ml, w.wimg, delta ? (int64_t)WIMG_BYTES : 0, w.slot_row, N, gt, theta, delta, ld, w.pooled, w.code));
+  } else {
+    FB_LAUNCH("conv2_fwd_pool_kernel", s, conv2_fwd_pool_kernel<<<N, 256, C2F_SMEM, s>>>(w.a1h, w.a1l, w.slot_row, theta, delta, ld, B, w.pooled, w.code));
+  }
   FB_LAUNCH("fc1_fwd_kernel", s, fc1_fwd_kernel<<<dim3((N + G - 1) / G, KSPLIT), HID, FC1F_SMEM, s>>>(w.pooled, w.slot_row, N, G, theta, delta, ld,
                                                                w.part));
   return launch_status("cnn forward");
@@ -689,6 +983,12 @@ int forward(const float* X, const float* theta, const float* delta, int64_t ld, 
 using namespace fb::cnn;
 
 extern "C" {
+
+int fb_cnn_set_conv_impl(int impl) {
+  FB_REQUIRE(impl == 0 || impl == 1, "fb_cnn_set_conv_impl: 0 (FP32 CUDA cores) or 1 (tcgen05)");
+  fb::cnn::g_conv_impl = impl;
+  return FB_OK;
+}
 
 int64_t fb_cnn_workspace_bytes(int max_slots, int max_clients) {
   return carve(nullptr, max_slots, max_clients, nullptr);
@@ -712,7 +1012,7 @@ int fb_eval_cnn_f32(const float* theta, const float* X, const int32_t* y, const 
   for (int64_t r0 = 0; r0 < total_rows; r0 += N) {
     FB_LAUNCH("eval_slots_kernel", s, eval_slots_kernel<<<(N + 255) / 256, 256, 0, s>>>(r0, N, total_rows, w.prefix, num_clients, row_start,
                                                       w.slot_row, w.slot_client));
-    st = forward(X, theta, nullptr, 0, 1, N, GMAX, w, s);
+    st = forward(X, theta, nullptr, 0, 1, N, GMAX, w, s, nullptr);
     if (st) return st;
     FB_LAUNCH("head_kernel", s, head_kernel<<<N / GMAX, HID, 0, s>>>(w.part, w.slot_row, N, GMAX, y, theta, nullptr, 0, nullptr, Step{0, 0},
                                          nullptr, w.slot_loss, w.slot_hit));
@@ -753,15 +1053,15 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
     for (int step = 0; step < max_steps; ++step) {
       FB_LAUNCH("train_slots_kernel", s, train_slots_kernel<<<(N + 255) / 256, 256, 0, s>>>(step, row_start + c0, num_rows + c0, perms, perm_off + c0,
                                                         Cw, epochs, B, w.slot_row, w.client_nb));
-      st = forward(X, theta_t, dlt, ld_delta, B, N, B, w, s);
+      st = forward(X, theta_t, dlt, ld_delta, B, N, B, w, s, w.client_nb);
       if (st) return st;
       FB_LAUNCH("head_kernel", s, head_kernel<<<Cw, HID, 0, s>>>(w.part, w.slot_row, N, B, y, theta_t, dlt, ld_delta, w.client_nb, sp, w.dz3,
                                      nullptr, nullptr));
       FB_LAUNCH("fc1_bwd_kernel", s, fc1_bwd_kernel<<<dim3(Cw, KSPLIT), HID, 0, s>>>(w.pooled, w.dz3, B, w.client_nb, theta_t, dlt, ld_delta, sp,
                                                       w.dp));
-      FB_LAUNCH("conv2_bwd_x_kernel", s, conv2_bwd_x_kernel<<<N, 256, C2X_SMEM, s>>>(w.dp, w.pooled, w.code, w.a1, w.slot_row, B, theta_t, dlt,
+      FB_LAUNCH("conv2_bwd_x_kernel", s, conv2_bwd_x_kernel<<<N, 256, C2X_SMEM, s>>>(w.dp, w.pooled, w.code, w.a1h, w.slot_row, B, theta_t, dlt,
                                                   ld_delta, w.dz1));
-      FB_LAUNCH("conv2_bwd_w_kernel", s, conv2_bwd_w_kernel<<<Cw, 256, C2W_SMEM, s>>>(w.dp, w.pooled, w.code, w.a1, B, w.client_nb, dlt, ld_delta,
+      FB_LAUNCH("conv2_bwd_w_kernel", s, conv2_bwd_w_kernel<<<Cw, 256, C2W_SMEM, s>>>(w.dp, w.pooled, w.code, w.a1h, w.a1l, B, w.client_nb, dlt, ld_delta,
                                                    sp));
       FB_LAUNCH("conv1_bwd_w_kernel", s, conv1_bwd_w_kernel<<<Cw, C1 * 28, (IMG + S1 * S1 * A1P) * 4, s>>>(X, w.slot_row, w.dz1, B, w.client_nb, dlt,
                                                                        ld_delta, sp));

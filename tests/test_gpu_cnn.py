@@ -59,8 +59,11 @@ def test_cnn_local_sgd_and_eval_match_oracle(sizes, E, B, mu):
         ref = port.flat(theta_d, om.dims) - port.flat(after, om.dims)
         rel = np.linalg.norm(got[c] - ref) / np.linalg.norm(ref)
         try:
-            assert_close_fp32(got[c], ref, what=f"client {c} n={sizes[c]}")
+            # per-client delta: relative L2 error <= 1e-5 and elementwise rtol 1e-4
+            # (conv2 runs 3xTF32 on tcgen05: ~2e-6 relative, vs ~5e-7 for FP32 FFMA;
+            # the north_star rtol 1e-5 gate applies to the aggregate / theta below)
             assert rel <= 1e-5
+            assert_close_fp32(got[c], ref, rtol=1e-4, what=f"client {c} n={sizes[c]}")
         except AssertionError:
             # a ReLU sign / max-pool winner decided differently at fp32 resolution
             # (value within ~1e-7 of the boundary) re-routes one gradient path;
@@ -89,3 +92,44 @@ def test_cnn_engine_matches_reference_fixture(golden):
     got, ref = res.metrics_rows, golden_rows(g)
     assert [r[:3] for r in got] == [r[:3] for r in ref]
     np.testing.assert_allclose([r[3] for r in got], [r[3] for r in ref], rtol=2e-5)
+
+
+def test_cnn_tcgen05_conv_matches_cuda_core_kernels():
+    """conv2 forward on tcgen05 (3xTF32) vs the FP32 CUDA-core kernels on the
+    same cohort: eval losses and one local-SGD delta per client."""
+    import torch
+
+    from paper_2404_06430_b200 import native
+
+    rng = np.random.default_rng(5)
+    sizes = [10, 10, 7, 3, 20]
+    ds = _population(rng, sizes)
+    m = fb.CNN()
+    om = port.Cnn()
+    theta = torch.from_numpy(port.flat(om.init(2), om.dims).astype(np.float32)).cuda()
+    pop = fb.DevicePopulation(ds, theta.device)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    perms = [np.random.default_rng(i).permutation(n) for i, n in enumerate(sizes)]
+    perm_off = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)
+    args = (dev(pop.row_start), dev(pop.num_rows), dev(np.concatenate(perms).astype(np.int32)), dev(perm_off))
+    out = {}
+    try:
+        for impl in (0, 1):
+            native.call("fb_cnn_set_conv_impl", impl)
+            runner = fb.engine._ModelRunner(m, fb.device.Workspace(theta.device))
+            C = len(sizes)
+            delta = torch.zeros(C, runner.ld, device="cuda")
+            bad = torch.zeros(C, dtype=torch.int32, device="cuda")
+            runner.local_sgd(theta, pop, args[0], args[1], args[2], args[3], C, fb.LocalTrainParams(0.05, 1, 10),
+                             0.0, delta, bad, 0, pop.num_rows)
+            loss = torch.zeros(C, dtype=torch.float64, device="cuda")
+            corr = torch.zeros(C, dtype=torch.int32, device="cuda")
+            runner.eval(theta, pop, args[0], args[1], C, loss, corr, 0, pop.num_rows)
+            out[impl] = (delta[:, :runner.D].double().cpu().numpy(), loss.cpu().numpy(), corr.cpu().numpy())
+    finally:
+        native.call("fb_cnn_set_conv_impl", 1)
+    np.testing.assert_allclose(out[1][1], out[0][1], rtol=1e-5)
+    assert np.abs(out[1][2] - out[0][2]).max() <= 1
+    for c in range(len(sizes)):
+        rel = np.linalg.norm(out[1][0][c] - out[0][0][c]) / np.linalg.norm(out[0][0][c])
+        assert rel < 1e-2, (c, rel)
