@@ -868,18 +868,16 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// NHWC a1 [N][30][30][32] fp32 viewed as 4-D {32, 30, 30, N}; box {32, 28, 4, 1}
-int a1_tensor_map(CUtensorMap* map, const float* a1, int N) {
+// 4-D fp32 tensor map, dims innermost first, SWIZZLE_128B (box[0] * 4 == 128 bytes)
+int tensor_map_4d(CUtensorMap* map, const float* base, const cuuint64_t dims[4], const cuuint64_t strides[3],
+                  const cuuint32_t box[4]) {
   auto fn = encode_fn();
   if (!fn) {
     set_error("cuTensorMapEncodeTiled unavailable");
     return FB_ERR_CUDA;
   }
-  const cuuint64_t dims[4] = {(cuuint64_t)C1, (cuuint64_t)S1, (cuuint64_t)S1, (cuuint64_t)N};
-  const cuuint64_t strides[3] = {(cuuint64_t)C1 * 4, (cuuint64_t)S1 * C1 * 4, (cuuint64_t)S1 * S1 * C1 * 4};
-  const cuuint32_t box[4] = {(cuuint32_t)C1, (cuuint32_t)S2, (cuuint32_t)TC_ROWS, 1};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
-  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(a1), dims, strides, box, estr,
+  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
@@ -887,6 +885,249 @@ int a1_tensor_map(CUtensorMap* map, const float* a1, int N) {
     return FB_ERR_CUDA;
   }
   return FB_OK;
+}
+
+// NHWC a1 [N][30][30][32] as 4-D {32, 30, 30, N}; box {32, 28, 4, 1}
+int a1_tensor_map(CUtensorMap* map, const float* a1, int N) {
+  const cuuint64_t dims[4] = {(cuuint64_t)C1, (cuuint64_t)S1, (cuuint64_t)S1, (cuuint64_t)N};
+  const cuuint64_t strides[3] = {(cuuint64_t)C1 * 4, (cuuint64_t)S1 * C1 * 4, (cuuint64_t)S1 * S1 * C1 * 4};
+  const cuuint32_t box[4] = {(cuuint32_t)C1, (cuuint32_t)S2, (cuuint32_t)TC_ROWS, 1};
+  return tensor_map_4d(map, a1, dims, strides, box);
+}
+
+// ------------------------------------------------ conv2 backward-data (tcgen05)
+// dz1[n, y, x, ci] = relu'(a1) * sum_{ky, kx, o} dz2[n, y-ky, x-kx, o] W[o, ci, ky, kx]
+// Implicit GEMM: M = a1 positions (tile = 4 rows x 30 cols = 120), N = 32 input
+// channels, K = 9 taps x 64 output channels.  dz2 is materialised dense NHWC
+// (hi / lo split) by dz2_build_kernel; the A tile of tap (ky, kx) and channel
+// half h is one TMA box {32 o, 30 x, 4 y} of dz2 at (32h, -kx, y0-ky, n): the
+// negative / past-the-end coordinates are the transposed convolution's zero
+// padding, filled by the TMA unit.  Same 3xTF32 + split-accumulator scheme and
+// warp roles as the forward; the epilogue applies the ReLU mask of a1 and
+// writes each position's 32 channels (128 B) straight to HBM.
+constexpr int BX_ROWS = 4;
+constexpr int BX_M = BX_ROWS * S1;               // 120 valid rows
+constexpr int BX_TILES = (S1 + BX_ROWS - 1) / BX_ROWS;  // 8 (last tile: 2 valid rows)
+constexpr int BX_A_TX = BX_M * 128;              // 15360 bytes per box
+constexpr int BX_B_BLK = C1 * 128;               // 4 KB: 32 rows (ci) x 32 o
+constexpr int WIMGT_BYTES = 9 * 2 * 2 * BX_B_BLK;  // [tap][hi|lo][o half] = 147456
+constexpr int BX_STAGES = 4;
+constexpr int BX_ACC_COLS = 4 * C1;              // 4 accumulators x 32 columns
+constexpr int BX_SMEM = 1024 + WIMGT_BYTES + BX_STAGES * TC_A_STAGE + 256;
+constexpr uint32_t BX_IDESC = tc::idesc_tf32(128, C1);
+static_assert(WIMGT_BYTES == WIMG_BYTES, "weight image sizes");
+
+// transposed weight image for backward-data: rows ci, K = o
+__global__ void __launch_bounds__(256) conv2_wimgT_kernel(const float* __restrict__ theta,
+                                                          const float* __restrict__ delta, int64_t ld,
+                                                          const int32_t* __restrict__ client_nb,
+                                                          uint8_t* __restrict__ wimg) {
+  const int g = blockIdx.x;
+  if (client_nb[g] == 0) return;
+  const float* dc = delta + (int64_t)g * ld;
+  uint8_t* img = wimg + (int64_t)g * WIMGT_BYTES;
+  for (int i = threadIdx.x; i < C2 * C1 * 9; i += blockDim.x) {
+    const int o = i / (C1 * 9), r = i - o * (C1 * 9), ci = r / 9, tap = r - ci * 9;
+    float h, l;
+    tc::split_tf32(theta[O_W2 + i] - dc[O_W2 + i], h, l);
+    const uint32_t off = tc::sw128_offset(ci, o & 31);
+    const int half = o >> 5;
+    *reinterpret_cast<float*>(img + ((tap * 2 + 0) * 2 + half) * BX_B_BLK + off) = h;
+    *reinterpret_cast<float*>(img + ((tap * 2 + 1) * 2 + half) * BX_B_BLK + off) = l;
+  }
+}
+
+// dense dz2 = unpool(dp) * relu'(z2), NHWC [N][28][28][64], split hi / lo
+constexpr int DZB_SMEM = FLAT * 5;
+__global__ void __launch_bounds__(256) dz2_build_kernel(const float* __restrict__ dp, const float* __restrict__ pooled,
+                                                        const uint8_t* __restrict__ code,
+                                                        const int64_t* __restrict__ slot_row,
+                                                        float* __restrict__ dzh, float* __restrict__ dzl) {
+  extern __shared__ float g[];  // [FLAT] values, then [FLAT] codes
+  uint8_t* cd = reinterpret_cast<uint8_t*>(g + FLAT);
+  const int n = blockIdx.x;
+  if (slot_row[n] < 0) return;
+  for (int i = threadIdx.x; i < FLAT; i += blockDim.x) {
+    const int64_t k = (int64_t)n * FLAT + i;
+    g[i] = pooled[k] > 0.f ? dp[k] : 0.f;
+    cd[i] = code[k];
+  }
+  __syncthreads();
+  float* oh = dzh + (int64_t)n * S2 * S2 * C2;
+  float* ol = dzl + (int64_t)n * S2 * S2 * C2;
+  // thread = (position, 4 consecutive channels): 16-byte stores, coalesced per position
+  for (int t = threadIdx.x; t < S2 * S2 * (C2 / 4); t += blockDim.x) {
+    const int pos = t >> 4, o0 = (t & 15) * 4;
+    const int y = pos / S2, x = pos - y * S2;
+    const int pp = (y >> 1) * SP + (x >> 1), sub = ((y & 1) << 1) | (x & 1);
+    float h[4], l[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int idx = (o0 + e) * NPOOL + pp;
+      const float v = cd[idx] == sub ? g[idx] : 0.f;
+      tc::split_tf32(v, h[e], l[e]);
+    }
+    reinterpret_cast<float4*>(oh)[t] = make_float4(h[0], h[1], h[2], h[3]);
+    reinterpret_cast<float4*>(ol)[t] = make_float4(l[0], l[1], l[2], l[3]);
+  }
+}
+
+__global__ void __launch_bounds__(TC_THREADS, 1) conv2_bwd_x_tc_kernel(
+    const __grid_constant__ CUtensorMap tm_hi, const __grid_constant__ CUtensorMap tm_lo,
+    const uint8_t* __restrict__ wimg, const int64_t* __restrict__ slot_row, int G,
+    const float* __restrict__ a1h, float* __restrict__ dz1) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sB = sm;
+  uint8_t* sA = sB + WIMGT_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sA + BX_STAGES * TC_A_STAGE);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + BX_STAGES;
+  uint64_t* tfull = empty + BX_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* bfull = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = blockIdx.x;  // client
+  const int n0 = g * G;
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < BX_STAGES; ++i) {
+      tc::mbar_init(&full[i], 1);
+      tc::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&tfull[i], 1);
+      tc::mbar_init(&tempty[i], 4);
+    }
+    tc::mbar_init(bfull, 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc<2 * BX_ACC_COLS>(tmem_slot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tc::tma_prefetch(&tm_hi);
+      tc::tma_prefetch(&tm_lo);
+      tc::mbar_arrive_expect_tx(bfull, WIMGT_BYTES);
+      tc::bulk_load(sB, wimg + (int64_t)g * WIMGT_BYTES, WIMGT_BYTES, bfull);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int b = 0; b < G; ++b) {
+        const int n = n0 + b;
+        if (slot_row[n] < 0) continue;
+        for (int t = 0; t < BX_TILES; ++t)
+          for (int tap = 0; tap < 9; ++tap)
+            for (int half = 0; half < 2; ++half)
+              for (int part = 0; part < 2; ++part) {
+                tc::mbar_wait(&empty[stage], phase ^ 1);
+                tc::mbar_arrive_expect_tx(&full[stage], BX_A_TX);
+                tc::tma_load_4d(sA + stage * TC_A_STAGE, part ? &tm_lo : &tm_hi, 32 * half, -(tap % 3),
+                                BX_ROWS * t - tap / 3, n, &full[stage]);
+                if (++stage == BX_STAGES) { stage = 0; phase ^= 1; }
+              }
+      }
+    }
+  } else if (warp == 1) {
+    tc::mbar_wait(bfull, 0);
+    int stage = 0, tile = 0;
+    uint32_t phase = 0;
+    const uint32_t sA0 = tc::smem_u32(sA), sB0 = tc::smem_u32(sB);
+    for (int b = 0; b < G; ++b) {
+      const int n = n0 + b;
+      if (slot_row[n] < 0) continue;
+      for (int t = 0; t < BX_TILES; ++t, ++tile) {
+        const int acc = tile & 1;
+        tc::mbar_wait(&tempty[acc], ((tile >> 1) & 1) ^ 1);
+        tc::tc_fence_after();
+        const uint32_t d = tmem + acc * BX_ACC_COLS;
+        for (int tap = 0; tap < 9; ++tap)
+          for (int half = 0; half < 2; ++half)
+            for (int part = 0; part < 2; ++part) {
+              tc::mbar_wait(&full[stage], phase);
+              tc::tc_fence_after();
+              if (lane == 0) {
+                const uint32_t a = sA0 + stage * TC_A_STAGE;
+                const uint32_t bh = sB0 + ((tap * 2 + 0) * 2 + half) * BX_B_BLK;
+                const uint32_t bl = sB0 + ((tap * 2 + 1) * 2 + half) * BX_B_BLK;
+                const uint32_t dmain = d + (tap / 3) * C1, dcross = d + 3 * C1;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  const uint64_t ad = tc::sdesc_k128(a + 32 * k);
+                  if (part == 0) {
+                    tc::mma_tf32(dmain, ad, tc::sdesc_k128(bh + 32 * k), BX_IDESC, (tap % 3 | half | k) != 0);
+                    tc::mma_tf32(dcross, ad, tc::sdesc_k128(bl + 32 * k), BX_IDESC, (tap | half | k) != 0);
+                  } else {
+                    tc::mma_tf32(dcross, ad, tc::sdesc_k128(bh + 32 * k), BX_IDESC, 1);
+                  }
+                }
+                tc::mma_commit(&empty[stage]);
+              }
+              __syncwarp();
+              if (++stage == BX_STAGES) { stage = 0; phase ^= 1; }
+            }
+        if (lane == 0) tc::mma_commit(&tfull[acc]);
+        __syncwarp();
+      }
+    }
+  } else {
+    const int ew = warp & 3;
+    const int row = ew * 32 + lane;
+    int tile = 0;
+    for (int b = 0; b < G; ++b) {
+      const int n = n0 + b;
+      if (slot_row[n] < 0) continue;
+      for (int t = 0; t < BX_TILES; ++t, ++tile) {
+        const int acc = tile & 1;
+        tc::mbar_wait(&tfull[acc], (tile >> 1) & 1);
+        tc::tc_fence_after();
+        const uint32_t base = tmem + ((uint32_t)(ew * 32) << 16) + acc * BX_ACC_COLS;
+        uint32_t v0[32], v1[32];
+        float z[32];
+        tc::tmem_ld32(base, v0);
+        tc::tmem_ld32(base + C1, v1);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) z[j] = __uint_as_float(v0[j]) + __uint_as_float(v1[j]);
+        tc::tmem_ld32(base + 2 * C1, v0);
+        tc::tmem_ld32(base + 3 * C1, v1);
+        tc::tmem_ld_wait();
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&tempty[acc]);  // accumulator drained: next tile may start
+#pragma unroll
+        for (int j = 0; j < 32; ++j) z[j] = (z[j] + __uint_as_float(v0[j])) + __uint_as_float(v1[j]);
+        const int r = row / S1, x = row - r * S1, y = BX_ROWS * t + r;
+        if (row < BX_M && y < S1) {
+          const int64_t off = ((int64_t)n * S1 * S1 + y * S1 + x) * C1;
+          const float4* m4 = reinterpret_cast<const float4*>(a1h + off);
+          float4* o4 = reinterpret_cast<float4*>(dz1 + off);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 m = m4[q];
+            o4[q] = make_float4(m.x > 0.f ? z[4 * q] : 0.f, m.y > 0.f ? z[4 * q + 1] : 0.f,
+                                m.z > 0.f ? z[4 * q + 2] : 0.f, m.w > 0.f ? z[4 * q + 3] : 0.f);
+          }
+        }
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  if (warp == 1) tc::tmem_dealloc<2 * BX_ACC_COLS>(tmem);
+}
+
+// dense dz2 NHWC [N][28][28][64] as 4-D {64, 28, 28, N}; box {32, 30, 4, 1}
+int dz2_tensor_map(CUtensorMap* map, const float* dz2, int N) {
+  const cuuint64_t dims[4] = {(cuuint64_t)C2, (cuuint64_t)S2, (cuuint64_t)S2, (cuuint64_t)N};
+  const cuuint64_t strides[3] = {(cuuint64_t)C2 * 4, (cuuint64_t)S2 * C2 * 4, (cuuint64_t)S2 * S2 * C2 * 4};
+  const cuuint32_t box[4] = {32, (cuuint32_t)S1, (cuuint32_t)BX_ROWS, 1};
+  return tensor_map_4d(map, dz2, dims, strides, box);
 }
 
 int g_conv_impl = 1;  // 1 = tcgen05 (product path), 0 = FP32 CUDA-core kernels (validation)
@@ -899,7 +1140,7 @@ struct Work {
   int64_t* prefix;
   double* slot_loss;
   int32_t* slot_hit;
-  float *a1h, *a1l, *pooled, *part, *dz3, *dp, *dz1;
+  float *a1h, *a1l, *pooled, *part, *dz3, *dp, *dz1, *dz2h, *dz2l;
   uint8_t* code;
   uint8_t* wimg;  // per-group conv2 weight images (tcgen05 B operand)
 };
@@ -918,7 +1159,8 @@ inline int64_t carve(void* base, int N, int Cmax, Work* w) {
                 o_pre = take(8LL * (Cmax + 1)), o_loss = take(8LL * N), o_hit = take(4LL * N),
                 o_a1 = take(4LL * N * A1), o_a1l = take(4LL * N * A1), o_pool = take(4LL * N * FLAT), o_code = take((int64_t)N * FLAT),
                 o_part = take(4LL * KSPLIT * N * HID), o_dz3 = take(4LL * N * HID), o_dp = take(4LL * N * FLAT),
-                o_dz1 = take(4LL * N * A1), o_wimg = take((int64_t)WIMG_BYTES * (Cmax + 1));
+                o_dz1 = take(4LL * N * A1), o_wimg = take((int64_t)WIMG_BYTES * (Cmax + 1)),
+                o_dz2h = take(4LL * N * S2 * S2 * C2), o_dz2l = take(4LL * N * S2 * S2 * C2);
   if (w && base) {
     char* b = static_cast<char*>(base);
     w->slot_row = reinterpret_cast<int64_t*>(b + o_row);
@@ -930,6 +1172,8 @@ inline int64_t carve(void* base, int N, int Cmax, Work* w) {
     w->a1h = reinterpret_cast<float*>(b + o_a1);
     w->a1l = reinterpret_cast<float*>(b + o_a1l);
     w->wimg = reinterpret_cast<uint8_t*>(b + o_wimg);
+    w->dz2h = reinterpret_cast<float*>(b + o_dz2h);
+    w->dz2l = reinterpret_cast<float*>(b + o_dz2l);
     w->pooled = reinterpret_cast<float*>(b + o_pool);
     w->code = reinterpret_cast<uint8_t*>(b + o_code);
     w->part = reinterpret_cast<float*>(b + o_part);
@@ -948,6 +1192,8 @@ int set_smem_limits() {
   cudaFuncSetAttribute(conv2_bwd_w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C2W_SMEM);
   cudaFuncSetAttribute(fc1_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FC1F_SMEM);
   cudaFuncSetAttribute(conv2_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+  cudaFuncSetAttribute(conv2_bwd_x_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BX_SMEM);
+  cudaFuncSetAttribute(dz2_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DZB_SMEM);
   cudaFuncSetAttribute(conv1_bwd_w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (IMG + S1 * S1 * A1P) * 4);
   done = true;
@@ -1059,8 +1305,19 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
                                      nullptr, nullptr));
       FB_LAUNCH("fc1_bwd_kernel", s, fc1_bwd_kernel<<<dim3(Cw, KSPLIT), HID, 0, s>>>(w.pooled, w.dz3, B, w.client_nb, theta_t, dlt, ld_delta, sp,
                                                       w.dp));
-      FB_LAUNCH("conv2_bwd_x_kernel", s, conv2_bwd_x_kernel<<<N, 256, C2X_SMEM, s>>>(w.dp, w.pooled, w.code, w.a1h, w.slot_row, B, theta_t, dlt,
-                                                  ld_delta, w.dz1));
+      if (g_conv_impl == 1) {
+        FB_LAUNCH("dz2_build_kernel", s, dz2_build_kernel<<<N, 256, DZB_SMEM, s>>>(w.dp, w.pooled, w.code, w.slot_row, w.dz2h, w.dz2l));
+        FB_LAUNCH("conv2_wimgT_kernel", s, conv2_wimgT_kernel<<<Cw, 256, 0, s>>>(theta_t, dlt, ld_delta, w.client_nb, w.wimg));
+        CUtensorMap mh, ml;
+        st = dz2_tensor_map(&mh, w.dz2h, N);
+        if (!st) st = dz2_tensor_map(&ml, w.dz2l, N);
+        if (st) return st;
+        FB_LAUNCH("conv2_bwd_x_tc_kernel", s, conv2_bwd_x_tc_kernel<<<Cw, TC_THREADS, BX_SMEM, s>>>(
+            mh, ml, w.wimg, w.slot_row, B, w.a1h, w.dz1));
+      } else {
+        FB_LAUNCH("conv2_bwd_x_kernel", s, conv2_bwd_x_kernel<<<N, 256, C2X_SMEM, s>>>(w.dp, w.pooled, w.code, w.a1h, w.slot_row, B, theta_t, dlt,
+                                                    ld_delta, w.dz1));
+      }
       FB_LAUNCH("conv2_bwd_w_kernel", s, conv2_bwd_w_kernel<<<Cw, 256, C2W_SMEM, s>>>(w.dp, w.pooled, w.code, w.a1h, w.a1l, B, w.client_nb, dlt, ld_delta,
                                                    sp));
       FB_LAUNCH("conv1_bwd_w_kernel", s, conv1_bwd_w_kernel<<<Cw, C1 * 28, (IMG + S1 * S1 * A1P) * 4, s>>>(X, w.slot_row, w.dz1, B, w.client_nb, dlt,
