@@ -2,6 +2,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -62,10 +63,27 @@ LaunchScope::LaunchScope(const char* n, cudaStream_t s) : name(n), stream(s), sl
   slot = (int)g_recs.size() - 1;
 }
 
+static int debug_sync() {  // FB_DEBUG_SYNC=1: synchronise after every launch, name the failing kernel
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FB_DEBUG_SYNC");
+    v = (e && *e && *e != '0') ? 1 : 0;
+  }
+  return v;
+}
+
 LaunchScope::~LaunchScope() {
-  if (slot < 0) return;
-  std::lock_guard<std::mutex> lk(g_mu);
-  cudaEventRecord(g_recs[slot].stop, stream);
+  if (slot >= 0) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    cudaEventRecord(g_recs[slot].stop, stream);
+  }
+  if (debug_sync()) {
+    const cudaError_t e = cudaStreamSynchronize(stream);
+    if (e != cudaSuccess) {
+      fprintf(stderr, "[fb] kernel %s failed: %s\n", name, cudaGetErrorString(e));
+      fflush(stderr);
+    }
+  }
 }
 
 }  // namespace fb

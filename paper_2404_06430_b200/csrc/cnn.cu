@@ -26,6 +26,8 @@
 #include "fb_common.cuh"
 #include "tc_common.cuh"
 
+#include <cuda_fp16.h>
+
 #include <cudaTypedefs.h>
 
 namespace fb {
@@ -46,9 +48,8 @@ constexpr int64_t O_W1 = 0, O_B1 = O_W1 + C1 * C0 * 9, O_W2 = O_B1 + C1, O_B2 = 
 static_assert(D == 1626442, "CNN parameter count");
 
 constexpr int GMAX = 16;       // max samples per weight group (batch size limit)
-constexpr int KSPLIT = 14;     // fc1 split-K factor (12544 = 14 * 896)
+constexpr int KSPLIT = 28;     // fc1 split-K factor (12544 = 28 * 448)
 constexpr int KCHUNK = FLAT / KSPLIT;
-constexpr int FC1F_SMEM = GMAX * KCHUNK * 4;
 static_assert(FLAT % KSPLIT == 0, "fc1 split");
 
 struct Step {
@@ -120,8 +121,12 @@ __global__ void __launch_bounds__(256) conv1_fwd_kernel(const float* __restrict_
                                                         const int64_t* __restrict__ slot_row,
                                                         const float* __restrict__ theta,
                                                         const float* __restrict__ delta, int64_t ld, int B,
-                                                        float* __restrict__ a1h, float* __restrict__ a1l) {
+                                                        float* __restrict__ a1h, float* __restrict__ a1l,
+                                                        __half* __restrict__ a1fh, __half* __restrict__ a1fl,
+                                                        float* __restrict__ a1scale) {
   __shared__ float img[IMG];
+  __shared__ float redmax[8];
+  float amax = 0.f;
   __shared__ float w[27 * C1 + C1];  // [tap27][o] then bias
   const int n = blockIdx.x;
   const int64_t row = slot_row[n];
@@ -159,10 +164,39 @@ __global__ void __launch_bounds__(256) conv1_fwd_kernel(const float* __restrict_
     for (int q = 0; q < C1 / 4; ++q) {
       float h[4], l[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) tc::split_tf32(fmaxf(acc[4 * q + e], 0.f), h[e], l[e]);
+      for (int e = 0; e < 4; ++e) {
+        const float v = fmaxf(acc[4 * q + e], 0.f);
+        amax = fmaxf(amax, v);
+        tc::split_tf32(v, h[e], l[e]);
+      }
       dh[q] = make_float4(h[0], h[1], h[2], h[3]);
       dl[q] = make_float4(l[0], l[1], l[2], l[3]);
     }
+  }
+  if (!a1fh) return;
+  // fp16 copy for the conv2 weight gradient (tcgen05 kind::f16): scaled by a
+  // per-sample power of two so the largest value is ~2^14, split hi + lo
+  amax = warp_max(amax);
+  if ((threadIdx.x & 31) == 0) redmax[threadIdx.x >> 5] = amax;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float m = threadIdx.x < (blockDim.x >> 5) ? redmax[threadIdx.x] : 0.f;
+    m = warp_max(m);
+    if (threadIdx.x == 0) redmax[0] = m > 0.f ? exp2f(14.f - ceilf(log2f(m))) : 1.f;
+  }
+  __syncthreads();
+  const float sc = redmax[0];
+  if (threadIdx.x == 0) a1scale[n] = sc;
+  __half* fh = a1fh + (int64_t)n * A1;
+  __half* fl = a1fl + (int64_t)n * A1;
+  for (int i = threadIdx.x; i < A1 / 2; i += blockDim.x) {
+    const float2 vh = reinterpret_cast<const float2*>(outh)[i];
+    const float2 vl = reinterpret_cast<const float2*>(outl)[i];
+    const float x0 = (vh.x + vl.x) * sc, x1 = (vh.y + vl.y) * sc;
+    const __half h0 = __float2half_rn(x0), h1 = __float2half_rn(x1);
+    reinterpret_cast<__half2*>(fh)[i] = __halves2half2(h0, h1);
+    reinterpret_cast<__half2*>(fl)[i] =
+        __halves2half2(__float2half_rn(x0 - __half2float(h0)), __float2half_rn(x1 - __half2float(h1)));
   }
 }
 
@@ -247,16 +281,24 @@ __global__ void __launch_bounds__(256) conv2_fwd_pool_kernel(const float* __rest
 
 // ---------------------------------------------------------------- fc1 fwd
 // grid (groups, KSPLIT): group = G consecutive slots sharing weights (a client
-// in training, G = B; a chunk of rows at theta_t in evaluation, G = GMAX);
-// thread j = output unit; part[split][n][j]
-__global__ void __launch_bounds__(HID) fc1_fwd_kernel(const float* __restrict__ pooled,
-                                                      const int64_t* __restrict__ slot_row, int N, int G,
-                                                      const float* __restrict__ theta,
-                                                      const float* __restrict__ delta, int64_t ld,
-                                                      float* __restrict__ part) {
-  extern __shared__ float ps_flat[];  // [GMAX][KCHUNK], rows >= G zero
-  auto ps = reinterpret_cast<float(*)[KCHUNK]>(ps_flat);
-  const int g = blockIdx.x, split = blockIdx.y, j = threadIdx.x;
+// in training, G = B; a chunk of rows at theta_t in evaluation, G = GMAX).
+// HBM stream of the client's fc1 delta: one warp per weight row, each lane a
+// float4 of the 128 units (coalesced 512 B rows, 4 rows in flight per warp);
+// the group's activations for the K chunk sit in smem; the 4 warps' partial
+// sums are reduced in smem and written as part[split][n][j].
+constexpr int FC1_WARPS = 4;
+constexpr int FC1F_SMEM = (GMAX * KCHUNK + FC1_WARPS * GMAX * HID) * 4;
+
+__global__ void __launch_bounds__(FC1_WARPS * 32) fc1_fwd_kernel(const float* __restrict__ pooled,
+                                                                  const int64_t* __restrict__ slot_row, int N, int G,
+                                                                  const float* __restrict__ theta,
+                                                                  const float* __restrict__ delta, int64_t ld,
+                                                                  float* __restrict__ part) {
+  extern __shared__ float fsm[];
+  float* ps = fsm;                       // [GMAX][KCHUNK], rows >= G zero
+  float* red = fsm + GMAX * KCHUNK;      // [FC1_WARPS][GMAX][HID]
+  const int g = blockIdx.x, split = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = g * G;
   const int k0 = split * KCHUNK;
   const float* dc = delta ? delta + (int64_t)g * ld : nullptr;
@@ -266,23 +308,42 @@ __global__ void __launch_bounds__(HID) fc1_fwd_kernel(const float* __restrict__ 
   for (int i = threadIdx.x; i < GMAX * KCHUNK; i += blockDim.x) {
     const int b = i / KCHUNK, k = i - b * KCHUNK;
     const int n = n0 + b;
-    ps[b][k] = (b < G && n < N && slot_row[n] >= 0) ? pooled[(int64_t)n * FLAT + k0 + k] : 0.f;
+    ps[i] = (b < G && n < N && slot_row[n] >= 0) ? pooled[(int64_t)n * FLAT + k0 + k] : 0.f;
   }
   __syncthreads();
-  float acc[GMAX];
+  float4 acc[GMAX];
 #pragma unroll
-  for (int b = 0; b < GMAX; ++b) acc[b] = 0.f;
-  const float* th = theta + O_F1 + (int64_t)k0 * HID + j;
-  const float* dd = dc ? dc + O_F1 + (int64_t)k0 * HID + j : nullptr;
+  for (int b = 0; b < GMAX; ++b) acc[b] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const float4* th4 = reinterpret_cast<const float4*>(theta + O_F1 + (int64_t)k0 * HID) + lane;
+  const float4* dl4 = dc ? reinterpret_cast<const float4*>(dc + O_F1 + (int64_t)k0 * HID) + lane : nullptr;
 #pragma unroll 4
-  for (int k = 0; k < KCHUNK; ++k) {
-    const float w = dd ? th[(int64_t)k * HID] - dd[(int64_t)k * HID] : th[(int64_t)k * HID];
+  for (int k = warp; k < KCHUNK; k += FC1_WARPS) {
+    float4 w = __ldg(th4 + (int64_t)k * (HID / 4));
+    if (dl4) {
+      const float4 d = __ldcs(dl4 + (int64_t)k * (HID / 4));
+      w.x -= d.x; w.y -= d.y; w.z -= d.z; w.w -= d.w;
+    }
 #pragma unroll
-    for (int b = 0; b < GMAX; ++b) acc[b] = fmaf(ps[b][k], w, acc[b]);
+    for (int b = 0; b < GMAX; ++b) {
+      const float p = ps[b * KCHUNK + k];
+      acc[b].x = fmaf(p, w.x, acc[b].x);
+      acc[b].y = fmaf(p, w.y, acc[b].y);
+      acc[b].z = fmaf(p, w.z, acc[b].z);
+      acc[b].w = fmaf(p, w.w, acc[b].w);
+    }
   }
 #pragma unroll
   for (int b = 0; b < GMAX; ++b)
-    if (b < G && n0 + b < N) part[((int64_t)split * N + n0 + b) * HID + j] = acc[b];
+    reinterpret_cast<float4*>(red + (warp * GMAX + b) * HID)[lane] = acc[b];
+  __syncthreads();
+  for (int i = threadIdx.x; i < G * HID; i += blockDim.x) {
+    const int b = i / HID, j = i - b * HID;
+    if (n0 + b >= N) continue;
+    float s = 0.f;
+#pragma unroll
+    for (int w2 = 0; w2 < FC1_WARPS; ++w2) s += red[(w2 * GMAX + b) * HID + j];
+    part[((int64_t)split * N + n0 + b) * HID + j] = s;
+  }
 }
 
 // ------------------------------------------------------------------ head
@@ -380,51 +441,78 @@ __global__ void __launch_bounds__(HID) head_kernel(const float* __restrict__ par
 }
 
 // ------------------------------------------------------- fc1 bwd + update
-// grid (C, KSPLIT); tiles of 32 rows x 128 units: dp = dz3 W^T at the old W,
-// then delta += lr * (p^T dz3 - mu * delta)
-__global__ void __launch_bounds__(HID) fc1_bwd_kernel(const float* __restrict__ pooled,
-                                                      const float* __restrict__ dz3, int B,
-                                                      const int32_t* __restrict__ client_nb,
-                                                      const float* __restrict__ theta, float* __restrict__ delta,
-                                                      int64_t ld, Step st, float* __restrict__ dp) {
-  constexpr int TR = 32;
-  __shared__ float wtile[TR][HID + 1];
-  __shared__ float dz[GMAX][HID];
-  __shared__ float pv[GMAX][TR];
-  const int c = blockIdx.x, split = blockIdx.y, j = threadIdx.x;
+// grid (C, KSPLIT), 8 warps; tiles of 64 weight rows.  Per row a warp streams
+// theta_t and the client's delta (float4 per lane, coalesced), forms the
+// gradient p^T dz3 for its 4 units, and writes delta += lr*(g - mu*delta)
+// back in the same pass; the old weights go to a padded smem tile from which
+// dp = dz3 W^T (old W) is computed for the tile's rows.
+constexpr int FB_WARPS = 8, FB_ROWS = 64, FB_LDW = HID + 1;
+constexpr int FC1B_SMEM = (FB_ROWS * FB_LDW + GMAX * HID + GMAX * KCHUNK) * 4;
+
+__global__ void __launch_bounds__(FB_WARPS * 32) fc1_bwd_kernel(const float* __restrict__ pooled,
+                                                                 const float* __restrict__ dz3, int B,
+                                                                 const int32_t* __restrict__ client_nb,
+                                                                 const float* __restrict__ theta,
+                                                                 float* __restrict__ delta, int64_t ld, Step st,
+                                                                 float* __restrict__ dp) {
+  extern __shared__ float bsm[];
+  float* wt_ = bsm;                         // [FB_ROWS][FB_LDW] old weights of the tile
+  float* dz = wt_ + FB_ROWS * FB_LDW;       // [GMAX][HID]
+  float* pv = dz + GMAX * HID;              // [GMAX][KCHUNK]
+  const int c = blockIdx.x, split = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nb = client_nb[c];
   if (nb == 0) return;
-  const int n0 = c * B;
+  const int n0 = c * B, k0 = split * KCHUNK;
   float* dc = delta + (int64_t)c * ld;
-  for (int b = 0; b < nb; ++b) dz[b][j] = dz3[(int64_t)(n0 + b) * HID + j];
-  for (int k0 = split * KCHUNK; k0 < (split + 1) * KCHUNK; k0 += TR) {
-    __syncthreads();
-    for (int i = j; i < nb * TR; i += blockDim.x) {
-      const int b = i / TR, r = i - b * TR;
-      pv[b][r] = pooled[(int64_t)(n0 + b) * FLAT + k0 + r];
-    }
-    float dl[TR];
+  for (int i = threadIdx.x; i < nb * HID; i += blockDim.x) dz[i] = dz3[(int64_t)n0 * HID + i];
+  for (int i = threadIdx.x; i < nb * KCHUNK; i += blockDim.x) {
+    const int b = i / KCHUNK, k = i - b * KCHUNK;
+    pv[i] = pooled[(int64_t)(n0 + b) * FLAT + k0 + k];
+  }
+  __syncthreads();
+  float4 dzr[GMAX];  // this lane's 4 units of every sample's dz3
 #pragma unroll
-    for (int r = 0; r < TR; ++r) {
-      const int64_t idx = O_F1 + (int64_t)(k0 + r) * HID + j;
-      dl[r] = dc[idx];
-      wtile[r][j] = theta[idx] - dl[r];
+  for (int b = 0; b < GMAX; ++b)
+    dzr[b] = b < nb ? reinterpret_cast<const float4*>(dz + b * HID)[lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+  const float lr = st.lr, mu = st.mu;
+  for (int t0 = 0; t0 < KCHUNK; t0 += FB_ROWS) {
+#pragma unroll 2
+    for (int r = warp; r < FB_ROWS; r += FB_WARPS) {
+      const int k = t0 + r;
+      const int64_t off = O_F1 + (int64_t)(k0 + k) * HID;
+      const float4 th = __ldg(reinterpret_cast<const float4*>(theta + off) + lane);
+      float4* dptr = reinterpret_cast<float4*>(dc + off) + lane;
+      const float4 d = *dptr;
+      float* wrow = wt_ + r * FB_LDW + 4 * lane;
+      wrow[0] = th.x - d.x; wrow[1] = th.y - d.y; wrow[2] = th.z - d.z; wrow[3] = th.w - d.w;
+      float4 gw = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int b = 0; b < GMAX; ++b) {
+        const float p = b < nb ? pv[b * KCHUNK + k] : 0.f;
+        gw.x = fmaf(p, dzr[b].x, gw.x);
+        gw.y = fmaf(p, dzr[b].y, gw.y);
+        gw.z = fmaf(p, dzr[b].z, gw.z);
+        gw.w = fmaf(p, dzr[b].w, gw.w);
+      }
+      *dptr = make_float4(d.x + lr * (gw.x - mu * d.x), d.y + lr * (gw.y - mu * d.y),
+                          d.z + lr * (gw.z - mu * d.z), d.w + lr * (gw.w - mu * d.w));
     }
     __syncthreads();
-    // dp[b][k0+r] = sum_j dz[b][j] * w[r][j]: thread handles (b, r) pairs
-    for (int t = j; t < nb * TR; t += blockDim.x) {
-      const int b = t / TR, r = t - b * TR;
-      float s = 0.f;
+    // dp[b][k] = sum_j dz[b][j] * w_old[k][j] for the tile's rows
+    for (int t = threadIdx.x; t < nb * FB_ROWS; t += blockDim.x) {
+      const int b = t / FB_ROWS, r = t - b * FB_ROWS;
+      const float* wr = wt_ + r * FB_LDW;
+      const float* zb = dz + b * HID;
+      float s0 = 0.f, s1 = 0.f;
 #pragma unroll 8
-      for (int h = 0; h < HID; ++h) s = fmaf(dz[b][h], wtile[r][h], s);
-      dp[(int64_t)(n0 + b) * FLAT + k0 + r] = s;
+      for (int j = 0; j < HID; j += 2) {
+        s0 = fmaf(zb[j], wr[j], s0);
+        s1 = fmaf(zb[j + 1], wr[j + 1], s1);
+      }
+      dp[(int64_t)(n0 + b) * FLAT + k0 + t0 + r] = s0 + s1;
     }
-#pragma unroll
-    for (int r = 0; r < TR; ++r) {
-      float gw = 0.f;
-      for (int b = 0; b < nb; ++b) gw = fmaf(pv[b][r], dz[b][j], gw);
-      dc[O_F1 + (int64_t)(k0 + r) * HID + j] = dl[r] + st.lr * (gw - st.mu * dl[r]);
-    }
+    __syncthreads();
   }
 }
 
@@ -562,45 +650,72 @@ __global__ void __launch_bounds__(256) conv2_bwd_w_kernel(const float* __restric
 }
 
 // ------------------------------------------- conv1 backward (weights) + update
-// one CTA per client; thread t < 864 owns dW1[o][ci][ky][kx], t in [864, 896) a bias
-__global__ void __launch_bounds__(C1 * 28) conv1_bwd_w_kernel(const float* __restrict__ X,
-                                                             const int64_t* __restrict__ slot_row,
-                                                             const float* __restrict__ dz1, int B,
-                                                             const int32_t* __restrict__ client_nb,
-                                                             float* __restrict__ delta, int64_t ld, Step st) {
-  extern __shared__ float sm[];
-  float* img = sm;                    // [3][32][32]
-  float* dz = img + IMG;              // [900][33]
+// one CTA per client, 12 warps: warp = (8 output channels, 1 input channel) tile
+// holding the 8 x 9 taps of dW1 in registers; lanes stride over the 900
+// positions of each of the client's samples (dz1 rows read straight from HBM,
+// the 3x32x32 input from smem); lane partials are warp-reduced at the end.
+constexpr int C1B_WARPS = 12;
+
+__global__ void __launch_bounds__(C1B_WARPS * 32) conv1_bwd_w_kernel(const float* __restrict__ X,
+                                                                    const int64_t* __restrict__ slot_row,
+                                                                    const float* __restrict__ dz1, int B,
+                                                                    const int32_t* __restrict__ client_nb,
+                                                                    float* __restrict__ delta, int64_t ld, Step st) {
+  __shared__ float img[IMG];
   const int c = blockIdx.x;
   const int nb = client_nb[c];
   if (nb == 0) return;
-  const int t = threadIdx.x;
-  const bool is_w = t < C1 * 27;
-  const int o = is_w ? t / 27 : t - C1 * 27;
-  const int r = is_w ? t - o * 27 : 0, ci = r / 9, ky = (r % 9) / 3, kx = r % 3;
-  float acc = 0.f;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int og = warp & 3, ci = warp >> 2;  // channels 8*og .. 8*og+7, input channel ci
+  float acc[8][9], accb[8];
+#pragma unroll
+  for (int o = 0; o < 8; ++o) {
+    accb[o] = 0.f;
+#pragma unroll
+    for (int t = 0; t < 9; ++t) acc[o][t] = 0.f;
+  }
   for (int b = 0; b < nb; ++b) {
     const int64_t n = (int64_t)c * B + b;
     const int64_t row = slot_row[n];
     __syncthreads();
-    for (int i = t; i < IMG; i += blockDim.x) img[i] = X[row * IMG + i];
-    for (int i = t; i < A1; i += blockDim.x) dz[(i >> 5) * A1P + (i & 31)] = dz1[n * A1 + i];
+    for (int i = threadIdx.x; i < IMG; i += blockDim.x) img[i] = X[row * IMG + i];
     __syncthreads();
-    if (is_w) {
-      const float* im = img + ci * S0 * S0 + ky * S0 + kx;
-      for (int y = 0; y < S1; ++y)
-        for (int x = 0; x < S1; ++x) acc = fmaf(dz[(y * S1 + x) * A1P + o], im[y * S0 + x], acc);
-    } else if (o < C1) {
-      for (int p = 0; p < S1 * S1; ++p) acc += dz[p * A1P + o];
+    const float* dzn = dz1 + n * A1 + og * 8;
+    const float* im = img + ci * S0 * S0;
+    for (int p = lane; p < S1 * S1; p += 32) {
+      const int y = p / S1, x = p - y * S1;
+      const float4 d0 = __ldg(reinterpret_cast<const float4*>(dzn + (int64_t)p * C1));
+      const float4 d1 = __ldg(reinterpret_cast<const float4*>(dzn + (int64_t)p * C1) + 1);
+      const float dv[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+      float pv[9];
+#pragma unroll
+      for (int t = 0; t < 9; ++t) pv[t] = im[(y + t / 3) * S0 + x + t % 3];
+#pragma unroll
+      for (int o = 0; o < 8; ++o) {
+        accb[o] += dv[o];
+#pragma unroll
+        for (int t = 0; t < 9; ++t) acc[o][t] = fmaf(dv[o], pv[t], acc[o][t]);
+      }
     }
   }
   float* dc = delta + (int64_t)c * ld;
-  if (is_w) {
-    float& dl = dc[O_W1 + t];
-    dl += st.lr * (acc - st.mu * dl);
-  } else if (o < C1) {
-    float& dl = dc[O_B1 + o];
-    dl += st.lr * (acc - st.mu * dl);
+#pragma unroll
+  for (int o = 0; o < 8; ++o) {
+#pragma unroll
+    for (int t = 0; t < 9; ++t) {
+      const float g = warp_sum(acc[o][t]);
+      if (lane == 0) {
+        float& dl = dc[O_W1 + (int64_t)(og * 8 + o) * (C0 * 9) + ci * 9 + t];
+        dl += st.lr * (g - st.mu * dl);
+      }
+    }
+    if (ci == 0) {
+      const float gb = warp_sum(accb[o]);
+      if (lane == 0) {
+        float& dl = dc[O_B1 + og * 8 + o];
+        dl += st.lr * (gb - st.mu * dl);
+      }
+    }
   }
 }
 
@@ -942,7 +1057,9 @@ constexpr int DZB_SMEM = FLAT * 5;
 __global__ void __launch_bounds__(256) dz2_build_kernel(const float* __restrict__ dp, const float* __restrict__ pooled,
                                                         const uint8_t* __restrict__ code,
                                                         const int64_t* __restrict__ slot_row,
-                                                        float* __restrict__ dzh, float* __restrict__ dzl) {
+                                                        float* __restrict__ dzh, float* __restrict__ dzl,
+                                                        __half* __restrict__ dzfh, __half* __restrict__ dzfl,
+                                                        float* __restrict__ dzscale, float* __restrict__ db2) {
   extern __shared__ float g[];  // [FLAT] values, then [FLAT] codes
   uint8_t* cd = reinterpret_cast<uint8_t*>(g + FLAT);
   const int n = blockIdx.x;
@@ -969,6 +1086,44 @@ __global__ void __launch_bounds__(256) dz2_build_kernel(const float* __restrict_
     }
     reinterpret_cast<float4*>(oh)[t] = make_float4(h[0], h[1], h[2], h[3]);
     reinterpret_cast<float4*>(ol)[t] = make_float4(l[0], l[1], l[2], l[3]);
+  }
+  // fp16 NHWC copy for the weight gradient, scaled by a per-sample power of two
+  __shared__ float redmax[8];
+  float m = 0.f;
+  for (int i = threadIdx.x; i < FLAT; i += blockDim.x) m = fmaxf(m, fabsf(g[i]));
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0) redmax[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float mm = threadIdx.x < (blockDim.x >> 5) ? redmax[threadIdx.x] : 0.f;
+    mm = warp_max(mm);
+    if (threadIdx.x == 0) redmax[0] = mm > 0.f ? exp2f(14.f - ceilf(log2f(mm))) : 1.f;
+  }
+  __syncthreads();
+  const float sc = redmax[0];
+  if (threadIdx.x == 0) dzscale[n] = sc;
+  __half* fh = dzfh + (int64_t)n * S2 * S2 * C2;
+  __half* fl = dzfl + (int64_t)n * S2 * S2 * C2;
+  for (int t = threadIdx.x; t < S2 * S2 * (C2 / 2); t += blockDim.x) {
+    const int pos = t >> 5, o0 = (t & 31) * 2;
+    const int y = pos / S2, x = pos - y * S2;
+    const int pp = (y >> 1) * SP + (x >> 1), sub = ((y & 1) << 1) | (x & 1);
+    float v[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int idx = (o0 + e) * NPOOL + pp;
+      v[e] = (cd[idx] == sub ? g[idx] : 0.f) * sc;
+    }
+    const __half h0 = __float2half_rn(v[0]), h1 = __float2half_rn(v[1]);
+    reinterpret_cast<__half2*>(fh)[t] = __halves2half2(h0, h1);
+    reinterpret_cast<__half2*>(fl)[t] =
+        __halves2half2(__float2half_rn(v[0] - __half2float(h0)), __float2half_rn(v[1] - __half2float(h1)));
+  }
+  // conv2 bias gradient of this sample: sum over positions of dz2 = sum of g
+  if (threadIdx.x < C2) {
+    float sb = 0.f;
+    for (int pp = 0; pp < NPOOL; ++pp) sb += g[threadIdx.x * NPOOL + pp];
+    db2[(int64_t)n * C2 + threadIdx.x] = sb;
   }
 }
 
@@ -1132,6 +1287,215 @@ int dz2_tensor_map(CUtensorMap* map, const float* dz2, int N) {
 
 int g_conv_impl = 1;  // 1 = tcgen05 (product path), 0 = FP32 CUDA-core kernels (validation)
 
+
+// ------------------------------------------------ conv2 backward-weights (tcgen05)
+// dW[o, ci, ky, kx] = sum over the client's samples and conv2-output positions
+// p of dz2[p, o] * a1[p + (ky, kx), ci]: a GEMM with K = positions.  Both
+// operands are NHWC (positions along rows) -> MN-major, which the tensor core
+// supports for 16-bit inputs: kind::f16 with fp32 accumulation, each fp32
+// value split into scaled fp16 hi + lo (per-sample power-of-two scale keeps
+// values normal; hi*hi + hi*lo + lo*hi ~ 2^-22 relative, as 3xTF32).
+// Positions run in the 30-wide space of a1 (dz2 rows are zero-filled by the
+// TMA in columns 28, 29), where the tap shift is a whole number of rows: one
+// staged a1 tile {32 ci, 30 x, 10 y} serves all nine taps -- the M = 128
+// operand for row ky is four 32-channel blocks at LBO = one 64-byte row
+// (kx = 0..3, the kx = 3 block discarded) starting at row ky*30.  A K block
+// = 8 output rows = 240 positions = 15 MMAs of K = 16; each K block starts
+// fresh TMEM accumulators per ky (hi*hi and cross terms separately), drained
+// by eight epilogue warps into fp32 registers with the per-sample unscale.
+constexpr int BW_ROWS = 8;                        // output rows per K block
+constexpr int BW_NKB = (S2 + BW_ROWS - 1) / BW_ROWS;  // 4 K blocks per sample
+constexpr int BW_KPOS = BW_ROWS * S1;             // 240 positions
+constexpr int BW_A_ROWS = 304;                    // a1 tile rows (300 loaded + 4 zero)
+constexpr int BW_A_BYTES = BW_A_ROWS * 64;        // 19456
+constexpr int BW_A_TX = (BW_ROWS + 2) * S1 * 64;  // 19200
+constexpr int BW_B_BYTES = BW_KPOS * 128;         // 30720
+constexpr int BW_STAGE = 2 * BW_A_BYTES + 2 * BW_B_BYTES;  // 100352
+constexpr int BW_STAGES = 2;
+constexpr int BW_EPI_WARPS = 8;
+constexpr int BW_THREADS = (2 + BW_EPI_WARPS) * 32;
+constexpr int BW_SMEM = 1024 + BW_STAGES * BW_STAGE + 256;
+constexpr uint32_t BW_IDESC = tc::idesc_f16_mn(128, C2);
+
+__global__ void __launch_bounds__(BW_THREADS, 1) conv2_bwd_w_tc_kernel(
+    const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
+    const __grid_constant__ CUtensorMap td_hi, const __grid_constant__ CUtensorMap td_lo, int B,
+    const int32_t* __restrict__ client_nb, const float* __restrict__ a1scale, const float* __restrict__ dzscale,
+    const float* __restrict__ db2, float* __restrict__ delta, int64_t ld, Step st) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + BW_STAGES * BW_STAGE);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + BW_STAGES;
+  uint64_t* tfull = empty + BW_STAGES;  // [3] one per ky
+  uint64_t* tempty = tfull + 3;         // [3]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 3);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x;
+  const int nb = client_nb[c];
+  if (nb == 0) return;
+  const int nblocks = nb * BW_NKB;
+  for (int s = 0; s < BW_STAGES; ++s)  // a1 rows 300..303 are read against zero dz2 rows: keep them finite
+    for (int i = threadIdx.x; i < (BW_A_BYTES - BW_A_TX) / 4; i += blockDim.x) {
+      reinterpret_cast<float*>(sm + s * BW_STAGE + BW_A_TX)[i] = 0.f;
+      reinterpret_cast<float*>(sm + s * BW_STAGE + BW_A_BYTES + BW_A_TX)[i] = 0.f;
+    }
+  tc::fence_proxy_async();
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < BW_STAGES; ++i) {
+      tc::mbar_init(&full[i], 1);
+      tc::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 3; ++i) {
+      tc::mbar_init(&tfull[i], 1);
+      tc::mbar_init(&tempty[i], BW_EPI_WARPS);
+    }
+    tc::fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc<512>(tmem_slot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tc::tma_prefetch(&ta_hi);
+      tc::tma_prefetch(&ta_lo);
+      tc::tma_prefetch(&td_hi);
+      tc::tma_prefetch(&td_lo);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int blk = 0; blk < nblocks; ++blk) {
+        const int n = c * B + blk / BW_NKB, y0 = BW_ROWS * (blk % BW_NKB);
+        tc::mbar_wait(&empty[stage], phase ^ 1);
+        tc::mbar_arrive_expect_tx(&full[stage], 2 * BW_A_TX + 2 * BW_B_BYTES);
+        uint8_t* st_ = sm + stage * BW_STAGE;
+        tc::tma_load_4d(st_, &ta_hi, 0, 0, y0, n, &full[stage]);
+        tc::tma_load_4d(st_ + BW_A_BYTES, &ta_lo, 0, 0, y0, n, &full[stage]);
+        tc::tma_load_4d(st_ + 2 * BW_A_BYTES, &td_hi, 0, 0, y0, n, &full[stage]);
+        tc::tma_load_4d(st_ + 2 * BW_A_BYTES + BW_B_BYTES, &td_lo, 0, 0, y0, n, &full[stage]);
+        if (++stage == BW_STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    int stage = 0;
+    uint32_t phase = 0;
+    const uint32_t s0 = tc::smem_u32(sm);
+    for (int blk = 0; blk < nblocks; ++blk) {
+      tc::mbar_wait(&full[stage], phase);
+      tc::tc_fence_after();
+      const uint32_t ah = s0 + stage * BW_STAGE, al = ah + BW_A_BYTES;
+      const uint32_t bh = ah + 2 * BW_A_BYTES, bl = bh + BW_B_BYTES;
+      for (int ky = 0; ky < 3; ++ky) {
+        tc::mbar_wait(&tempty[ky], (blk & 1) ^ 1);  // previous block's ky accumulators drained
+        tc::tc_fence_after();
+        if (lane == 0) {
+          const uint32_t dm = tmem + ky * 2 * C2, dx = dm + C2;
+          for (int ks = 0; ks < BW_KPOS / 16; ++ks) {
+            const uint32_t arow = ky * S1 + ks * 16;
+            const uint64_t adh = tc::sdesc(ah + arow * 64, 64, 512, 4);
+            const uint64_t adl = tc::sdesc(al + arow * 64, 64, 512, 4);
+            const uint64_t bdh = tc::sdesc(bh + ks * 16 * 128, 128, 1024, 2);
+            const uint64_t bdl = tc::sdesc(bl + ks * 16 * 128, 128, 1024, 2);
+            tc::mma_f16(dm, adh, bdh, BW_IDESC, ks != 0);
+            tc::mma_f16(dx, adh, bdl, BW_IDESC, ks != 0);
+            tc::mma_f16(dx, adl, bdh, BW_IDESC, 1);
+          }
+          tc::mma_commit(&tfull[ky]);
+          if (ky == 2) tc::mma_commit(&empty[stage]);
+        }
+        __syncwarp();
+      }
+      if (++stage == BW_STAGES) { stage = 0; phase ^= 1; }
+    }
+  } else {
+    const int ew = warp & 3;                 // TMEM lane quarter
+    const int hc = (warp - 2) >> 2;          // column half (o 0-31 / 32-63)
+    const int row = ew * 32 + lane;          // M row = kx * 32 + ci
+    float run[3][32];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 32; ++j) run[i][j] = 0.f;
+    for (int blk = 0; blk < nblocks; ++blk) {
+      const int n = c * B + blk / BW_NKB;
+      const float inv = 1.f / (a1scale[n] * dzscale[n]);  // exact: powers of two
+#pragma unroll
+      for (int ky = 0; ky < 3; ++ky) {
+        tc::mbar_wait(&tfull[ky], blk & 1);
+        tc::tc_fence_after();
+        uint32_t vm[32], vx[32];
+        const uint32_t base = tmem + ((uint32_t)(ew * 32) << 16) + ky * 2 * C2 + hc * 32;
+        tc::tmem_ld32(base, vm);
+        tc::tmem_ld32(base + C2, vx);
+        tc::tmem_ld_wait();
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&tempty[ky]);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) run[ky][j] += (__uint_as_float(vm[j]) + __uint_as_float(vx[j])) * inv;
+      }
+    }
+    const int kx = row >> 5, ci = row & 31;
+    float* dc = delta + (int64_t)c * ld;
+    if (kx < 3) {
+#pragma unroll
+      for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int o = hc * 32 + j;
+          float& dl = dc[O_W2 + (int64_t)o * (C1 * 9) + ci * 9 + ky * 3 + kx];
+          dl += st.lr * (run[ky][j] - st.mu * dl);
+        }
+    }
+    const int e = threadIdx.x - 64;
+    if (e < C2) {  // conv2 bias: sum of the client's per-sample partials
+      float gb = 0.f;
+      for (int b = 0; b < nb; ++b) gb += db2[(int64_t)(c * B + b) * C2 + e];
+      float& dl = dc[O_B2 + e];
+      dl += st.lr * (gb - st.mu * dl);
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  if (warp == 1) tc::tmem_dealloc<512>(tmem);
+}
+
+int tensor_map_4d_f16(CUtensorMap* map, const __half* base, const cuuint64_t dims[4], const cuuint64_t strides[3],
+                      const cuuint32_t box[4], CUtensorMapSwizzle swz) {
+  auto fn = encode_fn();
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return FB_ERR_CUDA;
+  }
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<__half*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (fp16) failed (%d)", (int)r);
+    return FB_ERR_CUDA;
+  }
+  return FB_OK;
+}
+// fp16 a1 NHWC {32, 30, 30, N}, box {32, 30, 10, 1}, 64-byte swizzle
+int a1f_tensor_map(CUtensorMap* map, const __half* a1, int N) {
+  const cuuint64_t dims[4] = {(cuuint64_t)C1, (cuuint64_t)S1, (cuuint64_t)S1, (cuuint64_t)N};
+  const cuuint64_t strides[3] = {(cuuint64_t)C1 * 2, (cuuint64_t)S1 * C1 * 2, (cuuint64_t)S1 * S1 * C1 * 2};
+  const cuuint32_t box[4] = {(cuuint32_t)C1, (cuuint32_t)S1, BW_ROWS + 2, 1};
+  return tensor_map_4d_f16(map, a1, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B);
+}
+// fp16 dz2 NHWC {64, 28, 28, N}, box {64, 30, 8, 1}, 128-byte swizzle
+int dzf_tensor_map(CUtensorMap* map, const __half* dz, int N) {
+  const cuuint64_t dims[4] = {(cuuint64_t)C2, (cuuint64_t)S2, (cuuint64_t)S2, (cuuint64_t)N};
+  const cuuint64_t strides[3] = {(cuuint64_t)C2 * 2, (cuuint64_t)S2 * C2 * 2, (cuuint64_t)S2 * S2 * C2 * 2};
+  const cuuint32_t box[4] = {(cuuint32_t)C2, (cuuint32_t)S1, BW_ROWS, 1};
+  return tensor_map_4d_f16(map, dz, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
 // ------------------------------------------------------------- workspace
 struct Work {
   int64_t* slot_row;
@@ -1140,7 +1504,8 @@ struct Work {
   int64_t* prefix;
   double* slot_loss;
   int32_t* slot_hit;
-  float *a1h, *a1l, *pooled, *part, *dz3, *dp, *dz1, *dz2h, *dz2l;
+  float *a1h, *a1l, *pooled, *part, *dz3, *dp, *dz1, *dz2h, *dz2l, *db2, *a1scale, *dzscale;
+  __half *a1fh, *a1fl, *dzfh, *dzfl;
   uint8_t* code;
   uint8_t* wimg;  // per-group conv2 weight images (tcgen05 B operand)
 };
@@ -1160,7 +1525,10 @@ inline int64_t carve(void* base, int N, int Cmax, Work* w) {
                 o_a1 = take(4LL * N * A1), o_a1l = take(4LL * N * A1), o_pool = take(4LL * N * FLAT), o_code = take((int64_t)N * FLAT),
                 o_part = take(4LL * KSPLIT * N * HID), o_dz3 = take(4LL * N * HID), o_dp = take(4LL * N * FLAT),
                 o_dz1 = take(4LL * N * A1), o_wimg = take((int64_t)WIMG_BYTES * (Cmax + 1)),
-                o_dz2h = take(4LL * N * S2 * S2 * C2), o_dz2l = take(4LL * N * S2 * S2 * C2);
+                o_dz2h = take(4LL * N * S2 * S2 * C2), o_dz2l = take(4LL * N * S2 * S2 * C2),
+                o_db2 = take(4LL * N * C2), o_a1fh = take(2LL * N * A1), o_a1fl = take(2LL * N * A1),
+                o_dzfh = take(2LL * N * S2 * S2 * C2), o_dzfl = take(2LL * N * S2 * S2 * C2),
+                o_a1s = take(4LL * N), o_dzs = take(4LL * N);
   if (w && base) {
     char* b = static_cast<char*>(base);
     w->slot_row = reinterpret_cast<int64_t*>(b + o_row);
@@ -1174,6 +1542,13 @@ inline int64_t carve(void* base, int N, int Cmax, Work* w) {
     w->wimg = reinterpret_cast<uint8_t*>(b + o_wimg);
     w->dz2h = reinterpret_cast<float*>(b + o_dz2h);
     w->dz2l = reinterpret_cast<float*>(b + o_dz2l);
+    w->db2 = reinterpret_cast<float*>(b + o_db2);
+    w->a1fh = reinterpret_cast<__half*>(b + o_a1fh);
+    w->a1fl = reinterpret_cast<__half*>(b + o_a1fl);
+    w->dzfh = reinterpret_cast<__half*>(b + o_dzfh);
+    w->dzfl = reinterpret_cast<__half*>(b + o_dzfl);
+    w->a1scale = reinterpret_cast<float*>(b + o_a1s);
+    w->dzscale = reinterpret_cast<float*>(b + o_dzs);
     w->pooled = reinterpret_cast<float*>(b + o_pool);
     w->code = reinterpret_cast<uint8_t*>(b + o_code);
     w->part = reinterpret_cast<float*>(b + o_part);
@@ -1191,11 +1566,11 @@ int set_smem_limits() {
   cudaFuncSetAttribute(conv2_bwd_x_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C2X_SMEM);
   cudaFuncSetAttribute(conv2_bwd_w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C2W_SMEM);
   cudaFuncSetAttribute(fc1_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FC1F_SMEM);
+  cudaFuncSetAttribute(fc1_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FC1B_SMEM);
   cudaFuncSetAttribute(conv2_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
   cudaFuncSetAttribute(conv2_bwd_x_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BX_SMEM);
   cudaFuncSetAttribute(dz2_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DZB_SMEM);
-  cudaFuncSetAttribute(conv1_bwd_w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (IMG + S1 * S1 * A1P) * 4);
+  cudaFuncSetAttribute(conv2_bwd_w_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BW_SMEM);
   done = true;
   return launch_status("cnn: cudaFuncSetAttribute");
 }
@@ -1203,7 +1578,8 @@ int set_smem_limits() {
 // forward of N slots (shared weights when delta == nullptr) up to the head
 int forward(const float* X, const float* theta, const float* delta, int64_t ld, int B, int N, int G,
             const Work& w, cudaStream_t s, const int32_t* client_nb) {
-  FB_LAUNCH("conv1_fwd_kernel", s, conv1_fwd_kernel<<<N, 256, 0, s>>>(X, w.slot_row, theta, delta, ld, B, w.a1h, w.a1l));
+  FB_LAUNCH("conv1_fwd_kernel", s, conv1_fwd_kernel<<<N, 256, 0, s>>>(X, w.slot_row, theta, delta, ld, B, w.a1h, w.a1l,
+                                                               delta ? w.a1fh : nullptr, w.a1fl, w.a1scale));
   if (g_conv_impl == 1) {
     // weight groups: one per client in training (G = B), one shared image at theta_t in evaluation
     const int groups = delta ? (N + B - 1) / B : 1;
@@ -1218,7 +1594,7 @@ int forward(const float* X, const float* theta, const float* delta, int64_t ld, 
   } else {
     FB_LAUNCH("conv2_fwd_pool_kernel", s, conv2_fwd_pool_kernel<<<N, 256, C2F_SMEM, s>>>(w.a1h, w.a1l, w.slot_row, theta, delta, ld, B, w.pooled, w.code));
   }
-  FB_LAUNCH("fc1_fwd_kernel", s, fc1_fwd_kernel<<<dim3((N + G - 1) / G, KSPLIT), HID, FC1F_SMEM, s>>>(w.pooled, w.slot_row, N, G, theta, delta, ld,
+  FB_LAUNCH("fc1_fwd_kernel", s, fc1_fwd_kernel<<<dim3((N + G - 1) / G, KSPLIT), FC1_WARPS * 32, FC1F_SMEM, s>>>(w.pooled, w.slot_row, N, G, theta, delta, ld,
                                                                w.part));
   return launch_status("cnn forward");
 }
@@ -1303,10 +1679,10 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
       if (st) return st;
       FB_LAUNCH("head_kernel", s, head_kernel<<<Cw, HID, 0, s>>>(w.part, w.slot_row, N, B, y, theta_t, dlt, ld_delta, w.client_nb, sp, w.dz3,
                                      nullptr, nullptr));
-      FB_LAUNCH("fc1_bwd_kernel", s, fc1_bwd_kernel<<<dim3(Cw, KSPLIT), HID, 0, s>>>(w.pooled, w.dz3, B, w.client_nb, theta_t, dlt, ld_delta, sp,
+      FB_LAUNCH("fc1_bwd_kernel", s, fc1_bwd_kernel<<<dim3(Cw, KSPLIT), FB_WARPS * 32, FC1B_SMEM, s>>>(w.pooled, w.dz3, B, w.client_nb, theta_t, dlt, ld_delta, sp,
                                                       w.dp));
       if (g_conv_impl == 1) {
-        FB_LAUNCH("dz2_build_kernel", s, dz2_build_kernel<<<N, 256, DZB_SMEM, s>>>(w.dp, w.pooled, w.code, w.slot_row, w.dz2h, w.dz2l));
+        FB_LAUNCH("dz2_build_kernel", s, dz2_build_kernel<<<N, 256, DZB_SMEM, s>>>(w.dp, w.pooled, w.code, w.slot_row, w.dz2h, w.dz2l, w.dzfh, w.dzfl, w.dzscale, w.db2));
         FB_LAUNCH("conv2_wimgT_kernel", s, conv2_wimgT_kernel<<<Cw, 256, 0, s>>>(theta_t, dlt, ld_delta, w.client_nb, w.wimg));
         CUtensorMap mh, ml;
         st = dz2_tensor_map(&mh, w.dz2h, N);
@@ -1318,9 +1694,20 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
         FB_LAUNCH("conv2_bwd_x_kernel", s, conv2_bwd_x_kernel<<<N, 256, C2X_SMEM, s>>>(w.dp, w.pooled, w.code, w.a1h, w.slot_row, B, theta_t, dlt,
                                                     ld_delta, w.dz1));
       }
-      FB_LAUNCH("conv2_bwd_w_kernel", s, conv2_bwd_w_kernel<<<Cw, 256, C2W_SMEM, s>>>(w.dp, w.pooled, w.code, w.a1h, w.a1l, B, w.client_nb, dlt, ld_delta,
-                                                   sp));
-      FB_LAUNCH("conv1_bwd_w_kernel", s, conv1_bwd_w_kernel<<<Cw, C1 * 28, (IMG + S1 * S1 * A1P) * 4, s>>>(X, w.slot_row, w.dz1, B, w.client_nb, dlt,
+      if (g_conv_impl == 1) {
+        CUtensorMap ah, al, dh, dl;
+        st = a1f_tensor_map(&ah, w.a1fh, N);
+        if (!st) st = a1f_tensor_map(&al, w.a1fl, N);
+        if (!st) st = dzf_tensor_map(&dh, w.dzfh, N);
+        if (!st) st = dzf_tensor_map(&dl, w.dzfl, N);
+        if (st) return st;
+        FB_LAUNCH("conv2_bwd_w_tc_kernel", s, conv2_bwd_w_tc_kernel<<<Cw, BW_THREADS, BW_SMEM, s>>>(
+            ah, al, dh, dl, B, w.client_nb, w.a1scale, w.dzscale, w.db2, dlt, ld_delta, sp));
+      } else {
+        FB_LAUNCH("conv2_bwd_w_kernel", s, conv2_bwd_w_kernel<<<Cw, 256, C2W_SMEM, s>>>(w.dp, w.pooled, w.code, w.a1h, w.a1l, B, w.client_nb, dlt, ld_delta,
+                                                     sp));
+      }
+      FB_LAUNCH("conv1_bwd_w_kernel", s, conv1_bwd_w_kernel<<<Cw, C1B_WARPS * 32, 0, s>>>(X, w.slot_row, w.dz1, B, w.client_nb, dlt,
                                                                        ld_delta, sp));
       st = fb::launch_status("local_sgd_cnn step");
       if (st) return st;

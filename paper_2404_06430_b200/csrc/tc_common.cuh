@@ -52,6 +52,14 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
 // 1-D bulk copy global -> shared (bytes multiple of 16, 16-byte aligned)
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -110,6 +118,42 @@ __device__ __forceinline__ uint64_t sdesc_k128(uint32_t smem_addr) {
          | ((uint64_t)(1024 >> 4) << 32)          // SBO
          | ((uint64_t)1 << 46)                    // descriptor version (sm_100)
          | ((uint64_t)2 << 61);                   // SWIZZLE_128B
+}
+// MN-major, SWIZZLE_128B smem descriptor: 128-byte rows hold 32 consecutive
+// M (or N) elements, 8-row K atoms at SBO = 1024 B, M/N blocks of 32 at `lbo`
+// bytes.  `base_off` = the start address's row phase within the 1024 B
+// swizzle atom when the start is not atom-aligned (0 when it is).
+__device__ __forceinline__ uint64_t sdesc_mn128(uint32_t smem_addr, uint32_t lbo, uint32_t base_off) {
+  return (uint64_t)((smem_addr >> 4) & 0x3FFFu)
+         | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16)
+         | ((uint64_t)(1024 >> 4) << 32)
+         | ((uint64_t)1 << 46)
+         | ((uint64_t)(base_off & 7u) << 49)
+         | ((uint64_t)2 << 61);
+}
+// generic smem descriptor: layout 2 = SWIZZLE_128B, 4 = SWIZZLE_64B
+__device__ __forceinline__ uint64_t sdesc(uint32_t smem_addr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+  return (uint64_t)((smem_addr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | ((uint64_t)1 << 46) | ((uint64_t)layout << 61);
+}
+// kind::f16 (fp16 inputs, fp32 accumulate), both operands MN-major.  (The
+// tensor core accepts MN-major operands for 16-bit kinds; kind::tf32 with an
+// MN-major operand produced no output on sm_100a in our tests.)
+__host__ __device__ constexpr uint32_t idesc_f16_mn(int M, int N) {
+  return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24) | (1u << 15) | (1u << 16);
+}
+__device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// kind::tf32 instruction descriptor with both operands MN-major
+__host__ __device__ constexpr uint32_t idesc_tf32_mn(int M, int N) {
+  return idesc_tf32(M, N) | (1u << 15) | (1u << 16);
 }
 __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                          uint32_t accumulate) {
