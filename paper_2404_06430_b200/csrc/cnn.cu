@@ -280,70 +280,62 @@ __global__ void __launch_bounds__(256) conv2_fwd_pool_kernel(const float* __rest
 }
 
 // ---------------------------------------------------------------- fc1 fwd
-// grid (groups, KSPLIT): group = G consecutive slots sharing weights (a client
-// in training, G = B; a chunk of rows at theta_t in evaluation, G = GMAX).
-// HBM stream of the client's fc1 delta: one warp per weight row, each lane a
-// float4 of the 128 units (coalesced 512 B rows, 4 rows in flight per warp);
-// the group's activations for the K chunk sit in smem; the 4 warps' partial
-// sums are reduced in smem and written as part[split][n][j].
-constexpr int FC1_WARPS = 4;
-constexpr int FC1F_SMEM = (GMAX * KCHUNK + FC1_WARPS * GMAX * HID) * 4;
-
-__global__ void __launch_bounds__(FC1_WARPS * 32) fc1_fwd_kernel(const float* __restrict__ pooled,
-                                                                  const int64_t* __restrict__ slot_row, int N, int G,
-                                                                  const float* __restrict__ theta,
-                                                                  const float* __restrict__ delta, int64_t ld,
-                                                                  float* __restrict__ part) {
-  extern __shared__ float fsm[];
-  float* ps = fsm;                       // [GMAX][KCHUNK], rows >= G zero
-  float* red = fsm + GMAX * KCHUNK;      // [FC1_WARPS][GMAX][HID]
-  const int g = blockIdx.x, split = blockIdx.y;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// grid (groups, KSPLIT), one warp per CTA: group = G consecutive slots sharing
+// weights (a client in training, G = B; a chunk of rows at theta_t in
+// evaluation, G = GMAX).  The warp streams its 448 weight rows (each lane a
+// float4 of the 128 units: coalesced 512-byte rows, 4 rows in flight);
+// the group's activations for 32 rows at a time are loaded one per lane and
+// broadcast with shuffles, so there is no shared memory and up to 32
+// single-warp CTAs per SM keep enough loads in flight for HBM.
+template <int GM>
+__global__ void __launch_bounds__(32) fc1_fwd_kernel(const float* __restrict__ pooled,
+                                                     const int64_t* __restrict__ slot_row, int N, int G,
+                                                     const float* __restrict__ theta, const float* __restrict__ delta,
+                                                     int64_t ld, float* __restrict__ part) {
+  const int g = blockIdx.x, split = blockIdx.y, lane = threadIdx.x;
   const int n0 = g * G;
   const int k0 = split * KCHUNK;
-  const float* dc = delta ? delta + (int64_t)g * ld : nullptr;
-  int live = 0;
-  for (int b = 0; b < G && n0 + b < N; ++b) live += slot_row[n0 + b] >= 0;
-  if (!live) return;
-  for (int i = threadIdx.x; i < GMAX * KCHUNK; i += blockDim.x) {
-    const int b = i / KCHUNK, k = i - b * KCHUNK;
-    const int n = n0 + b;
-    ps[i] = (b < G && n < N && slot_row[n] >= 0) ? pooled[(int64_t)n * FLAT + k0 + k] : 0.f;
-  }
-  __syncthreads();
-  float4 acc[GMAX];
+  bool live[GM];
+  int any = 0;
 #pragma unroll
-  for (int b = 0; b < GMAX; ++b) acc[b] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int b = 0; b < GM; ++b) {
+    live[b] = b < G && n0 + b < N && slot_row[n0 + b] >= 0;
+    any |= live[b];
+  }
+  if (!any) return;
+  const float* dc = delta ? delta + (int64_t)g * ld : nullptr;
+  float4 acc[GM];
+#pragma unroll
+  for (int b = 0; b < GM; ++b) acc[b] = make_float4(0.f, 0.f, 0.f, 0.f);
   const float4* th4 = reinterpret_cast<const float4*>(theta + O_F1 + (int64_t)k0 * HID) + lane;
   const float4* dl4 = dc ? reinterpret_cast<const float4*>(dc + O_F1 + (int64_t)k0 * HID) + lane : nullptr;
+  for (int r0 = 0; r0 < KCHUNK; r0 += 32) {
+    float pv[GM];  // lane l holds the activations of row r0 + l
+#pragma unroll
+    for (int b = 0; b < GM; ++b)
+      pv[b] = live[b] ? __ldg(pooled + (int64_t)(n0 + b) * FLAT + k0 + r0 + lane) : 0.f;
 #pragma unroll 4
-  for (int k = warp; k < KCHUNK; k += FC1_WARPS) {
-    float4 w = __ldg(th4 + (int64_t)k * (HID / 4));
-    if (dl4) {
-      const float4 d = __ldcs(dl4 + (int64_t)k * (HID / 4));
-      w.x -= d.x; w.y -= d.y; w.z -= d.z; w.w -= d.w;
-    }
+    for (int r = 0; r < 32; ++r) {
+      const int64_t k = r0 + r;
+      float4 w = __ldg(th4 + k * (HID / 4));
+      if (dl4) {
+        const float4 d = __ldcs(dl4 + k * (HID / 4));
+        w.x -= d.x; w.y -= d.y; w.z -= d.z; w.w -= d.w;
+      }
 #pragma unroll
-    for (int b = 0; b < GMAX; ++b) {
-      const float p = ps[b * KCHUNK + k];
-      acc[b].x = fmaf(p, w.x, acc[b].x);
-      acc[b].y = fmaf(p, w.y, acc[b].y);
-      acc[b].z = fmaf(p, w.z, acc[b].z);
-      acc[b].w = fmaf(p, w.w, acc[b].w);
+      for (int b = 0; b < GM; ++b) {
+        const float p = __shfl_sync(0xffffffffu, pv[b], r);
+        acc[b].x = fmaf(p, w.x, acc[b].x);
+        acc[b].y = fmaf(p, w.y, acc[b].y);
+        acc[b].z = fmaf(p, w.z, acc[b].z);
+        acc[b].w = fmaf(p, w.w, acc[b].w);
+      }
     }
   }
 #pragma unroll
-  for (int b = 0; b < GMAX; ++b)
-    reinterpret_cast<float4*>(red + (warp * GMAX + b) * HID)[lane] = acc[b];
-  __syncthreads();
-  for (int i = threadIdx.x; i < G * HID; i += blockDim.x) {
-    const int b = i / HID, j = i - b * HID;
-    if (n0 + b >= N) continue;
-    float s = 0.f;
-#pragma unroll
-    for (int w2 = 0; w2 < FC1_WARPS; ++w2) s += red[(w2 * GMAX + b) * HID + j];
-    part[((int64_t)split * N + n0 + b) * HID + j] = s;
-  }
+  for (int b = 0; b < GM; ++b)
+    if (b < G && n0 + b < N)
+      reinterpret_cast<float4*>(part + ((int64_t)split * N + n0 + b) * HID)[lane] = acc[b];
 }
 
 // ------------------------------------------------------------------ head
@@ -441,14 +433,16 @@ __global__ void __launch_bounds__(HID) head_kernel(const float* __restrict__ par
 }
 
 // ------------------------------------------------------- fc1 bwd + update
-// grid (C, KSPLIT), 8 warps; tiles of 64 weight rows.  Per row a warp streams
-// theta_t and the client's delta (float4 per lane, coalesced), forms the
-// gradient p^T dz3 for its 4 units, and writes delta += lr*(g - mu*delta)
-// back in the same pass; the old weights go to a padded smem tile from which
-// dp = dz3 W^T (old W) is computed for the tile's rows.
-constexpr int FB_WARPS = 8, FB_ROWS = 64, FB_LDW = HID + 1;
-constexpr int FC1B_SMEM = (FB_ROWS * FB_LDW + GMAX * HID + GMAX * KCHUNK) * 4;
+// grid (C, KSPLIT), 4 warps per CTA, each warp streaming 112 weight rows of
+// the client.  Per row: theta_t and delta as float4 per lane (coalesced), the
+// gradient p^T dz3 for the lane's 4 units (activations broadcast by shuffles,
+// dz3 in registers), delta += lr*(g - mu*delta) written back in the same
+// pass; the OLD weights go to a per-warp 16-row smem tile from which each lane
+// then computes dp = dz3 W^T for one row (conflict-free padded rows).
+constexpr int FB_WARPS = 4, FB_TR = 16, FB_LDW = HID + 1;
+constexpr int FC1B_SMEM = (FB_WARPS * FB_TR * FB_LDW + GMAX * HID) * 4;
 
+template <int GM>
 __global__ void __launch_bounds__(FB_WARPS * 32) fc1_bwd_kernel(const float* __restrict__ pooled,
                                                                  const float* __restrict__ dz3, int B,
                                                                  const int32_t* __restrict__ client_nb,
@@ -456,31 +450,30 @@ __global__ void __launch_bounds__(FB_WARPS * 32) fc1_bwd_kernel(const float* __r
                                                                  float* __restrict__ delta, int64_t ld, Step st,
                                                                  float* __restrict__ dp) {
   extern __shared__ float bsm[];
-  float* wt_ = bsm;                         // [FB_ROWS][FB_LDW] old weights of the tile
-  float* dz = wt_ + FB_ROWS * FB_LDW;       // [GMAX][HID]
-  float* pv = dz + GMAX * HID;              // [GMAX][KCHUNK]
   const int c = blockIdx.x, split = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nb = client_nb[c];
   if (nb == 0) return;
-  const int n0 = c * B, k0 = split * KCHUNK;
-  float* dc = delta + (int64_t)c * ld;
-  for (int i = threadIdx.x; i < nb * HID; i += blockDim.x) dz[i] = dz3[(int64_t)n0 * HID + i];
-  for (int i = threadIdx.x; i < nb * KCHUNK; i += blockDim.x) {
-    const int b = i / KCHUNK, k = i - b * KCHUNK;
-    pv[i] = pooled[(int64_t)(n0 + b) * FLAT + k0 + k];
-  }
+  float* dz = bsm;                                     // [GM][HID]
+  float* wt_ = bsm + GMAX * HID + warp * FB_TR * FB_LDW;  // this warp's [FB_TR][FB_LDW]
+  const int n0 = c * B;
+  for (int i = threadIdx.x; i < GM * HID; i += blockDim.x) dz[i] = i < nb * HID ? dz3[(int64_t)n0 * HID + i] : 0.f;
   __syncthreads();
-  float4 dzr[GMAX];  // this lane's 4 units of every sample's dz3
+  float4 dzr[GM];
 #pragma unroll
-  for (int b = 0; b < GMAX; ++b)
-    dzr[b] = b < nb ? reinterpret_cast<const float4*>(dz + b * HID)[lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int b = 0; b < GM; ++b) dzr[b] = reinterpret_cast<const float4*>(dz + b * HID)[lane];
+  float* dc = delta + (int64_t)c * ld;
   const float lr = st.lr, mu = st.mu;
-  for (int t0 = 0; t0 < KCHUNK; t0 += FB_ROWS) {
-#pragma unroll 2
-    for (int r = warp; r < FB_ROWS; r += FB_WARPS) {
-      const int k = t0 + r;
-      const int64_t off = O_F1 + (int64_t)(k0 + k) * HID;
+  constexpr int ROWS_PER_WARP = KCHUNK / FB_WARPS;  // 112
+  const int kw = split * KCHUNK + warp * ROWS_PER_WARP;
+  for (int r0 = 0; r0 < ROWS_PER_WARP; r0 += FB_TR) {
+    float pv[GM];  // lane l < FB_TR holds the activations of row r0 + l
+#pragma unroll
+    for (int b = 0; b < GM; ++b)
+      pv[b] = (b < nb && lane < FB_TR) ? __ldg(pooled + (int64_t)(n0 + b) * FLAT + kw + r0 + lane) : 0.f;
+#pragma unroll 4
+    for (int r = 0; r < FB_TR; ++r) {
+      const int64_t off = O_F1 + (int64_t)(kw + r0 + r) * HID;
       const float4 th = __ldg(reinterpret_cast<const float4*>(theta + off) + lane);
       float4* dptr = reinterpret_cast<float4*>(dc + off) + lane;
       const float4 d = *dptr;
@@ -488,8 +481,8 @@ __global__ void __launch_bounds__(FB_WARPS * 32) fc1_bwd_kernel(const float* __r
       wrow[0] = th.x - d.x; wrow[1] = th.y - d.y; wrow[2] = th.z - d.z; wrow[3] = th.w - d.w;
       float4 gw = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int b = 0; b < GMAX; ++b) {
-        const float p = b < nb ? pv[b * KCHUNK + k] : 0.f;
+      for (int b = 0; b < GM; ++b) {
+        const float p = __shfl_sync(0xffffffffu, pv[b], r);
         gw.x = fmaf(p, dzr[b].x, gw.x);
         gw.y = fmaf(p, dzr[b].y, gw.y);
         gw.z = fmaf(p, dzr[b].z, gw.z);
@@ -498,21 +491,24 @@ __global__ void __launch_bounds__(FB_WARPS * 32) fc1_bwd_kernel(const float* __r
       *dptr = make_float4(d.x + lr * (gw.x - mu * d.x), d.y + lr * (gw.y - mu * d.y),
                           d.z + lr * (gw.z - mu * d.z), d.w + lr * (gw.w - mu * d.w));
     }
-    __syncthreads();
-    // dp[b][k] = sum_j dz[b][j] * w_old[k][j] for the tile's rows
-    for (int t = threadIdx.x; t < nb * FB_ROWS; t += blockDim.x) {
-      const int b = t / FB_ROWS, r = t - b * FB_ROWS;
+    __syncwarp();
+    // dp[b][row] = sum_j dz[b][j] * w_old[row][j]: lanes 0..15 take one row each for b even,
+    // lanes 16..31 for b odd (two samples in flight per row)
+    {
+      const int r = lane & (FB_TR - 1), bpar = lane >> 4;
       const float* wr = wt_ + r * FB_LDW;
-      const float* zb = dz + b * HID;
-      float s0 = 0.f, s1 = 0.f;
+      for (int b = bpar; b < nb; b += 2) {
+        const float* zb = dz + b * HID;
+        float s0 = 0.f, s1 = 0.f;
 #pragma unroll 8
-      for (int j = 0; j < HID; j += 2) {
-        s0 = fmaf(zb[j], wr[j], s0);
-        s1 = fmaf(zb[j + 1], wr[j + 1], s1);
+        for (int j = 0; j < HID; j += 2) {
+          s0 = fmaf(zb[j], wr[j], s0);
+          s1 = fmaf(zb[j + 1], wr[j + 1], s1);
+        }
+        dp[(int64_t)(n0 + b) * FLAT + kw + r0 + r] = s0 + s1;
       }
-      dp[(int64_t)(n0 + b) * FLAT + k0 + t0 + r] = s0 + s1;
     }
-    __syncthreads();
+    __syncwarp();
   }
 }
 
@@ -1565,8 +1561,6 @@ int set_smem_limits() {
   cudaFuncSetAttribute(conv2_fwd_pool_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C2F_SMEM);
   cudaFuncSetAttribute(conv2_bwd_x_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C2X_SMEM);
   cudaFuncSetAttribute(conv2_bwd_w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C2W_SMEM);
-  cudaFuncSetAttribute(fc1_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FC1F_SMEM);
-  cudaFuncSetAttribute(fc1_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FC1B_SMEM);
   cudaFuncSetAttribute(conv2_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
   cudaFuncSetAttribute(conv2_bwd_x_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BX_SMEM);
   cudaFuncSetAttribute(dz2_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DZB_SMEM);
@@ -1594,8 +1588,19 @@ int forward(const float* X, const float* theta, const float* delta, int64_t ld, 
   } else {
     FB_LAUNCH("conv2_fwd_pool_kernel", s, conv2_fwd_pool_kernel<<<N, 256, C2F_SMEM, s>>>(w.a1h, w.a1l, w.slot_row, theta, delta, ld, B, w.pooled, w.code));
   }
-  FB_LAUNCH("fc1_fwd_kernel", s, fc1_fwd_kernel<<<dim3((N + G - 1) / G, KSPLIT), FC1_WARPS * 32, FC1F_SMEM, s>>>(w.pooled, w.slot_row, N, G, theta, delta, ld,
-                                                               w.part));
+  {
+    // weight-sharing group per warp: the client's B slots in training, 8 rows at theta_t in evaluation
+    const int gf = delta ? G : 8;
+    const dim3 grid((N + gf - 1) / gf, KSPLIT);
+    if (gf <= 8)
+      FB_LAUNCH("fc1_fwd_kernel", s, fc1_fwd_kernel<8><<<grid, 32, 0, s>>>(w.pooled, w.slot_row, N, gf, theta, delta, ld, w.part));
+    else if (gf <= 10)
+      FB_LAUNCH("fc1_fwd_kernel", s, fc1_fwd_kernel<10><<<grid, 32, 0, s>>>(w.pooled, w.slot_row, N, gf, theta, delta, ld, w.part));
+    else if (gf <= 12)
+      FB_LAUNCH("fc1_fwd_kernel", s, fc1_fwd_kernel<12><<<grid, 32, 0, s>>>(w.pooled, w.slot_row, N, gf, theta, delta, ld, w.part));
+    else
+      FB_LAUNCH("fc1_fwd_kernel", s, fc1_fwd_kernel<GMAX><<<grid, 32, 0, s>>>(w.pooled, w.slot_row, N, gf, theta, delta, ld, w.part));
+  }
   return launch_status("cnn forward");
 }
 
@@ -1679,8 +1684,15 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
       if (st) return st;
       FB_LAUNCH("head_kernel", s, head_kernel<<<Cw, HID, 0, s>>>(w.part, w.slot_row, N, B, y, theta_t, dlt, ld_delta, w.client_nb, sp, w.dz3,
                                      nullptr, nullptr));
-      FB_LAUNCH("fc1_bwd_kernel", s, fc1_bwd_kernel<<<dim3(Cw, KSPLIT), FB_WARPS * 32, FC1B_SMEM, s>>>(w.pooled, w.dz3, B, w.client_nb, theta_t, dlt, ld_delta, sp,
-                                                      w.dp));
+      if (B <= 8)
+        FB_LAUNCH("fc1_bwd_kernel", s, fc1_bwd_kernel<8><<<dim3(Cw, KSPLIT), FB_WARPS * 32, FC1B_SMEM, s>>>(
+            w.pooled, w.dz3, B, w.client_nb, theta_t, dlt, ld_delta, sp, w.dp));
+      else if (B <= 10)
+        FB_LAUNCH("fc1_bwd_kernel", s, fc1_bwd_kernel<10><<<dim3(Cw, KSPLIT), FB_WARPS * 32, FC1B_SMEM, s>>>(
+            w.pooled, w.dz3, B, w.client_nb, theta_t, dlt, ld_delta, sp, w.dp));
+      else
+        FB_LAUNCH("fc1_bwd_kernel", s, fc1_bwd_kernel<GMAX><<<dim3(Cw, KSPLIT), FB_WARPS * 32, FC1B_SMEM, s>>>(
+            w.pooled, w.dz3, B, w.client_nb, theta_t, dlt, ld_delta, sp, w.dp));
       if (g_conv_impl == 1) {
         FB_LAUNCH("dz2_build_kernel", s, dz2_build_kernel<<<N, 256, DZB_SMEM, s>>>(w.dp, w.pooled, w.code, w.slot_row, w.dz2h, w.dz2l, w.dzfh, w.dzfl, w.dzscale, w.db2));
         FB_LAUNCH("conv2_wimgT_kernel", s, conv2_wimgT_kernel<<<Cw, 256, 0, s>>>(theta_t, dlt, ld_delta, w.client_nb, w.wimg));
