@@ -62,6 +62,17 @@ int64_t fb_launch_count(void);
 void fb_timing_enable(int on);
 int fb_timing_report(char* names, int names_len, double* ms, int64_t* counts, int max_entries);
 
+/* [host] Per-user minibatch orders, bit-exact with the reference's
+ * default_rng(derive_seed(ctx, "user", uid)).permutation(n) per epoch
+ * (fedsim/core/seeds.py:18-33, fedsim/models/models.py:252-255): SHA-256,
+ * numpy SeedSequence + PCG64 and Generator.permutation restated natively.
+ * id_reprs holds repr(uid).encode() of every user back to back, user u at
+ * [id_off[u], id_off[u+1]).  Writes epochs * num_rows[u] int32 at
+ * perms_out + perm_off[u].  fb_derive_seed: the 63-bit seed of a message.  */
+int fb_user_permutations(uint64_t context_seed, const uint8_t* id_reprs, const int64_t* id_off, int num_users,
+                         const int32_t* num_rows, int epochs, int32_t* perms_out, const int64_t* perm_off);
+int fb_derive_seed(const uint8_t* data, int64_t len, uint64_t* out);
+
 /* ---------------------------------------------------------------- a4 eval
  * Per-client summed cross-entropy and correct count at the shared theta,
  * over all of the client's rows.  Replaces fedsim/models/kernels.py:70-83

@@ -68,6 +68,29 @@ def client_permutations(ctx_seed: int, user_ids: Sequence[str], sizes: Sequence[
     return out
 
 
+def native_permutations(ctx_seed: int, user_ids: Sequence[str], num_rows: np.ndarray, epochs: int,
+                        perm_off: np.ndarray, repr_cache: dict | None = None) -> np.ndarray:
+    """Same draws as :func:`client_permutations`, computed by the library's
+    native SHA-256 / SeedSequence / PCG64 restatement (fb_user_permutations):
+    ~2 us per user instead of ~20 us through numpy."""
+    cache = repr_cache if repr_cache is not None else {}
+    reprs = []
+    for uid in user_ids:
+        r = cache.get(uid)
+        if r is None:
+            r = cache[uid] = repr(uid).encode()
+        reprs.append(r)
+    blob = np.frombuffer(b"".join(reprs) or b"\0", dtype=np.uint8)
+    id_off = np.zeros(len(reprs) + 1, dtype=np.int64)
+    np.cumsum([len(r) for r in reprs], out=id_off[1:])
+    rows = np.ascontiguousarray(num_rows, dtype=np.int32)
+    out = np.empty(max(int(rows.astype(np.int64).sum()) * epochs, 1), dtype=np.int32)
+    native.check(native.load_library().fb_user_permutations(
+        int(ctx_seed), blob.ctypes.data, id_off.ctypes.data, len(reprs), rows.ctypes.data, int(epochs),
+        out.ctypes.data, np.ascontiguousarray(perm_off, dtype=np.int64).ctypes.data), "fb_user_permutations")
+    return out[: int(rows.astype(np.int64).sum()) * epochs]
+
+
 class _Staging:
     """Packs host arrays into one pinned buffer, one H2D copy, device views."""
 
@@ -215,6 +238,7 @@ class GpuSimulationEngine:
         self._staging = _Staging(self.device)
         self._pops: dict[Population, DevicePopulation] = {}
         self._runners: dict[int, _ModelRunner] = {}
+        self._repr_cache: dict[str, bytes] = {}
         self.stream = torch.cuda.current_stream(self.device)
         self.io_bytes = {"h2d": 0, "d2h": 0}  # cumulative host<->device traffic of run_iteration
 
@@ -291,11 +315,10 @@ class GpuSimulationEngine:
         host = [row_start, num_rows]
         if train:
             tp = plan.train
-            perms = client_permutations(ctx.seed, queue, num_rows.tolist(), tp.num_epochs)
-            perm_flat = (np.concatenate(perms) if perms else np.zeros(0)).astype(np.int32)
             perm_off = np.zeros(C, dtype=np.int64)
             if C > 1:
                 perm_off[1:] = np.cumsum(num_rows[:-1].astype(np.int64) * tp.num_epochs)
+            perm_flat = native_permutations(ctx.seed, queue, num_rows, tp.num_epochs, perm_off, self._repr_cache)
             w = (num_rows.astype(np.float32) if plan.weighting == "datapoints"
                  else np.ones(C, dtype=np.float32))
             host += [perm_flat, perm_off, w]

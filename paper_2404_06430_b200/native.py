@@ -33,6 +33,8 @@ SIGNATURES: dict[str, tuple] = {
     "fb_launch_count": (_i64, []),
     "fb_timing_enable": (None, [_i32]),
     "fb_timing_report": (_i32, [C.c_char_p, _i32, C.POINTER(_f64), C.POINTER(_i64), _i32]),
+    "fb_user_permutations": (_i32, [_u64, _p, _p, _i32, _p, _i32, _p, _p]),
+    "fb_derive_seed": (_i32, [_p, _i64, C.POINTER(_u64)]),
     "fb_eval_linear_f32": (_i32, [_p, _i32, _i32, _p, _p, _p, _p, _i32, _p, _p, _p]),
     "fb_eval_mlp_f32": (_i32, [_p, _i32, _i32, _i32, _p, _p, _p, _p, _i32, _p, _p, _p]),
     "fb_local_sgd_linear_f32": (

@@ -155,3 +155,26 @@ def test_engine_refuses_without_cuda():
     cfg = CONFIGS["mlp_dp"]
     with pytest.raises(fb.NativeUnavailable):
         fb.GpuSimulationEngine(product_datasets(cfg))
+
+
+def test_native_permutations_bit_exact_with_numpy(golden):
+    """fb_user_permutations (native SHA-256 + SeedSequence + PCG64 +
+    permutation) == the reference's numpy draws, ragged sizes, 2 epochs."""
+    from paper_2404_06430_b200 import native
+
+    if not native.LIB_PATH.exists():
+        pytest.skip("library not built")
+    from paper_2404_06430_b200.engine import native_permutations
+
+    g = golden("sampling")
+    for i in range(50):
+        ctx = fb.derive_seed(1, "cohort", i, "train")
+        got = native_permutations(ctx, [f"train{i:05d}"], np.array([50]), 2, np.array([0]))
+        np.testing.assert_array_equal(got, g["perms"][i])
+    rng = np.random.default_rng(0)
+    ids = [f"u{i}" for i in range(300)] + ["user with space", "ünïcode", "quote'd"]
+    sizes = rng.integers(1, 200, size=len(ids))
+    off = np.concatenate([[0], np.cumsum(sizes * 3)[:-1]])
+    got = native_permutations(12345, ids, sizes, 3, off)
+    want = np.concatenate(fb.client_permutations(12345, ids, sizes.tolist(), 3))
+    np.testing.assert_array_equal(got, want)
