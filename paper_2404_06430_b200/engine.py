@@ -68,6 +68,39 @@ def client_permutations(ctx_seed: int, user_ids: Sequence[str], sizes: Sequence[
     return out
 
 
+def plan_shard(dataset, ctx: CentralContext, rank: int, world_size: int, *, cohort_mode: str = "fixed",
+               poisson_rate: float | None = None, base_policy: str = "median", base_value: float = 0.0):
+    """Host half of a context on one rank: the cohort (identical on every
+    rank: same seed, fedsim/feddata/sampling.py:12-40) and this rank's LPT
+    queue over ``world_size`` workers (fedsim/engine/scheduling.py:34-78) --
+    the reference's worker assignment with num_workers = world_size."""
+    cohort = sample_cohort(dataset, ctx.cohort_size, ctx.seed, mode=cohort_mode, poisson_rate=poisson_rate)
+    if not cohort:
+        return cohort, ()
+    weights = {uid: float(dataset.users[uid].weight) for uid in cohort}
+    base = compute_base_weight(list(weights.values()), base_policy, base_value)
+    return cohort, schedule_users(weights, world_size, base).queues[rank]
+
+
+# layout of the per-context fp64 sums reduced across ranks
+SUM_FIELDS = ("loss", "correct", "points", "per_user_acc", "users", "clipped", "count", "norm", "weight")
+
+
+def reduce_across_ranks(sums: np.ndarray, agg_flat, group=None) -> np.ndarray:
+    """worker_reduce across ranks (fedsim/engine/aggregator.py:46-62): one
+    all-reduce(SUM) of the flat payload (NCCL over NVLink on GPUs) and one of
+    the fp64 metric / bookkeeping sums.  Returns the reduced sums."""
+    torch = _torch()
+    dist = torch.distributed
+    dev = agg_flat.device if agg_flat is not None else (
+        torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else torch.device("cpu"))
+    t = torch.from_numpy(np.ascontiguousarray(sums, dtype=np.float64)).to(dev)
+    dist.all_reduce(t, group=group)
+    if agg_flat is not None:
+        dist.all_reduce(agg_flat, group=group)
+    return t.cpu().numpy()
+
+
 def native_permutations(ctx_seed: int, user_ids: Sequence[str], num_rows: np.ndarray, epochs: int,
                         perm_off: np.ndarray, repr_cache: dict | None = None) -> np.ndarray:
     """Same draws as :func:`client_permutations`, computed by the library's
@@ -285,14 +318,11 @@ class GpuSimulationEngine:
         dataset = self._datasets.get(pop_key)
         if dataset is None:
             raise EngineError(f"iteration {ctx.iteration}: no dataset for population {pop_key.value!r}")
-        cohort = sample_cohort(dataset, ctx.cohort_size, ctx.seed, mode=self._cohort_mode,
-                               poisson_rate=self._poisson_rate)
+        cohort, queue = plan_shard(dataset, ctx, self.rank, self.world_size, cohort_mode=self._cohort_mode,
+                                   poisson_rate=self._poisson_rate, base_policy=self._base_policy,
+                                   base_value=self._base_value)
         if not cohort:
             return None, {}, cohort
-        users = dataset.users
-        weights = {uid: float(users[uid].weight) for uid in cohort}
-        base = compute_base_weight(list(weights.values()), self._base_policy, self._base_value)
-        queue = schedule_users(weights, self.world_size, base).queues[self.rank]
 
         plan = algorithm.cohort_plan(state, ctx)
         runner = self._runner(plan.model)
@@ -395,11 +425,7 @@ class GpuSimulationEngine:
             float((n_f if plan.weighting == "datapoints" else np.ones(C)).sum()) if train else 0.0,
         ], dtype=np.float64)
         if self.world_size > 1:
-            t = torch.from_numpy(sums).to(self.device)
-            torch.distributed.all_reduce(t, group=self.group)
-            if agg_flat is not None:
-                torch.distributed.all_reduce(agg_flat, group=self.group)
-            sums = t.cpu().numpy()
+            sums = reduce_across_ranks(sums, agg_flat, self.group)
         metrics: dict[str, MetricValue] = {}
         if sums[4] > 0:
             metrics = {
