@@ -402,13 +402,85 @@ def reference_arm(args, wl):
     print(json.dumps(line), flush=True)
 
 
+def aggregation_microbench(args):
+    """BASELINE configs[4]: clip / aggregate / noise over a 10M-parameter
+    update for cohort C on one GPU.  Client deltas come from a pool of P
+    materialised [P, D] fp32 buffers (P * 40 MB >> L2, so every pass streams
+    HBM); a step = K2 (norm + clip factor) and K3 (weighted sum) over all C
+    clients in chunks of P, then K4+K5 (Philox noise + /W + SGD) once."""
+    torch = _torch()
+    from paper_2404_06430_b200 import native
+
+    D, P, C = args.micro_dim, args.micro_pool, args.cohort or 1000
+    ld = (D + 3) & ~3
+    g = torch.Generator(device="cuda").manual_seed(0)
+    pool = torch.randn(P, ld, device="cuda", generator=g) * (1.0 / np.sqrt(D))
+    pool[P // 2:] *= 1e-4                      # half the pool below the bound: a clip mix
+    w = torch.ones(P, device="cuda")
+    norm = torch.empty(P, dtype=torch.float64, device="cuda")
+    coef = torch.empty(P, device="cuda")
+    clipped = torch.empty(P, dtype=torch.int32, device="cuda")
+    bad = torch.empty(P, dtype=torch.int32, device="cuda")
+    cws = torch.empty(max(native.call("fb_clip_workspace_bytes", P, D), 16), dtype=torch.uint8, device="cuda")
+    sws = torch.empty(max(native.call("fb_weighted_sum_workspace_bytes", P, D), 16), dtype=torch.uint8, device="cuda")
+    agg = torch.empty(D, device="cuda")
+    theta = torch.zeros(D, device="cuda")
+    s = native.stream_handle()
+
+    def step():
+        for c0 in range(0, C, P):
+            n = min(P, C - c0)
+            native.call("fb_delta_norm_clip_f32", pool.data_ptr(), ld, n, D, w.data_ptr(), 1.0, norm.data_ptr(),
+                        coef.data_ptr(), clipped.data_ptr(), bad.data_ptr(), cws.data_ptr(), cws.numel(), s)
+            native.call("fb_weighted_sum_f32", pool.data_ptr(), ld, n, D, coef.data_ptr(), agg.data_ptr(),
+                        int(c0 > 0), sws.data_ptr(), sws.numel(), s)
+        native.call("fb_noise_avg_sgd_f32", theta.data_ptr(), agg.data_ptr(), D, 0.1, 1234, None, 1.0 / C, 1.0,
+                    None, s)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    native.lib().fb_timing_enable(1)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        step()
+    ev1.record()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    rep = native.timing_report()
+    native.lib().fb_timing_enable(0)
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    b_alg = 4.0 * D * C + 12.0 * D   # SURVEY.md section 8(d): each client read once + aggregate + theta r/w
+    kern = {}
+    for name, bytes_per_step in (("row_sumsq_partial_kernel", 4.0 * D * C), ("weighted_sum_kernel", 4.0 * D * C + 4.0 * D * -(-C // P)),
+                                 ("noise_avg_sgd_kernel", 12.0 * D)):
+        if name in rep:
+            t = rep[name][0] / args.steps
+            kern[name] = {"ms": round(t, 3), "GB/s": round(bytes_per_step / (t * 1e-3) / 1e9, 1),
+                          "frac": round(bytes_per_step / (t * 1e-3) / 1e9 / hbm, 4)}
+    print(json.dumps({
+        "metric": "aggregation microbench (BASELINE configs[4]): clip + aggregate + noise, 10M-param update",
+        "value": 1e3 / ms, "unit": "iterations/s", "clients_per_sec": C * 1e3 / ms, "ms_per_step": ms,
+        "steps": args.steps, "warmup": args.warmup, "n_gpus": 1, "higher_is_better": True, "dtype": "f32",
+        "config": {"workload": "aggmicro", "D": D, "cohort": C, "pool": P,
+                   "l2": f"pool of {P} x {4 * ld / 1e6:.0f} MB client deltas >> L2"},
+        "roofline": {"bound": "hbm", "achieved": round(b_alg / (ms * 1e-3) / 1e9, 1), "peak": hbm, "unit": "GB/s",
+                     "frac": round(b_alg / (ms * 1e-3) / 1e9 / hbm, 4),
+                     "algorithmic_bytes_per_step": b_alg, "note": "K2 reads every client once more than B_alg counts"},
+        "kernels": kern}), flush=True)
+
+
 def main(argv=None):
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cnn")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS) + ["aggmicro"], default="cnn")
+    ap.add_argument("--micro-dim", type=int, default=10_000_000)
+    ap.add_argument("--micro-pool", type=int, default=64)
     ap.add_argument("--cohort", type=int, default=None)
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--e2e-warmup", type=int, default=2)
@@ -418,6 +490,9 @@ def main(argv=None):
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "ours":
         ap.error("--warmup must be >= 3")
+    if args.workload == "aggmicro":
+        aggregation_microbench(args)
+        return
     wl = dict(WORKLOADS[args.workload])
     if args.cohort:
         wl["cohort"] = args.cohort
