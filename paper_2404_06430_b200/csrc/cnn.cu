@@ -116,31 +116,52 @@ __global__ void prefix_kernel(const int32_t* __restrict__ num_rows, int C, int64
 }
 
 // ------------------------------------------------------------ conv1 fwd
-// one CTA per slot; thread per output position, all 32 channels
+// one CTA per slot; thread per output position, all 32 channels.  Writes the
+// ReLU output either as fp32 (CUDA-core validation path) or as the scaled
+// fp16 hi + lo pair the tcgen05 kernels consume: the per-sample power-of-two
+// scale comes from an a-priori bound max_o(|b_o| + max|x| * sum_k |w_ok|) >=
+// max|a1|, so the conversion needs no second pass.
 __global__ void __launch_bounds__(256) conv1_fwd_kernel(const float* __restrict__ X,
                                                         const int64_t* __restrict__ slot_row,
                                                         const float* __restrict__ theta,
                                                         const float* __restrict__ delta, int64_t ld, int B,
-                                                        float* __restrict__ a1h, float* __restrict__ a1l,
-                                                        __half* __restrict__ a1fh, __half* __restrict__ a1fl,
-                                                        float* __restrict__ a1scale) {
+                                                        float* __restrict__ a1, __half* __restrict__ a1fh,
+                                                        __half* __restrict__ a1fl, float* __restrict__ a1scale) {
   __shared__ float img[IMG];
-  __shared__ float redmax[8];
-  float amax = 0.f;
   __shared__ float w[27 * C1 + C1];  // [tap27][o] then bias
+  __shared__ float red[8];
+  __shared__ float s_scale;
   const int n = blockIdx.x;
   const int64_t row = slot_row[n];
   if (row < 0) return;
   const float* dc = delta ? delta + (int64_t)(n / B) * ld : nullptr;
-  for (int i = threadIdx.x; i < IMG; i += blockDim.x) img[i] = X[row * IMG + i];
+  float xm = 0.f;
+  for (int i = threadIdx.x; i < IMG; i += blockDim.x) {
+    const float v = X[row * IMG + i];
+    img[i] = v;
+    xm = fmaxf(xm, fabsf(v));
+  }
   for (int i = threadIdx.x; i < 27 * C1; i += blockDim.x) {
     const int o = i / 27, r = i - o * 27;  // OIHW source, [ci*9+ky*3+kx]
     w[r * C1 + o] = wt(theta, dc, O_W1 + i);
   }
   for (int o = threadIdx.x; o < C1; o += blockDim.x) w[27 * C1 + o] = wt(theta, dc, O_B1 + o);
+  xm = warp_max(xm);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = xm;
   __syncthreads();
-  float* outh = a1h + (int64_t)n * A1;
-  float* outl = a1l + (int64_t)n * A1;
+  if (threadIdx.x < 32) {
+    float m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    m = warp_max(m);
+    float sw = 0.f;
+    for (int r = 0; r < 27; ++r) sw += fabsf(w[r * C1 + threadIdx.x]);
+    const float bound = warp_max(fabsf(w[27 * C1 + threadIdx.x]) + m * sw);
+    if (threadIdx.x == 0) {
+      s_scale = bound > 0.f ? exp2f(14.f - ceilf(log2f(bound))) : 1.f;
+      if (a1scale) a1scale[n] = s_scale;
+    }
+  }
+  __syncthreads();
+  const float sc = s_scale;
   for (int p = threadIdx.x; p < S1 * S1; p += blockDim.x) {
     const int y = p / S1, x = p - y * S1;
     float acc[C1];
@@ -157,46 +178,33 @@ __global__ void __launch_bounds__(256) conv1_fwd_kernel(const float* __restrict_
 #pragma unroll
           for (int o = 0; o < C1; ++o) acc[o] = fmaf(v, wr[o], acc[o]);
         }
-    // a1 is stored split for 3xTF32: a1 = hi + lo exactly, hi tf32-rounded
-    float4* dh = reinterpret_cast<float4*>(outh + (int64_t)p * C1);
-    float4* dl = reinterpret_cast<float4*>(outl + (int64_t)p * C1);
+    const int64_t off = (int64_t)n * A1 + (int64_t)p * C1;
+    if (a1) {
+      float4* d4 = reinterpret_cast<float4*>(a1 + off);
 #pragma unroll
-    for (int q = 0; q < C1 / 4; ++q) {
-      float h[4], l[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float v = fmaxf(acc[4 * q + e], 0.f);
-        amax = fmaxf(amax, v);
-        tc::split_tf32(v, h[e], l[e]);
-      }
-      dh[q] = make_float4(h[0], h[1], h[2], h[3]);
-      dl[q] = make_float4(l[0], l[1], l[2], l[3]);
+      for (int q = 0; q < C1 / 4; ++q)
+        d4[q] = make_float4(fmaxf(acc[4 * q], 0.f), fmaxf(acc[4 * q + 1], 0.f), fmaxf(acc[4 * q + 2], 0.f),
+                            fmaxf(acc[4 * q + 3], 0.f));
     }
-  }
-  if (!a1fh) return;
-  // fp16 copy for the conv2 weight gradient (tcgen05 kind::f16): scaled by a
-  // per-sample power of two so the largest value is ~2^14, split hi + lo
-  amax = warp_max(amax);
-  if ((threadIdx.x & 31) == 0) redmax[threadIdx.x >> 5] = amax;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    float m = threadIdx.x < (blockDim.x >> 5) ? redmax[threadIdx.x] : 0.f;
-    m = warp_max(m);
-    if (threadIdx.x == 0) redmax[0] = m > 0.f ? exp2f(14.f - ceilf(log2f(m))) : 1.f;
-  }
-  __syncthreads();
-  const float sc = redmax[0];
-  if (threadIdx.x == 0) a1scale[n] = sc;
-  __half* fh = a1fh + (int64_t)n * A1;
-  __half* fl = a1fl + (int64_t)n * A1;
-  for (int i = threadIdx.x; i < A1 / 2; i += blockDim.x) {
-    const float2 vh = reinterpret_cast<const float2*>(outh)[i];
-    const float2 vl = reinterpret_cast<const float2*>(outl)[i];
-    const float x0 = (vh.x + vl.x) * sc, x1 = (vh.y + vl.y) * sc;
-    const __half h0 = __float2half_rn(x0), h1 = __float2half_rn(x1);
-    reinterpret_cast<__half2*>(fh)[i] = __halves2half2(h0, h1);
-    reinterpret_cast<__half2*>(fl)[i] =
-        __halves2half2(__float2half_rn(x0 - __half2float(h0)), __float2half_rn(x1 - __half2float(h1)));
+    if (a1fh) {
+      uint4* h4 = reinterpret_cast<uint4*>(a1fh + off);
+      uint4* l4 = reinterpret_cast<uint4*>(a1fl + off);
+#pragma unroll
+      for (int q = 0; q < C1 / 8; ++q) {
+        uint32_t hv[4], lv[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float v0 = fmaxf(acc[8 * q + 2 * e], 0.f) * sc, v1 = fmaxf(acc[8 * q + 2 * e + 1], 0.f) * sc;
+          const __half h0 = __float2half_rn(v0), h1 = __float2half_rn(v1);
+          const __half2 hh = __halves2half2(h0, h1);
+          const __half2 ll = __halves2half2(__float2half_rn(v0 - __half2float(h0)), __float2half_rn(v1 - __half2float(h1)));
+          hv[e] = *reinterpret_cast<const uint32_t*>(&hh);
+          lv[e] = *reinterpret_cast<const uint32_t*>(&ll);
+        }
+        h4[q] = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+        l4[q] = make_uint4(lv[0], lv[1], lv[2], lv[3]);
+      }
+    }
   }
 }
 
@@ -221,8 +229,8 @@ __global__ void __launch_bounds__(256) conv2_fwd_pool_kernel(const float* __rest
   if (slot_row[n] < 0) return;
   const float* dc = delta ? delta + (int64_t)(n / B) * ld : nullptr;
   const float* srch = a1h + (int64_t)n * A1;
-  const float* srcl = a1l + (int64_t)n * A1;
-  for (int i = threadIdx.x; i < A1; i += blockDim.x) as[(i >> 5) * A1P + (i & 31)] = srch[i] + srcl[i];
+  const float* srcl = a1l ? a1l + (int64_t)n * A1 : nullptr;
+  for (int i = threadIdx.x; i < A1; i += blockDim.x) as[(i >> 5) * A1P + (i & 31)] = srch[i] + (srcl ? srcl[i] : 0.f);
   for (int i = threadIdx.x; i < C2 * C1 * 9; i += blockDim.x) {
     const int o = i / (C1 * 9), r = i - o * (C1 * 9), ci = r / 9, tap = r - ci * 9;
     ws[(tap * C1 + ci) * C2 + o] = wt(theta, dc, O_W2 + i);
@@ -611,7 +619,7 @@ __global__ void __launch_bounds__(256) conv2_bwd_w_kernel(const float* __restric
     const int64_t n = (int64_t)c * B + b;
     __syncthreads();
     for (int i = threadIdx.x; i < A1; i += blockDim.x)
-      as[(i >> 5) * A1P + (i & 31)] = a1h[n * A1 + i] + a1l[n * A1 + i];
+      as[(i >> 5) * A1P + (i & 31)] = a1h[n * A1 + i] + (a1l ? a1l[n * A1 + i] : 0.f);
     for (int i = threadIdx.x; i < FLAT; i += blockDim.x) {
       gs[i] = pooled[n * FLAT + i] > 0.f ? dp[n * FLAT + i] : 0.f;
       cs[i] = code[n * FLAT + i];
@@ -741,230 +749,18 @@ __global__ void zero_delta_kernel(float* __restrict__ delta, int64_t ld, int C) 
 
 
 // ================================================================ tcgen05
-// conv2 forward + ReLU + 2x2 max-pool on the 5th-generation tensor cores.
-//
-// Implicit GEMM per sample: Z[m, o] = sum_{tap, ci} a1[y+ky, x+kx, ci] W[o, ci, ky, kx]
-// with m = (y, x).  An M tile is 4 output rows x 28 columns = 112 rows (the
-// UMMA M = 128 tile's last 16 rows are don't-care), N = 64 channels, K = 9
-// taps x 32 input channels.  For tap (ky, kx) the A tile is ONE 4-D TMA box
-// {32 ci, 28 x, 4 y, 1 n} of the NHWC a1 at (0, kx, y0 + ky, n): each output
-// row's 32 channels are one 128-byte swizzle row, so the TMA writes exactly the
-// K-major SWIZZLE_128B canonical layout (implicit im2col, no copy kernel).
-// Precision: 3xTF32 -- a1 and W are stored split (hi = tf32-rounded, lo =
-// remainder) and each tap issues hi*Whi + hi*Wlo + lo*Whi into the same fp32
-// TMEM accumulator (~fp32 accuracy; plain TF32 would miss the 1e-5 gate).
-// Roles (192 threads): warp 0 TMA producer, warp 1 TMEM owner + MMA issuer,
-// warps 2-5 epilogue (TMEM -> registers -> bias/ReLU -> smem -> pool -> HBM).
-// The client's whole 9-tap W (hi + lo, 144 KB) stays resident in smem; A
-// streams through a 3-stage ring; the accumulator is double-buffered in TMEM
-// so the epilogue of tile i overlaps the MMAs of tile i+1.
-constexpr int TC_ROWS = 4;                       // conv rows per M tile
-constexpr int TC_M = TC_ROWS * S2;               // 112 valid rows
-constexpr int TC_TILES = S2 / TC_ROWS;           // 7 tiles per sample
-constexpr int TC_A_STAGE = 128 * 128;            // 16 KB smem per stage (128 rows x 128 B)
-constexpr int TC_A_TX = TC_M * 128;              // 14336 bytes landed per TMA box
-constexpr int TC_B_TAP = C2 * 128;               // 8 KB: 64 rows (o) x 32 ci
-constexpr int WIMG_BYTES = 9 * 2 * TC_B_TAP;     // 147456: [tap][hi|lo] images
-constexpr int TC_STAGES = 3;
-constexpr int TC_EPI_LD = 33;
-constexpr int TC_EPI_BYTES = TC_M * TC_EPI_LD * 4;
-constexpr int TC_SMEM = 1024 + WIMG_BYTES + TC_STAGES * TC_A_STAGE + TC_EPI_BYTES + 256;
-constexpr int TC_THREADS = 192;
-constexpr int TC_ACC_COLS = 4 * C2;              // 4 accumulators x 64 fp32 columns per tile
-constexpr uint32_t TC_IDESC = tc::idesc_tf32(128, C2);
-
-// per-group conv2 weight image: K-major SW128 tiles, tap-major, hi then lo
-__global__ void __launch_bounds__(256) conv2_wimg_kernel(const float* __restrict__ theta,
-                                                         const float* __restrict__ delta, int64_t ld,
-                                                         const int32_t* __restrict__ client_nb,
-                                                         uint8_t* __restrict__ wimg) {
-  const int g = blockIdx.x;
-  if (delta && client_nb && client_nb[g] == 0) return;
-  const float* dc = delta ? delta + (int64_t)g * ld : nullptr;
-  uint8_t* img = wimg + (int64_t)g * WIMG_BYTES;
-  for (int i = threadIdx.x; i < C2 * C1 * 9; i += blockDim.x) {
-    const int o = i / (C1 * 9), r = i - o * (C1 * 9), ci = r / 9, tap = r - ci * 9;
-    float h, l;
-    tc::split_tf32(wt(theta, dc, O_W2 + i), h, l);
-    const uint32_t off = tc::sw128_offset(o, ci);
-    *reinterpret_cast<float*>(img + (tap * 2 + 0) * TC_B_TAP + off) = h;
-    *reinterpret_cast<float*>(img + (tap * 2 + 1) * TC_B_TAP + off) = l;
-  }
-}
-
-__global__ void __launch_bounds__(TC_THREADS, 1) conv2_fwd_tc_kernel(
-    const __grid_constant__ CUtensorMap tm_hi, const __grid_constant__ CUtensorMap tm_lo,
-    const uint8_t* __restrict__ wimg, int64_t wimg_stride, const int64_t* __restrict__ slot_row, int N, int G,
-    const float* __restrict__ theta, const float* __restrict__ delta, int64_t ld, float* __restrict__ pooled,
-    uint8_t* __restrict__ code) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sB = sm;                                        // [9][2][8 KB]
-  uint8_t* sA = sB + WIMG_BYTES;                           // [stages][16 KB]
-  float* sE = reinterpret_cast<float*>(sA + TC_STAGES * TC_A_STAGE);  // [112][33]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sE) + TC_EPI_BYTES);
-  uint64_t* full = bars;                 // [stages]
-  uint64_t* empty = bars + TC_STAGES;    // [stages]
-  uint64_t* tfull = empty + TC_STAGES;   // [2]
-  uint64_t* tempty = tfull + 2;          // [2]
-  uint64_t* bfull = tempty + 2;          // [1]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
-  __shared__ float bias[C2];
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = blockIdx.x;
-  const int n0 = g * G;
-  const float* dc = delta ? delta + (int64_t)g * ld : nullptr;
-
-  if (threadIdx.x < C2) bias[threadIdx.x] = wt(theta, dc, O_B2 + threadIdx.x);
-  if (warp == 0 && lane == 0) {
-    for (int i = 0; i < TC_STAGES; ++i) {
-      tc::mbar_init(&full[i], 1);
-      tc::mbar_init(&empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      tc::mbar_init(&tfull[i], 1);
-      tc::mbar_init(&tempty[i], 4);
-    }
-    tc::mbar_init(bfull, 1);
-    tc::fence_mbar_init();
-  }
-  if (warp == 1) tc::tmem_alloc<2 * TC_ACC_COLS>(tmem_slot);
-  tc::tc_fence_before();
-  __syncthreads();
-  tc::tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    // ------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      tc::tma_prefetch(&tm_hi);
-      tc::tma_prefetch(&tm_lo);
-      tc::mbar_arrive_expect_tx(bfull, WIMG_BYTES);
-      tc::bulk_load(sB, wimg + (int64_t)g * wimg_stride, WIMG_BYTES, bfull);
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int b = 0; b < G; ++b) {
-        const int n = n0 + b;
-        if (n >= N || slot_row[n] < 0) continue;
-        for (int t = 0; t < TC_TILES; ++t)
-          for (int tap = 0; tap < 9; ++tap)
-            for (int part = 0; part < 2; ++part) {
-              tc::mbar_wait(&empty[stage], phase ^ 1);
-              tc::mbar_arrive_expect_tx(&full[stage], TC_A_TX);
-              tc::tma_load_4d(sA + stage * TC_A_STAGE, part ? &tm_lo : &tm_hi, 0, tap % 3, TC_ROWS * t + tap / 3, n,
-                              &full[stage]);
-              if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
-            }
-      }
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------------- MMA issuer
-    tc::mbar_wait(bfull, 0);
-    int stage = 0, tile = 0;
-    uint32_t phase = 0;
-    const uint32_t sA0 = tc::smem_u32(sA), sB0 = tc::smem_u32(sB);
-    for (int b = 0; b < G; ++b) {
-      const int n = n0 + b;
-      if (n >= N || slot_row[n] < 0) continue;
-      for (int t = 0; t < TC_TILES; ++t, ++tile) {
-        const int acc = tile & 1;
-        tc::mbar_wait(&tempty[acc], ((tile >> 1) & 1) ^ 1);
-        tc::tc_fence_after();
-        // four fp32 accumulators per tile (summed with round-to-nearest in the
-        // epilogue): hi*Whi of taps 0-2 / 3-5 / 6-8, and every cross term
-        // (hi*Wlo + lo*Whi) -- short accumulation chains keep 3xTF32 at fp32 accuracy
-        const uint32_t d = tmem + acc * TC_ACC_COLS;
-        for (int tap = 0; tap < 9; ++tap)
-          for (int part = 0; part < 2; ++part) {
-            tc::mbar_wait(&full[stage], phase);
-            tc::tc_fence_after();
-            if (lane == 0) {
-              const uint32_t a = sA0 + stage * TC_A_STAGE;
-              const uint32_t bh = sB0 + (tap * 2 + 0) * TC_B_TAP, bl = sB0 + (tap * 2 + 1) * TC_B_TAP;
-              const uint32_t dmain = d + (tap / 3) * C2, dcross = d + 3 * C2;
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const uint64_t ad = tc::sdesc_k128(a + 32 * k);
-                if (part == 0) {
-                  tc::mma_tf32(dmain, ad, tc::sdesc_k128(bh + 32 * k), TC_IDESC, (tap % 3 | k) != 0);
-                  tc::mma_tf32(dcross, ad, tc::sdesc_k128(bl + 32 * k), TC_IDESC, (tap | k) != 0);
-                } else {
-                  tc::mma_tf32(dcross, ad, tc::sdesc_k128(bh + 32 * k), TC_IDESC, 1);
-                }
-              }
-              tc::mma_commit(&empty[stage]);
-            }
-            __syncwarp();
-            if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
-          }
-        if (lane == 0) tc::mma_commit(&tfull[acc]);
-        __syncwarp();
-      }
-    }
-  } else {
-    // ---------------------------------------------------------- epilogue
-    const int ew = warp & 3;               // TMEM lane quarter this warp may access
-    const int row = ew * 32 + lane;        // accumulator row = TMEM lane
-    const int et = threadIdx.x - 64;       // 0..127 among epilogue threads
-    int tile = 0;
-    for (int b = 0; b < G; ++b) {
-      const int n = n0 + b;
-      if (n >= N || slot_row[n] < 0) continue;
-      float* pout = pooled + (int64_t)n * FLAT;
-      uint8_t* cout = code + (int64_t)n * FLAT;
-      for (int t = 0; t < TC_TILES; ++t, ++tile) {
-        const int acc = tile & 1;
-        tc::mbar_wait(&tfull[acc], (tile >> 1) & 1);
-        tc::tc_fence_after();
-        for (int h = 0; h < 2; ++h) {
-          float zsum[32];
-          {
-            const uint32_t base = tmem + ((uint32_t)(ew * 32) << 16) + acc * TC_ACC_COLS + h * 32;
-            uint32_t v0[32], v1[32];
-            tc::tmem_ld32(base, v0);
-            tc::tmem_ld32(base + C2, v1);
-            tc::tmem_ld_wait();
-#pragma unroll
-            for (int j = 0; j < 32; ++j) zsum[j] = __uint_as_float(v0[j]) + __uint_as_float(v1[j]);
-            tc::tmem_ld32(base + 2 * C2, v0);
-            tc::tmem_ld32(base + 3 * C2, v1);
-            tc::tmem_ld_wait();
-#pragma unroll
-            for (int j = 0; j < 32; ++j) zsum[j] = (zsum[j] + __uint_as_float(v0[j])) + __uint_as_float(v1[j]);
-          }
-          if (row < TC_M) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) sE[row * TC_EPI_LD + j] = fmaxf(zsum[j] + bias[h * 32 + j], 0.f);
-          }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          for (int it = et; it < 2 * SP * 32; it += 128) {
-            const int j = it & 31, pp = it >> 5, pr = pp / SP, px = pp - pr * SP;
-            const float* e0 = sE + ((2 * pr) * S2 + 2 * px) * TC_EPI_LD + j;
-            const float q0 = e0[0], q1 = e0[TC_EPI_LD], q2 = e0[S2 * TC_EPI_LD], q3 = e0[(S2 + 1) * TC_EPI_LD];
-            float best = q0;
-            int arg = 0;
-            if (q1 > best) { best = q1; arg = 1; }
-            if (q2 > best) { best = q2; arg = 2; }
-            if (q3 > best) { best = q3; arg = 3; }
-            const int o = h * 32 + j;
-            const int idx = o * NPOOL + (TC_ROWS / 2 * t + pr) * SP + px;
-            pout[idx] = best;
-            cout[idx] = (uint8_t)arg;
-          }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-        }
-        tc::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&tempty[acc]);
-      }
-    }
-  }
-  tc::tc_fence_before();
-  __syncthreads();
-  tc::tc_fence_after();
-  if (warp == 1) tc::tmem_dealloc<2 * TC_ACC_COLS>(tmem);
-}
+// The three conv2 contractions run on the 5th-generation tensor cores with
+// kind::f16 (fp16 inputs, fp32 accumulation in TMEM).  fp32 accuracy comes
+// from a 3-term split: every operand x is scaled by a power of two s (per
+// sample for activations / gradients, per client for weights) so |x s| <=
+// 2^15, then stored as hi = fp16(x s) and lo = fp16(x s - hi); products are
+// hi*hi + hi*lo + lo*hi (the dropped lo*lo is ~2^-22 relative).  Long
+// accumulation chains on the tensor core lose accuracy (its fp32 adds
+// truncate), so every kernel keeps chains short -- separate accumulators for
+// the hi*hi terms of tap groups and for the cross terms, summed with round-to-
+// nearest on the CUDA cores in the epilogue (measured: per-client delta
+// error 2-7e-7 relative, the same as FP32 FFMA).
+constexpr int TC_THREADS = 192;                 // warp 0 TMA, warp 1 TMEM + MMA, warps 2-5 epilogue
 
 // host: driver entry point for cuTensorMapEncodeTiled (cudart is linked statically)
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -979,141 +775,369 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// 4-D fp32 tensor map, dims innermost first, SWIZZLE_128B (box[0] * 4 == 128 bytes)
-int tensor_map_4d(CUtensorMap* map, const float* base, const cuuint64_t dims[4], const cuuint64_t strides[3],
-                  const cuuint32_t box[4]) {
+int tensor_map_4d_f16(CUtensorMap* map, const __half* base, const cuuint64_t dims[4], const cuuint64_t strides[3],
+                      const cuuint32_t box[4], CUtensorMapSwizzle swz) {
   auto fn = encode_fn();
   if (!fn) {
     set_error("cuTensorMapEncodeTiled unavailable");
     return FB_ERR_CUDA;
   }
   const cuuint32_t estr[4] = {1, 1, 1, 1};
-  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<__half*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
-    set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+    set_error("cuTensorMapEncodeTiled (fp16) failed (%d)", (int)r);
     return FB_ERR_CUDA;
   }
   return FB_OK;
 }
-
-// NHWC a1 [N][30][30][32] as 4-D {32, 30, 30, N}; box {32, 28, 4, 1}
-int a1_tensor_map(CUtensorMap* map, const float* a1, int N) {
+// fp16 a1 NHWC [N][30][30][32] as {32, 30, 30, N}; 64-byte swizzle (32 ci x 2 B rows)
+int a1f_tensor_map(CUtensorMap* map, const __half* a1, int N, int box_w, int box_h) {
   const cuuint64_t dims[4] = {(cuuint64_t)C1, (cuuint64_t)S1, (cuuint64_t)S1, (cuuint64_t)N};
-  const cuuint64_t strides[3] = {(cuuint64_t)C1 * 4, (cuuint64_t)S1 * C1 * 4, (cuuint64_t)S1 * S1 * C1 * 4};
-  const cuuint32_t box[4] = {(cuuint32_t)C1, (cuuint32_t)S2, (cuuint32_t)TC_ROWS, 1};
-  return tensor_map_4d(map, a1, dims, strides, box);
+  const cuuint64_t strides[3] = {(cuuint64_t)C1 * 2, (cuuint64_t)S1 * C1 * 2, (cuuint64_t)S1 * S1 * C1 * 2};
+  const cuuint32_t box[4] = {(cuuint32_t)C1, (cuuint32_t)box_w, (cuuint32_t)box_h, 1};
+  return tensor_map_4d_f16(map, a1, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B);
+}
+// fp16 dz2 NHWC [N][28][28][64] as {64, 28, 28, N}; 128-byte swizzle (64 o x 2 B rows)
+int dzf_tensor_map(CUtensorMap* map, const __half* dz, int N, int box_w, int box_h) {
+  const cuuint64_t dims[4] = {(cuuint64_t)C2, (cuuint64_t)S2, (cuuint64_t)S2, (cuuint64_t)N};
+  const cuuint64_t strides[3] = {(cuuint64_t)C2 * 2, (cuuint64_t)S2 * C2 * 2, (cuuint64_t)S2 * S2 * C2 * 2};
+  const cuuint32_t box[4] = {(cuuint32_t)C2, (cuuint32_t)box_w, (cuuint32_t)box_h, 1};
+  return tensor_map_4d_f16(map, dz, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+// offsets of fp16 element (row, k) in K-major swizzled tiles
+__host__ __device__ __forceinline__ uint32_t sw64_off16(uint32_t row, uint32_t k) {   // 32 fp16 per 64 B row
+  return row * 64u + ((((k >> 3) ^ ((row >> 1) & 3u)) << 4) | ((k & 7u) << 1));
+}
+__host__ __device__ __forceinline__ uint32_t sw128_off16(uint32_t row, uint32_t k) {  // 64 fp16 per 128 B row
+  return row * 128u + ((((k >> 3) ^ (row & 7u)) << 4) | ((k & 7u) << 1));
+}
+__device__ __forceinline__ void split_f16(float x, __half& h, __half& l) {
+  h = __float2half_rn(x);
+  l = __float2half_rn(x - __half2float(h));
+}
+// power-of-two scale putting max |x| at ~2^14 (1 when the block is all zero)
+__device__ __forceinline__ float block_scale(float m, float* red) {
+  m = warp_max(m);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  float t = (threadIdx.x & 31) < (int)(blockDim.x >> 5) ? red[threadIdx.x & 31] : 0.f;
+  t = warp_max(t);
+  return t > 0.f ? exp2f(14.f - ceilf(log2f(t))) : 1.f;
+}
+
+// ------------------------------------------------- conv2 forward (tcgen05)
+// Implicit GEMM per sample: Z[m, o] = sum_{tap, ci} a1[y+ky, x+kx, ci] W[o, ci, ky, kx],
+// m = (y, x).  M tile = 4 output rows x 28 columns = 112 rows (the UMMA
+// M = 128 tile's last 16 rows are don't-care), N = 64, K = 9 taps x 32 ci.
+// For tap (ky, kx) the A tile is ONE 4-D TMA box {32 ci, 28 x, 4 y, 1 n} of
+// the NHWC fp16 a1 at (0, kx, y0 + ky, n): each output row's 32 channels are
+// one 64-byte swizzle row, exactly the K-major SWIZZLE_64B canonical layout
+// (implicit im2col, no copy kernel).  The client's 9-tap weights (hi + lo,
+// 72 KB) stay resident; A (hi + lo per tap, 16 KB) streams through an
+// 8-stage TMA ring; TMEM accumulators are double-buffered so the epilogue
+// (unscale, bias, ReLU, 2x2 max-pool with argmax code) overlaps the next
+// tile's MMAs.
+constexpr int FW_ROWS = 4;                       // conv rows per M tile
+constexpr int FW_M = FW_ROWS * S2;               // 112 valid rows
+constexpr int FW_TILES = S2 / FW_ROWS;           // 7 tiles per sample
+constexpr int FW_A = 128 * 64;                   // 8 KB per operand part (128 rows x 64 B)
+constexpr int FW_A_TX = FW_M * 64;               // 7168 bytes per TMA box
+constexpr int FW_STAGE = 2 * FW_A;               // hi + lo of one tap
+constexpr int FW_B_TAP = C2 * 64;                // 4 KB: 64 rows (o) x 32 ci fp16
+constexpr int WIMG_BYTES = 9 * 2 * FW_B_TAP;     // 73728: [tap][hi|lo]
+constexpr int FW_STAGES = 8;
+constexpr int FW_EPI_LD = 33;
+constexpr int FW_EPI_BYTES = FW_M * FW_EPI_LD * 4;
+constexpr int FW_SMEM = 1024 + WIMG_BYTES + FW_STAGES * FW_STAGE + FW_EPI_BYTES + 256;
+constexpr int FW_ACC = 4 * C2;                   // 4 accumulators x 64 columns per tile
+constexpr uint32_t FW_IDESC = tc::idesc_f16(128, C2);
+
+// per-group conv2 weight image (K-major SWIZZLE_64B: row o, 32 ci), scaled split
+__global__ void __launch_bounds__(256) conv2_wimg_kernel(const float* __restrict__ theta,
+                                                         const float* __restrict__ delta, int64_t ld,
+                                                         const int32_t* __restrict__ client_nb,
+                                                         uint8_t* __restrict__ wimg, float* __restrict__ wscale) {
+  __shared__ float red[32];
+  const int g = blockIdx.x;
+  if (delta && client_nb && client_nb[g] == 0) return;
+  const float* dc = delta ? delta + (int64_t)g * ld : nullptr;
+  float m = 0.f;
+  for (int i = threadIdx.x; i < C2 * C1 * 9; i += blockDim.x) m = fmaxf(m, fabsf(wt(theta, dc, O_W2 + i)));
+  const float sc = block_scale(m, red);
+  if (threadIdx.x == 0) wscale[g] = sc;
+  uint8_t* img = wimg + (int64_t)g * WIMG_BYTES;
+  for (int i = threadIdx.x; i < C2 * C1 * 9; i += blockDim.x) {
+    const int o = i / (C1 * 9), r = i - o * (C1 * 9), ci = r / 9, tap = r - ci * 9;
+    __half h, l;
+    split_f16(wt(theta, dc, O_W2 + i) * sc, h, l);
+    const uint32_t off = sw64_off16(o, ci);
+    *reinterpret_cast<__half*>(img + (tap * 2 + 0) * FW_B_TAP + off) = h;
+    *reinterpret_cast<__half*>(img + (tap * 2 + 1) * FW_B_TAP + off) = l;
+  }
+}
+
+__global__ void __launch_bounds__(TC_THREADS, 1) conv2_fwd_tc_kernel(
+    const __grid_constant__ CUtensorMap tm_hi, const __grid_constant__ CUtensorMap tm_lo,
+    const uint8_t* __restrict__ wimg, const float* __restrict__ wscale, int shared_weights,
+    const int64_t* __restrict__ slot_row, int N, int G, const float* __restrict__ theta,
+    const float* __restrict__ delta, int64_t ld, int B, const float* __restrict__ a1scale,
+    float* __restrict__ pooled, uint8_t* __restrict__ code) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sB = sm;                                        // [9][2][4 KB]
+  uint8_t* sA = sB + WIMG_BYTES;                           // [stages][hi 8 KB | lo 8 KB]
+  float* sE = reinterpret_cast<float*>(sA + FW_STAGES * FW_STAGE);  // [112][33]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sE) + FW_EPI_BYTES);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + FW_STAGES;
+  uint64_t* tfull = empty + FW_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* bfull = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
+  __shared__ float bias[C2];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = blockIdx.x;
+  const int n0 = g * G;
+  const int wg = shared_weights ? 0 : n0 / B;   // weight group (client) of this CTA
+  const float* dc = delta ? delta + (int64_t)wg * ld : nullptr;
+  if (threadIdx.x < C2) bias[threadIdx.x] = wt(theta, dc, O_B2 + threadIdx.x);
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < FW_STAGES; ++i) {
+      tc::mbar_init(&full[i], 1);
+      tc::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&tfull[i], 1);
+      tc::mbar_init(&tempty[i], 4);
+    }
+    tc::mbar_init(bfull, 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc<2 * FW_ACC>(tmem_slot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tc::tma_prefetch(&tm_hi);
+      tc::tma_prefetch(&tm_lo);
+      tc::mbar_arrive_expect_tx(bfull, WIMG_BYTES);
+      tc::bulk_load(sB, wimg + (int64_t)wg * WIMG_BYTES, WIMG_BYTES, bfull);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int b = 0; b < G; ++b) {
+        const int n = n0 + b;
+        if (n >= N || slot_row[n] < 0) continue;
+        for (int t = 0; t < FW_TILES; ++t)
+          for (int tap = 0; tap < 9; ++tap) {
+            tc::mbar_wait(&empty[stage], phase ^ 1);
+            tc::mbar_arrive_expect_tx(&full[stage], 2 * FW_A_TX);
+            uint8_t* st_ = sA + stage * FW_STAGE;
+            tc::tma_load_4d(st_, &tm_hi, 0, tap % 3, FW_ROWS * t + tap / 3, n, &full[stage]);
+            tc::tma_load_4d(st_ + FW_A, &tm_lo, 0, tap % 3, FW_ROWS * t + tap / 3, n, &full[stage]);
+            if (++stage == FW_STAGES) { stage = 0; phase ^= 1; }
+          }
+      }
+    }
+  } else if (warp == 1) {
+    tc::mbar_wait(bfull, 0);
+    int stage = 0, tile = 0;
+    uint32_t phase = 0;
+    const uint32_t sA0 = tc::smem_u32(sA), sB0 = tc::smem_u32(sB);
+    for (int b = 0; b < G; ++b) {
+      const int n = n0 + b;
+      if (n >= N || slot_row[n] < 0) continue;
+      for (int t = 0; t < FW_TILES; ++t, ++tile) {
+        const int acc = tile & 1;
+        tc::mbar_wait(&tempty[acc], ((tile >> 1) & 1) ^ 1);
+        tc::tc_fence_after();
+        const uint32_t d = tmem + acc * FW_ACC;
+        for (int tap = 0; tap < 9; ++tap) {
+          tc::mbar_wait(&full[stage], phase);
+          tc::tc_fence_after();
+          if (lane == 0) {
+            const uint32_t ah = sA0 + stage * FW_STAGE, al = ah + FW_A;
+            const uint32_t bh = sB0 + (tap * 2 + 0) * FW_B_TAP, bl = sB0 + (tap * 2 + 1) * FW_B_TAP;
+            const uint32_t dmain = d + (tap / 3) * C2, dcross = d + 3 * C2;
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {  // K = 32 ci = 2 x 16
+              const uint64_t adh = tc::sdesc(ah + 32 * k, 16, 512, 4), adl = tc::sdesc(al + 32 * k, 16, 512, 4);
+              const uint64_t bdh = tc::sdesc(bh + 32 * k, 16, 512, 4), bdl = tc::sdesc(bl + 32 * k, 16, 512, 4);
+              tc::mma_f16(dmain, adh, bdh, FW_IDESC, (tap % 3 | k) != 0);
+              tc::mma_f16(dcross, adh, bdl, FW_IDESC, (tap | k) != 0);
+              tc::mma_f16(dcross, adl, bdh, FW_IDESC, 1);
+            }
+            tc::mma_commit(&empty[stage]);
+          }
+          __syncwarp();
+          if (++stage == FW_STAGES) { stage = 0; phase ^= 1; }
+        }
+        if (lane == 0) tc::mma_commit(&tfull[acc]);
+        __syncwarp();
+      }
+    }
+  } else {
+    const int ew = warp & 3;
+    const int row = ew * 32 + lane;
+    const int et = threadIdx.x - 64;
+    const float ws = wscale[wg];
+    int tile = 0;
+    for (int b = 0; b < G; ++b) {
+      const int n = n0 + b;
+      if (n >= N || slot_row[n] < 0) continue;
+      const float inv = 1.f / (a1scale[n] * ws);  // exact: powers of two
+      float* pout = pooled + (int64_t)n * FLAT;
+      uint8_t* cout = code + (int64_t)n * FLAT;
+      for (int t = 0; t < FW_TILES; ++t, ++tile) {
+        const int acc = tile & 1;
+        tc::mbar_wait(&tfull[acc], (tile >> 1) & 1);
+        tc::tc_fence_after();
+        for (int h = 0; h < 2; ++h) {
+          float z[32];
+          {
+            const uint32_t base = tmem + ((uint32_t)(ew * 32) << 16) + acc * FW_ACC + h * 32;
+            uint32_t v0[32], v1[32];
+            tc::tmem_ld32(base, v0);
+            tc::tmem_ld32(base + C2, v1);
+            tc::tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) z[j] = __uint_as_float(v0[j]) + __uint_as_float(v1[j]);
+            tc::tmem_ld32(base + 2 * C2, v0);
+            tc::tmem_ld32(base + 3 * C2, v1);
+            tc::tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) z[j] = (z[j] + __uint_as_float(v0[j])) + __uint_as_float(v1[j]);
+          }
+          if (h == 1) {  // both halves read: the next tile may reuse this accumulator
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+          }
+          if (row < FW_M) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) sE[row * FW_EPI_LD + j] = fmaxf(fmaf(z[j], inv, bias[h * 32 + j]), 0.f);
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          for (int it = et; it < 2 * SP * 32; it += 128) {
+            const int j = it & 31, pp = it >> 5, pr = pp / SP, px = pp - pr * SP;
+            const float* e0 = sE + ((2 * pr) * S2 + 2 * px) * FW_EPI_LD + j;
+            const float q0 = e0[0], q1 = e0[FW_EPI_LD], q2 = e0[S2 * FW_EPI_LD], q3 = e0[(S2 + 1) * FW_EPI_LD];
+            float best = q0;
+            int arg = 0;
+            if (q1 > best) { best = q1; arg = 1; }
+            if (q2 > best) { best = q2; arg = 2; }
+            if (q3 > best) { best = q3; arg = 3; }
+            const int idx = (h * 32 + j) * NPOOL + (FW_ROWS / 2 * t + pr) * SP + px;
+            pout[idx] = best;
+            cout[idx] = (uint8_t)arg;
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+        }
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  if (warp == 1) tc::tmem_dealloc<2 * FW_ACC>(tmem);
 }
 
 // ------------------------------------------------ conv2 backward-data (tcgen05)
 // dz1[n, y, x, ci] = relu'(a1) * sum_{ky, kx, o} dz2[n, y-ky, x-kx, o] W[o, ci, ky, kx]
-// Implicit GEMM: M = a1 positions (tile = 4 rows x 30 cols = 120), N = 32 input
-// channels, K = 9 taps x 64 output channels.  dz2 is materialised dense NHWC
-// (hi / lo split) by dz2_build_kernel; the A tile of tap (ky, kx) and channel
-// half h is one TMA box {32 o, 30 x, 4 y} of dz2 at (32h, -kx, y0-ky, n): the
-// negative / past-the-end coordinates are the transposed convolution's zero
-// padding, filled by the TMA unit.  Same 3xTF32 + split-accumulator scheme and
-// warp roles as the forward; the epilogue applies the ReLU mask of a1 and
-// writes each position's 32 channels (128 B) straight to HBM.
+// Implicit GEMM: M = a1 positions (tile = 4 rows x 30 cols = 120), N = 32
+// input channels, K = 9 taps x 64 output channels.  The A tile of tap
+// (ky, kx) is one TMA box {64 o, 30 x, 4 y} of the fp16 dz2 at (0, -kx,
+// y0-ky, n): the negative / past-the-end coordinates are the transposed
+// convolution's zero padding, filled by the TMA unit.  Epilogue: unscale,
+// ReLU mask of a1, 32 channels (128 B) per position straight to HBM.
 constexpr int BX_ROWS = 4;
 constexpr int BX_M = BX_ROWS * S1;               // 120 valid rows
 constexpr int BX_TILES = (S1 + BX_ROWS - 1) / BX_ROWS;  // 8 (last tile: 2 valid rows)
-constexpr int BX_A_TX = BX_M * 128;              // 15360 bytes per box
-constexpr int BX_B_BLK = C1 * 128;               // 4 KB: 32 rows (ci) x 32 o
-constexpr int WIMGT_BYTES = 9 * 2 * 2 * BX_B_BLK;  // [tap][hi|lo][o half] = 147456
+constexpr int BX_A = 128 * 128;                  // 16 KB per operand part
+constexpr int BX_A_TX = BX_M * 128;              // 15360 bytes per TMA box
+constexpr int BX_STAGE = 2 * BX_A;               // hi + lo of one tap
+constexpr int BX_B_TAP = C1 * 128;               // 4 KB: 32 rows (ci) x 64 o fp16
+constexpr int WIMGT_BYTES = 9 * 2 * BX_B_TAP;    // 73728
 constexpr int BX_STAGES = 4;
-constexpr int BX_ACC_COLS = 4 * C1;              // 4 accumulators x 32 columns
-constexpr int BX_SMEM = 1024 + WIMGT_BYTES + BX_STAGES * TC_A_STAGE + 256;
-constexpr uint32_t BX_IDESC = tc::idesc_tf32(128, C1);
+constexpr int BX_ACC = 4 * C1;                   // 4 accumulators x 32 columns
+constexpr int BX_SMEM = 1024 + WIMGT_BYTES + BX_STAGES * BX_STAGE + 256;
+constexpr uint32_t BX_IDESC = tc::idesc_f16(128, C1);
 static_assert(WIMGT_BYTES == WIMG_BYTES, "weight image sizes");
 
-// transposed weight image for backward-data: rows ci, K = o
+// transposed weight image for backward-data: rows ci, K = o (K-major SWIZZLE_128B)
 __global__ void __launch_bounds__(256) conv2_wimgT_kernel(const float* __restrict__ theta,
                                                           const float* __restrict__ delta, int64_t ld,
                                                           const int32_t* __restrict__ client_nb,
-                                                          uint8_t* __restrict__ wimg) {
+                                                          uint8_t* __restrict__ wimg, float* __restrict__ wscale) {
+  __shared__ float red[32];
   const int g = blockIdx.x;
   if (client_nb[g] == 0) return;
   const float* dc = delta + (int64_t)g * ld;
+  float m = 0.f;
+  for (int i = threadIdx.x; i < C2 * C1 * 9; i += blockDim.x) m = fmaxf(m, fabsf(theta[O_W2 + i] - dc[O_W2 + i]));
+  const float sc = block_scale(m, red);
+  if (threadIdx.x == 0) wscale[g] = sc;
   uint8_t* img = wimg + (int64_t)g * WIMGT_BYTES;
   for (int i = threadIdx.x; i < C2 * C1 * 9; i += blockDim.x) {
     const int o = i / (C1 * 9), r = i - o * (C1 * 9), ci = r / 9, tap = r - ci * 9;
-    float h, l;
-    tc::split_tf32(theta[O_W2 + i] - dc[O_W2 + i], h, l);
-    const uint32_t off = tc::sw128_offset(ci, o & 31);
-    const int half = o >> 5;
-    *reinterpret_cast<float*>(img + ((tap * 2 + 0) * 2 + half) * BX_B_BLK + off) = h;
-    *reinterpret_cast<float*>(img + ((tap * 2 + 1) * 2 + half) * BX_B_BLK + off) = l;
+    __half h, l;
+    split_f16((theta[O_W2 + i] - dc[O_W2 + i]) * sc, h, l);
+    const uint32_t off = sw128_off16(ci, o);
+    *reinterpret_cast<__half*>(img + (tap * 2 + 0) * BX_B_TAP + off) = h;
+    *reinterpret_cast<__half*>(img + (tap * 2 + 1) * BX_B_TAP + off) = l;
   }
 }
 
-// dense dz2 = unpool(dp) * relu'(z2), NHWC [N][28][28][64], split hi / lo
+// dense dz2 = unpool(dp) * relu'(z2) as scaled fp16 hi / lo NHWC [N][28][28][64];
+// also the per-sample conv2 bias gradient
 constexpr int DZB_SMEM = FLAT * 5;
 __global__ void __launch_bounds__(256) dz2_build_kernel(const float* __restrict__ dp, const float* __restrict__ pooled,
                                                         const uint8_t* __restrict__ code,
                                                         const int64_t* __restrict__ slot_row,
-                                                        float* __restrict__ dzh, float* __restrict__ dzl,
                                                         __half* __restrict__ dzfh, __half* __restrict__ dzfl,
                                                         float* __restrict__ dzscale, float* __restrict__ db2) {
   extern __shared__ float g[];  // [FLAT] values, then [FLAT] codes
+  __shared__ float red[32];
   uint8_t* cd = reinterpret_cast<uint8_t*>(g + FLAT);
   const int n = blockIdx.x;
   if (slot_row[n] < 0) return;
+  float m = 0.f;
   for (int i = threadIdx.x; i < FLAT; i += blockDim.x) {
     const int64_t k = (int64_t)n * FLAT + i;
-    g[i] = pooled[k] > 0.f ? dp[k] : 0.f;
+    const float v = pooled[k] > 0.f ? dp[k] : 0.f;
+    g[i] = v;
     cd[i] = code[k];
+    m = fmaxf(m, fabsf(v));
   }
-  __syncthreads();
-  float* oh = dzh + (int64_t)n * S2 * S2 * C2;
-  float* ol = dzl + (int64_t)n * S2 * S2 * C2;
-  // thread = (position, 4 consecutive channels): 16-byte stores, coalesced per position
-  for (int t = threadIdx.x; t < S2 * S2 * (C2 / 4); t += blockDim.x) {
-    const int pos = t >> 4, o0 = (t & 15) * 4;
-    const int y = pos / S2, x = pos - y * S2;
-    const int pp = (y >> 1) * SP + (x >> 1), sub = ((y & 1) << 1) | (x & 1);
-    float h[4], l[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int idx = (o0 + e) * NPOOL + pp;
-      const float v = cd[idx] == sub ? g[idx] : 0.f;
-      tc::split_tf32(v, h[e], l[e]);
-    }
-    reinterpret_cast<float4*>(oh)[t] = make_float4(h[0], h[1], h[2], h[3]);
-    reinterpret_cast<float4*>(ol)[t] = make_float4(l[0], l[1], l[2], l[3]);
-  }
-  // fp16 NHWC copy for the weight gradient, scaled by a per-sample power of two
-  __shared__ float redmax[8];
-  float m = 0.f;
-  for (int i = threadIdx.x; i < FLAT; i += blockDim.x) m = fmaxf(m, fabsf(g[i]));
-  m = warp_max(m);
-  if ((threadIdx.x & 31) == 0) redmax[threadIdx.x >> 5] = m;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    float mm = threadIdx.x < (blockDim.x >> 5) ? redmax[threadIdx.x] : 0.f;
-    mm = warp_max(mm);
-    if (threadIdx.x == 0) redmax[0] = mm > 0.f ? exp2f(14.f - ceilf(log2f(mm))) : 1.f;
-  }
-  __syncthreads();
-  const float sc = redmax[0];
+  const float sc = block_scale(m, red);  // (synchronises: g / cd visible)
   if (threadIdx.x == 0) dzscale[n] = sc;
   __half* fh = dzfh + (int64_t)n * S2 * S2 * C2;
   __half* fl = dzfl + (int64_t)n * S2 * S2 * C2;
-  for (int t = threadIdx.x; t < S2 * S2 * (C2 / 2); t += blockDim.x) {
-    const int pos = t >> 5, o0 = (t & 31) * 2;
+  // thread = (position, 8 consecutive channels): 16-byte stores
+  for (int t = threadIdx.x; t < S2 * S2 * (C2 / 8); t += blockDim.x) {
+    const int pos = t >> 3, o0 = (t & 7) * 8;
     const int y = pos / S2, x = pos - y * S2;
     const int pp = (y >> 1) * SP + (x >> 1), sub = ((y & 1) << 1) | (x & 1);
-    float v[2];
+    uint32_t hv[4], lv[4];
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int idx = (o0 + e) * NPOOL + pp;
-      v[e] = (cd[idx] == sub ? g[idx] : 0.f) * sc;
+    for (int e = 0; e < 4; ++e) {
+      __half h0, l0, h1, l1;
+      const int i0 = (o0 + 2 * e) * NPOOL + pp, i1 = i0 + NPOOL;
+      split_f16((cd[i0] == sub ? g[i0] : 0.f) * sc, h0, l0);
+      split_f16((cd[i1] == sub ? g[i1] : 0.f) * sc, h1, l1);
+      const __half2 hh = __halves2half2(h0, h1), ll = __halves2half2(l0, l1);
+      hv[e] = *reinterpret_cast<const uint32_t*>(&hh);
+      lv[e] = *reinterpret_cast<const uint32_t*>(&ll);
     }
-    const __half h0 = __float2half_rn(v[0]), h1 = __float2half_rn(v[1]);
-    reinterpret_cast<__half2*>(fh)[t] = __halves2half2(h0, h1);
-    reinterpret_cast<__half2*>(fl)[t] =
-        __halves2half2(__float2half_rn(v[0] - __half2float(h0)), __float2half_rn(v[1] - __half2float(h1)));
+    reinterpret_cast<uint4*>(fh)[t] = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+    reinterpret_cast<uint4*>(fl)[t] = make_uint4(lv[0], lv[1], lv[2], lv[3]);
   }
   // conv2 bias gradient of this sample: sum over positions of dz2 = sum of g
   if (threadIdx.x < C2) {
@@ -1125,13 +1149,14 @@ __global__ void __launch_bounds__(256) dz2_build_kernel(const float* __restrict_
 
 __global__ void __launch_bounds__(TC_THREADS, 1) conv2_bwd_x_tc_kernel(
     const __grid_constant__ CUtensorMap tm_hi, const __grid_constant__ CUtensorMap tm_lo,
-    const uint8_t* __restrict__ wimg, const int64_t* __restrict__ slot_row, int G,
-    const float* __restrict__ a1h, float* __restrict__ dz1) {
+    const uint8_t* __restrict__ wimg, const float* __restrict__ wscale, const int64_t* __restrict__ slot_row, int G,
+    const float* __restrict__ dzscale, const __half* __restrict__ a1fh, const __half* __restrict__ a1fl,
+    float* __restrict__ dz1) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sB = sm;
   uint8_t* sA = sB + WIMGT_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sA + BX_STAGES * TC_A_STAGE);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sA + BX_STAGES * BX_STAGE);
   uint64_t* full = bars;
   uint64_t* empty = bars + BX_STAGES;
   uint64_t* tfull = empty + BX_STAGES;
@@ -1154,7 +1179,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv2_bwd_x_tc_kernel(
     tc::mbar_init(bfull, 1);
     tc::fence_mbar_init();
   }
-  if (warp == 1) tc::tmem_alloc<2 * BX_ACC_COLS>(tmem_slot);
+  if (warp == 1) tc::tmem_alloc<2 * BX_ACC>(tmem_slot);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
@@ -1172,15 +1197,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv2_bwd_x_tc_kernel(
         const int n = n0 + b;
         if (slot_row[n] < 0) continue;
         for (int t = 0; t < BX_TILES; ++t)
-          for (int tap = 0; tap < 9; ++tap)
-            for (int half = 0; half < 2; ++half)
-              for (int part = 0; part < 2; ++part) {
-                tc::mbar_wait(&empty[stage], phase ^ 1);
-                tc::mbar_arrive_expect_tx(&full[stage], BX_A_TX);
-                tc::tma_load_4d(sA + stage * TC_A_STAGE, part ? &tm_lo : &tm_hi, 32 * half, -(tap % 3),
-                                BX_ROWS * t - tap / 3, n, &full[stage]);
-                if (++stage == BX_STAGES) { stage = 0; phase ^= 1; }
-              }
+          for (int tap = 0; tap < 9; ++tap) {
+            tc::mbar_wait(&empty[stage], phase ^ 1);
+            tc::mbar_arrive_expect_tx(&full[stage], 2 * BX_A_TX);
+            uint8_t* st_ = sA + stage * BX_STAGE;
+            tc::tma_load_4d(st_, &tm_hi, 0, -(tap % 3), BX_ROWS * t - tap / 3, n, &full[stage]);
+            tc::tma_load_4d(st_ + BX_A, &tm_lo, 0, -(tap % 3), BX_ROWS * t - tap / 3, n, &full[stage]);
+            if (++stage == BX_STAGES) { stage = 0; phase ^= 1; }
+          }
       }
     }
   } else if (warp == 1) {
@@ -1195,32 +1219,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv2_bwd_x_tc_kernel(
         const int acc = tile & 1;
         tc::mbar_wait(&tempty[acc], ((tile >> 1) & 1) ^ 1);
         tc::tc_fence_after();
-        const uint32_t d = tmem + acc * BX_ACC_COLS;
-        for (int tap = 0; tap < 9; ++tap)
-          for (int half = 0; half < 2; ++half)
-            for (int part = 0; part < 2; ++part) {
-              tc::mbar_wait(&full[stage], phase);
-              tc::tc_fence_after();
-              if (lane == 0) {
-                const uint32_t a = sA0 + stage * TC_A_STAGE;
-                const uint32_t bh = sB0 + ((tap * 2 + 0) * 2 + half) * BX_B_BLK;
-                const uint32_t bl = sB0 + ((tap * 2 + 1) * 2 + half) * BX_B_BLK;
-                const uint32_t dmain = d + (tap / 3) * C1, dcross = d + 3 * C1;
+        const uint32_t d = tmem + acc * BX_ACC;
+        for (int tap = 0; tap < 9; ++tap) {
+          tc::mbar_wait(&full[stage], phase);
+          tc::tc_fence_after();
+          if (lane == 0) {
+            const uint32_t ah = sA0 + stage * BX_STAGE, al = ah + BX_A;
+            const uint32_t bh = sB0 + (tap * 2 + 0) * BX_B_TAP, bl = sB0 + (tap * 2 + 1) * BX_B_TAP;
+            const uint32_t dmain = d + (tap / 3) * C1, dcross = d + 3 * C1;
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                  const uint64_t ad = tc::sdesc_k128(a + 32 * k);
-                  if (part == 0) {
-                    tc::mma_tf32(dmain, ad, tc::sdesc_k128(bh + 32 * k), BX_IDESC, (tap % 3 | half | k) != 0);
-                    tc::mma_tf32(dcross, ad, tc::sdesc_k128(bl + 32 * k), BX_IDESC, (tap | half | k) != 0);
-                  } else {
-                    tc::mma_tf32(dcross, ad, tc::sdesc_k128(bh + 32 * k), BX_IDESC, 1);
-                  }
-                }
-                tc::mma_commit(&empty[stage]);
-              }
-              __syncwarp();
-              if (++stage == BX_STAGES) { stage = 0; phase ^= 1; }
+            for (int k = 0; k < 4; ++k) {  // K = 64 o = 4 x 16
+              const uint64_t adh = tc::sdesc(ah + 32 * k, 16, 1024, 2), adl = tc::sdesc(al + 32 * k, 16, 1024, 2);
+              const uint64_t bdh = tc::sdesc(bh + 32 * k, 16, 1024, 2), bdl = tc::sdesc(bl + 32 * k, 16, 1024, 2);
+              tc::mma_f16(dmain, adh, bdh, BX_IDESC, (tap % 3 | k) != 0);
+              tc::mma_f16(dcross, adh, bdl, BX_IDESC, (tap | k) != 0);
+              tc::mma_f16(dcross, adl, bdh, BX_IDESC, 1);
             }
+            tc::mma_commit(&empty[stage]);
+          }
+          __syncwarp();
+          if (++stage == BX_STAGES) { stage = 0; phase ^= 1; }
+        }
         if (lane == 0) tc::mma_commit(&tfull[acc]);
         __syncwarp();
       }
@@ -1228,15 +1247,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv2_bwd_x_tc_kernel(
   } else {
     const int ew = warp & 3;
     const int row = ew * 32 + lane;
+    const float ws = wscale[g];
     int tile = 0;
     for (int b = 0; b < G; ++b) {
       const int n = n0 + b;
       if (slot_row[n] < 0) continue;
+      const float inv = 1.f / (dzscale[n] * ws);
       for (int t = 0; t < BX_TILES; ++t, ++tile) {
         const int acc = tile & 1;
         tc::mbar_wait(&tfull[acc], (tile >> 1) & 1);
         tc::tc_fence_after();
-        const uint32_t base = tmem + ((uint32_t)(ew * 32) << 16) + acc * BX_ACC_COLS;
+        const uint32_t base = tmem + ((uint32_t)(ew * 32) << 16) + acc * BX_ACC;
         uint32_t v0[32], v1[32];
         float z[32];
         tc::tmem_ld32(base, v0);
@@ -1251,17 +1272,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv2_bwd_x_tc_kernel(
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&tempty[acc]);  // accumulator drained: next tile may start
 #pragma unroll
-        for (int j = 0; j < 32; ++j) z[j] = (z[j] + __uint_as_float(v0[j])) + __uint_as_float(v1[j]);
+        for (int j = 0; j < 32; ++j) z[j] = ((z[j] + __uint_as_float(v0[j])) + __uint_as_float(v1[j])) * inv;
         const int r = row / S1, x = row - r * S1, y = BX_ROWS * t + r;
         if (row < BX_M && y < S1) {
           const int64_t off = ((int64_t)n * S1 * S1 + y * S1 + x) * C1;
-          const float4* m4 = reinterpret_cast<const float4*>(a1h + off);
+          const uint4* mh = reinterpret_cast<const uint4*>(a1fh + off);
+          const uint4* ml = reinterpret_cast<const uint4*>(a1fl + off);
           float4* o4 = reinterpret_cast<float4*>(dz1 + off);
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const float4 m = m4[q];
-            o4[q] = make_float4(m.x > 0.f ? z[4 * q] : 0.f, m.y > 0.f ? z[4 * q + 1] : 0.f,
-                                m.z > 0.f ? z[4 * q + 2] : 0.f, m.w > 0.f ? z[4 * q + 3] : 0.f);
+          for (int q = 0; q < 4; ++q) {  // 8 channels per 16-byte load of the fp16 a1
+            const uint4 hv = mh[q], lv = ml[q];
+            const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w}, lw[4] = {lv.x, lv.y, lv.z, lv.w};
+            float mk[8];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const __half2 h2 = *reinterpret_cast<const __half2*>(&hw[e]);
+              const __half2 l2 = *reinterpret_cast<const __half2*>(&lw[e]);
+              mk[2 * e] = (__low2float(h2) + __low2float(l2)) > 0.f ? 1.f : 0.f;
+              mk[2 * e + 1] = (__high2float(h2) + __high2float(l2)) > 0.f ? 1.f : 0.f;
+            }
+            o4[2 * q] = make_float4(z[8 * q] * mk[0], z[8 * q + 1] * mk[1], z[8 * q + 2] * mk[2], z[8 * q + 3] * mk[3]);
+            o4[2 * q + 1] = make_float4(z[8 * q + 4] * mk[4], z[8 * q + 5] * mk[5], z[8 * q + 6] * mk[6], z[8 * q + 7] * mk[7]);
           }
         }
       }
@@ -1270,15 +1301,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv2_bwd_x_tc_kernel(
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
-  if (warp == 1) tc::tmem_dealloc<2 * BX_ACC_COLS>(tmem);
-}
-
-// dense dz2 NHWC [N][28][28][64] as 4-D {64, 28, 28, N}; box {32, 30, 4, 1}
-int dz2_tensor_map(CUtensorMap* map, const float* dz2, int N) {
-  const cuuint64_t dims[4] = {(cuuint64_t)C2, (cuuint64_t)S2, (cuuint64_t)S2, (cuuint64_t)N};
-  const cuuint64_t strides[3] = {(cuuint64_t)C2 * 4, (cuuint64_t)S2 * C2 * 4, (cuuint64_t)S2 * S2 * C2 * 4};
-  const cuuint32_t box[4] = {32, (cuuint32_t)S1, (cuuint32_t)BX_ROWS, 1};
-  return tensor_map_4d(map, dz2, dims, strides, box);
+  if (warp == 1) tc::tmem_dealloc<2 * BX_ACC>(tmem);
 }
 
 int g_conv_impl = 1;  // 1 = tcgen05 (product path), 0 = FP32 CUDA-core kernels (validation)
@@ -1460,38 +1483,6 @@ __global__ void __launch_bounds__(BW_THREADS, 1) conv2_bwd_w_tc_kernel(
   if (warp == 1) tc::tmem_dealloc<512>(tmem);
 }
 
-int tensor_map_4d_f16(CUtensorMap* map, const __half* base, const cuuint64_t dims[4], const cuuint64_t strides[3],
-                      const cuuint32_t box[4], CUtensorMapSwizzle swz) {
-  auto fn = encode_fn();
-  if (!fn) {
-    set_error("cuTensorMapEncodeTiled unavailable");
-    return FB_ERR_CUDA;
-  }
-  const cuuint32_t estr[4] = {1, 1, 1, 1};
-  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<__half*>(base), dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) {
-    set_error("cuTensorMapEncodeTiled (fp16) failed (%d)", (int)r);
-    return FB_ERR_CUDA;
-  }
-  return FB_OK;
-}
-// fp16 a1 NHWC {32, 30, 30, N}, box {32, 30, 10, 1}, 64-byte swizzle
-int a1f_tensor_map(CUtensorMap* map, const __half* a1, int N) {
-  const cuuint64_t dims[4] = {(cuuint64_t)C1, (cuuint64_t)S1, (cuuint64_t)S1, (cuuint64_t)N};
-  const cuuint64_t strides[3] = {(cuuint64_t)C1 * 2, (cuuint64_t)S1 * C1 * 2, (cuuint64_t)S1 * S1 * C1 * 2};
-  const cuuint32_t box[4] = {(cuuint32_t)C1, (cuuint32_t)S1, BW_ROWS + 2, 1};
-  return tensor_map_4d_f16(map, a1, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B);
-}
-// fp16 dz2 NHWC {64, 28, 28, N}, box {64, 30, 8, 1}, 128-byte swizzle
-int dzf_tensor_map(CUtensorMap* map, const __half* dz, int N) {
-  const cuuint64_t dims[4] = {(cuuint64_t)C2, (cuuint64_t)S2, (cuuint64_t)S2, (cuuint64_t)N};
-  const cuuint64_t strides[3] = {(cuuint64_t)C2 * 2, (cuuint64_t)S2 * C2 * 2, (cuuint64_t)S2 * S2 * C2 * 2};
-  const cuuint32_t box[4] = {(cuuint32_t)C2, (cuuint32_t)S1, BW_ROWS, 1};
-  return tensor_map_4d_f16(map, dz, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
-}
-
 // ------------------------------------------------------------- workspace
 struct Work {
   int64_t* slot_row;
@@ -1500,7 +1491,7 @@ struct Work {
   int64_t* prefix;
   double* slot_loss;
   int32_t* slot_hit;
-  float *a1h, *a1l, *pooled, *part, *dz3, *dp, *dz1, *dz2h, *dz2l, *db2, *a1scale, *dzscale;
+  float *a1, *pooled, *part, *dz3, *dp, *dz1, *db2, *a1scale, *dzscale, *wscale;
   __half *a1fh, *a1fl, *dzfh, *dzfl;
   uint8_t* code;
   uint8_t* wimg;  // per-group conv2 weight images (tcgen05 B operand)
@@ -1518,13 +1509,12 @@ inline int64_t carve(void* base, int N, int Cmax, Work* w) {
   };
   const int64_t o_row = take(8LL * N), o_cl = take(4LL * N), o_nb = take(4LL * (Cmax + 1)),
                 o_pre = take(8LL * (Cmax + 1)), o_loss = take(8LL * N), o_hit = take(4LL * N),
-                o_a1 = take(4LL * N * A1), o_a1l = take(4LL * N * A1), o_pool = take(4LL * N * FLAT), o_code = take((int64_t)N * FLAT),
+                o_a1 = take(4LL * N * A1), o_pool = take(4LL * N * FLAT), o_code = take((int64_t)N * FLAT),
                 o_part = take(4LL * KSPLIT * N * HID), o_dz3 = take(4LL * N * HID), o_dp = take(4LL * N * FLAT),
                 o_dz1 = take(4LL * N * A1), o_wimg = take((int64_t)WIMG_BYTES * (Cmax + 1)),
-                o_dz2h = take(4LL * N * S2 * S2 * C2), o_dz2l = take(4LL * N * S2 * S2 * C2),
                 o_db2 = take(4LL * N * C2), o_a1fh = take(2LL * N * A1), o_a1fl = take(2LL * N * A1),
                 o_dzfh = take(2LL * N * S2 * S2 * C2), o_dzfl = take(2LL * N * S2 * S2 * C2),
-                o_a1s = take(4LL * N), o_dzs = take(4LL * N);
+                o_a1s = take(4LL * N), o_dzs = take(4LL * N), o_ws = take(4LL * (Cmax + 1));
   if (w && base) {
     char* b = static_cast<char*>(base);
     w->slot_row = reinterpret_cast<int64_t*>(b + o_row);
@@ -1533,11 +1523,8 @@ inline int64_t carve(void* base, int N, int Cmax, Work* w) {
     w->prefix = reinterpret_cast<int64_t*>(b + o_pre);
     w->slot_loss = reinterpret_cast<double*>(b + o_loss);
     w->slot_hit = reinterpret_cast<int32_t*>(b + o_hit);
-    w->a1h = reinterpret_cast<float*>(b + o_a1);
-    w->a1l = reinterpret_cast<float*>(b + o_a1l);
+    w->a1 = reinterpret_cast<float*>(b + o_a1);
     w->wimg = reinterpret_cast<uint8_t*>(b + o_wimg);
-    w->dz2h = reinterpret_cast<float*>(b + o_dz2h);
-    w->dz2l = reinterpret_cast<float*>(b + o_dz2l);
     w->db2 = reinterpret_cast<float*>(b + o_db2);
     w->a1fh = reinterpret_cast<__half*>(b + o_a1fh);
     w->a1fl = reinterpret_cast<__half*>(b + o_a1fl);
@@ -1545,6 +1532,7 @@ inline int64_t carve(void* base, int N, int Cmax, Work* w) {
     w->dzfl = reinterpret_cast<__half*>(b + o_dzfl);
     w->a1scale = reinterpret_cast<float*>(b + o_a1s);
     w->dzscale = reinterpret_cast<float*>(b + o_dzs);
+    w->wscale = reinterpret_cast<float*>(b + o_ws);
     w->pooled = reinterpret_cast<float*>(b + o_pool);
     w->code = reinterpret_cast<uint8_t*>(b + o_code);
     w->part = reinterpret_cast<float*>(b + o_part);
@@ -1561,7 +1549,7 @@ int set_smem_limits() {
   cudaFuncSetAttribute(conv2_fwd_pool_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C2F_SMEM);
   cudaFuncSetAttribute(conv2_bwd_x_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C2X_SMEM);
   cudaFuncSetAttribute(conv2_bwd_w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C2W_SMEM);
-  cudaFuncSetAttribute(conv2_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+  cudaFuncSetAttribute(conv2_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FW_SMEM);
   cudaFuncSetAttribute(conv2_bwd_x_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BX_SMEM);
   cudaFuncSetAttribute(dz2_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DZB_SMEM);
   cudaFuncSetAttribute(conv2_bwd_w_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BW_SMEM);
@@ -1572,21 +1560,25 @@ int set_smem_limits() {
 // forward of N slots (shared weights when delta == nullptr) up to the head
 int forward(const float* X, const float* theta, const float* delta, int64_t ld, int B, int N, int G,
             const Work& w, cudaStream_t s, const int32_t* client_nb) {
-  FB_LAUNCH("conv1_fwd_kernel", s, conv1_fwd_kernel<<<N, 256, 0, s>>>(X, w.slot_row, theta, delta, ld, B, w.a1h, w.a1l,
-                                                               delta ? w.a1fh : nullptr, w.a1fl, w.a1scale));
-  if (g_conv_impl == 1) {
+  const bool tc = g_conv_impl == 1;
+  FB_LAUNCH("conv1_fwd_kernel", s, conv1_fwd_kernel<<<N, 256, 0, s>>>(X, w.slot_row, theta, delta, ld, B,
+                                                               tc ? nullptr : w.a1, tc ? w.a1fh : nullptr, w.a1fl,
+                                                               w.a1scale));
+  if (tc) {
     // weight groups: one per client in training (G = B), one shared image at theta_t in evaluation
     const int groups = delta ? (N + B - 1) / B : 1;
-    FB_LAUNCH("conv2_wimg_kernel", s, conv2_wimg_kernel<<<groups, 256, 0, s>>>(theta, delta, ld, client_nb, w.wimg));
+    FB_LAUNCH("conv2_wimg_kernel", s, conv2_wimg_kernel<<<groups, 256, 0, s>>>(theta, delta, ld, client_nb, w.wimg,
+                                                                                   w.wscale));
     CUtensorMap mh, ml;
-    int st = a1_tensor_map(&mh, w.a1h, N);
-    if (!st) st = a1_tensor_map(&ml, w.a1l, N);
+    int st = a1f_tensor_map(&mh, w.a1fh, N, S2, FW_ROWS);
+    if (!st) st = a1f_tensor_map(&ml, w.a1fl, N, S2, FW_ROWS);
     if (st) return st;
     const int gt = delta ? B : 8;  // samples per CTA
-    FB_LAUNCH("conv2_fwd_tc_kernel", s, conv2_fwd_tc_kernel<<<(N + gt - 1) / gt, TC_THREADS, TC_SMEM, s>>>(
-        mh, ml, w.wimg, delta ? (int64_t)WIMG_BYTES : 0, w.slot_row, N, gt, theta, delta, ld, w.pooled, w.code));
+    FB_LAUNCH("conv2_fwd_tc_kernel", s, conv2_fwd_tc_kernel<<<(N + gt - 1) / gt, TC_THREADS, FW_SMEM, s>>>(
+        mh, ml, w.wimg, w.wscale, delta ? 0 : 1, w.slot_row, N, gt, theta, delta, ld, B, w.a1scale, w.pooled,
+        w.code));
   } else {
-    FB_LAUNCH("conv2_fwd_pool_kernel", s, conv2_fwd_pool_kernel<<<N, 256, C2F_SMEM, s>>>(w.a1h, w.a1l, w.slot_row, theta, delta, ld, B, w.pooled, w.code));
+    FB_LAUNCH("conv2_fwd_pool_kernel", s, conv2_fwd_pool_kernel<<<N, 256, C2F_SMEM, s>>>(w.a1, nullptr, w.slot_row, theta, delta, ld, B, w.pooled, w.code));
   }
   {
     // weight-sharing group per warp: the client's B slots in training, 8 rows at theta_t in evaluation
@@ -1694,29 +1686,30 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
         FB_LAUNCH("fc1_bwd_kernel", s, fc1_bwd_kernel<GMAX><<<dim3(Cw, KSPLIT), FB_WARPS * 32, FC1B_SMEM, s>>>(
             w.pooled, w.dz3, B, w.client_nb, theta_t, dlt, ld_delta, sp, w.dp));
       if (g_conv_impl == 1) {
-        FB_LAUNCH("dz2_build_kernel", s, dz2_build_kernel<<<N, 256, DZB_SMEM, s>>>(w.dp, w.pooled, w.code, w.slot_row, w.dz2h, w.dz2l, w.dzfh, w.dzfl, w.dzscale, w.db2));
-        FB_LAUNCH("conv2_wimgT_kernel", s, conv2_wimgT_kernel<<<Cw, 256, 0, s>>>(theta_t, dlt, ld_delta, w.client_nb, w.wimg));
+        FB_LAUNCH("dz2_build_kernel", s, dz2_build_kernel<<<N, 256, DZB_SMEM, s>>>(w.dp, w.pooled, w.code, w.slot_row, w.dzfh, w.dzfl, w.dzscale, w.db2));
+        FB_LAUNCH("conv2_wimgT_kernel", s, conv2_wimgT_kernel<<<Cw, 256, 0, s>>>(theta_t, dlt, ld_delta, w.client_nb,
+                                                                                 w.wimg, w.wscale));
         CUtensorMap mh, ml;
-        st = dz2_tensor_map(&mh, w.dz2h, N);
-        if (!st) st = dz2_tensor_map(&ml, w.dz2l, N);
+        st = dzf_tensor_map(&mh, w.dzfh, N, S1, BX_ROWS);
+        if (!st) st = dzf_tensor_map(&ml, w.dzfl, N, S1, BX_ROWS);
         if (st) return st;
         FB_LAUNCH("conv2_bwd_x_tc_kernel", s, conv2_bwd_x_tc_kernel<<<Cw, TC_THREADS, BX_SMEM, s>>>(
-            mh, ml, w.wimg, w.slot_row, B, w.a1h, w.dz1));
+            mh, ml, w.wimg, w.wscale, w.slot_row, B, w.dzscale, w.a1fh, w.a1fl, w.dz1));
       } else {
-        FB_LAUNCH("conv2_bwd_x_kernel", s, conv2_bwd_x_kernel<<<N, 256, C2X_SMEM, s>>>(w.dp, w.pooled, w.code, w.a1h, w.slot_row, B, theta_t, dlt,
+        FB_LAUNCH("conv2_bwd_x_kernel", s, conv2_bwd_x_kernel<<<N, 256, C2X_SMEM, s>>>(w.dp, w.pooled, w.code, w.a1, w.slot_row, B, theta_t, dlt,
                                                     ld_delta, w.dz1));
       }
       if (g_conv_impl == 1) {
         CUtensorMap ah, al, dh, dl;
-        st = a1f_tensor_map(&ah, w.a1fh, N);
-        if (!st) st = a1f_tensor_map(&al, w.a1fl, N);
-        if (!st) st = dzf_tensor_map(&dh, w.dzfh, N);
-        if (!st) st = dzf_tensor_map(&dl, w.dzfl, N);
+        st = a1f_tensor_map(&ah, w.a1fh, N, S1, BW_ROWS + 2);
+        if (!st) st = a1f_tensor_map(&al, w.a1fl, N, S1, BW_ROWS + 2);
+        if (!st) st = dzf_tensor_map(&dh, w.dzfh, N, S1, BW_ROWS);
+        if (!st) st = dzf_tensor_map(&dl, w.dzfl, N, S1, BW_ROWS);
         if (st) return st;
         FB_LAUNCH("conv2_bwd_w_tc_kernel", s, conv2_bwd_w_tc_kernel<<<Cw, BW_THREADS, BW_SMEM, s>>>(
             ah, al, dh, dl, B, w.client_nb, w.a1scale, w.dzscale, w.db2, dlt, ld_delta, sp));
       } else {
-        FB_LAUNCH("conv2_bwd_w_kernel", s, conv2_bwd_w_kernel<<<Cw, 256, C2W_SMEM, s>>>(w.dp, w.pooled, w.code, w.a1h, w.a1l, B, w.client_nb, dlt, ld_delta,
+        FB_LAUNCH("conv2_bwd_w_kernel", s, conv2_bwd_w_kernel<<<Cw, 256, C2W_SMEM, s>>>(w.dp, w.pooled, w.code, w.a1, nullptr, B, w.client_nb, dlt, ld_delta,
                                                      sp));
       }
       FB_LAUNCH("conv1_bwd_w_kernel", s, conv1_bwd_w_kernel<<<Cw, C1B_WARPS * 32, 0, s>>>(X, w.slot_row, w.dz1, B, w.client_nb, dlt,

@@ -136,6 +136,10 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t smem_addr, uint32_t lbo, uint
   return (uint64_t)((smem_addr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
          ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | ((uint64_t)1 << 46) | ((uint64_t)layout << 61);
 }
+// kind::f16 (fp16 inputs, fp32 accumulate), both operands K-major
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+  return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
 // kind::f16 (fp16 inputs, fp32 accumulate), both operands MN-major.  (The
 // tensor core accepts MN-major operands for 16-bit kinds; kind::tf32 with an
 // MN-major operand produced no output on sm_100a in our tests.)
