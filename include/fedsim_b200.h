@@ -128,8 +128,14 @@ int fb_local_sgd_mlp_f32(const float* theta_t, int dim, int hidden, int num_clas
  * given max_slots and client count comes from fb_cnn_workspace_bytes.
  * max_steps = max over clients of epochs * ceil(n_c / batch_size).
  * batch_size <= 16.  nonfinite[] is zeroed (non-finite deltas are caught by
- * fb_delta_norm_clip_f32).                                                 */
-int64_t fb_cnn_workspace_bytes(int max_slots, int max_clients);
+ * fb_delta_norm_clip_f32).
+ * hist_steps selects the fc1 update form: 0 = every step reads and rewrites
+ * each client's fc1 delta (6.4 MB); >= max_steps (with hist_steps *
+ * batch_size <= 64) = factored: fc1 runs at theta_t plus a low-rank history
+ * correction and each client's fc1 delta is written once at the end (same
+ * arithmetic, see csrc/cnn.cu "fc1 in factored form").  The workspace must
+ * be sized with the same hist_steps.                                      */
+int64_t fb_cnn_workspace_bytes(int max_slots, int max_clients, int hist_steps);
 /* Validation knob: 1 (default) = conv2 forward on tcgen05 (3xTF32, TMA,
  * TMEM); 0 = the FP32 CUDA-core kernels kept as an independent check.     */
 int fb_cnn_set_conv_impl(int impl);
@@ -142,7 +148,8 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
                          const int32_t* perms, const int64_t* perm_off, int num_clients,
                          int epochs, int batch_size, int max_steps, float lr, float prox_mu,
                          float* delta_out, int64_t ld_delta, int32_t* nonfinite,
-                         int max_slots, void* workspace, int64_t workspace_bytes, void* stream);
+                         int max_slots, int hist_steps, void* workspace, int64_t workspace_bytes,
+                         void* stream);
 
 /* ------------------------------------------------------- data movement
  * Copy each cohort client's contiguous rows (num_rows[c] rows of row_bytes

@@ -15,6 +15,16 @@ MAX_SLOTS = 16384
 EVAL_GROUP = 16
 
 
+# factored fc1 (fb_local_sgd_cnn_f32 hist_steps): history rows per client
+FC1_RANK_MAX = 64
+FACTORED_FC1 = True
+
+
+def hist_steps(max_steps: int, B: int) -> int:
+    """History depth for the factored fc1 update, 0 = dense (too many steps)."""
+    return max_steps if FACTORED_FC1 and 0 < max_steps * B <= FC1_RANK_MAX else 0
+
+
 def _slots(C: int, B: int) -> int:
     per_wave = max(1, min(C, MAX_SLOTS // B))
     return per_wave * B
@@ -28,7 +38,7 @@ def _eval_slots(total_rows: int) -> int:
 def eval_cohort(runner, theta, pop, row_start, num_rows, C, loss, correct, stream, h_num_rows):
     total = int(np.asarray(h_num_rows, dtype=np.int64).sum())
     slots = _eval_slots(total)
-    nbytes = native.call("fb_cnn_workspace_bytes", slots, C)
+    nbytes = native.call("fb_cnn_workspace_bytes", slots, C, 0)
     ws = runner.ws.get("cnn_ws", nbytes)
     native.call("fb_eval_cnn_f32", native.ptr(theta), native.ptr(pop.X), native.ptr(pop.y), native.ptr(row_start),
                 native.ptr(num_rows), C, total, native.ptr(loss), native.ptr(correct), slots, native.ptr(ws),
@@ -41,9 +51,10 @@ def local_sgd_cohort(runner, theta, pop, row_start, num_rows, perms, perm_off, C
     n = np.asarray(h_num_rows, dtype=np.int64)
     max_steps = int((tp.num_epochs * ((n + B - 1) // B)).max()) if len(n) else 0
     slots = _slots(C, B)
-    nbytes = native.call("fb_cnn_workspace_bytes", slots, slots // B)
+    hist = hist_steps(max_steps, B)
+    nbytes = native.call("fb_cnn_workspace_bytes", slots, slots // B, hist)
     ws = runner.ws.get("cnn_ws", nbytes)
     native.call("fb_local_sgd_cnn_f32", native.ptr(theta), native.ptr(pop.X), native.ptr(pop.y),
                 native.ptr(row_start), native.ptr(num_rows), native.ptr(perms), native.ptr(perm_off), C,
                 tp.num_epochs, B, max_steps, float(tp.learning_rate), float(prox_mu), native.ptr(delta),
-                runner.ld, native.ptr(nonfinite), slots, native.ptr(ws), ws.numel(), stream)
+                runner.ld, native.ptr(nonfinite), slots, hist, native.ptr(ws), ws.numel(), stream)

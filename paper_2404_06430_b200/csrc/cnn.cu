@@ -28,6 +28,8 @@
 
 #include <cuda_fp16.h>
 
+#include <algorithm>
+
 #include <cudaTypedefs.h>
 
 namespace fb {
@@ -55,6 +57,36 @@ static_assert(FLAT % KSPLIT == 0, "fc1 split");
 struct Step {
   float lr, mu;
 };
+
+// Factored fc1 (see "fc1 in factored form" below): per-step history of the
+// pooled activations and fc1 output gradients of every slot, the per-step
+// batch sizes, and the per-client Gram matrix of the pooled rows.
+constexpr int FC_RMAX = 64;  // max history rows (steps x batch) per client
+struct Hist {
+  const float* phist;    // [S][N][FLAT] pooled activations (nullptr = dense fc1 updates)
+  int64_t pstride;       // N * FLAT
+  const float* dz3h;     // [S][N][HID] fc1 pre-activation gradients (0 for empty slots)
+  int64_t dstride;       // N * HID
+  const int32_t* nbh;    // [S][cstride] batch size of every client at every step
+  int cstride;
+  float* gram;           // [C][R][R] Gram matrix of the client's pooled rows (row j = s*B + b)
+  int R;
+  float* acoef;          // [C][GMAX][FC_RMAX] history coefficients of the current step's dp
+  int s;                 // current step
+};
+// lr * (1 - lr*mu)^(s-1-sp): weight of step sp's fc1 gradient in delta_s
+__host__ __device__ __forceinline__ float hist_coef(float lr, float mu, int s, int sp) {
+  float c = lr;
+  const float d = 1.f - lr * mu;
+  for (int i = sp + 1; i < s; ++i) c *= d;
+  return c;
+}
+
+// 3-term fp16 split of an already scaled value: x ~ hi + lo
+__device__ __forceinline__ void split_f16(float x, __half& h, __half& l) {
+  h = __float2half_rn(x);
+  l = __float2half_rn(x - __half2float(h));
+}
 
 // weight of the client owning `dc` (nullptr = shared theta_t)
 __device__ __forceinline__ float wt(const float* __restrict__ th, const float* __restrict__ dc, int64_t i) {
@@ -355,8 +387,11 @@ __global__ void __launch_bounds__(HID) head_kernel(const float* __restrict__ par
                                                    const float* __restrict__ theta, float* __restrict__ delta,
                                                    int64_t ld, const int32_t* __restrict__ client_nb, Step st,
                                                    float* __restrict__ dz3, double* __restrict__ slot_loss,
-                                                   int32_t* __restrict__ slot_hit) {
+                                                   int32_t* __restrict__ slot_hit, Hist hs, int nsplit,
+                                                   __half* __restrict__ dzfh, __half* __restrict__ dzfl,
+                                                   float* __restrict__ dzsc) {
   __shared__ float z3[GMAX][HID];
+  __shared__ float dzs[GMAX][HID];
   __shared__ float lg[GMAX][NCLS];
   __shared__ float w2[HID * NCLS + NCLS];
   __shared__ int lab[GMAX];
@@ -373,7 +408,20 @@ __global__ void __launch_bounds__(HID) head_kernel(const float* __restrict__ par
     float z = 0.f;
     if (n < N && slot_row[n] >= 0) {
       z = bf1;
-      for (int s = 0; s < KSPLIT; ++s) z += part[((int64_t)s * N + n) * HID + j];
+      for (int s = 0; s < nsplit; ++s) z += part[((int64_t)s * N + n) * HID + j];
+    }
+    if (train && hs.phist && b < nb) {
+      // factored fc1: z3 -= delta_s p = sum_{sp < s} coef * sum_bp dz3_{sp,bp} (p_{sp,bp} . p)
+      const float* grow = hs.gram + ((int64_t)g * hs.R + hs.s * G + b) * hs.R;
+      float corr = 0.f;
+      for (int sp = 0; sp < hs.s; ++sp) {
+        const int nbp = hs.nbh[sp * hs.cstride + g];
+        const float* dzp = hs.dz3h + sp * hs.dstride + (int64_t)n0 * HID + j;
+        float t = 0.f;
+        for (int bp = 0; bp < nbp; ++bp) t = fmaf(dzp[bp * HID], grow[sp * G + bp], t);
+        corr = fmaf(hist_coef(st.lr, st.mu, hs.s, sp), t, corr);
+      }
+      z -= corr;
     }
     z3[b][j] = z;
   }
@@ -418,7 +466,45 @@ __global__ void __launch_bounds__(HID) head_kernel(const float* __restrict__ par
     for (int q = 0; q < NCLS; ++q) d = fmaf(lg[b][q], w2[j * NCLS + q], d);
     d = z3[b][j] > 0.f ? d : 0.f;
     dz3[(int64_t)(n0 + b) * HID + j] = d;
+    dzs[b][j] = d;
     gb += d;
+  }
+  for (int b = nb; b < G; ++b) dz3[(int64_t)(n0 + b) * HID + j] = 0.f;
+  if (dzfh) {
+    // scaled fp16 hi / lo of dz3 (A operand of the tcgen05 fc1 backward)
+    __shared__ float red[GMAX][HID / 32];
+    for (int b = 0; b < nb; ++b) {
+      const float m = warp_max(fabsf(dzs[b][j]));
+      if ((j & 31) == 0) red[b][j >> 5] = m;
+    }
+    __syncthreads();
+    for (int b = 0; b < nb; ++b) {
+      float m = 0.f;
+#pragma unroll
+      for (int w = 0; w < HID / 32; ++w) m = fmaxf(m, red[b][w]);
+      const float sc = m > 0.f ? exp2f(14.f - ceilf(log2f(m))) : 1.f;
+      if (j == 0) dzsc[n0 + b] = sc;
+      __half h, l;
+      split_f16(dzs[b][j] * sc, h, l);
+      dzfh[(int64_t)(n0 + b) * HID + j] = h;
+      dzfl[(int64_t)(n0 + b) * HID + j] = l;
+    }
+  }
+  if (hs.phist) {
+    // coefficients of the history rows in this step's dp: a[b][j] = coef * (dz3_j . dz3_b)
+    __syncthreads();
+    const int J = hs.s * G;
+    float* ac = hs.acoef + (int64_t)g * GMAX * FC_RMAX;
+    for (int pr = j; pr < nb * J; pr += blockDim.x) {
+      const int b = pr / J, jj = pr - b * J, sp = jj / G, bp = jj - sp * G;
+      float a = 0.f;
+      if (bp < hs.nbh[sp * hs.cstride + g]) {
+        const float* zp = hs.dz3h + sp * hs.dstride + (int64_t)(n0 + bp) * HID;
+        for (int h = 0; h < HID; ++h) a = fmaf(dzs[b][h], zp[h], a);
+        a *= hist_coef(st.lr, st.mu, hs.s, sp);
+      }
+      ac[b * FC_RMAX + jj] = a;
+    }
   }
   // updates: theta <- theta - lr*(g + mu*(theta - theta_t)) == delta += lr*(g - mu*delta)
   {
@@ -742,9 +828,218 @@ __global__ void eval_reduce_kernel(const double* __restrict__ slot_loss, const i
   correct[c] += h;
 }
 
-__global__ void zero_delta_kernel(float* __restrict__ delta, int64_t ld, int C) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < (int64_t)C * ld) delta[i] = 0.f;
+// zero every client's delta row except [skip0, skip1) (float4; ld, skip0, skip1 multiples of 4)
+__global__ void zero_delta_kernel(float* __restrict__ delta, int64_t ld, int C, int64_t skip0, int64_t skip1) {
+  const int64_t q = ld >> 2;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)C * q;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t col = (i % q) << 2;
+    if (col < skip0 || col >= skip1) reinterpret_cast<float4*>(delta)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+// ------------------------------------------------------ fc1 in factored form
+// fc1's SGD update of one step is the rank-nb outer product dz3^T P of the
+// step's batch, so within one local-training run client c's fc1 weights are
+//   W_s = theta_t - delta_s,  delta_s = sum_{s' < s} lr (1 - lr mu)^{s-1-s'} dz3_{s'}^T P_{s'}
+// (exactly the recursion delta += lr*(g - mu*delta) of the dense path).  With
+// at most FC_RMAX history rows per client the run never forms delta_s:
+//   z3 = theta_t p - sum_j coef_j dz3_j (p_j . p)      (fc1_fwd at theta_t + Gram + head)
+//   dp = theta_t dz3 - sum_j coef_j (dz3_j . dz3) p_j  (fc1_bwd_fact)
+// and the client's fc1 delta is written once at the end (fc1_materialize).
+// Per step that replaces the 6.4 MB read (forward) + 12.8 MB read/write
+// (backward) of every client's fc1 delta with the history rows (~0.5 MB per
+// earlier step) and the L2-resident theta_t.
+
+// Gram rows of the current step: gram[c][(s*B + b)][j] = p_{s,b} . p_j for j < (s+1)*B.
+// One CTA per client; 64-wide K chunks of all (s+1)*B rows staged in smem;
+// thread = 2 current rows x 4 history rows, float4 along K.
+constexpr int GR_KC = 64, GR_KP = GR_KC + 4;
+__global__ void __launch_bounds__(128) fc1_gram_kernel(Hist hs, int B) {
+  __shared__ __align__(16) float tile[FC_RMAX][GR_KP];
+  const int c = blockIdx.x, t = threadIdx.x;
+  const int s = hs.s, J = (s + 1) * B;
+  if (hs.nbh[s * hs.cstride + c] == 0) return;
+  const int jq = t & 15, bq = t >> 4;
+  const int rb0 = min(s * B + bq, FC_RMAX - 1), rb1 = min(s * B + bq + 8, FC_RMAX - 1);
+  double acc[2][4] = {};  // per-chunk fp32 partials summed in fp64: the Gram entries are
+                          // long (12544-term) sums of positive products
+  for (int k0 = 0; k0 < FLAT; k0 += GR_KC) {
+    for (int i = t; i < J * (GR_KC / 4); i += blockDim.x) {
+      const int row = i >> 4, c4 = i & 15, sp = row / B, bp = row - sp * B;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (bp < hs.nbh[sp * hs.cstride + c])
+        v = __ldg(reinterpret_cast<const float4*>(hs.phist + sp * hs.pstride + (int64_t)(c * B + bp) * FLAT + k0) + c4);
+      *reinterpret_cast<float4*>(&tile[row][4 * c4]) = v;
+    }
+    __syncthreads();
+    float part[2][4] = {};
+#pragma unroll 4
+    for (int kk = 0; kk < GR_KC; kk += 4) {
+      const float4 x0 = *reinterpret_cast<const float4*>(&tile[rb0][kk]);
+      const float4 x1 = *reinterpret_cast<const float4*>(&tile[rb1][kk]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float4 y = *reinterpret_cast<const float4*>(&tile[jq + 16 * i][kk]);
+        part[0][i] = fmaf(x0.x, y.x, fmaf(x0.y, y.y, fmaf(x0.z, y.z, fmaf(x0.w, y.w, part[0][i]))));
+        part[1][i] = fmaf(x1.x, y.x, fmaf(x1.y, y.y, fmaf(x1.z, y.z, fmaf(x1.w, y.w, part[1][i]))));
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      acc[0][i] += part[0][i];
+      acc[1][i] += part[1][i];
+    }
+    __syncthreads();
+  }
+  float* gr = hs.gram + (int64_t)c * hs.R * hs.R;
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int b = bq + 8 * u;
+    if (b >= B) continue;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int j = jq + 16 * i;
+      if (j < J) gr[(s * B + b) * hs.R + j] = (float)acc[u][i];
+    }
+  }
+}
+
+// dp = dz3 theta_t^T - sum_j a[b][j] p_j.  grid (C, KSPLIT), 4 warps: the
+// theta_t part as in fc1_bwd (warp-streamed 16-row tiles, no delta), staged
+// in smem; then thread = 4 consecutive k of the chunk subtracts the history
+// rows (coalesced float4 reads) and writes dp.
+constexpr int FF_DPB = GMAX * KCHUNK;
+constexpr int FC1F_SMEM = (FB_WARPS * FB_TR * FB_LDW + GMAX * HID + GMAX * FC_RMAX + FF_DPB) * 4;
+
+template <int GM>
+__global__ void __launch_bounds__(FB_WARPS * 32) fc1_bwd_fact_kernel(const float* __restrict__ dz3, int B,
+                                                                      const int32_t* __restrict__ client_nb,
+                                                                      const float* __restrict__ theta, Hist hs,
+                                                                      float* __restrict__ dp) {
+  extern __shared__ float bsm[];
+  const int c = blockIdx.x, split = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nb = client_nb[c];
+  if (nb == 0) return;
+  float* dz = bsm;                                          // [GMAX][HID]
+  float* ac = dz + GMAX * HID;                              // [GMAX][FC_RMAX]
+  float* dpb = ac + GMAX * FC_RMAX;                         // [GMAX][KCHUNK]
+  float* wt_ = dpb + FF_DPB + warp * FB_TR * FB_LDW;        // this warp's [FB_TR][FB_LDW]
+  const int n0 = c * B;
+  const int J = hs.s * B;
+  for (int i = threadIdx.x; i < GM * HID; i += blockDim.x) dz[i] = i < nb * HID ? dz3[(int64_t)n0 * HID + i] : 0.f;
+  for (int i = threadIdx.x; i < nb * J; i += blockDim.x) {
+    const int b = i / J, jj = i - b * J;
+    ac[b * FC_RMAX + jj] = hs.acoef[((int64_t)c * GMAX + b) * FC_RMAX + jj];
+  }
+  __syncthreads();
+  float4 dzr[GM];
+#pragma unroll
+  for (int b = 0; b < GM; ++b) dzr[b] = reinterpret_cast<const float4*>(dz + b * HID)[lane];
+  (void)dzr;
+  constexpr int ROWS_PER_WARP = KCHUNK / FB_WARPS;  // 112
+  const int k0 = split * KCHUNK;
+  const int kw = warp * ROWS_PER_WARP;
+  for (int r0 = 0; r0 < ROWS_PER_WARP; r0 += FB_TR) {
+#pragma unroll 4
+    for (int r = 0; r < FB_TR; ++r) {
+      const int64_t off = O_F1 + (int64_t)(k0 + kw + r0 + r) * HID;
+      const float4 th = __ldg(reinterpret_cast<const float4*>(theta + off) + lane);
+      float* wrow = wt_ + r * FB_LDW + 4 * lane;
+      wrow[0] = th.x; wrow[1] = th.y; wrow[2] = th.z; wrow[3] = th.w;
+    }
+    __syncwarp();
+    {
+      const int r = lane & (FB_TR - 1), bpar = lane >> 4;
+      const float* wr = wt_ + r * FB_LDW;
+      for (int b = bpar; b < nb; b += 2) {
+        const float* zb = dz + b * HID;
+        float s0 = 0.f, s1 = 0.f;
+#pragma unroll 8
+        for (int j = 0; j < HID; j += 2) {
+          s0 = fmaf(zb[j], wr[j], s0);
+          s1 = fmaf(zb[j + 1], wr[j + 1], s1);
+        }
+        dpb[b * KCHUNK + kw + r0 + r] = s0 + s1;
+      }
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  const int t = threadIdx.x;
+  if (t < KCHUNK / 4) {
+    float4 acc[GM];
+#pragma unroll
+    for (int b = 0; b < GM; ++b)
+      acc[b] = b < nb ? *reinterpret_cast<const float4*>(dpb + b * KCHUNK + 4 * t) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int jj = 0; jj < J; ++jj) {
+      const int sp = jj / B, bp = jj - sp * B;
+      if (bp >= hs.nbh[sp * hs.cstride + c]) continue;
+      const float4 p =
+          __ldg(reinterpret_cast<const float4*>(hs.phist + sp * hs.pstride + (int64_t)(n0 + bp) * FLAT + k0) + t);
+#pragma unroll
+      for (int b = 0; b < GM; ++b) {
+        const float a = ac[b * FC_RMAX + jj];
+        acc[b].x = fmaf(-a, p.x, acc[b].x);
+        acc[b].y = fmaf(-a, p.y, acc[b].y);
+        acc[b].z = fmaf(-a, p.z, acc[b].z);
+        acc[b].w = fmaf(-a, p.w, acc[b].w);
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < GM; ++b)
+      if (b < nb) reinterpret_cast<float4*>(dp + (int64_t)(n0 + b) * FLAT + k0)[t] = acc[b];
+  }
+}
+
+// end of the run: delta_fc1[c][k][h] = sum_j coef_j dz3_j[h] p_j[k] over the
+// client's S_c active steps.  grid (C, FLAT/128); CTA = 128 k x 128 h, thread
+// = 8 k x 8 h register tile over the <= FC_RMAX history rows in smem.
+constexpr int FM_K = 128;
+constexpr int FC1M_SMEM = 2 * FC_RMAX * 128 * 4;
+__global__ void __launch_bounds__(256) fc1_materialize_kernel(Hist hs, int S, int B, float lr, float mu,
+                                                              float* __restrict__ delta, int64_t ld) {
+  extern __shared__ __align__(16) float msm[];
+  float* U = msm;                  // [FC_RMAX][HID]
+  float* P = msm + FC_RMAX * HID;  // [FC_RMAX][FM_K]
+  const int c = blockIdx.x, k0 = blockIdx.y * FM_K, t = threadIdx.x;
+  int Sc = 0;
+  while (Sc < S && hs.nbh[Sc * hs.cstride + c] > 0) ++Sc;
+  const int J = Sc * B;
+  for (int i = t; i < J * (HID / 4); i += blockDim.x) {
+    const int j = i / (HID / 4), q = i - j * (HID / 4), sp = j / B, bp = j - sp * B;
+    float4 u = make_float4(0.f, 0.f, 0.f, 0.f), p = u;
+    if (bp < hs.nbh[sp * hs.cstride + c]) {
+      const float cf = hist_coef(lr, mu, Sc, sp);
+      u = __ldg(reinterpret_cast<const float4*>(hs.dz3h + sp * hs.dstride + (int64_t)(c * B + bp) * HID) + q);
+      u.x *= cf; u.y *= cf; u.z *= cf; u.w *= cf;
+      p = __ldg(reinterpret_cast<const float4*>(hs.phist + sp * hs.pstride + (int64_t)(c * B + bp) * FLAT + k0) + q);
+    }
+    reinterpret_cast<float4*>(U + j * HID)[q] = u;
+    reinterpret_cast<float4*>(P + j * FM_K)[q] = p;
+  }
+  __syncthreads();
+  const int hb = t & 15, kb = t >> 4;
+  float acc[8][8] = {};
+  for (int j = 0; j < J; ++j) {
+    const float4 u0 = reinterpret_cast<const float4*>(U + j * HID)[2 * hb];
+    const float4 u1 = reinterpret_cast<const float4*>(U + j * HID)[2 * hb + 1];
+    const float4 p0 = reinterpret_cast<const float4*>(P + j * FM_K)[2 * kb];
+    const float4 p1 = reinterpret_cast<const float4*>(P + j * FM_K)[2 * kb + 1];
+    const float uu[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+    const float pp[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+      for (int b = 0; b < 8; ++b) acc[a][b] = fmaf(pp[a], uu[b], acc[a][b]);
+  }
+  float* out = delta + (int64_t)c * ld + O_F1 + (int64_t)(k0 + 8 * kb) * HID + 8 * hb;
+#pragma unroll
+  for (int a = 0; a < 8; ++a) {
+    reinterpret_cast<float4*>(out + a * HID)[0] = make_float4(acc[a][0], acc[a][1], acc[a][2], acc[a][3]);
+    reinterpret_cast<float4*>(out + a * HID)[1] = make_float4(acc[a][4], acc[a][5], acc[a][6], acc[a][7]);
+  }
 }
 
 
@@ -813,10 +1108,6 @@ __host__ __device__ __forceinline__ uint32_t sw64_off16(uint32_t row, uint32_t k
 }
 __host__ __device__ __forceinline__ uint32_t sw128_off16(uint32_t row, uint32_t k) {  // 64 fp16 per 128 B row
   return row * 128u + ((((k >> 3) ^ (row & 7u)) << 4) | ((k & 7u) << 1));
-}
-__device__ __forceinline__ void split_f16(float x, __half& h, __half& l) {
-  h = __float2half_rn(x);
-  l = __float2half_rn(x - __half2float(h));
 }
 // power-of-two scale putting max |x| at ~2^14 (1 when the block is all zero)
 __device__ __forceinline__ float block_scale(float m, float* red) {
@@ -1025,8 +1316,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv2_fwd_tc_kernel(
             for (int j = 0; j < 32; ++j) sE[row * FW_EPI_LD + j] = fmaxf(fmaf(z[j], inv, bias[h * 32 + j]), 0.f);
           }
           asm volatile("bar.sync 1, 128;" ::: "memory");
+          // consecutive threads -> consecutive pooled positions of one channel (28 contiguous floats)
           for (int it = et; it < 2 * SP * 32; it += 128) {
-            const int j = it & 31, pp = it >> 5, pr = pp / SP, px = pp - pr * SP;
+            const int j = it / (2 * SP), pp = it - j * (2 * SP), pr = pp / SP, px = pp - pr * SP;
             const float* e0 = sE + ((2 * pr) * S2 + 2 * px) * FW_EPI_LD + j;
             const float q0 = e0[0], q1 = e0[FW_EPI_LD], q2 = e0[S2 * FW_EPI_LD], q3 = e0[(S2 + 1) * FW_EPI_LD];
             float best = q0;
@@ -1047,6 +1339,329 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv2_fwd_tc_kernel(
   __syncthreads();
   tc::tc_fence_after();
   if (warp == 1) tc::tmem_dealloc<2 * FW_ACC>(tmem);
+}
+
+// ------------------------------------------------------- fc1 on tcgen05
+// Both fc1 contractions of the factored form run at theta_t, i.e. as plain
+// GEMMs over all slots of the step (kind::f16, 3-term split as above):
+//   forward   part[sp][n][h] = sum_{k in split sp} P[n][k] W[k][h]   (M = slots, N = 128, K = 12544)
+//   backward  dp[n][k]       = sum_h dz3[n][h] W[k][h]              (M = slots, N = 12544, K = 128)
+// One persistent kernel serves both: a work unit is one 128-row M tile x 128
+// output columns over a run of 64-wide K stages; each stage is four TMA
+// boxes (A hi / lo, B hi / lo: 128 rows x 128 B, SWIZZLE_128B) and 12 UMMAs
+// 128x128x16.  The TMEM accumulators (hi*hi and the two cross terms
+// separately) are drained every FT_WIN stages by the epilogue warps into
+// fp32 registers (round-to-nearest), double-buffered so the drain overlaps
+// the next window's MMAs -- the tensor core's own long accumulation chains
+// are not accurate enough for the 12544-long forward sum.  The operands are
+// scaled per row (slot) and per matrix (theta) by powers of two; the
+// epilogue unscales exactly.
+constexpr int FT_KS = 64;                              // K per stage (64 fp16 = one 128 B swizzle row)
+constexpr int FT_PART = 128 * 128;                     // 16 KB: 128 rows x 64 fp16
+constexpr int FT_STAGE = 4 * FT_PART;                  // A hi, A lo, B hi, B lo
+constexpr int FT_STAGES = 3;
+constexpr int FT_WIN = 2;                              // stages per accumulation window
+constexpr int FT_FSPLIT = 14;                          // forward K split: 12544 = 14 x 896
+constexpr int FT_FSTAGES = FLAT / FT_FSPLIT / FT_KS;   // 14 stages per forward unit
+constexpr int FT_BSTAGES = HID / FT_KS;                // 2 stages per backward unit
+constexpr int FT_SMEM = 1024 + FT_STAGES * FT_STAGE + 256;
+constexpr uint32_t FT_IDESC = tc::idesc_f16(128, 128);
+static_assert(FLAT % (FT_FSPLIT * FT_KS) == 0, "fc1 forward split");
+static_assert(FT_FSTAGES % FT_WIN == 0 && FT_BSTAGES % FT_WIN == 0, "fc1 windows");
+static_assert(FLAT % 128 == 0, "fc1 backward N tiles");
+
+// max |W_fc1| (float bits of a non-negative value compare as unsigned)
+__global__ void __launch_bounds__(256) fc1_theta_max_kernel(const float* __restrict__ theta,
+                                                            unsigned* __restrict__ tmax) {
+  float m = 0.f;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)FLAT * HID;
+       i += (int64_t)gridDim.x * blockDim.x)
+    m = fmaxf(m, fabsf(theta[O_F1 + i]));
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0) atomicMax(tmax, __float_as_uint(m));
+}
+
+// fp16 hi / lo images of W_fc1 * tscale: thT[h][k] (forward B operand, K = k)
+// and th[k][h] (backward B operand, K = h); one CTA per 64 rows of k
+__global__ void __launch_bounds__(256) fc1_theta_img_kernel(const float* __restrict__ theta,
+                                                            const unsigned* __restrict__ tmax,
+                                                            __half* __restrict__ thTh, __half* __restrict__ thTl,
+                                                            __half* __restrict__ thh, __half* __restrict__ thl,
+                                                            float* __restrict__ tscale) {
+  __shared__ float tile[64][HID + 1];
+  const float m = __uint_as_float(*tmax);
+  const float sc = m > 0.f ? exp2f(14.f - ceilf(log2f(m))) : 1.f;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *tscale = sc;
+  const int k0 = blockIdx.x * 64;
+  for (int i = threadIdx.x; i < 64 * HID; i += blockDim.x) {
+    const int r = i / HID, h = i - r * HID;
+    const int64_t o = (int64_t)(k0 + r) * HID + h;
+    const float v = theta[O_F1 + o] * sc;
+    tile[r][h] = v;
+    __half hh, ll;
+    split_f16(v, hh, ll);
+    thh[o] = hh;
+    thl[o] = ll;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 64 * HID; i += blockDim.x) {
+    const int h = i / 64, r = i - h * 64;
+    __half hh, ll;
+    split_f16(tile[r][h], hh, ll);
+    thTh[(int64_t)h * FLAT + k0 + r] = hh;
+    thTl[(int64_t)h * FLAT + k0 + r] = ll;
+  }
+}
+
+// pooled activations -> per-slot scaled fp16 hi / lo (forward A operand)
+__global__ void __launch_bounds__(256) pooled_split_kernel(const float* __restrict__ pooled,
+                                                           const int64_t* __restrict__ slot_row,
+                                                           __half* __restrict__ ph, __half* __restrict__ pl,
+                                                           float* __restrict__ pscale) {
+  __shared__ float red[32];
+  const int n = blockIdx.x;
+  if (slot_row[n] < 0) return;
+  const float4* src = reinterpret_cast<const float4*>(pooled + (int64_t)n * FLAT);
+  float m = 0.f;
+  for (int i = threadIdx.x; i < FLAT / 4; i += blockDim.x) {
+    const float4 v = src[i];
+    m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+  }
+  const float sc = block_scale(m, red);
+  if (threadIdx.x == 0) pscale[n] = sc;
+  uint2* dh = reinterpret_cast<uint2*>(ph + (int64_t)n * FLAT);
+  uint2* dl = reinterpret_cast<uint2*>(pl + (int64_t)n * FLAT);
+  for (int i = threadIdx.x; i < FLAT / 4; i += blockDim.x) {
+    const float4 v = src[i];
+    __half h0, l0, h1, l1, h2, l2, h3, l3;
+    split_f16(v.x * sc, h0, l0);
+    split_f16(v.y * sc, h1, l1);
+    split_f16(v.z * sc, h2, l2);
+    split_f16(v.w * sc, h3, l3);
+    const __half2 a = __halves2half2(h0, h1), b = __halves2half2(h2, h3);
+    const __half2 c = __halves2half2(l0, l1), d = __halves2half2(l2, l3);
+    dh[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b));
+    dl[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&c), *reinterpret_cast<const uint32_t*>(&d));
+  }
+}
+
+struct FtArgs {
+  int mode;               // 0 = forward (part), 1 = backward (dp)
+  int N;                  // slots (A rows)
+  int mtiles, units;
+  const float* rscale;    // per-slot operand scale (pooled / dz3)
+  const float* tscale;    // W_fc1 scale
+  float* out;
+};
+
+__global__ void __launch_bounds__(TC_THREADS, 1) fc1_tc_kernel(const __grid_constant__ CUtensorMap ta_h,
+                                                               const __grid_constant__ CUtensorMap ta_l,
+                                                               const __grid_constant__ CUtensorMap tb_h,
+                                                               const __grid_constant__ CUtensorMap tb_l, FtArgs fa) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + FT_STAGES * FT_STAGE);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + FT_STAGES;
+  uint64_t* tfull = empty + FT_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nst = fa.mode == 0 ? FT_FSTAGES : FT_BSTAGES;
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < FT_STAGES; ++i) {
+      tc::mbar_init(&full[i], 1);
+      tc::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&tfull[i], 1);
+      tc::mbar_init(&tempty[i], 4);
+    }
+    tc::fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc<512>(tmem_slot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // unit -> (A row, B row, first K, output)
+  auto unit_geom = [&](int u, int& arow, int& brow, int& kb, int& sp_or_nt) {
+    if (fa.mode == 0) {
+      const int mt = u / FT_FSPLIT;
+      sp_or_nt = u - mt * FT_FSPLIT;
+      arow = mt * 128;
+      brow = 0;
+      kb = sp_or_nt * FT_FSTAGES * FT_KS;
+    } else {
+      const int nt = u / fa.mtiles;
+      sp_or_nt = nt;
+      arow = (u - nt * fa.mtiles) * 128;
+      brow = nt * 128;
+      kb = 0;
+    }
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tc::tma_prefetch(&ta_h);
+      tc::tma_prefetch(&ta_l);
+      tc::tma_prefetch(&tb_h);
+      tc::tma_prefetch(&tb_l);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = blockIdx.x; u < fa.units; u += gridDim.x) {
+        int arow, brow, kb, x;
+        unit_geom(u, arow, brow, kb, x);
+        for (int st_ = 0; st_ < nst; ++st_) {
+          tc::mbar_wait(&empty[stage], phase ^ 1);
+          tc::mbar_arrive_expect_tx(&full[stage], FT_STAGE);
+          uint8_t* d = sm + stage * FT_STAGE;
+          const int k = kb + st_ * FT_KS;
+          tc::tma_load_2d(d, &ta_h, k, arow, &full[stage]);
+          tc::tma_load_2d(d + FT_PART, &ta_l, k, arow, &full[stage]);
+          tc::tma_load_2d(d + 2 * FT_PART, &tb_h, k, brow, &full[stage]);
+          tc::tma_load_2d(d + 3 * FT_PART, &tb_l, k, brow, &full[stage]);
+          if (++stage == FT_STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    int stage = 0, win = 0;
+    uint32_t phase = 0;
+    const uint32_t s0 = tc::smem_u32(sm);
+    for (int u = blockIdx.x; u < fa.units; u += gridDim.x) {
+      for (int st_ = 0; st_ < nst; ++st_) {
+        const int buf = win & 1;
+        if (st_ % FT_WIN == 0) {
+          tc::mbar_wait(&tempty[buf], ((win >> 1) & 1) ^ 1);
+          tc::tc_fence_after();
+        }
+        tc::mbar_wait(&full[stage], phase);
+        tc::tc_fence_after();
+        if (lane == 0) {
+          const uint32_t ah = s0 + stage * FT_STAGE, al = ah + FT_PART, bh = ah + 2 * FT_PART, bl = ah + 3 * FT_PART;
+          const uint32_t dmain = tmem + buf * 256, dcross = dmain + 128;
+#pragma unroll
+          for (int kk = 0; kk < FT_KS / 16; ++kk) {
+            const uint64_t adh = tc::sdesc(ah + 32 * kk, 16, 1024, 2), adl = tc::sdesc(al + 32 * kk, 16, 1024, 2);
+            const uint64_t bdh = tc::sdesc(bh + 32 * kk, 16, 1024, 2), bdl = tc::sdesc(bl + 32 * kk, 16, 1024, 2);
+            const uint32_t acc = (st_ % FT_WIN != 0 || kk != 0) ? 1u : 0u;
+            tc::mma_f16(dmain, adh, bdh, FT_IDESC, acc);
+            tc::mma_f16(dcross, adh, bdl, FT_IDESC, acc);
+            tc::mma_f16(dcross, adl, bdh, FT_IDESC, 1);
+          }
+          tc::mma_commit(&empty[stage]);
+          if (st_ % FT_WIN == FT_WIN - 1) tc::mma_commit(&tfull[buf]);
+        }
+        __syncwarp();
+        if (st_ % FT_WIN == FT_WIN - 1) ++win;
+        if (++stage == FT_STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else {
+    const int ew = warp & 3;
+    const int row = ew * 32 + lane;
+    const float ts = *fa.tscale;
+    int win = 0;
+    for (int u = blockIdx.x; u < fa.units; u += gridDim.x) {
+      int arow, brow, kb, x;
+      unit_geom(u, arow, brow, kb, x);
+      float sum[128];
+#pragma unroll
+      for (int i = 0; i < 128; ++i) sum[i] = 0.f;
+      for (int w = 0; w < nst / FT_WIN; ++w, ++win) {
+        const int buf = win & 1;
+        tc::mbar_wait(&tfull[buf], (win >> 1) & 1);
+        tc::tc_fence_after();
+        const uint32_t base = tmem + ((uint32_t)(ew * 32) << 16) + buf * 256;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint32_t v0[32], v1[32];
+          tc::tmem_ld32(base + q * 32, v0);
+          tc::tmem_ld32(base + 128 + q * 32, v1);
+          tc::tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) sum[q * 32 + i] += __uint_as_float(v0[i]) + __uint_as_float(v1[i]);
+        }
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&tempty[buf]);
+      }
+      const int n = arow + row;
+      if (n < fa.N) {
+        const float inv = 1.f / (fa.rscale[n] * ts);
+        float* o = fa.mode == 0 ? fa.out + ((int64_t)x * fa.N + n) * HID
+                                : fa.out + (int64_t)n * FLAT + (int64_t)x * 128;
+        float4* o4 = reinterpret_cast<float4*>(o);
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          o4[i] = make_float4(sum[4 * i] * inv, sum[4 * i + 1] * inv, sum[4 * i + 2] * inv, sum[4 * i + 3] * inv);
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  if (warp == 1) tc::tmem_dealloc<512>(tmem);
+}
+
+int tensor_map_2d_f16(CUtensorMap* map, const __half* base, int64_t inner, int64_t rows, int box_inner, int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return FB_ERR_CUDA;
+  }
+  const cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)inner * 2};
+  const cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (2-D fp16) failed (%d)", (int)r);
+    return FB_ERR_CUDA;
+  }
+  return FB_OK;
+}
+
+// dp -= sum_j a[b][j] p_j (history part of the factored backward); grid (C, KSPLIT), thread = 4 k
+template <int GM>
+__global__ void __launch_bounds__(KCHUNK / 4) fc1_dp_hist_kernel(int B, const int32_t* __restrict__ client_nb, Hist hs,
+                                                                 float* __restrict__ dp) {
+  __shared__ float ac[GMAX * FC_RMAX];
+  const int c = blockIdx.x, k0 = blockIdx.y * KCHUNK, t = threadIdx.x;
+  const int nb = client_nb[c];
+  const int J = hs.s * B;
+  if (nb == 0 || J == 0) return;
+  for (int i = t; i < nb * J; i += blockDim.x) {
+    const int b = i / J, jj = i - b * J;
+    ac[b * FC_RMAX + jj] = hs.acoef[((int64_t)c * GMAX + b) * FC_RMAX + jj];
+  }
+  __syncthreads();
+  const int n0 = c * B;
+  float4 acc[GM];
+#pragma unroll
+  for (int b = 0; b < GM; ++b)
+    acc[b] = b < nb ? reinterpret_cast<const float4*>(dp + (int64_t)(n0 + b) * FLAT + k0)[t]
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int jj = 0; jj < J; ++jj) {
+    const int sp = jj / B, bp = jj - sp * B;
+    if (bp >= hs.nbh[sp * hs.cstride + c]) continue;
+    const float4 p =
+        __ldg(reinterpret_cast<const float4*>(hs.phist + sp * hs.pstride + (int64_t)(n0 + bp) * FLAT + k0) + t);
+#pragma unroll
+    for (int b = 0; b < GM; ++b) {
+      const float a = ac[b * FC_RMAX + jj];
+      acc[b].x = fmaf(-a, p.x, acc[b].x);
+      acc[b].y = fmaf(-a, p.y, acc[b].y);
+      acc[b].z = fmaf(-a, p.z, acc[b].z);
+      acc[b].w = fmaf(-a, p.w, acc[b].w);
+    }
+  }
+#pragma unroll
+  for (int b = 0; b < GM; ++b)
+    if (b < nb) reinterpret_cast<float4*>(dp + (int64_t)(n0 + b) * FLAT + k0)[t] = acc[b];
 }
 
 // ------------------------------------------------ conv2 backward-data (tcgen05)
@@ -1492,6 +2107,10 @@ struct Work {
   double* slot_loss;
   int32_t* slot_hit;
   float *a1, *pooled, *part, *dz3, *dp, *dz1, *db2, *a1scale, *dzscale, *wscale;
+  float *gram, *acoef;  // factored fc1 (pooled / dz3 / client_nb then hold hist_steps steps)
+  __half *pfh, *pfl, *dz3fh, *dz3fl, *thTh, *thTl, *thh, *thl;  // tcgen05 fc1 operands
+  float *pscale, *dz3scale, *tscale;
+  unsigned* tmax;
   __half *a1fh, *a1fl, *dzfh, *dzfl;
   uint8_t* code;
   uint8_t* wimg;  // per-group conv2 weight images (tcgen05 B operand)
@@ -1500,21 +2119,28 @@ struct Work {
 inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
 
 // layout for N slots and up to Cmax clients
-inline int64_t carve(void* base, int N, int Cmax, Work* w) {
+inline int64_t carve(void* base, int N, int Cmax, int H, Work* w) {
+  const int64_t hs = H > 1 ? H : 1;
   int64_t off = 0;
   auto take = [&](int64_t bytes) {
     const int64_t o = off;
     off += align256(bytes);
     return o;
   };
-  const int64_t o_row = take(8LL * N), o_cl = take(4LL * N), o_nb = take(4LL * (Cmax + 1)),
+  const int64_t o_row = take(8LL * N), o_cl = take(4LL * N), o_nb = take(4LL * hs * (Cmax + 1)),
                 o_pre = take(8LL * (Cmax + 1)), o_loss = take(8LL * N), o_hit = take(4LL * N),
-                o_a1 = take(4LL * N * A1), o_pool = take(4LL * N * FLAT), o_code = take((int64_t)N * FLAT),
-                o_part = take(4LL * KSPLIT * N * HID), o_dz3 = take(4LL * N * HID), o_dp = take(4LL * N * FLAT),
+                o_a1 = take(4LL * N * A1), o_pool = take(4LL * hs * N * FLAT), o_code = take((int64_t)N * FLAT),
+                o_part = take(4LL * KSPLIT * N * HID), o_dz3 = take(4LL * hs * N * HID), o_dp = take(4LL * N * FLAT),
                 o_dz1 = take(4LL * N * A1), o_wimg = take((int64_t)WIMG_BYTES * (Cmax + 1)),
                 o_db2 = take(4LL * N * C2), o_a1fh = take(2LL * N * A1), o_a1fl = take(2LL * N * A1),
                 o_dzfh = take(2LL * N * S2 * S2 * C2), o_dzfl = take(2LL * N * S2 * S2 * C2),
-                o_a1s = take(4LL * N), o_dzs = take(4LL * N), o_ws = take(4LL * (Cmax + 1));
+                o_a1s = take(4LL * N), o_dzs = take(4LL * N), o_ws = take(4LL * (Cmax + 1)),
+                o_gram = H > 0 ? take(4LL * Cmax * FC_RMAX * FC_RMAX) : 0,
+                o_acoef = H > 0 ? take(4LL * Cmax * GMAX * FC_RMAX) : 0,
+                o_pfh = take(2LL * N * FLAT), o_pfl = take(2LL * N * FLAT), o_dz3fh = take(2LL * N * HID),
+                o_dz3fl = take(2LL * N * HID), o_thTh = take(2LL * FLAT * HID), o_thTl = take(2LL * FLAT * HID),
+                o_thh = take(2LL * FLAT * HID), o_thl = take(2LL * FLAT * HID), o_psc = take(4LL * N),
+                o_dz3sc = take(4LL * N), o_tsc = take(16);
   if (w && base) {
     char* b = static_cast<char*>(base);
     w->slot_row = reinterpret_cast<int64_t*>(b + o_row);
@@ -1533,6 +2159,20 @@ inline int64_t carve(void* base, int N, int Cmax, Work* w) {
     w->a1scale = reinterpret_cast<float*>(b + o_a1s);
     w->dzscale = reinterpret_cast<float*>(b + o_dzs);
     w->wscale = reinterpret_cast<float*>(b + o_ws);
+    w->gram = H > 0 ? reinterpret_cast<float*>(b + o_gram) : nullptr;
+    w->acoef = H > 0 ? reinterpret_cast<float*>(b + o_acoef) : nullptr;
+    w->pfh = reinterpret_cast<__half*>(b + o_pfh);
+    w->pfl = reinterpret_cast<__half*>(b + o_pfl);
+    w->dz3fh = reinterpret_cast<__half*>(b + o_dz3fh);
+    w->dz3fl = reinterpret_cast<__half*>(b + o_dz3fl);
+    w->thTh = reinterpret_cast<__half*>(b + o_thTh);
+    w->thTl = reinterpret_cast<__half*>(b + o_thTl);
+    w->thh = reinterpret_cast<__half*>(b + o_thh);
+    w->thl = reinterpret_cast<__half*>(b + o_thl);
+    w->pscale = reinterpret_cast<float*>(b + o_psc);
+    w->dz3scale = reinterpret_cast<float*>(b + o_dz3sc);
+    w->tscale = reinterpret_cast<float*>(b + o_tsc);
+    w->tmax = reinterpret_cast<unsigned*>(b + o_tsc + 4);
     w->pooled = reinterpret_cast<float*>(b + o_pool);
     w->code = reinterpret_cast<uint8_t*>(b + o_code);
     w->part = reinterpret_cast<float*>(b + o_part);
@@ -1552,14 +2192,35 @@ int set_smem_limits() {
   cudaFuncSetAttribute(conv2_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FW_SMEM);
   cudaFuncSetAttribute(conv2_bwd_x_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BX_SMEM);
   cudaFuncSetAttribute(dz2_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DZB_SMEM);
+  cudaFuncSetAttribute(fc1_bwd_fact_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, FC1F_SMEM);
+  cudaFuncSetAttribute(fc1_bwd_fact_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, FC1F_SMEM);
+  cudaFuncSetAttribute(fc1_bwd_fact_kernel<GMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, FC1F_SMEM);
+  cudaFuncSetAttribute(fc1_materialize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FC1M_SMEM);
+  cudaFuncSetAttribute(fc1_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FT_SMEM);
   cudaFuncSetAttribute(conv2_bwd_w_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BW_SMEM);
   done = true;
   return launch_status("cnn: cudaFuncSetAttribute");
 }
 
+// fc1 at theta_t on tcgen05: evaluation and factored training with the tcgen05 conv path
+inline bool fc1_tc(const float* delta, bool shared_fc1) { return g_conv_impl == 1 && (!delta || shared_fc1); }
+
+int g_num_sms = 148;
+
+// fp16 images of theta_t's fc1 weights for the tcgen05 fc1 kernels
+int prep_theta_images(const float* theta, const Work& w, cudaStream_t s) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaMemsetAsync(w.tmax, 0, sizeof(unsigned), s);
+  FB_LAUNCH("fc1_theta_max_kernel", s, fc1_theta_max_kernel<<<296, 256, 0, s>>>(theta, w.tmax));
+  FB_LAUNCH("fc1_theta_img_kernel", s, fc1_theta_img_kernel<<<FLAT / 64, 256, 0, s>>>(theta, w.tmax, w.thTh, w.thTl,
+                                                                                      w.thh, w.thl, w.tscale));
+  return launch_status("cnn fc1 theta images");
+}
+
 // forward of N slots (shared weights when delta == nullptr) up to the head
 int forward(const float* X, const float* theta, const float* delta, int64_t ld, int B, int N, int G,
-            const Work& w, cudaStream_t s, const int32_t* client_nb) {
+            const Work& w, cudaStream_t s, const int32_t* client_nb, bool shared_fc1 = false) {
   const bool tc = g_conv_impl == 1;
   FB_LAUNCH("conv1_fwd_kernel", s, conv1_fwd_kernel<<<N, 256, 0, s>>>(X, w.slot_row, theta, delta, ld, B,
                                                                tc ? nullptr : w.a1, tc ? w.a1fh : nullptr, w.a1fl,
@@ -1580,18 +2241,33 @@ int forward(const float* X, const float* theta, const float* delta, int64_t ld, 
   } else {
     FB_LAUNCH("conv2_fwd_pool_kernel", s, conv2_fwd_pool_kernel<<<N, 256, C2F_SMEM, s>>>(w.a1, nullptr, w.slot_row, theta, delta, ld, B, w.pooled, w.code));
   }
-  {
+  if (fc1_tc(delta, shared_fc1)) {
+    FB_LAUNCH("pooled_split_kernel", s, pooled_split_kernel<<<N, 256, 0, s>>>(w.pooled, w.slot_row, w.pfh, w.pfl,
+                                                                               w.pscale));
+    CUtensorMap ah, al, bh, bl;
+    int st = tensor_map_2d_f16(&ah, w.pfh, FLAT, N, FT_KS, 128);
+    if (!st) st = tensor_map_2d_f16(&al, w.pfl, FLAT, N, FT_KS, 128);
+    if (!st) st = tensor_map_2d_f16(&bh, w.thTh, FLAT, HID, FT_KS, 128);
+    if (!st) st = tensor_map_2d_f16(&bl, w.thTl, FLAT, HID, FT_KS, 128);
+    if (st) return st;
+    FtArgs fa{0, N, (N + 127) / 128, 0, w.pscale, w.tscale, w.part};
+    fa.units = fa.mtiles * FT_FSPLIT;
+    FB_LAUNCH("fc1_tc_kernel", s, fc1_tc_kernel<<<std::min(fa.units, g_num_sms), TC_THREADS, FT_SMEM, s>>>(
+                                      ah, al, bh, bl, fa));
+  } else {
     // weight-sharing group per warp: the client's B slots in training, 8 rows at theta_t in evaluation
-    const int gf = delta ? G : 8;
+    // (factored fc1: every slot at theta_t, the history correction is applied in the head)
+    const float* fd = shared_fc1 ? nullptr : delta;
+    const int gf = fd ? G : 8;
     const dim3 grid((N + gf - 1) / gf, KSPLIT);
     if (gf <= 8)
-      FB_LAUNCH("fc1_fwd_kernel", s, fc1_fwd_kernel<8><<<grid, 32, 0, s>>>(w.pooled, w.slot_row, N, gf, theta, delta, ld, w.part));
+      FB_LAUNCH("fc1_fwd_kernel", s, fc1_fwd_kernel<8><<<grid, 32, 0, s>>>(w.pooled, w.slot_row, N, gf, theta, fd, ld, w.part));
     else if (gf <= 10)
-      FB_LAUNCH("fc1_fwd_kernel", s, fc1_fwd_kernel<10><<<grid, 32, 0, s>>>(w.pooled, w.slot_row, N, gf, theta, delta, ld, w.part));
+      FB_LAUNCH("fc1_fwd_kernel", s, fc1_fwd_kernel<10><<<grid, 32, 0, s>>>(w.pooled, w.slot_row, N, gf, theta, fd, ld, w.part));
     else if (gf <= 12)
-      FB_LAUNCH("fc1_fwd_kernel", s, fc1_fwd_kernel<12><<<grid, 32, 0, s>>>(w.pooled, w.slot_row, N, gf, theta, delta, ld, w.part));
+      FB_LAUNCH("fc1_fwd_kernel", s, fc1_fwd_kernel<12><<<grid, 32, 0, s>>>(w.pooled, w.slot_row, N, gf, theta, fd, ld, w.part));
     else
-      FB_LAUNCH("fc1_fwd_kernel", s, fc1_fwd_kernel<GMAX><<<grid, 32, 0, s>>>(w.pooled, w.slot_row, N, gf, theta, delta, ld, w.part));
+      FB_LAUNCH("fc1_fwd_kernel", s, fc1_fwd_kernel<GMAX><<<grid, 32, 0, s>>>(w.pooled, w.slot_row, N, gf, theta, fd, ld, w.part));
   }
   return launch_status("cnn forward");
 }
@@ -1609,32 +2285,39 @@ int fb_cnn_set_conv_impl(int impl) {
   return FB_OK;
 }
 
-int64_t fb_cnn_workspace_bytes(int max_slots, int max_clients) {
-  return carve(nullptr, max_slots, max_clients, nullptr);
+int64_t fb_cnn_workspace_bytes(int max_slots, int max_clients, int hist_steps) {
+  if (max_slots < 0 || max_clients < 0 || hist_steps < 0) return -1;
+  return carve(nullptr, max_slots, max_clients, hist_steps, nullptr);
 }
 
 int fb_eval_cnn_f32(const float* theta, const float* X, const int32_t* y, const int64_t* row_start,
                     const int32_t* num_rows, int num_clients, int64_t total_rows, double* loss_sum,
                     int32_t* correct, int max_slots, void* workspace, int64_t workspace_bytes, void* stream) {
   FB_REQUIRE(num_clients >= 0 && total_rows >= 0 && max_slots >= GMAX, "eval_cnn: bad arguments");
-  FB_REQUIRE(workspace_bytes >= carve(nullptr, max_slots, num_clients, nullptr), "eval_cnn: workspace too small");
+  FB_REQUIRE(workspace_bytes >= carve(nullptr, max_slots, num_clients, 0, nullptr), "eval_cnn: workspace too small");
   if (num_clients == 0) return FB_OK;
   int st = set_smem_limits();
   if (st) return st;
   cudaStream_t s = fb::as_stream(stream);
   Work w;
-  carve(workspace, max_slots, num_clients, &w);
+  carve(workspace, max_slots, num_clients, 0, &w);
   const int N = (max_slots / GMAX) * GMAX;
   cudaMemsetAsync(loss_sum, 0, sizeof(double) * num_clients, s);
   cudaMemsetAsync(correct, 0, sizeof(int32_t) * num_clients, s);
   FB_LAUNCH("prefix_kernel", s, prefix_kernel<<<1, 1, 0, s>>>(num_rows, num_clients, w.prefix));
+  const bool tcf = fc1_tc(nullptr, false);
+  if (tcf) {
+    st = prep_theta_images(theta, w, s);
+    if (st) return st;
+  }
   for (int64_t r0 = 0; r0 < total_rows; r0 += N) {
     FB_LAUNCH("eval_slots_kernel", s, eval_slots_kernel<<<(N + 255) / 256, 256, 0, s>>>(r0, N, total_rows, w.prefix, num_clients, row_start,
                                                       w.slot_row, w.slot_client));
     st = forward(X, theta, nullptr, 0, 1, N, GMAX, w, s, nullptr);
     if (st) return st;
     FB_LAUNCH("head_kernel", s, head_kernel<<<N / GMAX, HID, 0, s>>>(w.part, w.slot_row, N, GMAX, y, theta, nullptr, 0, nullptr, Step{0, 0},
-                                         nullptr, w.slot_loss, w.slot_hit));
+                                         nullptr, w.slot_loss, w.slot_hit, Hist{}, tcf ? FT_FSPLIT : KSPLIT,
+                                         nullptr, nullptr, nullptr));
     FB_LAUNCH("eval_reduce_kernel", s, eval_reduce_kernel<<<(num_clients + 127) / 128, 128, 0, s>>>(w.slot_loss, w.slot_hit, w.slot_client, N, r0,
                                                                  w.prefix, num_clients, loss_sum, correct));
     st = fb::launch_status("eval_cnn");
@@ -1646,77 +2329,144 @@ int fb_eval_cnn_f32(const float* theta, const float* X, const int32_t* y, const 
 int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y, const int64_t* row_start,
                          const int32_t* num_rows, const int32_t* perms, const int64_t* perm_off, int num_clients,
                          int epochs, int batch_size, int max_steps, float lr, float prox_mu, float* delta_out,
-                         int64_t ld_delta, int32_t* nonfinite, int max_slots, void* workspace,
+                         int64_t ld_delta, int32_t* nonfinite, int max_slots, int hist_steps, void* workspace,
                          int64_t workspace_bytes, void* stream) {
-  FB_REQUIRE(num_clients >= 0 && epochs >= 0 && batch_size >= 1 && max_steps >= 0, "local_sgd_cnn: bad arguments");
+  FB_REQUIRE(num_clients >= 0 && epochs >= 0 && batch_size >= 1 && max_steps >= 0 && hist_steps >= 0,
+             "local_sgd_cnn: bad arguments");
   FB_UNSUPPORTED(batch_size <= GMAX, "local_sgd_cnn: batch_size %d > %d", batch_size, GMAX);
   FB_REQUIRE(ld_delta >= D && (ld_delta & 3) == 0, "local_sgd_cnn: ld_delta must be >= D and a multiple of 4");
   FB_REQUIRE(max_slots >= batch_size, "local_sgd_cnn: max_slots < batch_size");
+  FB_REQUIRE(hist_steps == 0 || (hist_steps >= max_steps && hist_steps * batch_size <= FC_RMAX),
+             "local_sgd_cnn: hist_steps must be 0 (dense fc1) or >= max_steps with hist_steps*batch_size <= %d",
+             FC_RMAX);
   const int per = max_slots / batch_size;  // clients per wave
-  FB_REQUIRE(workspace_bytes >= carve(nullptr, max_slots, per, nullptr), "local_sgd_cnn: workspace too small");
+  FB_REQUIRE(workspace_bytes >= carve(nullptr, max_slots, per, hist_steps, nullptr),
+             "local_sgd_cnn: workspace too small");
   if (num_clients == 0) return FB_OK;
   int st = set_smem_limits();
   if (st) return st;
   cudaStream_t s = fb::as_stream(stream);
   Work w;
-  carve(workspace, max_slots, per, &w);
-  const int64_t tot = (int64_t)num_clients * ld_delta;
-  FB_LAUNCH("zero_delta_kernel", s, zero_delta_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(delta_out, ld_delta, num_clients));
+  carve(workspace, max_slots, per, hist_steps, &w);
+  const bool fact = hist_steps > 0;
+  const int64_t tot4 = (int64_t)num_clients * (ld_delta / 4);
+  // factored fc1: the fc1 weight block is written whole by fc1_materialize
+  FB_LAUNCH("zero_delta_kernel", s, zero_delta_kernel<<<(unsigned)std::min<int64_t>((tot4 + 255) / 256, 148 * 16), 256, 0, s>>>(
+                                        delta_out, ld_delta, num_clients, fact ? O_F1 : 0, fact ? O_BF1 : 0));
   cudaMemsetAsync(nonfinite, 0, sizeof(int32_t) * num_clients, s);
   const Step sp{lr, prox_mu};
   const int B = batch_size;
+  const bool tcf = fc1_tc(delta_out, fact);
+  if (tcf) {
+    st = prep_theta_images(theta_t, w, s);
+    if (st) return st;
+  }
   for (int c0 = 0; c0 < num_clients; c0 += per) {
     const int Cw = min(per, num_clients - c0);
     const int N = Cw * B;
     float* dlt = delta_out + (int64_t)c0 * ld_delta;
+    Hist hs{};
+    if (fact) {
+      hs.phist = w.pooled;
+      hs.pstride = (int64_t)N * FLAT;
+      hs.dz3h = w.dz3;
+      hs.dstride = (int64_t)N * HID;
+      hs.nbh = w.client_nb;
+      hs.cstride = per + 1;
+      hs.gram = w.gram;
+      hs.R = FC_RMAX;
+      hs.acoef = w.acoef;
+    }
     for (int step = 0; step < max_steps; ++step) {
+      Work ws = w;  // this step's slices of the history buffers
+      if (fact) {
+        ws.pooled = w.pooled + step * hs.pstride;
+        ws.dz3 = w.dz3 + step * hs.dstride;
+        ws.client_nb = w.client_nb + step * hs.cstride;
+        hs.s = step;
+      }
       FB_LAUNCH("train_slots_kernel", s, train_slots_kernel<<<(N + 255) / 256, 256, 0, s>>>(step, row_start + c0, num_rows + c0, perms, perm_off + c0,
-                                                        Cw, epochs, B, w.slot_row, w.client_nb));
-      st = forward(X, theta_t, dlt, ld_delta, B, N, B, w, s, w.client_nb);
+                                                        Cw, epochs, B, ws.slot_row, ws.client_nb));
+      st = forward(X, theta_t, dlt, ld_delta, B, N, B, ws, s, ws.client_nb, fact);
       if (st) return st;
-      FB_LAUNCH("head_kernel", s, head_kernel<<<Cw, HID, 0, s>>>(w.part, w.slot_row, N, B, y, theta_t, dlt, ld_delta, w.client_nb, sp, w.dz3,
-                                     nullptr, nullptr));
-      if (B <= 8)
+      if (fact) FB_LAUNCH("fc1_gram_kernel", s, fc1_gram_kernel<<<Cw, 128, 0, s>>>(hs, B));
+      FB_LAUNCH("head_kernel", s, head_kernel<<<Cw, HID, 0, s>>>(ws.part, ws.slot_row, N, B, y, theta_t, dlt, ld_delta, ws.client_nb, sp, ws.dz3,
+                                     nullptr, nullptr, hs, tcf ? FT_FSPLIT : KSPLIT, tcf ? ws.dz3fh : nullptr,
+                                     ws.dz3fl, ws.dz3scale));
+      if (tcf) {
+        CUtensorMap ah, al, bh, bl;
+        st = tensor_map_2d_f16(&ah, ws.dz3fh, HID, N, FT_KS, 128);
+        if (!st) st = tensor_map_2d_f16(&al, ws.dz3fl, HID, N, FT_KS, 128);
+        if (!st) st = tensor_map_2d_f16(&bh, ws.thh, HID, FLAT, FT_KS, 128);
+        if (!st) st = tensor_map_2d_f16(&bl, ws.thl, HID, FLAT, FT_KS, 128);
+        if (st) return st;
+        FtArgs fa{1, N, (N + 127) / 128, 0, ws.dz3scale, ws.tscale, ws.dp};
+        fa.units = fa.mtiles * (FLAT / 128);
+        FB_LAUNCH("fc1_tc_kernel", s, fc1_tc_kernel<<<std::min(fa.units, g_num_sms), TC_THREADS, FT_SMEM, s>>>(
+                                          ah, al, bh, bl, fa));
+        if (step > 0) {
+          if (B <= 8)
+            FB_LAUNCH("fc1_dp_hist_kernel", s, fc1_dp_hist_kernel<8><<<dim3(Cw, KSPLIT), KCHUNK / 4, 0, s>>>(
+                                                  B, ws.client_nb, hs, ws.dp));
+          else if (B <= 10)
+            FB_LAUNCH("fc1_dp_hist_kernel", s, fc1_dp_hist_kernel<10><<<dim3(Cw, KSPLIT), KCHUNK / 4, 0, s>>>(
+                                                  B, ws.client_nb, hs, ws.dp));
+          else
+            FB_LAUNCH("fc1_dp_hist_kernel", s, fc1_dp_hist_kernel<GMAX><<<dim3(Cw, KSPLIT), KCHUNK / 4, 0, s>>>(
+                                                  B, ws.client_nb, hs, ws.dp));
+        }
+      } else if (fact) {
+        if (B <= 8)
+          FB_LAUNCH("fc1_bwd_fact_kernel", s, fc1_bwd_fact_kernel<8><<<dim3(Cw, KSPLIT), FB_WARPS * 32, FC1F_SMEM, s>>>(
+              ws.dz3, B, ws.client_nb, theta_t, hs, ws.dp));
+        else if (B <= 10)
+          FB_LAUNCH("fc1_bwd_fact_kernel", s, fc1_bwd_fact_kernel<10><<<dim3(Cw, KSPLIT), FB_WARPS * 32, FC1F_SMEM, s>>>(
+              ws.dz3, B, ws.client_nb, theta_t, hs, ws.dp));
+        else
+          FB_LAUNCH("fc1_bwd_fact_kernel", s, fc1_bwd_fact_kernel<GMAX><<<dim3(Cw, KSPLIT), FB_WARPS * 32, FC1F_SMEM, s>>>(
+              ws.dz3, B, ws.client_nb, theta_t, hs, ws.dp));
+      } else if (B <= 8) {
         FB_LAUNCH("fc1_bwd_kernel", s, fc1_bwd_kernel<8><<<dim3(Cw, KSPLIT), FB_WARPS * 32, FC1B_SMEM, s>>>(
-            w.pooled, w.dz3, B, w.client_nb, theta_t, dlt, ld_delta, sp, w.dp));
-      else if (B <= 10)
+            ws.pooled, ws.dz3, B, ws.client_nb, theta_t, dlt, ld_delta, sp, ws.dp));
+      } else if (B <= 10) {
         FB_LAUNCH("fc1_bwd_kernel", s, fc1_bwd_kernel<10><<<dim3(Cw, KSPLIT), FB_WARPS * 32, FC1B_SMEM, s>>>(
-            w.pooled, w.dz3, B, w.client_nb, theta_t, dlt, ld_delta, sp, w.dp));
-      else
+            ws.pooled, ws.dz3, B, ws.client_nb, theta_t, dlt, ld_delta, sp, ws.dp));
+      } else {
         FB_LAUNCH("fc1_bwd_kernel", s, fc1_bwd_kernel<GMAX><<<dim3(Cw, KSPLIT), FB_WARPS * 32, FC1B_SMEM, s>>>(
-            w.pooled, w.dz3, B, w.client_nb, theta_t, dlt, ld_delta, sp, w.dp));
+            ws.pooled, ws.dz3, B, ws.client_nb, theta_t, dlt, ld_delta, sp, ws.dp));
+      }
       if (g_conv_impl == 1) {
-        FB_LAUNCH("dz2_build_kernel", s, dz2_build_kernel<<<N, 256, DZB_SMEM, s>>>(w.dp, w.pooled, w.code, w.slot_row, w.dzfh, w.dzfl, w.dzscale, w.db2));
-        FB_LAUNCH("conv2_wimgT_kernel", s, conv2_wimgT_kernel<<<Cw, 256, 0, s>>>(theta_t, dlt, ld_delta, w.client_nb,
-                                                                                 w.wimg, w.wscale));
+        FB_LAUNCH("dz2_build_kernel", s, dz2_build_kernel<<<N, 256, DZB_SMEM, s>>>(ws.dp, ws.pooled, ws.code, ws.slot_row, ws.dzfh, ws.dzfl, ws.dzscale, ws.db2));
+        FB_LAUNCH("conv2_wimgT_kernel", s, conv2_wimgT_kernel<<<Cw, 256, 0, s>>>(theta_t, dlt, ld_delta, ws.client_nb,
+                                                                                 ws.wimg, ws.wscale));
         CUtensorMap mh, ml;
-        st = dzf_tensor_map(&mh, w.dzfh, N, S1, BX_ROWS);
-        if (!st) st = dzf_tensor_map(&ml, w.dzfl, N, S1, BX_ROWS);
+        st = dzf_tensor_map(&mh, ws.dzfh, N, S1, BX_ROWS);
+        if (!st) st = dzf_tensor_map(&ml, ws.dzfl, N, S1, BX_ROWS);
         if (st) return st;
         FB_LAUNCH("conv2_bwd_x_tc_kernel", s, conv2_bwd_x_tc_kernel<<<Cw, TC_THREADS, BX_SMEM, s>>>(
-            mh, ml, w.wimg, w.wscale, w.slot_row, B, w.dzscale, w.a1fh, w.a1fl, w.dz1));
-      } else {
-        FB_LAUNCH("conv2_bwd_x_kernel", s, conv2_bwd_x_kernel<<<N, 256, C2X_SMEM, s>>>(w.dp, w.pooled, w.code, w.a1, w.slot_row, B, theta_t, dlt,
-                                                    ld_delta, w.dz1));
-      }
-      if (g_conv_impl == 1) {
+            mh, ml, ws.wimg, ws.wscale, ws.slot_row, B, ws.dzscale, ws.a1fh, ws.a1fl, ws.dz1));
         CUtensorMap ah, al, dh, dl;
-        st = a1f_tensor_map(&ah, w.a1fh, N, S1, BW_ROWS + 2);
-        if (!st) st = a1f_tensor_map(&al, w.a1fl, N, S1, BW_ROWS + 2);
-        if (!st) st = dzf_tensor_map(&dh, w.dzfh, N, S1, BW_ROWS);
-        if (!st) st = dzf_tensor_map(&dl, w.dzfl, N, S1, BW_ROWS);
+        st = a1f_tensor_map(&ah, ws.a1fh, N, S1, BW_ROWS + 2);
+        if (!st) st = a1f_tensor_map(&al, ws.a1fl, N, S1, BW_ROWS + 2);
+        if (!st) st = dzf_tensor_map(&dh, ws.dzfh, N, S1, BW_ROWS);
+        if (!st) st = dzf_tensor_map(&dl, ws.dzfl, N, S1, BW_ROWS);
         if (st) return st;
         FB_LAUNCH("conv2_bwd_w_tc_kernel", s, conv2_bwd_w_tc_kernel<<<Cw, BW_THREADS, BW_SMEM, s>>>(
-            ah, al, dh, dl, B, w.client_nb, w.a1scale, w.dzscale, w.db2, dlt, ld_delta, sp));
+            ah, al, dh, dl, B, ws.client_nb, ws.a1scale, ws.dzscale, ws.db2, dlt, ld_delta, sp));
       } else {
-        FB_LAUNCH("conv2_bwd_w_kernel", s, conv2_bwd_w_kernel<<<Cw, 256, C2W_SMEM, s>>>(w.dp, w.pooled, w.code, w.a1, nullptr, B, w.client_nb, dlt, ld_delta,
+        FB_LAUNCH("conv2_bwd_x_kernel", s, conv2_bwd_x_kernel<<<N, 256, C2X_SMEM, s>>>(ws.dp, ws.pooled, ws.code, ws.a1, ws.slot_row, B, theta_t, dlt,
+                                                    ld_delta, ws.dz1));
+        FB_LAUNCH("conv2_bwd_w_kernel", s, conv2_bwd_w_kernel<<<Cw, 256, C2W_SMEM, s>>>(ws.dp, ws.pooled, ws.code, ws.a1, nullptr, B, ws.client_nb, dlt, ld_delta,
                                                      sp));
       }
-      FB_LAUNCH("conv1_bwd_w_kernel", s, conv1_bwd_w_kernel<<<Cw, C1B_WARPS * 32, 0, s>>>(X, w.slot_row, w.dz1, B, w.client_nb, dlt,
+      FB_LAUNCH("conv1_bwd_w_kernel", s, conv1_bwd_w_kernel<<<Cw, C1B_WARPS * 32, 0, s>>>(X, ws.slot_row, ws.dz1, B, ws.client_nb, dlt,
                                                                        ld_delta, sp));
       st = fb::launch_status("local_sgd_cnn step");
       if (st) return st;
     }
+    if (fact)
+      FB_LAUNCH("fc1_materialize_kernel", s, fc1_materialize_kernel<<<dim3(Cw, FLAT / FM_K), 256, FC1M_SMEM, s>>>(
+                                                   hs, max_steps, B, lr, prox_mu, dlt, ld_delta));
   }
   return FB_OK;
 }
