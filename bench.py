@@ -192,9 +192,9 @@ def kernel_work(wl: dict, counts: dict) -> dict:
     fc1_bytes = 12544 * 128 * 4
     fwd, train, steps = counts["fwd"], counts["train"], counts["client_steps"]
     return {
-        "conv2_fwd_tc_kernel": ("tensor", conv2 * fwd, "3xTF32 tcgen05"),
+        "conv2_fwd_tc_kernel": ("tensor", conv2 * fwd, "3-term fp16 tcgen05"),
         "conv2_fwd_pool_kernel": ("tensor", conv2 * fwd, "FP32 FFMA"),
-        "conv2_bwd_x_tc_kernel": ("tensor", conv2 * train, "3xTF32 tcgen05"),
+        "conv2_bwd_x_tc_kernel": ("tensor", conv2 * train, "3-term fp16 tcgen05"),
         "conv2_bwd_x_kernel": ("tensor", conv2 * train, "FP32 FFMA"),
         "conv2_bwd_w_tc_kernel": ("tensor", conv2 * train, "3-term fp16 tcgen05"),
         "conv2_bwd_w_kernel": ("tensor", conv2 * train, "FP32 FFMA"),
