@@ -1121,31 +1121,39 @@ __device__ __forceinline__ float block_scale(float m, float* red) {
 }
 
 // ------------------------------------------------- conv2 forward (tcgen05)
-// Implicit GEMM per sample: Z[m, o] = sum_{tap, ci} a1[y+ky, x+kx, ci] W[o, ci, ky, kx],
-// m = (y, x).  M tile = 4 output rows x 28 columns = 112 rows (the UMMA
-// M = 128 tile's last 16 rows are don't-care), N = 64, K = 9 taps x 32 ci.
-// For tap (ky, kx) the A tile is ONE 4-D TMA box {32 ci, 28 x, 4 y, 1 n} of
-// the NHWC fp16 a1 at (0, kx, y0 + ky, n): each output row's 32 channels are
-// one 64-byte swizzle row, exactly the K-major SWIZZLE_64B canonical layout
-// (implicit im2col, no copy kernel).  The client's 9-tap weights (hi + lo,
-// 72 KB) stay resident; A (hi + lo per tap, 16 KB) streams through an
-// 8-stage TMA ring; TMEM accumulators are double-buffered so the epilogue
-// (unscale, bias, ReLU, 2x2 max-pool with argmax code) overlaps the next
-// tile's MMAs.
+// Implicit GEMM per sample: Z[m, o] = sum_{tap, ci} a1[y+ky, x+kx, ci] W[o, ci, ky, kx].
+// Output positions run in the 30-wide space of a1 (m = r*30 + x; columns 28,
+// 29 are discarded), where the tap shift (ky, kx) is the whole-row offset
+// ky*30 + kx.  An M tile = 4 conv rows = 120 rows (the UMMA M = 128 tile's
+// last 8 rows are don't-care), N = 64, K = 9 taps x 32 ci.  Per tile ONE
+// 4-D TMA box {32 ci, 30 x, 7 y, 1 n} of the NHWC fp16 a1 (hi and lo, rows
+// past the image zero-filled) is staged as 64-byte K-major SWIZZLE_64B rows;
+// the nine tap operands are the same band with the descriptor start moved by
+// (ky*30 + kx) rows (the swizzle is a function of the absolute smem address,
+// so a row-shifted start stays a valid canonical tile).  Each a1 byte crosses
+// L2 -> SMEM 7/4 times instead of 9.  The client's 9-tap weights (hi + lo,
+// 72 KB) stay resident; TMEM accumulators are double-buffered so the
+// epilogue (unscale, bias, ReLU, 2x2 max-pool with argmax code) overlaps the
+// next tile's MMAs.
 constexpr int FW_ROWS = 4;                       // conv rows per M tile
-constexpr int FW_M = FW_ROWS * S2;               // 112 valid rows
+constexpr int FW_M = FW_ROWS * S2;               // 112 valid outputs per tile
+constexpr int FW_MW = FW_ROWS * S1;              // 120 rows in the 30-wide space
 constexpr int FW_TILES = S2 / FW_ROWS;           // 7 tiles per sample
-constexpr int FW_A = 128 * 64;                   // 8 KB per operand part (128 rows x 64 B)
-constexpr int FW_A_TX = FW_M * 64;               // 7168 bytes per TMA box
-constexpr int FW_STAGE = 2 * FW_A;               // hi + lo of one tap
+constexpr int FW_BAND = FW_ROWS + 3;             // 7 a1 rows per band (6 + the garbage rows' spill)
+constexpr int FW_A_TX = FW_BAND * S1 * 64;       // 13440 bytes per TMA box
+constexpr int FW_A = 14 * 1024;                  // band part, 1 KB aligned
+constexpr int FW_STAGE = 2 * FW_A;               // hi + lo band
 constexpr int FW_B_TAP = C2 * 64;                // 4 KB: 64 rows (o) x 32 ci fp16
 constexpr int WIMG_BYTES = 9 * 2 * FW_B_TAP;     // 73728: [tap][hi|lo]
-constexpr int FW_STAGES = 8;
-constexpr int FW_EPI_LD = 33;
-constexpr int FW_EPI_BYTES = FW_M * FW_EPI_LD * 4;
+constexpr int FW_STAGES = 4;
+constexpr int FW_EPI_WARPS = 16;                 // 4 per TMEM lane quadrant, 16 channels each
+constexpr int FW_THREADS = (2 + FW_EPI_WARPS) * 32;
+constexpr int FW_PL = 2 * FW_ROWS / 2 * SP;      // 56 horizontal pair maxima per channel and tile
+constexpr int FW_EPI_BYTES = 2 * C2 * FW_PL * 4 + 2 * FW_PL * 4 * 2;  // double-buffered [64 ch][56] values + [56][4] code masks
 constexpr int FW_SMEM = 1024 + WIMG_BYTES + FW_STAGES * FW_STAGE + FW_EPI_BYTES + 256;
 constexpr int FW_ACC = 4 * C2;                   // 4 accumulators x 64 columns per tile
 constexpr uint32_t FW_IDESC = tc::idesc_f16(128, C2);
+static_assert(127 + 2 * S1 + 2 < FW_BAND * S1 && FW_A_TX <= FW_A, "conv2 fwd band: every tap row inside the band");
 
 // per-group conv2 weight image (K-major SWIZZLE_64B: row o, 32 ci), scaled split
 __global__ void __launch_bounds__(256) conv2_wimg_kernel(const float* __restrict__ theta,
@@ -1171,7 +1179,10 @@ __global__ void __launch_bounds__(256) conv2_wimg_kernel(const float* __restrict
   }
 }
 
-__global__ void __launch_bounds__(TC_THREADS, 1) conv2_fwd_tc_kernel(
+#ifdef FB_FWD_PROF
+__device__ unsigned long long g_prof[8];
+#endif
+__global__ void __launch_bounds__(FW_THREADS, 1) conv2_fwd_tc_kernel(
     const __grid_constant__ CUtensorMap tm_hi, const __grid_constant__ CUtensorMap tm_lo,
     const uint8_t* __restrict__ wimg, const float* __restrict__ wscale, int shared_weights,
     const int64_t* __restrict__ slot_row, int N, int G, const float* __restrict__ theta,
@@ -1181,8 +1192,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv2_fwd_tc_kernel(
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sB = sm;                                        // [9][2][4 KB]
   uint8_t* sA = sB + WIMG_BYTES;                           // [stages][hi 8 KB | lo 8 KB]
-  float* sE = reinterpret_cast<float*>(sA + FW_STAGES * FW_STAGE);  // [112][33]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sE) + FW_EPI_BYTES);
+  uint8_t* sP = sA + FW_STAGES * FW_STAGE;  // [2][64 ch][56] fp32 pair maxima, then [2][56][4] u16 code masks
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + FW_EPI_BYTES);
   uint64_t* full = bars;
   uint64_t* empty = bars + FW_STAGES;
   uint64_t* tfull = empty + FW_STAGES;
@@ -1204,7 +1215,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv2_fwd_tc_kernel(
     }
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&tfull[i], 1);
-      tc::mbar_init(&tempty[i], 4);
+      tc::mbar_init(&tempty[i], FW_EPI_WARPS);
     }
     tc::mbar_init(bfull, 1);
     tc::fence_mbar_init();
@@ -1226,15 +1237,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv2_fwd_tc_kernel(
       for (int b = 0; b < G; ++b) {
         const int n = n0 + b;
         if (n >= N || slot_row[n] < 0) continue;
-        for (int t = 0; t < FW_TILES; ++t)
-          for (int tap = 0; tap < 9; ++tap) {
-            tc::mbar_wait(&empty[stage], phase ^ 1);
-            tc::mbar_arrive_expect_tx(&full[stage], 2 * FW_A_TX);
-            uint8_t* st_ = sA + stage * FW_STAGE;
-            tc::tma_load_4d(st_, &tm_hi, 0, tap % 3, FW_ROWS * t + tap / 3, n, &full[stage]);
-            tc::tma_load_4d(st_ + FW_A, &tm_lo, 0, tap % 3, FW_ROWS * t + tap / 3, n, &full[stage]);
-            if (++stage == FW_STAGES) { stage = 0; phase ^= 1; }
-          }
+        for (int t = 0; t < FW_TILES; ++t) {
+          tc::mbar_wait(&empty[stage], phase ^ 1);
+#ifdef FB_FWD_NOTMA  // timing experiment only: no operand traffic
+          tc::mbar_arrive(&full[stage]);
+#else
+          tc::mbar_arrive_expect_tx(&full[stage], 2 * FW_A_TX);
+          uint8_t* st_ = sA + stage * FW_STAGE;
+          tc::tma_load_4d(st_, &tm_hi, 0, 0, FW_ROWS * t, n, &full[stage]);
+          tc::tma_load_4d(st_ + FW_A, &tm_lo, 0, 0, FW_ROWS * t, n, &full[stage]);
+#endif
+          if (++stage == FW_STAGES) { stage = 0; phase ^= 1; }
+        }
       }
     }
   } else if (warp == 1) {
@@ -1242,43 +1256,71 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv2_fwd_tc_kernel(
     int stage = 0, tile = 0;
     uint32_t phase = 0;
     const uint32_t sA0 = tc::smem_u32(sA), sB0 = tc::smem_u32(sB);
+#ifdef FB_FWD_PROF
+    long long p_t0 = clock64(), p_te = 0, p_tf = 0;
+#endif
     for (int b = 0; b < G; ++b) {
       const int n = n0 + b;
       if (n >= N || slot_row[n] < 0) continue;
       for (int t = 0; t < FW_TILES; ++t, ++tile) {
         const int acc = tile & 1;
+#ifdef FB_FWD_PROF
+        long long p_a = clock64();
+#endif
         tc::mbar_wait(&tempty[acc], ((tile >> 1) & 1) ^ 1);
         tc::tc_fence_after();
         const uint32_t d = tmem + acc * FW_ACC;
-        for (int tap = 0; tap < 9; ++tap) {
-          tc::mbar_wait(&full[stage], phase);
-          tc::tc_fence_after();
-          if (lane == 0) {
-            const uint32_t ah = sA0 + stage * FW_STAGE, al = ah + FW_A;
+#ifdef FB_FWD_PROF
+        long long p_b = clock64();
+#endif
+        tc::mbar_wait(&full[stage], phase);
+        tc::tc_fence_after();
+#ifdef FB_FWD_PROF
+        long long p_c = clock64();
+        p_te += p_b - p_a;
+        p_tf += p_c - p_b;
+#endif
+        if (tc::elect_one()) {
+#pragma unroll
+          for (int tap = 0; tap < 9; ++tap) {
+            const uint32_t ah = sA0 + stage * FW_STAGE + ((tap / 3) * S1 + tap % 3) * 64, al = ah + FW_A;
             const uint32_t bh = sB0 + (tap * 2 + 0) * FW_B_TAP, bl = sB0 + (tap * 2 + 1) * FW_B_TAP;
             const uint32_t dmain = d + (tap / 3) * C2, dcross = d + 3 * C2;
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {  // K = 32 ci = 2 x 16
-              const uint64_t adh = tc::sdesc(ah + 32 * k, 16, 512, 4), adl = tc::sdesc(al + 32 * k, 16, 512, 4);
-              const uint64_t bdh = tc::sdesc(bh + 32 * k, 16, 512, 4), bdl = tc::sdesc(bl + 32 * k, 16, 512, 4);
-              tc::mma_f16(dmain, adh, bdh, FW_IDESC, (tap % 3 | k) != 0);
-              tc::mma_f16(dcross, adh, bdl, FW_IDESC, (tap | k) != 0);
-              tc::mma_f16(dcross, adl, bdh, FW_IDESC, 1);
-            }
-            tc::mma_commit(&empty[stage]);
+            // K = 32 ci = 2 x 16: the second K step starts 32 B (2 descriptor units) later
+            tc::mma3_f16_ks<2, 2, 2>(dmain, dcross, tc::sdesc(ah, 16, 512, 4), tc::sdesc(al, 16, 512, 4),
+                                     tc::sdesc(bh, 16, 512, 4), tc::sdesc(bl, 16, 512, 4), FW_IDESC, tap % 3 != 0,
+                                     tap != 0);
           }
-          __syncwarp();
-          if (++stage == FW_STAGES) { stage = 0; phase ^= 1; }
+          tc::mma_commit(&empty[stage]);
+          tc::mma_commit(&tfull[acc]);
         }
-        if (lane == 0) tc::mma_commit(&tfull[acc]);
         __syncwarp();
+        if (++stage == FW_STAGES) { stage = 0; phase ^= 1; }
       }
     }
+#ifdef FB_FWD_PROF
+    if (lane == 0) {
+      atomicAdd(&g_prof[0], (unsigned long long)(clock64() - p_t0));
+      atomicAdd(&g_prof[1], (unsigned long long)p_te);
+      atomicAdd(&g_prof[2], (unsigned long long)p_tf);
+      atomicAdd(&g_prof[3], 1ull);
+    }
+#endif
   } else {
-    const int ew = warp & 3;
-    const int row = ew * 32 + lane;
+    // 16 epilogue warps: TMEM lane quadrant q = warp % 4 (rows m = 32q + lane),
+    // channel group cg of 16.  The 2x2 max-pool is done as a horizontal pair
+    // max across lanes (x, x+1 are lanes m, m+1) and a vertical max through
+    // shared memory; pairwise first-wins maxima equal the sequential argmax
+    // (q0, q1, q2, q3 order, strict >).  Pair winners' codes travel as one
+    // 16-bit mask per (position, channel group).
+    const int q = warp & 3, cg = (warp - 2) >> 2;
+    const int row = q * 32 + lane;
+    const int r = row / S1, x = row - r * S1;
+    const bool keep = row < FW_MW && x < S2 && !(x & 1);
+    const int pcol = r * SP + (x >> 1);
     const int et = threadIdx.x - 64;
     const float ws = wscale[wg];
+    const uint32_t sPv = tc::smem_u32(sP), sPc = sPv + 2 * C2 * FW_PL * 4;
     int tile = 0;
     for (int b = 0; b < G; ++b) {
       const int n = n0 + b;
@@ -1288,49 +1330,58 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv2_fwd_tc_kernel(
       uint8_t* cout = code + (int64_t)n * FLAT;
       for (int t = 0; t < FW_TILES; ++t, ++tile) {
         const int acc = tile & 1;
+        const uint32_t pv = sPv + acc * (C2 * FW_PL * 4), pc = sPc + acc * (FW_PL * 4 * 2);
+#ifdef FB_FWD_PROF
+        long long p_a = clock64();
+#endif
         tc::mbar_wait(&tfull[acc], (tile >> 1) & 1);
         tc::tc_fence_after();
-        for (int h = 0; h < 2; ++h) {
-          float z[32];
-          {
-            const uint32_t base = tmem + ((uint32_t)(ew * 32) << 16) + acc * FW_ACC + h * 32;
-            uint32_t v0[32], v1[32];
-            tc::tmem_ld32(base, v0);
-            tc::tmem_ld32(base + C2, v1);
-            tc::tmem_ld_wait();
+#ifdef FB_FWD_PROF
+        if (warp == 2 && lane == 0) atomicAdd(&g_prof[4], (unsigned long long)(clock64() - p_a));
+#endif
+        float z[16];
+        {
+          const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + acc * FW_ACC + cg * 16;
+          uint32_t v0[16], v1[16], v2[16], v3[16];
+          tc::tmem_ld16(base, v0);
+          tc::tmem_ld16(base + C2, v1);
+          tc::tmem_ld16(base + 2 * C2, v2);
+          tc::tmem_ld16(base + 3 * C2, v3);
+          tc::tmem_ld_wait();
+          tc::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&tempty[acc]);  // accumulator drained: the next tile may reuse it
 #pragma unroll
-            for (int j = 0; j < 32; ++j) z[j] = __uint_as_float(v0[j]) + __uint_as_float(v1[j]);
-            tc::tmem_ld32(base + 2 * C2, v0);
-            tc::tmem_ld32(base + 3 * C2, v1);
-            tc::tmem_ld_wait();
+          for (int j = 0; j < 16; ++j)
+            z[j] = ((__uint_as_float(v0[j]) + __uint_as_float(v1[j])) + __uint_as_float(v2[j])) + __uint_as_float(v3[j]);
+        }
+#ifdef FB_FWD_NOEPI  // timing experiment only: drain TMEM, skip the pooling epilogue
+        if (z[0] == 1.2345f) pout[0] = z[1];
+        continue;
+#endif
+        uint32_t mask = 0;
+        const uint32_t pa = pv + (cg * 16 * FW_PL + pcol) * 4;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) z[j] = (z[j] + __uint_as_float(v0[j])) + __uint_as_float(v1[j]);
-          }
-          if (h == 1) {  // both halves read: the next tile may reuse this accumulator
-            tc::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&tempty[acc]);
-          }
-          if (row < FW_M) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) sE[row * FW_EPI_LD + j] = fmaxf(fmaf(z[j], inv, bias[h * 32 + j]), 0.f);
-          }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          // consecutive threads -> consecutive pooled positions of one channel (28 contiguous floats)
-          for (int it = et; it < 2 * SP * 32; it += 128) {
-            const int j = it / (2 * SP), pp = it - j * (2 * SP), pr = pp / SP, px = pp - pr * SP;
-            const float* e0 = sE + ((2 * pr) * S2 + 2 * px) * FW_EPI_LD + j;
-            const float q0 = e0[0], q1 = e0[FW_EPI_LD], q2 = e0[S2 * FW_EPI_LD], q3 = e0[(S2 + 1) * FW_EPI_LD];
-            float best = q0;
-            int arg = 0;
-            if (q1 > best) { best = q1; arg = 1; }
-            if (q2 > best) { best = q2; arg = 2; }
-            if (q3 > best) { best = q3; arg = 3; }
-            const int idx = (h * 32 + j) * NPOOL + (FW_ROWS / 2 * t + pr) * SP + px;
-            pout[idx] = best;
-            cout[idx] = (uint8_t)arg;
-          }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
+        for (int j = 0; j < 16; ++j) {
+          const float v = fmaxf(fmaf(z[j], inv, bias[cg * 16 + j]), 0.f);
+          const float o = __shfl_xor_sync(0xffffffffu, v, 1);
+          const bool right = o > v;
+          mask |= (uint32_t)right << j;
+          if (keep) tc::sts_f32(pa + j * FW_PL * 4, right ? o : v);
+        }
+        if (keep) tc::sts_u16(pc + (pcol * 4 + cg) * 2, (uint16_t)mask);
+        asm volatile("bar.sync 1, %0;" ::"n"(FW_EPI_WARPS * 32) : "memory");
+        // consecutive threads -> consecutive pooled positions of one channel (28 contiguous outputs)
+        for (int it = et; it < C2 * 2 * SP; it += FW_EPI_WARPS * 32) {
+          const int ch = it / (2 * SP), pp = it - ch * (2 * SP), pr = pp >= SP, px = pp - pr * SP;
+          const int c0 = 2 * pr * SP + px;
+          const float top = tc::lds_f32(pv + (ch * FW_PL + c0) * 4), bot = tc::lds_f32(pv + (ch * FW_PL + c0 + SP) * 4);
+          const uint32_t mt = tc::lds_u16(pc + (c0 * 4 + (ch >> 4)) * 2);
+          const uint32_t mb = tc::lds_u16(pc + ((c0 + SP) * 4 + (ch >> 4)) * 2);
+          const bool lower = bot > top;
+          const int idx = ch * NPOOL + FW_ROWS / 2 * t * SP + pp;
+          pout[idx] = lower ? bot : top;
+          cout[idx] = (uint8_t)(lower ? 2 + ((mb >> (ch & 15)) & 1) : ((mt >> (ch & 15)) & 1));
         }
       }
     }
@@ -1538,18 +1589,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) fc1_tc_kernel(const __grid_cons
         }
         tc::mbar_wait(&full[stage], phase);
         tc::tc_fence_after();
-        if (lane == 0) {
+        if (tc::elect_one()) {
           const uint32_t ah = s0 + stage * FT_STAGE, al = ah + FT_PART, bh = ah + 2 * FT_PART, bl = ah + 3 * FT_PART;
           const uint32_t dmain = tmem + buf * 256, dcross = dmain + 128;
-#pragma unroll
-          for (int kk = 0; kk < FT_KS / 16; ++kk) {
-            const uint64_t adh = tc::sdesc(ah + 32 * kk, 16, 1024, 2), adl = tc::sdesc(al + 32 * kk, 16, 1024, 2);
-            const uint64_t bdh = tc::sdesc(bh + 32 * kk, 16, 1024, 2), bdl = tc::sdesc(bl + 32 * kk, 16, 1024, 2);
-            const uint32_t acc = (st_ % FT_WIN != 0 || kk != 0) ? 1u : 0u;
-            tc::mma_f16(dmain, adh, bdh, FT_IDESC, acc);
-            tc::mma_f16(dcross, adh, bdl, FT_IDESC, acc);
-            tc::mma_f16(dcross, adl, bdh, FT_IDESC, 1);
-          }
+          static_assert(FT_KS == 64, "fc1 stage = 4 K steps");
+          const uint32_t acc = st_ % FT_WIN != 0 ? 1u : 0u;  // a window's first stage starts fresh accumulators
+          tc::mma3_f16_ks<4, 2, 2>(dmain, dcross, tc::sdesc(ah, 16, 1024, 2), tc::sdesc(al, 16, 1024, 2),
+                                   tc::sdesc(bh, 16, 1024, 2), tc::sdesc(bl, 16, 1024, 2), FT_IDESC, acc, acc);
           tc::mma_commit(&empty[stage]);
           if (st_ % FT_WIN == FT_WIN - 1) tc::mma_commit(&tfull[buf]);
         }
@@ -1667,24 +1713,32 @@ __global__ void __launch_bounds__(KCHUNK / 4) fc1_dp_hist_kernel(int B, const in
 // ------------------------------------------------ conv2 backward-data (tcgen05)
 // dz1[n, y, x, ci] = relu'(a1) * sum_{ky, kx, o} dz2[n, y-ky, x-kx, o] W[o, ci, ky, kx]
 // Implicit GEMM: M = a1 positions (tile = 4 rows x 30 cols = 120), N = 32
-// input channels, K = 9 taps x 64 output channels.  The A tile of tap
-// (ky, kx) is one TMA box {64 o, 30 x, 4 y} of the fp16 dz2 at (0, -kx,
-// y0-ky, n): the negative / past-the-end coordinates are the transposed
-// convolution's zero padding, filled by the TMA unit.  Epilogue: unscale,
-// ReLU mask of a1, 32 channels (128 B) per position straight to HBM.
+// input channels, K = 9 taps x 64 output channels.  Per tile ONE TMA box
+// {64 o, 30 x, 7 y} of the fp16 dz2 at (0, -2, y0-2, n) is staged (128-byte
+// K-major SWIZZLE_128B rows); the negative / past-the-end coordinates are
+// the transposed convolution's zero padding, filled by the TMA unit.  In this
+// 30-wide band the tap (ky, kx) operand of output row m is band row
+// m + (2-ky)*30 + (2-kx) (a column shift past x = 27 lands on the zero-filled
+// columns -2, -1 of the next row), so the nine tap operands are the one band
+// with the descriptor start moved by whole rows.  Epilogue: unscale, ReLU
+// mask of a1, 32 channels (128 B) per position straight to HBM.
 constexpr int BX_ROWS = 4;
 constexpr int BX_M = BX_ROWS * S1;               // 120 valid rows
 constexpr int BX_TILES = (S1 + BX_ROWS - 1) / BX_ROWS;  // 8 (last tile: 2 valid rows)
-constexpr int BX_A = 128 * 128;                  // 16 KB per operand part
-constexpr int BX_A_TX = BX_M * 128;              // 15360 bytes per TMA box
-constexpr int BX_STAGE = 2 * BX_A;               // hi + lo of one tap
+constexpr int BX_BAND = BX_ROWS + 3;             // 7 dz2 rows per band
+constexpr int BX_A_TX = BX_BAND * S1 * 128;      // 26880 bytes per TMA box
+constexpr int BX_A = 27 * 1024;                  // band part, 1 KB aligned
+constexpr int BX_STAGE = 2 * BX_A;               // hi + lo band
 constexpr int BX_B_TAP = C1 * 128;               // 4 KB: 32 rows (ci) x 64 o fp16
 constexpr int WIMGT_BYTES = 9 * 2 * BX_B_TAP;    // 73728
-constexpr int BX_STAGES = 4;
+constexpr int BX_STAGES = 2;
 constexpr int BX_ACC = 4 * C1;                   // 4 accumulators x 32 columns
 constexpr int BX_SMEM = 1024 + WIMGT_BYTES + BX_STAGES * BX_STAGE + 256;
+constexpr int BX_EPI_WARPS = 16;                 // 4 per TMEM lane quadrant, 8 input channels each
+constexpr int BX_THREADS = (2 + BX_EPI_WARPS) * 32;
 constexpr uint32_t BX_IDESC = tc::idesc_f16(128, C1);
 static_assert(WIMGT_BYTES == WIMG_BYTES, "weight image sizes");
+static_assert(127 + 2 * S1 + 2 < BX_BAND * S1 && BX_A_TX <= BX_A, "conv2 bwd-x band: every tap row inside the band");
 
 // transposed weight image for backward-data: rows ci, K = o (K-major SWIZZLE_128B)
 __global__ void __launch_bounds__(256) conv2_wimgT_kernel(const float* __restrict__ theta,
@@ -1762,7 +1816,7 @@ __global__ void __launch_bounds__(256) dz2_build_kernel(const float* __restrict_
   }
 }
 
-__global__ void __launch_bounds__(TC_THREADS, 1) conv2_bwd_x_tc_kernel(
+__global__ void __launch_bounds__(BX_THREADS, 1) conv2_bwd_x_tc_kernel(
     const __grid_constant__ CUtensorMap tm_hi, const __grid_constant__ CUtensorMap tm_lo,
     const uint8_t* __restrict__ wimg, const float* __restrict__ wscale, const int64_t* __restrict__ slot_row, int G,
     const float* __restrict__ dzscale, const __half* __restrict__ a1fh, const __half* __restrict__ a1fl,
@@ -1789,7 +1843,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv2_bwd_x_tc_kernel(
     }
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&tfull[i], 1);
-      tc::mbar_init(&tempty[i], 4);
+      tc::mbar_init(&tempty[i], BX_EPI_WARPS);
     }
     tc::mbar_init(bfull, 1);
     tc::fence_mbar_init();
@@ -1811,15 +1865,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv2_bwd_x_tc_kernel(
       for (int b = 0; b < G; ++b) {
         const int n = n0 + b;
         if (slot_row[n] < 0) continue;
-        for (int t = 0; t < BX_TILES; ++t)
-          for (int tap = 0; tap < 9; ++tap) {
-            tc::mbar_wait(&empty[stage], phase ^ 1);
-            tc::mbar_arrive_expect_tx(&full[stage], 2 * BX_A_TX);
-            uint8_t* st_ = sA + stage * BX_STAGE;
-            tc::tma_load_4d(st_, &tm_hi, 0, -(tap % 3), BX_ROWS * t - tap / 3, n, &full[stage]);
-            tc::tma_load_4d(st_ + BX_A, &tm_lo, 0, -(tap % 3), BX_ROWS * t - tap / 3, n, &full[stage]);
-            if (++stage == BX_STAGES) { stage = 0; phase ^= 1; }
-          }
+        for (int t = 0; t < BX_TILES; ++t) {
+          tc::mbar_wait(&empty[stage], phase ^ 1);
+          tc::mbar_arrive_expect_tx(&full[stage], 2 * BX_A_TX);
+          uint8_t* st_ = sA + stage * BX_STAGE;
+          tc::tma_load_4d(st_, &tm_hi, 0, -2, BX_ROWS * t - 2, n, &full[stage]);
+          tc::tma_load_4d(st_ + BX_A, &tm_lo, 0, -2, BX_ROWS * t - 2, n, &full[stage]);
+          if (++stage == BX_STAGES) { stage = 0; phase ^= 1; }
+        }
       }
     }
   } else if (warp == 1) {
@@ -1835,33 +1888,32 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv2_bwd_x_tc_kernel(
         tc::mbar_wait(&tempty[acc], ((tile >> 1) & 1) ^ 1);
         tc::tc_fence_after();
         const uint32_t d = tmem + acc * BX_ACC;
-        for (int tap = 0; tap < 9; ++tap) {
-          tc::mbar_wait(&full[stage], phase);
-          tc::tc_fence_after();
-          if (lane == 0) {
-            const uint32_t ah = sA0 + stage * BX_STAGE, al = ah + BX_A;
+        tc::mbar_wait(&full[stage], phase);
+        tc::tc_fence_after();
+        if (tc::elect_one()) {
+#pragma unroll
+          for (int tap = 0; tap < 9; ++tap) {
+            const uint32_t ah = sA0 + stage * BX_STAGE + ((2 - tap / 3) * S1 + 2 - tap % 3) * 128, al = ah + BX_A;
             const uint32_t bh = sB0 + (tap * 2 + 0) * BX_B_TAP, bl = sB0 + (tap * 2 + 1) * BX_B_TAP;
             const uint32_t dmain = d + (tap / 3) * C1, dcross = d + 3 * C1;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {  // K = 64 o = 4 x 16
-              const uint64_t adh = tc::sdesc(ah + 32 * k, 16, 1024, 2), adl = tc::sdesc(al + 32 * k, 16, 1024, 2);
-              const uint64_t bdh = tc::sdesc(bh + 32 * k, 16, 1024, 2), bdl = tc::sdesc(bl + 32 * k, 16, 1024, 2);
-              tc::mma_f16(dmain, adh, bdh, BX_IDESC, (tap % 3 | k) != 0);
-              tc::mma_f16(dcross, adh, bdl, BX_IDESC, (tap | k) != 0);
-              tc::mma_f16(dcross, adl, bdh, BX_IDESC, 1);
-            }
-            tc::mma_commit(&empty[stage]);
+            // K = 64 o = 4 x 16, each K step 32 B (2 descriptor units) further along the row
+            tc::mma3_f16_ks<4, 2, 2>(dmain, dcross, tc::sdesc(ah, 16, 1024, 2), tc::sdesc(al, 16, 1024, 2),
+                                     tc::sdesc(bh, 16, 1024, 2), tc::sdesc(bl, 16, 1024, 2), BX_IDESC, tap % 3 != 0,
+                                     tap != 0);
           }
-          __syncwarp();
-          if (++stage == BX_STAGES) { stage = 0; phase ^= 1; }
+          tc::mma_commit(&empty[stage]);
+          tc::mma_commit(&tfull[acc]);
         }
-        if (lane == 0) tc::mma_commit(&tfull[acc]);
         __syncwarp();
+        if (++stage == BX_STAGES) { stage = 0; phase ^= 1; }
       }
     }
   } else {
-    const int ew = warp & 3;
-    const int row = ew * 32 + lane;
+    // 16 epilogue warps: TMEM lane quadrant q = warp % 4, input-channel group of 8;
+    // the a1 ReLU-mask loads are issued before waiting on the accumulator
+    const int q = warp & 3, cg = (warp - 2) >> 2;
+    const int row = q * 32 + lane;
+    const int r = row / S1, x = row - r * S1;
     const float ws = wscale[g];
     int tile = 0;
     for (int b = 0; b < G; ++b) {
@@ -1870,45 +1922,45 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv2_bwd_x_tc_kernel(
       const float inv = 1.f / (dzscale[n] * ws);
       for (int t = 0; t < BX_TILES; ++t, ++tile) {
         const int acc = tile & 1;
+        const int y = BX_ROWS * t + r;
+        const bool ok = row < BX_M && y < S1;
+        const int64_t off = ((int64_t)n * S1 * S1 + y * S1 + x) * C1 + cg * 8;
+        uint4 hv = make_uint4(0, 0, 0, 0), lv = hv;
+        if (ok) {
+          hv = *reinterpret_cast<const uint4*>(a1fh + off);
+          lv = *reinterpret_cast<const uint4*>(a1fl + off);
+        }
         tc::mbar_wait(&tfull[acc], (tile >> 1) & 1);
         tc::tc_fence_after();
-        const uint32_t base = tmem + ((uint32_t)(ew * 32) << 16) + acc * BX_ACC;
-        uint32_t v0[32], v1[32];
-        float z[32];
-        tc::tmem_ld32(base, v0);
-        tc::tmem_ld32(base + C1, v1);
-        tc::tmem_ld_wait();
-#pragma unroll
-        for (int j = 0; j < 32; ++j) z[j] = __uint_as_float(v0[j]) + __uint_as_float(v1[j]);
-        tc::tmem_ld32(base + 2 * C1, v0);
-        tc::tmem_ld32(base + 3 * C1, v1);
+        const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + acc * BX_ACC + cg * 8;
+        uint32_t v0[8], v1[8], v2[8], v3[8];
+        tc::tmem_ld8(base, v0);
+        tc::tmem_ld8(base + C1, v1);
+        tc::tmem_ld8(base + 2 * C1, v2);
+        tc::tmem_ld8(base + 3 * C1, v3);
         tc::tmem_ld_wait();
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&tempty[acc]);  // accumulator drained: next tile may start
+        if (ok) {
+          const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w}, lw[4] = {lv.x, lv.y, lv.z, lv.w};
+          float o[8];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) z[j] = ((z[j] + __uint_as_float(v0[j])) + __uint_as_float(v1[j])) * inv;
-        const int r = row / S1, x = row - r * S1, y = BX_ROWS * t + r;
-        if (row < BX_M && y < S1) {
-          const int64_t off = ((int64_t)n * S1 * S1 + y * S1 + x) * C1;
-          const uint4* mh = reinterpret_cast<const uint4*>(a1fh + off);
-          const uint4* ml = reinterpret_cast<const uint4*>(a1fl + off);
-          float4* o4 = reinterpret_cast<float4*>(dz1 + off);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {  // 8 channels per 16-byte load of the fp16 a1
-            const uint4 hv = mh[q], lv = ml[q];
-            const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w}, lw[4] = {lv.x, lv.y, lv.z, lv.w};
-            float mk[8];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const __half2 h2 = *reinterpret_cast<const __half2*>(&hw[e]);
-              const __half2 l2 = *reinterpret_cast<const __half2*>(&lw[e]);
-              mk[2 * e] = (__low2float(h2) + __low2float(l2)) > 0.f ? 1.f : 0.f;
-              mk[2 * e + 1] = (__high2float(h2) + __high2float(l2)) > 0.f ? 1.f : 0.f;
-            }
-            o4[2 * q] = make_float4(z[8 * q] * mk[0], z[8 * q + 1] * mk[1], z[8 * q + 2] * mk[2], z[8 * q + 3] * mk[3]);
-            o4[2 * q + 1] = make_float4(z[8 * q + 4] * mk[4], z[8 * q + 5] * mk[5], z[8 * q + 6] * mk[6], z[8 * q + 7] * mk[7]);
+          for (int e = 0; e < 4; ++e) {
+            const __half2 h2 = *reinterpret_cast<const __half2*>(&hw[e]);
+            const __half2 l2 = *reinterpret_cast<const __half2*>(&lw[e]);
+            const bool m0 = (__low2float(h2) + __low2float(l2)) > 0.f, m1 = (__high2float(h2) + __high2float(l2)) > 0.f;
+            const int j = 2 * e;
+            const float z0 = (((__uint_as_float(v0[j]) + __uint_as_float(v1[j])) + __uint_as_float(v2[j])) +
+                              __uint_as_float(v3[j])) * inv;
+            const float z1 = (((__uint_as_float(v0[j + 1]) + __uint_as_float(v1[j + 1])) + __uint_as_float(v2[j + 1])) +
+                              __uint_as_float(v3[j + 1])) * inv;
+            o[j] = m0 ? z0 : 0.f;
+            o[j + 1] = m1 ? z1 : 0.f;
           }
+          float4* o4 = reinterpret_cast<float4*>(dz1 + off);
+          o4[0] = make_float4(o[0], o[1], o[2], o[3]);
+          o4[1] = make_float4(o[4], o[5], o[6], o[7]);
         }
       }
     }
@@ -2025,17 +2077,16 @@ __global__ void __launch_bounds__(BW_THREADS, 1) conv2_bwd_w_tc_kernel(
       for (int ky = 0; ky < 3; ++ky) {
         tc::mbar_wait(&tempty[ky], (blk & 1) ^ 1);  // previous block's ky accumulators drained
         tc::tc_fence_after();
-        if (lane == 0) {
+        if (tc::elect_one()) {
           const uint32_t dm = tmem + ky * 2 * C2, dx = dm + C2;
+#pragma unroll 5
           for (int ks = 0; ks < BW_KPOS / 16; ++ks) {
             const uint32_t arow = ky * S1 + ks * 16;
             const uint64_t adh = tc::sdesc(ah + arow * 64, 64, 512, 4);
             const uint64_t adl = tc::sdesc(al + arow * 64, 64, 512, 4);
             const uint64_t bdh = tc::sdesc(bh + ks * 16 * 128, 128, 1024, 2);
             const uint64_t bdl = tc::sdesc(bl + ks * 16 * 128, 128, 1024, 2);
-            tc::mma_f16(dm, adh, bdh, BW_IDESC, ks != 0);
-            tc::mma_f16(dx, adh, bdl, BW_IDESC, ks != 0);
-            tc::mma_f16(dx, adl, bdh, BW_IDESC, 1);
+            tc::mma3_f16(dm, dx, adh, adl, bdh, bdl, BW_IDESC, ks != 0, ks != 0);
           }
           tc::mma_commit(&tfull[ky]);
           if (ky == 2) tc::mma_commit(&empty[stage]);
@@ -2231,11 +2282,11 @@ int forward(const float* X, const float* theta, const float* delta, int64_t ld, 
     FB_LAUNCH("conv2_wimg_kernel", s, conv2_wimg_kernel<<<groups, 256, 0, s>>>(theta, delta, ld, client_nb, w.wimg,
                                                                                    w.wscale));
     CUtensorMap mh, ml;
-    int st = a1f_tensor_map(&mh, w.a1fh, N, S2, FW_ROWS);
-    if (!st) st = a1f_tensor_map(&ml, w.a1fl, N, S2, FW_ROWS);
+    int st = a1f_tensor_map(&mh, w.a1fh, N, S1, FW_BAND);
+    if (!st) st = a1f_tensor_map(&ml, w.a1fl, N, S1, FW_BAND);
     if (st) return st;
     const int gt = delta ? B : 8;  // samples per CTA
-    FB_LAUNCH("conv2_fwd_tc_kernel", s, conv2_fwd_tc_kernel<<<(N + gt - 1) / gt, TC_THREADS, FW_SMEM, s>>>(
+    FB_LAUNCH("conv2_fwd_tc_kernel", s, conv2_fwd_tc_kernel<<<(N + gt - 1) / gt, FW_THREADS, FW_SMEM, s>>>(
         mh, ml, w.wimg, w.wscale, delta ? 0 : 1, w.slot_row, N, gt, theta, delta, ld, B, w.a1scale, w.pooled,
         w.code));
   } else {
@@ -2278,6 +2329,15 @@ int forward(const float* X, const float* theta, const float* delta, int64_t ld, 
 using namespace fb::cnn;
 
 extern "C" {
+
+#ifdef FB_FWD_PROF
+int fb_debug_prof(unsigned long long* out) {  // timing experiments only
+  cudaMemcpyFromSymbol(out, g_prof, sizeof(unsigned long long) * 8);
+  unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  cudaMemcpyToSymbol(g_prof, z, sizeof(z));
+  return 0;
+}
+#endif
 
 int fb_cnn_set_conv_impl(int impl) {
   FB_REQUIRE(impl == 0 || impl == 1, "fb_cnn_set_conv_impl: 0 (FP32 CUDA cores) or 1 (tcgen05)");
@@ -2440,10 +2500,10 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
         FB_LAUNCH("conv2_wimgT_kernel", s, conv2_wimgT_kernel<<<Cw, 256, 0, s>>>(theta_t, dlt, ld_delta, ws.client_nb,
                                                                                  ws.wimg, ws.wscale));
         CUtensorMap mh, ml;
-        st = dzf_tensor_map(&mh, ws.dzfh, N, S1, BX_ROWS);
-        if (!st) st = dzf_tensor_map(&ml, ws.dzfl, N, S1, BX_ROWS);
+        st = dzf_tensor_map(&mh, ws.dzfh, N, S1, BX_BAND);
+        if (!st) st = dzf_tensor_map(&ml, ws.dzfl, N, S1, BX_BAND);
         if (st) return st;
-        FB_LAUNCH("conv2_bwd_x_tc_kernel", s, conv2_bwd_x_tc_kernel<<<Cw, TC_THREADS, BX_SMEM, s>>>(
+        FB_LAUNCH("conv2_bwd_x_tc_kernel", s, conv2_bwd_x_tc_kernel<<<Cw, BX_THREADS, BX_SMEM, s>>>(
             mh, ml, ws.wimg, ws.wscale, ws.slot_row, B, ws.dzscale, ws.a1fh, ws.a1fl, ws.dz1));
         CUtensorMap ah, al, dh, dl;
         st = a1f_tensor_map(&ah, ws.a1fh, N, S1, BW_ROWS + 2);

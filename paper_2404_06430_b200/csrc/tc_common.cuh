@@ -76,6 +76,26 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
       : "memory");
 }
 
+// explicit shared-window loads / stores (32-bit smem addresses): pointers
+// derived from the manually aligned dynamic-smem base are generic to the
+// compiler, which then emits 64-bit generic ST/LD with address arithmetic
+__device__ __forceinline__ void sts_f32(uint32_t a, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
+__device__ __forceinline__ void sts_u16(uint32_t a, uint16_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"(v) : "memory");
+}
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
+  uint16_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
+  return v;
+}
+
 // ----------------------------------------------------------------- TMEM
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {  // one full warp
@@ -104,6 +124,20 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
         "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
         "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
       : "r"(taddr));
+}
+// 32 lanes x 16 consecutive 32-bit columns -> 16 registers per thread
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+// 32 lanes x 8 consecutive 32-bit columns -> 8 registers per thread
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
@@ -161,6 +195,71 @@ __device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t adesc, uint64_
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
+}
+// The 3-term split product of one K step, issued from ONE asm statement so the
+// compiler elects / broadcasts the operands once per group instead of once per
+// MMA (the single-thread issue path costs ~13 instructions per UTCHMMA):
+//   dmain += Ahi*Bhi (accumulate if pm), dcross += Ahi*Blo (if px), dcross += Alo*Bhi.
+__device__ __forceinline__ void mma3_f16(uint32_t dmain, uint32_t dcross, uint64_t ah, uint64_t al, uint64_t bh,
+                                         uint64_t bl, uint32_t idesc, uint32_t pm, uint32_t px) {
+  asm volatile(
+      "{\n\t.reg .pred pm, px, pt;\n\t"
+      "setp.ne.b32 pm, %7, 0;\n\t"
+      "setp.ne.b32 px, %8, 0;\n\t"
+      "setp.eq.b32 pt, %6, %6;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %4, %6, pm;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%1], %2, %5, %6, px;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%1], %3, %4, %6, pt;\n}" ::"r"(dmain),
+      "r"(dcross), "l"(ah), "l"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(pm), "r"(px)
+      : "memory");
+}
+// KS consecutive K steps of mma3_f16 in one asm statement: step k uses the
+// descriptors advanced by k * AINC / BINC (descriptor units of 16 bytes); only
+// step 0 takes the pm / px accumulate flags, later steps always accumulate.
+template <int KS, int AINC, int BINC>
+__device__ __forceinline__ void mma3_f16_ks(uint32_t dmain, uint32_t dcross, uint64_t ah, uint64_t al, uint64_t bh,
+                                            uint64_t bl, uint32_t idesc, uint32_t pm, uint32_t px) {
+  static_assert(KS == 2 || KS == 4, "mma3_f16_ks: 2 or 4 K steps");
+  if constexpr (KS == 2) {
+    asm volatile(
+        "{\n\t.reg .pred pm, px, pt;\n\t.reg .b64 a1, c1, b1, e1;\n\t"
+        "setp.ne.b32 pm, %7, 0;\n\t"
+        "setp.ne.b32 px, %8, 0;\n\t"
+        "setp.eq.b32 pt, %6, %6;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %4, %6, pm;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%1], %2, %5, %6, px;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%1], %3, %4, %6, pt;\n\t"
+        "add.s64 a1, %2, %9;\n\tadd.s64 c1, %3, %9;\n\tadd.s64 b1, %4, %10;\n\tadd.s64 e1, %5, %10;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %6, pt;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%1], a1, e1, %6, pt;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%1], c1, b1, %6, pt;\n}" ::"r"(dmain),
+        "r"(dcross), "l"(ah), "l"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(pm), "r"(px), "n"(AINC), "n"(BINC)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred pm, px, pt;\n\t.reg .b64 a1, c1, b1, e1;\n\t"
+        "setp.ne.b32 pm, %7, 0;\n\t"
+        "setp.ne.b32 px, %8, 0;\n\t"
+        "setp.eq.b32 pt, %6, %6;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %4, %6, pm;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%1], %2, %5, %6, px;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%1], %3, %4, %6, pt;\n\t"
+        "add.s64 a1, %2, %9;\n\tadd.s64 c1, %3, %9;\n\tadd.s64 b1, %4, %10;\n\tadd.s64 e1, %5, %10;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %6, pt;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%1], a1, e1, %6, pt;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%1], c1, b1, %6, pt;\n\t"
+        "add.s64 a1, %2, %11;\n\tadd.s64 c1, %3, %11;\n\tadd.s64 b1, %4, %12;\n\tadd.s64 e1, %5, %12;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %6, pt;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%1], a1, e1, %6, pt;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%1], c1, b1, %6, pt;\n\t"
+        "add.s64 a1, %2, %13;\n\tadd.s64 c1, %3, %13;\n\tadd.s64 b1, %4, %14;\n\tadd.s64 e1, %5, %14;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %6, pt;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%1], a1, e1, %6, pt;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%1], c1, b1, %6, pt;\n}" ::"r"(dmain),
+        "r"(dcross), "l"(ah), "l"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(pm), "r"(px), "n"(AINC), "n"(BINC),
+        "n"(2 * AINC), "n"(2 * BINC), "n"(3 * AINC), "n"(3 * BINC)
+        : "memory");
+  }
 }
 // kind::tf32 instruction descriptor with both operands MN-major
 __host__ __device__ constexpr uint32_t idesc_tf32_mn(int M, int N) {
