@@ -208,6 +208,37 @@ int fb_noise_avg_sgd_f32(float* theta, const float* agg, int64_t D,
                          double noise_std, uint64_t seed, const float* injected,
                          double inv_weight, double lr, float* agg_out, void* stream);
 
+/* ------------------------------------------ a10 + a12 with central Adam
+ * a = (agg + noise) * inv_weight (noise as in fb_noise_avg_sgd_f32), then
+ * one bias-corrected Adam step at step count `step` (>= 1):
+ *   m1 = b1*m1 + (1-b1)*a,  m2 = b2*m2 + (1-b2)*a^2   (in place)
+ *   theta -= lr * (m1/(1-b1^step)) / (sqrt(m2/(1-b2^step)) + eps)
+ * Replaces AdamOptimizer.step (fedsim/models/optimizers.py:24-68) after
+ * average (fedsim/core/statistics.py:105-113).  eps = adaptivity_degree.   */
+int fb_noise_avg_adam_f32(float* theta, float* m1, float* m2, const float* agg, int64_t D,
+                          double noise_std, uint64_t seed, const float* injected,
+                          double inv_weight, double lr, double beta1, double beta2, double eps,
+                          int64_t step, float* agg_out, void* stream);
+
+/* ------------------------------------------ SCAFFOLD control variates
+ * (fedsim/algorithms/scaffold.py:46-79).  Per-user controls live in a
+ * device store [rows, ld_store]; rows[c] = store row of client c, -1 = zero
+ * control (first participation).
+ * correction[c] = server - store[rows[c]]       -> the local-SGD control term
+ * payload[c]    = [delta_c | delta_c*scale_c - server]   (model/, control/)
+ * new_control[c] = store[rows[c]] - server + delta_c*scale_c
+ * with scale_c = 1 / (steps_c * lr).  fb_scatter_rows_f32 writes
+ * store[rows[c]] = src[c] (the user updates of process_aggregated_...). */
+int fb_scaffold_correction_f32(const float* server, const float* store, int64_t ld_store,
+                               const int32_t* rows, int num_clients, int64_t D, float* out,
+                               int64_t ld_out, void* stream);
+int fb_scaffold_payload_f32(const float* delta, int64_t ld_delta, const float* server,
+                            const float* store, int64_t ld_store, const int32_t* rows,
+                            const float* scale, int num_clients, int64_t D, float* payload,
+                            int64_t ld_payload, float* new_control, int64_t ld_new, void* stream);
+int fb_scatter_rows_f32(float* store, int64_t ld_store, const int32_t* rows, const float* src,
+                        int64_t ld_src, int num_rows, int64_t D, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

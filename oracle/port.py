@@ -315,15 +315,20 @@ class ContextResult:
     weight: float = 0.0
     noise: np.ndarray | None = None
     metrics: dict = field(default_factory=dict)
+    user_updates: list = field(default_factory=list)
 
 
 def run_context(model, theta: dict, users: dict, cohort_size: int, ctx_seed: int, *, train=None,
                 weighting="datapoints", bound=None, sigma=0.0, r=1.0, noise_base=0, t=0, pop="train",
-                world=1, rank=0, base_policy="median", noise=True):
+                world=1, rank=0, base_policy="median", noise=True, mu=0.0, scaffold=None):
     """One context of SimulationEngine._run_context (fedsim/engine/runtime.py:106-171)
     with FedAvg users (fedsim/algorithms/fedavg.py:127-180), ClippingPostprocessor
     (fedsim/privacy/clipping.py:105-146) and GaussianCentralMechanism
-    (fedsim/privacy/mechanisms.py:146-193).  ``train`` = (lr, epochs, batch)."""
+    (fedsim/privacy/mechanisms.py:146-193).  ``train`` = (lr, epochs, batch).
+    ``mu``: FedProx proximal term (fedsim/algorithms/fedavg.py:218-227).
+    ``scaffold``: dict(server=flat control, users={uid: flat control}) for
+    Scaffold users (fedsim/algorithms/scaffold.py:46-79): the payload is
+    [model delta | control delta] and ``res.user_updates`` the new controls."""
     ids = tuple(users)
     cohort = sample_cohort(ids, cohort_size, ctx_seed)
     w_all = {u: float(users[u][0].shape[0]) for u in cohort}
@@ -339,9 +344,20 @@ def run_context(model, theta: dict, users: dict, cohort_size: int, ctx_seed: int
         if train is None:
             continue
         lr, E, B = train
-        after = fit_local(model, theta, X, y, user_perms(ctx_seed, uid, X.shape[0], E), lr, B) if E else theta
+        control = None
+        if scaffold is not None:
+            Dm = int(sum(dims.values()))
+            uc = scaffold["users"].get(uid, np.zeros(Dm))
+            control = _unflat(scaffold["server"] - uc, dims)
+        after = (fit_local(model, theta, X, y, user_perms(ctx_seed, uid, X.shape[0], E), lr, B, mu=mu,
+                           control=control) if E else theta)
         w = float(X.shape[0]) if weighting == "datapoints" else 1.0
         d = w * (flat(theta, dims) - flat(after, dims))       # fedsim/models/params.py:32-45
+        if scaffold is not None:                              # fedsim/algorithms/scaffold.py:63-79
+            steps = E * (-(-X.shape[0] // B))
+            new_c = uc - scaffold["server"] + d * (1.0 / (steps * lr))
+            res.user_updates.append((uid, new_c))
+            d = np.concatenate([d, new_c - uc])
         nrm = float(np.linalg.norm(d))
         c = bound is not None and nrm > bound                 # fedsim/privacy/clipping.py:49
         if c:
@@ -369,8 +385,14 @@ def run_context(model, theta: dict, users: dict, cohort_size: int, ctx_seed: int
             res.metrics["snr"] = (sig / np.sqrt(res.aggregate.size * std**2), 1.0)
         if std > 0 and noise:
             rng = np.random.default_rng(noise_seed(noise_base, t, pop))
-            res.noise = np.concatenate([rng.normal(0.0, std, k) for k in dims.values()])
+            groups = 2 if scaffold is not None else 1   # model/* entries, then control/*
+            res.noise = np.concatenate([rng.normal(0.0, std, k) for _ in range(groups) for k in dims.values()])
     return res
+
+
+def _unflat(v, dims):
+    off = np.cumsum([0] + list(dims.values()))
+    return {n: v[off[i]:off[i + 1]] for i, n in enumerate(dims)}
 
 
 def central_sgd(theta_flat: np.ndarray, aggregate: np.ndarray, weight: float, lr: float, noise=None):
@@ -380,13 +402,45 @@ def central_sgd(theta_flat: np.ndarray, aggregate: np.ndarray, weight: float, lr
     return theta_flat - lr * (agg * (1.0 / weight))
 
 
+def central_adam(theta_flat: np.ndarray, aggregate: np.ndarray, weight: float, lr: float, state: dict,
+                 beta1: float = 0.9, beta2: float = 0.99, eps: float = 0.1, noise=None):
+    """average -> AdamOptimizer.step (fedsim/models/optimizers.py:24-68, float64).
+    ``state`` carries m, v and the step count between calls (zero at start)."""
+    g = (aggregate if noise is None else aggregate + noise) * (1.0 / weight)
+    m = beta1 * state.get("m", np.zeros_like(g)) + (1 - beta1) * g
+    v = beta2 * state.get("v", np.zeros_like(g)) + (1 - beta2) * g * g
+    t = state.get("t", 0) + 1
+    state.update(m=m, v=v, t=t)
+    return theta_flat - lr * (m / (1 - beta1**t)) / (np.sqrt(v / (1 - beta2**t)) + eps)
+
+
+def adafedprox_update_mu(mu, previous, current, dec=0.9, inc=1.1, floor=1e-4, cap=1.0):
+    """fedsim/algorithms/fedavg.py:230-245."""
+    if current < previous:
+        return max(mu * dec, floor)
+    if current > previous:
+        return min(mu * inc, cap)
+    return mu
+
+
 def run_fedavg(model, train_users: dict, val_users: dict, *, iterations, cohort, eval_cohort, eval_every,
-               lr, epochs, batch, clr, weighting, bound, sigma, r, noise_base, run_seed, init_seed, world=1):
+               lr, epochs, batch, clr, weighting, bound, sigma, r, noise_base, run_seed, init_seed, world=1,
+               algorithm=None, optimizer=None):
     """run_simulation (fedsim/engine/loop.py:45-88) over FedAvg contexts
     (fedsim/algorithms/fedavg.py:97-125,183-198).  Returns per-iteration
-    flat thetas, metric rows sorted by (population, name), cohort digest."""
+    flat thetas, metric rows sorted by (population, name), cohort digest.
+    ``algorithm``: None / dict(kind="fedprox"|"adafedprox", mu) /
+    dict(kind="scaffold", num_train_users) (fedsim/algorithms/fedavg.py:201-296,
+    fedsim/algorithms/scaffold.py:28-120); ``optimizer``: None (SGD at clr) or
+    dict(kind="adam", lr, beta1, beta2, eps) (fedsim/models/optimizers.py:24-68)."""
     dims = model.dims
     theta = model.init(init_seed)
+    algo = algorithm or dict(kind="fedavg")
+    mu = float(algo.get("mu", 0.0)) if algo["kind"] in ("fedprox", "adafedprox") else 0.0
+    prev_loss = None
+    Dm = int(sum(dims.values()))
+    scaffold = dict(server=np.zeros(Dm), users={}) if algo["kind"] == "scaffold" else None
+    adam = {}
     thetas, rows = [], []
     digest = hashlib.sha256()
     for t in range(iterations):
@@ -400,7 +454,8 @@ def run_fedavg(model, train_users: dict, val_users: dict, *, iterations, cohort,
             parts = [run_context(model, theta, users, csize, cohort_seed(run_seed, t, pop),
                                  train=(lr, epochs, batch) if train else None, weighting=weighting,
                                  bound=bound, sigma=sigma, r=r, noise_base=noise_base, t=t, pop=pop,
-                                 world=world, rank=k) for k in range(world)]
+                                 world=world, rank=k, mu=mu, scaffold=scaffold if train else None)
+                     for k in range(world)]
             cohorts.append((pop, parts[0].cohort))
             for k, v in _merge_parts(parts).items():
                 metrics[(pop, k)] = v
@@ -408,11 +463,30 @@ def run_fedavg(model, train_users: dict, val_users: dict, *, iterations, cohort,
                 agg = sum(p.aggregate for p in parts if len(p.queue))
                 weight = sum(p.weight for p in parts)
                 agg_state = (agg, weight, parts[0].noise)  # one draw per context (rank-independent)
+            if train and scaffold is not None:
+                for p in parts:
+                    for uid, c in p.user_updates:
+                        scaffold["users"][uid] = c
         if agg_state is not None:
             agg, weight, nz = agg_state
-            new = central_sgd(flat(theta, dims), agg, weight, clr, nz)
-            off = np.cumsum([0] + list(dims.values()))
-            theta = {n: new[off[i]:off[i + 1]] for i, n in enumerate(dims)}
+            ctrl = None
+            if scaffold is not None:   # split the [model | control] payload
+                ctrl = (agg[Dm:] + (nz[Dm:] if nz is not None else 0.0)) * (1.0 / weight)
+                agg, nz = agg[:Dm], (nz[:Dm] if nz is not None else None)
+            if optimizer is not None and optimizer["kind"] == "adam":
+                new = central_adam(flat(theta, dims), agg, weight, optimizer["lr"], adam, optimizer["beta1"],
+                                   optimizer["beta2"], optimizer["eps"], nz)
+            else:
+                new = central_sgd(flat(theta, dims), agg, weight, clr, nz)
+            theta = _unflat(new, dims)
+            if ctrl is not None:
+                scaffold["server"] = scaffold["server"] + (weight / algo["num_train_users"]) * ctrl
+        if algo["kind"] == "adafedprox" and ("train", "loss") in metrics:
+            num, den = metrics[("train", "loss")]
+            cur = num / den
+            if prev_loss is not None:
+                mu = adafedprox_update_mu(mu, prev_loss, cur)
+            prev_loss = cur
         thetas.append(flat(theta, dims))
         for pop, c in cohorts:
             digest.update(repr((t, pop, c)).encode())

@@ -8,7 +8,17 @@ cohort work runs in hand-written sm_100a kernels (libfedsim_b200.so).
 """
 
 from .aggregator import Aggregator, SumAggregator, worker_reduce_sum
-from .algorithms import AlgorithmState, CohortPlan, FederatedAlgorithm, FedAvg, FedProx, UserResult
+from .algorithms import (
+    AdaFedProx,
+    AlgorithmState,
+    CohortPlan,
+    FederatedAlgorithm,
+    FedAvg,
+    FedProx,
+    Scaffold,
+    UserResult,
+    adafedprox_update_mu,
+)
 from .core import (
     CentralContext,
     Constant,
@@ -35,7 +45,7 @@ from .core import (
     user_seed,
     weighted,
 )
-from .device import DeviceParams, DevicePopulation, DeviceStatistics
+from .device import ControlStore, DeviceParams, DevicePopulation, DeviceStatistics
 from .engine import GpuSimulationEngine, IterationResult, client_permutations
 from .errors import (
     CohortTooLarge,
@@ -48,6 +58,7 @@ from .errors import (
     NativeUnavailable,
     NotClippedUpstream,
     TooFewPoints,
+    ZeroLocalSteps,
     ZeroWeight,
 )
 from .feddata import (
@@ -60,7 +71,7 @@ from .feddata import (
     save_partition,
 )
 from .loop import MetricsRow, SimulationResult, run_simulation
-from .models import CNN, MLP, LogisticRegression, Model, SGDOptimizer, central_step, count_local_steps
+from .models import CNN, MLP, AdamOptimizer, LogisticRegression, Model, SGDOptimizer, central_step, count_local_steps
 from .privacy import (
     AdaptiveClipConfig,
     ClippingPostprocessor,

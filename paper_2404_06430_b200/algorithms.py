@@ -10,7 +10,7 @@ fallback on the product path).
 
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+from dataclasses import dataclass, field, replace
 from typing import Any, Sequence
 
 from .core import (
@@ -56,6 +56,7 @@ class CohortPlan:
     weighting: str                  # "datapoints" (w = n_u) or "uniform" (w = 1)
     prox_mu: float = 0.0
     eval_batch_size: int = 0
+    scaffold: bool = False          # SCAFFOLD users: control-corrected SGD, [model | control] payload
 
 
 class FederatedAlgorithm:
@@ -188,3 +189,115 @@ class FedProx(FedAvg):
 
     def _algo_params(self, state: AlgorithmState, iteration: int) -> dict[str, float]:
         return {"mu": resolve(self.mu, iteration)}
+
+
+def adafedprox_update_mu(mu: float, previous_loss: float, current_loss: float, decrease_factor: float = 0.9,
+                         increase_factor: float = 1.1, floor: float = 1e-4, cap: float = 1.0) -> float:
+    """Loss-driven proximal strength (fedsim/algorithms/fedavg.py:230-245):
+    relax when the central training loss improves, tighten when it does not."""
+    if current_loss < previous_loss:
+        return max(mu * decrease_factor, floor)
+    if current_loss > previous_loss:
+        return min(mu * increase_factor, cap)
+    return mu
+
+
+class AdaFedProx(FedProx):
+    """FedProx with ``mu`` adapted from the central training loss
+    (fedsim/algorithms/fedavg.py:248-296).  The loss metric comes from the
+    GPU engine's pre-training evaluation of the train cohort."""
+
+    def __init__(self, *args, mu: float = 0.1, mu_decrease_factor: float = 0.9, mu_increase_factor: float = 1.1,
+                 mu_floor: float = 1e-4, mu_cap: float = 1.0, **kwargs):
+        super().__init__(*args, mu=mu, **kwargs)
+        self.mu_decrease_factor = mu_decrease_factor
+        self.mu_increase_factor = mu_increase_factor
+        self.mu_floor = mu_floor
+        self.mu_cap = mu_cap
+
+    def initial_state(self) -> AlgorithmState:
+        state = super().initial_state()
+        state.extra["mu"] = resolve(self.mu, 0)
+        state.extra["previous_train_loss"] = None
+        return state
+
+    def _algo_params(self, state: AlgorithmState, iteration: int) -> dict[str, float]:
+        return {"mu": state.extra["mu"]}
+
+    def process_aggregated_statistics_all_contexts(self, state, contexts, aggregates, iteration_metrics,
+                                                   user_updates) -> AlgorithmState:
+        state = super().process_aggregated_statistics_all_contexts(state, contexts, aggregates, iteration_metrics,
+                                                                   user_updates)
+        loss = iteration_metrics.get((Population.TRAIN.value, "loss"))
+        if loss is not None:
+            current = loss.value
+            previous = state.extra["previous_train_loss"]
+            if previous is not None:
+                state.extra["mu"] = adafedprox_update_mu(state.extra["mu"], previous, current,
+                                                         self.mu_decrease_factor, self.mu_increase_factor,
+                                                         self.mu_floor, self.mu_cap)
+            state.extra["previous_train_loss"] = current
+        return state
+
+
+MODEL_PREFIX = "model/"
+CONTROL_PREFIX = "control/"
+
+
+class Scaffold(FedAvg):
+    """Stochastic controlled averaging with per-user control variates
+    (fedsim/algorithms/scaffold.py:28-120).  Same constructor and semantics:
+    uniform weighting only; users train with g - c_i + c and report
+    [model delta | control delta]; the server control moves by the cohort
+    fraction of the mean control delta.  On the GPU the controls live in a
+    device store (``state.extra["user_controls"]``, a :class:`ControlStore`)
+    and the server control is a flat fp32 device vector; the engine runs
+    the cohort's corrections, payload and user updates as kernels
+    (fb_scaffold_*)."""
+
+    def __init__(self, *args, num_train_users: int, **kwargs):
+        kwargs.setdefault("weighting", "uniform")
+        if kwargs["weighting"] != "uniform":
+            raise ValueError("control-variate averaging must be uniform")
+        super().__init__(*args, **kwargs)
+        if num_train_users < 1:
+            raise ValueError("num_train_users must be >= 1")
+        self.num_train_users = num_train_users
+
+    def initial_state(self) -> AlgorithmState:
+        state = super().initial_state()
+        state.extra["server_control"] = None   # flat device vector, created by the engine (zeros)
+        state.extra["user_controls"] = None    # ControlStore, created by the engine
+        return state
+
+    def cohort_plan(self, state: AlgorithmState, context: CentralContext) -> CohortPlan:
+        plan = super().cohort_plan(state, context)
+        return CohortPlan(plan.model, plan.train, plan.weighting, 0.0, plan.eval_batch_size, scaffold=True)
+
+    def process_aggregated_statistics_all_contexts(self, state, contexts, aggregates, iteration_metrics,
+                                                   user_updates) -> AlgorithmState:
+        store = state.extra["user_controls"]
+        if user_updates:
+            if hasattr(user_updates, "matrix"):
+                store.set_rows(user_updates.uids, user_updates.matrix)
+            else:
+                for uid, vec in user_updates:
+                    store.set_rows([uid], vec.reshape(1, -1))
+        agg = next((a for c, a in zip(contexts, aggregates) if c.do_training), None)
+        if agg is None:
+            return state
+        D = state.params.num_params
+        averaged = average(agg)
+        model_part, control_part = averaged.split_payload([D, D])
+        model_part = replace(model_part, dims={n[len(MODEL_PREFIX):]: k for n, k in model_part.dims.items()})
+        state.params = central_step(state.optimizer, state.params, model_part, contexts[0].iteration)
+        # server control moves by the cohort fraction of the mean control delta
+        fraction = agg.weight / self.num_train_users
+        server = state.extra["server_control"]
+        from . import native  # local import: the host mirror imports without the library
+
+        nz = control_part.noise
+        native.call("fb_noise_avg_sgd_f32", native.ptr(server), native.ptr(control_part.flat), D, 0.0, 0,
+                    native.ptr(nz.injected) if nz is not None and nz.injected is not None else None,
+                    float(control_part.scale), -float(fraction), None, native.stream_handle())
+        return state

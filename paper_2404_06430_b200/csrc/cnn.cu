@@ -1971,6 +1971,181 @@ __global__ void __launch_bounds__(BX_THREADS, 1) conv2_bwd_x_tc_kernel(
   if (warp == 1) tc::tmem_dealloc<2 * BX_ACC>(tmem);
 }
 
+// ------------------------------------------ conv1 backward-weights (tcgen05)
+// dW1[o, k] = sum over the client's samples and positions p of dz1[p, o] * xcol[p, k],
+// k = (ci, ky, kx) (27) plus a constant-1 column k = 27 that yields the bias
+// gradient.  A GEMM with K = positions, done on the tensor core in kind::tf32
+// with a 3xTF32-style split held in the operand ROWS instead of extra MMAs:
+//   A (M = 128) rows 0-31 = tf32(dz1) hi, rows 32-63 = lo  (rows 64-127 unused)
+//   B (N = 64)  rows 0-31 = tf32(xcol) hi, rows 32-63 = lo
+// so ONE 128x64x8 MMA per 8 positions forms hi*hi, hi*lo, lo*hi and lo*lo in
+// four quadrants of the accumulator.  Operands are staged per 128-position
+// chunk by the CTA (K-major SWIZZLE_128B, transposed from the NHWC dz1 and
+// im2col'ed from the image in smem), double-buffered against the MMAs; each
+// chunk's accumulator (a 16-MMA chain) is drained by warps 0 / 1 into fp32
+// registers (round-to-nearest adds) while the next chunk runs.
+constexpr int W1_CH = 64;                           // positions per chunk
+constexpr int W1_CPS = (S1 * S1 + W1_CH - 1) / W1_CH;  // 15 chunks per sample (last: 4 positions)
+constexpr int W1_ATOM = 16 * 1024;                  // per 32-position K atom: A rows 0-63 (8 KB) | B rows 0-63 (8 KB)
+constexpr int W1_STAGE = (W1_CH / 32) * W1_ATOM;    // 32 KB
+constexpr int W1_THREADS = 256;
+constexpr int W1_SMEM = 1024 + 2 * W1_STAGE + IMG * 4 + 32 * 33 * 4 + 64;
+constexpr uint32_t W1_IDESC = tc::idesc_tf32(128, 64);
+
+__global__ void __launch_bounds__(W1_THREADS, 2) conv1_bwd_w_tc_kernel(const float* __restrict__ X,
+                                                                      const int64_t* __restrict__ slot_row,
+                                                                      const float* __restrict__ dz1, int B,
+                                                                      const int32_t* __restrict__ client_nb,
+                                                                      float* __restrict__ delta, int64_t ld, Step st) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* img = reinterpret_cast<float*>(sm + 2 * W1_STAGE);  // [3][32][32]
+  float* red = img + IMG;                                    // [32][33]: warp 1's sums
+  uint64_t* done = reinterpret_cast<uint64_t*>(red + 32 * 33);  // [2] MMA completion per stage
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 2);
+  const int c = blockIdx.x;
+  const int nb = client_nb[c];
+  if (nb == 0) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, t = threadIdx.x;
+  const uint32_t s0 = tc::smem_u32(sm), simg = tc::smem_u32(img);
+  // rows 28-31 / 60-63 of B (padding of k) stay zero; staging never writes them
+  for (int i = t; i < 2 * W1_STAGE / 16; i += W1_THREADS) reinterpret_cast<uint4*>(sm)[i] = make_uint4(0, 0, 0, 0);
+  if (t == 0) {
+    tc::mbar_init(&done[0], 1);
+    tc::mbar_init(&done[1], 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc<128>(tmem_slot);
+  tc::fence_proxy_async();
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  float run[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) run[k] = 0.f;
+  // drain chunk i's accumulator into run[] (warp 0: hi rows, warp 1: lo rows)
+  auto drain = [&](int i) {
+    tc::mbar_wait(&done[i & 1], (i >> 1) & 1);
+    tc::tc_fence_after();
+    const uint32_t base = tmem + ((uint32_t)(warp * 32) << 16) + (i & 1) * 64;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      uint32_t v0[16], v1[16];
+      tc::tmem_ld16(base + 16 * h, v0);
+      tc::tmem_ld16(base + 32 + 16 * h, v1);
+      tc::tmem_ld_wait();
+#pragma unroll
+      for (int k = 0; k < 16; ++k) run[16 * h + k] += __uint_as_float(v0[k]) + __uint_as_float(v1[k]);
+    }
+    tc::tc_fence_before();
+  };
+  // A staging: coalesced float4 f = j * 256 + t of the chunk's [64 pos][32 o] dz1 block
+  // (position f / 8, channel quad f % 8); the next chunk is prefetched into
+  // registers a chunk ahead
+  const int nchunks = nb * W1_CPS;
+  auto load_dz = [&](int i, float4 (&v)[W1_CH / 32]) {
+    const int b = i / W1_CPS, p0 = (i - b * W1_CPS) * W1_CH;
+    const float4* dzn = reinterpret_cast<const float4*>(dz1 + ((int64_t)c * B + b) * A1 + (int64_t)p0 * C1);
+#pragma unroll
+    for (int j = 0; j < W1_CH / 32; ++j) {
+      const int f = j * W1_THREADS + t;
+      v[j] = p0 + (f >> 3) < S1 * S1 ? __ldg(dzn + f) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  float4 cur[W1_CH / 32], nxt[W1_CH / 32];
+  load_dz(0, cur);
+  const int kq = t >> 6;
+  uint32_t koff[7];  // byte offset of im2col row kq*7+kk relative to the output position
+#pragma unroll
+  for (int kk = 0; kk < 7; ++kk) {
+    const int k = min(kq * 7 + kk, 26), ci = k / 9, ky = (k % 9) / 3, kx = k % 3;
+    koff[kk] = 4 * (ci * S0 * S0 + ky * S0 + kx);
+  }
+  for (int i = 0; i < nchunks; ++i) {
+    const int b = i / W1_CPS, ch = i - b * W1_CPS, p0 = ch * W1_CH;
+    const int64_t n = (int64_t)c * B + b;
+    const uint32_t stg = s0 + (i & 1) * W1_STAGE;
+    if (i + 1 < nchunks) load_dz(i + 1, nxt);
+    if (i >= 2) tc::mbar_wait(&done[i & 1], ((i - 2) >> 1) & 1);  // chunk i-2's MMAs done reading this stage
+    if (ch == 0) {
+      __syncthreads();  // previous sample's im2col reads finished
+      const float4* src = reinterpret_cast<const float4*>(X + slot_row[n] * IMG);
+      for (int q = t; q < IMG / 4; q += W1_THREADS) reinterpret_cast<float4*>(img)[q] = __ldg(src + q);
+      __syncthreads();
+    }
+#pragma unroll
+    for (int j = 0; j < W1_CH / 32; ++j) {
+      const int f = j * W1_THREADS + t, pl = f >> 3, oq = f & 7;
+      const float vv[4] = {cur[j].x, cur[j].y, cur[j].z, cur[j].w};
+      const uint32_t atom = stg + (pl >> 5) * W1_ATOM;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float hi, lo;
+        tc::split_tf32(vv[e], hi, lo);
+        const int o = 4 * oq + e;
+        tc::sts_f32(atom + tc::sw128_offset(o, pl & 31), hi);
+        tc::sts_f32(atom + tc::sw128_offset(32 + o, pl & 31), lo);
+      }
+    }
+    // B: thread = position (64) x 7 of the 28 im2col rows (k = kq*7 + kk)
+    {
+      const int pl = t & (W1_CH - 1);
+      const int p = p0 + pl, y = p / S1, x = p - y * S1;
+      const bool valid = p < S1 * S1;
+      const uint32_t atom = stg + (pl >> 5) * W1_ATOM + 8192;
+      const uint32_t ib = simg + 4 * (y * S0 + x);
+#pragma unroll
+      for (int kk = 0; kk < 7; ++kk) {
+        const int k = kq * 7 + kk;
+        float v = 0.f;
+        if (valid) v = k < 27 ? tc::lds_f32(ib + koff[kk]) : 1.f;
+        float hi, lo;
+        tc::split_tf32(v, hi, lo);
+        tc::sts_f32(atom + tc::sw128_offset(k, pl & 31), hi);
+        tc::sts_f32(atom + tc::sw128_offset(32 + k, pl & 31), lo);
+      }
+    }
+    tc::fence_proxy_async();
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    if (warp == 0) {
+      if (tc::elect_one()) {
+        const uint32_t d = tmem + (i & 1) * 64;
+#pragma unroll
+        for (int kk = 0; kk < W1_CH / 8; ++kk) {
+          const uint32_t a = stg + (kk >> 2) * W1_ATOM + (kk & 3) * 32;
+          tc::mma_tf32(d, tc::sdesc_k128(a), tc::sdesc_k128(a + 8192), W1_IDESC, kk != 0);
+        }
+        tc::mma_commit(&done[i & 1]);
+      }
+      __syncwarp();
+    }
+    if (warp < 2 && i >= 1) drain(i - 1);
+#pragma unroll
+    for (int j = 0; j < W1_CH / 32; ++j) cur[j] = nxt[j];
+  }
+  if (warp < 2) drain(nchunks - 1);
+  // combine the hi-row (warp 0) and lo-row (warp 1) sums; update dW1 and b1
+  if (warp == 1)
+#pragma unroll
+    for (int k = 0; k < 32; ++k) red[lane * 33 + k] = run[k];
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  if (warp == 0) {
+    float* dc = delta + (int64_t)c * ld;
+#pragma unroll
+    for (int k = 0; k < 28; ++k) {
+      const float g = run[k] + red[lane * 33 + k];
+      float& dl = k < 27 ? dc[O_W1 + (int64_t)lane * (C0 * 9) + k] : dc[O_B1 + lane];
+      dl += st.lr * (g - st.mu * dl);
+    }
+    tc::tmem_dealloc<128>(tmem);
+  }
+}
+
 int g_conv_impl = 1;  // 1 = tcgen05 (product path), 0 = FP32 CUDA-core kernels (validation)
 
 
@@ -2249,6 +2424,7 @@ int set_smem_limits() {
   cudaFuncSetAttribute(fc1_materialize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FC1M_SMEM);
   cudaFuncSetAttribute(fc1_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FT_SMEM);
   cudaFuncSetAttribute(conv2_bwd_w_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BW_SMEM);
+  cudaFuncSetAttribute(conv1_bwd_w_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, W1_SMEM);
   done = true;
   return launch_status("cnn: cudaFuncSetAttribute");
 }
@@ -2519,8 +2695,12 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
         FB_LAUNCH("conv2_bwd_w_kernel", s, conv2_bwd_w_kernel<<<Cw, 256, C2W_SMEM, s>>>(ws.dp, ws.pooled, ws.code, ws.a1, nullptr, B, ws.client_nb, dlt, ld_delta,
                                                      sp));
       }
-      FB_LAUNCH("conv1_bwd_w_kernel", s, conv1_bwd_w_kernel<<<Cw, C1B_WARPS * 32, 0, s>>>(X, ws.slot_row, ws.dz1, B, ws.client_nb, dlt,
-                                                                       ld_delta, sp));
+      if (g_conv_impl == 1)
+        FB_LAUNCH("conv1_bwd_w_tc_kernel", s, conv1_bwd_w_tc_kernel<<<Cw, W1_THREADS, W1_SMEM, s>>>(
+                                                   X, ws.slot_row, ws.dz1, B, ws.client_nb, dlt, ld_delta, sp));
+      else
+        FB_LAUNCH("conv1_bwd_w_kernel", s, conv1_bwd_w_kernel<<<Cw, C1B_WARPS * 32, 0, s>>>(
+                                                X, ws.slot_row, ws.dz1, B, ws.client_nb, dlt, ld_delta, sp));
       st = fb::launch_status("local_sgd_cnn step");
       if (st) return st;
     }

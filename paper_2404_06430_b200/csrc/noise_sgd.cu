@@ -107,6 +107,32 @@ __global__ void __launch_bounds__(kThreads) noise_avg_sgd_kernel(
   }
 }
 
+// K4 + central Adam (fedsim/models/optimizers.py:24-68): the noised sum is
+// averaged (a = (agg + noise) * inv_weight) and used as the gradient of one
+// bias-corrected Adam step; m and v are updated in place.
+__global__ void __launch_bounds__(kThreads) noise_avg_adam_kernel(
+    float* __restrict__ theta, float* __restrict__ m1, float* __restrict__ m2, const float* __restrict__ agg,
+    int64_t D, float noise_std, uint64_t seed, const float* __restrict__ injected, float inv_weight, float lr,
+    float b1, float b2, float eps, float inv_bc1, float inv_bc2, float* __restrict__ agg_out) {
+  const int64_t g = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  const int64_t i0 = g << 2;
+  if (i0 >= D) return;
+  float z[4] = {0.f, 0.f, 0.f, 0.f};
+  if (!injected && noise_std != 0.0f) normal4(seed, g, z);
+  for (int j = 0; j < 4 && i0 + j < D; ++j) {
+    const int64_t i = i0 + j;
+    float a = agg[i];
+    a = injected ? a + injected[i] : fmaf(noise_std, z[j], a);
+    if (agg_out) agg_out[i] = a;
+    a *= inv_weight;
+    const float m = fmaf(b1, m1[i], (1.f - b1) * a);
+    const float v = fmaf(b2, m2[i], (1.f - b2) * a * a);
+    m1[i] = m;
+    m2[i] = v;
+    theta[i] -= lr * (m * inv_bc1) / (sqrtf(v * inv_bc2) + eps);
+  }
+}
+
 }  // namespace
 }  // namespace fb
 
@@ -134,6 +160,25 @@ int fb_noise_avg_sgd_f32(float* theta, const float* agg, int64_t D, double noise
                              fb::as_stream(stream)>>>(theta, agg, D, (float)noise_std, seed, injected,
                                                       (float)(lr * inv_weight), agg_out));
   return fb::launch_status("noise_avg_sgd_kernel");
+}
+
+int fb_noise_avg_adam_f32(float* theta, float* m1, float* m2, const float* agg, int64_t D, double noise_std,
+                          uint64_t seed, const float* injected, double inv_weight, double lr, double beta1,
+                          double beta2, double eps, int64_t step, float* agg_out, void* stream) {
+  FB_REQUIRE(D >= 0 && noise_std >= 0.0, "noise_avg_adam: need D >= 0 and noise_std >= 0");
+  FB_REQUIRE(inv_weight >= 0.0 && isfinite(inv_weight), "noise_avg_adam: bad inverse weight");
+  FB_REQUIRE(beta1 >= 0.0 && beta1 < 1.0 && beta2 >= 0.0 && beta2 < 1.0, "noise_avg_adam: betas must be in [0, 1)");
+  FB_REQUIRE(eps > 0.0 && step >= 1, "noise_avg_adam: need adaptivity_degree > 0 and step >= 1");
+  if (D == 0) return FB_OK;
+  // bias corrections in double on the host side of the launch (1 - beta^t)
+  const double bc1 = 1.0 - pow(beta1, (double)step), bc2 = 1.0 - pow(beta2, (double)step);
+  const int64_t groups = (D + 3) >> 2;
+  FB_LAUNCH("noise_avg_adam_kernel", fb::as_stream(stream),
+            fb::noise_avg_adam_kernel<<<(unsigned)((groups + fb::kThreads - 1) / fb::kThreads), fb::kThreads, 0,
+                                        fb::as_stream(stream)>>>(
+                theta, m1, m2, agg, D, (float)noise_std, seed, injected, (float)inv_weight, (float)lr, (float)beta1,
+                (float)beta2, (float)eps, (float)(1.0 / bc1), (float)(1.0 / bc2), agg_out));
+  return fb::launch_status("noise_avg_adam_kernel");
 }
 
 }  // extern "C"

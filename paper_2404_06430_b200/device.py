@@ -15,7 +15,7 @@
 from __future__ import annotations
 
 from dataclasses import dataclass, field, replace
-from typing import Iterator, Mapping
+from typing import Iterator, Mapping, Sequence
 
 import numpy as np
 
@@ -209,6 +209,63 @@ class DeviceStatistics:
             torch.distributed.broadcast(out, src=0, group=comm.group)
         return DeviceParams(out, params.dims)
 
+    def apply_adam(self, params: DeviceParams, opt, lr: float) -> DeviceParams:
+        """One central Adam step (fedsim/models/optimizers.py:24-68) on the
+        averaged noised aggregate: K4 + Adam in one kernel.  The moments live
+        on the device in ``opt`` (lazily zero on the first step, as the
+        reference); multi-rank as :meth:`apply_sgd`."""
+        if params.num_params != self.flat.numel():
+            raise IncompatibleShapes("aggregate and parameters differ in size")
+        torch = _torch()
+        if opt.first_moment is None:
+            opt.first_moment = torch.zeros_like(params.flat)
+            opt.second_moment = torch.zeros_like(params.flat)
+        opt.step_count += 1
+        out = params.flat.clone()
+        comm = self.comm
+        run_here = comm.world_size == 1 or comm.epilogue == "replicated" or comm.rank == 0
+        if run_here:
+            nz = self.noise
+            native.call(
+                "fb_noise_avg_adam_f32", native.ptr(out), native.ptr(opt.first_moment), native.ptr(opt.second_moment),
+                native.ptr(self.flat), self.flat.numel(), nz.std if nz else 0.0, nz.seed if nz else 0,
+                native.ptr(nz.injected) if nz is not None and nz.injected is not None else None,
+                float(self.scale), float(lr), float(opt.beta1), float(opt.beta2), float(opt.adaptivity_degree),
+                int(opt.step_count), None, native.stream_handle(),
+            )
+        if comm.world_size > 1 and comm.epilogue == "rank0":
+            torch.distributed.broadcast(out, src=0, group=comm.group)
+        return DeviceParams(out, params.dims)
+
+    def split_payload(self, sizes: Sequence[int]) -> list["DeviceStatistics"]:
+        """Consecutive payload groups of an (averaged) aggregate as separate
+        device statistics sharing its scale and weight; the pending noise is
+        sliced the same way (Philox draws are materialised once for the whole
+        vector so every element keeps its counter)."""
+        torch = _torch()
+        nz = self.noise
+        full = None
+        if nz is not None and nz.std != 0.0:
+            full = nz.injected
+            if full is None:
+                full = torch.empty_like(self.flat)
+                native.call("fb_gaussian_f32", native.ptr(full), full.numel(), nz.std, nz.seed, 0, 0,
+                            native.stream_handle())
+        out, lo = [], 0
+        names = list(self.dims)
+        for k in sizes:
+            sub, acc = {}, 0
+            while names and acc < k:
+                n = names.pop(0)
+                sub[n] = self.dims[n]
+                acc += self.dims[n]
+            if acc != k:
+                raise IncompatibleShapes("payload groups do not align with the entries")
+            noise = None if nz is None else PendingNoise(nz.std, nz.seed, None if full is None else full[lo:lo + k])
+            out.append(replace(self, flat=self.flat[lo:lo + k], dims=sub, bookkeeping={}, noise=noise))
+            lo += k
+        return out
+
     def materialize(self):
         """Device fp32 payload with pending noise and scale applied."""
         torch = _torch()
@@ -270,3 +327,68 @@ class DevicePopulation:
             self.y = torch.from_numpy(y).pin_memory()
         self.total_rows = total
         self.max_label = int(y.max()) if total else 0
+
+
+class ControlStore:
+    """Per-user SCAFFOLD control vectors on the device (the reference keeps
+    them server-side keyed by user id, fedsim/algorithms/scaffold.py:34-57):
+    one [capacity, ld] fp32 matrix plus a host user -> row map; a user
+    without a row has the zero control."""
+
+    def __init__(self, D: int, device):
+        self.D = int(D)
+        self.ld = (self.D + 3) & ~3
+        self.device = device
+        self.index: dict[str, int] = {}
+        self.mat = None
+
+    def __len__(self) -> int:
+        return len(self.index)
+
+    def __contains__(self, uid) -> bool:
+        return uid in self.index
+
+    def _reserve(self, n: int) -> None:
+        torch = _torch()
+        cap = 0 if self.mat is None else self.mat.shape[0]
+        if n <= cap:
+            return
+        new = torch.zeros((max(n, 2 * cap, 16), self.ld), dtype=torch.float32, device=self.device)
+        if self.mat is not None:
+            new[:cap].copy_(self.mat)
+        self.mat = new
+
+    def rows_of(self, uids: Sequence[str]) -> np.ndarray:
+        return np.fromiter((self.index.get(u, -1) for u in uids), dtype=np.int32, count=len(uids))
+
+    def matrix(self):
+        self._reserve(1)
+        return self.mat
+
+    def set_rows(self, uids: Sequence[str], src) -> None:
+        """store[uid] = src[c] for every user (one scatter kernel)."""
+        for u in uids:
+            if u not in self.index:
+                self.index[u] = len(self.index)
+        self._reserve(len(self.index))
+        torch = _torch()
+        rows = torch.from_numpy(self.rows_of(uids)).to(self.device)
+        native.call("fb_scatter_rows_f32", native.ptr(self.mat), self.ld, native.ptr(rows), native.ptr(src),
+                    src.stride(0), len(uids), self.D, native.stream_handle())
+
+    def get(self, uid: str) -> np.ndarray:
+        """Host copy of one user's control (tests / inspection)."""
+        if uid not in self.index:
+            return np.zeros(self.D)
+        return self.mat[self.index[uid], : self.D].double().cpu().numpy()
+
+
+class ControlUpdates(list):
+    """The engine's SCAFFOLD user updates: a list of (user_id, device row)
+    pairs as the reference's ``user_updates`` (fedsim/algorithms/scaffold.py:79),
+    with the batched [C, ld] matrix kept for a one-kernel store update."""
+
+    def __init__(self, uids: Sequence[str], matrix):
+        super().__init__((u, matrix[c]) for c, u in enumerate(uids))
+        self.uids = list(uids)
+        self.matrix = matrix

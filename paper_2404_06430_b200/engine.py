@@ -28,7 +28,8 @@ import numpy as np
 from . import cnn, native
 from .aggregator import SumAggregator
 from .core import CentralContext, MetricKind, MetricValue, Population, merge_metrics, user_seed
-from .device import Comm, DeviceParams, DevicePopulation, DeviceStatistics, Workspace
+from .algorithms import CONTROL_PREFIX, MODEL_PREFIX
+from .device import Comm, ControlStore, ControlUpdates, DeviceParams, DevicePopulation, DeviceStatistics, Workspace
 from .errors import EngineError
 from .feddata import FederatedDataset, sample_cohort
 from .models import CNN, MLP, LogisticRegression
@@ -189,14 +190,19 @@ class _ModelRunner:
                     stream)
 
     def local_sgd(self, theta, pop, row_start, num_rows, perms, perm_off, C, tp, prox_mu, delta, nonfinite, stream,
-                  h_num_rows):
+                  h_num_rows, control=None):
         if self.kind == "cnn":
+            if control is not None:
+                raise ValueError("GpuSimulationEngine: control variates are supported for the logistic / MLP "
+                                 "models (the reference's own models), not the CNN")
             return cnn.local_sgd_cohort(self, theta, pop, row_start, num_rows, perms, perm_off, C, tp,
                                         prox_mu, delta, nonfinite, stream, h_num_rows)
         fn = f"fb_local_sgd_{self.kind}_f32"
         native.call(fn, native.ptr(theta), *self.dims, native.ptr(pop.X), native.ptr(pop.y),
                     native.ptr(row_start), native.ptr(num_rows), native.ptr(perms), native.ptr(perm_off), C,
-                    tp.num_epochs, tp.batch_size, float(tp.learning_rate), float(prox_mu), None, 0,
+                    tp.num_epochs, tp.batch_size, float(tp.learning_rate), float(prox_mu),
+                    native.ptr(control) if control is not None else None,
+                    control.stride(0) if control is not None else 0,
                     native.ptr(delta), self.ld, native.ptr(nonfinite), stream)
 
 
@@ -300,18 +306,30 @@ class GpuSimulationEngine:
             raise ValueError(f"GpuSimulationEngine: unsupported algorithm {type(algorithm).__name__}")
         if not isinstance(state.params, DeviceParams):
             state.params = DeviceParams.from_host(state.params, self.device)
-        aggregates, metrics, cohorts = [], {}, []
+        aggregates, metrics, cohorts, updates = [], {}, [], []
         for ctx in contexts:
-            agg, ctx_metrics, cohort = self._run_context(algorithm, state, ctx)
+            agg, ctx_metrics, cohort, ctx_updates = self._run_context(algorithm, state, ctx)
+            if ctx_updates:
+                updates = ctx_updates if not updates else updates + list(ctx_updates)
             aggregates.append(agg)
             pop = ctx.population.value
             for name, val in ctx_metrics.items():
                 key = (pop, name)
                 metrics[key] = metrics[key] + val if key in metrics else val
             cohorts.append((pop, cohort))
-        return IterationResult(tuple(aggregates), metrics, [], tuple(cohorts))
+        return IterationResult(tuple(aggregates), metrics, updates, tuple(cohorts))
 
     # ------------------------------------------------------------ internals
+    def _controls(self, state, D: int):
+        """SCAFFOLD server control (flat fp32) and per-user control store,
+        created on the device on first use (zero, as the reference)."""
+        torch = _torch()
+        if state.extra.get("server_control") is None:
+            state.extra["server_control"] = torch.zeros(D, dtype=torch.float32, device=self.device)
+        if state.extra.get("user_controls") is None:
+            state.extra["user_controls"] = ControlStore(D, self.device)
+        return state.extra["server_control"], state.extra["user_controls"]
+
     def _run_context(self, algorithm, state, ctx: CentralContext):
         torch = _torch()
         pop_key = ctx.population
@@ -322,10 +340,14 @@ class GpuSimulationEngine:
                                    poisson_rate=self._poisson_rate, base_policy=self._base_policy,
                                    base_value=self._base_value)
         if not cohort:
-            return None, {}, cohort
+            return None, {}, cohort, None
 
         plan = algorithm.cohort_plan(state, ctx)
         runner = self._runner(plan.model)
+        scaffold = bool(getattr(plan, "scaffold", False)) and plan.train is not None
+        if scaffold and self.world_size > 1:
+            raise ValueError("GpuSimulationEngine: Scaffold runs single-rank (the per-user control store is not "
+                             "sharded across ranks)")
         pop = self.population(pop_key)
         if pop.dim != plan.model.input_dim:
             raise ValueError(f"dataset dim {pop.dim} != model input dim {plan.model.input_dim}")
@@ -352,6 +374,16 @@ class GpuSimulationEngine:
             w = (num_rows.astype(np.float32) if plan.weighting == "datapoints"
                  else np.ones(C, dtype=np.float32))
             host += [perm_flat, perm_off, w]
+            if scaffold:  # control update scale 1 / (steps * lr) (fedsim/algorithms/scaffold.py:46-70)
+                steps = tp.num_epochs * (-(-num_rows.astype(np.int64) // tp.batch_size))
+                denom = steps.astype(np.float64) * float(tp.learning_rate)
+                if C and (denom == 0.0).any():
+                    c0 = int(np.flatnonzero(denom == 0.0)[0])
+                    raise EngineError(
+                        f"iteration {ctx.iteration}, population {pop_key.value!r}, user {queue[c0]!r}: "
+                        f"control update divides by steps * learning_rate; got {int(steps[c0])} steps at lr "
+                        f"{tp.learning_rate}")
+                ctrl_scale = (1.0 / denom).astype(np.float32) if C else np.zeros(0, dtype=np.float32)
         if gathered:
             host.append(src_start)
         dev = self._staging.upload(host)
@@ -380,25 +412,45 @@ class GpuSimulationEngine:
             runner.eval(theta.flat, pop, d_row_start, d_num_rows, C, loss, correct, stream, num_rows)
 
         agg_flat = None
+        updates = None
         if train:
             d_perms, d_perm_off, d_w = dev[2], dev[3], dev[4]
-            agg_flat = torch.empty(runner.D, dtype=torch.float32, device=self.device)
+            # SCAFFOLD: the payload is [model delta | control delta] (fedsim/algorithms/scaffold.py:63-79)
+            Dp = 2 * runner.D if scaffold else runner.D
+            agg_flat = torch.empty(Dp, dtype=torch.float32, device=self.device)
             if C:
                 delta = self.ws.tensor("delta", (C, runner.ld), torch.float32)
+                control = None
+                if scaffold:
+                    server, store = self._controls(state, runner.D)
+                    d_rows = torch.from_numpy(store.rows_of(queue)).to(self.device, non_blocking=True)
+                    control = self.ws.tensor("scaffold_correction", (C, runner.ld), torch.float32)
+                    native.call("fb_scaffold_correction_f32", native.ptr(server), native.ptr(store.matrix()),
+                                store.ld, native.ptr(d_rows), C, runner.D, native.ptr(control), runner.ld, stream)
                 runner.local_sgd(theta.flat, pop, d_row_start, d_num_rows, d_perms, d_perm_off, C, plan.train,
-                                 plan.prox_mu, delta, nonfinite, stream, num_rows)
+                                 plan.prox_mu, delta, nonfinite, stream, num_rows, control=control)
+                payload, ldp = delta, runner.ld
+                if scaffold:
+                    ldp = (Dp + 3) & ~3
+                    payload = self.ws.tensor("scaffold_payload", (C, ldp), torch.float32)
+                    new_control = torch.empty((C, runner.ld), dtype=torch.float32, device=self.device)
+                    d_scale = torch.from_numpy(ctrl_scale).to(self.device, non_blocking=True)
+                    native.call("fb_scaffold_payload_f32", native.ptr(delta), runner.ld, native.ptr(server),
+                                native.ptr(store.matrix()), store.ld, native.ptr(d_rows), native.ptr(d_scale), C,
+                                runner.D, native.ptr(payload), ldp, native.ptr(new_control), runner.ld, stream)
+                    updates = ControlUpdates(queue, new_control)
                 coef = self.ws.tensor("coef", (Cp,), torch.float32)
                 bound = self._clip.current_bound if self._clip is not None else 0.0
-                wsb = native.call("fb_clip_workspace_bytes", C, runner.D)
+                wsb = native.call("fb_clip_workspace_bytes", C, Dp)
                 kws = self.ws.get("clip_ws", wsb)
                 nf2 = self.ws.tensor("nonfinite2", (Cp,), torch.int32)
-                native.call("fb_delta_norm_clip_f32", native.ptr(delta), runner.ld, C, runner.D, native.ptr(d_w),
+                native.call("fb_delta_norm_clip_f32", native.ptr(payload), ldp, C, Dp, native.ptr(d_w),
                             float(bound), native.ptr(norm), native.ptr(coef), native.ptr(clipped),
                             native.ptr(nf2), native.ptr(kws), kws.numel(), stream)
                 torch.bitwise_or(nonfinite[:C], nf2[:C], out=nonfinite[:C])
-                wsb = native.call("fb_weighted_sum_workspace_bytes", C, runner.D)
+                wsb = native.call("fb_weighted_sum_workspace_bytes", C, Dp)
                 sws = self.ws.get("sum_ws", wsb)
-                native.call("fb_weighted_sum_f32", native.ptr(delta), runner.ld, C, runner.D, native.ptr(coef),
+                native.call("fb_weighted_sum_f32", native.ptr(payload), ldp, C, Dp, native.ptr(coef),
                             native.ptr(agg_flat), 0, native.ptr(sws), sws.numel(), stream)
             else:
                 agg_flat.zero_()
@@ -434,13 +486,16 @@ class GpuSimulationEngine:
                 "per_user_accuracy": MetricValue(MetricKind.PER_USER, float(sums[3]), float(sums[4])),
             }
         if not train:
-            return None, metrics, cohort
+            return None, metrics, cohort, None
 
         book = {}
         if self._clip is not None:
             book = {CLIPPED_KEY: np.array([sums[5]]), COUNT_KEY: np.array([sums[6]]),
                     NORM_KEY: np.array([sums[7]])}
-        aggregate = DeviceStatistics(flat=agg_flat, dims=dict(plan.model.param_dims), weight=float(sums[8]),
+        dims = dict(plan.model.param_dims)
+        if scaffold:
+            dims = {**{MODEL_PREFIX + n: k for n, k in dims.items()}, **{CONTROL_PREFIX + n: k for n, k in dims.items()}}
+        aggregate = DeviceStatistics(flat=agg_flat, dims=dims, weight=float(sums[8]),
                                      bookkeeping=book, workspace=self.ws, comm=self._comm)
         for proc in reversed(self._postprocessors):
             try:
@@ -451,4 +506,4 @@ class GpuSimulationEngine:
                     f"{type(proc).__name__} failed: {exc}"
                 ) from exc
             metrics = merge_metrics(metrics, server_metrics)
-        return aggregate, metrics, cohort
+        return aggregate, metrics, cohort, updates

@@ -56,3 +56,8 @@ class NativeUnavailable(FedsimError):
 
 class NativeError(FedsimError):
     """A C-ABI entry point returned a non-zero status."""
+
+
+class ZeroLocalSteps(FedsimError):
+    """A control-variate update requires at least one local optimizer step
+    (fedsim/errors.py:42-43)."""

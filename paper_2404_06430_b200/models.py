@@ -192,7 +192,53 @@ class SGDOptimizer:
         return {n: params[n] - lr * direction[n] for n in params}
 
 
-CentralOptimizer = SGDOptimizer
+class AdamOptimizer:
+    """Adam with bias correction, treating the averaged delta as gradient
+    (fedsim/models/optimizers.py:24-68); ``adaptivity_degree`` is the epsilon
+    added to the root of the bias-corrected second moment.
+
+    On the GPU path the step is one fused kernel (fb_noise_avg_adam_f32) that
+    also adds the pending central DP noise and divides by the total weight;
+    the moments are flat fp32 device vectors."""
+
+    def __init__(self, learning_rate: "float | HyperParam", beta1: float = 0.9, beta2: float = 0.99,
+                 adaptivity_degree: float = 0.1):
+        if not 0.0 <= beta1 < 1.0 or not 0.0 <= beta2 < 1.0:
+            raise ValueError("betas must be in [0, 1)")
+        if adaptivity_degree <= 0.0:
+            raise ValueError("adaptivity_degree must be > 0")
+        self.learning_rate = learning_rate
+        self.beta1 = beta1
+        self.beta2 = beta2
+        self.adaptivity_degree = adaptivity_degree
+        self.step_count = 0
+        self.first_moment = None
+        self.second_moment = None
+
+    def step(self, params, direction, iteration: int):
+        lr = resolve(self.learning_rate, iteration)
+        if hasattr(direction, "apply_adam"):
+            return direction.apply_adam(params, self, lr)
+        # host dicts (unit tests of the mirror): the reference's float64 update
+        if self.first_moment is None:
+            self.first_moment = {n: np.zeros_like(v) for n, v in params.items()}
+            self.second_moment = {n: np.zeros_like(v) for n, v in params.items()}
+        self.step_count += 1
+        t = self.step_count
+        out = {}
+        for name, theta in params.items():
+            g = direction[name]
+            m = self.beta1 * self.first_moment[name] + (1 - self.beta1) * g
+            v = self.beta2 * self.second_moment[name] + (1 - self.beta2) * g * g
+            self.first_moment[name] = m
+            self.second_moment[name] = v
+            m_hat = m / (1 - self.beta1**t)
+            v_hat = v / (1 - self.beta2**t)
+            out[name] = theta - lr * m_hat / (np.sqrt(v_hat) + self.adaptivity_degree)
+        return out
+
+
+CentralOptimizer = SGDOptimizer | AdamOptimizer
 
 
 def central_step(optimizer, params, averaged_delta, iteration: int):

@@ -19,3 +19,21 @@ CONFIGS = {
                    weighting="uniform", bound=0.5, sigma=0.9, r=0.2, noise_seed=3, run_seed=4,
                    init_seed=1, iterations=2, eval_every=1, workers=1),
 }
+
+# Algorithm / central-optimizer variants: the
+# same data recipes run through the reference's FedProx, AdaFedProx, Scaffold
+# and AdamOptimizer.
+_VARIANTS = {
+    "mlp_adam_dp": ("mlp_dp", dict(optimizer=dict(kind="adam", lr=0.05, beta1=0.9, beta2=0.99, eps=0.1),
+                                   iterations=4)),
+    "logistic_fedprox": ("logistic_dp", dict(algorithm=dict(kind="fedprox", mu=0.3))),
+    "mlp_adafedprox": ("mlp_dp", dict(algorithm=dict(kind="adafedprox", mu=0.1), bound=None, sigma=0.0,
+                                      iterations=4, eval_every=1)),
+    "mlp_scaffold_dp": ("mlp_dp", dict(algorithm=dict(kind="scaffold", num_train_users=60), cohort=30,
+                                       iterations=3)),
+    "logistic_scaffold": ("logistic_dp", dict(algorithm=dict(kind="scaffold", num_train_users=40), bound=None,
+                                              sigma=0.0, weighting="uniform", epochs=2, cohort=20, iterations=4,
+                                              workers=1)),
+}
+for _name, (_base, _over) in _VARIANTS.items():
+    CONFIGS[_name] = {**CONFIGS[_base], **_over}

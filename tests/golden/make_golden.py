@@ -28,10 +28,13 @@ sys.path.insert(0, str(REF_SRC))
 sys.path.insert(0, str(HERE.parent.parent))
 
 from fedsim.algorithms import FedAvg  # noqa: E402
+from fedsim.algorithms.fedavg import AdaFedProx, FedProx  # noqa: E402
+from fedsim.algorithms.scaffold import Scaffold  # noqa: E402
 from fedsim.core import LocalTrainParams, Population, cohort_seed, derive_seed, user_seed  # noqa: E402
 from fedsim.engine import SimulationEngine, compute_base_weight, run_simulation, schedule_users  # noqa: E402
 from fedsim.feddata import make_synthetic_classification, partition_iid, sample_cohort  # noqa: E402
 from fedsim.models import MLP, LogisticRegression, Model, SGDOptimizer, local_train_sgd  # noqa: E402
+from fedsim.models.optimizers import AdamOptimizer  # noqa: E402
 from fedsim.privacy import ClippingPostprocessor, GaussianCentralMechanism  # noqa: E402
 
 from oracle.port import Cnn  # noqa: E402
@@ -81,13 +84,28 @@ def build_model(cfg):
     return RefCNN()
 
 
+def build_algorithm(cfg, model):
+    o = cfg.get("optimizer", dict(kind="sgd"))
+    opt = (AdamOptimizer(o["lr"], beta1=o["beta1"], beta2=o["beta2"], adaptivity_degree=o["eps"])
+           if o["kind"] == "adam" else SGDOptimizer(cfg["clr"]))
+    a = cfg.get("algorithm", dict(kind="fedavg"))
+    kw = dict(total_iterations=cfg["iterations"], cohort_size=cfg["cohort"], local_learning_rate=cfg["lr"],
+              local_num_epochs=cfg["epochs"], local_batch_size=cfg["batch"], eval_frequency=cfg["eval_every"],
+              eval_cohort_size=cfg["eval_cohort"], weighting=cfg["weighting"], run_seed=cfg["run_seed"],
+              init_seed=cfg["init_seed"])
+    if a["kind"] == "fedprox":
+        return FedProx(model, opt, mu=a["mu"], **kw)
+    if a["kind"] == "adafedprox":
+        return AdaFedProx(model, opt, mu=a["mu"], **kw)
+    if a["kind"] == "scaffold":
+        return Scaffold(model, opt, num_train_users=a["num_train_users"], **kw)
+    return FedAvg(model, opt, **kw)
+
+
 def run_config(name, cfg):
     ds = datasets(cfg)
     model = build_model(cfg)
-    alg = FedAvg(model, SGDOptimizer(cfg["clr"]), total_iterations=cfg["iterations"], cohort_size=cfg["cohort"],
-                 local_learning_rate=cfg["lr"], local_num_epochs=cfg["epochs"], local_batch_size=cfg["batch"],
-                 eval_frequency=cfg["eval_every"], eval_cohort_size=cfg["eval_cohort"],
-                 weighting=cfg["weighting"], run_seed=cfg["run_seed"], init_seed=cfg["init_seed"])
+    alg = build_algorithm(cfg, model)
     post = []
     if cfg["bound"] is not None:
         clip = ClippingPostprocessor(cfg["bound"])
@@ -170,5 +188,7 @@ def sampling():
 
 if __name__ == "__main__":
     sampling()
+    only = set(sys.argv[1:])
     for name, cfg in CONFIGS.items():
-        run_config(name, cfg)
+        if not only or name in only:
+            run_config(name, cfg)

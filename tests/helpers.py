@@ -42,13 +42,29 @@ def noise_base(cfg) -> int:
     return fb.derive_seed(cfg["run_seed"], "noise-stream", cfg["noise_seed"])
 
 
+def product_algorithm(cfg):
+    """The configured algorithm / central optimizer, built with the mirror API
+    (the same classes and arguments make_golden.py hands to the reference)."""
+    o = cfg.get("optimizer", dict(kind="sgd"))
+    opt = (fb.AdamOptimizer(o["lr"], beta1=o["beta1"], beta2=o["beta2"], adaptivity_degree=o["eps"])
+           if o["kind"] == "adam" else fb.SGDOptimizer(cfg["clr"]))
+    a = cfg.get("algorithm", dict(kind="fedavg"))
+    kw = dict(total_iterations=cfg["iterations"], cohort_size=cfg["cohort"], local_learning_rate=cfg["lr"],
+              local_num_epochs=cfg["epochs"], local_batch_size=cfg["batch"], eval_frequency=cfg["eval_every"],
+              eval_cohort_size=cfg["eval_cohort"], weighting=cfg["weighting"], run_seed=cfg["run_seed"],
+              init_seed=cfg["init_seed"])
+    if a["kind"] == "fedprox":
+        return fb.FedProx(product_model(cfg), opt, mu=a["mu"], **kw)
+    if a["kind"] == "adafedprox":
+        return fb.AdaFedProx(product_model(cfg), opt, mu=a["mu"], **kw)
+    if a["kind"] == "scaffold":
+        return fb.Scaffold(product_model(cfg), opt, num_train_users=a["num_train_users"], **kw)
+    return fb.FedAvg(product_model(cfg), opt, **kw)
+
+
 def product_run_parts(cfg, noise_source="numpy", sigma=None):
     """(algorithm, postprocessors) built with the product's mirror API."""
-    alg = fb.FedAvg(product_model(cfg), fb.SGDOptimizer(cfg["clr"]), total_iterations=cfg["iterations"],
-                    cohort_size=cfg["cohort"], local_learning_rate=cfg["lr"], local_num_epochs=cfg["epochs"],
-                    local_batch_size=cfg["batch"], eval_frequency=cfg["eval_every"],
-                    eval_cohort_size=cfg["eval_cohort"], weighting=cfg["weighting"], run_seed=cfg["run_seed"],
-                    init_seed=cfg["init_seed"])
+    alg = product_algorithm(cfg)
     post = []
     if cfg["bound"] is not None:
         clip = fb.ClippingPostprocessor(cfg["bound"])
@@ -70,7 +86,8 @@ def oracle_run(cfg, world=None):
         eval_every=cfg["eval_every"], lr=cfg["lr"], epochs=cfg["epochs"], batch=cfg["batch"], clr=cfg["clr"],
         weighting=cfg["weighting"], bound=cfg["bound"], sigma=cfg["sigma"], r=cfg["r"],
         noise_base=noise_base(cfg), run_seed=cfg["run_seed"], init_seed=cfg["init_seed"],
-        world=cfg["workers"] if world is None else world)
+        world=cfg["workers"] if world is None else world, algorithm=cfg.get("algorithm"),
+        optimizer=cfg.get("optimizer"))
 
 
 def golden_rows(g):
@@ -78,5 +95,5 @@ def golden_rows(g):
             for t, p, n, v, w in zip(g["row_t"], g["row_pop"], g["row_name"], g["row_value"], g["row_weight"])]
 
 
-__all__ = ["CONFIGS", "product_datasets", "product_model", "oracle_model", "product_run_parts", "oracle_run",
+__all__ = ["CONFIGS", "product_datasets", "product_model", "product_algorithm", "oracle_model", "product_run_parts", "oracle_run",
            "golden_rows", "users_of", "noise_base"]

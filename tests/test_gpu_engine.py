@@ -26,7 +26,8 @@ def run_engine(cfg, noise_source="numpy", **engine_kw):
     return res, np.array(thetas)
 
 
-@pytest.mark.parametrize("name", ["mlp_dp", "logistic_dp", "mlp_noclip"])
+@pytest.mark.parametrize("name", ["mlp_dp", "logistic_dp", "mlp_noclip", "mlp_adam_dp", "logistic_fedprox",
+                                  "mlp_adafedprox", "mlp_scaffold_dp", "logistic_scaffold"])
 def test_engine_matches_reference_run(name, golden):
     g = golden(name)
     res, thetas = run_engine(CONFIGS[name])
@@ -51,7 +52,7 @@ def test_engine_clip_factors_match_oracle():
     state = alg.initial_state()
     state.params = fb.DeviceParams.from_host(state.params, eng.device)
     ctx = alg.get_next_central_contexts(state, 0)[0]
-    agg, metrics, cohort = eng._run_context(alg, state, ctx)
+    agg, metrics, cohort, _ = eng._run_context(alg, state, ctx)
     m = oracle_model(cfg)
     ref = port.run_context(m, m.init(cfg["init_seed"]), users_of(ds[fb.Population.TRAIN]), cfg["cohort"],
                            ctx.seed, train=(cfg["lr"], cfg["epochs"], cfg["batch"]), weighting=cfg["weighting"],
@@ -108,3 +109,46 @@ def test_engine_philox_noise_statistics():
     n = z.size
     assert abs(z.mean()) <= 3 * std / np.sqrt(n)
     assert abs(z.std() - std) <= 3 * std / np.sqrt(2 * n) + 1e-7
+
+
+def test_scaffold_controls_match_oracle():
+    """Per-user control vectors and the server control after a Scaffold run
+    (device store) against the oracle's float64 restatement."""
+    from oracle import port
+    from tests.helpers import oracle_model, users_of
+
+    cfg = CONFIGS["logistic_scaffold"]
+    ds = product_datasets(cfg)
+    alg, post = product_run_parts(cfg)
+    eng = fb.GpuSimulationEngine(ds, postprocessors=post)
+    res = fb.run_simulation(alg, eng)
+    store = res.state.extra["user_controls"]
+    # replay the oracle and capture its controls
+    model = oracle_model(cfg)
+    scaffold = dict(server=np.zeros(sum(model.dims.values())), users={})
+    theta = model.init(cfg["init_seed"])
+    for t in range(cfg["iterations"]):
+        r = port.run_context(model, theta, users_of(ds[fb.Population.TRAIN]), cfg["cohort"],
+                             port.cohort_seed(cfg["run_seed"], t, "train"), train=(cfg["lr"], cfg["epochs"], cfg["batch"]),
+                             weighting="uniform", scaffold=scaffold)
+        for uid, c in r.user_updates:
+            scaffold["users"][uid] = c
+        D = r.aggregate.size // 2
+        new = port.central_sgd(port.flat(theta, model.dims), r.aggregate[:D], r.weight, cfg["clr"])
+        scaffold["server"] = scaffold["server"] + (r.weight / cfg["algorithm"]["num_train_users"]) * (
+            r.aggregate[D:] / r.weight)
+        theta = port._unflat(new, model.dims)
+    assert len(store) == len(scaffold["users"])
+    for uid, ref in scaffold["users"].items():
+        assert_close_fp32(store.get(uid), ref, what=f"control of {uid}")
+    assert_close_fp32(res.state.extra["server_control"].double().cpu().numpy(), scaffold["server"],
+                      what="server control")
+
+
+def test_scaffold_zero_local_steps_raises_with_provenance():
+    cfg = dict(CONFIGS["logistic_scaffold"])
+    ds = product_datasets(cfg)
+    alg, post = product_run_parts({**cfg, "lr": 0.0})
+    eng = fb.GpuSimulationEngine(ds, postprocessors=post)
+    with pytest.raises(fb.EngineError, match="control update divides by steps"):
+        fb.run_simulation(alg, eng)

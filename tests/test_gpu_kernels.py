@@ -235,6 +235,58 @@ def test_noise_avg_sgd(D):
     assert_close_fp32(t2.double().cpu().numpy(), ref2)
 
 
+@pytest.mark.parametrize("D", [7, 2762, 1_626_442])
+def test_noise_avg_adam_matches_oracle(D):
+    """fb_noise_avg_adam_f32 over 4 steps vs the float64 AdamOptimizer
+    restatement (fedsim/models/optimizers.py:24-68), injected noise."""
+    from oracle import port
+
+    rng = np.random.default_rng(D + 1)
+    theta = rng.normal(size=D).astype(np.float32)
+    t, m, v = dev(theta), torch.zeros(D, device="cuda"), torch.zeros(D, device="cuda")
+    ref, st = theta.astype(np.float64), {}
+    for k in range(1, 5):
+        agg = rng.normal(size=D).astype(np.float32)
+        inj = rng.normal(scale=0.1, size=D).astype(np.float32)
+        native.call("fb_noise_avg_adam_f32", t.data_ptr(), m.data_ptr(), v.data_ptr(), dev(agg).data_ptr(), D, 0.0, 0,
+                    dev(inj).data_ptr(), 1.0 / 20, 0.05, 0.9, 0.99, 0.1, k, None, S())
+        ref = port.central_adam(ref, agg.astype(np.float64), 20.0, 0.05, st, 0.9, 0.99, 0.1,
+                                noise=inj.astype(np.float64))
+        assert_close_fp32(t.double().cpu().numpy(), ref, what=f"adam step {k}")
+    with pytest.raises(ValueError, match="step >= 1"):
+        native.call("fb_noise_avg_adam_f32", t.data_ptr(), m.data_ptr(), v.data_ptr(), t.data_ptr(), D, 0.0, 0, None,
+                    1.0, 0.1, 0.9, 0.99, 0.1, 0, None, S())
+
+
+def test_scaffold_kernels():
+    """correction / payload / scatter against numpy (fedsim/algorithms/scaffold.py:46-79)."""
+    rng = np.random.default_rng(3)
+    C, D, ld, lds = 5, 37, 40, 44
+    server = rng.normal(size=D).astype(np.float32)
+    store = rng.normal(size=(4, lds)).astype(np.float32)
+    rows = np.array([2, -1, 0, 3, -1], dtype=np.int32)
+    u = np.where(rows[:, None] >= 0, store[np.maximum(rows, 0), :D], 0.0)
+    corr = torch.zeros(C, ld, device="cuda")
+    d_store, d_rows = dev(store), dev(rows)
+    native.call("fb_scaffold_correction_f32", dev(server).data_ptr(), d_store.data_ptr(), lds, d_rows.data_ptr(), C, D,
+                corr.data_ptr(), ld, S())
+    np.testing.assert_array_equal(corr.cpu().numpy()[:, :D], (server[None, :] - u).astype(np.float32))
+    delta = rng.normal(size=(C, ld)).astype(np.float32)
+    scale = rng.uniform(1, 3, size=C).astype(np.float32)
+    pay = torch.zeros(C, 2 * D + 2, device="cuda")
+    newc = torch.zeros(C, ld, device="cuda")
+    native.call("fb_scaffold_payload_f32", dev(delta).data_ptr(), ld, dev(server).data_ptr(), d_store.data_ptr(), lds,
+                d_rows.data_ptr(), dev(scale).data_ptr(), C, D, pay.data_ptr(), 2 * D + 2, newc.data_ptr(), ld, S())
+    ds = delta[:, :D] * scale[:, None]
+    np.testing.assert_allclose(pay.cpu().numpy()[:, :D], delta[:, :D])
+    np.testing.assert_allclose(pay.cpu().numpy()[:, D:2 * D], ds - server[None, :], rtol=1e-6, atol=1e-6)
+    np.testing.assert_allclose(newc.cpu().numpy()[:, :D], (u - server[None, :]) + ds, rtol=1e-6, atol=1e-6)
+    tgt = torch.zeros(6, lds, device="cuda")
+    native.call("fb_scatter_rows_f32", tgt.data_ptr(), lds, dev(np.array([4, 1], dtype=np.int32)).data_ptr(),
+                newc.data_ptr(), ld, 2, D, S())
+    np.testing.assert_array_equal(tgt.cpu().numpy()[[4, 1], :D], newc.cpu().numpy()[:2, :D])
+
+
 def test_bad_arguments_raise_value_error():
     with pytest.raises(ValueError, match="bad shape"):
         native.call("fb_delta_norm_clip_f32", None, 2, 1, 4, None, 1.0, None, None, None, None, None, 0, S())

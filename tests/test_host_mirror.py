@@ -178,3 +178,40 @@ def test_native_permutations_bit_exact_with_numpy(golden):
     got = native_permutations(12345, ids, sizes, 3, off)
     want = np.concatenate(fb.client_permutations(12345, ids, sizes.tolist(), 3))
     np.testing.assert_array_equal(got, want)
+
+
+def test_adam_host_step_matches_reference_analytic_first_step():
+    """tests/test_models.py:197-215 of the reference: first step = -lr g / (|g| + eps);
+    zero delta leaves the parameters unchanged."""
+    lr, eps = 0.1, 0.3
+    opt = fb.AdamOptimizer(learning_rate=lr, adaptivity_degree=eps)
+    rng = np.random.default_rng(5)
+    params = {"a": rng.normal(size=6)}
+    g = rng.normal(size=6)
+    out = opt.step(params, {"a": g}, iteration=0)
+    np.testing.assert_allclose(out["a"], params["a"] - lr * g / (np.abs(g) + eps), rtol=1e-12)
+    assert opt.step_count == 1
+    z = fb.AdamOptimizer(0.1).step({"a": np.array([3.0, -1.0])}, {"a": np.zeros(2)}, 0)
+    np.testing.assert_array_equal(z["a"], [3.0, -1.0])
+    with pytest.raises(ValueError):
+        fb.AdamOptimizer(0.1, beta1=1.0)
+    with pytest.raises(ValueError):
+        fb.AdamOptimizer(0.1, adaptivity_degree=0.0)
+
+
+def test_adafedprox_mu_rule_and_scaffold_validation():
+    assert fb.adafedprox_update_mu(0.5, 1.0, 0.9) == pytest.approx(0.45)
+    assert fb.adafedprox_update_mu(0.95, 1.0, 1.1) == pytest.approx(1.0)  # capped
+    assert fb.adafedprox_update_mu(1e-4, 1.0, 0.5) == pytest.approx(1e-4)  # floored
+    assert fb.adafedprox_update_mu(0.3, 1.0, 1.0) == 0.3
+    kw = dict(total_iterations=1, cohort_size=2, local_learning_rate=0.1, local_num_epochs=1, local_batch_size=2,
+              eval_frequency=1, eval_cohort_size=1)
+    with pytest.raises(ValueError, match="uniform"):
+        fb.Scaffold(fb.MLP(4, 3, 2), fb.SGDOptimizer(1.0), num_train_users=3, weighting="datapoints", **kw)
+    with pytest.raises(ValueError, match="num_train_users"):
+        fb.Scaffold(fb.MLP(4, 3, 2), fb.SGDOptimizer(1.0), num_train_users=0, **kw)
+    alg = fb.Scaffold(fb.MLP(4, 3, 2), fb.SGDOptimizer(1.0), num_train_users=3, **kw)
+    st = alg.initial_state()
+    ctx = alg.get_next_central_contexts(st, 0)[0]
+    plan = alg.cohort_plan(st, ctx)
+    assert plan.scaffold and plan.weighting == "uniform"

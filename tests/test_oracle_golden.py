@@ -11,7 +11,8 @@ from oracle import port
 from tests.helpers import CONFIGS, golden_rows, oracle_model, oracle_run, product_datasets, users_of
 
 
-@pytest.mark.parametrize("name", ["mlp_dp", "logistic_dp", "mlp_noclip", "cnn_dp"])
+@pytest.mark.parametrize("name", ["mlp_dp", "logistic_dp", "mlp_noclip", "cnn_dp", "mlp_adam_dp", "logistic_fedprox",
+                                  "mlp_adafedprox", "mlp_scaffold_dp", "logistic_scaffold"])
 def test_oracle_reproduces_reference_run(name, golden):
     g = golden(name)
     cfg = CONFIGS[name]
