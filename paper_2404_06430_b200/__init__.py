@@ -19,6 +19,7 @@ from .algorithms import (
     UserResult,
     adafedprox_update_mu,
 )
+from .checkpoint import CsvMetricsWriter, load_params, save_params
 from .core import (
     CentralContext,
     Constant,

@@ -1049,12 +1049,15 @@ __global__ void __launch_bounds__(256) fc1_materialize_kernel(Hist hs, int S, in
 // from a 3-term split: every operand x is scaled by a power of two s (per
 // sample for activations / gradients, per client for weights) so |x s| <=
 // 2^15, then stored as hi = fp16(x s) and lo = fp16(x s - hi); products are
-// hi*hi + hi*lo + lo*hi (the dropped lo*lo is ~2^-22 relative).  Long
-// accumulation chains on the tensor core lose accuracy (its fp32 adds
-// truncate), so every kernel keeps chains short -- separate accumulators for
-// the hi*hi terms of tap groups and for the cross terms, summed with round-to-
-// nearest on the CUDA cores in the epilogue (measured: per-client delta
-// error 2-7e-7 relative, the same as FP32 FFMA).
+// hi*hi + hi*lo + lo*hi (the dropped lo*lo is ~2^-22 relative).  The hi*hi
+// ("main") and cross terms accumulate in separate TMEM accumulators, summed
+// with round-to-nearest on the CUDA cores in the epilogue.  TMEM fp32
+// accumulation chains of up to 36 K=16 MMAs were measured as accurate as a
+// sequential fp32 sum (scratch/acc_bench.cu: mean error 2-3e-8 of sum|p|);
+// the conv kernels chain at most 18 (forward / backward-data: 9 taps x K
+// steps) or 15 (weight gradient: one 240-position block), longer sums are
+// drained into fp32 registers.  Per-client delta error 2-7e-7 relative,
+// the same as FP32 FFMA.
 constexpr int TC_THREADS = 192;                 // warp 0 TMA, warp 1 TMEM + MMA, warps 2-5 epilogue
 
 // host: driver entry point for cuTensorMapEncodeTiled (cudart is linked statically)
@@ -1136,7 +1139,6 @@ __device__ __forceinline__ float block_scale(float m, float* red) {
 // epilogue (unscale, bias, ReLU, 2x2 max-pool with argmax code) overlaps the
 // next tile's MMAs.
 constexpr int FW_ROWS = 4;                       // conv rows per M tile
-constexpr int FW_M = FW_ROWS * S2;               // 112 valid outputs per tile
 constexpr int FW_MW = FW_ROWS * S1;              // 120 rows in the 30-wide space
 constexpr int FW_TILES = S2 / FW_ROWS;           // 7 tiles per sample
 constexpr int FW_BAND = FW_ROWS + 3;             // 7 a1 rows per band (6 + the garbage rows' spill)
@@ -1151,8 +1153,9 @@ constexpr int FW_THREADS = (2 + FW_EPI_WARPS) * 32;
 constexpr int FW_PL = 2 * FW_ROWS / 2 * SP;      // 56 horizontal pair maxima per channel and tile
 constexpr int FW_EPI_BYTES = 2 * C2 * FW_PL * 4 + 2 * FW_PL * 4 * 2;  // double-buffered [64 ch][56] values + [56][4] code masks
 constexpr int FW_SMEM = 1024 + WIMG_BYTES + FW_STAGES * FW_STAGE + FW_EPI_BYTES + 256;
-constexpr int FW_ACC = 4 * C2;                   // 4 accumulators x 64 columns per tile
+constexpr int FW_ACC = 2 * C2;                   // main | cross accumulators (64 columns each) per tile
 constexpr uint32_t FW_IDESC = tc::idesc_f16(128, C2);
+constexpr uint32_t FW_IDESC2 = tc::idesc_f16(128, 2 * C2);  // B = [W hi; W lo] stacked along N
 static_assert(127 + 2 * S1 + 2 < FW_BAND * S1 && FW_A_TX <= FW_A, "conv2 fwd band: every tap row inside the band");
 
 // per-group conv2 weight image (K-major SWIZZLE_64B: row o, 32 ci), scaled split
@@ -1284,12 +1287,10 @@ __global__ void __launch_bounds__(FW_THREADS, 1) conv2_fwd_tc_kernel(
 #pragma unroll
           for (int tap = 0; tap < 9; ++tap) {
             const uint32_t ah = sA0 + stage * FW_STAGE + ((tap / 3) * S1 + tap % 3) * 64, al = ah + FW_A;
-            const uint32_t bh = sB0 + (tap * 2 + 0) * FW_B_TAP, bl = sB0 + (tap * 2 + 1) * FW_B_TAP;
-            const uint32_t dmain = d + (tap / 3) * C2, dcross = d + 3 * C2;
+            const uint32_t bh = sB0 + tap * 2 * FW_B_TAP;  // [hi 64 rows | lo 64 rows]: one 128-row operand
             // K = 32 ci = 2 x 16: the second K step starts 32 B (2 descriptor units) later
-            tc::mma3_f16_ks<2, 2, 2>(dmain, dcross, tc::sdesc(ah, 16, 512, 4), tc::sdesc(al, 16, 512, 4),
-                                     tc::sdesc(bh, 16, 512, 4), tc::sdesc(bl, 16, 512, 4), FW_IDESC, tap % 3 != 0,
-                                     tap != 0);
+            tc::mma2s_f16_ks<2, 2, 2>(d, d + C2, tc::sdesc(ah, 16, 512, 4), tc::sdesc(al, 16, 512, 4),
+                                      tc::sdesc(bh, 16, 512, 4), FW_IDESC2, FW_IDESC, tap != 0);
           }
           tc::mma_commit(&empty[stage]);
           tc::mma_commit(&tfull[acc]);
@@ -1342,18 +1343,15 @@ __global__ void __launch_bounds__(FW_THREADS, 1) conv2_fwd_tc_kernel(
         float z[16];
         {
           const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + acc * FW_ACC + cg * 16;
-          uint32_t v0[16], v1[16], v2[16], v3[16];
+          uint32_t v0[16], v1[16];
           tc::tmem_ld16(base, v0);
           tc::tmem_ld16(base + C2, v1);
-          tc::tmem_ld16(base + 2 * C2, v2);
-          tc::tmem_ld16(base + 3 * C2, v3);
           tc::tmem_ld_wait();
           tc::tc_fence_before();
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(&tempty[acc]);  // accumulator drained: the next tile may reuse it
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            z[j] = ((__uint_as_float(v0[j]) + __uint_as_float(v1[j])) + __uint_as_float(v2[j])) + __uint_as_float(v3[j]);
+          for (int j = 0; j < 16; ++j) z[j] = __uint_as_float(v0[j]) + __uint_as_float(v1[j]);
         }
 #ifdef FB_FWD_NOEPI  // timing experiment only: drain TMEM, skip the pooling epilogue
         if (z[0] == 1.2345f) pout[0] = z[1];
@@ -1732,8 +1730,9 @@ constexpr int BX_STAGE = 2 * BX_A;               // hi + lo band
 constexpr int BX_B_TAP = C1 * 128;               // 4 KB: 32 rows (ci) x 64 o fp16
 constexpr int WIMGT_BYTES = 9 * 2 * BX_B_TAP;    // 73728
 constexpr int BX_STAGES = 2;
-constexpr int BX_ACC = 4 * C1;                   // 4 accumulators x 32 columns
+constexpr int BX_ACC = 2 * C1;                   // main | cross accumulators (32 columns each)
 constexpr int BX_SMEM = 1024 + WIMGT_BYTES + BX_STAGES * BX_STAGE + 256;
+constexpr uint32_t BX_IDESC2 = tc::idesc_f16(128, 2 * C1);  // B = [W^T hi; W^T lo] stacked along N
 constexpr int BX_EPI_WARPS = 16;                 // 4 per TMEM lane quadrant, 8 input channels each
 constexpr int BX_THREADS = (2 + BX_EPI_WARPS) * 32;
 constexpr uint32_t BX_IDESC = tc::idesc_f16(128, C1);
@@ -1894,12 +1893,10 @@ __global__ void __launch_bounds__(BX_THREADS, 1) conv2_bwd_x_tc_kernel(
 #pragma unroll
           for (int tap = 0; tap < 9; ++tap) {
             const uint32_t ah = sA0 + stage * BX_STAGE + ((2 - tap / 3) * S1 + 2 - tap % 3) * 128, al = ah + BX_A;
-            const uint32_t bh = sB0 + (tap * 2 + 0) * BX_B_TAP, bl = sB0 + (tap * 2 + 1) * BX_B_TAP;
-            const uint32_t dmain = d + (tap / 3) * C1, dcross = d + 3 * C1;
+            const uint32_t bh = sB0 + tap * 2 * BX_B_TAP;  // [hi 32 rows | lo 32 rows]: one 64-row operand
             // K = 64 o = 4 x 16, each K step 32 B (2 descriptor units) further along the row
-            tc::mma3_f16_ks<4, 2, 2>(dmain, dcross, tc::sdesc(ah, 16, 1024, 2), tc::sdesc(al, 16, 1024, 2),
-                                     tc::sdesc(bh, 16, 1024, 2), tc::sdesc(bl, 16, 1024, 2), BX_IDESC, tap % 3 != 0,
-                                     tap != 0);
+            tc::mma2s_f16_ks<4, 2, 2>(d, d + C1, tc::sdesc(ah, 16, 1024, 2), tc::sdesc(al, 16, 1024, 2),
+                                      tc::sdesc(bh, 16, 1024, 2), BX_IDESC2, BX_IDESC, tap != 0);
           }
           tc::mma_commit(&empty[stage]);
           tc::mma_commit(&tfull[acc]);
@@ -1933,11 +1930,9 @@ __global__ void __launch_bounds__(BX_THREADS, 1) conv2_bwd_x_tc_kernel(
         tc::mbar_wait(&tfull[acc], (tile >> 1) & 1);
         tc::tc_fence_after();
         const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + acc * BX_ACC + cg * 8;
-        uint32_t v0[8], v1[8], v2[8], v3[8];
+        uint32_t v0[8], v1[8];
         tc::tmem_ld8(base, v0);
         tc::tmem_ld8(base + C1, v1);
-        tc::tmem_ld8(base + 2 * C1, v2);
-        tc::tmem_ld8(base + 3 * C1, v3);
         tc::tmem_ld_wait();
         tc::tc_fence_before();
         __syncwarp();
@@ -1951,10 +1946,8 @@ __global__ void __launch_bounds__(BX_THREADS, 1) conv2_bwd_x_tc_kernel(
             const __half2 l2 = *reinterpret_cast<const __half2*>(&lw[e]);
             const bool m0 = (__low2float(h2) + __low2float(l2)) > 0.f, m1 = (__high2float(h2) + __high2float(l2)) > 0.f;
             const int j = 2 * e;
-            const float z0 = (((__uint_as_float(v0[j]) + __uint_as_float(v1[j])) + __uint_as_float(v2[j])) +
-                              __uint_as_float(v3[j])) * inv;
-            const float z1 = (((__uint_as_float(v0[j + 1]) + __uint_as_float(v1[j + 1])) + __uint_as_float(v2[j + 1])) +
-                              __uint_as_float(v3[j + 1])) * inv;
+            const float z0 = (__uint_as_float(v0[j]) + __uint_as_float(v1[j])) * inv;
+            const float z1 = (__uint_as_float(v0[j + 1]) + __uint_as_float(v1[j + 1])) * inv;
             o[j] = m0 ? z0 : 0.f;
             o[j + 1] = m1 ? z1 : 0.f;
           }
@@ -2177,6 +2170,8 @@ constexpr int BW_EPI_WARPS = 8;
 constexpr int BW_THREADS = (2 + BW_EPI_WARPS) * 32;
 constexpr int BW_SMEM = 1024 + BW_STAGES * BW_STAGE + 256;
 constexpr uint32_t BW_IDESC = tc::idesc_f16_mn(128, C2);
+constexpr uint32_t BW_IDESC2 = tc::idesc_f16_mn(128, 2 * C2);  // B = [dz2 hi | dz2 lo] along N
+static_assert(BW_B_BYTES % 16 == 0 && (BW_B_BYTES >> 4) < (1 << 14), "bwd-w: hi/lo N-block stride fits the LBO field");
 
 __global__ void __launch_bounds__(BW_THREADS, 1) conv2_bwd_w_tc_kernel(
     const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
@@ -2248,7 +2243,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1) conv2_bwd_w_tc_kernel(
       tc::mbar_wait(&full[stage], phase);
       tc::tc_fence_after();
       const uint32_t ah = s0 + stage * BW_STAGE, al = ah + BW_A_BYTES;
-      const uint32_t bh = ah + 2 * BW_A_BYTES, bl = bh + BW_B_BYTES;
+      const uint32_t bh = ah + 2 * BW_A_BYTES;  // dz2 lo follows at + BW_B_BYTES
       for (int ky = 0; ky < 3; ++ky) {
         tc::mbar_wait(&tempty[ky], (blk & 1) ^ 1);  // previous block's ky accumulators drained
         tc::tc_fence_after();
@@ -2259,9 +2254,10 @@ __global__ void __launch_bounds__(BW_THREADS, 1) conv2_bwd_w_tc_kernel(
             const uint32_t arow = ky * S1 + ks * 16;
             const uint64_t adh = tc::sdesc(ah + arow * 64, 64, 512, 4);
             const uint64_t adl = tc::sdesc(al + arow * 64, 64, 512, 4);
-            const uint64_t bdh = tc::sdesc(bh + ks * 16 * 128, 128, 1024, 2);
-            const uint64_t bdl = tc::sdesc(bl + ks * 16 * 128, 128, 1024, 2);
-            tc::mma3_f16(dm, dx, adh, adl, bdh, bdl, BW_IDESC, ks != 0, ks != 0);
+            // B = [dz2 hi | dz2 lo] as ONE N = 128 MN-major operand: the two 64-wide N blocks are the
+            // hi and lo tiles, BW_B_BYTES apart (LBO)
+            const uint64_t bdh = tc::sdesc(bh + ks * 16 * 128, BW_B_BYTES, 1024, 2);
+            tc::mma2_f16(dm, dx, adh, adl, bdh, BW_IDESC2, BW_IDESC, ks != 0);
           }
           tc::mma_commit(&tfull[ky]);
           if (ky == 2) tc::mma_commit(&empty[stage]);

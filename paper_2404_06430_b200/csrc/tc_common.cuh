@@ -213,6 +213,19 @@ __device__ __forceinline__ void mma3_f16(uint32_t dmain, uint32_t dcross, uint64
       "r"(dcross), "l"(ah), "l"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(pm), "r"(px)
       : "memory");
 }
+// mma2s for one K step with explicit descriptors: d (2N wide) += Ahi*[Bhi;Blo]
+// (accumulate iff pacc), dcross (N wide) += Alo*Bhi.
+__device__ __forceinline__ void mma2_f16(uint32_t d, uint32_t dcross, uint64_t ah, uint64_t al, uint64_t bh,
+                                         uint32_t idesc2n, uint32_t idescn, uint32_t pacc) {
+  asm volatile(
+      "{\n\t.reg .pred pa, pt;\n\t"
+      "setp.ne.b32 pa, %7, 0;\n\t"
+      "setp.eq.b32 pt, %5, %5;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %4, %5, pa;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%1], %3, %4, %6, pt;\n}" ::"r"(d),
+      "r"(dcross), "l"(ah), "l"(al), "l"(bh), "r"(idesc2n), "r"(idescn), "r"(pacc)
+      : "memory");
+}
 // KS consecutive K steps of mma3_f16 in one asm statement: step k uses the
 // descriptors advanced by k * AINC / BINC (descriptor units of 16 bytes); only
 // step 0 takes the pm / px accumulate flags, later steps always accumulate.
@@ -257,6 +270,49 @@ __device__ __forceinline__ void mma3_f16_ks(uint32_t dmain, uint32_t dcross, uin
         "tcgen05.mma.cta_group::1.kind::f16 [%1], a1, e1, %6, pt;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%1], c1, b1, %6, pt;\n}" ::"r"(dmain),
         "r"(dcross), "l"(ah), "l"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(pm), "r"(px), "n"(AINC), "n"(BINC),
+        "n"(2 * AINC), "n"(2 * BINC), "n"(3 * AINC), "n"(3 * BINC)
+        : "memory");
+  }
+}
+// The 3-term split product with the weight operand's hi and lo parts stacked
+// along N: B = [Bhi; Blo] (2N rows) so ONE MMA of width 2N forms Ahi*Bhi into
+// d[0, N) and Ahi*Blo into d[N, 2N); a second MMA of width N adds Alo*Bhi
+// into d[N, 2N).  Two MMAs per K step instead of three, and the epilogue
+// sums two accumulators (main | cross).  KS K steps at AINC / BINC
+// descriptor units apart; step 0 accumulates iff pacc.
+template <int KS, int AINC, int BINC>
+__device__ __forceinline__ void mma2s_f16_ks(uint32_t d, uint32_t dcross, uint64_t ah, uint64_t al, uint64_t bh,
+                                             uint32_t idesc2n, uint32_t idescn, uint32_t pacc) {
+  static_assert(KS == 2 || KS == 4, "mma2s_f16_ks: 2 or 4 K steps");
+  if constexpr (KS == 2) {
+    asm volatile(
+        "{\n\t.reg .pred pa, pt;\n\t.reg .b64 a1, c1, b1;\n\t"
+        "setp.ne.b32 pa, %7, 0;\n\t"
+        "setp.eq.b32 pt, %5, %5;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %4, %5, pa;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%1], %3, %4, %6, pt;\n\t"
+        "add.s64 a1, %2, %8;\n\tadd.s64 c1, %3, %8;\n\tadd.s64 b1, %4, %9;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %5, pt;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%1], c1, b1, %6, pt;\n}" ::"r"(d),
+        "r"(dcross), "l"(ah), "l"(al), "l"(bh), "r"(idesc2n), "r"(idescn), "r"(pacc), "n"(AINC), "n"(BINC)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred pa, pt;\n\t.reg .b64 a1, c1, b1;\n\t"
+        "setp.ne.b32 pa, %7, 0;\n\t"
+        "setp.eq.b32 pt, %5, %5;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %4, %5, pa;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%1], %3, %4, %6, pt;\n\t"
+        "add.s64 a1, %2, %8;\n\tadd.s64 c1, %3, %8;\n\tadd.s64 b1, %4, %9;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %5, pt;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%1], c1, b1, %6, pt;\n\t"
+        "add.s64 a1, %2, %10;\n\tadd.s64 c1, %3, %10;\n\tadd.s64 b1, %4, %11;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %5, pt;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%1], c1, b1, %6, pt;\n\t"
+        "add.s64 a1, %2, %12;\n\tadd.s64 c1, %3, %12;\n\tadd.s64 b1, %4, %13;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %5, pt;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%1], c1, b1, %6, pt;\n}" ::"r"(d),
+        "r"(dcross), "l"(ah), "l"(al), "l"(bh), "r"(idesc2n), "r"(idescn), "r"(pacc), "n"(AINC), "n"(BINC),
         "n"(2 * AINC), "n"(2 * BINC), "n"(3 * AINC), "n"(3 * BINC)
         : "memory");
   }

@@ -152,3 +152,26 @@ def test_scaffold_zero_local_steps_raises_with_provenance():
     eng = fb.GpuSimulationEngine(ds, postprocessors=post)
     with pytest.raises(fb.EngineError, match="control update divides by steps"):
         fb.run_simulation(alg, eng)
+
+
+def test_engine_metrics_csv_and_checkpoint(golden, tmp_path):
+    """The GPU run writes the reference's metrics CSV / checkpoint formats:
+    rows equal the reference run's (values rtol 2e-5), the checkpoint holds
+    the final device theta exactly."""
+    import io
+
+    cfg = CONFIGS["mlp_dp"]
+    g = golden("mlp_dp")
+    ds = product_datasets(cfg)
+    alg, post = product_run_parts(cfg)
+    buf = io.StringIO()
+    res = fb.run_simulation(alg, fb.GpuSimulationEngine(ds, postprocessors=post), callbacks=[fb.CsvMetricsWriter(buf)])
+    lines = buf.getvalue().splitlines()
+    assert lines[0] == "iteration,population,metric,value,weight"
+    got = [ln.split(",") for ln in lines[1:]]
+    ref = golden_rows(g)
+    assert [(int(a), b, c) for a, b, c, _, _ in got] == [r[:3] for r in ref]
+    np.testing.assert_allclose([float(r[3]) for r in got], [r[3] for r in ref], rtol=2e-5)
+    fb.save_params(res.params, tmp_path / "checkpoint.csv")
+    back = fb.load_params(tmp_path / "checkpoint.csv")
+    np.testing.assert_array_equal(np.concatenate([back[n] for n in back]), res.params.flat_host())

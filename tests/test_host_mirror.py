@@ -215,3 +215,28 @@ def test_adafedprox_mu_rule_and_scaffold_validation():
     ctx = alg.get_next_central_contexts(st, 0)[0]
     plan = alg.cohort_plan(st, ctx)
     assert plan.scaffold and plan.weighting == "uniform"
+
+
+def test_checkpoint_roundtrip_and_metrics_csv(tmp_path):
+    """fedsim/models/checkpoint.py layout (lossless) and the runner's metrics
+    CSV rows (fedsim/cli/runner.py:39-57)."""
+    import io
+
+    rng = np.random.default_rng(0)
+    p = {"layer1/weights": rng.normal(size=7), "layer1/bias": np.array([0.1, -2.5e-300, 3.0])}
+    path = tmp_path / "checkpoint.csv"
+    fb.save_params(p, path)
+    lines = path.read_text().splitlines()
+    assert lines[:2] == ["fedsim-params,1", "name,index,value"]
+    assert lines[2].startswith("layer1/weights,0,")
+    back = fb.load_params(path)
+    assert list(back) == list(p)
+    for n in p:
+        np.testing.assert_array_equal(back[n], p[n])
+    with pytest.raises(fb.DataError):
+        fb.load_params(tmp_path / "missing.csv")
+    buf = io.StringIO()
+    w = fb.CsvMetricsWriter(buf)
+    assert w(None, [(0, "train", "loss", 0.5, 12.0), (0, "val", "accuracy", 1 / 3, 6.0)], 0) is False
+    assert buf.getvalue().splitlines() == ["iteration,population,metric,value,weight", "0,train,loss,0.5,12.0",
+                                           f"0,val,accuracy,{1 / 3!r},6.0"]
