@@ -1053,7 +1053,7 @@ __global__ void __launch_bounds__(256) fc1_materialize_kernel(Hist hs, int S, in
 // ("main") and cross terms accumulate in separate TMEM accumulators, summed
 // with round-to-nearest on the CUDA cores in the epilogue.  TMEM fp32
 // accumulation chains of up to 36 K=16 MMAs were measured as accurate as a
-// sequential fp32 sum (scratch/acc_bench.cu: mean error 2-3e-8 of sum|p|);
+// sequential fp32 sum (tools/microbench/acc_bench.cu: mean error 1-3e-8 of sum|p|);
 // the conv kernels chain at most 18 (forward / backward-data: 9 taps x K
 // steps) or 15 (weight gradient: one 240-position block), longer sums are
 // drained into fp32 registers.  Per-client delta error 2-7e-7 relative,
