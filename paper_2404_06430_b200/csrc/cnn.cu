@@ -1964,6 +1964,210 @@ __global__ void __launch_bounds__(BX_THREADS, 1) conv2_bwd_x_tc_kernel(
   if (warp == 1) tc::tmem_dealloc<2 * BX_ACC>(tmem);
 }
 
+// ------------------------------------------------- conv1 forward (tcgen05)
+// a1[p, o] = ReLU(b_o + sum_k xcol[p, k] W1[o, k]), k = (ci, ky, kx) (27), as a
+// GEMM M = 128 positions, N = 32 channels, K = 27 + a constant-1 column
+// (k = 27) that adds the bias, padded to 32 = 4 kind::tf32 K steps.  The
+// split is 3xTF32 with the weight parts stacked along N: B = [W hi; W lo]
+// (64 rows), so per K step ONE N = 64 MMA forms xhi*Whi | xhi*Wlo and one
+// N = 32 MMA adds xlo*Whi to the cross half.  im2col A tiles (hi / lo, K-major
+// SWIZZLE_128B: one 128-byte row = the position's 32 k) are staged by the CTA
+// from the image in smem.  Software pipeline over the CTA's tiles (8 per
+// sample): stage tile i (A double-buffered) -> issue its MMAs -> epilogue of
+// tile i-1 (main + cross, ReLU, the per-sample power-of-two scale of
+// conv1_fwd_kernel's a-priori bound, fp16 hi / lo NHWC stores); the next
+// sample's image is fetched by a bulk async copy while the current one is
+// processed.  One CTA per weight group of G slots.
+constexpr int C1F_TILE = 128;
+constexpr int C1F_TILES = (S1 * S1 + C1F_TILE - 1) / C1F_TILE;  // 8 (last: 4 positions)
+constexpr int C1F_A = C1F_TILE * 128;                           // 16 KB per part
+constexpr int C1F_STAGE = 2 * C1F_A;                            // hi | lo
+constexpr int C1F_B = 64 * 128;                                 // [W hi; W lo] x 32 k
+constexpr int C1F_THREADS = 256;
+constexpr int C1F_GMAX = 16;
+constexpr int C1F_SMEM = 1024 + C1F_B + 2 * C1F_STAGE + 2 * IMG * 4 + 256;  // ~97 KB: 2 CTAs per SM
+constexpr uint32_t C1F_IDESC2 = tc::idesc_tf32(128, 2 * C1);
+constexpr uint32_t C1F_IDESC = tc::idesc_tf32(128, C1);
+
+__global__ void __launch_bounds__(C1F_THREADS, 2) conv1_fwd_tc_kernel(
+    const float* __restrict__ X, const int64_t* __restrict__ slot_row, const float* __restrict__ theta,
+    const float* __restrict__ delta, int64_t ld, int B, int N, int G, __half* __restrict__ a1fh,
+    __half* __restrict__ a1fl, float* __restrict__ a1scale) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sB = sm;
+  uint8_t* sA = sm + C1F_B;                                         // [2][hi 16 KB | lo 16 KB]
+  float* img = reinterpret_cast<float*>(sA + 2 * C1F_STAGE);        // [2][3][32][32]
+  uint64_t* done = reinterpret_cast<uint64_t*>(img + 2 * IMG);      // [2] MMA completion per A stage
+  uint64_t* imfull = done + 2;                                      // [2] image arrival
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(imfull + 2);
+  __shared__ float wsum[C1];   // sum_k |W[o, k]| (a1 bound)
+  __shared__ float red[8];
+  __shared__ float s_scale[2];
+  __shared__ int s_slot[C1F_GMAX];
+  __shared__ int s_ns;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, t = threadIdx.x;
+  const int n0 = blockIdx.x * G;
+  const float* dc = delta ? delta + (int64_t)(n0 / B) * ld : nullptr;
+  const uint32_t sB0 = tc::smem_u32(sB), sA0 = tc::smem_u32(sA), simg = tc::smem_u32(img);
+  // B: rows o (hi) and 32 + o (lo), k = 0..26 weights, 27 bias, 28..31 zero
+  for (int i = t; i < C1 * 32; i += C1F_THREADS) {
+    const int o = i >> 5, k = i & 31;
+    const float v = k < 27 ? wt(theta, dc, O_W1 + o * 27 + k) : (k == 27 ? wt(theta, dc, O_B1 + o) : 0.f);
+    float hi, lo;
+    tc::split_tf32(v, hi, lo);
+    tc::sts_f32(sB0 + tc::sw128_offset(o, k), hi);
+    tc::sts_f32(sB0 + tc::sw128_offset(C1 + o, k), lo);
+  }
+  if (t < C1) {
+    float sw = 0.f;
+    for (int k = 0; k < 27; ++k) sw += fabsf(wt(theta, dc, O_W1 + t * 27 + k));
+    wsum[t] = sw;
+  }
+  if (t == 0) {
+    int ns = 0;
+    for (int b = 0; b < G && n0 + b < N; ++b)
+      if (slot_row[n0 + b] >= 0) s_slot[ns++] = n0 + b;
+    s_ns = ns;
+    for (int j = 0; j < 2; ++j) {
+      tc::mbar_init(&done[j], 1);
+      tc::mbar_init(&imfull[j], 1);
+    }
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc<128>(tmem_slot);
+  tc::fence_proxy_async();
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int ns = s_ns;
+  if (ns == 0) {
+    if (warp == 0) tc::tmem_dealloc<128>(tmem);
+    return;
+  }
+  auto fetch = [&](int j) {  // bulk async copy of sample j's image into img[j & 1]
+    tc::mbar_arrive_expect_tx(&imfull[j & 1], IMG * 4);
+    tc::bulk_load(img + (j & 1) * IMG, X + slot_row[s_slot[j]] * IMG, IMG * 4, &imfull[j & 1]);
+  };
+  if (t == 0) fetch(0);
+  // im2col job: position row pl, k range [16*kh, 16*kh + 16)
+  const int pl = t & (C1F_TILE - 1), kh = t >> 7;
+  uint32_t koff[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int k = min(16 * kh + j, 26), ci = k / 9, ky = (k % 9) / 3, kx = k % 3;
+    koff[j] = 4 * (ci * S0 * S0 + ky * S0 + kx);
+  }
+  // epilogue job: TMEM lane quadrant q = warp % 4, channel half chh = warp / 4
+  const int q = warp & 3, chh = warp >> 2;
+  auto epilogue = [&](int i) {
+    const int buf = i & 1, j = i / C1F_TILES, tile = i - j * C1F_TILES, n = s_slot[j];
+    tc::mbar_wait(&done[buf], (i >> 1) & 1);
+    tc::tc_fence_after();
+    const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + buf * 64 + chh * 16;
+    uint32_t v0[16], v1[16];
+    tc::tmem_ld16(base, v0);
+    tc::tmem_ld16(base + C1, v1);
+    tc::tmem_ld_wait();
+    tc::tc_fence_before();
+    const float sc = s_scale[j & 1];
+    const int p = tile * C1F_TILE + q * 32 + lane;
+    if (p < S1 * S1) {
+      uint32_t hw[8], lw[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float z0 = fmaxf(__uint_as_float(v0[2 * e]) + __uint_as_float(v1[2 * e]), 0.f) * sc;
+        const float z1 = fmaxf(__uint_as_float(v0[2 * e + 1]) + __uint_as_float(v1[2 * e + 1]), 0.f) * sc;
+        __half h0, l0, h1, l1;
+        split_f16(z0, h0, l0);
+        split_f16(z1, h1, l1);
+        const __half2 hh = __halves2half2(h0, h1), ll = __halves2half2(l0, l1);
+        hw[e] = *reinterpret_cast<const uint32_t*>(&hh);
+        lw[e] = *reinterpret_cast<const uint32_t*>(&ll);
+      }
+      const int64_t off = (int64_t)n * A1 + (int64_t)p * C1 + chh * 16;
+      uint4* dh = reinterpret_cast<uint4*>(a1fh + off);
+      uint4* dl = reinterpret_cast<uint4*>(a1fl + off);
+      dh[0] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+      dh[1] = make_uint4(hw[4], hw[5], hw[6], hw[7]);
+      dl[0] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+      dl[1] = make_uint4(lw[4], lw[5], lw[6], lw[7]);
+    }
+  };
+  const int T = ns * C1F_TILES;
+  for (int i = 0; i < T; ++i) {
+    const int buf = i & 1, j = i / C1F_TILES, tile = i - j * C1F_TILES;
+    const uint32_t im = simg + (j & 1) * IMG * 4;
+    if (tile == 0) {  // sample j starts: its image has landed; per-sample a1 scale
+      tc::mbar_wait(&imfull[j & 1], (j >> 1) & 1);
+      float xm = 0.f;
+      for (int e = t; e < IMG; e += C1F_THREADS) xm = fmaxf(xm, fabsf(tc::lds_f32(im + 4 * e)));
+      xm = warp_max(xm);
+      if (lane == 0) red[warp] = xm;
+      __syncthreads();  // also: every thread is past the staging of sample j-1 (its image buffer is free)
+      if (warp == 0) {
+        float m = lane < C1F_THREADS / 32 ? red[lane] : 0.f;
+        m = warp_max(m);
+        const float bound = warp_max(fabsf(wt(theta, dc, O_B1 + lane)) + m * wsum[lane]);
+        if (lane == 0) {
+          const float scv = bound > 0.f ? exp2f(14.f - ceilf(log2f(bound))) : 1.f;
+          s_scale[j & 1] = scv;
+          a1scale[s_slot[j]] = scv;
+          if (j + 1 < ns) fetch(j + 1);
+        }
+      }
+    }
+    if (i >= 2) tc::mbar_wait(&done[buf], ((i - 2) >> 1) & 1);  // tile i-2's MMAs are done with this A stage
+    {
+      const int p = tile * C1F_TILE + pl, y = p / S1, x = p - y * S1;
+      const bool valid = p < S1 * S1;
+      const uint32_t ib = im + 4 * (y * S0 + x);
+      const uint32_t ah = sA0 + buf * C1F_STAGE, al = ah + C1F_A;
+#pragma unroll
+      for (int c4 = 0; c4 < 4; ++c4) {
+        float hv[4], lv[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int jj = 4 * c4 + e, k = 16 * kh + jj;
+          float v = 0.f;
+          if (valid) v = k < 27 ? tc::lds_f32(ib + koff[jj]) : (k == 27 ? 1.f : 0.f);
+          tc::split_tf32(v, hv[e], lv[e]);
+        }
+        const uint32_t off = tc::sw128_offset(pl, 16 * kh + 4 * c4);
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(ah + off), "f"(hv[0]), "f"(hv[1]), "f"(hv[2]),
+                     "f"(hv[3]) : "memory");
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(al + off), "f"(lv[0]), "f"(lv[1]), "f"(lv[2]),
+                     "f"(lv[3]) : "memory");
+      }
+    }
+    tc::fence_proxy_async();
+    tc::tc_fence_before();
+    __syncthreads();  // tile i staged; tile i-2's TMEM accumulator drained (epilogue of i-2 ran before)
+    tc::tc_fence_after();
+    if (warp == 0) {
+      if (tc::elect_one()) {
+        const uint32_t d = tmem + buf * 64;
+        const uint32_t ah = sA0 + buf * C1F_STAGE, al = ah + C1F_A;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const uint64_t bd = tc::sdesc_k128(sB0 + 32 * kk);
+          tc::mma_tf32(d, tc::sdesc_k128(ah + 32 * kk), bd, C1F_IDESC2, kk != 0);
+          tc::mma_tf32(d + C1, tc::sdesc_k128(al + 32 * kk), bd, C1F_IDESC, 1);
+        }
+        tc::mma_commit(&done[buf]);
+      }
+      __syncwarp();
+    }
+    if (i >= 1) epilogue(i - 1);
+  }
+  epilogue(T - 1);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  if (warp == 0) tc::tmem_dealloc<128>(tmem);
+}
+
 // ------------------------------------------ conv1 backward-weights (tcgen05)
 // dW1[o, k] = sum over the client's samples and positions p of dz1[p, o] * xcol[p, k],
 // k = (ci, ky, kx) (27) plus a constant-1 column k = 27 that yields the bias
@@ -2421,6 +2625,7 @@ int set_smem_limits() {
   cudaFuncSetAttribute(fc1_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FT_SMEM);
   cudaFuncSetAttribute(conv2_bwd_w_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BW_SMEM);
   cudaFuncSetAttribute(conv1_bwd_w_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, W1_SMEM);
+  cudaFuncSetAttribute(conv1_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C1F_SMEM);
   done = true;
   return launch_status("cnn: cudaFuncSetAttribute");
 }
@@ -2445,9 +2650,14 @@ int prep_theta_images(const float* theta, const Work& w, cudaStream_t s) {
 int forward(const float* X, const float* theta, const float* delta, int64_t ld, int B, int N, int G,
             const Work& w, cudaStream_t s, const int32_t* client_nb, bool shared_fc1 = false) {
   const bool tc = g_conv_impl == 1;
-  FB_LAUNCH("conv1_fwd_kernel", s, conv1_fwd_kernel<<<N, 256, 0, s>>>(X, w.slot_row, theta, delta, ld, B,
-                                                               tc ? nullptr : w.a1, tc ? w.a1fh : nullptr, w.a1fl,
-                                                               w.a1scale));
+  if (tc) {
+    const int g1 = delta ? B : C1F_GMAX;  // slots per CTA: one client's batch (its own weights), or 16 at theta_t
+    FB_LAUNCH("conv1_fwd_tc_kernel", s, conv1_fwd_tc_kernel<<<(N + g1 - 1) / g1, C1F_THREADS, C1F_SMEM, s>>>(
+                                            X, w.slot_row, theta, delta, ld, B, N, g1, w.a1fh, w.a1fl, w.a1scale));
+  } else {
+    FB_LAUNCH("conv1_fwd_kernel", s, conv1_fwd_kernel<<<N, 256, 0, s>>>(X, w.slot_row, theta, delta, ld, B, w.a1,
+                                                                        nullptr, nullptr, w.a1scale));
+  }
   if (tc) {
     // weight groups: one per client in training (G = B), one shared image at theta_t in evaluation
     const int groups = delta ? (N + B - 1) / B : 1;
