@@ -1469,7 +1469,13 @@ __global__ void __launch_bounds__(256) pooled_split_kernel(const float* __restri
                                                            float* __restrict__ pscale) {
   __shared__ float red[32];
   const int n = blockIdx.x;
-  if (slot_row[n] < 0) return;
+  if (slot_row[n] < 0) {  // inactive slot: zero operand rows (the factored fc1 history reads every slot)
+    uint2* dh = reinterpret_cast<uint2*>(ph + (int64_t)n * FLAT);
+    uint2* dl = reinterpret_cast<uint2*>(pl + (int64_t)n * FLAT);
+    for (int i = threadIdx.x; i < FLAT / 4; i += blockDim.x) dh[i] = dl[i] = make_uint2(0u, 0u);
+    if (threadIdx.x == 0) pscale[n] = 1.f;
+    return;
+  }
   const float4* src = reinterpret_cast<const float4*>(pooled + (int64_t)n * FLAT);
   float m = 0.f;
   for (int i = threadIdx.x; i < FLAT / 4; i += blockDim.x) {
@@ -1706,6 +1712,214 @@ __global__ void __launch_bounds__(KCHUNK / 4) fc1_dp_hist_kernel(int B, const in
 #pragma unroll
   for (int b = 0; b < GM; ++b)
     if (b < nb) reinterpret_cast<float4*>(dp + (int64_t)(n0 + b) * FLAT + k0)[t] = acc[b];
+}
+
+// ----------------------------------------- fc1 materialize (tcgen05)
+// End of a factored-fc1 run: delta_fc1[c][k][h] = sum_j coef_j dz3_j[h] p_j[k]
+// over the client's <= 64 history rows j = (step s, slot b).  A GEMM per
+// client with M = k (98 tiles of 128), N = h (128), K = j (64 = 4 x 16):
+// A = P^T from the fp16 hi / lo pooled history the tcgen05 fc1 forward
+// already wrote (per-row power-of-two scale pscale_j), MN-major: one 3-D TMA
+// box {64 k, B slots, S steps} per 64-wide M block lands the client's rows
+// j = s*B + b as consecutive 128-byte K rows; B = U' = coef_j dz3_j /
+// pscale_j * beta (beta: per-client power of two), built once per CTA and
+// split hi / lo, stacked along N ([U hi | U lo], N = 256) so per K step one
+// N = 256 and one N = 128 MMA form the three split products.  TMEM tiles
+// (main | cross, 256 columns) are double-buffered; 8 epilogue warps sum,
+// unscale and write the client's fp32 fc1 delta (6.4 MB, the HBM floor).
+constexpr int FMT_TILE = 128;
+constexpr int FMT_TILES = FLAT / FMT_TILE;        // 98
+constexpr int FMT_SPLIT = 7;                      // CTAs per client: 14 tiles each
+constexpr int FMT_BLK = FC_RMAX * 128;            // 8 KB: 64 j rows x 64 fp16
+constexpr int FMT_STAGE = 4 * FMT_BLK;            // A hi (2 M blocks) | A lo (2 M blocks)
+constexpr int FMT_STAGES = 3;
+constexpr int FMT_BOP = 4 * FMT_BLK;              // U hi (2 N blocks) | U lo (2 N blocks)
+constexpr int FMT_EPI_WARPS = 8;
+constexpr int FMT_THREADS = (2 + FMT_EPI_WARPS) * 32;
+constexpr int FMT_SMEM = 1024 + FMT_BOP + FMT_STAGES * FMT_STAGE + 256;
+constexpr uint32_t FMT_IDESC2 = tc::idesc_f16_mn(128, 2 * HID);
+constexpr uint32_t FMT_IDESC = tc::idesc_f16_mn(128, HID);
+static_assert(FLAT % FMT_TILE == 0 && FMT_TILES % FMT_SPLIT == 0, "fc1 materialize tiles");
+
+// 3-D fp16 map of the pooled history [S][N][FLAT]: box {64 k, B slots, S steps}
+int hist_tensor_map(CUtensorMap* map, const __half* base, int N, int S, int B) {
+  auto fn = encode_fn();
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return FB_ERR_CUDA;
+  }
+  const cuuint64_t dims[3] = {(cuuint64_t)FLAT, (cuuint64_t)N, (cuuint64_t)S};
+  const cuuint64_t strides[2] = {(cuuint64_t)FLAT * 2, (cuuint64_t)N * FLAT * 2};
+  const cuuint32_t box[3] = {64, (cuuint32_t)B, (cuuint32_t)S};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<__half*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (3-D history) failed (%d)", (int)r);
+    return FB_ERR_CUDA;
+  }
+  return FB_OK;
+}
+
+__global__ void __launch_bounds__(FMT_THREADS, 1) fc1_mat_tc_kernel(
+    const __grid_constant__ CUtensorMap tm_hi, const __grid_constant__ CUtensorMap tm_lo, Hist hs,
+    const float* __restrict__ pscale_hist, int N, int S, int B, float lr, float mu, float* __restrict__ delta,
+    int64_t ld) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sB = sm;                                  // [U hi blk0 | U hi blk1 | U lo blk0 | U lo blk1]
+  uint8_t* sA = sm + FMT_BOP;                        // [stage][hi blk0 | hi blk1 | lo blk0 | lo blk1]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sA + FMT_STAGES * FMT_STAGE);
+  uint64_t* full = bars;
+  uint64_t* empty = full + FMT_STAGES;
+  uint64_t* tfull = empty + FMT_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  __shared__ float red[32];
+  __shared__ int s_sc;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, t = threadIdx.x;
+  const int c = blockIdx.x, t0 = blockIdx.y * (FMT_TILES / FMT_SPLIT), nt = FMT_TILES / FMT_SPLIT;
+  const int J = S * B;
+  if (t == 0) {
+    int Sc = 0;
+    while (Sc < S && hs.nbh[Sc * hs.cstride + c] > 0) ++Sc;
+    s_sc = Sc;
+  }
+  __syncthreads();
+  const int Sc = s_sc;
+  if (Sc == 0) return;  // the client never trained: its fc1 delta stays as zero_delta left it
+  // U' rows j = s*B + b (zero when inactive); per-client power-of-two beta puts max |U'| at ~2^14
+  float m = 0.f;
+  for (int i = t; i < FC_RMAX * HID; i += FMT_THREADS) {
+    const int j = i / HID, h = i - j * HID, sp = j / B, bp = j - sp * B;
+    if (j < J && sp < Sc && bp < hs.nbh[sp * hs.cstride + c]) {
+      const int64_t slot = (int64_t)c * B + bp;
+      const float v = hist_coef(lr, mu, Sc, sp) * hs.dz3h[sp * hs.dstride + slot * HID + h] /
+                      pscale_hist[(int64_t)sp * N + slot];
+      m = fmaxf(m, fabsf(v));
+    }
+  }
+  const float beta = block_scale(m, red);
+  for (int i = t; i < FC_RMAX * HID; i += FMT_THREADS) {
+    const int j = i / HID, h = i - j * HID, sp = j / B, bp = j - sp * B;
+    float v = 0.f;
+    if (j < J && sp < Sc && bp < hs.nbh[sp * hs.cstride + c]) {
+      const int64_t slot = (int64_t)c * B + bp;
+      v = hist_coef(lr, mu, Sc, sp) * hs.dz3h[sp * hs.dstride + slot * HID + h] / pscale_hist[(int64_t)sp * N + slot] *
+          beta;
+    }
+    __half hi, lo;
+    split_f16(v, hi, lo);
+    const uint32_t off = (h >> 6) * FMT_BLK + sw128_off16(j, h & 63);
+    *reinterpret_cast<__half*>(sB + off) = hi;
+    *reinterpret_cast<__half*>(sB + 2 * FMT_BLK + off) = lo;
+  }
+  // A rows J..63 of every stage / block stay zero (the TMA box fills rows 0..J-1 only)
+  for (int st = 0; st < FMT_STAGES; ++st)
+    for (int i = t; i < 4 * (FC_RMAX - J) * 32; i += FMT_THREADS) {
+      const int blk = i / ((FC_RMAX - J) * 32), r = i - blk * (FC_RMAX - J) * 32;
+      reinterpret_cast<uint32_t*>(sA + st * FMT_STAGE + blk * FMT_BLK + J * 128)[r] = 0u;
+    }
+  if (t == 0) {
+    for (int i = 0; i < FMT_STAGES; ++i) {
+      tc::mbar_init(&full[i], 1);
+      tc::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&tfull[i], 1);
+      tc::mbar_init(&tempty[i], FMT_EPI_WARPS);
+    }
+    tc::fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc<512>(tmem_slot);
+  tc::fence_proxy_async();
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (warp == 0) {
+    if (lane == 0) {
+      tc::tma_prefetch(&tm_hi);
+      tc::tma_prefetch(&tm_lo);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int ti = 0; ti < nt; ++ti) {
+        const int k0 = (t0 + ti) * FMT_TILE;
+        tc::mbar_wait(&empty[stage], phase ^ 1);
+        tc::mbar_arrive_expect_tx(&full[stage], 4 * J * 128);
+        uint8_t* st_ = sA + stage * FMT_STAGE;
+        tc::tma_load_3d(st_, &tm_hi, k0, c * B, 0, &full[stage]);
+        tc::tma_load_3d(st_ + FMT_BLK, &tm_hi, k0 + 64, c * B, 0, &full[stage]);
+        tc::tma_load_3d(st_ + 2 * FMT_BLK, &tm_lo, k0, c * B, 0, &full[stage]);
+        tc::tma_load_3d(st_ + 3 * FMT_BLK, &tm_lo, k0 + 64, c * B, 0, &full[stage]);
+        if (++stage == FMT_STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    int stage = 0;
+    uint32_t phase = 0;
+    const uint32_t sA0 = tc::smem_u32(sA), sB0 = tc::smem_u32(sB);
+    for (int ti = 0; ti < nt; ++ti) {
+      const int acc = ti & 1;
+      tc::mbar_wait(&tempty[acc], ((ti >> 1) & 1) ^ 1);
+      tc::tc_fence_after();
+      tc::mbar_wait(&full[stage], phase);
+      tc::tc_fence_after();
+      if (tc::elect_one()) {
+        const uint32_t d = tmem + acc * 256;
+        const uint32_t ah = sA0 + stage * FMT_STAGE, al = ah + 2 * FMT_BLK;
+#pragma unroll
+        for (int ks = 0; ks < FC_RMAX / 16; ++ks) {  // 16 history rows = two 8-row K atoms per step
+          const uint64_t adh = tc::sdesc(ah + ks * 2048, FMT_BLK, 1024, 2);
+          const uint64_t adl = tc::sdesc(al + ks * 2048, FMT_BLK, 1024, 2);
+          const uint64_t bd = tc::sdesc(sB0 + ks * 2048, FMT_BLK, 1024, 2);
+          tc::mma2_f16(d, d + HID, adh, adl, bd, FMT_IDESC2, FMT_IDESC, ks != 0);
+        }
+        tc::mma_commit(&empty[stage]);
+        tc::mma_commit(&tfull[acc]);
+      }
+      __syncwarp();
+      if (++stage == FMT_STAGES) { stage = 0; phase ^= 1; }
+    }
+  } else {
+    const int q = warp & 3, hh = (warp - 2) >> 2;  // TMEM lane quadrant, h half
+    const float inv = 1.f / beta;                   // exact: power of two
+    float* dc = delta + (int64_t)c * ld + O_F1;
+    for (int ti = 0; ti < nt; ++ti) {
+      const int acc = ti & 1;
+      tc::mbar_wait(&tfull[acc], (ti >> 1) & 1);
+      tc::tc_fence_after();
+      const int k = (t0 + ti) * FMT_TILE + q * 32 + lane;
+      float* out = dc + (int64_t)k * HID + hh * 64;
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + acc * 256 + hh * 64 + half * 32;
+        uint32_t v0[32], v1[32];
+        tc::tmem_ld32(base, v0);
+        tc::tmem_ld32(base + HID, v1);
+        tc::tmem_ld_wait();
+        if (half == 1) {
+          tc::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          float4 o;
+          o.x = (__uint_as_float(v0[4 * e]) + __uint_as_float(v1[4 * e])) * inv;
+          o.y = (__uint_as_float(v0[4 * e + 1]) + __uint_as_float(v1[4 * e + 1])) * inv;
+          o.z = (__uint_as_float(v0[4 * e + 2]) + __uint_as_float(v1[4 * e + 2])) * inv;
+          o.w = (__uint_as_float(v0[4 * e + 3]) + __uint_as_float(v1[4 * e + 3])) * inv;
+          reinterpret_cast<float4*>(out + half * 32)[e] = o;
+        }
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  if (warp == 1) tc::tmem_dealloc<512>(tmem);
 }
 
 // ------------------------------------------------ conv2 backward-data (tcgen05)
@@ -2563,9 +2777,9 @@ inline int64_t carve(void* base, int N, int Cmax, int H, Work* w) {
                 o_a1s = take(4LL * N), o_dzs = take(4LL * N), o_ws = take(4LL * (Cmax + 1)),
                 o_gram = H > 0 ? take(4LL * Cmax * FC_RMAX * FC_RMAX) : 0,
                 o_acoef = H > 0 ? take(4LL * Cmax * GMAX * FC_RMAX) : 0,
-                o_pfh = take(2LL * N * FLAT), o_pfl = take(2LL * N * FLAT), o_dz3fh = take(2LL * N * HID),
+                o_pfh = take(2LL * hs * N * FLAT), o_pfl = take(2LL * hs * N * FLAT), o_dz3fh = take(2LL * N * HID),
                 o_dz3fl = take(2LL * N * HID), o_thTh = take(2LL * FLAT * HID), o_thTl = take(2LL * FLAT * HID),
-                o_thh = take(2LL * FLAT * HID), o_thl = take(2LL * FLAT * HID), o_psc = take(4LL * N),
+                o_thh = take(2LL * FLAT * HID), o_thl = take(2LL * FLAT * HID), o_psc = take(4LL * hs * N),
                 o_dz3sc = take(4LL * N), o_tsc = take(16);
   if (w && base) {
     char* b = static_cast<char*>(base);
@@ -2626,6 +2840,7 @@ int set_smem_limits() {
   cudaFuncSetAttribute(conv2_bwd_w_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BW_SMEM);
   cudaFuncSetAttribute(conv1_bwd_w_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, W1_SMEM);
   cudaFuncSetAttribute(conv1_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C1F_SMEM);
+  cudaFuncSetAttribute(fc1_mat_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FMT_SMEM);
   done = true;
   return launch_status("cnn: cudaFuncSetAttribute");
 }
@@ -2823,6 +3038,9 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
       Work ws = w;  // this step's slices of the history buffers
       if (fact) {
         ws.pooled = w.pooled + step * hs.pstride;
+        ws.pfh = w.pfh + step * hs.pstride;  // fp16 hi / lo pooled history (tcgen05 fc1 materialize)
+        ws.pfl = w.pfl + step * hs.pstride;
+        ws.pscale = w.pscale + (int64_t)step * N;
         ws.dz3 = w.dz3 + step * hs.dstride;
         ws.client_nb = w.client_nb + step * hs.cstride;
         hs.s = step;
@@ -2910,9 +3128,17 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
       st = fb::launch_status("local_sgd_cnn step");
       if (st) return st;
     }
-    if (fact)
+    if (fact && tcf) {
+      CUtensorMap mh, ml;
+      st = hist_tensor_map(&mh, w.pfh, N, max_steps, B);
+      if (!st) st = hist_tensor_map(&ml, w.pfl, N, max_steps, B);
+      if (st) return st;
+      FB_LAUNCH("fc1_mat_tc_kernel", s, fc1_mat_tc_kernel<<<dim3(Cw, FMT_SPLIT), FMT_THREADS, FMT_SMEM, s>>>(
+                                            mh, ml, hs, w.pscale, N, max_steps, B, lr, prox_mu, dlt, ld_delta));
+    } else if (fact) {
       FB_LAUNCH("fc1_materialize_kernel", s, fc1_materialize_kernel<<<dim3(Cw, FLAT / FM_K), 256, FC1M_SMEM, s>>>(
                                                    hs, max_steps, B, lr, prox_mu, dlt, ld_delta));
+    }
   }
   return FB_OK;
 }
