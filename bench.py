@@ -200,6 +200,10 @@ def kernel_work(wl: dict, counts: dict) -> dict:
         "conv2_bwd_w_kernel": ("tensor", conv2 * train, "FP32 FFMA"),
         "conv1_fwd_kernel": ("tensor", 2 * CNN_MACS["conv1"] * fwd, "FP32 FFMA"),
         "conv1_bwd_w_kernel": ("tensor", 2 * CNN_MACS["conv1"] * train, "FP32 FFMA"),
+        "conv1_fwd_tc_kernel": ("tensor", 2 * CNN_MACS["conv1"] * fwd, "3xTF32 tcgen05 (hi/lo weights stacked along N)"),
+        "conv1_bwd_w_tc_kernel": ("tensor", 2 * CNN_MACS["conv1"] * train, "3xTF32 tcgen05 (hi/lo in operand rows)"),
+        # the client's fp32 fc1 delta written once per run (6.4 MB per client)
+        "fc1_mat_tc_kernel": ("hbm", counts["clients"] * 12544 * 128 * 4, "bytes"),
         # per client-step: read the client's fc1 delta (fwd); read + write it (bwd)
         "fc1_fwd_kernel": ("hbm", steps * fc1_bytes + fwd * 12544 * 4, "bytes"),
         "fc1_bwd_kernel": ("hbm", steps * 2 * fc1_bytes + 2 * train * 12544 * 4, "bytes"),
@@ -207,6 +211,17 @@ def kernel_work(wl: dict, counts: dict) -> dict:
         "weighted_sum_kernel": ("hbm", counts["clients"] * counts["D"] * 4 + counts["D"] * 4 * counts["iters"], "bytes"),
         "zero_delta_kernel": ("hbm", counts["clients"] * counts["D"] * 4, "bytes"),
     }
+
+
+def _ncu_traffic(name: str):
+    """DRAM bytes (read + write) of one launch of `name` from the committed
+    ncu --set full capture (profiles/ncu_traffic.json), with the launch size."""
+    try:
+        k = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())["kernels"][name]
+    except (OSError, KeyError, ValueError):
+        return None
+    return {"dram_bytes_per_launch": k["dram_bytes"], "slots_per_launch": k["slots"],
+            "algorithmic_bytes_per_launch": k.get("algorithmic_bytes"), "source": "profiles/ncu_traffic.json"}
 
 
 def roofline(report: dict, wl: dict, counts: dict, peaks: dict) -> tuple[dict, dict]:
@@ -236,11 +251,13 @@ def roofline(report: dict, wl: dict, counts: dict, peaks: dict) -> tuple[dict, d
     if name in per:
         k = per[name]
         peak = peaks.get("bf16_tflops", 1590.0) if k["bound"] == "tensor" else peaks.get("hbm_gbs", 6650.0)
-        out.update(bound=k["bound"], achieved=k["achieved"], peak=peak, unit=k["unit"], frac=k["frac"], traffic=None,
+        out.update(bound=k["bound"], achieved=k["achieved"], peak=peak, unit=k["unit"], frac=k["frac"],
+                   traffic=_ncu_traffic(name),
                    peak_source=("MEASURED_PEAKS.json bf16_tflops (dense bf16 cuBLAS); the kernel's own math is "
-                                + k.get("math", "") + " (3 MMAs per product on the TF32 half-rate pipe -> at most "
-                                "~1/6 of the bf16 figure in algorithmic FLOP/s)") if k["bound"] == "tensor"
-                   else "MEASURED_PEAKS.json hbm_gbs",
+                                + k.get("math", "") + ": per algorithmic product one N=128 MMA (hi*[Whi;Wlo]) + one "
+                                "N=64 MMA (lo*Whi) -> at most 1/3 of the fp16/bf16 dense rate, and the N=64 half is "
+                                "bound by shared-memory operand reads (tools/microbench/README.md)")
+                   if k["bound"] == "tensor" else "MEASURED_PEAKS.json hbm_gbs",
                    algorithmic=f"{work[name][1]:.4g} {'FLOP' if k['bound'] == 'tensor' else 'bytes'} over {launches} launches")
     else:
         out.update(bound="hbm", achieved=None, peak=peaks.get("hbm_gbs", 6650.0), unit="GB/s", frac=None, traffic=None)
