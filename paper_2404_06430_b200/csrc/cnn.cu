@@ -1147,11 +1147,10 @@ constexpr int FW_A = 14 * 1024;                  // band part, 1 KB aligned
 constexpr int FW_STAGE = 2 * FW_A;               // hi + lo band
 constexpr int FW_B_TAP = C2 * 64;                // 4 KB: 64 rows (o) x 32 ci fp16
 constexpr int WIMG_BYTES = 9 * 2 * FW_B_TAP;     // 73728: [tap][hi|lo]
-constexpr int FW_STAGES = 4;
+constexpr int FW_STAGES = 3;
 constexpr int FW_EPI_WARPS = 16;                 // 4 per TMEM lane quadrant, 16 channels each
 constexpr int FW_THREADS = (2 + FW_EPI_WARPS) * 32;
-constexpr int FW_PL = 2 * FW_ROWS / 2 * SP;      // 56 horizontal pair maxima per channel and tile
-constexpr int FW_EPI_BYTES = 2 * C2 * FW_PL * 4 + 2 * FW_PL * 4 * 2;  // double-buffered [64 ch][56] values + [56][4] code masks
+constexpr int FW_EPI_BYTES = 2 * C2 * 128 * 4;   // double-buffered [64 ch][128 rows] conv outputs (post-ReLU)
 constexpr int FW_SMEM = 1024 + WIMG_BYTES + FW_STAGES * FW_STAGE + FW_EPI_BYTES + 256;
 constexpr int FW_ACC = 2 * C2;                   // main | cross accumulators (64 columns each) per tile
 constexpr uint32_t FW_IDESC = tc::idesc_f16(128, C2);
@@ -1195,7 +1194,7 @@ __global__ void __launch_bounds__(FW_THREADS, 1) conv2_fwd_tc_kernel(
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sB = sm;                                        // [9][2][4 KB]
   uint8_t* sA = sB + WIMG_BYTES;                           // [stages][hi 8 KB | lo 8 KB]
-  uint8_t* sP = sA + FW_STAGES * FW_STAGE;  // [2][64 ch][56] fp32 pair maxima, then [2][56][4] u16 code masks
+  uint8_t* sP = sA + FW_STAGES * FW_STAGE;  // [2][64 ch][128 rows] fp32 conv outputs
   uint64_t* bars = reinterpret_cast<uint64_t*>(sP + FW_EPI_BYTES);
   uint64_t* full = bars;
   uint64_t* empty = bars + FW_STAGES;
@@ -1308,20 +1307,21 @@ __global__ void __launch_bounds__(FW_THREADS, 1) conv2_fwd_tc_kernel(
     }
 #endif
   } else {
-    // 16 epilogue warps: TMEM lane quadrant q = warp % 4 (rows m = 32q + lane),
-    // channel group cg of 16.  The 2x2 max-pool is done as a horizontal pair
-    // max across lanes (x, x+1 are lanes m, m+1) and a vertical max through
-    // shared memory; pairwise first-wins maxima equal the sequential argmax
-    // (q0, q1, q2, q3 order, strict >).  Pair winners' codes travel as one
-    // 16-bit mask per (position, channel group).
+    // 16 epilogue warps.  Phase 1: TMEM lane quadrant q = warp % 4 (row m =
+    // 32q + lane of the 30-wide space), channel group cg of 16 -> bias, ReLU,
+    // unscale into a channel-major smem tile [64 ch][128 rows] (consecutive
+    // lanes -> consecutive rows: conflict-free).  Phase 2: every epilogue
+    // thread takes whole 2x2 windows (sequential argmax in q0, q1, q2, q3
+    // order, strict >) and writes pooled value + code, consecutive threads ->
+    // consecutive pooled positions of one channel.  Tiles alternate between
+    // two smem buffers, so one named barrier per tile orders both phases.
+    // (A two-group producer / consumer split of the phases measured no faster:
+    // MMA operand reads, TMA and these 64 KB per tile share the SMEM bandwidth.)
     const int q = warp & 3, cg = (warp - 2) >> 2;
     const int row = q * 32 + lane;
-    const int r = row / S1, x = row - r * S1;
-    const bool keep = row < FW_MW && x < S2 && !(x & 1);
-    const int pcol = r * SP + (x >> 1);
     const int et = threadIdx.x - 64;
     const float ws = wscale[wg];
-    const uint32_t sPv = tc::smem_u32(sP), sPc = sPv + 2 * C2 * FW_PL * 4;
+    const uint32_t sE0 = tc::smem_u32(sP);
     int tile = 0;
     for (int b = 0; b < G; ++b) {
       const int n = n0 + b;
@@ -1331,7 +1331,7 @@ __global__ void __launch_bounds__(FW_THREADS, 1) conv2_fwd_tc_kernel(
       uint8_t* cout = code + (int64_t)n * FLAT;
       for (int t = 0; t < FW_TILES; ++t, ++tile) {
         const int acc = tile & 1;
-        const uint32_t pv = sPv + acc * (C2 * FW_PL * 4), pc = sPc + acc * (FW_PL * 4 * 2);
+        const uint32_t sE = sE0 + acc * (C2 * 128 * 4);
 #ifdef FB_FWD_PROF
         long long p_a = clock64();
 #endif
@@ -1340,7 +1340,6 @@ __global__ void __launch_bounds__(FW_THREADS, 1) conv2_fwd_tc_kernel(
 #ifdef FB_FWD_PROF
         if (warp == 2 && lane == 0) atomicAdd(&g_prof[4], (unsigned long long)(clock64() - p_a));
 #endif
-        float z[16];
         {
           const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + acc * FW_ACC + cg * 16;
           uint32_t v0[16], v1[16];
@@ -1350,36 +1349,31 @@ __global__ void __launch_bounds__(FW_THREADS, 1) conv2_fwd_tc_kernel(
           tc::tc_fence_before();
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(&tempty[acc]);  // accumulator drained: the next tile may reuse it
-#pragma unroll
-          for (int j = 0; j < 16; ++j) z[j] = __uint_as_float(v0[j]) + __uint_as_float(v1[j]);
-        }
 #ifdef FB_FWD_NOEPI  // timing experiment only: drain TMEM, skip the pooling epilogue
-        if (z[0] == 1.2345f) pout[0] = z[1];
-        continue;
+          if (__uint_as_float(v0[0]) == 1.2345f) pout[0] = __uint_as_float(v1[1]);
+          continue;
 #endif
-        uint32_t mask = 0;
-        const uint32_t pa = pv + (cg * 16 * FW_PL + pcol) * 4;
+          const uint32_t dst = sE + ((cg * 16) * 128 + row) * 4;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float v = fmaxf(fmaf(z[j], inv, bias[cg * 16 + j]), 0.f);
-          const float o = __shfl_xor_sync(0xffffffffu, v, 1);
-          const bool right = o > v;
-          mask |= (uint32_t)right << j;
-          if (keep) tc::sts_f32(pa + j * FW_PL * 4, right ? o : v);
+          for (int j = 0; j < 16; ++j)
+            tc::sts_f32(dst + j * 128 * 4,
+                        fmaxf(fmaf(__uint_as_float(v0[j]) + __uint_as_float(v1[j]), inv, bias[cg * 16 + j]), 0.f));
         }
-        if (keep) tc::sts_u16(pc + (pcol * 4 + cg) * 2, (uint16_t)mask);
         asm volatile("bar.sync 1, %0;" ::"n"(FW_EPI_WARPS * 32) : "memory");
-        // consecutive threads -> consecutive pooled positions of one channel (28 contiguous outputs)
         for (int it = et; it < C2 * 2 * SP; it += FW_EPI_WARPS * 32) {
           const int ch = it / (2 * SP), pp = it - ch * (2 * SP), pr = pp >= SP, px = pp - pr * SP;
-          const int c0 = 2 * pr * SP + px;
-          const float top = tc::lds_f32(pv + (ch * FW_PL + c0) * 4), bot = tc::lds_f32(pv + (ch * FW_PL + c0 + SP) * 4);
-          const uint32_t mt = tc::lds_u16(pc + (c0 * 4 + (ch >> 4)) * 2);
-          const uint32_t mb = tc::lds_u16(pc + ((c0 + SP) * 4 + (ch >> 4)) * 2);
-          const bool lower = bot > top;
+          const uint32_t e0 = sE + (ch * 128 + 2 * pr * S1 + 2 * px) * 4;  // 8-byte aligned: (x, x+1) pairs
+          float q0, q1, q2, q3;
+          asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(q0), "=f"(q1) : "r"(e0) : "memory");
+          asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(q2), "=f"(q3) : "r"(e0 + S1 * 4) : "memory");
+          float best = q0;
+          int arg = 0;
+          if (q1 > best) { best = q1; arg = 1; }
+          if (q2 > best) { best = q2; arg = 2; }
+          if (q3 > best) { best = q3; arg = 3; }
           const int idx = ch * NPOOL + FW_ROWS / 2 * t * SP + pp;
-          pout[idx] = lower ? bot : top;
-          cout[idx] = (uint8_t)(lower ? 2 + ((mb >> (ch & 15)) & 1) : ((mt >> (ch & 15)) & 1));
+          pout[idx] = best;
+          cout[idx] = (uint8_t)arg;
         }
       }
     }
