@@ -905,6 +905,77 @@ __global__ void __launch_bounds__(128) fc1_gram_kernel(Hist hs, int B) {
   }
 }
 
+// Split-K Gram for the current step (replaces fc1_gram_kernel's smem tiles):
+// grid (C, GR_KS), warp w owns history rows j = 8w .. 8w+7, lane = k (strided
+// by 32 over the CTA's K range): per k the lane loads the step's nb <= GM new
+// rows and its 8 history rows straight from the (L2-resident) history with
+// coalesced 128-byte warp loads and does GM x 8 FMAs; each lane sums <= 98
+// products in fp32 (pooled >= 0: no cancellation), the warp tree-reduces and
+// the K splits are summed in fp64 in fixed order by fc1_gram_reduce_kernel.
+constexpr int GR_KS = 4;                       // K splits per client
+constexpr int GR_JW = 8;                       // history rows per warp
+constexpr int GR_WARPS = FC_RMAX / GR_JW;      // 8
+static_assert(FLAT % (GR_KS * 32) == 0, "gram K split");
+template <int GM>
+__global__ void __launch_bounds__(GR_WARPS * 32) fc1_gram_split_kernel(Hist hs, int B, double* __restrict__ part) {
+  const int c = blockIdx.x, ks = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s = hs.s, J = (s + 1) * B;
+  const int nb = hs.nbh[s * hs.cstride + c];
+  if (nb == 0 || warp * GR_JW >= J) return;
+  // new rows are consecutive slots of step s; history rows as 32-bit element offsets
+  // (the host checks S * N * FLAT < 2^31)
+  const float* newp = hs.phist + s * hs.pstride + (int64_t)c * B * FLAT;
+  uint32_t hoff[GR_JW];
+  int live = 0;
+#pragma unroll
+  for (int i = 0; i < GR_JW; ++i) {
+    const int j = min(warp * GR_JW + i, J - 1), sp = j / B, bp = j - sp * B;
+    const bool act = warp * GR_JW + i < J && bp < hs.nbh[sp * hs.cstride + c];
+    live |= act << i;
+    hoff[i] = (uint32_t)(sp * hs.pstride + (int64_t)(c * B + bp) * FLAT);
+  }
+  float acc[GM][GR_JW];
+#pragma unroll
+  for (int b = 0; b < GM; ++b)
+#pragma unroll
+    for (int i = 0; i < GR_JW; ++i) acc[b][i] = 0.f;
+  const int k0 = ks * (FLAT / GR_KS), k1 = k0 + FLAT / GR_KS;
+#pragma unroll 1
+  for (int k = k0 + lane; k < k1; k += 32) {
+    float x[GM], h[GR_JW];
+#pragma unroll
+    for (int b = 0; b < GM; ++b) x[b] = b < nb ? __ldg(newp + b * FLAT + k) : 0.f;
+#pragma unroll
+    for (int i = 0; i < GR_JW; ++i) h[i] = __ldg(hs.phist + hoff[i] + k);
+#pragma unroll
+    for (int b = 0; b < GM; ++b)
+#pragma unroll
+      for (int i = 0; i < GR_JW; ++i) acc[b][i] = fmaf(x[b], h[i], acc[b][i]);
+  }
+  double* out = part + (((int64_t)c * GR_KS + ks) * GMAX) * FC_RMAX;
+#pragma unroll
+  for (int b = 0; b < GM; ++b)
+#pragma unroll
+    for (int i = 0; i < GR_JW; ++i) {
+      const float v = warp_sum(acc[b][i]);
+      if (lane == 0 && b < nb && ((live >> i) & 1)) out[b * FC_RMAX + warp * GR_JW + i] = (double)v;
+    }
+}
+
+__global__ void __launch_bounds__(256) fc1_gram_reduce_kernel(Hist hs, int B, const double* __restrict__ part) {
+  const int c = blockIdx.x;
+  const int s = hs.s, J = (s + 1) * B;
+  const int nb = hs.nbh[s * hs.cstride + c];
+  float* gr = hs.gram + (int64_t)c * hs.R * hs.R;
+  for (int i = threadIdx.x; i < nb * J; i += blockDim.x) {
+    const int b = i / J, j = i - b * J, sp = j / B, bp = j - sp * B;
+    if (bp >= hs.nbh[sp * hs.cstride + c]) continue;
+    double v = 0.0;
+    for (int ks = 0; ks < GR_KS; ++ks) v += part[(((int64_t)c * GR_KS + ks) * GMAX + b) * FC_RMAX + j];
+    gr[(s * B + b) * hs.R + j] = (float)v;
+  }
+}
+
 // dp = dz3 theta_t^T - sum_j a[b][j] p_j.  grid (C, KSPLIT), 4 warps: the
 // theta_t part as in fc1_bwd (warp-streamed 16-row tiles, no delta), staged
 // in smem; then thread = 4 consecutive k of the chunk subtracts the history
@@ -2742,6 +2813,7 @@ struct Work {
   int32_t* slot_hit;
   float *a1, *pooled, *part, *dz3, *dp, *dz1, *db2, *a1scale, *dzscale, *wscale;
   float *gram, *acoef;  // factored fc1 (pooled / dz3 / client_nb then hold hist_steps steps)
+  double* gram_part;    // [Cmax][GR_KS][GMAX][FC_RMAX] split-K Gram partials
   __half *pfh, *pfl, *dz3fh, *dz3fl, *thTh, *thTl, *thh, *thl;  // tcgen05 fc1 operands
   float *pscale, *dz3scale, *tscale;
   unsigned* tmax;
@@ -2770,6 +2842,7 @@ inline int64_t carve(void* base, int N, int Cmax, int H, Work* w) {
                 o_dzfh = take(2LL * N * S2 * S2 * C2), o_dzfl = take(2LL * N * S2 * S2 * C2),
                 o_a1s = take(4LL * N), o_dzs = take(4LL * N), o_ws = take(4LL * (Cmax + 1)),
                 o_gram = H > 0 ? take(4LL * Cmax * FC_RMAX * FC_RMAX) : 0,
+                o_gpart = H > 0 ? take(8LL * Cmax * GR_KS * GMAX * FC_RMAX) : 0,
                 o_acoef = H > 0 ? take(4LL * Cmax * GMAX * FC_RMAX) : 0,
                 o_pfh = take(2LL * hs * N * FLAT), o_pfl = take(2LL * hs * N * FLAT), o_dz3fh = take(2LL * N * HID),
                 o_dz3fl = take(2LL * N * HID), o_thTh = take(2LL * FLAT * HID), o_thTl = take(2LL * FLAT * HID),
@@ -2794,6 +2867,7 @@ inline int64_t carve(void* base, int N, int Cmax, int H, Work* w) {
     w->dzscale = reinterpret_cast<float*>(b + o_dzs);
     w->wscale = reinterpret_cast<float*>(b + o_ws);
     w->gram = H > 0 ? reinterpret_cast<float*>(b + o_gram) : nullptr;
+    w->gram_part = H > 0 ? reinterpret_cast<double*>(b + o_gpart) : nullptr;
     w->acoef = H > 0 ? reinterpret_cast<float*>(b + o_acoef) : nullptr;
     w->pfh = reinterpret_cast<__half*>(b + o_pfh);
     w->pfl = reinterpret_cast<__half*>(b + o_pfl);
@@ -3043,7 +3117,19 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
                                                         Cw, epochs, B, ws.slot_row, ws.client_nb));
       st = forward(X, theta_t, dlt, ld_delta, B, N, B, ws, s, ws.client_nb, fact);
       if (st) return st;
-      if (fact) FB_LAUNCH("fc1_gram_kernel", s, fc1_gram_kernel<<<Cw, 128, 0, s>>>(hs, B));
+      if (fact) {
+        FB_REQUIRE((int64_t)max_steps * N * FLAT < (1LL << 31), "local_sgd_cnn: factored-fc1 history exceeds 2^31 elements");
+        if (B <= 8)
+          FB_LAUNCH("fc1_gram_split_kernel", s, fc1_gram_split_kernel<8><<<dim3(Cw, GR_KS), GR_WARPS * 32, 0, s>>>(
+                                                    hs, B, w.gram_part));
+        else if (B <= 10)
+          FB_LAUNCH("fc1_gram_split_kernel", s, fc1_gram_split_kernel<10><<<dim3(Cw, GR_KS), GR_WARPS * 32, 0, s>>>(
+                                                    hs, B, w.gram_part));
+        else
+          FB_LAUNCH("fc1_gram_split_kernel", s, fc1_gram_split_kernel<GMAX><<<dim3(Cw, GR_KS), GR_WARPS * 32, 0, s>>>(
+                                                    hs, B, w.gram_part));
+        FB_LAUNCH("fc1_gram_reduce_kernel", s, fc1_gram_reduce_kernel<<<Cw, 256, 0, s>>>(hs, B, w.gram_part));
+      }
       FB_LAUNCH("head_kernel", s, head_kernel<<<Cw, HID, 0, s>>>(ws.part, ws.slot_row, N, B, y, theta_t, dlt, ld_delta, ws.client_nb, sp, ws.dz3,
                                      nullptr, nullptr, hs, tcf ? FT_FSPLIT : KSPLIT, tcf ? ws.dz3fh : nullptr,
                                      ws.dz3fl, ws.dz3scale));
