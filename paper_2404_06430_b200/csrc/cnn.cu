@@ -2044,24 +2044,33 @@ __global__ void __launch_bounds__(256) conv2_wimgT_kernel(const float* __restric
 
 // dense dz2 = unpool(dp) * relu'(z2) as scaled fp16 hi / lo NHWC [N][28][28][64];
 // also the per-sample conv2 bias gradient
-constexpr int DZB_SMEM = FLAT * 5;
+constexpr int DZB_LD = NPOOL + 1;               // padded channel stride: channel planes hit different banks
+constexpr int DZB_SMEM = C2 * DZB_LD * 5;
 __global__ void __launch_bounds__(256) dz2_build_kernel(const float* __restrict__ dp, const float* __restrict__ pooled,
                                                         const uint8_t* __restrict__ code,
                                                         const int64_t* __restrict__ slot_row,
                                                         __half* __restrict__ dzfh, __half* __restrict__ dzfl,
                                                         float* __restrict__ dzscale, float* __restrict__ db2) {
-  extern __shared__ float g[];  // [FLAT] values, then [FLAT] codes
+  extern __shared__ float g[];  // [64][197] values, then [64][197] codes
   __shared__ float red[32];
-  uint8_t* cd = reinterpret_cast<uint8_t*>(g + FLAT);
+  uint8_t* cd = reinterpret_cast<uint8_t*>(g + C2 * DZB_LD);
   const int n = blockIdx.x;
   if (slot_row[n] < 0) return;
   float m = 0.f;
-  for (int i = threadIdx.x; i < FLAT; i += blockDim.x) {
-    const int64_t k = (int64_t)n * FLAT + i;
-    const float v = pooled[k] > 0.f ? dp[k] : 0.f;
-    g[i] = v;
-    cd[i] = code[k];
-    m = fmaxf(m, fabsf(v));
+  // vectorised staging: 4 consecutive pooled positions of one channel per load (196 % 4 == 0)
+  const float4* dp4 = reinterpret_cast<const float4*>(dp + (int64_t)n * FLAT);
+  const float4* po4 = reinterpret_cast<const float4*>(pooled + (int64_t)n * FLAT);
+  const uchar4* cd4 = reinterpret_cast<const uchar4*>(code + (int64_t)n * FLAT);
+#pragma unroll 4
+  for (int q = threadIdx.x; q < FLAT / 4; q += blockDim.x) {
+    const float4 d = __ldg(dp4 + q), p = __ldg(po4 + q);
+    const uchar4 c = __ldg(cd4 + q);
+    const int k = 4 * q, ch = k / NPOOL, i = ch * DZB_LD + (k - ch * NPOOL);
+    const float v0 = p.x > 0.f ? d.x : 0.f, v1 = p.y > 0.f ? d.y : 0.f, v2 = p.z > 0.f ? d.z : 0.f,
+                v3 = p.w > 0.f ? d.w : 0.f;
+    g[i] = v0; g[i + 1] = v1; g[i + 2] = v2; g[i + 3] = v3;
+    cd[i] = c.x; cd[i + 1] = c.y; cd[i + 2] = c.z; cd[i + 3] = c.w;
+    m = fmaxf(m, fmaxf(fmaxf(fabsf(v0), fabsf(v1)), fmaxf(fabsf(v2), fabsf(v3))));
   }
   const float sc = block_scale(m, red);  // (synchronises: g / cd visible)
   if (threadIdx.x == 0) dzscale[n] = sc;
@@ -2076,7 +2085,7 @@ __global__ void __launch_bounds__(256) dz2_build_kernel(const float* __restrict_
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       __half h0, l0, h1, l1;
-      const int i0 = (o0 + 2 * e) * NPOOL + pp, i1 = i0 + NPOOL;
+      const int i0 = (o0 + 2 * e) * DZB_LD + pp, i1 = i0 + DZB_LD;
       split_f16((cd[i0] == sub ? g[i0] : 0.f) * sc, h0, l0);
       split_f16((cd[i1] == sub ? g[i1] : 0.f) * sc, h1, l1);
       const __half2 hh = __halves2half2(h0, h1), ll = __halves2half2(l0, l1);
@@ -2089,7 +2098,7 @@ __global__ void __launch_bounds__(256) dz2_build_kernel(const float* __restrict_
   // conv2 bias gradient of this sample: sum over positions of dz2 = sum of g
   if (threadIdx.x < C2) {
     float sb = 0.f;
-    for (int pp = 0; pp < NPOOL; ++pp) sb += g[threadIdx.x * NPOOL + pp];
+    for (int pp = 0; pp < NPOOL; ++pp) sb += g[threadIdx.x * DZB_LD + pp];
     db2[(int64_t)n * C2 + threadIdx.x] = sb;
   }
 }
