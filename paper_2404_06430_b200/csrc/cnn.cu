@@ -1241,15 +1241,21 @@ __global__ void __launch_bounds__(256) conv2_wimg_kernel(const float* __restrict
   for (int i = threadIdx.x; i < C2 * C1 * 9; i += blockDim.x) m = fmaxf(m, fabsf(wt(theta, dc, O_W2 + i)));
   const float sc = block_scale(m, red);
   if (threadIdx.x == 0) wscale[g] = sc;
-  uint8_t* img = wimg + (int64_t)g * WIMG_BYTES;
+  // the 72 KB image is assembled in smem (scattered 2-byte swizzled stores) and
+  // written out with coalesced 16-byte stores
+  extern __shared__ uint4 wim_s[];
+  uint8_t* simg = reinterpret_cast<uint8_t*>(wim_s);
   for (int i = threadIdx.x; i < C2 * C1 * 9; i += blockDim.x) {
     const int o = i / (C1 * 9), r = i - o * (C1 * 9), ci = r / 9, tap = r - ci * 9;
     __half h, l;
     split_f16(wt(theta, dc, O_W2 + i) * sc, h, l);
     const uint32_t off = sw64_off16(o, ci);
-    *reinterpret_cast<__half*>(img + (tap * 2 + 0) * FW_B_TAP + off) = h;
-    *reinterpret_cast<__half*>(img + (tap * 2 + 1) * FW_B_TAP + off) = l;
+    *reinterpret_cast<__half*>(simg + (tap * 2 + 0) * FW_B_TAP + off) = h;
+    *reinterpret_cast<__half*>(simg + (tap * 2 + 1) * FW_B_TAP + off) = l;
   }
+  __syncthreads();
+  uint4* img = reinterpret_cast<uint4*>(wimg + (int64_t)g * WIMG_BYTES);
+  for (int i = threadIdx.x; i < WIMG_BYTES / 16; i += blockDim.x) img[i] = wim_s[i];
 }
 
 #ifdef FB_FWD_PROF
@@ -2031,15 +2037,19 @@ __global__ void __launch_bounds__(256) conv2_wimgT_kernel(const float* __restric
   for (int i = threadIdx.x; i < C2 * C1 * 9; i += blockDim.x) m = fmaxf(m, fabsf(theta[O_W2 + i] - dc[O_W2 + i]));
   const float sc = block_scale(m, red);
   if (threadIdx.x == 0) wscale[g] = sc;
-  uint8_t* img = wimg + (int64_t)g * WIMGT_BYTES;
+  extern __shared__ uint4 wim_s[];  // assembled in smem, written out coalesced
+  uint8_t* simg = reinterpret_cast<uint8_t*>(wim_s);
   for (int i = threadIdx.x; i < C2 * C1 * 9; i += blockDim.x) {
     const int o = i / (C1 * 9), r = i - o * (C1 * 9), ci = r / 9, tap = r - ci * 9;
     __half h, l;
     split_f16((theta[O_W2 + i] - dc[O_W2 + i]) * sc, h, l);
     const uint32_t off = sw128_off16(ci, o);
-    *reinterpret_cast<__half*>(img + (tap * 2 + 0) * BX_B_TAP + off) = h;
-    *reinterpret_cast<__half*>(img + (tap * 2 + 1) * BX_B_TAP + off) = l;
+    *reinterpret_cast<__half*>(simg + (tap * 2 + 0) * BX_B_TAP + off) = h;
+    *reinterpret_cast<__half*>(simg + (tap * 2 + 1) * BX_B_TAP + off) = l;
   }
+  __syncthreads();
+  uint4* img = reinterpret_cast<uint4*>(wimg + (int64_t)g * WIMGT_BYTES);
+  for (int i = threadIdx.x; i < WIMGT_BYTES / 16; i += blockDim.x) img[i] = wim_s[i];
 }
 
 // dense dz2 = unpool(dp) * relu'(z2) as scaled fp16 hi / lo NHWC [N][28][28][64];
@@ -2494,7 +2504,10 @@ __global__ void __launch_bounds__(W1_THREADS, 2) conv1_bwd_w_tc_kernel(const flo
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, t = threadIdx.x;
   const uint32_t s0 = tc::smem_u32(sm), simg = tc::smem_u32(img);
   // rows 28-31 / 60-63 of B (padding of k) stay zero; staging never writes them
-  for (int i = t; i < 2 * W1_STAGE / 16; i += W1_THREADS) reinterpret_cast<uint4*>(sm)[i] = make_uint4(0, 0, 0, 0);
+  for (int i = t; i < 2 * (W1_CH / 32) * 2 * 4 * 8; i += W1_THREADS) {  // stage, atom, hi/lo, 4 rows, 8 x 16 B
+    const int q = i & 7, r = (i >> 3) & 3, part = (i >> 5) & 1, atom = i >> 6;
+    reinterpret_cast<uint4*>(sm + atom * W1_ATOM + 8192 + (part * 32 + 28 + r) * 128)[q] = make_uint4(0, 0, 0, 0);
+  }
   if (t == 0) {
     tc::mbar_init(&done[0], 1);
     tc::mbar_init(&done[1], 1);
@@ -2918,6 +2931,8 @@ int set_smem_limits() {
   cudaFuncSetAttribute(conv1_bwd_w_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, W1_SMEM);
   cudaFuncSetAttribute(conv1_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C1F_SMEM);
   cudaFuncSetAttribute(fc1_mat_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FMT_SMEM);
+  cudaFuncSetAttribute(conv2_wimg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, WIMG_BYTES);
+  cudaFuncSetAttribute(conv2_wimgT_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, WIMGT_BYTES);
   done = true;
   return launch_status("cnn: cudaFuncSetAttribute");
 }
@@ -2953,7 +2968,7 @@ int forward(const float* X, const float* theta, const float* delta, int64_t ld, 
   if (tc) {
     // weight groups: one per client in training (G = B), one shared image at theta_t in evaluation
     const int groups = delta ? (N + B - 1) / B : 1;
-    FB_LAUNCH("conv2_wimg_kernel", s, conv2_wimg_kernel<<<groups, 256, 0, s>>>(theta, delta, ld, client_nb, w.wimg,
+    FB_LAUNCH("conv2_wimg_kernel", s, conv2_wimg_kernel<<<groups, 256, WIMG_BYTES, s>>>(theta, delta, ld, client_nb, w.wimg,
                                                                                    w.wscale));
     CUtensorMap mh, ml;
     int st = a1f_tensor_map(&mh, w.a1fh, N, S1, FW_BAND);
@@ -3186,7 +3201,7 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
       }
       if (g_conv_impl == 1) {
         FB_LAUNCH("dz2_build_kernel", s, dz2_build_kernel<<<N, 256, DZB_SMEM, s>>>(ws.dp, ws.pooled, ws.code, ws.slot_row, ws.dzfh, ws.dzfl, ws.dzscale, ws.db2));
-        FB_LAUNCH("conv2_wimgT_kernel", s, conv2_wimgT_kernel<<<Cw, 256, 0, s>>>(theta_t, dlt, ld_delta, ws.client_nb,
+        FB_LAUNCH("conv2_wimgT_kernel", s, conv2_wimgT_kernel<<<Cw, 256, WIMGT_BYTES, s>>>(theta_t, dlt, ld_delta, ws.client_nb,
                                                                                  ws.wimg, ws.wscale));
         CUtensorMap mh, ml;
         st = dzf_tensor_map(&mh, ws.dzfh, N, S1, BX_BAND);
