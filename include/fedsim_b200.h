@@ -161,6 +161,12 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
 int fb_gather_rows(const void* src, int64_t row_bytes, const int64_t* row_start,
                    const int32_t* num_rows, int num_clients, const int64_t* dst_start,
                    void* dst, int64_t max_rows_per_client, void* stream);
+/* The same copy with at most num_blocks thread blocks, each copying whole
+ * clients: for a copy stream running beside the compute kernels (the
+ * engine's prefetch of iteration t+1's cohort rows during iteration t). */
+int fb_gather_rows_lite(const void* src, int64_t row_bytes, const int64_t* row_start,
+                        const int32_t* num_rows, int num_clients, const int64_t* dst_start,
+                        void* dst, int num_blocks, void* stream);
 
 /* ------------------------------------------------- a6 + a7 (kernel K2)
  * For every client c: norm[c] = || w[c] * delta[c, :D] ||_2 (fp64

@@ -35,6 +35,38 @@ __global__ void __launch_bounds__(kThreads) gather_rows_kernel(const uint8_t* __
   }
 }
 
+// few-block variant for a copy stream beside the compute kernels: block b
+// copies clients b, b + gridDim.x, ... whole, 4 x 16 B in flight per thread
+__global__ void __launch_bounds__(kThreads) gather_rows_lite_kernel(const uint8_t* __restrict__ src,
+                                                                    int64_t row_bytes,
+                                                                    const int64_t* __restrict__ row_start,
+                                                                    const int32_t* __restrict__ num_rows,
+                                                                    const int64_t* __restrict__ dst_start, int C,
+                                                                    uint8_t* __restrict__ dst) {
+  for (int c = blockIdx.x; c < C; c += gridDim.x) {
+    const int64_t bytes = (int64_t)num_rows[c] * row_bytes;
+    const uint8_t* s = src + row_start[c] * row_bytes;
+    uint8_t* d = dst + dst_start[c] * row_bytes;
+    const bool vec = ((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(d) | (uintptr_t)bytes) & 15u) == 0;
+    if (vec) {
+      const int64_t n16 = bytes >> 4;
+      const uint4* s4 = reinterpret_cast<const uint4*>(s);
+      uint4* d4 = reinterpret_cast<uint4*>(d);
+      int64_t i = threadIdx.x;
+      for (; i + 3 * kThreads < n16; i += 4 * kThreads) {
+        const uint4 a = s4[i], b = s4[i + kThreads], e = s4[i + 2 * kThreads], f = s4[i + 3 * kThreads];
+        d4[i] = a;
+        d4[i + kThreads] = b;
+        d4[i + 2 * kThreads] = e;
+        d4[i + 3 * kThreads] = f;
+      }
+      for (; i < n16; i += kThreads) d4[i] = s4[i];
+    } else {
+      for (int64_t i = threadIdx.x; i < bytes; i += kThreads) d[i] = s[i];
+    }
+  }
+}
+
 }  // namespace
 }  // namespace fb
 
@@ -56,6 +88,18 @@ int fb_gather_rows(const void* src, int64_t row_bytes, const int64_t* row_start,
                 static_cast<const uint8_t*>(src), row_bytes, row_start, num_rows, dst_start,
                 static_cast<uint8_t*>(dst)));
   return fb::launch_status("gather_rows_kernel");
+}
+
+int fb_gather_rows_lite(const void* src, int64_t row_bytes, const int64_t* row_start, const int32_t* num_rows,
+                        int num_clients, const int64_t* dst_start, void* dst, int num_blocks, void* stream) {
+  FB_REQUIRE(row_bytes > 0 && num_clients >= 0 && num_blocks >= 1, "gather_rows_lite: bad arguments");
+  if (num_clients == 0) return FB_OK;
+  cudaStream_t s = fb::as_stream(stream);
+  FB_LAUNCH("gather_rows_lite_kernel", s,
+            fb::gather_rows_lite_kernel<<<(unsigned)(num_blocks < num_clients ? num_blocks : num_clients), fb::kThreads, 0,
+                                          s>>>(static_cast<const uint8_t*>(src), row_bytes, row_start, num_rows,
+                                               dst_start, num_clients, static_cast<uint8_t*>(dst)));
+  return fb::launch_status("gather_rows_lite_kernel");
 }
 
 }  // extern "C"

@@ -83,6 +83,9 @@ def plan_shard(dataset, ctx: CentralContext, rank: int, world_size: int, *, coho
     return cohort, schedule_users(weights, world_size, base).queues[rank]
 
 
+# thread blocks of the prefetch copy (each keeps 4 x 16 B x 256 threads in flight over PCIe)
+PREFETCH_BLOCKS = 48
+
 # layout of the per-context fp64 sums reduced across ranks
 SUM_FIELDS = ("loss", "correct", "points", "per_user_acc", "users", "clipped", "count", "norm", "weight")
 
@@ -231,6 +234,7 @@ class GpuSimulationEngine:
         process_group=None,
         central_epilogue: str = "rank0",
         data_residency: str = "device",
+        prefetch: bool = True,
     ):
         if num_workers < 1:
             raise ValueError("num_workers must be >= 1")
@@ -280,6 +284,13 @@ class GpuSimulationEngine:
         self._repr_cache: dict[str, bytes] = {}
         self.stream = torch.cuda.current_stream(self.device)
         self.io_bytes = {"h2d": 0, "d2h": 0}  # cumulative host<->device traffic of run_iteration
+        # host-resident data: the next iteration's cohort rows are gathered on a copy
+        # stream while this iteration computes (prefetching t+1 during t)
+        self._prefetch = bool(prefetch) and data_residency == "host"
+        self._copy_stream = torch.cuda.Stream(self.device) if self._prefetch else None
+        self._pf: dict = {}
+        self._pf_bufs: dict = {}
+        self._pf_done: dict = {}
 
     @property
     def num_workers(self) -> int:
@@ -307,6 +318,10 @@ class GpuSimulationEngine:
         if not isinstance(state.params, DeviceParams):
             state.params = DeviceParams.from_host(state.params, self.device)
         aggregates, metrics, cohorts, updates = [], {}, [], []
+        if self._prefetch and contexts:
+            # issue iteration t+1's cohort-row copy now, so it runs beside this iteration's
+            # kernels (run_iteration blocks on its per-client results further down)
+            self._prefetch_next(algorithm, state, contexts[0].iteration + 1)
         for ctx in contexts:
             agg, ctx_metrics, cohort, ctx_updates = self._run_context(algorithm, state, ctx)
             if ctx_updates:
@@ -317,7 +332,70 @@ class GpuSimulationEngine:
                 key = (pop, name)
                 metrics[key] = metrics[key] + val if key in metrics else val
             cohorts.append((pop, cohort))
+        if self._prefetch and contexts:
+            done = _torch().cuda.Event()
+            done.record(self.stream)  # every kernel of iteration t that reads its prefetched rows is before this
+            self._pf_done[contexts[0].iteration & 1] = done
+            self._pf.pop(contexts[0].iteration, None)
         return IterationResult(tuple(aggregates), metrics, updates, tuple(cohorts))
+
+    def _prefetch_next(self, algorithm, state, t: int) -> None:
+        """Gather iteration t's cohort rows (host-resident dataset) on the copy
+        stream, overlapping the current iteration's kernels.  Used by
+        _run_context only if the context it is given has the same population,
+        seed and cohort size (so a mispredicted plan just falls back to the
+        synchronous gather)."""
+        torch = _torch()
+        try:
+            nxt = algorithm.get_next_central_contexts(state, t)
+        except Exception:  # noqa: BLE001 -- prediction only
+            return
+        # buffers of this parity were last read by iteration t-2 (its end-of-iteration event)
+        prev = self._pf_done.get(t & 1)
+        if prev is not None:
+            self._copy_stream.wait_event(prev)
+        new = {}
+        for k, ctx in enumerate(nxt):
+            dataset = self._datasets.get(ctx.population)
+            if dataset is None:
+                continue
+            cohort, queue = plan_shard(dataset, ctx, self.rank, self.world_size, cohort_mode=self._cohort_mode,
+                                       poisson_rate=self._poisson_rate, base_policy=self._base_policy,
+                                       base_value=self._base_value)
+            if not queue:
+                continue
+            pop = self.population(ctx.population)
+            idx = np.fromiter((pop.index[u] for u in queue), dtype=np.int64, count=len(queue))
+            num_rows = pop.num_rows[idx].astype(np.int32)
+            dst = np.zeros(len(queue), dtype=np.int64)
+            if len(queue) > 1:
+                dst[1:] = np.cumsum(num_rows[:-1].astype(np.int64))
+            rows = int(num_rows.astype(np.int64).sum())
+            key = (k, t & 1)
+            bufs = self._pf_bufs.get(key)
+            if bufs is None or bufs[0].shape[0] < rows or bufs[0].shape[1] != pop.dim:
+                bufs = (torch.empty((max(rows, 1), pop.dim), dtype=torch.float32, device=self.device),
+                        torch.empty((max(rows, 1),), dtype=torch.int32, device=self.device))
+                self._pf_bufs[key] = bufs
+            meta_h = torch.from_numpy(np.concatenate([pop.row_start[idx].astype(np.int64), dst,
+                                                      num_rows.astype(np.int64)])).pin_memory()
+            with torch.cuda.stream(self._copy_stream):
+                meta = meta_h.to(self.device, non_blocking=True)
+                C = len(queue)
+                src_d, dst_d = meta[:C], meta[C:2 * C]
+                nr_d = meta[2 * C:].to(torch.int32)
+                cs = native.stream_handle(self._copy_stream)
+                # a few blocks only: the copy runs beside the compute kernels without taking their SM slots
+                native.call("fb_gather_rows_lite", native.ptr(pop.X), 4 * pop.dim, native.ptr(src_d), native.ptr(nr_d),
+                            C, native.ptr(dst_d), native.ptr(bufs[0]), PREFETCH_BLOCKS, cs)
+                native.call("fb_gather_rows_lite", native.ptr(pop.y), 4, native.ptr(src_d), native.ptr(nr_d), C,
+                            native.ptr(dst_d), native.ptr(bufs[1]), PREFETCH_BLOCKS, cs)
+                ev = torch.cuda.Event()
+                ev.record(self._copy_stream)
+            self.io_bytes["h2d"] += int(meta_h.numel()) * 8 + rows * (4 * pop.dim + 4)
+            new[(ctx.population, ctx.seed, ctx.cohort_size)] = dict(queue=tuple(queue), X=bufs[0], y=bufs[1],
+                                                                    event=ev, keep=(meta_h, meta, nr_d))
+        self._pf[t] = new
 
     # ------------------------------------------------------------ internals
     def _controls(self, state, D: int):
@@ -389,7 +467,11 @@ class GpuSimulationEngine:
         dev = self._staging.upload(host)
         self.io_bytes["h2d"] += sum(int(a.nbytes) for a in host)
         d_row_start, d_num_rows = dev[0], dev[1]
-        if gathered:
+        pf = self._pf.get(ctx.iteration, {}).pop((pop_key, ctx.seed, ctx.cohort_size), None) if gathered else None
+        if pf is not None and pf["queue"] == tuple(queue):  # rows already on the device (copy stream)
+            self.stream.wait_event(pf["event"])
+            pop = _GatheredPopulation(pf["X"], pf["y"], pop.dim)
+        elif gathered:
             rows = int(num_rows.sum())
             gX = self.ws.tensor("gather_X", (max(rows, 1), pop.dim), torch.float32)
             gy = self.ws.tensor("gather_y", (max(rows, 1),), torch.int32)

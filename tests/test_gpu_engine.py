@@ -175,3 +175,17 @@ def test_engine_metrics_csv_and_checkpoint(golden, tmp_path):
     fb.save_params(res.params, tmp_path / "checkpoint.csv")
     back = fb.load_params(tmp_path / "checkpoint.csv")
     np.testing.assert_array_equal(np.concatenate([back[n] for n in back]), res.params.flat_host())
+
+
+@pytest.mark.parametrize("prefetch", [False, True], ids=["sync-gather", "prefetch"])
+def test_host_resident_dataset_matches_reference_run(golden, prefetch):
+    """data_residency="host": cohort rows gathered from pinned host memory each
+    context (synchronously, or for iteration t+1 on a copy stream during t):
+    identical results to the device-resident run and the reference."""
+    g = golden("mlp_dp")
+    res, thetas = run_engine(CONFIGS["mlp_dp"], data_residency="host", prefetch=prefetch)
+    assert res.cohort_digest == str(g["digest"])
+    for t in range(len(thetas)):
+        assert_close_fp32(thetas[t], g["thetas"][t], what=f"theta after iteration {t}")
+    _, dev_thetas = run_engine(CONFIGS["mlp_dp"])
+    np.testing.assert_array_equal(thetas, dev_thetas)
