@@ -1807,7 +1807,7 @@ constexpr int FMT_STAGES = 3;
 constexpr int FMT_BOP = 4 * FMT_BLK;              // U hi (2 N blocks) | U lo (2 N blocks)
 constexpr int FMT_EPI_WARPS = 8;
 constexpr int FMT_THREADS = (2 + FMT_EPI_WARPS) * 32;
-constexpr int FMT_SMEM = 1024 + FMT_BOP + FMT_STAGES * FMT_STAGE + 256;
+constexpr int FMT_SMEM = 1024 + FMT_BOP + FMT_STAGES * FMT_STAGE + 256 + FMT_EPI_WARPS * 32 * 33 * 4;
 constexpr uint32_t FMT_IDESC2 = tc::idesc_f16_mn(128, 2 * HID);
 constexpr uint32_t FMT_IDESC = tc::idesc_f16_mn(128, HID);
 static_assert(FLAT % FMT_TILE == 0 && FMT_TILES % FMT_SPLIT == 0, "fc1 materialize tiles");
@@ -1957,12 +1957,14 @@ __global__ void __launch_bounds__(FMT_THREADS, 1) fc1_mat_tc_kernel(
     const int q = warp & 3, hh = (warp - 2) >> 2;  // TMEM lane quadrant, h half
     const float inv = 1.f / beta;                   // exact: power of two
     float* dc = delta + (int64_t)c * ld + O_F1;
+    // per-warp 32 x 33 transpose tile: lane = k row in TMEM; the stores go out as
+    // 4 rows x 128 contiguous bytes per instruction instead of 32 rows x 16 B
+    const uint32_t tw = tc::smem_u32(sA + FMT_STAGES * FMT_STAGE + 256) + (warp - 2) * 32 * 33 * 4;
     for (int ti = 0; ti < nt; ++ti) {
       const int acc = ti & 1;
       tc::mbar_wait(&tfull[acc], (ti >> 1) & 1);
       tc::tc_fence_after();
-      const int k = (t0 + ti) * FMT_TILE + q * 32 + lane;
-      float* out = dc + (int64_t)k * HID + hh * 64;
+      const int kbase = (t0 + ti) * FMT_TILE + q * 32;
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
         const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + acc * 256 + hh * 64 + half * 32;
@@ -1976,14 +1978,21 @@ __global__ void __launch_bounds__(FMT_THREADS, 1) fc1_mat_tc_kernel(
           if (lane == 0) tc::mbar_arrive(&tempty[acc]);
         }
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
+        for (int j = 0; j < 32; ++j)
+          tc::sts_f32(tw + (lane * 33 + j) * 4, (__uint_as_float(v0[j]) + __uint_as_float(v1[j])) * inv);
+        __syncwarp();
+        const int r = lane >> 3, c4 = (lane & 7) * 4;
+#pragma unroll
+        for (int rr = 0; rr < 8; ++rr) {
+          const int row = rr * 4 + r;
           float4 o;
-          o.x = (__uint_as_float(v0[4 * e]) + __uint_as_float(v1[4 * e])) * inv;
-          o.y = (__uint_as_float(v0[4 * e + 1]) + __uint_as_float(v1[4 * e + 1])) * inv;
-          o.z = (__uint_as_float(v0[4 * e + 2]) + __uint_as_float(v1[4 * e + 2])) * inv;
-          o.w = (__uint_as_float(v0[4 * e + 3]) + __uint_as_float(v1[4 * e + 3])) * inv;
-          reinterpret_cast<float4*>(out + half * 32)[e] = o;
+          o.x = tc::lds_f32(tw + (row * 33 + c4) * 4);
+          o.y = tc::lds_f32(tw + (row * 33 + c4 + 1) * 4);
+          o.z = tc::lds_f32(tw + (row * 33 + c4 + 2) * 4);
+          o.w = tc::lds_f32(tw + (row * 33 + c4 + 3) * 4);
+          *reinterpret_cast<float4*>(dc + (int64_t)(kbase + row) * HID + hh * 64 + half * 32 + c4) = o;
         }
+        __syncwarp();
       }
     }
   }
