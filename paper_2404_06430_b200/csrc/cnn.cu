@@ -1800,7 +1800,7 @@ __global__ void __launch_bounds__(KCHUNK / 4) fc1_dp_hist_kernel(int B, const in
 // unscale and write the client's fp32 fc1 delta (6.4 MB, the HBM floor).
 constexpr int FMT_TILE = 128;
 constexpr int FMT_TILES = FLAT / FMT_TILE;        // 98
-constexpr int FMT_SPLIT = 7;                      // CTAs per client: 14 tiles each
+constexpr int FMT_SPLIT = 2;                      // CTAs per client: 49 tiles each (U' built twice per client)
 constexpr int FMT_BLK = FC_RMAX * 128;            // 8 KB: 64 j rows x 64 fp16
 constexpr int FMT_STAGE = 4 * FMT_BLK;            // A hi (2 M blocks) | A lo (2 M blocks)
 constexpr int FMT_STAGES = 3;
