@@ -2493,6 +2493,9 @@ constexpr int W1_CPS = (S1 * S1 + W1_CH - 1) / W1_CH;  // 15 chunks per sample (
 constexpr int W1_ATOM = 16 * 1024;                  // per 32-position K atom: A rows 0-63 (8 KB) | B rows 0-63 (8 KB)
 constexpr int W1_STAGE = (W1_CH / 32) * W1_ATOM;    // 32 KB
 constexpr int W1_THREADS = 256;
+constexpr int W1_NLD = W1_CH * 8 / W1_THREADS;      // dz1 float4 loads per thread per chunk
+constexpr int W1_KPER = 28 / (W1_THREADS / W1_CH);  // im2col rows per thread
+static_assert(W1_NLD * W1_THREADS == W1_CH * 8 && W1_KPER * (W1_THREADS / W1_CH) == 28, "conv1 bwd-w staging split");
 constexpr int W1_SMEM = 1024 + 2 * W1_STAGE + IMG * 4 + 32 * 33 * 4 + 64;
 constexpr uint32_t W1_IDESC = tc::idesc_tf32(128, 64);
 
@@ -2551,18 +2554,18 @@ __global__ void __launch_bounds__(W1_THREADS, 2) conv1_bwd_w_tc_kernel(const flo
   // (position f / 8, channel quad f % 8); the next chunk is prefetched into
   // registers a chunk ahead
   const int nchunks = nb * W1_CPS;
-  auto load_dz = [&](int i, float4 (&v)[W1_CH / 32]) {
+  auto load_dz = [&](int i, float4 (&v)[W1_NLD]) {
     const int b = i / W1_CPS, p0 = (i - b * W1_CPS) * W1_CH;
     const float4* dzn = reinterpret_cast<const float4*>(dz1 + ((int64_t)c * B + b) * A1 + (int64_t)p0 * C1);
 #pragma unroll
-    for (int j = 0; j < W1_CH / 32; ++j) {
+    for (int j = 0; j < W1_NLD; ++j) {
       const int f = j * W1_THREADS + t;
       v[j] = p0 + (f >> 3) < S1 * S1 ? __ldg(dzn + f) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
   };
-  float4 cur[W1_CH / 32], nxt[W1_CH / 32];
+  float4 cur[W1_NLD], nxt[W1_NLD];
   load_dz(0, cur);
-  const int kq = t >> 6;
+  const int kq = t / W1_CH;
   uint32_t koff[7];  // byte offset of im2col row kq*7+kk relative to the output position
 #pragma unroll
   for (int kk = 0; kk < 7; ++kk) {
@@ -2582,7 +2585,7 @@ __global__ void __launch_bounds__(W1_THREADS, 2) conv1_bwd_w_tc_kernel(const flo
       __syncthreads();
     }
 #pragma unroll
-    for (int j = 0; j < W1_CH / 32; ++j) {
+    for (int j = 0; j < W1_NLD; ++j) {
       const int f = j * W1_THREADS + t, pl = f >> 3, oq = f & 7;
       const float vv[4] = {cur[j].x, cur[j].y, cur[j].z, cur[j].w};
       const uint32_t atom = stg + (pl >> 5) * W1_ATOM;
@@ -2631,7 +2634,7 @@ __global__ void __launch_bounds__(W1_THREADS, 2) conv1_bwd_w_tc_kernel(const flo
     }
     if (warp < 2 && i >= 1) drain(i - 1);
 #pragma unroll
-    for (int j = 0; j < W1_CH / 32; ++j) cur[j] = nxt[j];
+    for (int j = 0; j < W1_NLD; ++j) cur[j] = nxt[j];
   }
   if (warp < 2) drain(nchunks - 1);
   // combine the hi-row (warp 0) and lo-row (warp 1) sums; update dW1 and b1
