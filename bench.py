@@ -273,9 +273,14 @@ def gpu_arm(args, wl):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dist = torch.distributed
+    local = local % max(torch.cuda.device_count(), 1)  # (ranks share a device only in the gloo test mode)
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("FB_DIST_BACKEND", "nccl")  # "gloo": N ranks on one GPU (flow test only)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
 
     ds = build(wl)
