@@ -912,10 +912,10 @@ __global__ void __launch_bounds__(128) fc1_gram_kernel(Hist hs, int B) {
 // coalesced 128-byte warp loads and does GM x 8 FMAs; each lane sums <= 98
 // products in fp32 (pooled >= 0: no cancellation), the warp tree-reduces and
 // the K splits are summed in fp64 in fixed order by fc1_gram_reduce_kernel.
-constexpr int GR_KS = 4;                       // K splits per client
+constexpr int GR_KS = 8;                       // max K splits per client (runtime: gridDim.y = 4 or 8)
 constexpr int GR_JW = 8;                       // history rows per warp
 constexpr int GR_WARPS = FC_RMAX / GR_JW;      // 8
-static_assert(FLAT % (GR_KS * 32) == 0, "gram K split");
+static_assert(FLAT % (GR_KS * 32) == 0 && FLAT % (4 * 32) == 0, "gram K split");
 template <int GM>
 __global__ void __launch_bounds__(GR_WARPS * 32) fc1_gram_split_kernel(Hist hs, int B, double* __restrict__ part) {
   const int c = blockIdx.x, ks = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -939,7 +939,8 @@ __global__ void __launch_bounds__(GR_WARPS * 32) fc1_gram_split_kernel(Hist hs, 
   for (int b = 0; b < GM; ++b)
 #pragma unroll
     for (int i = 0; i < GR_JW; ++i) acc[b][i] = 0.f;
-  const int k0 = ks * (FLAT / GR_KS), k1 = k0 + FLAT / GR_KS;
+  const int nks = gridDim.y;
+  const int k0 = ks * (FLAT / nks), k1 = k0 + FLAT / nks;
 #pragma unroll 1
   for (int k = k0 + lane; k < k1; k += 32) {
     float x[GM], h[GR_JW];
@@ -952,7 +953,7 @@ __global__ void __launch_bounds__(GR_WARPS * 32) fc1_gram_split_kernel(Hist hs, 
 #pragma unroll
       for (int i = 0; i < GR_JW; ++i) acc[b][i] = fmaf(x[b], h[i], acc[b][i]);
   }
-  double* out = part + (((int64_t)c * GR_KS + ks) * GMAX) * FC_RMAX;
+  double* out = part + (((int64_t)c * nks + ks) * GMAX) * FC_RMAX;
 #pragma unroll
   for (int b = 0; b < GM; ++b)
 #pragma unroll
@@ -962,7 +963,7 @@ __global__ void __launch_bounds__(GR_WARPS * 32) fc1_gram_split_kernel(Hist hs, 
     }
 }
 
-__global__ void __launch_bounds__(256) fc1_gram_reduce_kernel(Hist hs, int B, const double* __restrict__ part) {
+__global__ void __launch_bounds__(256) fc1_gram_reduce_kernel(Hist hs, int B, int nks, const double* __restrict__ part) {
   const int c = blockIdx.x;
   const int s = hs.s, J = (s + 1) * B;
   const int nb = hs.nbh[s * hs.cstride + c];
@@ -971,7 +972,7 @@ __global__ void __launch_bounds__(256) fc1_gram_reduce_kernel(Hist hs, int B, co
     const int b = i / J, j = i - b * J, sp = j / B, bp = j - sp * B;
     if (bp >= hs.nbh[sp * hs.cstride + c]) continue;
     double v = 0.0;
-    for (int ks = 0; ks < GR_KS; ++ks) v += part[(((int64_t)c * GR_KS + ks) * GMAX + b) * FC_RMAX + j];
+    for (int ks = 0; ks < nks; ++ks) v += part[(((int64_t)c * nks + ks) * GMAX + b) * FC_RMAX + j];
     gr[(s * B + b) * hs.R + j] = (float)v;
   }
 }
@@ -1810,7 +1811,7 @@ constexpr int FMT_THREADS = (2 + FMT_EPI_WARPS) * 32;
 constexpr int FMT_SMEM = 1024 + FMT_BOP + FMT_STAGES * FMT_STAGE + 256 + FMT_EPI_WARPS * 32 * 33 * 4;
 constexpr uint32_t FMT_IDESC2 = tc::idesc_f16_mn(128, 2 * HID);
 constexpr uint32_t FMT_IDESC = tc::idesc_f16_mn(128, HID);
-static_assert(FLAT % FMT_TILE == 0 && FMT_TILES % FMT_SPLIT == 0, "fc1 materialize tiles");
+static_assert(FLAT % FMT_TILE == 0 && FMT_TILES % FMT_SPLIT == 0 && FMT_TILES % 7 == 0, "fc1 materialize tiles");
 
 // 3-D fp16 map of the pooled history [S][N][FLAT]: box {64 k, B slots, S steps}
 int hist_tensor_map(CUtensorMap* map, const __half* base, int N, int S, int B) {
@@ -1850,7 +1851,8 @@ __global__ void __launch_bounds__(FMT_THREADS, 1) fc1_mat_tc_kernel(
   __shared__ float red[32];
   __shared__ int s_sc;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, t = threadIdx.x;
-  const int c = blockIdx.x, t0 = blockIdx.y * (FMT_TILES / FMT_SPLIT), nt = FMT_TILES / FMT_SPLIT;
+  const int nt = FMT_TILES / gridDim.y;  // tiles per CTA (gridDim.y divides 98)
+  const int c = blockIdx.x, t0 = blockIdx.y * nt;
   const int J = S * B;
   if (t == 0) {
     int Sc = 0;
@@ -2125,7 +2127,7 @@ __global__ void __launch_bounds__(256) dz2_build_kernel(const float* __restrict_
 __global__ void __launch_bounds__(BX_THREADS, 1) conv2_bwd_x_tc_kernel(
     const __grid_constant__ CUtensorMap tm_hi, const __grid_constant__ CUtensorMap tm_lo,
     const uint8_t* __restrict__ wimg, const float* __restrict__ wscale, const int64_t* __restrict__ slot_row, int G,
-    const float* __restrict__ dzscale, const __half* __restrict__ a1fh, const __half* __restrict__ a1fl,
+    int B, const float* __restrict__ dzscale, const __half* __restrict__ a1fh, const __half* __restrict__ a1fl,
     float* __restrict__ dz1) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -2140,8 +2142,8 @@ __global__ void __launch_bounds__(BX_THREADS, 1) conv2_bwd_x_tc_kernel(
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = blockIdx.x;  // client
-  const int n0 = g * G;
+  const int n0 = blockIdx.x * G;  // G slots of one client (G divides the batch B)
+  const int g = n0 / B;           // the client: its weight image
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < BX_STAGES; ++i) {
       tc::mbar_init(&full[i], 1);
@@ -2925,9 +2927,13 @@ inline int64_t carve(void* base, int N, int Cmax, int H, Work* w) {
   return off;
 }
 
+int g_num_sms = 148;
+
 int set_smem_limits() {
   static bool done = false;
   if (done) return FB_OK;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   cudaFuncSetAttribute(conv2_fwd_pool_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C2F_SMEM);
   cudaFuncSetAttribute(conv2_bwd_x_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C2X_SMEM);
   cudaFuncSetAttribute(conv2_bwd_w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C2W_SMEM);
@@ -2952,7 +2958,19 @@ int set_smem_limits() {
 // fc1 at theta_t on tcgen05: evaluation and factored training with the tcgen05 conv path
 inline bool fc1_tc(const float* delta, bool shared_fc1) { return g_conv_impl == 1 && (!delta || shared_fc1); }
 
-int g_num_sms = 148;
+// CTAs per client for the per-client kernels when a launch has few clients (a
+// rank's shard at N > 1): split each client's B slots into d groups (d | B)
+// until the grid fills one wave of `per_sm` CTAs per SM.
+inline int client_split(int clients, int B, int per_sm) {
+  int d = 1;
+  while (clients * d < g_num_sms * per_sm) {
+    int nd = d + 1;
+    while (nd <= B && B % nd) ++nd;
+    if (nd > B) break;
+    d = nd;
+  }
+  return d;
+}
 
 // fp16 images of theta_t's fc1 weights for the tcgen05 fc1 kernels
 int prep_theta_images(const float* theta, const Work& w, cudaStream_t s) {
@@ -2970,7 +2988,8 @@ int forward(const float* X, const float* theta, const float* delta, int64_t ld, 
             const Work& w, cudaStream_t s, const int32_t* client_nb, bool shared_fc1 = false) {
   const bool tc = g_conv_impl == 1;
   if (tc) {
-    const int g1 = delta ? B : C1F_GMAX;  // slots per CTA: one client's batch (its own weights), or 16 at theta_t
+    // slots per CTA: (part of) one client's batch (its own weights), or 16 at theta_t
+    const int g1 = delta ? B / client_split(N / B, B, 2) : C1F_GMAX;
     FB_LAUNCH("conv1_fwd_tc_kernel", s, conv1_fwd_tc_kernel<<<(N + g1 - 1) / g1, C1F_THREADS, C1F_SMEM, s>>>(
                                             X, w.slot_row, theta, delta, ld, B, N, g1, w.a1fh, w.a1fl, w.a1scale));
   } else {
@@ -2986,7 +3005,7 @@ int forward(const float* X, const float* theta, const float* delta, int64_t ld, 
     int st = a1f_tensor_map(&mh, w.a1fh, N, S1, FW_BAND);
     if (!st) st = a1f_tensor_map(&ml, w.a1fl, N, S1, FW_BAND);
     if (st) return st;
-    const int gt = delta ? B : 8;  // samples per CTA
+    const int gt = delta ? B / client_split(N / B, B, 1) : 8;  // samples per CTA
     FB_LAUNCH("conv2_fwd_tc_kernel", s, conv2_fwd_tc_kernel<<<(N + gt - 1) / gt, FW_THREADS, FW_SMEM, s>>>(
         mh, ml, w.wimg, w.wscale, delta ? 0 : 1, w.slot_row, N, gt, theta, delta, ld, B, w.a1scale, w.pooled,
         w.code));
@@ -3155,16 +3174,17 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
       if (st) return st;
       if (fact) {
         FB_REQUIRE((int64_t)max_steps * N * FLAT < (1LL << 31), "local_sgd_cnn: factored-fc1 history exceeds 2^31 elements");
+        const int gks = Cw * 4 >= 2 * g_num_sms ? 4 : 8;  // more K splits for a small shard
         if (B <= 8)
-          FB_LAUNCH("fc1_gram_split_kernel", s, fc1_gram_split_kernel<8><<<dim3(Cw, GR_KS), GR_WARPS * 32, 0, s>>>(
+          FB_LAUNCH("fc1_gram_split_kernel", s, fc1_gram_split_kernel<8><<<dim3(Cw, gks), GR_WARPS * 32, 0, s>>>(
                                                     hs, B, w.gram_part));
         else if (B <= 10)
-          FB_LAUNCH("fc1_gram_split_kernel", s, fc1_gram_split_kernel<10><<<dim3(Cw, GR_KS), GR_WARPS * 32, 0, s>>>(
+          FB_LAUNCH("fc1_gram_split_kernel", s, fc1_gram_split_kernel<10><<<dim3(Cw, gks), GR_WARPS * 32, 0, s>>>(
                                                     hs, B, w.gram_part));
         else
-          FB_LAUNCH("fc1_gram_split_kernel", s, fc1_gram_split_kernel<GMAX><<<dim3(Cw, GR_KS), GR_WARPS * 32, 0, s>>>(
+          FB_LAUNCH("fc1_gram_split_kernel", s, fc1_gram_split_kernel<GMAX><<<dim3(Cw, gks), GR_WARPS * 32, 0, s>>>(
                                                     hs, B, w.gram_part));
-        FB_LAUNCH("fc1_gram_reduce_kernel", s, fc1_gram_reduce_kernel<<<Cw, 256, 0, s>>>(hs, B, w.gram_part));
+        FB_LAUNCH("fc1_gram_reduce_kernel", s, fc1_gram_reduce_kernel<<<Cw, 256, 0, s>>>(hs, B, gks, w.gram_part));
       }
       FB_LAUNCH("head_kernel", s, head_kernel<<<Cw, HID, 0, s>>>(ws.part, ws.slot_row, N, B, y, theta_t, dlt, ld_delta, ws.client_nb, sp, ws.dz3,
                                      nullptr, nullptr, hs, tcf ? FT_FSPLIT : KSPLIT, tcf ? ws.dz3fh : nullptr,
@@ -3219,8 +3239,9 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
         st = dzf_tensor_map(&mh, ws.dzfh, N, S1, BX_BAND);
         if (!st) st = dzf_tensor_map(&ml, ws.dzfl, N, S1, BX_BAND);
         if (st) return st;
-        FB_LAUNCH("conv2_bwd_x_tc_kernel", s, conv2_bwd_x_tc_kernel<<<Cw, BX_THREADS, BX_SMEM, s>>>(
-            mh, ml, ws.wimg, ws.wscale, ws.slot_row, B, ws.dzscale, ws.a1fh, ws.a1fl, ws.dz1));
+        const int split = client_split(Cw, B, 1);
+        FB_LAUNCH("conv2_bwd_x_tc_kernel", s, conv2_bwd_x_tc_kernel<<<Cw * split, BX_THREADS, BX_SMEM, s>>>(
+            mh, ml, ws.wimg, ws.wscale, ws.slot_row, B / split, B, ws.dzscale, ws.a1fh, ws.a1fl, ws.dz1));
         CUtensorMap ah, al, dh, dl;
         st = a1f_tensor_map(&ah, ws.a1fh, N, S1, BW_ROWS + 2);
         if (!st) st = a1f_tensor_map(&al, ws.a1fl, N, S1, BW_ROWS + 2);
@@ -3249,7 +3270,8 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
       st = hist_tensor_map(&mh, w.pfh, N, max_steps, B);
       if (!st) st = hist_tensor_map(&ml, w.pfl, N, max_steps, B);
       if (st) return st;
-      FB_LAUNCH("fc1_mat_tc_kernel", s, fc1_mat_tc_kernel<<<dim3(Cw, FMT_SPLIT), FMT_THREADS, FMT_SMEM, s>>>(
+      const int msplit = Cw * FMT_SPLIT >= g_num_sms ? FMT_SPLIT : 7;  // 2 CTAs per client, 7 for a small shard
+      FB_LAUNCH("fc1_mat_tc_kernel", s, fc1_mat_tc_kernel<<<dim3(Cw, msplit), FMT_THREADS, FMT_SMEM, s>>>(
                                             mh, ml, hs, w.pscale, N, max_steps, B, lr, prox_mu, dlt, ld_delta));
     } else if (fact) {
       FB_LAUNCH("fc1_materialize_kernel", s, fc1_materialize_kernel<<<dim3(Cw, FLAT / FM_K), 256, FC1M_SMEM, s>>>(
