@@ -50,6 +50,16 @@ WORKLOADS = {
     "logistic": dict(model="logistic", dim=32, users=1000, val_users=100, ppu=50, cohort=1000, eval_cohort=100,
                      epochs=1, batch=10, lr=0.1, clr=1.0, bound=1.0, sigma=SIGMA_T1500, noise_cohort=1000,
                      eval_every=10, name="logistic fedavg+gaussian-dp cohort1000 (reference-native shape)"),
+    # ragged clients (the reference-native shapes): per-user sizes drawn like
+    # fedsim/cli/bench.py:61-63 -- lognormal(mean 3, sigma 1), rounded, clipped to [1, 500]
+    "mlp-ragged": dict(model="mlp", dim=32, hidden=64, users=1000, val_users=100, ppu=None, ragged=True, cohort=400,
+                       eval_cohort=100, epochs=1, batch=10, lr=0.1, clr=1.0, bound=1.0, sigma=SIGMA_T1500,
+                       noise_cohort=1000, eval_every=10,
+                       name="mlp(64) fedavg+gaussian-dp cohort400, ragged users (StackOverflow-shaped sizes)"),
+    "cnn-ragged": dict(model="cnn", dim=3072, users=1000, val_users=100, ppu=None, ragged=True, cohort=200,
+                       eval_cohort=100, epochs=1, batch=10, lr=0.1, clr=1.0, bound=1.0, sigma=SIGMA_T1500,
+                       noise_cohort=1000, eval_every=10,
+                       name="cifar10-cnn fedavg+gaussian-dp cohort200, ragged users 1-500 (FLAIR-shaped sizes)"),
 }
 
 # algorithmic FLOPs per processed sample for the CNN kernels (2 x MACs of the
@@ -66,9 +76,37 @@ def _torch():
 # ------------------------------------------------------------------ setup
 
 
+def ragged_sizes(n_users: int, seed: int) -> np.ndarray:
+    """fedsim/cli/bench.py:61-63: max(1, round(lognormal(3, 1))), capped at 500."""
+    raw = np.random.default_rng(seed).lognormal(mean=3.0, sigma=1.0, size=n_users)
+    return np.clip(np.maximum(1, np.round(raw)), 1, 500).astype(np.int64)
+
+
+def build_ragged(wl: dict):
+    import paper_2404_06430_b200 as fb
+    from paper_2404_06430_b200.feddata import FederatedDataset, UserDataset
+
+    sizes = {"train": ragged_sizes(wl["users"], 1), "val": ragged_sizes(wl["val_users"], 2)}
+    total = int(sizes["train"].sum() + sizes["val"].sum())
+    X, y = fb.make_synthetic_classification(total, dim=wl["dim"], num_classes=10, margin=6.0,
+                                            seed=fb.derive_seed(0, "pool"))
+    X = X.astype(np.float32)
+    out, off = {}, 0
+    for pop, key in ((fb.Population.TRAIN, "train"), (fb.Population.VAL, "val")):
+        users = {}
+        for i, n in enumerate(sizes[key]):
+            uid = f"{key}{i:05d}"
+            users[uid] = UserDataset(uid, X[off:off + n], y[off:off + n])
+            off += int(n)
+        out[pop] = FederatedDataset(users=users, population=pop)
+    return out
+
+
 def build(wl: dict):
     import paper_2404_06430_b200 as fb
 
+    if wl.get("ragged"):
+        return build_ragged(wl)
     ppu = wl["ppu"]
     ntr, nva = wl["users"] * ppu, wl["val_users"] * ppu
     X, y = fb.make_synthetic_classification(ntr + nva, dim=wl["dim"], num_classes=10, margin=6.0,
@@ -302,9 +340,10 @@ def gpu_arm(args, wl):
     C = wl["cohort"]
     per_rank = C / world
     val_iters = sum(1 for t in range(W, W + K) if t % wl["eval_every"] == 0)
-    steps = wl["epochs"] * -(-wl["ppu"] // wl["batch"])
-    train_samples = per_rank * wl["ppu"] * wl["epochs"] * K
-    fwd_samples = train_samples + per_rank * wl["ppu"] * K + val_iters * (wl["eval_cohort"] / world) * wl["ppu"]
+    ppu = wl["ppu"] or float(np.mean([u.num_points for u in ds[fb.Population.TRAIN].users.values()]))
+    steps = wl["epochs"] * -(-int(round(ppu)) // wl["batch"])  # (ragged: at the mean size; approximate)
+    train_samples = per_rank * ppu * wl["epochs"] * K
+    fwd_samples = train_samples + per_rank * ppu * K + val_iters * (wl["eval_cohort"] / world) * ppu
     D = make_model(wl).num_params
     counts = {"train": train_samples, "fwd": fwd_samples, "client_steps": per_rank * steps * K,
               "clients": per_rank * K, "D": (D + 3) & ~3, "iters": K}
@@ -335,7 +374,8 @@ def gpu_arm(args, wl):
             "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": wl["name"], "model": wl["model"], "cohort": C, "users": wl["users"],
-                       "points_per_user": wl["ppu"], "local_epochs": wl["epochs"], "batch": wl["batch"],
+                       "points_per_user": wl["ppu"] or f"ragged lognormal(3,1) in [1,500], mean {ppu:.1f}",
+                       "local_epochs": wl["epochs"], "batch": wl["batch"],
                        "local_steps_per_client": steps, "sigma": wl["sigma"], "clip_bound": wl["bound"],
                        "eval_every": wl["eval_every"], "parallelism": f"cohort-dp{world}",
                        "l2": "inputs larger than L2 (dataset 614 MB + per-iteration working set of GBs)"},

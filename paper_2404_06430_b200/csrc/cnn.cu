@@ -1285,6 +1285,11 @@ __global__ void __launch_bounds__(FW_THREADS, 1) conv2_fwd_tc_kernel(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = blockIdx.x;
   const int n0 = g * G;
+  {  // nothing to do (clients past their last local step, tail of the last chunk): leave before any setup
+    bool any = false;
+    for (int b = 0; b < G && n0 + b < N; ++b) any |= slot_row[n0 + b] >= 0;
+    if (!any) return;
+  }
   const int wg = shared_weights ? 0 : n0 / B;   // weight group (client) of this CTA
   const float* dc = delta ? delta + (int64_t)wg * ld : nullptr;
   if (threadIdx.x < C2) bias[threadIdx.x] = wt(theta, dc, O_B2 + threadIdx.x);
@@ -2144,6 +2149,11 @@ __global__ void __launch_bounds__(BX_THREADS, 1) conv2_bwd_x_tc_kernel(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * G;  // G slots of one client (G divides the batch B)
   const int g = n0 / B;           // the client: its weight image
+  {  // a client past its last local step: leave before any setup
+    bool any = false;
+    for (int b = 0; b < G; ++b) any |= slot_row[n0 + b] >= 0;
+    if (!any) return;
+  }
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < BX_STAGES; ++i) {
       tc::mbar_init(&full[i], 1);
@@ -2317,6 +2327,11 @@ __global__ void __launch_bounds__(C1F_THREADS, 2) conv1_fwd_tc_kernel(
   __shared__ int s_ns;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, t = threadIdx.x;
   const int n0 = blockIdx.x * G;
+  {  // no active slot (client past its last local step / tail chunk): leave before any setup
+    bool any = false;
+    for (int b = 0; b < G && n0 + b < N; ++b) any |= slot_row[n0 + b] >= 0;
+    if (!any) return;
+  }
   const float* dc = delta ? delta + (int64_t)(n0 / B) * ld : nullptr;
   const uint32_t sB0 = tc::smem_u32(sB), sA0 = tc::smem_u32(sA), simg = tc::smem_u32(img);
   // B: rows o (hi) and 32 + o (lo), k = 0..26 weights, 27 bias, 28..31 zero
