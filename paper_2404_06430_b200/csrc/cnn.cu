@@ -1467,6 +1467,7 @@ __global__ void __launch_bounds__(FW_THREADS, 1) conv2_fwd_tc_kernel(
   if (warp == 1) tc::tmem_dealloc<2 * FW_ACC>(tmem);
 }
 
+
 // ------------------------------------------------------- fc1 on tcgen05
 // Both fc1 contractions of the factored form run at theta_t, i.e. as plain
 // GEMMs over all slots of the step (kind::f16, 3-term split as above):
@@ -3022,8 +3023,8 @@ int forward(const float* X, const float* theta, const float* delta, int64_t ld, 
     if (st) return st;
     const int gt = delta ? B / client_split(N / B, B, 1) : 8;  // samples per CTA
     FB_LAUNCH("conv2_fwd_tc_kernel", s, conv2_fwd_tc_kernel<<<(N + gt - 1) / gt, FW_THREADS, FW_SMEM, s>>>(
-        mh, ml, w.wimg, w.wscale, delta ? 0 : 1, w.slot_row, N, gt, theta, delta, ld, B, w.a1scale, w.pooled,
-        w.code));
+          mh, ml, w.wimg, w.wscale, delta ? 0 : 1, w.slot_row, N, gt, theta, delta, ld, B, w.a1scale, w.pooled,
+          w.code));
   } else {
     FB_LAUNCH("conv2_fwd_pool_kernel", s, conv2_fwd_pool_kernel<<<N, 256, C2F_SMEM, s>>>(w.a1, nullptr, w.slot_row, theta, delta, ld, B, w.pooled, w.code));
   }
