@@ -291,6 +291,8 @@ class GpuSimulationEngine:
         self._pf: dict = {}
         self._pf_bufs: dict = {}
         self._pf_done: dict = {}
+        self._plans: dict = {}      # host plans computed ahead (key: population, seed, cohort size, epochs)
+        self._planned: set = set()
 
     @property
     def num_workers(self) -> int:
@@ -356,12 +358,9 @@ class GpuSimulationEngine:
             self._copy_stream.wait_event(prev)
         new = {}
         for k, ctx in enumerate(nxt):
-            dataset = self._datasets.get(ctx.population)
-            if dataset is None:
+            if ctx.population not in self._datasets:
                 continue
-            cohort, queue = plan_shard(dataset, ctx, self.rank, self.world_size, cohort_mode=self._cohort_mode,
-                                       poisson_rate=self._poisson_rate, base_policy=self._base_policy,
-                                       base_value=self._base_value)
+            queue = self._peek_plan(ctx)["queue"]
             if not queue:
                 continue
             pop = self.population(ctx.population)
@@ -398,6 +397,52 @@ class GpuSimulationEngine:
         self._pf[t] = new
 
     # ------------------------------------------------------------ internals
+    def _host_plan(self, ctx: CentralContext) -> dict:
+        """Cohort, this rank's LPT queue and (training) the minibatch permutations of
+        one context -- computed ahead by _plan_ahead when possible."""
+        epochs = ctx.local_params.num_epochs if ctx.do_training and ctx.local_params is not None else 0
+        key = (ctx.population, ctx.seed, ctx.cohort_size, epochs)
+        hp = self._plans.pop(key, None)
+        if hp is not None:
+            return hp
+        dataset = self._datasets[ctx.population]
+        cohort, queue = plan_shard(dataset, ctx, self.rank, self.world_size, cohort_mode=self._cohort_mode,
+                                   poisson_rate=self._poisson_rate, base_policy=self._base_policy,
+                                   base_value=self._base_value)
+        return {"cohort": cohort, "queue": queue}
+
+    def _peek_plan(self, ctx: CentralContext) -> dict:
+        """The context's host plan, computed now if needed and kept for _run_context."""
+        epochs = ctx.local_params.num_epochs if ctx.do_training and ctx.local_params is not None else 0
+        key = (ctx.population, ctx.seed, ctx.cohort_size, epochs)
+        if key not in self._plans:
+            self._plans[key] = self._host_plan(ctx)
+        return self._plans[key]
+
+    def _plan_ahead(self, algorithm, state, t: int) -> None:
+        """Prefetch the host work of iteration t: same seeds, same calls."""
+        if t in self._planned:
+            return
+        self._planned = {t}
+        try:
+            nxt = algorithm.get_next_central_contexts(state, t)
+        except Exception:  # noqa: BLE001 -- prediction only
+            return
+        for ctx in nxt:
+            if ctx.population not in self._datasets:
+                continue
+            hp = self._peek_plan(ctx)
+            epochs = ctx.local_params.num_epochs if ctx.do_training and ctx.local_params is not None else 0
+            if epochs and hp["queue"] and "perms" not in hp:
+                pop = self.population(ctx.population)
+                idx = np.fromiter((pop.index[u] for u in hp["queue"]), dtype=np.int64, count=len(hp["queue"]))
+                num_rows = pop.num_rows[idx]
+                perm_off = np.zeros(len(idx), dtype=np.int64)
+                if len(idx) > 1:
+                    perm_off[1:] = np.cumsum(num_rows[:-1].astype(np.int64) * epochs)
+                hp["perms"] = native_permutations(ctx.seed, hp["queue"], num_rows, epochs, perm_off,
+                                                  self._repr_cache)
+
     def _controls(self, state, D: int):
         """SCAFFOLD server control (flat fp32) and per-user control store,
         created on the device on first use (zero, as the reference)."""
@@ -414,9 +459,8 @@ class GpuSimulationEngine:
         dataset = self._datasets.get(pop_key)
         if dataset is None:
             raise EngineError(f"iteration {ctx.iteration}: no dataset for population {pop_key.value!r}")
-        cohort, queue = plan_shard(dataset, ctx, self.rank, self.world_size, cohort_mode=self._cohort_mode,
-                                   poisson_rate=self._poisson_rate, base_policy=self._base_policy,
-                                   base_value=self._base_value)
+        hp = self._host_plan(ctx)
+        cohort, queue = hp["cohort"], hp["queue"]
         if not cohort:
             return None, {}, cohort, None
 
@@ -448,7 +492,9 @@ class GpuSimulationEngine:
             perm_off = np.zeros(C, dtype=np.int64)
             if C > 1:
                 perm_off[1:] = np.cumsum(num_rows[:-1].astype(np.int64) * tp.num_epochs)
-            perm_flat = native_permutations(ctx.seed, queue, num_rows, tp.num_epochs, perm_off, self._repr_cache)
+            perm_flat = hp.get("perms")
+            if perm_flat is None or len(perm_flat) != int(num_rows.astype(np.int64).sum()) * tp.num_epochs:
+                perm_flat = native_permutations(ctx.seed, queue, num_rows, tp.num_epochs, perm_off, self._repr_cache)
             w = (num_rows.astype(np.float32) if plan.weighting == "datapoints"
                  else np.ones(C, dtype=np.float32))
             host += [perm_flat, perm_off, w]
@@ -537,6 +583,10 @@ class GpuSimulationEngine:
             else:
                 agg_flat.zero_()
 
+        # the host half of the next iteration (sampling, LPT shard, permutations) runs here,
+        # while the GPU works through this context, instead of between iterations
+        if train:
+            self._plan_ahead(algorithm, state, ctx.iteration + 1)
         # one D2H copy of the per-client results
         host_res = res[: 16 * Cp + 12 * Cp].to("cpu", non_blocking=False)
         self.io_bytes["d2h"] += int(host_res.numel())
