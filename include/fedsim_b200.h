@@ -134,7 +134,9 @@ int fb_local_sgd_mlp_f32(const float* theta_t, int dim, int hidden, int num_clas
  * batch_size <= 64) = factored: fc1 runs at theta_t plus a low-rank history
  * correction and each client's fc1 delta is written once at the end (same
  * arithmetic, see csrc/cnn.cu "fc1 in factored form").  The workspace must
- * be sized with the same hist_steps.                                      */
+ * be sized with the same hist_steps.  fc1_sumsq (nullable, [num_clients],
+ * factored form only) receives each client's sum of squares of its fc1
+ * weight delta block [O_F1, O_BF1), for fb_delta_norm_clip_ex_f32.          */
 int64_t fb_cnn_workspace_bytes(int max_slots, int max_clients, int hist_steps);
 /* Validation knob: 1 (default) = conv2 forward on tcgen05 (3xTF32, TMA,
  * TMEM); 0 = the FP32 CUDA-core kernels kept as an independent check.     */
@@ -149,7 +151,7 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
                          int epochs, int batch_size, int max_steps, float lr, float prox_mu,
                          float* delta_out, int64_t ld_delta, int32_t* nonfinite,
                          int max_slots, int hist_steps, void* workspace, int64_t workspace_bytes,
-                         void* stream);
+                         double* fc1_sumsq, void* stream);
 
 /* ------------------------------------------------------- data movement
  * Copy each cohort client's contiguous rows (num_rows[c] rows of row_bytes
@@ -181,6 +183,16 @@ int fb_delta_norm_clip_f32(const float* delta, int64_t ld_delta, int num_clients
                            const float* w, double bound,
                            double* norm, float* coef, int32_t* clipped, int32_t* nonfinite,
                            void* workspace, int64_t workspace_bytes, void* stream);
+/* K2 with the columns [skip_lo, skip_hi) excluded from the scan and their
+ * per-client sum of squares supplied in extra_sumsq[C] (nullable = 0): the
+ * CNN's factored fc1 block, whose squares fb_local_sgd_cnn_f32 sums while it
+ * materialises the block (same values, fp64, fixed order).  skip_hi must be
+ * a multiple of 4; workspace >= fb_clip_workspace_bytes(C, D) + 16 * C bytes. */
+int fb_delta_norm_clip_ex_f32(const float* delta, int64_t ld_delta, int num_clients, int64_t D,
+                              int64_t skip_lo, int64_t skip_hi, const double* extra_sumsq,
+                              const float* w, double bound, double* norm, float* coef,
+                              int32_t* clipped, int32_t* nonfinite, void* workspace,
+                              int64_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------------- a8 (kernel K3)
  * agg[i] (+)= sum_c coef[c] * delta[c*ld + i], fp64 accumulation per

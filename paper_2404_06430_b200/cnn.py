@@ -45,8 +45,14 @@ def eval_cohort(runner, theta, pop, row_start, num_rows, C, loss, correct, strea
                 ws.numel(), stream)
 
 
+# (row range of the fc1 weight block in the flat parameter vector: models.CNN.param_dims order)
+FC1_LO, FC1_HI = 19392, 19392 + 12544 * 128
+
+
 def local_sgd_cohort(runner, theta, pop, row_start, num_rows, perms, perm_off, C, tp, prox_mu, delta, nonfinite,
                      stream, h_num_rows):
+    """Returns the per-client fc1-block sum of squares (fp64 device [C]) when the
+    factored tcgen05 path produced it, else None (K2 then scans the whole row)."""
     B = tp.batch_size
     n = np.asarray(h_num_rows, dtype=np.int64)
     max_steps = int((tp.num_epochs * ((n + B - 1) // B)).max()) if len(n) else 0
@@ -54,7 +60,14 @@ def local_sgd_cohort(runner, theta, pop, row_start, num_rows, perms, perm_off, C
     hist = hist_steps(max_steps, B)
     nbytes = native.call("fb_cnn_workspace_bytes", slots, slots // B, hist)
     ws = runner.ws.get("cnn_ws", nbytes)
+    sq = None
+    if hist > 0 and max_steps > 0:
+        import torch
+
+        sq = runner.ws.tensor("cnn_fc1_sumsq", (max(C, 1),), torch.float64)
     native.call("fb_local_sgd_cnn_f32", native.ptr(theta), native.ptr(pop.X), native.ptr(pop.y),
                 native.ptr(row_start), native.ptr(num_rows), native.ptr(perms), native.ptr(perm_off), C,
                 tp.num_epochs, B, max_steps, float(tp.learning_rate), float(prox_mu), native.ptr(delta),
-                runner.ld, native.ptr(nonfinite), slots, hist, native.ptr(ws), ws.numel(), stream)
+                runner.ld, native.ptr(nonfinite), slots, hist, native.ptr(ws), ws.numel(),
+                native.ptr(sq) if sq is not None else None, stream)
+    return sq

@@ -81,6 +81,28 @@ __global__ void clip_finalize_kernel(const double* __restrict__ partial, int chu
   coef[c] = bad ? 0.0f : (float)(clip ? wc * (bound / nrm) : wc);
 }
 
+// K2 with a column range [skip_lo, skip_hi) whose sum of squares comes precomputed
+// (extra[c]; the CNN's factored fc1 block, summed while it is materialised)
+__global__ void clip_finalize_ex_kernel(const double* __restrict__ pa, int ca, const double* __restrict__ pb, int cb,
+                                        const double* __restrict__ extra, int C, const float* __restrict__ w,
+                                        double bound, double* __restrict__ norm, float* __restrict__ coef,
+                                        int32_t* __restrict__ clipped, int32_t* __restrict__ nonfinite) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  double s = 0.0;
+  for (int x = 0; x < ca; ++x) s += pa[(int64_t)c * ca + x];
+  if (extra) s += extra[c];
+  for (int x = 0; x < cb; ++x) s += pb[(int64_t)c * cb + x];
+  const double wc = (double)w[c];
+  const double nrm = fabs(wc) * sqrt(s);
+  const bool bad = !isfinite(nrm);
+  const bool clip = !bad && bound > 0.0 && nrm > bound;
+  norm[c] = nrm;
+  clipped[c] = clip;
+  nonfinite[c] = bad;
+  coef[c] = bad ? 0.0f : (float)(clip ? wc * (bound / nrm) : wc);
+}
+
 // K3: out[i] = sum_{c in [c0, c1)} coef[c] * delta[c, i]; four elements per
 // thread via 128-bit loads, fp64 accumulation, clients unrolled by 4 so each
 // thread keeps four independent loads in flight.
@@ -227,6 +249,39 @@ int fb_delta_norm_clip_f32(const float* delta, int64_t ld_delta, int num_clients
   FB_LAUNCH("clip_finalize_kernel", s, fb::clip_finalize_kernel<<<(num_clients + 127) / 128, 128, 0, s>>>(
       partial, chunks, num_clients, w, bound, norm, coef, clipped, nonfinite));
   return fb::launch_status("clip_finalize_kernel");
+}
+
+int fb_delta_norm_clip_ex_f32(const float* delta, int64_t ld_delta, int num_clients, int64_t D, int64_t skip_lo,
+                              int64_t skip_hi, const double* extra_sumsq, const float* w, double bound, double* norm,
+                              float* coef, int32_t* clipped, int32_t* nonfinite, void* workspace,
+                              int64_t workspace_bytes, void* stream) {
+  FB_REQUIRE(num_clients >= 0 && D >= 0 && ld_delta >= D, "delta_norm_clip_ex: bad shape");
+  FB_REQUIRE(0 <= skip_lo && skip_lo <= skip_hi && skip_hi <= D && (skip_hi & 3) == 0,
+             "delta_norm_clip_ex: need 0 <= skip_lo <= skip_hi <= D, skip_hi a multiple of 4");
+  FB_REQUIRE(num_clients <= 65535, "delta_norm_clip_ex: at most 65535 clients per call");
+  if (num_clients == 0) return FB_OK;
+  const int64_t Da = skip_lo, Db = D - skip_hi;
+  const int ca = Da > 0 ? fb::clip_chunks(num_clients, Da) : 0, cb = Db > 0 ? fb::clip_chunks(num_clients, Db) : 0;
+  FB_REQUIRE(workspace_bytes >= (int64_t)sizeof(double) * num_clients * (ca + cb),
+             "delta_norm_clip_ex: workspace %lld bytes too small", (long long)workspace_bytes);
+  double* pa = static_cast<double*>(workspace);
+  double* pb = pa + (int64_t)num_clients * ca;
+  cudaStream_t s = fb::as_stream(stream);
+  if (ca) {
+    const int64_t chunk = ((Da + ca - 1) / ca + 3) & ~int64_t(3);
+    FB_LAUNCH("row_sumsq_partial_kernel", s, fb::row_sumsq_partial_kernel<<<dim3(ca, num_clients), fb::kThreads, 0, s>>>(
+        delta, ld_delta, Da, ca, chunk, pa));
+  }
+  if (cb) {
+    const int64_t chunk = ((Db + cb - 1) / cb + 3) & ~int64_t(3);
+    FB_LAUNCH("row_sumsq_partial_kernel", s, fb::row_sumsq_partial_kernel<<<dim3(cb, num_clients), fb::kThreads, 0, s>>>(
+        delta + skip_hi, ld_delta, Db, cb, chunk, pb));
+  }
+  int st = fb::launch_status("row_sumsq_partial_kernel (ex)");
+  if (st) return st;
+  FB_LAUNCH("clip_finalize_kernel", s, fb::clip_finalize_ex_kernel<<<(num_clients + 127) / 128, 128, 0, s>>>(
+      pa, ca, pb, cb, extra_sumsq, num_clients, w, bound, norm, coef, clipped, nonfinite));
+  return fb::launch_status("clip_finalize_ex_kernel");
 }
 
 int64_t fb_weighted_sum_workspace_bytes(int num_clients, int64_t D) {

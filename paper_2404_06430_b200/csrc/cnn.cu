@@ -1843,7 +1843,7 @@ int hist_tensor_map(CUtensorMap* map, const __half* base, int N, int S, int B) {
 __global__ void __launch_bounds__(FMT_THREADS, 1) fc1_mat_tc_kernel(
     const __grid_constant__ CUtensorMap tm_hi, const __grid_constant__ CUtensorMap tm_lo, Hist hs,
     const float* __restrict__ pscale_hist, int N, int S, int B, float lr, float mu, float* __restrict__ delta,
-    int64_t ld) {
+    int64_t ld, double* __restrict__ sumsq_part) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sB = sm;                                  // [U hi blk0 | U hi blk1 | U lo blk0 | U lo blk1]
@@ -1855,6 +1855,7 @@ __global__ void __launch_bounds__(FMT_THREADS, 1) fc1_mat_tc_kernel(
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   __shared__ float red[32];
+  __shared__ double red_sq[FMT_EPI_WARPS];
   __shared__ int s_sc;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, t = threadIdx.x;
   const int nt = FMT_TILES / gridDim.y;  // tiles per CTA (gridDim.y divides 98)
@@ -1968,6 +1969,7 @@ __global__ void __launch_bounds__(FMT_THREADS, 1) fc1_mat_tc_kernel(
     // per-warp 32 x 33 transpose tile: lane = k row in TMEM; the stores go out as
     // 4 rows x 128 contiguous bytes per instruction instead of 32 rows x 16 B
     const uint32_t tw = tc::smem_u32(sA + FMT_STAGES * FMT_STAGE + 256) + (warp - 2) * 32 * 33 * 4;
+    double sq = 0.0;  // sum of squares of this thread's stored values (fixed order)
     for (int ti = 0; ti < nt; ++ti) {
       const int acc = ti & 1;
       tc::mbar_wait(&tfull[acc], (ti >> 1) & 1);
@@ -1986,8 +1988,11 @@ __global__ void __launch_bounds__(FMT_THREADS, 1) fc1_mat_tc_kernel(
           if (lane == 0) tc::mbar_arrive(&tempty[acc]);
         }
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-          tc::sts_f32(tw + (lane * 33 + j) * 4, (__uint_as_float(v0[j]) + __uint_as_float(v1[j])) * inv);
+        for (int j = 0; j < 32; ++j) {
+          const float z = (__uint_as_float(v0[j]) + __uint_as_float(v1[j])) * inv;
+          sq = fma((double)z, (double)z, sq);
+          tc::sts_f32(tw + (lane * 33 + j) * 4, z);
+        }
         __syncwarp();
         const int r = lane >> 3, c4 = (lane & 7) * 4;
 #pragma unroll
@@ -2003,11 +2008,49 @@ __global__ void __launch_bounds__(FMT_THREADS, 1) fc1_mat_tc_kernel(
         __syncwarp();
       }
     }
+    if (sumsq_part) {  // per-CTA partial: warp tree, then the 8 warps in order
+      sq = warp_sum(sq);
+      if (lane == 0) red_sq[warp - 2] = sq;
+    }
   }
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
+  if (sumsq_part && threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int i = 0; i < FMT_EPI_WARPS; ++i) tot += red_sq[i];
+    sumsq_part[(int64_t)c * gridDim.y + blockIdx.y] = tot;
+  }
   if (warp == 1) tc::tmem_dealloc<512>(tmem);
+}
+
+// the same sum by a pass over the materialised block (FP32 CUDA-core validation path)
+__global__ void __launch_bounds__(256) fc1_sumsq_scan_kernel(const float* __restrict__ delta, int64_t ld,
+                                                             const int32_t* __restrict__ nb0,
+                                                             double* __restrict__ out) {
+  __shared__ double red[32];
+  const int c = blockIdx.x;
+  double acc = 0.0;
+  if (nb0[c] > 0) {
+    const float4* p = reinterpret_cast<const float4*>(delta + (int64_t)c * ld + O_F1);
+    for (int i = threadIdx.x; i < FLAT * HID / 4; i += blockDim.x) {
+      const float4 v = p[i];
+      acc += (double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z + (double)v.w * v.w;
+    }
+  }
+  const double t = block_sum(acc, red);
+  if (threadIdx.x == 0) out[c] = t;
+}
+
+// each client's fc1 sum of squares: its fc1_mat CTAs' partials in order
+__global__ void fc1_sumsq_reduce_kernel(const double* __restrict__ part, int splits, int C,
+                                        const int32_t* __restrict__ nb0, double* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  double t = 0.0;
+  if (nb0[c] > 0)  // a client with no step kept its zeroed fc1 block (fc1_mat returned early)
+    for (int x = 0; x < splits; ++x) t += part[(int64_t)c * splits + x];
+  out[c] = t;
 }
 
 // ------------------------------------------------ conv2 backward-data (tcgen05)
@@ -3126,7 +3169,7 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
                          const int32_t* num_rows, const int32_t* perms, const int64_t* perm_off, int num_clients,
                          int epochs, int batch_size, int max_steps, float lr, float prox_mu, float* delta_out,
                          int64_t ld_delta, int32_t* nonfinite, int max_slots, int hist_steps, void* workspace,
-                         int64_t workspace_bytes, void* stream) {
+                         int64_t workspace_bytes, double* fc1_sumsq, void* stream) {
   FB_REQUIRE(num_clients >= 0 && epochs >= 0 && batch_size >= 1 && max_steps >= 0 && hist_steps >= 0,
              "local_sgd_cnn: bad arguments");
   FB_UNSUPPORTED(batch_size <= GMAX, "local_sgd_cnn: batch_size %d > %d", batch_size, GMAX);
@@ -3288,10 +3331,17 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
       if (st) return st;
       const int msplit = Cw * FMT_SPLIT >= g_num_sms ? FMT_SPLIT : 7;  // 2 CTAs per client, 7 for a small shard
       FB_LAUNCH("fc1_mat_tc_kernel", s, fc1_mat_tc_kernel<<<dim3(Cw, msplit), FMT_THREADS, FMT_SMEM, s>>>(
-                                            mh, ml, hs, w.pscale, N, max_steps, B, lr, prox_mu, dlt, ld_delta));
+                                            mh, ml, hs, w.pscale, N, max_steps, B, lr, prox_mu, dlt, ld_delta,
+                                            fc1_sumsq ? w.gram_part : nullptr));
+      if (fc1_sumsq)
+        FB_LAUNCH("fc1_sumsq_reduce_kernel", s, fc1_sumsq_reduce_kernel<<<(Cw + 127) / 128, 128, 0, s>>>(
+                                                    w.gram_part, msplit, Cw, w.client_nb, fc1_sumsq + c0));
     } else if (fact) {
       FB_LAUNCH("fc1_materialize_kernel", s, fc1_materialize_kernel<<<dim3(Cw, FLAT / FM_K), 256, FC1M_SMEM, s>>>(
                                                    hs, max_steps, B, lr, prox_mu, dlt, ld_delta));
+      if (fc1_sumsq)  // (validation path) the block's squares by a plain pass over it
+        FB_LAUNCH("fc1_sumsq_scan_kernel", s, fc1_sumsq_scan_kernel<<<Cw, 256, 0, s>>>(
+                                                  dlt, ld_delta, w.client_nb, fc1_sumsq + c0));
     }
   }
   return FB_OK;

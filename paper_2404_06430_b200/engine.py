@@ -194,7 +194,7 @@ class _ModelRunner:
 
     def local_sgd(self, theta, pop, row_start, num_rows, perms, perm_off, C, tp, prox_mu, delta, nonfinite, stream,
                   h_num_rows, control=None):
-        if self.kind == "cnn":
+        if self.kind == "cnn":  # returns the fc1-block sum of squares when the factored path made it
             if control is not None:
                 raise ValueError("GpuSimulationEngine: control variates are supported for the logistic / MLP "
                                  "models (the reference's own models), not the CNN")
@@ -555,8 +555,9 @@ class GpuSimulationEngine:
                     control = self.ws.tensor("scaffold_correction", (C, runner.ld), torch.float32)
                     native.call("fb_scaffold_correction_f32", native.ptr(server), native.ptr(store.matrix()),
                                 store.ld, native.ptr(d_rows), C, runner.D, native.ptr(control), runner.ld, stream)
-                runner.local_sgd(theta.flat, pop, d_row_start, d_num_rows, d_perms, d_perm_off, C, plan.train,
-                                 plan.prox_mu, delta, nonfinite, stream, num_rows, control=control)
+                fc1_sq = runner.local_sgd(theta.flat, pop, d_row_start, d_num_rows, d_perms, d_perm_off, C,
+                                          plan.train, plan.prox_mu, delta, nonfinite, stream, num_rows,
+                                          control=control)
                 payload, ldp = delta, runner.ld
                 if scaffold:
                     ldp = (Dp + 3) & ~3
@@ -569,12 +570,18 @@ class GpuSimulationEngine:
                     updates = ControlUpdates(queue, new_control)
                 coef = self.ws.tensor("coef", (Cp,), torch.float32)
                 bound = self._clip.current_bound if self._clip is not None else 0.0
-                wsb = native.call("fb_clip_workspace_bytes", C, Dp)
+                wsb = native.call("fb_clip_workspace_bytes", C, Dp) + 16 * C  # (+ the two-range K2 variant)
                 kws = self.ws.get("clip_ws", wsb)
                 nf2 = self.ws.tensor("nonfinite2", (Cp,), torch.int32)
-                native.call("fb_delta_norm_clip_f32", native.ptr(payload), ldp, C, Dp, native.ptr(d_w),
-                            float(bound), native.ptr(norm), native.ptr(coef), native.ptr(clipped),
-                            native.ptr(nf2), native.ptr(kws), kws.numel(), stream)
+                if fc1_sq is not None and not scaffold:  # fc1 block's squares came with its materialisation
+                    native.call("fb_delta_norm_clip_ex_f32", native.ptr(payload), ldp, C, Dp, cnn.FC1_LO,
+                                cnn.FC1_HI, native.ptr(fc1_sq), native.ptr(d_w), float(bound), native.ptr(norm),
+                                native.ptr(coef), native.ptr(clipped), native.ptr(nf2), native.ptr(kws), kws.numel(),
+                                stream)
+                else:
+                    native.call("fb_delta_norm_clip_f32", native.ptr(payload), ldp, C, Dp, native.ptr(d_w),
+                                float(bound), native.ptr(norm), native.ptr(coef), native.ptr(clipped),
+                                native.ptr(nf2), native.ptr(kws), kws.numel(), stream)
                 torch.bitwise_or(nonfinite[:C], nf2[:C], out=nonfinite[:C])
                 wsb = native.call("fb_weighted_sum_workspace_bytes", C, Dp)
                 sws = self.ws.get("sum_ws", wsb)

@@ -287,6 +287,39 @@ def test_scaffold_kernels():
     np.testing.assert_array_equal(tgt.cpu().numpy()[[4, 1], :D], newc.cpu().numpy()[:2, :D])
 
 
+def test_delta_norm_clip_ex_matches_full_scan():
+    """K2 with a skipped column range plus its precomputed squares == the full scan."""
+    rng = np.random.default_rng(11)
+    C, D, ld = 37, 5003, 5004
+    lo, hi = 1000, 4000
+    delta = rng.normal(size=(C, ld)).astype(np.float32)
+    w = rng.uniform(0.5, 2.0, size=C).astype(np.float32)
+    d = dev(delta)
+    extra = dev(np.square(delta[:, lo:hi].astype(np.float64)).sum(axis=1))
+    outs = []
+    for ex in (False, True):
+        norm = torch.zeros(C, dtype=torch.float64, device="cuda")
+        coef = torch.zeros(C, device="cuda")
+        clipped = torch.zeros(C, dtype=torch.int32, device="cuda")
+        bad = torch.zeros(C, dtype=torch.int32, device="cuda")
+        wsb = native.call("fb_clip_workspace_bytes", C, D) + 16 * C
+        ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+        if ex:
+            native.call("fb_delta_norm_clip_ex_f32", d.data_ptr(), ld, C, D, lo, hi, extra.data_ptr(), dev(w).data_ptr(),
+                        50.0, norm.data_ptr(), coef.data_ptr(), clipped.data_ptr(), bad.data_ptr(), ws.data_ptr(), wsb,
+                        S())
+        else:
+            native.call("fb_delta_norm_clip_f32", d.data_ptr(), ld, C, D, dev(w).data_ptr(), 50.0, norm.data_ptr(),
+                        coef.data_ptr(), clipped.data_ptr(), bad.data_ptr(), ws.data_ptr(), wsb, S())
+        outs.append((norm.cpu().numpy(), coef.cpu().numpy(), clipped.cpu().numpy()))
+    np.testing.assert_allclose(outs[1][0], outs[0][0], rtol=1e-13)
+    np.testing.assert_allclose(outs[1][1], outs[0][1], rtol=1e-6)
+    np.testing.assert_array_equal(outs[1][2], outs[0][2])
+    with pytest.raises(ValueError, match="skip"):
+        native.call("fb_delta_norm_clip_ex_f32", d.data_ptr(), ld, C, D, 10, 5, None, dev(w).data_ptr(), 1.0,
+                    None, None, None, None, None, 0, S())
+
+
 def test_bad_arguments_raise_value_error():
     with pytest.raises(ValueError, match="bad shape"):
         native.call("fb_delta_norm_clip_f32", None, 2, 1, 4, None, 1.0, None, None, None, None, None, 0, S())
