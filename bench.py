@@ -245,9 +245,9 @@ def kernel_work(wl: dict, counts: dict) -> dict:
         # per client-step: read the client's fc1 delta (fwd); read + write it (bwd)
         "fc1_fwd_kernel": ("hbm", steps * fc1_bytes + fwd * 12544 * 4, "bytes"),
         "fc1_bwd_kernel": ("hbm", steps * 2 * fc1_bytes + 2 * train * 12544 * 4, "bytes"),
-        "row_sumsq_partial_kernel": ("hbm", counts["clients"] * counts["D"] * 4, "bytes"),
+        "row_sumsq_partial_kernel": ("hbm", counts["clients"] * counts["D_dense"] * 4, "bytes"),
         "weighted_sum_kernel": ("hbm", counts["clients"] * counts["D"] * 4 + counts["D"] * 4 * counts["iters"], "bytes"),
-        "zero_delta_kernel": ("hbm", counts["clients"] * counts["D"] * 4, "bytes"),
+        "zero_delta_kernel": ("hbm", counts["clients"] * counts["D_dense"] * 4, "bytes"),
     }
 
 
@@ -345,8 +345,14 @@ def gpu_arm(args, wl):
     train_samples = per_rank * ppu * wl["epochs"] * K
     fwd_samples = train_samples + per_rank * ppu * K + val_iters * (wl["eval_cohort"] / world) * ppu
     D = make_model(wl).num_params
+    # columns the dense per-client passes (zero_delta, K2) touch: the factored CNN fc1
+    # block is written by fc1_mat_tc and its squares come out of that kernel
+    from paper_2404_06430_b200 import cnn as cnn_mod
+    dense_D = (D + 3) & ~3
+    if wl["model"] == "cnn" and cnn_mod.hist_steps(max(int(steps), 1), wl["batch"]):
+        dense_D -= cnn_mod.FC1_HI - cnn_mod.FC1_LO
     counts = {"train": train_samples, "fwd": fwd_samples, "client_steps": per_rank * steps * K,
-              "clients": per_rank * K, "D": (D + 3) & ~3, "iters": K}
+              "clients": per_rank * K, "D": (D + 3) & ~3, "D_dense": dense_D, "iters": K}
 
     # end-to-end: dataset in pinned host memory, cohort rows moved every iteration
     e2e = None

@@ -829,12 +829,14 @@ __global__ void eval_reduce_kernel(const double* __restrict__ slot_loss, const i
 }
 
 // zero every client's delta row except [skip0, skip1) (float4; ld, skip0, skip1 multiples of 4)
+// zero every client row except the columns [skip0, skip1) (the factored fc1 block, written whole
+// later): the grid strides over the kept quads only (skip0 / skip1 multiples of 4)
 __global__ void zero_delta_kernel(float* __restrict__ delta, int64_t ld, int C, int64_t skip0, int64_t skip1) {
-  const int64_t q = ld >> 2;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)C * q;
+  const int64_t q = ld >> 2, q0 = skip0 >> 2, qs = (skip1 - skip0) >> 2, kept = q - qs;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)C * kept;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t col = (i % q) << 2;
-    if (col < skip0 || col >= skip1) reinterpret_cast<float4*>(delta)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int64_t c = i / kept, j = i - c * kept;
+    reinterpret_cast<float4*>(delta)[c * q + (j < q0 ? j : j + qs)] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
 }
 
@@ -1868,7 +1870,11 @@ __global__ void __launch_bounds__(FMT_THREADS, 1) fc1_mat_tc_kernel(
   }
   __syncthreads();
   const int Sc = s_sc;
-  if (Sc == 0) return;  // the client never trained: its fc1 delta stays as zero_delta left it
+  if (Sc == 0) {  // the client never trained (no rows): its fc1 delta block is zero (zero_delta skipped it)
+    float4* z = reinterpret_cast<float4*>(delta + (int64_t)c * ld + O_F1 + (int64_t)t0 * FMT_TILE * HID);
+    for (int i = t; i < nt * FMT_TILE * HID / 4; i += FMT_THREADS) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    return;
+  }
   // U' rows j = s*B + b (zero when inactive); per-client power-of-two beta puts max |U'| at ~2^14
   float m = 0.f;
   for (int i = t; i < FC_RMAX * HID; i += FMT_THREADS) {
