@@ -29,6 +29,7 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include <cudaTypedefs.h>
 
@@ -86,6 +87,15 @@ __host__ __device__ __forceinline__ float hist_coef(float lr, float mu, int s, i
 __device__ __forceinline__ void split_f16(float x, __half& h, __half& l) {
   h = __float2half_rn(x);
   l = __float2half_rn(x - __half2float(h));
+}
+
+// the same split for a pair, packed (hi = (x0, x1), lo likewise): one cvt per pair
+__device__ __forceinline__ void split_f16x2(float x0, float x1, uint32_t& hw, uint32_t& lw) {
+  const __half2 h = __floats2half2_rn(x0, x1);
+  const float2 f = __half22float2(h);
+  const __half2 l = __floats2half2_rn(x0 - f.x, x1 - f.y);
+  hw = *reinterpret_cast<const uint32_t*>(&h);
+  lw = *reinterpret_cast<const uint32_t*>(&l);
 }
 
 // weight of the client owning `dc` (nullptr = shared theta_t)
@@ -907,23 +917,26 @@ __global__ void __launch_bounds__(128) fc1_gram_kernel(Hist hs, int B) {
   }
 }
 
-// Split-K Gram for the current step (replaces fc1_gram_kernel's smem tiles):
-// grid (C, GR_KS), warp w owns history rows j = 8w .. 8w+7, lane = k (strided
-// by 32 over the CTA's K range): per k the lane loads the step's nb <= GM new
-// rows and its 8 history rows straight from the (L2-resident) history with
-// coalesced 128-byte warp loads and does GM x 8 FMAs; each lane sums <= 98
-// products in fp32 (pooled >= 0: no cancellation), the warp tree-reduces and
-// the K splits are summed in fp64 in fixed order by fc1_gram_reduce_kernel.
-constexpr int GR_KS = 8;                       // max K splits per client (runtime: gridDim.y = 4 or 8)
+// Split-K Gram for the current step: grid (C, nks, 4), CTA = 2 warps, warp owns
+// history rows j = 16 z + 8 w .. +7, lane = 4 consecutive k (float4, strided by 128
+// over the CTA's K range): per k-quad the lane loads the step's nb <= GM new rows and
+// its 8 history rows (coalesced 512-byte warp loads, 18 in flight per warp) and does
+// GM x 8 x 4 FMAs; each lane sums <= 98 products per (b, j) in fp32 (pooled >= 0: no
+// cancellation), the warp tree-reduces and the K splits are summed in fp64 in fixed
+// order by fc1_gram_reduce_kernel.  Small CTAs so that the register file, not
+// exited warps, bounds residency (the old 8-warp CTA left 15% of warps active).
+constexpr int GR_KS = 14;                      // max K splits per client (runtime: gridDim.y = 7 or 14)
 constexpr int GR_JW = 8;                       // history rows per warp
-constexpr int GR_WARPS = FC_RMAX / GR_JW;      // 8
-static_assert(FLAT % (GR_KS * 32) == 0 && FLAT % (4 * 32) == 0, "gram K split");
+constexpr int GR_WARPS = 2;                    // warps per CTA
+constexpr int GR_Z = FC_RMAX / (GR_JW * GR_WARPS);  // 4 row groups
+static_assert(FLAT % (GR_KS * 128) == 0 && FLAT % (7 * 128) == 0, "gram K split");
 template <int GM>
 __global__ void __launch_bounds__(GR_WARPS * 32) fc1_gram_split_kernel(Hist hs, int B, double* __restrict__ part) {
   const int c = blockIdx.x, ks = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int s = hs.s, J = (s + 1) * B;
   const int nb = hs.nbh[s * hs.cstride + c];
-  if (nb == 0 || warp * GR_JW >= J) return;
+  const int j0 = (blockIdx.z * GR_WARPS + warp) * GR_JW;
+  if (nb == 0 || j0 >= J) return;
   // new rows are consecutive slots of step s; history rows as 32-bit element offsets
   // (the host checks S * N * FLAT < 2^31)
   const float* newp = hs.phist + s * hs.pstride + (int64_t)c * B * FLAT;
@@ -931,8 +944,8 @@ __global__ void __launch_bounds__(GR_WARPS * 32) fc1_gram_split_kernel(Hist hs, 
   int live = 0;
 #pragma unroll
   for (int i = 0; i < GR_JW; ++i) {
-    const int j = min(warp * GR_JW + i, J - 1), sp = j / B, bp = j - sp * B;
-    const bool act = warp * GR_JW + i < J && bp < hs.nbh[sp * hs.cstride + c];
+    const int j = min(j0 + i, J - 1), sp = j / B, bp = j - sp * B;
+    const bool act = j0 + i < J && bp < hs.nbh[sp * hs.cstride + c];
     live |= act << i;
     hoff[i] = (uint32_t)(sp * hs.pstride + (int64_t)(c * B + bp) * FLAT);
   }
@@ -944,16 +957,18 @@ __global__ void __launch_bounds__(GR_WARPS * 32) fc1_gram_split_kernel(Hist hs, 
   const int nks = gridDim.y;
   const int k0 = ks * (FLAT / nks), k1 = k0 + FLAT / nks;
 #pragma unroll 1
-  for (int k = k0 + lane; k < k1; k += 32) {
-    float x[GM], h[GR_JW];
+  for (int k = k0 + 4 * lane; k < k1; k += 128) {
+    float4 x[GM], h[GR_JW];
 #pragma unroll
-    for (int b = 0; b < GM; ++b) x[b] = b < nb ? __ldg(newp + b * FLAT + k) : 0.f;
+    for (int b = 0; b < GM; ++b)
+      x[b] = b < nb ? __ldg(reinterpret_cast<const float4*>(newp + b * FLAT + k)) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-    for (int i = 0; i < GR_JW; ++i) h[i] = __ldg(hs.phist + hoff[i] + k);
+    for (int i = 0; i < GR_JW; ++i) h[i] = __ldg(reinterpret_cast<const float4*>(hs.phist + hoff[i] + k));
 #pragma unroll
     for (int b = 0; b < GM; ++b)
 #pragma unroll
-      for (int i = 0; i < GR_JW; ++i) acc[b][i] = fmaf(x[b], h[i], acc[b][i]);
+      for (int i = 0; i < GR_JW; ++i)
+        acc[b][i] = fmaf(x[b].w, h[i].w, fmaf(x[b].z, h[i].z, fmaf(x[b].y, h[i].y, fmaf(x[b].x, h[i].x, acc[b][i]))));
   }
   double* out = part + (((int64_t)c * nks + ks) * GMAX) * FC_RMAX;
 #pragma unroll
@@ -961,7 +976,7 @@ __global__ void __launch_bounds__(GR_WARPS * 32) fc1_gram_split_kernel(Hist hs, 
 #pragma unroll
     for (int i = 0; i < GR_JW; ++i) {
       const float v = warp_sum(acc[b][i]);
-      if (lane == 0 && b < nb && ((live >> i) & 1)) out[b * FC_RMAX + warp * GR_JW + i] = (double)v;
+      if (lane == 0 && b < nb && ((live >> i) & 1)) out[b * FC_RMAX + j0 + i] = (double)v;
     }
 }
 
@@ -1568,15 +1583,11 @@ __global__ void __launch_bounds__(256) pooled_split_kernel(const float* __restri
   uint2* dl = reinterpret_cast<uint2*>(pl + (int64_t)n * FLAT);
   for (int i = threadIdx.x; i < FLAT / 4; i += blockDim.x) {
     const float4 v = src[i];
-    __half h0, l0, h1, l1, h2, l2, h3, l3;
-    split_f16(v.x * sc, h0, l0);
-    split_f16(v.y * sc, h1, l1);
-    split_f16(v.z * sc, h2, l2);
-    split_f16(v.w * sc, h3, l3);
-    const __half2 a = __halves2half2(h0, h1), b = __halves2half2(h2, h3);
-    const __half2 c = __halves2half2(l0, l1), d = __halves2half2(l2, l3);
-    dh[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b));
-    dl[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&c), *reinterpret_cast<const uint32_t*>(&d));
+    uint32_t a, b, c, d;
+    split_f16x2(v.x * sc, v.y * sc, a, c);
+    split_f16x2(v.z * sc, v.w * sc, b, d);
+    dh[i] = make_uint2(a, b);
+    dl[i] = make_uint2(c, d);
   }
 }
 
@@ -1755,34 +1766,69 @@ int tensor_map_2d_f16(CUtensorMap* map, const __half* base, int64_t inner, int64
   return FB_OK;
 }
 
-// dp -= sum_j a[b][j] p_j (history part of the factored backward); grid (C, KSPLIT), thread = 4 k
+// dp -= sum_j a[b][j] p_j (history part of the factored backward); grid (C, KSPLIT),
+// thread = 4 k.  The client's active history rows are compacted first so the row loop
+// has no branch and issues four independent float4 loads per trip.
 template <int GM>
 __global__ void __launch_bounds__(KCHUNK / 4) fc1_dp_hist_kernel(int B, const int32_t* __restrict__ client_nb, Hist hs,
                                                                  float* __restrict__ dp) {
-  __shared__ float ac[GMAX * FC_RMAX];
+  __shared__ float ac[FC_RMAX * GMAX];  // [compact row q][b]
+  __shared__ uint32_t roff[FC_RMAX];
+  __shared__ int jsrc[FC_RMAX];
+  __shared__ int s_nj;
   const int c = blockIdx.x, k0 = blockIdx.y * KCHUNK, t = threadIdx.x;
   const int nb = client_nb[c];
   const int J = hs.s * B;
   if (nb == 0 || J == 0) return;
-  for (int i = t; i < nb * J; i += blockDim.x) {
-    const int b = i / J, jj = i - b * J;
-    ac[b * FC_RMAX + jj] = hs.acoef[((int64_t)c * GMAX + b) * FC_RMAX + jj];
+  const int n0 = c * B;
+  if (t == 0) {
+    int q = 0;
+    for (int jj = 0; jj < J; ++jj) {
+      const int sp = jj / B, bp = jj - sp * B;
+      if (bp < hs.nbh[sp * hs.cstride + c]) {
+        jsrc[q] = jj;
+        roff[q] = (uint32_t)(sp * hs.pstride + (int64_t)(n0 + bp) * FLAT + k0);  // host checks S*N*FLAT < 2^31
+        ++q;
+      }
+    }
+    s_nj = q;
   }
   __syncthreads();
-  const int n0 = c * B;
+  const int nj = s_nj;
+  for (int i = t; i < nj * GM; i += blockDim.x) {
+    const int q = i / GM, b = i - q * GM;
+    ac[i] = b < nb ? hs.acoef[((int64_t)c * GMAX + b) * FC_RMAX + jsrc[q]] : 0.f;
+  }
+  __syncthreads();
   float4 acc[GM];
 #pragma unroll
   for (int b = 0; b < GM; ++b)
     acc[b] = b < nb ? reinterpret_cast<const float4*>(dp + (int64_t)(n0 + b) * FLAT + k0)[t]
                     : make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int jj = 0; jj < J; ++jj) {
-    const int sp = jj / B, bp = jj - sp * B;
-    if (bp >= hs.nbh[sp * hs.cstride + c]) continue;
-    const float4 p =
-        __ldg(reinterpret_cast<const float4*>(hs.phist + sp * hs.pstride + (int64_t)(n0 + bp) * FLAT + k0) + t);
+  const float4* ph = reinterpret_cast<const float4*>(hs.phist);
+  int q = 0;
+#pragma unroll 1
+  for (; q + 4 <= nj; q += 4) {
+    float4 p[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) p[u] = __ldg(ph + (roff[q + u] >> 2) + t);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int b = 0; b < GM; ++b) {
+        const float a = ac[(q + u) * GM + b];
+        acc[b].x = fmaf(-a, p[u].x, acc[b].x);
+        acc[b].y = fmaf(-a, p[u].y, acc[b].y);
+        acc[b].z = fmaf(-a, p[u].z, acc[b].z);
+        acc[b].w = fmaf(-a, p[u].w, acc[b].w);
+      }
+  }
+#pragma unroll 1
+  for (; q < nj; ++q) {
+    const float4 p = __ldg(ph + (roff[q] >> 2) + t);
 #pragma unroll
     for (int b = 0; b < GM; ++b) {
-      const float a = ac[b * FC_RMAX + jj];
+      const float a = ac[q * GM + b];
       acc[b].x = fmaf(-a, p.x, acc[b].x);
       acc[b].y = fmaf(-a, p.y, acc[b].y);
       acc[b].z = fmaf(-a, p.z, acc[b].z);
@@ -2160,13 +2206,8 @@ __global__ void __launch_bounds__(256) dz2_build_kernel(const float* __restrict_
     uint32_t hv[4], lv[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      __half h0, l0, h1, l1;
       const int i0 = (o0 + 2 * e) * DZB_LD + pp, i1 = i0 + DZB_LD;
-      split_f16((cd[i0] == sub ? g[i0] : 0.f) * sc, h0, l0);
-      split_f16((cd[i1] == sub ? g[i1] : 0.f) * sc, h1, l1);
-      const __half2 hh = __halves2half2(h0, h1), ll = __halves2half2(l0, l1);
-      hv[e] = *reinterpret_cast<const uint32_t*>(&hh);
-      lv[e] = *reinterpret_cast<const uint32_t*>(&ll);
+      split_f16x2((cd[i0] == sub ? g[i0] : 0.f) * sc, (cd[i1] == sub ? g[i1] : 0.f) * sc, hv[e], lv[e]);
     }
     reinterpret_cast<uint4*>(fh)[t] = make_uint4(hv[0], hv[1], hv[2], hv[3]);
     reinterpret_cast<uint4*>(fl)[t] = make_uint4(lv[0], lv[1], lv[2], lv[3]);
@@ -2427,12 +2468,6 @@ __global__ void __launch_bounds__(C1F_THREADS, 2) conv1_fwd_tc_kernel(
   if (t == 0) fetch(0);
   // im2col job: position row pl, k range [16*kh, 16*kh + 16)
   const int pl = t & (C1F_TILE - 1), kh = t >> 7;
-  uint32_t koff[16];
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const int k = min(16 * kh + j, 26), ci = k / 9, ky = (k % 9) / 3, kx = k % 3;
-    koff[j] = 4 * (ci * S0 * S0 + ky * S0 + kx);
-  }
   // epilogue job: TMEM lane quadrant q = warp % 4, channel half chh = warp / 4
   const int q = warp & 3, chh = warp >> 2;
   auto epilogue = [&](int i) {
@@ -2453,12 +2488,7 @@ __global__ void __launch_bounds__(C1F_THREADS, 2) conv1_fwd_tc_kernel(
       for (int e = 0; e < 8; ++e) {
         const float z0 = fmaxf(__uint_as_float(v0[2 * e]) + __uint_as_float(v1[2 * e]), 0.f) * sc;
         const float z1 = fmaxf(__uint_as_float(v0[2 * e + 1]) + __uint_as_float(v1[2 * e + 1]), 0.f) * sc;
-        __half h0, l0, h1, l1;
-        split_f16(z0, h0, l0);
-        split_f16(z1, h1, l1);
-        const __half2 hh = __halves2half2(h0, h1), ll = __halves2half2(l0, l1);
-        hw[e] = *reinterpret_cast<const uint32_t*>(&hh);
-        lw[e] = *reinterpret_cast<const uint32_t*>(&ll);
+        split_f16x2(z0, z1, hw[e], lw[e]);
       }
       const int64_t off = (int64_t)n * A1 + (int64_t)p * C1 + chh * 16;
       uint4* dh = reinterpret_cast<uint4*>(a1fh + off);
@@ -2494,26 +2524,36 @@ __global__ void __launch_bounds__(C1F_THREADS, 2) conv1_fwd_tc_kernel(
     }
     if (i >= 2) tc::mbar_wait(&done[buf], ((i - 2) >> 1) & 1);  // tile i-2's MMAs are done with this A stage
     {
-      const int p = tile * C1F_TILE + pl, y = p / S1, x = p - y * S1;
-      const bool valid = p < S1 * S1;
+      // rows past the 900 positions (last tile) read position 899: their outputs are dropped
+      const int p = min(tile * C1F_TILE + pl, S1 * S1 - 1), y = p / S1, x = p - y * S1;
       const uint32_t ib = im + 4 * (y * S0 + x);
       const uint32_t ah = sA0 + buf * C1F_STAGE, al = ah + C1F_A;
+      auto stage = [&](auto khc) {  // khc: compile-time k half (warp-uniform)
+        constexpr int KH = decltype(khc)::value;
 #pragma unroll
-      for (int c4 = 0; c4 < 4; ++c4) {
-        float hv[4], lv[4];
+        for (int c4 = 0; c4 < 4; ++c4) {
+          float hv[4], lv[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int jj = 4 * c4 + e, k = 16 * kh + jj;
-          float v = 0.f;
-          if (valid) v = k < 27 ? tc::lds_f32(ib + koff[jj]) : (k == 27 ? 1.f : 0.f);
-          tc::split_tf32(v, hv[e], lv[e]);
+          for (int e = 0; e < 4; ++e) {
+            const int k = 16 * KH + 4 * c4 + e;
+            if (k < 27) {
+              tc::split_tf32(tc::lds_f32(ib + 4 * ((k / 9) * S0 * S0 + ((k % 9) / 3) * S0 + k % 3)), hv[e], lv[e]);
+            } else {
+              hv[e] = k == 27 ? 1.f : 0.f;
+              lv[e] = 0.f;
+            }
+          }
+          const uint32_t off = tc::sw128_offset(pl, 16 * KH + 4 * c4);
+          asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(ah + off), "f"(hv[0]), "f"(hv[1]),
+                       "f"(hv[2]), "f"(hv[3]) : "memory");
+          asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(al + off), "f"(lv[0]), "f"(lv[1]),
+                       "f"(lv[2]), "f"(lv[3]) : "memory");
         }
-        const uint32_t off = tc::sw128_offset(pl, 16 * kh + 4 * c4);
-        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(ah + off), "f"(hv[0]), "f"(hv[1]), "f"(hv[2]),
-                     "f"(hv[3]) : "memory");
-        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(al + off), "f"(lv[0]), "f"(lv[1]), "f"(lv[2]),
-                     "f"(lv[3]) : "memory");
-      }
+      };
+      if (kh == 0)
+        stage(std::integral_constant<int, 0>{});
+      else
+        stage(std::integral_constant<int, 1>{});
     }
     tc::fence_proxy_async();
     tc::tc_fence_before();
@@ -3239,15 +3279,16 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
       if (st) return st;
       if (fact) {
         FB_REQUIRE((int64_t)max_steps * N * FLAT < (1LL << 31), "local_sgd_cnn: factored-fc1 history exceeds 2^31 elements");
-        const int gks = Cw * 4 >= 2 * g_num_sms ? 4 : 8;  // more K splits for a small shard
+        const int gks = Cw * 7 >= 4 * g_num_sms ? 7 : 14;  // more K splits for a small shard
+        const dim3 ggrid(Cw, gks, std::min(GR_Z, (int)((step + 1) * B + GR_JW * GR_WARPS - 1) / (GR_JW * GR_WARPS)));
         if (B <= 8)
-          FB_LAUNCH("fc1_gram_split_kernel", s, fc1_gram_split_kernel<8><<<dim3(Cw, gks), GR_WARPS * 32, 0, s>>>(
+          FB_LAUNCH("fc1_gram_split_kernel", s, fc1_gram_split_kernel<8><<<ggrid, GR_WARPS * 32, 0, s>>>(
                                                     hs, B, w.gram_part));
         else if (B <= 10)
-          FB_LAUNCH("fc1_gram_split_kernel", s, fc1_gram_split_kernel<10><<<dim3(Cw, gks), GR_WARPS * 32, 0, s>>>(
+          FB_LAUNCH("fc1_gram_split_kernel", s, fc1_gram_split_kernel<10><<<ggrid, GR_WARPS * 32, 0, s>>>(
                                                     hs, B, w.gram_part));
         else
-          FB_LAUNCH("fc1_gram_split_kernel", s, fc1_gram_split_kernel<GMAX><<<dim3(Cw, gks), GR_WARPS * 32, 0, s>>>(
+          FB_LAUNCH("fc1_gram_split_kernel", s, fc1_gram_split_kernel<GMAX><<<ggrid, GR_WARPS * 32, 0, s>>>(
                                                     hs, B, w.gram_part));
         FB_LAUNCH("fc1_gram_reduce_kernel", s, fc1_gram_reduce_kernel<<<Cw, 256, 0, s>>>(hs, B, gks, w.gram_part));
       }

@@ -343,9 +343,10 @@ __device__ __forceinline__ void fence_proxy_async() {
 // fp32 -> (hi, lo) split for 3xTF32: hi = rna(x) (a tf32 value), lo = x - hi
 // (exact in fp32; the tensor core reads its top tf32 bits)
 __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
-  uint32_t h;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
-  hi = __uint_as_float(h);
+  // rna to 10 mantissa bits as integer add + mask (2 instructions; cvt.rna.tf32 adds an
+  // inf test): equal to cvt.rna.tf32.f32 for every finite x; a non-finite x leaves a
+  // non-finite hi or lo, so the product stays non-finite
+  hi = __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
 #ifdef FB_SPLIT_RNA_LO
   uint32_t l;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(x - hi));
