@@ -69,18 +69,24 @@ def client_permutations(ctx_seed: int, user_ids: Sequence[str], sizes: Sequence[
     return out
 
 
-def plan_shard(dataset, ctx: CentralContext, rank: int, world_size: int, *, cohort_mode: str = "fixed",
-               poisson_rate: float | None = None, base_policy: str = "median", base_value: float = 0.0):
-    """Host half of a context on one rank: the cohort (identical on every
-    rank: same seed, fedsim/feddata/sampling.py:12-40) and this rank's LPT
-    queue over ``world_size`` workers (fedsim/engine/scheduling.py:34-78) --
-    the reference's worker assignment with num_workers = world_size."""
+def plan_queues(dataset, ctx: CentralContext, world_size: int, *, cohort_mode: str = "fixed",
+                poisson_rate: float | None = None, base_policy: str = "median", base_value: float = 0.0):
+    """The cohort (identical on every rank: same seed, fedsim/feddata/sampling.py:12-40)
+    and every rank's LPT queue over ``world_size`` workers
+    (fedsim/engine/scheduling.py:34-78) -- the reference's worker assignment with
+    num_workers = world_size."""
     cohort = sample_cohort(dataset, ctx.cohort_size, ctx.seed, mode=cohort_mode, poisson_rate=poisson_rate)
     if not cohort:
-        return cohort, ()
+        return cohort, tuple(() for _ in range(world_size))
     weights = {uid: float(dataset.users[uid].weight) for uid in cohort}
     base = compute_base_weight(list(weights.values()), base_policy, base_value)
-    return cohort, schedule_users(weights, world_size, base).queues[rank]
+    return cohort, tuple(schedule_users(weights, world_size, base).queues)
+
+
+def plan_shard(dataset, ctx: CentralContext, rank: int, world_size: int, **kw):
+    """Host half of a context on one rank: the cohort and this rank's queue (:func:`plan_queues`)."""
+    cohort, queues = plan_queues(dataset, ctx, world_size, **kw)
+    return cohort, queues[rank]
 
 
 # thread blocks of the prefetch copy (each keeps 4 x 16 B x 256 threads in flight over PCIe)
@@ -397,6 +403,24 @@ class GpuSimulationEngine:
         self._pf[t] = new
 
     # ------------------------------------------------------------ internals
+    def _gather_controls(self, queues, local, ld: int):
+        """SCAFFOLD across ranks: all-gather the new per-user controls of every
+        rank's shard (padded to the longest queue) so each rank's replicated
+        control store sees the whole cohort's updates, in rank-then-queue order
+        (the reference merges its workers' user_updates,
+        fedsim/engine/runtime.py:95-104)."""
+        torch = _torch()
+        cmax = max(max((len(q) for q in queues), default=0), 1)
+        buf = torch.zeros((cmax, ld), dtype=torch.float32, device=self.device)
+        if local is not None and len(local):
+            buf[: len(local)].copy_(local.matrix[: len(local)])
+        outs = [torch.empty_like(buf) for _ in range(self.world_size)]
+        torch.distributed.all_gather(outs, buf, group=self.group)
+        uids = [u for q in queues for u in q]
+        if not uids:
+            return None
+        return ControlUpdates(uids, torch.cat([o[: len(q)] for o, q in zip(outs, queues)]))
+
     def _host_plan(self, ctx: CentralContext) -> dict:
         """Cohort, this rank's LPT queue and (training) the minibatch permutations of
         one context -- computed ahead by _plan_ahead when possible."""
@@ -406,10 +430,10 @@ class GpuSimulationEngine:
         if hp is not None:
             return hp
         dataset = self._datasets[ctx.population]
-        cohort, queue = plan_shard(dataset, ctx, self.rank, self.world_size, cohort_mode=self._cohort_mode,
-                                   poisson_rate=self._poisson_rate, base_policy=self._base_policy,
-                                   base_value=self._base_value)
-        return {"cohort": cohort, "queue": queue}
+        cohort, queues = plan_queues(dataset, ctx, self.world_size, cohort_mode=self._cohort_mode,
+                                     poisson_rate=self._poisson_rate, base_policy=self._base_policy,
+                                     base_value=self._base_value)
+        return {"cohort": cohort, "queue": queues[self.rank], "queues": queues}
 
     def _peek_plan(self, ctx: CentralContext) -> dict:
         """The context's host plan, computed now if needed and kept for _run_context."""
@@ -467,9 +491,6 @@ class GpuSimulationEngine:
         plan = algorithm.cohort_plan(state, ctx)
         runner = self._runner(plan.model)
         scaffold = bool(getattr(plan, "scaffold", False)) and plan.train is not None
-        if scaffold and self.world_size > 1:
-            raise ValueError("GpuSimulationEngine: Scaffold runs single-rank (the per-user control store is not "
-                             "sharded across ranks)")
         pop = self.population(pop_key)
         if pop.dim != plan.model.input_dim:
             raise ValueError(f"dataset dim {pop.dim} != model input dim {plan.model.input_dim}")
@@ -499,14 +520,18 @@ class GpuSimulationEngine:
                  else np.ones(C, dtype=np.float32))
             host += [perm_flat, perm_off, w]
             if scaffold:  # control update scale 1 / (steps * lr) (fedsim/algorithms/scaffold.py:46-70)
+                # checked over every rank's queue (in rank order) so all ranks raise together
+                for q in hp.get("queues", (queue,)):
+                    n_q = np.fromiter((dataset.users[u].num_points for u in q), dtype=np.int64, count=len(q))
+                    steps_q = tp.num_epochs * (-(-n_q // tp.batch_size))
+                    bad = np.flatnonzero(steps_q.astype(np.float64) * float(tp.learning_rate) == 0.0)
+                    if len(bad):
+                        raise EngineError(
+                            f"iteration {ctx.iteration}, population {pop_key.value!r}, user {q[int(bad[0])]!r}: "
+                            f"control update divides by steps * learning_rate; got {int(steps_q[bad[0]])} steps "
+                            f"at lr {tp.learning_rate}")
                 steps = tp.num_epochs * (-(-num_rows.astype(np.int64) // tp.batch_size))
                 denom = steps.astype(np.float64) * float(tp.learning_rate)
-                if C and (denom == 0.0).any():
-                    c0 = int(np.flatnonzero(denom == 0.0)[0])
-                    raise EngineError(
-                        f"iteration {ctx.iteration}, population {pop_key.value!r}, user {queue[c0]!r}: "
-                        f"control update divides by steps * learning_rate; got {int(steps[c0])} steps at lr "
-                        f"{tp.learning_rate}")
                 ctrl_scale = (1.0 / denom).astype(np.float32) if C else np.zeros(0, dtype=np.float32)
         if gathered:
             host.append(src_start)
@@ -589,6 +614,8 @@ class GpuSimulationEngine:
                             native.ptr(agg_flat), 0, native.ptr(sws), sws.numel(), stream)
             else:
                 agg_flat.zero_()
+            if scaffold and self.world_size > 1:  # every rank's store takes the whole cohort's controls
+                updates = self._gather_controls(hp["queues"], updates, runner.ld)
 
         # the host half of the next iteration (sampling, LPT shard, permutations) runs here,
         # while the GPU works through this context, instead of between iterations
