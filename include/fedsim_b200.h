@@ -151,7 +151,8 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
                          int epochs, int batch_size, int max_steps, float lr, float prox_mu,
                          float* delta_out, int64_t ld_delta, int32_t* nonfinite,
                          int max_slots, int hist_steps, void* workspace, int64_t workspace_bytes,
-                         double* fc1_sumsq, void* stream);
+                         double* fc1_sumsq, const float* control /* nullable [C, ld_control]: c - c_i */,
+                         int64_t ld_control, void* stream);
 
 /* ------------------------------------------------------- data movement
  * Copy each cohort client's contiguous rows (num_rows[c] rows of row_bytes

@@ -50,14 +50,16 @@ FC1_LO, FC1_HI = 19392, 19392 + 12544 * 128
 
 
 def local_sgd_cohort(runner, theta, pop, row_start, num_rows, perms, perm_off, C, tp, prox_mu, delta, nonfinite,
-                     stream, h_num_rows):
+                     stream, h_num_rows, control=None):
     """Returns the per-client fc1-block sum of squares (fp64 device [C]) when the
-    factored tcgen05 path produced it, else None (K2 then scans the whole row)."""
+    factored tcgen05 path produced it, else None (K2 then scans the whole row).
+    ``control`` ([C, ld] device, c - c_i per client; SCAFFOLD) selects the dense
+    fc1 form: a per-client dense control term has no low-rank history."""
     B = tp.batch_size
     n = np.asarray(h_num_rows, dtype=np.int64)
     max_steps = int((tp.num_epochs * ((n + B - 1) // B)).max()) if len(n) else 0
     slots = _slots(C, B)
-    hist = hist_steps(max_steps, B)
+    hist = hist_steps(max_steps, B) if control is None else 0
     nbytes = native.call("fb_cnn_workspace_bytes", slots, slots // B, hist)
     ws = runner.ws.get("cnn_ws", nbytes)
     sq = None
@@ -69,5 +71,7 @@ def local_sgd_cohort(runner, theta, pop, row_start, num_rows, perms, perm_off, C
                 native.ptr(row_start), native.ptr(num_rows), native.ptr(perms), native.ptr(perm_off), C,
                 tp.num_epochs, B, max_steps, float(tp.learning_rate), float(prox_mu), native.ptr(delta),
                 runner.ld, native.ptr(nonfinite), slots, hist, native.ptr(ws), ws.numel(),
-                native.ptr(sq) if sq is not None else None, stream)
+                native.ptr(sq) if sq is not None else None,
+                native.ptr(control) if control is not None else None,
+                control.stride(0) if control is not None else 0, stream)
     return sq

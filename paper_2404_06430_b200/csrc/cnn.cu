@@ -3211,13 +3211,39 @@ int fb_eval_cnn_f32(const float* theta, const float* X, const int32_t* y, const 
   return FB_OK;
 }
 
+// SCAFFOLD control term of one local step (fedsim/models/kernels.py:66-67,117-120 with
+// c = c - c_i, fedsim/algorithms/scaffold.py:46-57): delta_c += lr * corr_c for every
+// client that took this step (nb > 0); float4 over the row, tail past D masked
+__global__ void control_step_kernel(float* __restrict__ delta, int64_t ld, const float* __restrict__ corr,
+                                    int64_t ldc, int C, const int32_t* __restrict__ nb, float lr) {
+  const int64_t q = (D + 3) / 4;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)C * q;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i / q);
+    const int64_t j = i - (int64_t)c * q;
+    if (nb[c] == 0) continue;
+    float4 d = reinterpret_cast<float4*>(delta + (int64_t)c * ld)[j];
+    const float4 g = __ldg(reinterpret_cast<const float4*>(corr + (int64_t)c * ldc) + j);
+    const int64_t e = 4 * j;
+    d.x = fmaf(lr, g.x, d.x);
+    if (e + 1 < D) d.y = fmaf(lr, g.y, d.y);
+    if (e + 2 < D) d.z = fmaf(lr, g.z, d.z);
+    if (e + 3 < D) d.w = fmaf(lr, g.w, d.w);
+    reinterpret_cast<float4*>(delta + (int64_t)c * ld)[j] = d;
+  }
+}
+
 int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y, const int64_t* row_start,
                          const int32_t* num_rows, const int32_t* perms, const int64_t* perm_off, int num_clients,
                          int epochs, int batch_size, int max_steps, float lr, float prox_mu, float* delta_out,
                          int64_t ld_delta, int32_t* nonfinite, int max_slots, int hist_steps, void* workspace,
-                         int64_t workspace_bytes, double* fc1_sumsq, void* stream) {
+                         int64_t workspace_bytes, double* fc1_sumsq, const float* control, int64_t ld_control,
+                         void* stream) {
   FB_REQUIRE(num_clients >= 0 && epochs >= 0 && batch_size >= 1 && max_steps >= 0 && hist_steps >= 0,
              "local_sgd_cnn: bad arguments");
+  FB_REQUIRE(!control || (hist_steps == 0 && ld_control >= D && (ld_control & 3) == 0),
+             "local_sgd_cnn: control variates need the dense fc1 form (hist_steps 0) and ld_control >= D, "
+             "a multiple of 4");
   FB_UNSUPPORTED(batch_size <= GMAX, "local_sgd_cnn: batch_size %d > %d", batch_size, GMAX);
   FB_REQUIRE(ld_delta >= D && (ld_delta & 3) == 0, "local_sgd_cnn: ld_delta must be >= D and a multiple of 4");
   FB_REQUIRE(max_slots >= batch_size, "local_sgd_cnn: max_slots < batch_size");
@@ -3368,6 +3394,10 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
       else
         FB_LAUNCH("conv1_bwd_w_kernel", s, conv1_bwd_w_kernel<<<Cw, C1B_WARPS * 32, 0, s>>>(
                                                 X, ws.slot_row, ws.dz1, B, ws.client_nb, dlt, ld_delta, sp));
+      if (control)  // SCAFFOLD: theta -= lr * (g + c - c_i), the gradient part applied above
+        FB_LAUNCH("control_step_kernel", s, control_step_kernel<<<g_num_sms * 8, 256, 0, s>>>(
+                                                dlt, ld_delta, control + (int64_t)c0 * ld_control, ld_control, Cw,
+                                                ws.client_nb, lr));
       st = fb::launch_status("local_sgd_cnn step");
       if (st) return st;
     }

@@ -201,11 +201,8 @@ class _ModelRunner:
     def local_sgd(self, theta, pop, row_start, num_rows, perms, perm_off, C, tp, prox_mu, delta, nonfinite, stream,
                   h_num_rows, control=None):
         if self.kind == "cnn":  # returns the fc1-block sum of squares when the factored path made it
-            if control is not None:
-                raise ValueError("GpuSimulationEngine: control variates are supported for the logistic / MLP "
-                                 "models (the reference's own models), not the CNN")
             return cnn.local_sgd_cohort(self, theta, pop, row_start, num_rows, perms, perm_off, C, tp,
-                                        prox_mu, delta, nonfinite, stream, h_num_rows)
+                                        prox_mu, delta, nonfinite, stream, h_num_rows, control=control)
         fn = f"fb_local_sgd_{self.kind}_f32"
         native.call(fn, native.ptr(theta), *self.dims, native.ptr(pop.X), native.ptr(pop.y),
                     native.ptr(row_start), native.ptr(num_rows), native.ptr(perms), native.ptr(perm_off), C,

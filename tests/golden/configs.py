@@ -34,6 +34,7 @@ _VARIANTS = {
     "logistic_scaffold": ("logistic_dp", dict(algorithm=dict(kind="scaffold", num_train_users=40), bound=None,
                                               sigma=0.0, weighting="uniform", epochs=2, cohort=20, iterations=4,
                                               workers=1)),
+    "cnn_scaffold": ("cnn_dp", dict(algorithm=dict(kind="scaffold", num_train_users=8), iterations=3)),
 }
 for _name, (_base, _over) in _VARIANTS.items():
     CONFIGS[_name] = {**CONFIGS[_base], **_over}

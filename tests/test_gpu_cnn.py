@@ -81,9 +81,11 @@ def test_cnn_local_sgd_and_eval_match_oracle(sizes, E, B, mu, factored, monkeypa
     assert len(flips) <= max(1, C // 4), f"too many decision flips: {flips}"
 
 
-def test_cnn_engine_matches_reference_fixture(golden):
-    g = golden("cnn_dp")
-    cfg = CONFIGS["cnn_dp"]
+@pytest.mark.parametrize("name", ["cnn_dp", "cnn_scaffold"])
+def test_cnn_engine_matches_reference_fixture(name, golden):
+    """cnn_scaffold: SCAFFOLD on the CNN (dense fc1 form + per-step control term)."""
+    g = golden(name)
+    cfg = CONFIGS[name]
     ds = product_datasets(cfg)
     alg, post = product_run_parts(cfg, noise_source="numpy")
     eng = fb.GpuSimulationEngine(ds, postprocessors=post)

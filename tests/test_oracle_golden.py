@@ -12,7 +12,7 @@ from tests.helpers import CONFIGS, golden_rows, oracle_model, oracle_run, produc
 
 
 @pytest.mark.parametrize("name", ["mlp_dp", "logistic_dp", "mlp_noclip", "cnn_dp", "mlp_adam_dp", "logistic_fedprox",
-                                  "mlp_adafedprox", "mlp_scaffold_dp", "logistic_scaffold"])
+                                  "mlp_adafedprox", "mlp_scaffold_dp", "logistic_scaffold", "cnn_scaffold"])
 def test_oracle_reproduces_reference_run(name, golden):
     g = golden(name)
     cfg = CONFIGS[name]
