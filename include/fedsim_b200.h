@@ -152,7 +152,9 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
                          float* delta_out, int64_t ld_delta, int32_t* nonfinite,
                          int max_slots, int hist_steps, void* workspace, int64_t workspace_bytes,
                          double* fc1_sumsq, const float* control /* nullable [C, ld_control]: c - c_i */,
-                         int64_t ld_control, void* stream);
+                         int64_t ld_control,
+                         const int32_t* h_client_steps /* nullable HOST [C]: local steps per client */,
+                         void* stream);
 
 /* ------------------------------------------------------- data movement
  * Copy each cohort client's contiguous rows (num_rows[c] rows of row_bytes

@@ -57,7 +57,8 @@ def local_sgd_cohort(runner, theta, pop, row_start, num_rows, perms, perm_off, C
     fc1 form: a per-client dense control term has no low-rank history."""
     B = tp.batch_size
     n = np.asarray(h_num_rows, dtype=np.int64)
-    max_steps = int((tp.num_epochs * ((n + B - 1) // B)).max()) if len(n) else 0
+    steps = np.ascontiguousarray(tp.num_epochs * ((n + B - 1) // B), dtype=np.int32)  # host, per client
+    max_steps = int(steps.max()) if len(n) else 0
     slots = _slots(C, B)
     hist = hist_steps(max_steps, B) if control is None else 0
     nbytes = native.call("fb_cnn_workspace_bytes", slots, slots // B, hist)
@@ -73,5 +74,5 @@ def local_sgd_cohort(runner, theta, pop, row_start, num_rows, perms, perm_off, C
                 runner.ld, native.ptr(nonfinite), slots, hist, native.ptr(ws), ws.numel(),
                 native.ptr(sq) if sq is not None else None,
                 native.ptr(control) if control is not None else None,
-                control.stride(0) if control is not None else 0, stream)
+                control.stride(0) if control is not None else 0, steps.ctypes.data, stream)
     return sq

@@ -3089,12 +3089,14 @@ int prep_theta_images(const float* theta, const Work& w, cudaStream_t s) {
 }
 
 // forward of N slots (shared weights when delta == nullptr) up to the head
+// `active`: clients with a slot this step (host-known; sizes the per-client CTA split), -1 = all
 int forward(const float* X, const float* theta, const float* delta, int64_t ld, int B, int N, int G,
-            const Work& w, cudaStream_t s, const int32_t* client_nb, bool shared_fc1 = false) {
+            const Work& w, cudaStream_t s, const int32_t* client_nb, bool shared_fc1 = false, int active = -1) {
+  if (active < 0) active = N / B;
   const bool tc = g_conv_impl == 1;
   if (tc) {
     // slots per CTA: (part of) one client's batch (its own weights), or 16 at theta_t
-    const int g1 = delta ? B / client_split(N / B, B, 2) : C1F_GMAX;
+    const int g1 = delta ? B / client_split(active, B, 2) : C1F_GMAX;
     FB_LAUNCH("conv1_fwd_tc_kernel", s, conv1_fwd_tc_kernel<<<(N + g1 - 1) / g1, C1F_THREADS, C1F_SMEM, s>>>(
                                             X, w.slot_row, theta, delta, ld, B, N, g1, w.a1fh, w.a1fl, w.a1scale));
   } else {
@@ -3110,7 +3112,7 @@ int forward(const float* X, const float* theta, const float* delta, int64_t ld, 
     int st = a1f_tensor_map(&mh, w.a1fh, N, S1, FW_BAND);
     if (!st) st = a1f_tensor_map(&ml, w.a1fl, N, S1, FW_BAND);
     if (st) return st;
-    const int gt = delta ? B / client_split(N / B, B, 1) : 8;  // samples per CTA
+    const int gt = delta ? B / client_split(active, B, 1) : 8;  // samples per CTA
     FB_LAUNCH("conv2_fwd_tc_kernel", s, conv2_fwd_tc_kernel<<<(N + gt - 1) / gt, FW_THREADS, FW_SMEM, s>>>(
           mh, ml, w.wimg, w.wscale, delta ? 0 : 1, w.slot_row, N, gt, theta, delta, ld, B, w.a1scale, w.pooled,
           w.code));
@@ -3238,7 +3240,7 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
                          int epochs, int batch_size, int max_steps, float lr, float prox_mu, float* delta_out,
                          int64_t ld_delta, int32_t* nonfinite, int max_slots, int hist_steps, void* workspace,
                          int64_t workspace_bytes, double* fc1_sumsq, const float* control, int64_t ld_control,
-                         void* stream) {
+                         const int32_t* h_client_steps, void* stream) {
   FB_REQUIRE(num_clients >= 0 && epochs >= 0 && batch_size >= 1 && max_steps >= 0 && hist_steps >= 0,
              "local_sgd_cnn: bad arguments");
   FB_REQUIRE(!control || (hist_steps == 0 && ld_control >= D && (ld_control & 3) == 0),
@@ -3301,7 +3303,13 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
       }
       FB_LAUNCH("train_slots_kernel", s, train_slots_kernel<<<(N + 255) / 256, 256, 0, s>>>(step, row_start + c0, num_rows + c0, perms, perm_off + c0,
                                                         Cw, epochs, B, ws.slot_row, ws.client_nb));
-      st = forward(X, theta_t, dlt, ld_delta, B, N, B, ws, s, ws.client_nb, fact);
+      int active = Cw;  // clients still training at this step (ragged cohorts: a few long clients)
+      if (h_client_steps) {
+        active = 0;
+        for (int c = 0; c < Cw; ++c) active += h_client_steps[c0 + c] > step;
+        active = std::max(active, 1);
+      }
+      st = forward(X, theta_t, dlt, ld_delta, B, N, B, ws, s, ws.client_nb, fact, active);
       if (st) return st;
       if (fact) {
         FB_REQUIRE((int64_t)max_steps * N * FLAT < (1LL << 31), "local_sgd_cnn: factored-fc1 history exceeds 2^31 elements");
@@ -3371,7 +3379,7 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
         st = dzf_tensor_map(&mh, ws.dzfh, N, S1, BX_BAND);
         if (!st) st = dzf_tensor_map(&ml, ws.dzfl, N, S1, BX_BAND);
         if (st) return st;
-        const int split = client_split(Cw, B, 1);
+        const int split = client_split(active, B, 1);
         FB_LAUNCH("conv2_bwd_x_tc_kernel", s, conv2_bwd_x_tc_kernel<<<Cw * split, BX_THREADS, BX_SMEM, s>>>(
             mh, ml, ws.wimg, ws.wscale, ws.slot_row, B / split, B, ws.dzscale, ws.a1fh, ws.a1fl, ws.dz1));
         CUtensorMap ah, al, dh, dl;
