@@ -330,21 +330,26 @@ __global__ void __launch_bounds__(256) conv2_fwd_pool_kernel(const float* __rest
 }
 
 // ---------------------------------------------------------------- fc1 fwd
-// grid (groups, KSPLIT), one warp per CTA: group = G consecutive slots sharing
+// grid (groups, KSPLIT), 7 warps per CTA: group = G consecutive slots sharing
 // weights (a client in training, G = B; a chunk of rows at theta_t in
-// evaluation, G = GMAX).  The warp streams its 448 weight rows (each lane a
-// float4 of the 128 units: coalesced 512-byte rows, 4 rows in flight);
-// the group's activations for 32 rows at a time are loaded one per lane and
-// broadcast with shuffles, so there is no shared memory and up to 32
-// single-warp CTAs per SM keep enough loads in flight for HBM.
+// evaluation, G = GMAX).  Each warp streams 64 of the CTA's 448 weight rows
+// (each lane a float4 of the 128 units: coalesced 512-byte rows, 4 rows in
+// flight); the group's activations for 32 rows at a time are loaded one per
+// lane and broadcast with shuffles.  The 7 warp partials are summed in fixed
+// order through shared memory.  (7 warps per CTA keep enough loads in flight
+// when only a few clients train at a step -- ragged cohorts.)
+constexpr int FF_WARPS = 7, FF_ROWS = KCHUNK / FF_WARPS;  // 64 rows per warp
+static_assert(FF_ROWS % 32 == 0, "fc1 fwd rows per warp");
 template <int GM>
-__global__ void __launch_bounds__(32) fc1_fwd_kernel(const float* __restrict__ pooled,
-                                                     const int64_t* __restrict__ slot_row, int N, int G,
-                                                     const float* __restrict__ theta, const float* __restrict__ delta,
-                                                     int64_t ld, float* __restrict__ part) {
-  const int g = blockIdx.x, split = blockIdx.y, lane = threadIdx.x;
+__global__ void __launch_bounds__(FF_WARPS * 32) fc1_fwd_kernel(const float* __restrict__ pooled,
+                                                              const int64_t* __restrict__ slot_row, int N, int G,
+                                                              const float* __restrict__ theta,
+                                                              const float* __restrict__ delta, int64_t ld,
+                                                              float* __restrict__ part) {
+  __shared__ float4 red[FF_WARPS - 1][8][32];
+  const int g = blockIdx.x, split = blockIdx.y, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int n0 = g * G;
-  const int k0 = split * KCHUNK;
+  const int k0 = split * KCHUNK + warp * FF_ROWS;
   bool live[GM];
   int any = 0;
 #pragma unroll
@@ -359,7 +364,7 @@ __global__ void __launch_bounds__(32) fc1_fwd_kernel(const float* __restrict__ p
   for (int b = 0; b < GM; ++b) acc[b] = make_float4(0.f, 0.f, 0.f, 0.f);
   const float4* th4 = reinterpret_cast<const float4*>(theta + O_F1 + (int64_t)k0 * HID) + lane;
   const float4* dl4 = dc ? reinterpret_cast<const float4*>(dc + O_F1 + (int64_t)k0 * HID) + lane : nullptr;
-  for (int r0 = 0; r0 < KCHUNK; r0 += 32) {
+  for (int r0 = 0; r0 < FF_ROWS; r0 += 32) {
     float pv[GM];  // lane l holds the activations of row r0 + l
 #pragma unroll
     for (int b = 0; b < GM; ++b)
@@ -383,9 +388,26 @@ __global__ void __launch_bounds__(32) fc1_fwd_kernel(const float* __restrict__ p
     }
   }
 #pragma unroll
-  for (int b = 0; b < GM; ++b)
-    if (b < G && n0 + b < N)
-      reinterpret_cast<float4*>(part + ((int64_t)split * N + n0 + b) * HID)[lane] = acc[b];
+  for (int b0 = 0; b0 < GM; b0 += 8) {
+    if (warp > 0) {
+#pragma unroll
+      for (int b = b0; b < b0 + 8 && b < GM; ++b) red[warp - 1][b - b0][lane] = acc[b];
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+      for (int b = b0; b < b0 + 8 && b < GM; ++b) {
+        float4 a = acc[b];
+#pragma unroll
+        for (int w = 0; w < FF_WARPS - 1; ++w) {
+          const float4 o = red[w][b - b0][lane];
+          a.x += o.x; a.y += o.y; a.z += o.z; a.w += o.w;
+        }
+        if (b < G && n0 + b < N) reinterpret_cast<float4*>(part + ((int64_t)split * N + n0 + b) * HID)[lane] = a;
+      }
+    }
+    __syncthreads();
+  }
 }
 
 // ------------------------------------------------------------------ head
@@ -552,9 +574,11 @@ __global__ void __launch_bounds__(FB_WARPS * 32) fc1_bwd_kernel(const float* __r
                                                                  const int32_t* __restrict__ client_nb,
                                                                  const float* __restrict__ theta,
                                                                  float* __restrict__ delta, int64_t ld, Step st,
-                                                                 float* __restrict__ dp) {
+                                                                 float* __restrict__ dp, int rsplit) {
   extern __shared__ float bsm[];
-  const int c = blockIdx.x, split = blockIdx.y;
+  // grid.y = KSPLIT * rsplit (rsplit 1 or 7): rows are independent, so a few active
+  // clients (ragged cohorts) spread their rows over 7x more CTAs
+  const int c = blockIdx.x, split = blockIdx.y / rsplit, sub = blockIdx.y - split * rsplit;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nb = client_nb[c];
   if (nb == 0) return;
@@ -569,8 +593,9 @@ __global__ void __launch_bounds__(FB_WARPS * 32) fc1_bwd_kernel(const float* __r
   float* dc = delta + (int64_t)c * ld;
   const float lr = st.lr, mu = st.mu;
   constexpr int ROWS_PER_WARP = KCHUNK / FB_WARPS;  // 112
-  const int kw = split * KCHUNK + warp * ROWS_PER_WARP;
-  for (int r0 = 0; r0 < ROWS_PER_WARP; r0 += FB_TR) {
+  const int rows = ROWS_PER_WARP / rsplit;
+  const int kw = split * KCHUNK + warp * ROWS_PER_WARP + sub * rows;
+  for (int r0 = 0; r0 < rows; r0 += FB_TR) {
     float pv[GM];  // lane l < FB_TR holds the activations of row r0 + l
 #pragma unroll
     for (int b = 0; b < GM; ++b)
@@ -2781,6 +2806,7 @@ int g_conv_impl = 1;  // 1 = tcgen05 (product path), 0 = FP32 CUDA-core kernels 
 // = 8 output rows = 240 positions = 15 MMAs of K = 16; each K block starts
 // fresh TMEM accumulators per ky (hi*hi and cross terms separately), drained
 // by eight epilogue warps into fp32 registers with the per-sample unscale.
+constexpr int BW_PART = 3 * 64 * 96;  // floats per split partial of conv2_bwd_w_tc ([ky][o][kx*32+ci])
 constexpr int BW_ROWS = 8;                        // output rows per K block
 constexpr int BW_NKB = (S2 + BW_ROWS - 1) / BW_ROWS;  // 4 K blocks per sample
 constexpr int BW_KPOS = BW_ROWS * S1;             // 240 positions
@@ -2801,7 +2827,8 @@ __global__ void __launch_bounds__(BW_THREADS, 1) conv2_bwd_w_tc_kernel(
     const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
     const __grid_constant__ CUtensorMap td_hi, const __grid_constant__ CUtensorMap td_lo, int B,
     const int32_t* __restrict__ client_nb, const float* __restrict__ a1scale, const float* __restrict__ dzscale,
-    const float* __restrict__ db2, float* __restrict__ delta, int64_t ld, Step st) {
+    const float* __restrict__ db2, float* __restrict__ delta, int64_t ld, Step st, int split,
+    float* __restrict__ wpart) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + BW_STAGES * BW_STAGE);
@@ -2812,10 +2839,13 @@ __global__ void __launch_bounds__(BW_THREADS, 1) conv2_bwd_w_tc_kernel(
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 3);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c = blockIdx.x;
-  const int nb = client_nb[c];
-  if (nb == 0) return;
-  const int nblocks = nb * BW_NKB;
+  // split > 1 (few active clients): CTA (c, part) takes samples [b0, b1) of client c and
+  // writes its partial gradient to wpart; conv2_bwd_w_reduce_kernel applies the update
+  const int c = blockIdx.x / split, part = blockIdx.x - c * split;
+  const int nbc = client_nb[c];
+  const int b0 = part * nbc / split, b1 = (part + 1) * nbc / split;
+  if (b1 <= b0) return;
+  const int nblocks = (b1 - b0) * BW_NKB;
   for (int s = 0; s < BW_STAGES; ++s)  // a1 rows 300..303 are read against zero dz2 rows: keep them finite
     for (int i = threadIdx.x; i < (BW_A_BYTES - BW_A_TX) / 4; i += blockDim.x) {
       reinterpret_cast<float*>(sm + s * BW_STAGE + BW_A_TX)[i] = 0.f;
@@ -2848,7 +2878,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1) conv2_bwd_w_tc_kernel(
       int stage = 0;
       uint32_t phase = 0;
       for (int blk = 0; blk < nblocks; ++blk) {
-        const int n = c * B + blk / BW_NKB, y0 = BW_ROWS * (blk % BW_NKB);
+        const int n = c * B + b0 + blk / BW_NKB, y0 = BW_ROWS * (blk % BW_NKB);
         tc::mbar_wait(&empty[stage], phase ^ 1);
         tc::mbar_arrive_expect_tx(&full[stage], 2 * BW_A_TX + 2 * BW_B_BYTES);
         uint8_t* st_ = sm + stage * BW_STAGE;
@@ -2900,7 +2930,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1) conv2_bwd_w_tc_kernel(
 #pragma unroll
       for (int j = 0; j < 32; ++j) run[i][j] = 0.f;
     for (int blk = 0; blk < nblocks; ++blk) {
-      const int n = c * B + blk / BW_NKB;
+      const int n = c * B + b0 + blk / BW_NKB;
       const float inv = 1.f / (a1scale[n] * dzscale[n]);  // exact: powers of two
 #pragma unroll
       for (int ky = 0; ky < 3; ++ky) {
@@ -2920,7 +2950,14 @@ __global__ void __launch_bounds__(BW_THREADS, 1) conv2_bwd_w_tc_kernel(
     }
     const int kx = row >> 5, ci = row & 31;
     float* dc = delta + (int64_t)c * ld;
-    if (kx < 3) {
+    if (split > 1) {  // partial [ky][o][kx * 32 + ci] of this sample range
+      float* wp = wpart + (int64_t)blockIdx.x * BW_PART;
+      if (kx < 3)
+#pragma unroll
+        for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+          for (int j = 0; j < 32; ++j) wp[(ky * C2 + hc * 32 + j) * 96 + row] = run[ky][j];
+    } else if (kx < 3) {
 #pragma unroll
       for (int ky = 0; ky < 3; ++ky)
 #pragma unroll
@@ -2931,7 +2968,8 @@ __global__ void __launch_bounds__(BW_THREADS, 1) conv2_bwd_w_tc_kernel(
         }
     }
     const int e = threadIdx.x - 64;
-    if (e < C2) {  // conv2 bias: sum of the client's per-sample partials
+    if (split == 1 && e < C2) {  // conv2 bias: sum of the client's per-sample partials
+      const int nb = nbc;
       float gb = 0.f;
       for (int b = 0; b < nb; ++b) gb += db2[(int64_t)(c * B + b) * C2 + e];
       float& dl = dc[O_B2 + e];
@@ -2942,6 +2980,31 @@ __global__ void __launch_bounds__(BW_THREADS, 1) conv2_bwd_w_tc_kernel(
   __syncthreads();
   tc::tc_fence_after();
   if (warp == 1) tc::tmem_dealloc<512>(tmem);
+}
+
+// split conv2 weight gradient: sum the CTA partials of each client in fixed order and
+// apply delta += lr * (g - mu * delta) (conv2 weights and bias)
+__global__ void conv2_bwd_w_reduce_kernel(const float* __restrict__ wpart, int split, int B,
+                                          const int32_t* __restrict__ client_nb, const float* __restrict__ db2,
+                                          float* __restrict__ delta, int64_t ld, Step st) {
+  const int c = blockIdx.x;
+  const int nb = client_nb[c];
+  if (nb == 0) return;
+  float* dc = delta + (int64_t)c * ld;
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < BW_PART; e += gridDim.y * blockDim.x) {
+    float g = 0.f;
+    for (int p = 0; p < split; ++p)  // (a part with an empty sample range wrote nothing)
+      if ((p + 1) * nb / split > p * nb / split) g += wpart[((int64_t)c * split + p) * BW_PART + e];
+    const int row = e % 96, ko = e / 96, o = ko % C2, ky = ko / C2, kx = row >> 5, ci = row & 31;
+    float& dl = dc[O_W2 + (int64_t)o * (C1 * 9) + ci * 9 + ky * 3 + kx];
+    dl += st.lr * (g - st.mu * dl);
+  }
+  if (blockIdx.y == 0 && threadIdx.x < C2) {
+    float gb = 0.f;
+    for (int b = 0; b < nb; ++b) gb += db2[(int64_t)(c * B + b) * C2 + threadIdx.x];
+    float& dl = dc[O_B2 + threadIdx.x];
+    dl += st.lr * (gb - st.mu * dl);
+  }
 }
 
 // ------------------------------------------------------------- workspace
@@ -3139,13 +3202,13 @@ int forward(const float* X, const float* theta, const float* delta, int64_t ld, 
     const int gf = fd ? G : 8;
     const dim3 grid((N + gf - 1) / gf, KSPLIT);
     if (gf <= 8)
-      FB_LAUNCH("fc1_fwd_kernel", s, fc1_fwd_kernel<8><<<grid, 32, 0, s>>>(w.pooled, w.slot_row, N, gf, theta, fd, ld, w.part));
+      FB_LAUNCH("fc1_fwd_kernel", s, fc1_fwd_kernel<8><<<grid, FF_WARPS * 32, 0, s>>>(w.pooled, w.slot_row, N, gf, theta, fd, ld, w.part));
     else if (gf <= 10)
-      FB_LAUNCH("fc1_fwd_kernel", s, fc1_fwd_kernel<10><<<grid, 32, 0, s>>>(w.pooled, w.slot_row, N, gf, theta, fd, ld, w.part));
+      FB_LAUNCH("fc1_fwd_kernel", s, fc1_fwd_kernel<10><<<grid, FF_WARPS * 32, 0, s>>>(w.pooled, w.slot_row, N, gf, theta, fd, ld, w.part));
     else if (gf <= 12)
-      FB_LAUNCH("fc1_fwd_kernel", s, fc1_fwd_kernel<12><<<grid, 32, 0, s>>>(w.pooled, w.slot_row, N, gf, theta, fd, ld, w.part));
+      FB_LAUNCH("fc1_fwd_kernel", s, fc1_fwd_kernel<12><<<grid, FF_WARPS * 32, 0, s>>>(w.pooled, w.slot_row, N, gf, theta, fd, ld, w.part));
     else
-      FB_LAUNCH("fc1_fwd_kernel", s, fc1_fwd_kernel<GMAX><<<grid, 32, 0, s>>>(w.pooled, w.slot_row, N, gf, theta, fd, ld, w.part));
+      FB_LAUNCH("fc1_fwd_kernel", s, fc1_fwd_kernel<GMAX><<<grid, FF_WARPS * 32, 0, s>>>(w.pooled, w.slot_row, N, gf, theta, fd, ld, w.part));
   }
   return launch_status("cnn forward");
 }
@@ -3310,6 +3373,7 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
         active = std::max(active, 1);
       }
       st = forward(X, theta_t, dlt, ld_delta, B, N, B, ws, s, ws.client_nb, fact, active);
+      const int rs = active * KSPLIT < 4 * g_num_sms ? 7 : 1;
       if (st) return st;
       if (fact) {
         FB_REQUIRE((int64_t)max_steps * N * FLAT < (1LL << 31), "local_sgd_cnn: factored-fc1 history exceeds 2^31 elements");
@@ -3361,15 +3425,15 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
         else
           FB_LAUNCH("fc1_bwd_fact_kernel", s, fc1_bwd_fact_kernel<GMAX><<<dim3(Cw, KSPLIT), FB_WARPS * 32, FC1F_SMEM, s>>>(
               ws.dz3, B, ws.client_nb, theta_t, hs, ws.dp));
-      } else if (B <= 8) {
-        FB_LAUNCH("fc1_bwd_kernel", s, fc1_bwd_kernel<8><<<dim3(Cw, KSPLIT), FB_WARPS * 32, FC1B_SMEM, s>>>(
-            ws.pooled, ws.dz3, B, ws.client_nb, theta_t, dlt, ld_delta, sp, ws.dp));
+      } else if (B <= 8) {  // (rs: row split of the dense fc1 update when few clients are active)
+        FB_LAUNCH("fc1_bwd_kernel", s, fc1_bwd_kernel<8><<<dim3(Cw, KSPLIT * rs), FB_WARPS * 32, FC1B_SMEM, s>>>(
+            ws.pooled, ws.dz3, B, ws.client_nb, theta_t, dlt, ld_delta, sp, ws.dp, rs));
       } else if (B <= 10) {
-        FB_LAUNCH("fc1_bwd_kernel", s, fc1_bwd_kernel<10><<<dim3(Cw, KSPLIT), FB_WARPS * 32, FC1B_SMEM, s>>>(
-            ws.pooled, ws.dz3, B, ws.client_nb, theta_t, dlt, ld_delta, sp, ws.dp));
+        FB_LAUNCH("fc1_bwd_kernel", s, fc1_bwd_kernel<10><<<dim3(Cw, KSPLIT * rs), FB_WARPS * 32, FC1B_SMEM, s>>>(
+            ws.pooled, ws.dz3, B, ws.client_nb, theta_t, dlt, ld_delta, sp, ws.dp, rs));
       } else {
-        FB_LAUNCH("fc1_bwd_kernel", s, fc1_bwd_kernel<GMAX><<<dim3(Cw, KSPLIT), FB_WARPS * 32, FC1B_SMEM, s>>>(
-            ws.pooled, ws.dz3, B, ws.client_nb, theta_t, dlt, ld_delta, sp, ws.dp));
+        FB_LAUNCH("fc1_bwd_kernel", s, fc1_bwd_kernel<GMAX><<<dim3(Cw, KSPLIT * rs), FB_WARPS * 32, FC1B_SMEM, s>>>(
+            ws.pooled, ws.dz3, B, ws.client_nb, theta_t, dlt, ld_delta, sp, ws.dp, rs));
       }
       if (g_conv_impl == 1) {
         FB_LAUNCH("dz2_build_kernel", s, dz2_build_kernel<<<N, 256, DZB_SMEM, s>>>(ws.dp, ws.pooled, ws.code, ws.slot_row, ws.dzfh, ws.dzfl, ws.dzscale, ws.db2));
@@ -3388,8 +3452,16 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
         if (!st) st = dzf_tensor_map(&dh, ws.dzfh, N, S1, BW_ROWS);
         if (!st) st = dzf_tensor_map(&dl, ws.dzfl, N, S1, BW_ROWS);
         if (st) return st;
-        FB_LAUNCH("conv2_bwd_w_tc_kernel", s, conv2_bwd_w_tc_kernel<<<Cw, BW_THREADS, BW_SMEM, s>>>(
-            ah, al, dh, dl, B, ws.client_nb, ws.a1scale, ws.dzscale, ws.db2, dlt, ld_delta, sp));
+        // few active clients: split each client's samples over CTAs, partials in the (consumed) dp buffer
+        int wsplit = 1;
+        while (wsplit < B && active * (wsplit + 1) <= g_num_sms &&
+               (int64_t)Cw * (wsplit + 1) * BW_PART <= (int64_t)N * FLAT)
+          ++wsplit;
+        FB_LAUNCH("conv2_bwd_w_tc_kernel", s, conv2_bwd_w_tc_kernel<<<Cw * wsplit, BW_THREADS, BW_SMEM, s>>>(
+            ah, al, dh, dl, B, ws.client_nb, ws.a1scale, ws.dzscale, ws.db2, dlt, ld_delta, sp, wsplit, ws.dp));
+        if (wsplit > 1)
+          FB_LAUNCH("conv2_bwd_w_reduce_kernel", s, conv2_bwd_w_reduce_kernel<<<dim3(Cw, 8), 256, 0, s>>>(
+                                                        ws.dp, wsplit, B, ws.client_nb, ws.db2, dlt, ld_delta, sp));
       } else {
         FB_LAUNCH("conv2_bwd_x_kernel", s, conv2_bwd_x_kernel<<<N, 256, C2X_SMEM, s>>>(ws.dp, ws.pooled, ws.code, ws.a1, ws.slot_row, B, theta_t, dlt,
                                                     ld_delta, ws.dz1));
