@@ -2620,6 +2620,7 @@ __global__ void __launch_bounds__(C1F_THREADS, 2) conv1_fwd_tc_kernel(
 // im2col'ed from the image in smem), double-buffered against the MMAs; each
 // chunk's accumulator (a 16-MMA chain) is drained by warps 0 / 1 into fp32
 // registers (round-to-nearest adds) while the next chunk runs.
+constexpr int W1_PART = 28 * 32;  // floats per split partial of conv1_bwd_w_tc ([k][o])
 constexpr int W1_CH = 64;                           // positions per chunk
 constexpr int W1_CPS = (S1 * S1 + W1_CH - 1) / W1_CH;  // 15 chunks per sample (last: 4 positions)
 constexpr int W1_ATOM = 16 * 1024;                  // per 32-position K atom: A rows 0-63 (8 KB) | B rows 0-63 (8 KB)
@@ -2631,20 +2632,33 @@ static_assert(W1_NLD * W1_THREADS == W1_CH * 8 && W1_KPER * (W1_THREADS / W1_CH)
 constexpr int W1_SMEM = 1024 + 2 * W1_STAGE + IMG * 4 + 32 * 33 * 4 + 64;
 constexpr uint32_t W1_IDESC = tc::idesc_tf32(128, 64);
 
+template <bool SPLIT>
 __global__ void __launch_bounds__(W1_THREADS, 2) conv1_bwd_w_tc_kernel(const float* __restrict__ X,
                                                                       const int64_t* __restrict__ slot_row,
                                                                       const float* __restrict__ dz1, int B,
                                                                       const int32_t* __restrict__ client_nb,
-                                                                      float* __restrict__ delta, int64_t ld, Step st) {
+                                                                      float* __restrict__ delta, int64_t ld, Step st,
+                                                                      int split, float* __restrict__ wpart) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* img = reinterpret_cast<float*>(sm + 2 * W1_STAGE);  // [3][32][32]
   float* red = img + IMG;                                    // [32][33]: warp 1's sums
   uint64_t* done = reinterpret_cast<uint64_t*>(red + 32 * 33);  // [2] MMA completion per stage
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 2);
-  const int c = blockIdx.x;
-  const int nb = client_nb[c];
-  if (nb == 0) return;
+  // split > 1 (few active clients): CTA (c, part) takes samples [b0, b1) and writes a
+  // partial [28][32] gradient; conv1_bwd_w_reduce_kernel applies the update
+  // (SPLIT = false: the plain one-CTA-per-client kernel, compiled separately)
+  int c = blockIdx.x, b0 = 0, b1;
+  if constexpr (SPLIT) {
+    c = blockIdx.x / split;
+    const int part = blockIdx.x - c * split, nbc = client_nb[c];
+    b0 = part * nbc / split;
+    b1 = (part + 1) * nbc / split;
+    if (b1 <= b0) return;
+  } else {
+    b1 = client_nb[c];
+    if (b1 == 0) return;
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, t = threadIdx.x;
   const uint32_t s0 = tc::smem_u32(sm), simg = tc::smem_u32(img);
   // rows 28-31 / 60-63 of B (padding of k) stay zero; staging never writes them
@@ -2685,10 +2699,10 @@ __global__ void __launch_bounds__(W1_THREADS, 2) conv1_bwd_w_tc_kernel(const flo
   // A staging: coalesced float4 f = j * 256 + t of the chunk's [64 pos][32 o] dz1 block
   // (position f / 8, channel quad f % 8); the next chunk is prefetched into
   // registers a chunk ahead
-  const int nchunks = nb * W1_CPS;
+  const int nchunks = (b1 - b0) * W1_CPS;
   auto load_dz = [&](int i, float4 (&v)[W1_NLD]) {
     const int b = i / W1_CPS, p0 = (i - b * W1_CPS) * W1_CH;
-    const float4* dzn = reinterpret_cast<const float4*>(dz1 + ((int64_t)c * B + b) * A1 + (int64_t)p0 * C1);
+    const float4* dzn = reinterpret_cast<const float4*>(dz1 + ((int64_t)c * B + b0 + b) * A1 + (int64_t)p0 * C1);
 #pragma unroll
     for (int j = 0; j < W1_NLD; ++j) {
       const int f = j * W1_THREADS + t;
@@ -2706,7 +2720,7 @@ __global__ void __launch_bounds__(W1_THREADS, 2) conv1_bwd_w_tc_kernel(const flo
   }
   for (int i = 0; i < nchunks; ++i) {
     const int b = i / W1_CPS, ch = i - b * W1_CPS, p0 = ch * W1_CH;
-    const int64_t n = (int64_t)c * B + b;
+    const int64_t n = (int64_t)c * B + b0 + b;
     const uint32_t stg = s0 + (i & 1) * W1_STAGE;
     if (i + 1 < nchunks) load_dz(i + 1, nxt);
     if (i >= 2) tc::mbar_wait(&done[i & 1], ((i - 2) >> 1) & 1);  // chunk i-2's MMAs done reading this stage
@@ -2776,7 +2790,12 @@ __global__ void __launch_bounds__(W1_THREADS, 2) conv1_bwd_w_tc_kernel(const flo
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
-  if (warp == 0) {
+  if (SPLIT && warp == 0) {
+    float* wp = wpart + (int64_t)blockIdx.x * W1_PART;
+#pragma unroll
+    for (int k = 0; k < 28; ++k) wp[k * 32 + lane] = run[k] + red[lane * 33 + k];
+    tc::tmem_dealloc<128>(tmem);
+  } else if (warp == 0) {
     float* dc = delta + (int64_t)c * ld;
 #pragma unroll
     for (int k = 0; k < 28; ++k) {
@@ -2785,6 +2804,24 @@ __global__ void __launch_bounds__(W1_THREADS, 2) conv1_bwd_w_tc_kernel(const flo
       dl += st.lr * (g - st.mu * dl);
     }
     tc::tmem_dealloc<128>(tmem);
+  }
+}
+
+// split conv1 weight gradient: fixed-order sum of the client's CTA partials, then the update
+__global__ void conv1_bwd_w_reduce_kernel(const float* __restrict__ wpart, int split,
+                                          const int32_t* __restrict__ client_nb, float* __restrict__ delta,
+                                          int64_t ld, Step st) {
+  const int c = blockIdx.x;
+  const int nb = client_nb[c];
+  if (nb == 0) return;
+  float* dc = delta + (int64_t)c * ld;
+  for (int e = threadIdx.x; e < W1_PART; e += blockDim.x) {
+    float g = 0.f;
+    for (int p = 0; p < split; ++p)  // (a part with an empty sample range wrote nothing)
+      if ((p + 1) * nb / split > p * nb / split) g += wpart[((int64_t)c * split + p) * W1_PART + e];
+    const int k = e >> 5, o = e & 31;
+    float& dl = k < 27 ? dc[O_W1 + (int64_t)o * (C0 * 9) + k] : dc[O_B1 + o];
+    dl += st.lr * (g - st.mu * dl);
   }
 }
 
@@ -3114,7 +3151,8 @@ int set_smem_limits() {
   cudaFuncSetAttribute(fc1_materialize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FC1M_SMEM);
   cudaFuncSetAttribute(fc1_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FT_SMEM);
   cudaFuncSetAttribute(conv2_bwd_w_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BW_SMEM);
-  cudaFuncSetAttribute(conv1_bwd_w_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, W1_SMEM);
+  cudaFuncSetAttribute(conv1_bwd_w_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, W1_SMEM);
+  cudaFuncSetAttribute(conv1_bwd_w_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, W1_SMEM);
   cudaFuncSetAttribute(conv1_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C1F_SMEM);
   cudaFuncSetAttribute(fc1_mat_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FMT_SMEM);
   cudaFuncSetAttribute(conv2_wimg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, WIMG_BYTES);
@@ -3469,8 +3507,21 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
                                                      sp));
       }
       if (g_conv_impl == 1)
-        FB_LAUNCH("conv1_bwd_w_tc_kernel", s, conv1_bwd_w_tc_kernel<<<Cw, W1_THREADS, W1_SMEM, s>>>(
-                                                   X, ws.slot_row, ws.dz1, B, ws.client_nb, dlt, ld_delta, sp));
+      {
+        int split1 = 1;  // few active clients: split each client's samples over CTAs (2 CTAs per SM)
+        while (split1 < B && active * (split1 + 1) <= 2 * g_num_sms) ++split1;
+        if (split1 > 1) {
+          FB_LAUNCH("conv1_bwd_w_tc_kernel", s, conv1_bwd_w_tc_kernel<true><<<Cw * split1, W1_THREADS, W1_SMEM, s>>>(
+                                                     X, ws.slot_row, ws.dz1, B, ws.client_nb, dlt, ld_delta, sp,
+                                                     split1, ws.dp));
+          FB_LAUNCH("conv1_bwd_w_reduce_kernel", s, conv1_bwd_w_reduce_kernel<<<Cw, 256, 0, s>>>(
+                                                        ws.dp, split1, ws.client_nb, dlt, ld_delta, sp));
+        } else {
+          FB_LAUNCH("conv1_bwd_w_tc_kernel", s, conv1_bwd_w_tc_kernel<false><<<Cw, W1_THREADS, W1_SMEM, s>>>(
+                                                     X, ws.slot_row, ws.dz1, B, ws.client_nb, dlt, ld_delta, sp,
+                                                     1, nullptr));
+        }
+      }
       else
         FB_LAUNCH("conv1_bwd_w_kernel", s, conv1_bwd_w_kernel<<<Cw, C1B_WARPS * 32, 0, s>>>(
                                                 X, ws.slot_row, ws.dz1, B, ws.client_nb, dlt, ld_delta, sp));
