@@ -172,6 +172,12 @@ int fb_gather_rows(const void* src, int64_t row_bytes, const int64_t* row_start,
 int fb_gather_rows_lite(const void* src, int64_t row_bytes, const int64_t* row_start,
                         const int32_t* num_rows, int num_clients, const int64_t* dst_start,
                         void* dst, int num_blocks, void* stream);
+/* Upload `bytes` (multiple of 16, 16-byte aligned pointers) from pinned host
+ * memory to the device with a kernel reading the host buffer over UVA, not a
+ * copy-engine memcpy: the engine's per-context descriptors (row offsets,
+ * permutations, weights) then never queue behind the copy engines' prefetch
+ * of the next iteration's cohort rows. */
+int fb_upload_pinned(const void* host_src, void* dst, int64_t bytes, void* stream);
 
 /* ------------------------------------------------- a6 + a7 (kernel K2)
  * For every client c: norm[c] = || w[c] * delta[c, :D] ||_2 (fp64

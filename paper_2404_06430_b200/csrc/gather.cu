@@ -8,6 +8,8 @@
 
 #include "fb_common.cuh"
 
+#include <algorithm>
+
 namespace fb {
 namespace {
 
@@ -33,6 +35,21 @@ __global__ void __launch_bounds__(kThreads) gather_rows_kernel(const uint8_t* __
   } else {
     for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < bytes; i += stride) d[i] = s[i];
   }
+}
+
+// grid-stride 16-byte copy, 4 loads in flight per thread (host source over PCIe)
+__global__ void __launch_bounds__(kThreads) upload_pinned_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                                                 int64_t n16) {
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  for (; i + 3 * stride < n16; i += 4 * stride) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = src[i + u * stride];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) dst[i + u * stride] = v[u];
+  }
+  for (; i < n16; i += stride) dst[i] = src[i];
 }
 
 // few-block variant for a copy stream beside the compute kernels: block b
@@ -100,6 +117,24 @@ int fb_gather_rows_lite(const void* src, int64_t row_bytes, const int64_t* row_s
                                           s>>>(static_cast<const uint8_t*>(src), row_bytes, row_start, num_rows,
                                                dst_start, num_clients, static_cast<uint8_t*>(dst)));
   return fb::launch_status("gather_rows_lite_kernel");
+}
+
+// Small host->device upload read by the SMs from pinned host memory (UVA): keeps the
+// compute stream's per-context descriptors off the copy engines, which the prefetch of
+// the next iteration's cohort rows occupies (an H2D memcpy queued behind it would stall
+// the compute stream for the whole prefetch).
+int fb_upload_pinned(const void* host_src, void* dst, int64_t bytes, void* stream) {
+  FB_REQUIRE(bytes >= 0 && (bytes & 15) == 0 && ((reinterpret_cast<uintptr_t>(host_src) |
+                                                  reinterpret_cast<uintptr_t>(dst)) & 15u) == 0,
+             "upload_pinned: pointers and size must be 16-byte aligned");
+  if (bytes == 0) return FB_OK;
+  cudaStream_t s = fb::as_stream(stream);
+  const int64_t n16 = bytes >> 4;
+  const unsigned blocks = (unsigned)std::min<int64_t>((n16 + fb::kThreads * 4 - 1) / (fb::kThreads * 4), 32);
+  FB_LAUNCH("upload_pinned_kernel", s,
+            fb::upload_pinned_kernel<<<blocks, fb::kThreads, 0, s>>>(static_cast<const uint4*>(host_src),
+                                                                    static_cast<uint4*>(dst), n16));
+  return fb::launch_status("upload_pinned_kernel");
 }
 
 }  // extern "C"

@@ -47,6 +47,7 @@ SIGNATURES: dict[str, tuple] = {
     ),
     "fb_gather_rows": (_i32, [_p, _i64, _p, _p, _i32, _p, _p, _i64, _p]),
     "fb_gather_rows_lite": (_i32, [_p, _i64, _p, _p, _i32, _p, _p, _i32, _p]),
+    "fb_upload_pinned": (_i32, [_p, _p, _i64, _p]),
     "fb_cnn_workspace_bytes": (_i64, [_i32, _i32, _i32]),
     "fb_cnn_set_conv_impl": (_i32, [_i32]),
     "fb_eval_cnn_f32": (_i32, [_p, _p, _p, _p, _p, _i32, _i64, _p, _p, _i32, _p, _i64, _p]),

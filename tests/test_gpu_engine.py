@@ -177,11 +177,16 @@ def test_engine_metrics_csv_and_checkpoint(golden, tmp_path):
     np.testing.assert_array_equal(np.concatenate([back[n] for n in back]), res.params.flat_host())
 
 
-@pytest.mark.parametrize("prefetch", [False, True], ids=["sync-gather", "prefetch"])
-def test_host_resident_dataset_matches_reference_run(golden, prefetch):
+@pytest.mark.parametrize("prefetch,max_runs", [(False, 64), (True, 64), (True, 0)],
+                         ids=["sync-gather", "prefetch-dma", "prefetch-gather-kernel"])
+def test_host_resident_dataset_matches_reference_run(golden, prefetch, max_runs, monkeypatch):
     """data_residency="host": cohort rows gathered from pinned host memory each
-    context (synchronously, or for iteration t+1 on a copy stream during t):
-    identical results to the device-resident run and the reference."""
+    context (synchronously, or for iteration t+1 on a copy stream during t, by
+    copy-engine runs in host order or by the gather kernel): identical results
+    to the device-resident run and the reference."""
+    from paper_2404_06430_b200 import engine
+
+    monkeypatch.setattr(engine, "PREFETCH_MAX_RUNS", max_runs)
     g = golden("mlp_dp")
     res, thetas = run_engine(CONFIGS["mlp_dp"], data_residency="host", prefetch=prefetch)
     assert res.cohort_digest == str(g["digest"])
