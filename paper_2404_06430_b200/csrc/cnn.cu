@@ -1264,7 +1264,8 @@ constexpr int WIMG_BYTES = 9 * 2 * FW_B_TAP;     // 73728: [tap][hi|lo]
 constexpr int FW_STAGES = 3;
 constexpr int FW_EPI_WARPS = 16;                 // 4 per TMEM lane quadrant, 16 channels each
 constexpr int FW_THREADS = (2 + FW_EPI_WARPS) * 32;
-constexpr int FW_EPI_BYTES = 2 * C2 * 128 * 4;   // double-buffered [64 ch][128 rows] conv outputs (post-ReLU)
+constexpr int FW_XLD = 66;                       // x-pooled pairs per channel row (64 + 2: conflict-free)
+constexpr int FW_EPI_BYTES = 2 * C2 * FW_XLD * 4; // double-buffered [64 ch][66] x-pooled conv outputs (post-ReLU)
 constexpr int FW_SMEM = 1024 + WIMG_BYTES + FW_STAGES * FW_STAGE + FW_EPI_BYTES + 256;
 constexpr int FW_ACC = 2 * C2;                   // main | cross accumulators (64 columns each) per tile
 constexpr uint32_t FW_IDESC = tc::idesc_f16(128, C2);
@@ -1456,7 +1457,7 @@ __global__ void __launch_bounds__(FW_THREADS, 1) conv2_fwd_tc_kernel(
       uint8_t* cout = code + (int64_t)n * FLAT;
       for (int t = 0; t < FW_TILES; ++t, ++tile) {
         const int acc = tile & 1;
-        const uint32_t sE = sE0 + acc * (C2 * 128 * 4);
+        const uint32_t sE = sE0 + acc * (C2 * FW_XLD * 4);
 #ifdef FB_FWD_PROF
         long long p_a = clock64();
 #endif
@@ -1478,24 +1479,35 @@ __global__ void __launch_bounds__(FW_THREADS, 1) conv2_fwd_tc_kernel(
           if (__uint_as_float(v0[0]) == 1.2345f) pout[0] = __uint_as_float(v1[1]);
           continue;
 #endif
-          const uint32_t dst = sE + ((cg * 16) * 128 + row) * 4;
+          float v[16];
 #pragma unroll
           for (int j = 0; j < 16; ++j)
-            tc::sts_f32(dst + j * 128 * 4,
-                        fmaxf(fmaf(__uint_as_float(v0[j]) + __uint_as_float(v1[j]), inv, bias[cg * 16 + j]), 0.f));
+            v[j] = fmaxf(fmaf(__uint_as_float(v0[j]) + __uint_as_float(v1[j]), inv, bias[cg * 16 + j]), 0.f);
+          // x half of the 2x2 pool in registers: rows m, m^1 are (x, x+1) of one conv row
+          // (row starts are multiples of 30, even).  The even lane keeps channels 0-7 of the
+          // group, the odd lane 8-15; the winner bit (x+1 strictly greater) rides in the sign
+          // of the post-ReLU (>= 0) value.  Halves the epilogue's smem traffic.
+          const bool odd = lane & 1;
+          const uint32_t dst = sE + ((cg * 16 + (odd ? 8 : 0)) * FW_XLD + (row >> 1)) * 4;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float mine = odd ? v[8 + j] : v[j];
+            const float other = __shfl_xor_sync(0xffffffffu, odd ? v[j] : v[8 + j], 1);
+            const float a = odd ? other : mine, b = odd ? mine : other;  // (x, x+1)
+            const bool win = b > a;
+            tc::sts_f32(dst + j * FW_XLD * 4, __int_as_float(__float_as_int(win ? b : a) | ((int)win << 31)));
+          }
         }
         asm volatile("bar.sync 1, %0;" ::"n"(FW_EPI_WARPS * 32) : "memory");
         for (int it = et; it < C2 * 2 * SP; it += FW_EPI_WARPS * 32) {
           const int ch = it / (2 * SP), pp = it - ch * (2 * SP), pr = pp >= SP, px = pp - pr * SP;
-          const uint32_t e0 = sE + (ch * 128 + 2 * pr * S1 + 2 * px) * 4;  // 8-byte aligned: (x, x+1) pairs
-          float q0, q1, q2, q3;
-          asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(q0), "=f"(q1) : "r"(e0) : "memory");
-          asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(q2), "=f"(q3) : "r"(e0 + S1 * 4) : "memory");
-          float best = q0;
-          int arg = 0;
-          if (q1 > best) { best = q1; arg = 1; }
-          if (q2 > best) { best = q2; arg = 2; }
-          if (q3 > best) { best = q3; arg = 3; }
+          const uint32_t e0 = sE + (ch * FW_XLD + pr * S1 + px) * 4;  // row 2pr pair px; row 2pr+1 is 15 pairs on
+          const float ta = tc::lds_f32(e0), tb = tc::lds_f32(e0 + (S1 / 2) * 4);
+          const float a = fabsf(ta), b = fabsf(tb);
+          // first maximum in (y,x), (y,x+1), (y+1,x), (y+1,x+1) order, as the sequential scan
+          const bool low = b > a;
+          const float best = low ? b : a;
+          const int arg = low ? 2 + (int)signbit(tb) : (int)signbit(ta);
           const int idx = ch * NPOOL + FW_ROWS / 2 * t * SP + pp;
           pout[idx] = best;
           cout[idx] = (uint8_t)arg;
