@@ -2507,14 +2507,19 @@ __global__ void __launch_bounds__(C1F_THREADS, 2) conv1_fwd_tc_kernel(
   const int pl = t & (C1F_TILE - 1), kh = t >> 7;
   // epilogue job: TMEM lane quadrant q = warp % 4, channel half chh = warp / 4
   const int q = warp & 3, chh = warp >> 2;
-  auto epilogue = [&](int i) {
-    const int buf = i & 1, j = i / C1F_TILES, tile = i - j * C1F_TILES, n = s_slot[j];
+  // epilogue of tile i in two halves: epi_load issues the TMEM loads (asynchronous), the
+  // next tile's im2col staging runs while they are in flight, epi_store finishes
+  uint32_t v0[16], v1[16];
+  auto epi_load = [&](int i) {
+    const int buf = i & 1;
     tc::mbar_wait(&done[buf], (i >> 1) & 1);
     tc::tc_fence_after();
     const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + buf * 64 + chh * 16;
-    uint32_t v0[16], v1[16];
     tc::tmem_ld16(base, v0);
     tc::tmem_ld16(base + C1, v1);
+  };
+  auto epi_store = [&](int i) {
+    const int j = i / C1F_TILES, tile = i - j * C1F_TILES, n = s_slot[j];
     tc::tmem_ld_wait();
     tc::tc_fence_before();
     const float sc = s_scale[j & 1];
@@ -2559,7 +2564,9 @@ __global__ void __launch_bounds__(C1F_THREADS, 2) conv1_fwd_tc_kernel(
         }
       }
     }
-    if (i >= 2) tc::mbar_wait(&done[buf], ((i - 2) >> 1) & 1);  // tile i-2's MMAs are done with this A stage
+    // tile i-1's accumulator: wait its MMAs (which also frees this A stage: tile i-2's MMAs
+    // completed before them) and start the TMEM loads; they land while tile i is staged
+    if (i >= 1) epi_load(i - 1);
     {
       // rows past the 900 positions (last tile) read position 899: their outputs are dropped
       const int p = min(tile * C1F_TILE + pl, S1 * S1 - 1), y = p / S1, x = p - y * S1;
@@ -2592,9 +2599,10 @@ __global__ void __launch_bounds__(C1F_THREADS, 2) conv1_fwd_tc_kernel(
       else
         stage(std::integral_constant<int, 1>{});
     }
+    if (i >= 1) epi_store(i - 1);
     tc::fence_proxy_async();
     tc::tc_fence_before();
-    __syncthreads();  // tile i staged; tile i-2's TMEM accumulator drained (epilogue of i-2 ran before)
+    __syncthreads();  // tile i staged; tile i-1's TMEM accumulator drained (its buffer is tile i+1's)
     tc::tc_fence_after();
     if (warp == 0) {
       if (tc::elect_one()) {
@@ -2610,9 +2618,9 @@ __global__ void __launch_bounds__(C1F_THREADS, 2) conv1_fwd_tc_kernel(
       }
       __syncwarp();
     }
-    if (i >= 1) epilogue(i - 1);
   }
-  epilogue(T - 1);
+  epi_load(T - 1);
+  epi_store(T - 1);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
