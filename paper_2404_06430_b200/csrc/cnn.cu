@@ -2369,11 +2369,10 @@ __global__ void __launch_bounds__(BX_THREADS, 1) conv2_bwd_x_tc_kernel(
         const int y = BX_ROWS * t + r;
         const bool ok = row < BX_M && y < S1;
         const int64_t off = ((int64_t)n * S1 * S1 + y * S1 + x) * C1 + cg * 8;
-        uint4 hv = make_uint4(0, 0, 0, 0), lv = hv;
-        if (ok) {
-          hv = *reinterpret_cast<const uint4*>(a1fh + off);
-          lv = *reinterpret_cast<const uint4*>(a1fl + off);
-        }
+        // ReLU mask from the hi part alone: a1 >= 0, and hi = rn(a1 * s) is 0 exactly when
+        // hi + lo is (a value too small for hi rounds to 0 in lo as well)
+        uint4 hv = make_uint4(0, 0, 0, 0);
+        if (ok) hv = *reinterpret_cast<const uint4*>(a1fh + off);
         tc::mbar_wait(&tfull[acc], (tile >> 1) & 1);
         tc::tc_fence_after();
         const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + acc * BX_ACC + cg * 8;
@@ -2385,13 +2384,11 @@ __global__ void __launch_bounds__(BX_THREADS, 1) conv2_bwd_x_tc_kernel(
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&tempty[acc]);  // accumulator drained: next tile may start
         if (ok) {
-          const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w}, lw[4] = {lv.x, lv.y, lv.z, lv.w};
+          const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
           float o[8];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const __half2 h2 = *reinterpret_cast<const __half2*>(&hw[e]);
-            const __half2 l2 = *reinterpret_cast<const __half2*>(&lw[e]);
-            const bool m0 = (__low2float(h2) + __low2float(l2)) > 0.f, m1 = (__high2float(h2) + __high2float(l2)) > 0.f;
+            const bool m0 = (hw[e] & 0xffffu) != 0u, m1 = (hw[e] >> 16) != 0u;
             const int j = 2 * e;
             const float z0 = (__uint_as_float(v0[j]) + __uint_as_float(v1[j])) * inv;
             const float z1 = (__uint_as_float(v0[j + 1]) + __uint_as_float(v1[j + 1])) * inv;
