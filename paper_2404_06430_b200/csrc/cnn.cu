@@ -2870,7 +2870,8 @@ constexpr int BW_A_TX = (BW_ROWS + 2) * S1 * 64;  // 19200
 constexpr int BW_B_BYTES = BW_KPOS * 128;         // 30720
 constexpr int BW_STAGE = 2 * BW_A_BYTES + 2 * BW_B_BYTES;  // 100352
 constexpr int BW_STAGES = 2;
-constexpr int BW_EPI_WARPS = 8;
+constexpr int BW_EPI_WARPS = 16;                  // 4 lane quarters x 4 groups of 16 output channels
+constexpr int BW_EPI_COLS = C2 / (BW_EPI_WARPS / 4);  // 16
 constexpr int BW_THREADS = (2 + BW_EPI_WARPS) * 32;
 constexpr int BW_SMEM = 1024 + BW_STAGES * BW_STAGE + 256;
 constexpr uint32_t BW_IDESC = tc::idesc_f16_mn(128, C2);
@@ -2976,13 +2977,13 @@ __global__ void __launch_bounds__(BW_THREADS, 1) conv2_bwd_w_tc_kernel(
     }
   } else {
     const int ew = warp & 3;                 // TMEM lane quarter
-    const int hc = (warp - 2) >> 2;          // column half (o 0-31 / 32-63)
-    const int row = ew * 32 + lane;          // M row = kx * 32 + ci
-    float run[3][32];
+    const int hc = (warp - 2) >> 2;          // column group (o 16 hc .. 16 hc + 15)
+    const int row = ew * 32 + lane;          // M row = kx * 32 + ci (quarter 3: kx = 3, unused rows)
+    float run[3][BW_EPI_COLS];
 #pragma unroll
     for (int i = 0; i < 3; ++i)
 #pragma unroll
-      for (int j = 0; j < 32; ++j) run[i][j] = 0.f;
+      for (int j = 0; j < BW_EPI_COLS; ++j) run[i][j] = 0.f;
     for (int blk = 0; blk < nblocks; ++blk) {
       const int n = c * B + b0 + blk / BW_NKB;
       const float inv = 1.f / (a1scale[n] * dzscale[n]);  // exact: powers of two
@@ -2990,16 +2991,21 @@ __global__ void __launch_bounds__(BW_THREADS, 1) conv2_bwd_w_tc_kernel(
       for (int ky = 0; ky < 3; ++ky) {
         tc::mbar_wait(&tfull[ky], blk & 1);
         tc::tc_fence_after();
-        uint32_t vm[32], vx[32];
-        const uint32_t base = tmem + ((uint32_t)(ew * 32) << 16) + ky * 2 * C2 + hc * 32;
-        tc::tmem_ld32(base, vm);
-        tc::tmem_ld32(base + C2, vx);
+        if (ew == 3) {  // the kx = 3 rows carry no weight: nothing to drain
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&tempty[ky]);
+          continue;
+        }
+        uint32_t vm[BW_EPI_COLS], vx[BW_EPI_COLS];
+        const uint32_t base = tmem + ((uint32_t)(ew * 32) << 16) + ky * 2 * C2 + hc * BW_EPI_COLS;
+        tc::tmem_ld16(base, vm);
+        tc::tmem_ld16(base + C2, vx);
         tc::tmem_ld_wait();
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&tempty[ky]);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) run[ky][j] += (__uint_as_float(vm[j]) + __uint_as_float(vx[j])) * inv;
+        for (int j = 0; j < BW_EPI_COLS; ++j) run[ky][j] += (__uint_as_float(vm[j]) + __uint_as_float(vx[j])) * inv;
       }
     }
     const int kx = row >> 5, ci = row & 31;
@@ -3010,13 +3016,13 @@ __global__ void __launch_bounds__(BW_THREADS, 1) conv2_bwd_w_tc_kernel(
 #pragma unroll
         for (int ky = 0; ky < 3; ++ky)
 #pragma unroll
-          for (int j = 0; j < 32; ++j) wp[(ky * C2 + hc * 32 + j) * 96 + row] = run[ky][j];
+          for (int j = 0; j < BW_EPI_COLS; ++j) wp[(ky * C2 + hc * BW_EPI_COLS + j) * 96 + row] = run[ky][j];
     } else if (kx < 3) {
 #pragma unroll
       for (int ky = 0; ky < 3; ++ky)
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int o = hc * 32 + j;
+        for (int j = 0; j < BW_EPI_COLS; ++j) {
+          const int o = hc * BW_EPI_COLS + j;
           float& dl = dc[O_W2 + (int64_t)o * (C1 * 9) + ci * 9 + ky * 3 + kx];
           dl += st.lr * (run[ky][j] - st.mu * dl);
         }
