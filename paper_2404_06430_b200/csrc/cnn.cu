@@ -2863,6 +2863,7 @@ int g_conv_impl = 1;  // 1 = tcgen05 (product path), 0 = FP32 CUDA-core kernels 
 constexpr int BW_PART = 3 * 64 * 96;  // floats per split partial of conv2_bwd_w_tc ([ky][o][kx*32+ci])
 constexpr int BW_ROWS = 8;                        // output rows per K block
 constexpr int BW_NKB = (S2 + BW_ROWS - 1) / BW_ROWS;  // 4 K blocks per sample
+static_assert(BW_NKB % 2 == 0, "conv2 weight gradient drains pairs of K blocks of one sample");
 constexpr int BW_KPOS = BW_ROWS * S1;             // 240 positions
 constexpr int BW_A_ROWS = 304;                    // a1 tile rows (300 loaded + 4 zero)
 constexpr int BW_A_BYTES = BW_A_ROWS * 64;        // 19456
@@ -2953,9 +2954,14 @@ __global__ void __launch_bounds__(BW_THREADS, 1) conv2_bwd_w_tc_kernel(
       tc::tc_fence_after();
       const uint32_t ah = s0 + stage * BW_STAGE, al = ah + BW_A_BYTES;
       const uint32_t bh = ah + 2 * BW_A_BYTES;  // dz2 lo follows at + BW_B_BYTES
+      // accumulators are drained once per PAIR of blocks (same sample: BW_NKB is even), a
+      // 30-step main chain per drain (<= 36: as accurate as fp32, tools/microbench)
+      const bool first = (blk & 1) == 0, last = (blk & 1) == 1;
       for (int ky = 0; ky < 3; ++ky) {
-        tc::mbar_wait(&tempty[ky], (blk & 1) ^ 1);  // previous block's ky accumulators drained
-        tc::tc_fence_after();
+        if (first) {
+          tc::mbar_wait(&tempty[ky], ((blk >> 1) & 1) ^ 1);  // previous pair's ky accumulators drained
+          tc::tc_fence_after();
+        }
         if (tc::elect_one()) {
           const uint32_t dm = tmem + ky * 2 * C2, dx = dm + C2;
 #pragma unroll 5
@@ -2966,9 +2972,9 @@ __global__ void __launch_bounds__(BW_THREADS, 1) conv2_bwd_w_tc_kernel(
             // B = [dz2 hi | dz2 lo] as ONE N = 128 MN-major operand: the two 64-wide N blocks are the
             // hi and lo tiles, BW_B_BYTES apart (LBO)
             const uint64_t bdh = tc::sdesc(bh + ks * 16 * 128, BW_B_BYTES, 1024, 2);
-            tc::mma2_f16(dm, dx, adh, adl, bdh, BW_IDESC2, BW_IDESC, ks != 0);
+            tc::mma2_f16(dm, dx, adh, adl, bdh, BW_IDESC2, BW_IDESC, !first || ks != 0);
           }
-          tc::mma_commit(&tfull[ky]);
+          if (last) tc::mma_commit(&tfull[ky]);
           if (ky == 2) tc::mma_commit(&empty[stage]);
         }
         __syncwarp();
@@ -2984,12 +2990,12 @@ __global__ void __launch_bounds__(BW_THREADS, 1) conv2_bwd_w_tc_kernel(
     for (int i = 0; i < 3; ++i)
 #pragma unroll
       for (int j = 0; j < BW_EPI_COLS; ++j) run[i][j] = 0.f;
-    for (int blk = 0; blk < nblocks; ++blk) {
+    for (int blk = 1; blk < nblocks; blk += 2) {  // one drain per pair of blocks
       const int n = c * B + b0 + blk / BW_NKB;
       const float inv = 1.f / (a1scale[n] * dzscale[n]);  // exact: powers of two
 #pragma unroll
       for (int ky = 0; ky < 3; ++ky) {
-        tc::mbar_wait(&tfull[ky], blk & 1);
+        tc::mbar_wait(&tfull[ky], (blk >> 1) & 1);
         tc::tc_fence_after();
         if (ew == 3) {  // the kx = 3 rows carry no weight: nothing to drain
           __syncwarp();
