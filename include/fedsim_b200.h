@@ -138,8 +138,10 @@ int fb_local_sgd_mlp_f32(const float* theta_t, int dim, int hidden, int num_clas
  * factored form only) receives each client's sum of squares of its fc1
  * weight delta block [O_F1, O_BF1), for fb_delta_norm_clip_ex_f32.          */
 int64_t fb_cnn_workspace_bytes(int max_slots, int max_clients, int hist_steps);
-/* Validation knob: 1 (default) = conv2 forward on tcgen05 (3xTF32, TMA,
- * TMEM); 0 = the FP32 CUDA-core kernels kept as an independent check.     */
+/* Validation knob: 1 (default) = the convolutions on tcgen05; 2 = tcgen05
+ * with the conv2 forward on 2-CTA clusters (cta_group::2, M = 256; correct,
+ * measured slower); 0 = the FP32 CUDA-core kernels kept as an independent
+ * check.                                                                    */
 int fb_cnn_set_conv_impl(int impl);
 int fb_eval_cnn_f32(const float* theta, const float* X, const int32_t* y,
                     const int64_t* row_start, const int32_t* num_rows, int num_clients,

@@ -1522,6 +1522,211 @@ __global__ void __launch_bounds__(FW_THREADS, 1) conv2_fwd_tc_kernel(
 }
 
 
+// ------------------------------------------- conv2 forward on CTA pairs (cta_group::2)
+// The same implicit GEMM as conv2_fwd_tc_kernel, run by a 2-CTA cluster: each pair
+// step is ONE M = 256 MMA chain over two tiles (the leader's tile 2k in rows 0-127,
+// the peer's tile 2k+1 in rows 128-255, each band in its own CTA's smem).  B is
+// split along N: the leader holds W hi (rows 0-63 of [W hi; W lo]) and rows 0-31 of
+// W hi, the peer W lo and rows 32-63 of W hi, so each SM reads half of the weight
+// operand per MMA (11 KB of smem operand traffic per K step and SM instead of 14).
+// Only the leader issues MMAs; both CTAs' TMA completions count on the leader's
+// stage barrier; commits multicast to both CTAs; the peer's epilogue warps arrive on
+// the leader's accumulator-free barrier.  Each CTA's epilogue pools its own 128 rows.
+constexpr int FW2_B_TAP = 6 * 1024;                       // [64 rows W hi|lo][32 rows of W hi] x 64 B
+constexpr int FW2_WBYTES = 9 * FW2_B_TAP;                 // 54 KB per CTA
+constexpr int FW2_STAGES = 3;
+constexpr int FW2_SMEM = 1024 + FW2_WBYTES + FW2_STAGES * FW_STAGE + FW_EPI_BYTES + 256;
+constexpr uint32_t FW2_IDESC = tc::idesc_f16(256, C2);
+constexpr uint32_t FW2_IDESC2 = tc::idesc_f16(256, 2 * C2);
+constexpr int FW2_MAXS = 16;                              // samples per pair (G <= B <= GMAX)
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FW_THREADS, 1) conv2_fwd_tc2_kernel(
+    const __grid_constant__ CUtensorMap tm_hi, const __grid_constant__ CUtensorMap tm_lo,
+    const uint8_t* __restrict__ wimg, const float* __restrict__ wscale, int shared_weights,
+    const int64_t* __restrict__ slot_row, int N, int G, const float* __restrict__ theta,
+    const float* __restrict__ delta, int64_t ld, int B, const float* __restrict__ a1scale,
+    float* __restrict__ pooled, uint8_t* __restrict__ code) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sB = sm;                                        // [9][6 KB]
+  uint8_t* sA = sB + FW2_WBYTES;                           // [stages][hi | lo band]
+  uint8_t* sP = sA + FW2_STAGES * FW_STAGE;                 // [2][64 ch][66] x-pooled outputs
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + FW_EPI_BYTES);
+  uint64_t* full = bars;                 // [stages] leader: both CTAs' bands landed (2 arrivals + bytes)
+  uint64_t* empty = full + FW2_STAGES;    // [stages] per CTA: the pair's MMAs are done with the stage
+  uint64_t* tfull = empty + FW2_STAGES;   // [2] per CTA: accumulator ready
+  uint64_t* tempty = tfull + 2;          // [2] leader: both CTAs drained the accumulator
+  uint64_t* bfull = tempty + 2;          // per CTA: this CTA's weight half landed
+  uint64_t* bready = bfull + 1;          // leader: the peer's weight half landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bready + 1);
+  __shared__ float bias[C2];
+  __shared__ int s_list[FW2_MAXS];
+  __shared__ int s_ns;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = tc::cluster_ctarank();
+  const int g = blockIdx.x >> 1;  // pair index
+  const int n0 = g * G;
+  {  // nothing to do: both CTAs of the pair see the same slots and leave together
+    bool any = false;
+    for (int b = 0; b < G && n0 + b < N; ++b) any |= slot_row[n0 + b] >= 0;
+    if (!any) return;
+  }
+  const int wg = shared_weights ? 0 : n0 / B;
+  const float* dc = delta ? delta + (int64_t)wg * ld : nullptr;
+  if (threadIdx.x < C2) bias[threadIdx.x] = wt(theta, dc, O_B2 + threadIdx.x);
+  if (threadIdx.x == 0) {
+    int ns = 0;
+    for (int b = 0; b < G && n0 + b < N; ++b)
+      if (slot_row[n0 + b] >= 0) s_list[ns++] = n0 + b;
+    s_ns = ns;
+    for (int i = 0; i < FW2_STAGES; ++i) {
+      tc::mbar_init(&full[i], 2);
+      tc::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&tfull[i], 1);
+      tc::mbar_init(&tempty[i], 2 * FW_EPI_WARPS);
+    }
+    tc::mbar_init(bfull, 1);
+    tc::mbar_init(bready, 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc2<2 * FW_ACC>(tmem_slot);
+  tc::tc_fence_before();
+  tc::cluster_sync();  // barriers of both CTAs initialised, TMEM allocated in both
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int T = s_ns * FW_TILES;       // tiles of the pair
+  const int steps = (T + 1) >> 1;      // pair steps (the peer's last tile is a dummy when T is odd)
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tc::tma_prefetch(&tm_hi);
+      tc::tma_prefetch(&tm_lo);
+      // this CTA's weight half: per tap [W hi (leader) | W lo (peer)] and rows 32*rank .. +31 of W hi
+      tc::mbar_arrive_expect_tx(bfull, FW2_WBYTES);
+      const uint8_t* wsrc = wimg + (int64_t)wg * WIMG_BYTES;
+      for (int tap = 0; tap < 9; ++tap) {
+        tc::bulk_load(sB + tap * FW2_B_TAP, wsrc + (tap * 2 + rank) * FW_B_TAP, FW_B_TAP, bfull);
+        tc::bulk_load(sB + tap * FW2_B_TAP + FW_B_TAP, wsrc + tap * 2 * FW_B_TAP + rank * (FW_B_TAP / 2),
+                      FW_B_TAP / 2, bfull);
+      }
+      const uint32_t lead_full0 = tc::mapa_shared(tc::smem_u32(full), 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int k = 0; k < steps; ++k) {
+        const int ti = min(2 * k + (int)rank, T - 1);  // (a dummy tile re-reads the last band)
+        const int n = s_list[ti / FW_TILES], t = ti - (ti / FW_TILES) * FW_TILES;
+        tc::mbar_wait(&empty[stage], phase ^ 1);
+        const uint32_t fb = lead_full0 + stage * 8;
+        tc::mbar_arrive_expect_tx_cluster(fb, 2 * FW_A_TX);
+        uint8_t* st_ = sA + stage * FW_STAGE;
+        tc::tma_load_4d_2sm(st_, &tm_hi, 0, 0, FW_ROWS * t, n, fb);
+        tc::tma_load_4d_2sm(st_ + FW_A, &tm_lo, 0, 0, FW_ROWS * t, n, fb);
+        if (++stage == FW2_STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 1) {  // tell the leader this CTA's weight half is resident
+      tc::mbar_wait(bfull, 0);
+      if (lane == 0) tc::mbar_arrive_cluster(tc::mapa_shared(tc::smem_u32(bready), 0));
+    } else {
+      tc::mbar_wait(bfull, 0);
+      tc::mbar_wait(bready, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      const uint32_t sA0 = tc::smem_u32(sA), sB0 = tc::smem_u32(sB);
+      for (int k = 0; k < steps; ++k) {
+        const int acc = k & 1;
+        tc::mbar_wait(&tempty[acc], ((k >> 1) & 1) ^ 1);
+        tc::tc_fence_after();
+        const uint32_t d = tmem + acc * FW_ACC;
+        tc::mbar_wait(&full[stage], phase);
+        tc::tc_fence_after();
+        if (tc::elect_one()) {
+#pragma unroll
+          for (int tap = 0; tap < 9; ++tap) {
+            const uint32_t ah = sA0 + stage * FW_STAGE + ((tap / 3) * S1 + tap % 3) * 64, al = ah + FW_A;
+            const uint32_t b1 = sB0 + tap * FW2_B_TAP, b2 = b1 + FW_B_TAP;
+            tc::mma2p_f16_ks2(d, d + C2, tc::sdesc(ah, 16, 512, 4), tc::sdesc(al, 16, 512, 4),
+                              tc::sdesc(b1, 16, 512, 4), tc::sdesc(b2, 16, 512, 4), FW2_IDESC2, FW2_IDESC,
+                              tap != 0);
+          }
+          tc::mma_commit2_mc(&empty[stage], 3);
+          tc::mma_commit2_mc(&tfull[acc], 3);
+        }
+        __syncwarp();
+        if (++stage == FW2_STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else {
+    // epilogue: as conv2_fwd_tc_kernel, on this CTA's tile 2k + rank of every pair step
+    const int q = warp & 3, cg = (warp - 2) >> 2;
+    const int row = q * 32 + lane;
+    const int et = threadIdx.x - 64;
+    const float ws = wscale[wg];
+    const uint32_t sE0 = tc::smem_u32(sP);
+    const uint32_t lead_tempty0 = tc::mapa_shared(tc::smem_u32(tempty), 0);
+    for (int k = 0; k < steps; ++k) {
+      const int acc = k & 1;
+      const int ti = 2 * k + (int)rank;
+      const bool real = ti < T;
+      const int n = real ? s_list[ti / FW_TILES] : 0, t = ti - (ti / FW_TILES) * FW_TILES;
+      const uint32_t sE = sE0 + acc * (C2 * FW_XLD * 4);
+      tc::mbar_wait(&tfull[acc], (k >> 1) & 1);
+      tc::tc_fence_after();
+      uint32_t v0[16], v1[16];
+      if (real) {
+        const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + acc * FW_ACC + cg * 16;
+        tc::tmem_ld16(base, v0);
+        tc::tmem_ld16(base + C2, v1);
+        tc::tmem_ld_wait();
+      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive_cluster(lead_tempty0 + acc * 8);  // accumulator drained (pair-wide)
+      if (!real) continue;  // (uniform across the CTA: no named barrier below for a dummy tile)
+      const float inv = 1.f / (a1scale[n] * ws);  // exact: powers of two
+      {
+        float v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          v[j] = fmaxf(fmaf(__uint_as_float(v0[j]) + __uint_as_float(v1[j]), inv, bias[cg * 16 + j]), 0.f);
+        const bool odd = lane & 1;
+        const uint32_t dst = sE + ((cg * 16 + (odd ? 8 : 0)) * FW_XLD + (row >> 1)) * 4;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float mine = odd ? v[8 + j] : v[j];
+          const float other = __shfl_xor_sync(0xffffffffu, odd ? v[j] : v[8 + j], 1);
+          const float a = odd ? other : mine, b = odd ? mine : other;
+          const bool win = b > a;
+          tc::sts_f32(dst + j * FW_XLD * 4, __int_as_float(__float_as_int(win ? b : a) | ((int)win << 31)));
+        }
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(FW_EPI_WARPS * 32) : "memory");
+      float* pout = pooled + (int64_t)n * FLAT;
+      uint8_t* cout = code + (int64_t)n * FLAT;
+      for (int it = et; it < C2 * 2 * SP; it += FW_EPI_WARPS * 32) {
+        const int ch = it / (2 * SP), pp = it - ch * (2 * SP), pr = pp >= SP, px = pp - pr * SP;
+        const uint32_t e0 = sE + (ch * FW_XLD + pr * S1 + px) * 4;
+        const float ta = tc::lds_f32(e0), tb = tc::lds_f32(e0 + (S1 / 2) * 4);
+        const float a = fabsf(ta), b = fabsf(tb);
+        const bool low = b > a;
+        const float best = low ? b : a;
+        const int arg = low ? 2 + (int)signbit(tb) : (int)signbit(ta);
+        const int idx = ch * NPOOL + FW_ROWS / 2 * t * SP + pp;
+        pout[idx] = best;
+        cout[idx] = (uint8_t)arg;
+      }
+    }
+  }
+  tc::tc_fence_before();
+  tc::cluster_sync();  // both CTAs done with the pair's TMEM and barriers
+  tc::tc_fence_after();
+  if (warp == 1) tc::tmem_dealloc2<2 * FW_ACC>(tmem);
+}
+
 // ------------------------------------------------------- fc1 on tcgen05
 // Both fc1 contractions of the factored form run at theta_t, i.e. as plain
 // GEMMs over all slots of the step (kind::f16, 3-term split as above):
@@ -2843,6 +3048,9 @@ __global__ void conv1_bwd_w_reduce_kernel(const float* __restrict__ wpart, int s
 }
 
 int g_conv_impl = 1;  // 1 = tcgen05 (product path), 0 = FP32 CUDA-core kernels (validation)
+// conv2 forward on CTA pairs (conv2_fwd_tc2_kernel): correct (tests) but measured slower
+// than the single-CTA kernel (10.7 vs 7.9 ms per iteration), so off by default
+bool g_conv2_pairs = false;
 
 
 // ------------------------------------------------ conv2 backward-weights (tcgen05)
@@ -3172,6 +3380,7 @@ int set_smem_limits() {
   cudaFuncSetAttribute(conv2_bwd_x_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C2X_SMEM);
   cudaFuncSetAttribute(conv2_bwd_w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C2W_SMEM);
   cudaFuncSetAttribute(conv2_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FW_SMEM);
+  cudaFuncSetAttribute(conv2_fwd_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FW2_SMEM);
   cudaFuncSetAttribute(conv2_bwd_x_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BX_SMEM);
   cudaFuncSetAttribute(dz2_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DZB_SMEM);
   cudaFuncSetAttribute(fc1_bwd_fact_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, FC1F_SMEM);
@@ -3243,9 +3452,14 @@ int forward(const float* X, const float* theta, const float* delta, int64_t ld, 
     if (!st) st = a1f_tensor_map(&ml, w.a1fl, N, S1, FW_BAND);
     if (st) return st;
     const int gt = delta ? B / client_split(active, B, 1) : 8;  // samples per CTA
-    FB_LAUNCH("conv2_fwd_tc_kernel", s, conv2_fwd_tc_kernel<<<(N + gt - 1) / gt, FW_THREADS, FW_SMEM, s>>>(
-          mh, ml, w.wimg, w.wscale, delta ? 0 : 1, w.slot_row, N, gt, theta, delta, ld, B, w.a1scale, w.pooled,
-          w.code));
+    if (g_conv2_pairs)  // one CTA pair per former CTA's samples (cluster dims 2)
+      FB_LAUNCH("conv2_fwd_tc_kernel", s, conv2_fwd_tc2_kernel<<<2 * ((N + gt - 1) / gt), FW_THREADS, FW2_SMEM, s>>>(
+            mh, ml, w.wimg, w.wscale, delta ? 0 : 1, w.slot_row, N, gt, theta, delta, ld, B, w.a1scale, w.pooled,
+            w.code));
+    else
+      FB_LAUNCH("conv2_fwd_tc_kernel", s, conv2_fwd_tc_kernel<<<(N + gt - 1) / gt, FW_THREADS, FW_SMEM, s>>>(
+            mh, ml, w.wimg, w.wscale, delta ? 0 : 1, w.slot_row, N, gt, theta, delta, ld, B, w.a1scale, w.pooled,
+            w.code));
   } else {
     FB_LAUNCH("conv2_fwd_pool_kernel", s, conv2_fwd_pool_kernel<<<N, 256, C2F_SMEM, s>>>(w.a1, nullptr, w.slot_row, theta, delta, ld, B, w.pooled, w.code));
   }
@@ -3297,8 +3511,10 @@ int fb_debug_prof(unsigned long long* out) {  // timing experiments only
 #endif
 
 int fb_cnn_set_conv_impl(int impl) {
-  FB_REQUIRE(impl == 0 || impl == 1, "fb_cnn_set_conv_impl: 0 (FP32 CUDA cores) or 1 (tcgen05)");
-  fb::cnn::g_conv_impl = impl;
+  FB_REQUIRE(impl >= 0 && impl <= 2,
+             "fb_cnn_set_conv_impl: 0 (FP32 CUDA cores), 1 (tcgen05) or 2 (tcgen05, CTA-pair conv2 forward)");
+  fb::cnn::g_conv_impl = impl == 0 ? 0 : 1;
+  fb::cnn::g_conv2_pairs = impl == 2;
   return FB_OK;
 }
 

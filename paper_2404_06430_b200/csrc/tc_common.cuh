@@ -335,6 +335,77 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
+// ------------------------------------------------------ CTA pairs (cta_group::2)
+// The two CTAs of a 2-CTA cluster run one M = 256 MMA: A rows 0-127 come from
+// CTA 0's shared memory, rows 128-255 from CTA 1's (same offsets), B is split
+// along N (CTA 0 holds the first N/2 rows), each CTA's TMEM holds its 128 rows.
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same smem offset in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx_cluster(uint32_t cluster_addr, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(cluster_addr),
+               "r"(bytes)
+               : "memory");
+}
+// 4-D tiled load into this CTA's smem, completion bytes counted on an mbarrier of
+// either CTA of the pair (the leader's, for the pair's MMA issuer)
+__device__ __forceinline__ void tma_load_4d_2sm(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                                uint32_t bar_cluster_addr) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], "
+      "[%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar_cluster_addr)
+      : "memory");
+}
+template <uint32_t kCols>
+__device__ __forceinline__ void tmem_alloc2(uint32_t* dst_smem) {  // one warp of EACH CTA (same warp id)
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "n"(kCols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+template <uint32_t kCols>
+__device__ __forceinline__ void tmem_dealloc2(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols) : "memory");
+}
+// arrive on `bar` (same offset) in every CTA of `mask` once the pair's MMAs complete
+__device__ __forceinline__ void mma_commit2_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::
+                   "r"(smem_u32(bar)),
+               "h"(mask)
+               : "memory");
+}
+// M = 256 pair MMAs of the 3-term split for KS = 2 K steps: d[0, 2N) += ah * b1 (b1 = the
+// CTA halves of [W hi; W lo]), d[N, 2N) += al * b2 (b2 = halves of W hi)
+__device__ __forceinline__ void mma2p_f16_ks2(uint32_t d, uint32_t dcross, uint64_t ah, uint64_t al, uint64_t b1,
+                                              uint64_t b2, uint32_t idesc2n, uint32_t idescn, uint32_t pacc) {
+  asm volatile(
+      "{\n\t.reg .pred pa, pt;\n\t.reg .b64 a1, c1, e1, f1;\n\t"
+      "setp.ne.b32 pa, %8, 0;\n\t"
+      "setp.eq.b32 pt, %6, %6;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %2, %4, %6, pa;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%1], %3, %5, %7, pt;\n\t"
+      "add.s64 a1, %2, 2;\n\tadd.s64 c1, %3, 2;\n\tadd.s64 e1, %4, 2;\n\tadd.s64 f1, %5, 2;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], a1, e1, %6, pt;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%1], c1, f1, %7, pt;\n}" ::"r"(d),
+      "r"(dcross), "l"(ah), "l"(al), "l"(b1), "l"(b2), "r"(idesc2n), "r"(idescn), "r"(pacc)
+      : "memory");
+}
+
 // generic-proxy smem writes -> visible to the async proxy (TMA / tensor core)
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

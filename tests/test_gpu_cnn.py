@@ -121,7 +121,7 @@ def test_cnn_tcgen05_conv_matches_cuda_core_kernels():
     args = (dev(pop.row_start), dev(pop.num_rows), dev(np.concatenate(perms).astype(np.int32)), dev(perm_off))
     out = {}
     try:
-        for impl in (0, 1):
+        for impl in (0, 1, 2):  # FP32 CUDA cores / tcgen05 / tcgen05 with the CTA-pair conv2 forward
             native.call("fb_cnn_set_conv_impl", impl)
             runner = fb.engine._ModelRunner(m, fb.device.Workspace(theta.device))
             C = len(sizes)
@@ -135,6 +135,9 @@ def test_cnn_tcgen05_conv_matches_cuda_core_kernels():
             out[impl] = (delta[:, :runner.D].double().cpu().numpy(), loss.cpu().numpy(), corr.cpu().numpy())
     finally:
         native.call("fb_cnn_set_conv_impl", 1)
+    np.testing.assert_allclose(out[2][1], out[0][1], rtol=1e-5)
+    np.testing.assert_allclose(out[1][1], out[2][1], rtol=1e-6)  # the two tcgen05 conv2 forwards agree
+    np.testing.assert_allclose(out[1][0], out[2][0], rtol=1e-5, atol=1e-7)
     np.testing.assert_allclose(out[1][1], out[0][1], rtol=1e-5)
     assert np.abs(out[1][2] - out[0][2]).max() <= 1
     for c in range(len(sizes)):
