@@ -299,6 +299,7 @@ class GpuSimulationEngine:
         self._pf: dict = {}
         self._pf_bufs: dict = {}
         self._pf_done: dict = {}
+        self._pf_pending = None
         self._plans: dict = {}      # host plans computed ahead (key: population, seed, cohort size, epochs)
         self._planned: set = set()
 
@@ -329,9 +330,10 @@ class GpuSimulationEngine:
             state.params = DeviceParams.from_host(state.params, self.device)
         aggregates, metrics, cohorts, updates = [], {}, [], []
         if self._prefetch and contexts:
-            # issue iteration t+1's cohort-row copy now, so it runs beside this iteration's
-            # kernels (run_iteration blocks on its per-client results further down)
-            self._prefetch_next(algorithm, state, contexts[0].iteration + 1)
+            # iteration t+1's cohort-row copy is issued by the first context once its own
+            # kernels are queued (the host work then overlaps them), so it runs beside this
+            # iteration's kernels (run_iteration blocks on its per-client results further down)
+            self._pf_pending = (algorithm, state, contexts[0].iteration + 1)
         for ctx in contexts:
             agg, ctx_metrics, cohort, ctx_updates = self._run_context(algorithm, state, ctx)
             if ctx_updates:
@@ -342,12 +344,18 @@ class GpuSimulationEngine:
                 key = (pop, name)
                 metrics[key] = metrics[key] + val if key in metrics else val
             cohorts.append((pop, cohort))
+        self._issue_prefetch()
         if self._prefetch and contexts:
             done = _torch().cuda.Event()
             done.record(self.stream)  # every kernel of iteration t that reads its prefetched rows is before this
             self._pf_done[contexts[0].iteration & 1] = done
             self._pf.pop(contexts[0].iteration, None)
         return IterationResult(tuple(aggregates), metrics, updates, tuple(cohorts))
+
+    def _issue_prefetch(self) -> None:
+        pending, self._pf_pending = self._pf_pending, None
+        if pending is not None:
+            self._prefetch_next(*pending)
 
     def _prefetch_next(self, algorithm, state, t: int) -> None:
         """Gather iteration t's cohort rows (host-resident dataset) on the copy
@@ -592,6 +600,7 @@ class GpuSimulationEngine:
         correct, clipped, nonfinite = ints[:Cp], ints[Cp:2 * Cp], ints[2 * Cp:3 * Cp]
         if C:
             runner.eval(theta.flat, pop, d_row_start, d_num_rows, C, loss, correct, stream, num_rows)
+        self._issue_prefetch()  # next iteration's rows: host work now overlaps the queued kernels
 
         agg_flat = None
         updates = None
