@@ -156,7 +156,19 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
                          double* fc1_sumsq, const float* control /* nullable [C, ld_control]: c - c_i */,
                          int64_t ld_control,
                          const int32_t* h_client_steps /* nullable HOST [C]: local steps per client */,
-                         void* stream);
+                         int fc1_store, void* stream);
+/* fc1_store = 0 (factored tcgen05 form, one wave of clients, fc1_sumsq set):
+ * the clients' fc1 weight-delta blocks [O_F1, O_BF1) are NOT materialised --
+ * fc1_sumsq still receives their sums of squares (for the clip norms) and
+ * fb_cnn_fc1_aggregate_f32 then forms sum_c coef[c] * delta_c over that block
+ * straight from the low-rank history left in the workspace (K3 for the fc1
+ * block; replaces the fc1 part of SumAggregator.accumulate,
+ * fedsim/engine/aggregator.py:39-44).  Call it after this function with the
+ * same workspace and arguments, before the workspace is reused; agg_fc1 is
+ * the [12544 x 128] fc1 block of the aggregate (overwritten).                */
+int fb_cnn_fc1_aggregate_f32(const float* coef, int num_clients, int batch_size, int max_steps, float lr,
+                             float prox_mu, int max_slots, int hist_steps, void* workspace,
+                             int64_t workspace_bytes, float* agg_fc1, void* stream);
 
 /* ------------------------------------------------------- data movement
  * Copy each cohort client's contiguous rows (num_rows[c] rows of row_bytes

@@ -50,11 +50,14 @@ FC1_LO, FC1_HI = 19392, 19392 + 12544 * 128
 
 
 def local_sgd_cohort(runner, theta, pop, row_start, num_rows, perms, perm_off, C, tp, prox_mu, delta, nonfinite,
-                     stream, h_num_rows, control=None):
+                     stream, h_num_rows, control=None, defer_fc1=False):
     """Returns the per-client fc1-block sum of squares (fp64 device [C]) when the
     factored tcgen05 path produced it, else None (K2 then scans the whole row).
     ``control`` ([C, ld] device, c - c_i per client; SCAFFOLD) selects the dense
-    fc1 form: a per-client dense control term has no low-rank history."""
+    fc1 form: a per-client dense control term has no low-rank history.
+    ``defer_fc1``: when the factored form runs in one wave, leave the clients'
+    fc1 blocks unmaterialised and record the call in ``runner.fc1_pending`` for
+    :func:`fc1_aggregate` (the engine's K3 for that block)."""
     B = tp.batch_size
     n = np.asarray(h_num_rows, dtype=np.int64)
     steps = np.ascontiguousarray(tp.num_epochs * ((n + B - 1) // B), dtype=np.int32)  # host, per client
@@ -68,11 +71,23 @@ def local_sgd_cohort(runner, theta, pop, row_start, num_rows, perms, perm_off, C
         import torch
 
         sq = runner.ws.tensor("cnn_fc1_sumsq", (max(C, 1),), torch.float64)
+    defer = bool(defer_fc1 and sq is not None and 0 < C <= slots // B)
+    runner.fc1_pending = (dict(C=C, B=B, max_steps=max_steps, lr=float(tp.learning_rate), mu=float(prox_mu),
+                               slots=slots, hist=hist, ws=ws) if defer else None)
     native.call("fb_local_sgd_cnn_f32", native.ptr(theta), native.ptr(pop.X), native.ptr(pop.y),
                 native.ptr(row_start), native.ptr(num_rows), native.ptr(perms), native.ptr(perm_off), C,
                 tp.num_epochs, B, max_steps, float(tp.learning_rate), float(prox_mu), native.ptr(delta),
                 runner.ld, native.ptr(nonfinite), slots, hist, native.ptr(ws), ws.numel(),
                 native.ptr(sq) if sq is not None else None,
                 native.ptr(control) if control is not None else None,
-                control.stride(0) if control is not None else 0, steps.ctypes.data, stream)
+                control.stride(0) if control is not None else 0, steps.ctypes.data, 0 if defer else 1, stream)
     return sq
+
+
+def fc1_aggregate(runner, coef, agg_fc1, stream) -> None:
+    """agg_fc1[k, h] = sum_c coef[c] * delta_c[k, h] over the fc1 weight block of the
+    deferred local-SGD call (runner.fc1_pending), from its low-rank history."""
+    p = runner.fc1_pending
+    runner.fc1_pending = None
+    native.call("fb_cnn_fc1_aggregate_f32", native.ptr(coef), p["C"], p["B"], p["max_steps"], p["lr"], p["mu"],
+                p["slots"], p["hist"], native.ptr(p["ws"]), p["ws"].numel(), native.ptr(agg_fc1), stream)

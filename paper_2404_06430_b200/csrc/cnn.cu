@@ -2133,7 +2133,7 @@ int hist_tensor_map(CUtensorMap* map, const __half* base, int N, int S, int B) {
 __global__ void __launch_bounds__(FMT_THREADS, 1) fc1_mat_tc_kernel(
     const __grid_constant__ CUtensorMap tm_hi, const __grid_constant__ CUtensorMap tm_lo, Hist hs,
     const float* __restrict__ pscale_hist, int N, int S, int B, float lr, float mu, float* __restrict__ delta,
-    int64_t ld, double* __restrict__ sumsq_part) {
+    int64_t ld, double* __restrict__ sumsq_part, int store) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sB = sm;                                  // [U hi blk0 | U hi blk1 | U lo blk0 | U lo blk1]
@@ -2159,6 +2159,10 @@ __global__ void __launch_bounds__(FMT_THREADS, 1) fc1_mat_tc_kernel(
   __syncthreads();
   const int Sc = s_sc;
   if (Sc == 0) {  // the client never trained (no rows): its fc1 delta block is zero (zero_delta skipped it)
+    if (!store) {
+      if (sumsq_part && t == 0) sumsq_part[(int64_t)c * gridDim.y + blockIdx.y] = 0.0;
+      return;
+    }
     float4* z = reinterpret_cast<float4*>(delta + (int64_t)c * ld + O_F1 + (int64_t)t0 * FMT_TILE * HID);
     for (int i = t; i < nt * FMT_TILE * HID / 4; i += FMT_THREADS) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     return;
@@ -2281,6 +2285,17 @@ __global__ void __launch_bounds__(FMT_THREADS, 1) fc1_mat_tc_kernel(
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(&tempty[acc]);
         }
+        if (!store) {  // squares only (the factored aggregate never materialises the block):
+          // four independent fp32 chains of 8 per half, then one fp64 add
+          float q4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float z = (__uint_as_float(v0[j]) + __uint_as_float(v1[j])) * inv;
+            q4[j & 3] = fmaf(z, z, q4[j & 3]);
+          }
+          sq += (double)((q4[0] + q4[1]) + (q4[2] + q4[3]));
+          continue;
+        }
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const float z = (__uint_as_float(v0[j]) + __uint_as_float(v1[j])) * inv;
@@ -2316,6 +2331,221 @@ __global__ void __launch_bounds__(FMT_THREADS, 1) fc1_mat_tc_kernel(
     sumsq_part[(int64_t)c * gridDim.y + blockIdx.y] = tot;
   }
   if (warp == 1) tc::tmem_dealloc<512>(tmem);
+}
+
+// ------------------------------------------- factored fc1 aggregate (tcgen05)
+// K3 for the fc1 weight block without materialising any client's delta:
+//   agg[k][h] = sum_c coef_c delta_c[k][h] = sum_c sum_j p_cj[k] U'_cj[h],
+//   U'_cj = coef_c * hist_coef_j * dz3_cj / pscale_cj,
+// one GEMM with M = k (98 tiles of 128), N = h (128) and K = every history row of
+// the cohort.  U' is built once per client (fp16 hi / lo with ONE cohort-wide
+// power-of-two scale so clients accumulate in the same TMEM tile) and streamed by
+// TMA with the pooled-history tiles; a CTA owns one k tile and a chunk of clients,
+// drains its accumulator every FAG_DRAIN clients (32-step chains) into fp32
+// registers and writes a per-chunk partial; fc1_agg_reduce_kernel sums the chunks in
+// fixed order.  Reads 2.5 GB of history instead of writing + re-reading the 6.4 GB of
+// per-client fc1 deltas.  (Clip norms come from fc1_mat_tc_kernel in squares-only mode.)
+constexpr int FAG_CHUNKS = 8;                          // client chunks (grid.y)
+constexpr int FAG_DRAIN = 8;                           // clients per TMEM accumulation chain
+constexpr int FAG_UBYTES = 4 * FMT_BLK;                // U' hi blk0 | blk1 | lo blk0 | blk1 (32 KB)
+constexpr int FAG_STAGE = FMT_STAGE + FAG_UBYTES;      // P tile (32 KB) + U' (32 KB)
+constexpr int FAG_STAGES = 3;
+constexpr int FAG_SMEM = 1024 + FAG_STAGES * FAG_STAGE + 256;
+
+// cohort max |U'| (float bits of a non-negative value compare as unsigned)
+__global__ void __launch_bounds__(256) fc1_umax_kernel(Hist hs, const float* __restrict__ pscale_hist,
+                                                       const float* __restrict__ coef, int N, int S, int B,
+                                                       float lr, float mu, unsigned* __restrict__ umax) {
+  const int c = blockIdx.x;
+  int Sc = 0;
+  while (Sc < S && hs.nbh[Sc * hs.cstride + c] > 0) ++Sc;
+  float m = 0.f;
+  const float k = coef[c];
+  for (int i = threadIdx.x; i < S * B * HID; i += blockDim.x) {
+    const int j = i / HID, h = i - j * HID, sp = j / B, bp = j - sp * B;
+    if (sp < Sc && bp < hs.nbh[sp * hs.cstride + c]) {
+      const int64_t slot = (int64_t)c * B + bp;
+      m = fmaxf(m, fabsf(k * hist_coef(lr, mu, Sc, sp) * hs.dz3h[sp * hs.dstride + slot * HID + h] /
+                         pscale_hist[(int64_t)sp * N + slot]));
+    }
+  }
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0) atomicMax(umax, __float_as_uint(m));
+}
+
+// U' of client c as fp16 hi / lo, [c][hi|lo][64 rows j][128 h] (rows past the client's
+// history and inactive slots zero), scaled by the cohort-wide power of two
+__global__ void __launch_bounds__(256) fc1_ubuild_kernel(Hist hs, const float* __restrict__ pscale_hist,
+                                                         const float* __restrict__ coef, int N, int S, int B,
+                                                         float lr, float mu, const unsigned* __restrict__ umax,
+                                                         __half* __restrict__ u) {
+  const int c = blockIdx.x;
+  int Sc = 0;
+  while (Sc < S && hs.nbh[Sc * hs.cstride + c] > 0) ++Sc;
+  const float m = __uint_as_float(*umax);
+  const float beta = m > 0.f ? exp2f(14.f - ceilf(log2f(m))) : 1.f;
+  const float k = coef[c] * beta;
+  __half* uh = u + (int64_t)c * 2 * FC_RMAX * HID;
+  __half* ul = uh + FC_RMAX * HID;
+  for (int i = threadIdx.x; i < FC_RMAX * HID / 2; i += blockDim.x) {
+    const int j = (2 * i) / HID, h = 2 * i - j * HID, sp = j / B, bp = j - sp * B;
+    float v0 = 0.f, v1 = 0.f;
+    if (j < S * B && sp < Sc && bp < hs.nbh[sp * hs.cstride + c]) {
+      const int64_t slot = (int64_t)c * B + bp;
+      const float f = k * hist_coef(lr, mu, Sc, sp) / pscale_hist[(int64_t)sp * N + slot];
+      v0 = f * hs.dz3h[sp * hs.dstride + slot * HID + h];
+      v1 = f * hs.dz3h[sp * hs.dstride + slot * HID + h + 1];
+    }
+    uint32_t hw, lw;
+    split_f16x2(v0, v1, hw, lw);
+    reinterpret_cast<uint32_t*>(uh)[i] = hw;
+    reinterpret_cast<uint32_t*>(ul)[i] = lw;
+  }
+}
+
+__global__ void __launch_bounds__(FMT_THREADS, 1) fc1_agg_tc_kernel(
+    const __grid_constant__ CUtensorMap tm_hi, const __grid_constant__ CUtensorMap tm_lo,
+    const __grid_constant__ CUtensorMap tm_u, int C, int S, int B, int chunk, const unsigned* __restrict__ umax,
+    float* __restrict__ part) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = sm;  // [stage][P hi blk0 | blk1 | P lo blk0 | blk1 | U hi blk0 | blk1 | U lo blk0 | blk1]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sA + FAG_STAGES * FAG_STAGE);
+  uint64_t* full = bars;
+  uint64_t* empty = full + FAG_STAGES;
+  uint64_t* tfull = empty + FAG_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, t = threadIdx.x;
+  const int kt = blockIdx.x, c0 = blockIdx.y * chunk, c1 = min(C, c0 + chunk), nc = c1 - c0;
+  const int J = S * B;
+  float* out = part + (int64_t)blockIdx.y * FLAT * HID + (int64_t)kt * FMT_TILE * HID;
+  if (nc <= 0) {  // an empty chunk contributes zeros
+    for (int i = t; i < FMT_TILE * HID / 4; i += FMT_THREADS)
+      reinterpret_cast<float4*>(out)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    return;
+  }
+  for (int st = 0; st < FAG_STAGES; ++st)  // P rows J..63 stay zero (the TMA box fills rows 0..J-1)
+    for (int i = t; i < 4 * (FC_RMAX - J) * 32; i += FMT_THREADS) {
+      const int blk = i / ((FC_RMAX - J) * 32), r = i - blk * (FC_RMAX - J) * 32;
+      reinterpret_cast<uint32_t*>(sA + st * FAG_STAGE + blk * FMT_BLK + J * 128)[r] = 0u;
+    }
+  if (t == 0) {
+    for (int i = 0; i < FAG_STAGES; ++i) {
+      tc::mbar_init(&full[i], 1);
+      tc::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&tfull[i], 1);
+      tc::mbar_init(&tempty[i], FMT_EPI_WARPS);
+    }
+    tc::fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc<512>(tmem_slot);
+  tc::fence_proxy_async();
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int ngroups = (nc + FAG_DRAIN - 1) / FAG_DRAIN;
+  if (warp == 0) {
+    if (lane == 0) {
+      tc::tma_prefetch(&tm_hi);
+      tc::tma_prefetch(&tm_lo);
+      tc::tma_prefetch(&tm_u);
+      const int k0 = kt * FMT_TILE;
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int i = 0; i < nc; ++i) {
+        const int c = c0 + i;
+        tc::mbar_wait(&empty[stage], phase ^ 1);
+        tc::mbar_arrive_expect_tx(&full[stage], 4 * J * 128 + FAG_UBYTES);
+        uint8_t* st_ = sA + stage * FAG_STAGE;
+        tc::tma_load_3d(st_, &tm_hi, k0, c * B, 0, &full[stage]);
+        tc::tma_load_3d(st_ + FMT_BLK, &tm_hi, k0 + 64, c * B, 0, &full[stage]);
+        tc::tma_load_3d(st_ + 2 * FMT_BLK, &tm_lo, k0, c * B, 0, &full[stage]);
+        tc::tma_load_3d(st_ + 3 * FMT_BLK, &tm_lo, k0 + 64, c * B, 0, &full[stage]);
+        uint8_t* su = st_ + FMT_STAGE;
+        tc::tma_load_2d(su, &tm_u, 0, (c * 2) * FC_RMAX, &full[stage]);
+        tc::tma_load_2d(su + FMT_BLK, &tm_u, 64, (c * 2) * FC_RMAX, &full[stage]);
+        tc::tma_load_2d(su + 2 * FMT_BLK, &tm_u, 0, (c * 2 + 1) * FC_RMAX, &full[stage]);
+        tc::tma_load_2d(su + 3 * FMT_BLK, &tm_u, 64, (c * 2 + 1) * FC_RMAX, &full[stage]);
+        if (++stage == FAG_STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    int stage = 0;
+    uint32_t phase = 0;
+    const uint32_t sA0 = tc::smem_u32(sA);
+    for (int i = 0; i < nc; ++i) {
+      const int grp = i / FAG_DRAIN, acc = grp & 1;
+      const bool first = i % FAG_DRAIN == 0, last = i % FAG_DRAIN == FAG_DRAIN - 1 || i == nc - 1;
+      if (first) {
+        tc::mbar_wait(&tempty[acc], ((grp >> 1) & 1) ^ 1);
+        tc::tc_fence_after();
+      }
+      tc::mbar_wait(&full[stage], phase);
+      tc::tc_fence_after();
+      if (tc::elect_one()) {
+        const uint32_t d = tmem + acc * 256;
+        const uint32_t ah = sA0 + stage * FAG_STAGE, al = ah + 2 * FMT_BLK, bu = ah + FMT_STAGE;
+#pragma unroll
+        for (int ks = 0; ks < FC_RMAX / 16; ++ks) {
+          const uint64_t adh = tc::sdesc(ah + ks * 2048, FMT_BLK, 1024, 2);
+          const uint64_t adl = tc::sdesc(al + ks * 2048, FMT_BLK, 1024, 2);
+          const uint64_t bd = tc::sdesc(bu + ks * 2048, FMT_BLK, 1024, 2);
+          tc::mma2_f16(d, d + HID, adh, adl, bd, FMT_IDESC2, FMT_IDESC, !first || ks != 0);
+        }
+        tc::mma_commit(&empty[stage]);
+        if (last) tc::mma_commit(&tfull[acc]);
+      }
+      __syncwarp();
+      if (++stage == FAG_STAGES) { stage = 0; phase ^= 1; }
+    }
+  } else {
+    const int q = warp & 3, hh = (warp - 2) >> 2;  // TMEM lane quadrant (k rows), h half
+    float run[64];
+#pragma unroll
+    for (int j = 0; j < 64; ++j) run[j] = 0.f;
+    for (int grp = 0; grp < ngroups; ++grp) {
+      const int acc = grp & 1;
+      tc::mbar_wait(&tfull[acc], (grp >> 1) & 1);
+      tc::tc_fence_after();
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + acc * 256 + hh * 64 + half * 32;
+        uint32_t v0[32], v1[32];
+        tc::tmem_ld32(base, v0);
+        tc::tmem_ld32(base + HID, v1);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) run[half * 32 + j] += __uint_as_float(v0[j]) + __uint_as_float(v1[j]);
+      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+    }
+    const float m = __uint_as_float(*umax);
+    const float inv = m > 0.f ? 1.f / exp2f(14.f - ceilf(log2f(m))) : 1.f;  // exact: power of two
+    float4* o4 = reinterpret_cast<float4*>(out + (int64_t)(q * 32 + lane) * HID + hh * 64);
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      o4[j] = make_float4(run[4 * j] * inv, run[4 * j + 1] * inv, run[4 * j + 2] * inv, run[4 * j + 3] * inv);
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  if (warp == 1) tc::tmem_dealloc<512>(tmem);
+}
+
+// agg[e] = sum over the client chunks of their partials (fixed order, fp64)
+__global__ void fc1_agg_reduce_kernel(const float* __restrict__ part, int nchunks, float* __restrict__ agg) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)FLAT * HID;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double a = 0.0;
+    for (int k = 0; k < nchunks; ++k) a += part[(int64_t)k * FLAT * HID + e];
+    agg[e] = (float)a;
+  }
 }
 
 // the same sum by a pass over the materialised block (FP32 CUDA-core validation path)
@@ -3295,6 +3525,9 @@ struct Work {
   __half *pfh, *pfl, *dz3fh, *dz3fl, *thTh, *thTl, *thh, *thl;  // tcgen05 fc1 operands
   float *pscale, *dz3scale, *tscale;
   unsigned* tmax;
+  unsigned* umax;     // factored fc1 aggregate: cohort max |U'|
+  __half* uprime;     // [Cmax][hi|lo][FC_RMAX][HID]
+  float* aggpart;     // [FAG_CHUNKS][FLAT][HID]
   __half *a1fh, *a1fl, *dzfh, *dzfl;
   uint8_t* code;
   uint8_t* wimg;  // per-group conv2 weight images (tcgen05 B operand)
@@ -3325,7 +3558,9 @@ inline int64_t carve(void* base, int N, int Cmax, int H, Work* w) {
                 o_pfh = take(2LL * hs * N * FLAT), o_pfl = take(2LL * hs * N * FLAT), o_dz3fh = take(2LL * N * HID),
                 o_dz3fl = take(2LL * N * HID), o_thTh = take(2LL * FLAT * HID), o_thTl = take(2LL * FLAT * HID),
                 o_thh = take(2LL * FLAT * HID), o_thl = take(2LL * FLAT * HID), o_psc = take(4LL * hs * N),
-                o_dz3sc = take(4LL * N), o_tsc = take(16);
+                o_dz3sc = take(4LL * N), o_tsc = take(16),
+                o_u = H > 0 ? take(2LL * Cmax * 2 * FC_RMAX * HID) : 0,          // factored aggregate: U' hi / lo
+                o_agp = H > 0 ? take(4LL * FAG_CHUNKS * FLAT * HID) : 0;         // its per-chunk partials
   if (w && base) {
     char* b = static_cast<char*>(base);
     w->slot_row = reinterpret_cast<int64_t*>(b + o_row);
@@ -3359,6 +3594,9 @@ inline int64_t carve(void* base, int N, int Cmax, int H, Work* w) {
     w->dz3scale = reinterpret_cast<float*>(b + o_dz3sc);
     w->tscale = reinterpret_cast<float*>(b + o_tsc);
     w->tmax = reinterpret_cast<unsigned*>(b + o_tsc + 4);
+    w->umax = reinterpret_cast<unsigned*>(b + o_tsc + 8);
+    w->uprime = H > 0 ? reinterpret_cast<__half*>(b + o_u) : nullptr;
+    w->aggpart = H > 0 ? reinterpret_cast<float*>(b + o_agp) : nullptr;
     w->pooled = reinterpret_cast<float*>(b + o_pool);
     w->code = reinterpret_cast<uint8_t*>(b + o_code);
     w->part = reinterpret_cast<float*>(b + o_part);
@@ -3381,6 +3619,7 @@ int set_smem_limits() {
   cudaFuncSetAttribute(conv2_bwd_w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C2W_SMEM);
   cudaFuncSetAttribute(conv2_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FW_SMEM);
   cudaFuncSetAttribute(conv2_fwd_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FW2_SMEM);
+  cudaFuncSetAttribute(fc1_agg_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FAG_SMEM);
   cudaFuncSetAttribute(conv2_bwd_x_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BX_SMEM);
   cudaFuncSetAttribute(dz2_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DZB_SMEM);
   cudaFuncSetAttribute(fc1_bwd_fact_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, FC1F_SMEM);
@@ -3510,6 +3749,49 @@ int fb_debug_prof(unsigned long long* out) {  // timing experiments only
 }
 #endif
 
+int fb_cnn_fc1_aggregate_f32(const float* coef, int num_clients, int batch_size, int max_steps, float lr,
+                             float prox_mu, int max_slots, int hist_steps, void* workspace, int64_t workspace_bytes,
+                             float* agg_fc1, void* stream) {
+  using namespace fb::cnn;
+  FB_REQUIRE(num_clients >= 1 && batch_size >= 1 && batch_size <= GMAX && max_steps >= 1 && hist_steps >= max_steps &&
+                 hist_steps * batch_size <= FC_RMAX && max_slots >= batch_size,
+             "cnn_fc1_aggregate: bad arguments");
+  const int per = max_slots / batch_size;
+  FB_REQUIRE(num_clients <= per, "cnn_fc1_aggregate: the cohort must have run as one wave (%d > %d clients)",
+             num_clients, per);
+  FB_REQUIRE(workspace_bytes >= carve(nullptr, max_slots, per, hist_steps, nullptr),
+             "cnn_fc1_aggregate: workspace too small");
+  int st = set_smem_limits();
+  if (st) return st;
+  cudaStream_t s = fb::as_stream(stream);
+  Work w;
+  carve(workspace, max_slots, per, hist_steps, &w);
+  const int B = batch_size, C = num_clients, N = C * B;
+  Hist hs{};
+  hs.phist = w.pooled;
+  hs.pstride = (int64_t)N * FLAT;
+  hs.dz3h = w.dz3;
+  hs.dstride = (int64_t)N * HID;
+  hs.nbh = w.client_nb;
+  hs.cstride = per + 1;
+  cudaMemsetAsync(w.umax, 0, sizeof(unsigned), s);
+  FB_LAUNCH("fc1_umax_kernel", s, fc1_umax_kernel<<<C, 256, 0, s>>>(hs, w.pscale, coef, N, max_steps, B, lr,
+                                                                    prox_mu, w.umax));
+  FB_LAUNCH("fc1_ubuild_kernel", s, fc1_ubuild_kernel<<<C, 256, 0, s>>>(hs, w.pscale, coef, N, max_steps, B, lr,
+                                                                        prox_mu, w.umax, w.uprime));
+  CUtensorMap mh, ml, mu;
+  st = hist_tensor_map(&mh, w.pfh, N, max_steps, B);
+  if (!st) st = hist_tensor_map(&ml, w.pfl, N, max_steps, B);
+  if (!st) st = tensor_map_2d_f16(&mu, w.uprime, HID, (int64_t)C * 2 * FC_RMAX, 64, FC_RMAX);
+  if (st) return st;
+  const int chunk = (C + FAG_CHUNKS - 1) / FAG_CHUNKS;
+  FB_LAUNCH("fc1_agg_tc_kernel", s, fc1_agg_tc_kernel<<<dim3(FMT_TILES, FAG_CHUNKS), FMT_THREADS, FAG_SMEM, s>>>(
+                                        mh, ml, mu, C, max_steps, B, chunk, w.umax, w.aggpart));
+  FB_LAUNCH("fc1_agg_reduce_kernel", s, fc1_agg_reduce_kernel<<<g_num_sms * 4, 256, 0, s>>>(w.aggpart, FAG_CHUNKS,
+                                                                                          agg_fc1));
+  return fb::launch_status("cnn_fc1_aggregate");
+}
+
 int fb_cnn_set_conv_impl(int impl) {
   FB_REQUIRE(impl >= 0 && impl <= 2,
              "fb_cnn_set_conv_impl: 0 (FP32 CUDA cores), 1 (tcgen05) or 2 (tcgen05, CTA-pair conv2 forward)");
@@ -3586,9 +3868,11 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
                          int epochs, int batch_size, int max_steps, float lr, float prox_mu, float* delta_out,
                          int64_t ld_delta, int32_t* nonfinite, int max_slots, int hist_steps, void* workspace,
                          int64_t workspace_bytes, double* fc1_sumsq, const float* control, int64_t ld_control,
-                         const int32_t* h_client_steps, void* stream) {
+                         const int32_t* h_client_steps, int fc1_store, void* stream) {
   FB_REQUIRE(num_clients >= 0 && epochs >= 0 && batch_size >= 1 && max_steps >= 0 && hist_steps >= 0,
              "local_sgd_cnn: bad arguments");
+  FB_REQUIRE(fc1_store || (hist_steps > 0 && fc1_sumsq && g_conv_impl == 1 && num_clients <= max_slots / batch_size),
+             "local_sgd_cnn: fc1_store = 0 needs the factored tcgen05 form, fc1_sumsq and one wave of clients");
   FB_REQUIRE(!control || (hist_steps == 0 && ld_control >= D && (ld_control & 3) == 0),
              "local_sgd_cnn: control variates need the dense fc1 form (hist_steps 0) and ld_control >= D, "
              "a multiple of 4");
@@ -3785,7 +4069,7 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
       const int msplit = Cw * FMT_SPLIT >= g_num_sms ? FMT_SPLIT : 7;  // 2 CTAs per client, 7 for a small shard
       FB_LAUNCH("fc1_mat_tc_kernel", s, fc1_mat_tc_kernel<<<dim3(Cw, msplit), FMT_THREADS, FMT_SMEM, s>>>(
                                             mh, ml, hs, w.pscale, N, max_steps, B, lr, prox_mu, dlt, ld_delta,
-                                            fc1_sumsq ? w.gram_part : nullptr));
+                                            fc1_sumsq ? w.gram_part : nullptr, fc1_store));
       if (fc1_sumsq)
         FB_LAUNCH("fc1_sumsq_reduce_kernel", s, fc1_sumsq_reduce_kernel<<<(Cw + 127) / 128, 128, 0, s>>>(
                                                     w.gram_part, msplit, Cw, w.client_nb, fc1_sumsq + c0));

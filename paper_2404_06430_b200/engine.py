@@ -204,10 +204,11 @@ class _ModelRunner:
                     stream)
 
     def local_sgd(self, theta, pop, row_start, num_rows, perms, perm_off, C, tp, prox_mu, delta, nonfinite, stream,
-                  h_num_rows, control=None):
+                  h_num_rows, control=None, defer_fc1=False):
         if self.kind == "cnn":  # returns the fc1-block sum of squares when the factored path made it
             return cnn.local_sgd_cohort(self, theta, pop, row_start, num_rows, perms, perm_off, C, tp,
-                                        prox_mu, delta, nonfinite, stream, h_num_rows, control=control)
+                                        prox_mu, delta, nonfinite, stream, h_num_rows, control=control,
+                                        defer_fc1=defer_fc1)
         fn = f"fb_local_sgd_{self.kind}_f32"
         native.call(fn, native.ptr(theta), *self.dims, native.ptr(pop.X), native.ptr(pop.y),
                     native.ptr(row_start), native.ptr(num_rows), native.ptr(perms), native.ptr(perm_off), C,
@@ -225,6 +226,9 @@ class GpuSimulationEngine:
     over ``world_size`` workers and rank r simulates ``queues[r]``.
     ``central_epilogue``: "rank0" (noise + step on rank 0, broadcast theta)
     or "replicated" (every rank applies the same counter-based noise).
+    ``factored_aggregate`` (CNN): the fc1 block of the aggregate is formed from
+    the clients' low-rank fc1 histories instead of materialised per-client
+    deltas (``fb_cnn_fc1_aggregate_f32``); False keeps the materialising path.
     """
 
     def __init__(
@@ -243,6 +247,7 @@ class GpuSimulationEngine:
         central_epilogue: str = "rank0",
         data_residency: str = "device",
         prefetch: bool = True,
+        factored_aggregate: bool = True,
     ):
         if num_workers < 1:
             raise ValueError("num_workers must be >= 1")
@@ -295,6 +300,8 @@ class GpuSimulationEngine:
         # host-resident data: the next iteration's cohort rows are gathered on a copy
         # stream while this iteration computes (prefetching t+1 during t)
         self._prefetch = bool(prefetch) and data_residency == "host"
+        # CNN: aggregate the fc1 block from the clients' low-rank histories (no per-client materialisation)
+        self._factored_aggregate = bool(factored_aggregate)
         self._copy_stream = torch.cuda.Stream(self.device) if self._prefetch else None
         self._pf: dict = {}
         self._pf_bufs: dict = {}
@@ -620,7 +627,8 @@ class GpuSimulationEngine:
                                 store.ld, native.ptr(d_rows), C, runner.D, native.ptr(control), runner.ld, stream)
                 fc1_sq = runner.local_sgd(theta.flat, pop, d_row_start, d_num_rows, d_perms, d_perm_off, C,
                                           plan.train, plan.prox_mu, delta, nonfinite, stream, num_rows,
-                                          control=control)
+                                          control=control, defer_fc1=self._factored_aggregate and not scaffold)
+                deferred = getattr(runner, "fc1_pending", None) is not None
                 payload, ldp = delta, runner.ld
                 if scaffold:
                     ldp = (Dp + 3) & ~3
@@ -647,9 +655,21 @@ class GpuSimulationEngine:
                                 native.ptr(nf2), native.ptr(kws), kws.numel(), stream)
                 torch.bitwise_or(nonfinite[:C], nf2[:C], out=nonfinite[:C])
                 wsb = native.call("fb_weighted_sum_workspace_bytes", C, Dp)
+                if deferred:  # (a narrow column range may use more client slices)
+                    wsb = max(wsb, native.call("fb_weighted_sum_workspace_bytes", C, cnn.FC1_LO),
+                              native.call("fb_weighted_sum_workspace_bytes", C, Dp - cnn.FC1_HI))
                 sws = self.ws.get("sum_ws", wsb)
-                native.call("fb_weighted_sum_f32", native.ptr(payload), ldp, C, Dp, native.ptr(coef),
-                            native.ptr(agg_flat), 0, native.ptr(sws), sws.numel(), stream)
+                if deferred:  # K3 around the CNN's fc1 block, which comes from the low-rank history
+                    lo, hi = cnn.FC1_LO, cnn.FC1_HI
+                    native.call("fb_weighted_sum_f32", native.ptr(payload), ldp, C, lo, native.ptr(coef),
+                                native.ptr(agg_flat), 0, native.ptr(sws), sws.numel(), stream)
+                    native.call("fb_weighted_sum_f32", native.ptr(payload) + 4 * hi, ldp, C, Dp - hi,
+                                native.ptr(coef), native.ptr(agg_flat) + 4 * hi, 0, native.ptr(sws), sws.numel(),
+                                stream)
+                    cnn.fc1_aggregate(runner, coef, agg_flat[lo:hi], stream)
+                else:
+                    native.call("fb_weighted_sum_f32", native.ptr(payload), ldp, C, Dp, native.ptr(coef),
+                                native.ptr(agg_flat), 0, native.ptr(sws), sws.numel(), stream)
             else:
                 agg_flat.zero_()
             if scaffold and self.world_size > 1:  # every rank's store takes the whole cohort's controls

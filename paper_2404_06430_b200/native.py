@@ -54,8 +54,9 @@ SIGNATURES: dict[str, tuple] = {
     "fb_local_sgd_cnn_f32": (
         _i32,
         [_p, _p, _p, _p, _p, _p, _p, _i32, _i32, _i32, _i32, _f32, _f32, _p, _i64, _p, _i32, _i32, _p, _i64, _p, _p,
-         _i64, _p, _p],
+         _i64, _p, _i32, _p],
     ),
+    "fb_cnn_fc1_aggregate_f32": (_i32, [_p, _i32, _i32, _i32, _f32, _f32, _i32, _i32, _p, _i64, _p, _p]),
     "fb_clip_workspace_bytes": (_i64, [_i32, _i64]),
     "fb_delta_norm_clip_f32": (_i32, [_p, _i64, _i32, _i64, _p, _f64, _p, _p, _p, _p, _p, _i64, _p]),
     "fb_delta_norm_clip_ex_f32": (_i32, [_p, _i64, _i32, _i64, _i64, _i64, _p, _p, _f64, _p, _p, _p, _p, _p, _i64, _p]),

@@ -143,3 +143,24 @@ def test_cnn_tcgen05_conv_matches_cuda_core_kernels():
     for c in range(len(sizes)):
         rel = np.linalg.norm(out[1][0][c] - out[0][0][c]) / np.linalg.norm(out[0][0][c])
         assert rel < 1e-2, (c, rel)
+
+
+def test_cnn_factored_aggregate_matches_materialised():
+    """The fc1 block of the aggregate formed from the clients' low-rank histories
+    (fb_cnn_fc1_aggregate_f32: no per-client materialisation) equals the
+    materialise-then-K3 path: 70 clients, so client chunks hold several TMEM drain
+    groups and some chunks are ragged."""
+    from tests.helpers import product_datasets, product_run_parts
+
+    cfg = {**CONFIGS["cnn_dp"], "users": 80, "val_users": 4, "ppu": 6, "cohort": 70, "eval_cohort": 3,
+           "iterations": 2, "eval_every": 5}
+    ds = product_datasets(cfg)
+    thetas = {}
+    for fact in (False, True):
+        alg, post = product_run_parts(cfg, noise_source="numpy")
+        eng = fb.GpuSimulationEngine(ds, postprocessors=post, factored_aggregate=fact)
+        out = []
+        fb.run_simulation(alg, eng, callbacks=[lambda p, rows, t: out.append(p.flat_host()) and False])
+        thetas[fact] = np.array(out)
+    for t in range(len(thetas[True])):
+        assert_close_fp32(thetas[True][t], thetas[False][t], what=f"theta after iteration {t}")
