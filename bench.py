@@ -240,8 +240,10 @@ def kernel_work(wl: dict, counts: dict) -> dict:
         "conv1_bwd_w_kernel": ("tensor", 2 * CNN_MACS["conv1"] * train, "FP32 FFMA"),
         "conv1_fwd_tc_kernel": ("tensor", 2 * CNN_MACS["conv1"] * fwd, "3xTF32 tcgen05 (hi/lo weights stacked along N)"),
         "conv1_bwd_w_tc_kernel": ("tensor", 2 * CNN_MACS["conv1"] * train, "3xTF32 tcgen05 (hi/lo in operand rows)"),
-        # the client's fp32 fc1 delta written once per run (6.4 MB per client)
-        "fc1_mat_tc_kernel": ("hbm", counts["clients"] * 12544 * 128 * 4, "bytes"),
+        # factored fc1 (squares-only materialisation and the factored aggregate): each reads the
+        # client's fp16 hi/lo pooled history once, 4 B per history row element (steps x batch rows)
+        "fc1_mat_tc_kernel": ("hbm", counts["client_steps"] * wl["batch"] * 12544 * 4, "bytes"),
+        "fc1_agg_tc_kernel": ("hbm", counts["client_steps"] * wl["batch"] * 12544 * 4, "bytes"),
         # per client-step: read the client's fc1 delta (fwd); read + write it (bwd)
         "fc1_fwd_kernel": ("hbm", steps * fc1_bytes + fwd * 12544 * 4, "bytes"),
         "fc1_bwd_kernel": ("hbm", steps * 2 * fc1_bytes + 2 * train * 12544 * 4, "bytes"),

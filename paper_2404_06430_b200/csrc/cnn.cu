@@ -3072,6 +3072,7 @@ __global__ void __launch_bounds__(C1F_THREADS, 2) conv1_fwd_tc_kernel(
 // im2col'ed from the image in smem), double-buffered against the MMAs; each
 // chunk's accumulator (a 16-MMA chain) is drained by warps 0 / 1 into fp32
 // registers (round-to-nearest adds) while the next chunk runs.
+constexpr int W1_GRP = 4;  // conv1 weight gradient: chunks per TMEM accumulation chain (4 x 8 MMAs)
 constexpr int W1_PART = 28 * 32;  // floats per split partial of conv1_bwd_w_tc ([k][o])
 constexpr int W1_CH = 64;                           // positions per chunk
 constexpr int W1_CPS = (S1 * S1 + W1_CH - 1) / W1_CH;  // 15 chunks per sample (last: 4 positions)
@@ -3133,10 +3134,12 @@ __global__ void __launch_bounds__(W1_THREADS, 2) conv1_bwd_w_tc_kernel(const flo
 #pragma unroll
   for (int k = 0; k < 32; ++k) run[k] = 0.f;
   // drain chunk i's accumulator into run[] (warp 0: hi rows, warp 1: lo rows)
+  // accumulators are drained once per group of W1_GRP chunks (a 32-MMA chain), from
+  // TMEM buffer (group & 1), after the group's last chunk i completed
   auto drain = [&](int i) {
     tc::mbar_wait(&done[i & 1], (i >> 1) & 1);
     tc::tc_fence_after();
-    const uint32_t base = tmem + ((uint32_t)(warp * 32) << 16) + (i & 1) * 64;
+    const uint32_t base = tmem + ((uint32_t)(warp * 32) << 16) + ((i / W1_GRP) & 1) * 64;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       uint32_t v0[16], v1[16];
@@ -3220,21 +3223,22 @@ __global__ void __launch_bounds__(W1_THREADS, 2) conv1_bwd_w_tc_kernel(const flo
     tc::tc_fence_after();
     if (warp == 0) {
       if (tc::elect_one()) {
-        const uint32_t d = tmem + (i & 1) * 64;
+        const uint32_t d = tmem + ((i / W1_GRP) & 1) * 64;
+        const bool fresh = i % W1_GRP == 0;
 #pragma unroll
         for (int kk = 0; kk < W1_CH / 8; ++kk) {
           const uint32_t a = stg + (kk >> 2) * W1_ATOM + (kk & 3) * 32;
-          tc::mma_tf32(d, tc::sdesc_k128(a), tc::sdesc_k128(a + 8192), W1_IDESC, kk != 0);
+          tc::mma_tf32(d, tc::sdesc_k128(a), tc::sdesc_k128(a + 8192), W1_IDESC, !fresh || kk != 0);
         }
         tc::mma_commit(&done[i & 1]);
       }
       __syncwarp();
     }
-    if (warp < 2 && i >= 1) drain(i - 1);
+    if (warp < 2 && i >= 1 && (i - 1) % W1_GRP == W1_GRP - 1) drain(i - 1);
 #pragma unroll
     for (int j = 0; j < W1_NLD; ++j) cur[j] = nxt[j];
   }
-  if (warp < 2) drain(nchunks - 1);
+  if (warp < 2) drain(nchunks - 1);  // the last chunk closes the last group
   // combine the hi-row (warp 0) and lo-row (warp 1) sums; update dW1 and b1
   if (warp == 1)
 #pragma unroll
