@@ -2864,11 +2864,18 @@ constexpr int C1F_STAGE = 2 * C1F_A;                            // hi | lo
 constexpr int C1F_B = 64 * 128;                                 // [W hi; W lo] x 32 k
 constexpr int C1F_THREADS = 256;
 constexpr int C1F_GMAX = 16;
-constexpr int C1F_SMEM = 1024 + C1F_B + 2 * C1F_STAGE + 2 * IMG * 4 + 256;  // ~97 KB: 2 CTAs per SM
+#ifndef C1F_ASTAGES
+#define C1F_ASTAGES 1  // A stages: 1 -> ~65 KB, 3 CTAs per SM (the next tile is staged after its TMEM
+                       // predecessor's MMAs completed, which epi_load waits for anyway)
+#endif
+#ifndef C1F_MINB
+#define C1F_MINB 3
+#endif
+constexpr int C1F_SMEM = 1024 + C1F_B + C1F_ASTAGES * C1F_STAGE + 2 * IMG * 4 + 256;
 constexpr uint32_t C1F_IDESC2 = tc::idesc_tf32(128, 2 * C1);
 constexpr uint32_t C1F_IDESC = tc::idesc_tf32(128, C1);
 
-__global__ void __launch_bounds__(C1F_THREADS, 2) conv1_fwd_tc_kernel(
+__global__ void __launch_bounds__(C1F_THREADS, C1F_MINB) conv1_fwd_tc_kernel(
     const float* __restrict__ X, const int64_t* __restrict__ slot_row, const float* __restrict__ theta,
     const float* __restrict__ delta, int64_t ld, int B, int N, int G, __half* __restrict__ a1fh,
     __half* __restrict__ a1fl, float* __restrict__ a1scale) {
@@ -2876,7 +2883,7 @@ __global__ void __launch_bounds__(C1F_THREADS, 2) conv1_fwd_tc_kernel(
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sB = sm;
   uint8_t* sA = sm + C1F_B;                                         // [2][hi 16 KB | lo 16 KB]
-  float* img = reinterpret_cast<float*>(sA + 2 * C1F_STAGE);        // [2][3][32][32]
+  float* img = reinterpret_cast<float*>(sA + C1F_ASTAGES * C1F_STAGE);  // [2][3][32][32]
   uint64_t* done = reinterpret_cast<uint64_t*>(img + 2 * IMG);      // [2] MMA completion per A stage
   uint64_t* imfull = done + 2;                                      // [2] image arrival
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(imfull + 2);
@@ -3003,7 +3010,7 @@ __global__ void __launch_bounds__(C1F_THREADS, 2) conv1_fwd_tc_kernel(
       // rows past the 900 positions (last tile) read position 899: their outputs are dropped
       const int p = min(tile * C1F_TILE + pl, S1 * S1 - 1), y = p / S1, x = p - y * S1;
       const uint32_t ib = im + 4 * (y * S0 + x);
-      const uint32_t ah = sA0 + buf * C1F_STAGE, al = ah + C1F_A;
+      const uint32_t ah = sA0 + (i % C1F_ASTAGES) * C1F_STAGE, al = ah + C1F_A;
       auto stage = [&](auto khc) {  // khc: compile-time k half (warp-uniform)
         constexpr int KH = decltype(khc)::value;
 #pragma unroll
@@ -3039,7 +3046,7 @@ __global__ void __launch_bounds__(C1F_THREADS, 2) conv1_fwd_tc_kernel(
     if (warp == 0) {
       if (tc::elect_one()) {
         const uint32_t d = tmem + buf * 64;
-        const uint32_t ah = sA0 + buf * C1F_STAGE, al = ah + C1F_A;
+        const uint32_t ah = sA0 + (i % C1F_ASTAGES) * C1F_STAGE, al = ah + C1F_A;
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
           const uint64_t bd = tc::sdesc_k128(sB0 + 32 * kk);
