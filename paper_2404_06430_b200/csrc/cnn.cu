@@ -3089,11 +3089,17 @@ constexpr int W1_THREADS = 256;
 constexpr int W1_NLD = W1_CH * 8 / W1_THREADS;      // dz1 float4 loads per thread per chunk
 constexpr int W1_KPER = 28 / (W1_THREADS / W1_CH);  // im2col rows per thread
 static_assert(W1_NLD * W1_THREADS == W1_CH * 8 && W1_KPER * (W1_THREADS / W1_CH) == 28, "conv1 bwd-w staging split");
-constexpr int W1_SMEM = 1024 + 2 * W1_STAGE + IMG * 4 + 32 * 33 * 4 + 64;
+#ifndef W1_ASTAGES
+#define W1_ASTAGES 2  // operand stages (1: the previous chunk's MMAs must finish before staging)
+#endif
+#ifndef W1_MINB
+#define W1_MINB 2
+#endif
+constexpr int W1_SMEM = 1024 + W1_ASTAGES * W1_STAGE + IMG * 4 + 32 * 33 * 4 + 64;
 constexpr uint32_t W1_IDESC = tc::idesc_tf32(128, 64);
 
 template <bool SPLIT>
-__global__ void __launch_bounds__(W1_THREADS, 2) conv1_bwd_w_tc_kernel(const float* __restrict__ X,
+__global__ void __launch_bounds__(W1_THREADS, W1_MINB) conv1_bwd_w_tc_kernel(const float* __restrict__ X,
                                                                       const int64_t* __restrict__ slot_row,
                                                                       const float* __restrict__ dz1, int B,
                                                                       const int32_t* __restrict__ client_nb,
@@ -3101,7 +3107,7 @@ __global__ void __launch_bounds__(W1_THREADS, 2) conv1_bwd_w_tc_kernel(const flo
                                                                       int split, float* __restrict__ wpart) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  float* img = reinterpret_cast<float*>(sm + 2 * W1_STAGE);  // [3][32][32]
+  float* img = reinterpret_cast<float*>(sm + W1_ASTAGES * W1_STAGE);  // [3][32][32]
   float* red = img + IMG;                                    // [32][33]: warp 1's sums
   uint64_t* done = reinterpret_cast<uint64_t*>(red + 32 * 33);  // [2] MMA completion per stage
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 2);
@@ -3122,7 +3128,7 @@ __global__ void __launch_bounds__(W1_THREADS, 2) conv1_bwd_w_tc_kernel(const flo
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, t = threadIdx.x;
   const uint32_t s0 = tc::smem_u32(sm), simg = tc::smem_u32(img);
   // rows 28-31 / 60-63 of B (padding of k) stay zero; staging never writes them
-  for (int i = t; i < 2 * (W1_CH / 32) * 2 * 4 * 8; i += W1_THREADS) {  // stage, atom, hi/lo, 4 rows, 8 x 16 B
+  for (int i = t; i < W1_ASTAGES * (W1_CH / 32) * 2 * 4 * 8; i += W1_THREADS) {  // stage, atom, hi/lo, 4 rows, 8 x 16 B
     const int q = i & 7, r = (i >> 3) & 3, part = (i >> 5) & 1, atom = i >> 6;
     reinterpret_cast<uint4*>(sm + atom * W1_ATOM + 8192 + (part * 32 + 28 + r) * 128)[q] = make_uint4(0, 0, 0, 0);
   }
@@ -3183,9 +3189,10 @@ __global__ void __launch_bounds__(W1_THREADS, 2) conv1_bwd_w_tc_kernel(const flo
   for (int i = 0; i < nchunks; ++i) {
     const int b = i / W1_CPS, ch = i - b * W1_CPS, p0 = ch * W1_CH;
     const int64_t n = (int64_t)c * B + b0 + b;
-    const uint32_t stg = s0 + (i & 1) * W1_STAGE;
+    const uint32_t stg = s0 + (i % W1_ASTAGES) * W1_STAGE;
     if (i + 1 < nchunks) load_dz(i + 1, nxt);
-    if (i >= 2) tc::mbar_wait(&done[i & 1], ((i - 2) >> 1) & 1);  // chunk i-2's MMAs done reading this stage
+    if (i >= W1_ASTAGES)  // chunk i - W1_ASTAGES's MMAs done reading this stage
+      tc::mbar_wait(&done[(i - W1_ASTAGES) & 1], ((i - W1_ASTAGES) >> 1) & 1);
     if (ch == 0) {
       __syncthreads();  // previous sample's im2col reads finished
       const float4* src = reinterpret_cast<const float4*>(X + slot_row[n] * IMG);
