@@ -2345,7 +2345,10 @@ __global__ void __launch_bounds__(FMT_THREADS, 1) fc1_mat_tc_kernel(
 // registers and writes a per-chunk partial; fc1_agg_reduce_kernel sums the chunks in
 // fixed order.  Reads 2.5 GB of history instead of writing + re-reading the 6.4 GB of
 // per-client fc1 deltas.  (Clip norms come from fc1_mat_tc_kernel in squares-only mode.)
-constexpr int FAG_CHUNKS = 8;                          // client chunks (grid.y)
+#ifndef FAG_NCHUNKS
+#define FAG_NCHUNKS 6  // 588 CTAs: ~4 full waves on 148 SMs (measured 0.47 vs 0.53 ms at 8)
+#endif
+constexpr int FAG_CHUNKS = FAG_NCHUNKS;                // client chunks (grid.y)
 constexpr int FAG_DRAIN = 8;                           // clients per TMEM accumulation chain
 constexpr int FAG_UBYTES = 4 * FMT_BLK;                // U' hi blk0 | blk1 | lo blk0 | blk1 (32 KB)
 constexpr int FAG_STAGE = FMT_STAGE + FAG_UBYTES;      // P tile (32 KB) + U' (32 KB)
@@ -4084,7 +4087,11 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
       st = hist_tensor_map(&mh, w.pfh, N, max_steps, B);
       if (!st) st = hist_tensor_map(&ml, w.pfl, N, max_steps, B);
       if (st) return st;
-      const int msplit = Cw * FMT_SPLIT >= g_num_sms ? FMT_SPLIT : 7;  // 2 CTAs per client, 7 for a small shard
+#ifndef FMT_SQ_SPLIT
+#define FMT_SQ_SPLIT 1  // squares only: one CTA per client (U' built once; 0.80 vs 1.05 ms at 2)
+#endif
+      const int fs = fc1_store ? FMT_SPLIT : FMT_SQ_SPLIT;
+      const int msplit = Cw * fs >= g_num_sms ? fs : 7;  // CTAs per client (7 for a small shard)
       FB_LAUNCH("fc1_mat_tc_kernel", s, fc1_mat_tc_kernel<<<dim3(Cw, msplit), FMT_THREADS, FMT_SMEM, s>>>(
                                             mh, ml, hs, w.pscale, N, max_steps, B, lr, prox_mu, dlt, ld_delta,
                                             fc1_sumsq ? w.gram_part : nullptr, fc1_store));
