@@ -1273,6 +1273,30 @@ constexpr uint32_t FW_IDESC2 = tc::idesc_f16(128, 2 * C2);  // B = [W hi; W lo] 
 static_assert(127 + 2 * S1 + 2 < FW_BAND * S1 && FW_A_TX <= FW_A, "conv2 fwd band: every tap row inside the band");
 
 // per-group conv2 weight image (K-major SWIZZLE_64B: row o, 32 ci), scaled split
+// the client's conv2 weights (theta_t - delta_c, or theta_t) as float4 registers:
+// 256 threads x WQ quads cover the 18432 weights (O_W2 is 16-byte aligned), all loads
+// of a thread in flight together; returns max |w| of the thread's part
+constexpr int WQ = C2 * C1 * 9 / 4 / 256;  // 18
+static_assert(C2 * C1 * 9 == WQ * 4 * 256 && O_W2 % 4 == 0, "conv2 weight quads");
+__device__ __forceinline__ float load_w2(const float* __restrict__ theta, const float* __restrict__ dc,
+                                         float4 (&v)[WQ]) {
+  const float4* t4 = reinterpret_cast<const float4*>(theta + O_W2);
+  const float4* d4 = dc ? reinterpret_cast<const float4*>(dc + O_W2) : nullptr;
+  float m = 0.f;
+#pragma unroll
+  for (int u = 0; u < WQ; ++u) {
+    const int q = threadIdx.x + u * 256;
+    float4 w = __ldg(t4 + q);
+    if (d4) {
+      const float4 d = d4[q];
+      w.x -= d.x; w.y -= d.y; w.z -= d.z; w.w -= d.w;
+    }
+    v[u] = w;
+    m = fmaxf(m, fmaxf(fmaxf(fabsf(w.x), fabsf(w.y)), fmaxf(fabsf(w.z), fabsf(w.w))));
+  }
+  return m;
+}
+
 __global__ void __launch_bounds__(256) conv2_wimg_kernel(const float* __restrict__ theta,
                                                          const float* __restrict__ delta, int64_t ld,
                                                          const int32_t* __restrict__ client_nb,
@@ -1281,21 +1305,26 @@ __global__ void __launch_bounds__(256) conv2_wimg_kernel(const float* __restrict
   const int g = blockIdx.x;
   if (delta && client_nb && client_nb[g] == 0) return;
   const float* dc = delta ? delta + (int64_t)g * ld : nullptr;
-  float m = 0.f;
-  for (int i = threadIdx.x; i < C2 * C1 * 9; i += blockDim.x) m = fmaxf(m, fabsf(wt(theta, dc, O_W2 + i)));
-  const float sc = block_scale(m, red);
+  float4 v[WQ];
+  const float sc = block_scale(load_w2(theta, dc, v), red);
   if (threadIdx.x == 0) wscale[g] = sc;
   // the 72 KB image is assembled in smem (scattered 2-byte swizzled stores) and
   // written out with coalesced 16-byte stores
   extern __shared__ uint4 wim_s[];
   uint8_t* simg = reinterpret_cast<uint8_t*>(wim_s);
-  for (int i = threadIdx.x; i < C2 * C1 * 9; i += blockDim.x) {
-    const int o = i / (C1 * 9), r = i - o * (C1 * 9), ci = r / 9, tap = r - ci * 9;
-    __half h, l;
-    split_f16(wt(theta, dc, O_W2 + i) * sc, h, l);
-    const uint32_t off = sw64_off16(o, ci);
-    *reinterpret_cast<__half*>(simg + (tap * 2 + 0) * FW_B_TAP + off) = h;
-    *reinterpret_cast<__half*>(simg + (tap * 2 + 1) * FW_B_TAP + off) = l;
+#pragma unroll
+  for (int u = 0; u < WQ; ++u) {
+    const float e4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int i = 4 * (threadIdx.x + u * 256) + e;
+      const int o = i / (C1 * 9), r = i - o * (C1 * 9), ci = r / 9, tap = r - ci * 9;
+      __half h, l;
+      split_f16(e4[e] * sc, h, l);
+      const uint32_t off = sw64_off16(o, ci);
+      *reinterpret_cast<__half*>(simg + (tap * 2 + 0) * FW_B_TAP + off) = h;
+      *reinterpret_cast<__half*>(simg + (tap * 2 + 1) * FW_B_TAP + off) = l;
+    }
   }
   __syncthreads();
   uint4* img = reinterpret_cast<uint4*>(wimg + (int64_t)g * WIMG_BYTES);
@@ -2629,19 +2658,24 @@ __global__ void __launch_bounds__(256) conv2_wimgT_kernel(const float* __restric
   const int g = blockIdx.x;
   if (client_nb[g] == 0) return;
   const float* dc = delta + (int64_t)g * ld;
-  float m = 0.f;
-  for (int i = threadIdx.x; i < C2 * C1 * 9; i += blockDim.x) m = fmaxf(m, fabsf(theta[O_W2 + i] - dc[O_W2 + i]));
-  const float sc = block_scale(m, red);
+  float4 v[WQ];
+  const float sc = block_scale(load_w2(theta, dc, v), red);
   if (threadIdx.x == 0) wscale[g] = sc;
   extern __shared__ uint4 wim_s[];  // assembled in smem, written out coalesced
   uint8_t* simg = reinterpret_cast<uint8_t*>(wim_s);
-  for (int i = threadIdx.x; i < C2 * C1 * 9; i += blockDim.x) {
-    const int o = i / (C1 * 9), r = i - o * (C1 * 9), ci = r / 9, tap = r - ci * 9;
-    __half h, l;
-    split_f16((theta[O_W2 + i] - dc[O_W2 + i]) * sc, h, l);
-    const uint32_t off = sw128_off16(ci, o);
-    *reinterpret_cast<__half*>(simg + (tap * 2 + 0) * BX_B_TAP + off) = h;
-    *reinterpret_cast<__half*>(simg + (tap * 2 + 1) * BX_B_TAP + off) = l;
+#pragma unroll
+  for (int u = 0; u < WQ; ++u) {
+    const float e4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int i = 4 * (threadIdx.x + u * 256) + e;
+      const int o = i / (C1 * 9), r = i - o * (C1 * 9), ci = r / 9, tap = r - ci * 9;
+      __half h, l;
+      split_f16(e4[e] * sc, h, l);
+      const uint32_t off = sw128_off16(ci, o);
+      *reinterpret_cast<__half*>(simg + (tap * 2 + 0) * BX_B_TAP + off) = h;
+      *reinterpret_cast<__half*>(simg + (tap * 2 + 1) * BX_B_TAP + off) = l;
+    }
   }
   __syncthreads();
   uint4* img = reinterpret_cast<uint4*>(wimg + (int64_t)g * WIMGT_BYTES);
