@@ -435,27 +435,41 @@ __global__ void __launch_bounds__(HID) head_kernel(const float* __restrict__ par
   if (train && nb == 0) return;
   for (int i = j; i < HID * NCLS + NCLS; i += blockDim.x) w2[i] = wt(theta, dc, O_F2 + i);
   const float bf1 = wt(theta, dc, O_BF1 + j);
-  for (int b = 0; b < G; ++b) {
+  // factored fc1: z3[b] -= delta_s p_b = sum_{sp < s, bp} coef_sp dz3_{sp,bp} (p_{sp,bp} . p_b):
+  // each history dz3 value is loaded once and applied to every new row b (Gram rows in smem)
+  float corr[GMAX];
+#pragma unroll
+  for (int b = 0; b < GMAX; ++b) corr[b] = 0.f;
+  if (train && hs.phist && hs.s > 0) {
+    __shared__ float gsm[GMAX][FC_RMAX];
+    const int Jp = hs.s * G;
+    for (int i = j; i < nb * Jp; i += blockDim.x) {
+      const int b = i / Jp, r = i - b * Jp;
+      gsm[b][r] = hs.gram[((int64_t)g * hs.R + hs.s * G + b) * hs.R + r];
+    }
+    __syncthreads();
+    for (int sp = 0; sp < hs.s; ++sp) {
+      const int nbp = hs.nbh[sp * hs.cstride + g];
+      const float cf = hist_coef(st.lr, st.mu, hs.s, sp);
+      const float* dzp = hs.dz3h + sp * hs.dstride + (int64_t)n0 * HID + j;
+      for (int bp = 0; bp < nbp; ++bp) {
+        const float d = cf * dzp[bp * HID];
+#pragma unroll
+        for (int b = 0; b < GMAX; ++b)
+          if (b < nb) corr[b] = fmaf(d, gsm[b][sp * G + bp], corr[b]);
+      }
+    }
+  }
+#pragma unroll
+  for (int b = 0; b < GMAX; ++b) {
+    if (b >= G) break;
     const int n = n0 + b;
     float z = 0.f;
     if (n < N && slot_row[n] >= 0) {
       z = bf1;
       for (int s = 0; s < nsplit; ++s) z += part[((int64_t)s * N + n) * HID + j];
     }
-    if (train && hs.phist && b < nb) {
-      // factored fc1: z3 -= delta_s p = sum_{sp < s} coef * sum_bp dz3_{sp,bp} (p_{sp,bp} . p)
-      const float* grow = hs.gram + ((int64_t)g * hs.R + hs.s * G + b) * hs.R;
-      float corr = 0.f;
-      for (int sp = 0; sp < hs.s; ++sp) {
-        const int nbp = hs.nbh[sp * hs.cstride + g];
-        const float* dzp = hs.dz3h + sp * hs.dstride + (int64_t)n0 * HID + j;
-        float t = 0.f;
-        for (int bp = 0; bp < nbp; ++bp) t = fmaf(dzp[bp * HID], grow[sp * G + bp], t);
-        corr = fmaf(hist_coef(st.lr, st.mu, hs.s, sp), t, corr);
-      }
-      z -= corr;
-    }
-    z3[b][j] = z;
+    z3[b][j] = z - corr[b];
   }
   if (j < G) {
     const int n = n0 + j;
