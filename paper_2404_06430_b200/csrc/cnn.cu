@@ -2063,6 +2063,9 @@ int tensor_map_2d_f16(CUtensorMap* map, const __half* base, int64_t inner, int64
 // dp -= sum_j a[b][j] p_j (history part of the factored backward); grid (C, KSPLIT),
 // thread = 4 k.  The client's active history rows are compacted first so the row loop
 // has no branch and issues four independent float4 loads per trip.
+#ifndef DPH_U
+#define DPH_U 4  // history rows loaded per trip of fc1_dp_hist_kernel
+#endif
 template <int GM>
 __global__ void __launch_bounds__(KCHUNK / 4) fc1_dp_hist_kernel(int B, const int32_t* __restrict__ client_nb, Hist hs,
                                                                  float* __restrict__ dp) {
@@ -2102,12 +2105,12 @@ __global__ void __launch_bounds__(KCHUNK / 4) fc1_dp_hist_kernel(int B, const in
   const float4* ph = reinterpret_cast<const float4*>(hs.phist);
   int q = 0;
 #pragma unroll 1
-  for (; q + 4 <= nj; q += 4) {
-    float4 p[4];
+  for (; q + DPH_U <= nj; q += DPH_U) {
+    float4 p[DPH_U];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) p[u] = __ldg(ph + (roff[q + u] >> 2) + t);
+    for (int u = 0; u < DPH_U; ++u) p[u] = __ldg(ph + (roff[q + u] >> 2) + t);
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < DPH_U; ++u)
 #pragma unroll
       for (int b = 0; b < GM; ++b) {
         const float a = ac[(q + u) * GM + b];
@@ -4025,7 +4028,10 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
       if (st) return st;
       if (fact) {
         FB_REQUIRE((int64_t)max_steps * N * FLAT < (1LL << 31), "local_sgd_cnn: factored-fc1 history exceeds 2^31 elements");
-        const int gks = Cw * 7 >= 4 * g_num_sms ? 7 : 14;  // more K splits for a small shard
+#ifndef GR_NKS
+#define GR_NKS 7
+#endif
+        const int gks = Cw * GR_NKS >= 4 * g_num_sms ? GR_NKS : 14;  // more K splits for a small shard
         const dim3 ggrid(Cw, gks, std::min(GR_Z, (int)((step + 1) * B + GR_JW * GR_WARPS - 1) / (GR_JW * GR_WARPS)));
         if (B <= 8)
           FB_LAUNCH("fc1_gram_split_kernel", s, fc1_gram_split_kernel<8><<<ggrid, GR_WARPS * 32, 0, s>>>(
