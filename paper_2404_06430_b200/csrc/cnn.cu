@@ -3774,7 +3774,10 @@ int forward(const float* X, const float* theta, const float* delta, int64_t ld, 
     int st = a1f_tensor_map(&mh, w.a1fh, N, S1, FW_BAND);
     if (!st) st = a1f_tensor_map(&ml, w.a1fl, N, S1, FW_BAND);
     if (st) return st;
-    const int gt = delta ? B / client_split(active, B, 1) : 8;  // samples per CTA
+#ifndef FW_EVAL_G
+#define FW_EVAL_G 8
+#endif
+    const int gt = delta ? B / client_split(active, B, 1) : FW_EVAL_G;  // samples per CTA
     if (g_conv2_pairs)  // one CTA pair per former CTA's samples (cluster dims 2)
       FB_LAUNCH("conv2_fwd_tc_kernel", s, conv2_fwd_tc2_kernel<<<2 * ((N + gt - 1) / gt), FW_THREADS, FW2_SMEM, s>>>(
             mh, ml, w.wimg, w.wscale, delta ? 0 : 1, w.slot_row, N, gt, theta, delta, ld, B, w.a1scale, w.pooled,
