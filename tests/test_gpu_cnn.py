@@ -145,22 +145,26 @@ def test_cnn_tcgen05_conv_matches_cuda_core_kernels():
         assert rel < 1e-2, (c, rel)
 
 
-def test_cnn_factored_aggregate_matches_materialised():
+def test_cnn_factored_aggregate_matches_materialised(monkeypatch):
     """The fc1 block of the aggregate formed from the clients' low-rank histories
     (fb_cnn_fc1_aggregate_f32: no per-client materialisation) equals the
     materialise-then-K3 path: 70 clients, so client chunks hold several TMEM drain
-    groups and some chunks are ragged."""
+    groups and some chunks are ragged.  A cohort that needs several slot waves falls
+    back to materialisation (the history holds one wave) with the same result."""
+    from paper_2404_06430_b200 import cnn
     from tests.helpers import product_datasets, product_run_parts
 
     cfg = {**CONFIGS["cnn_dp"], "users": 80, "val_users": 4, "ppu": 6, "cohort": 70, "eval_cohort": 3,
            "iterations": 2, "eval_every": 5}
     ds = product_datasets(cfg)
     thetas = {}
-    for fact in (False, True):
+    for key, fact, max_slots in (("mat", False, cnn.MAX_SLOTS), ("fact", True, cnn.MAX_SLOTS), ("waves", True, 90)):
+        monkeypatch.setattr(cnn, "MAX_SLOTS", max_slots)  # 90 slots: 30 clients per wave at batch 3
         alg, post = product_run_parts(cfg, noise_source="numpy")
         eng = fb.GpuSimulationEngine(ds, postprocessors=post, factored_aggregate=fact)
         out = []
         fb.run_simulation(alg, eng, callbacks=[lambda p, rows, t: out.append(p.flat_host()) and False])
-        thetas[fact] = np.array(out)
-    for t in range(len(thetas[True])):
-        assert_close_fp32(thetas[True][t], thetas[False][t], what=f"theta after iteration {t}")
+        thetas[key] = np.array(out)
+    for t in range(len(thetas["fact"])):
+        assert_close_fp32(thetas["fact"][t], thetas["mat"][t], what=f"theta after iteration {t}")
+        assert_close_fp32(thetas["waves"][t], thetas["mat"][t], what=f"theta after iteration {t} (3 waves)")
