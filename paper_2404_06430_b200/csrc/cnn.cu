@@ -1542,18 +1542,26 @@ __global__ void __launch_bounds__(FW_THREADS, 1) conv2_fwd_tc_kernel(
           }
         }
         asm volatile("bar.sync 1, %0;" ::"n"(FW_EPI_WARPS * 32) : "memory");
-        for (int it = et; it < C2 * 2 * SP; it += FW_EPI_WARPS * 32) {
-          const int ch = it / (2 * SP), pp = it - ch * (2 * SP), pr = pp >= SP, px = pp - pr * SP;
-          const uint32_t e0 = sE + (ch * FW_XLD + pr * S1 + px) * 4;  // row 2pr pair px; row 2pr+1 is 15 pairs on
-          const float ta = tc::lds_f32(e0), tb = tc::lds_f32(e0 + (S1 / 2) * 4);
-          const float a = fabsf(ta), b = fabsf(tb);
-          // first maximum in (y,x), (y,x+1), (y+1,x), (y+1,x+1) order, as the sequential scan
-          const bool low = b > a;
-          const float best = low ? b : a;
-          const int arg = low ? 2 + (int)signbit(tb) : (int)signbit(ta);
-          const int idx = ch * NPOOL + FW_ROWS / 2 * t * SP + pp;
-          pout[idx] = best;
-          cout[idx] = (uint8_t)arg;
+        // four consecutive pooled outputs of one channel per thread: one float4 + one
+        // 4-byte code store (the 28 outputs of a tile row pair start 16-byte aligned)
+        for (int it = et; it < C2 * 2 * SP / 4; it += FW_EPI_WARPS * 32) {
+          const int ch = it / (2 * SP / 4), pp0 = 4 * (it - ch * (2 * SP / 4));
+          float best[4];
+          uint32_t codes = 0;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int pp = pp0 + e, pr = pp >= SP, px = pp - pr * SP;
+            const uint32_t e0 = sE + (ch * FW_XLD + pr * S1 + px) * 4;  // row 2pr pair px; row 2pr+1 is 15 pairs on
+            const float ta = tc::lds_f32(e0), tb = tc::lds_f32(e0 + (S1 / 2) * 4);
+            const float a = fabsf(ta), b = fabsf(tb);
+            // first maximum in (y,x), (y,x+1), (y+1,x), (y+1,x+1) order, as the sequential scan
+            const bool low = b > a;
+            best[e] = low ? b : a;
+            codes |= (uint32_t)(low ? 2 + (int)signbit(tb) : (int)signbit(ta)) << (8 * e);
+          }
+          const int idx = ch * NPOOL + FW_ROWS / 2 * t * SP + pp0;
+          *reinterpret_cast<float4*>(pout + idx) = make_float4(best[0], best[1], best[2], best[3]);
+          *reinterpret_cast<uint32_t*>(cout + idx) = codes;
         }
       }
     }
