@@ -1561,7 +1561,7 @@ __global__ void __launch_bounds__(FW_THREADS, 1) conv2_fwd_tc_kernel(
           }
           const int idx = ch * NPOOL + FW_ROWS / 2 * t * SP + pp0;
           *reinterpret_cast<float4*>(pout + idx) = make_float4(best[0], best[1], best[2], best[3]);
-          *reinterpret_cast<uint32_t*>(cout + idx) = codes;
+          if (!shared_weights) *reinterpret_cast<uint32_t*>(cout + idx) = codes;  // (evaluation: no backward)
         }
       }
     }
