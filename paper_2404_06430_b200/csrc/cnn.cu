@@ -2080,26 +2080,32 @@ __global__ void __launch_bounds__(KCHUNK / 4) fc1_dp_hist_kernel(int B, const in
   __shared__ float ac[FC_RMAX * GMAX];  // [compact row q][b]
   __shared__ uint32_t roff[FC_RMAX];
   __shared__ int jsrc[FC_RMAX];
-  __shared__ int s_nj;
+  __shared__ int s_cnt[2];
   const int c = blockIdx.x, k0 = blockIdx.y * KCHUNK, t = threadIdx.x;
   const int nb = client_nb[c];
   const int J = hs.s * B;
   if (nb == 0 || J == 0) return;
   const int n0 = c * B;
-  if (t == 0) {
-    int q = 0;
-    for (int jj = 0; jj < J; ++jj) {
-      const int sp = jj / B, bp = jj - sp * B;
-      if (bp < hs.nbh[sp * hs.cstride + c]) {
-        jsrc[q] = jj;
-        roff[q] = (uint32_t)(sp * hs.pstride + (int64_t)(n0 + bp) * FLAT + k0);  // host checks S*N*FLAT < 2^31
-        ++q;
-      }
-    }
-    s_nj = q;
+  // compact the active history rows in parallel (J <= 64: warps 0 and 1, ballot + popc),
+  // keeping row order; a serial scan here cost one dependent L2 round trip per row
+  static_assert(FC_RMAX <= 64 && KCHUNK / 4 >= 64, "dp_hist compaction: two warps");
+  bool act = false;
+  int sp = 0, bp = 0;
+  if (t < 64) {
+    sp = t / B;
+    bp = t - sp * B;
+    act = t < J && bp < hs.nbh[sp * hs.cstride + c];
+  }
+  const unsigned bal = t < 64 ? __ballot_sync(0xffffffffu, act) : 0u;
+  if (t < 64 && (t & 31) == 0) s_cnt[t >> 5] = __popc(bal);
+  __syncthreads();
+  if (act) {
+    const int q = (t >= 32 ? s_cnt[0] : 0) + __popc(bal & ((1u << (t & 31)) - 1u));
+    jsrc[q] = t;
+    roff[q] = (uint32_t)(sp * hs.pstride + (int64_t)(n0 + bp) * FLAT + k0);  // host checks S*N*FLAT < 2^31
   }
   __syncthreads();
-  const int nj = s_nj;
+  const int nj = s_cnt[0] + s_cnt[1];
   for (int i = t; i < nj * GM; i += blockDim.x) {
     const int q = i / GM, b = i - q * GM;
     ac[i] = b < nb ? hs.acoef[((int64_t)c * GMAX + b) * FC_RMAX + jsrc[q]] : 0.f;
