@@ -1372,9 +1372,9 @@ __global__ void __launch_bounds__(FW_THREADS, 1) conv2_fwd_tc_kernel(
   const int g = blockIdx.x;
   const int n0 = g * G;
   {  // nothing to do (clients past their last local step, tail of the last chunk): leave before any setup
-    bool any = false;
-    for (int b = 0; b < G && n0 + b < N; ++b) any |= slot_row[n0 + b] >= 0;
-    if (!any) return;
+    // (one slot per thread, one block-wide OR: a serial scan paid an L2 round trip per slot)
+    const int b = threadIdx.x;
+    if (!__syncthreads_or(b < G && n0 + b < N && slot_row[n0 + b] >= 0)) return;
   }
   const int wg = shared_weights ? 0 : n0 / B;   // weight group (client) of this CTA
   const float* dc = delta ? delta + (int64_t)wg * ld : nullptr;
@@ -1619,9 +1619,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FW_THREADS, 1) conv2
   const int g = blockIdx.x >> 1;  // pair index
   const int n0 = g * G;
   {  // nothing to do: both CTAs of the pair see the same slots and leave together
-    bool any = false;
-    for (int b = 0; b < G && n0 + b < N; ++b) any |= slot_row[n0 + b] >= 0;
-    if (!any) return;
+    // (one slot per thread, one block-wide OR: a serial scan paid an L2 round trip per slot)
+    const int b = threadIdx.x;
+    if (!__syncthreads_or(b < G && n0 + b < N && slot_row[n0 + b] >= 0)) return;
   }
   const int wg = shared_weights ? 0 : n0 / B;
   const float* dc = delta ? delta + (int64_t)wg * ld : nullptr;
@@ -2793,9 +2793,8 @@ __global__ void __launch_bounds__(BX_THREADS, 1) conv2_bwd_x_tc_kernel(
   const int n0 = blockIdx.x * G;  // G slots of one client (G divides the batch B)
   const int g = n0 / B;           // the client: its weight image
   {  // a client past its last local step: leave before any setup
-    bool any = false;
-    for (int b = 0; b < G; ++b) any |= slot_row[n0 + b] >= 0;
-    if (!any) return;
+    const int b = threadIdx.x;
+    if (!__syncthreads_or(b < G && slot_row[n0 + b] >= 0)) return;
   }
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < BX_STAGES; ++i) {
@@ -2975,9 +2974,9 @@ __global__ void __launch_bounds__(C1F_THREADS, C1F_MINB) conv1_fwd_tc_kernel(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, t = threadIdx.x;
   const int n0 = blockIdx.x * G;
   {  // no active slot (client past its last local step / tail chunk): leave before any setup
-    bool any = false;
-    for (int b = 0; b < G && n0 + b < N; ++b) any |= slot_row[n0 + b] >= 0;
-    if (!any) return;
+    // (one slot per thread, one block-wide OR: a serial scan paid an L2 round trip per slot)
+    const int b = threadIdx.x;
+    if (!__syncthreads_or(b < G && n0 + b < N && slot_row[n0 + b] >= 0)) return;
   }
   const float* dc = delta ? delta + (int64_t)(n0 / B) * ld : nullptr;
   const uint32_t sB0 = tc::smem_u32(sB), sA0 = tc::smem_u32(sA), simg = tc::smem_u32(img);
@@ -2995,11 +2994,13 @@ __global__ void __launch_bounds__(C1F_THREADS, C1F_MINB) conv1_fwd_tc_kernel(
     for (int k = 0; k < 27; ++k) sw += fabsf(wt(theta, dc, O_W1 + t * 27 + k));
     wsum[t] = sw;
   }
+  if (warp == 0) {  // active slots of the group, compacted in order (ballot + popc; G <= 32)
+    const bool a = lane < G && n0 + lane < N && slot_row[n0 + lane] >= 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, a);
+    if (a) s_slot[__popc(bal & ((1u << lane) - 1u))] = n0 + lane;
+    if (lane == 0) s_ns = __popc(bal);
+  }
   if (t == 0) {
-    int ns = 0;
-    for (int b = 0; b < G && n0 + b < N; ++b)
-      if (slot_row[n0 + b] >= 0) s_slot[ns++] = n0 + b;
-    s_ns = ns;
     for (int j = 0; j < 2; ++j) {
       tc::mbar_init(&done[j], 1);
       tc::mbar_init(&imfull[j], 1);
