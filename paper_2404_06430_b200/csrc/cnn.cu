@@ -466,8 +466,17 @@ __global__ void __launch_bounds__(HID) head_kernel(const float* __restrict__ par
     const int n = n0 + b;
     float z = 0.f;
     if (n < N && slot_row[n] >= 0) {
+      // the K-split partials: loads issued 7 at a time, summed in split order
       z = bf1;
-      for (int s = 0; s < nsplit; ++s) z += part[((int64_t)s * N + n) * HID + j];
+      int s = 0;
+      for (; s + 7 <= nsplit; s += 7) {
+        float v[7];
+#pragma unroll
+        for (int u = 0; u < 7; ++u) v[u] = part[((int64_t)(s + u) * N + n) * HID + j];
+#pragma unroll
+        for (int u = 0; u < 7; ++u) z += v[u];
+      }
+      for (; s < nsplit; ++s) z += part[((int64_t)s * N + n) * HID + j];
     }
     z3[b][j] = z - corr[b];
   }
