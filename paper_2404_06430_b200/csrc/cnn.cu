@@ -2245,28 +2245,32 @@ __global__ void __launch_bounds__(FMT_THREADS, 1) fc1_mat_tc_kernel(
     for (int i = t; i < nt * FMT_TILE * HID / 4; i += FMT_THREADS) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     return;
   }
-  // U' rows j = s*B + b (zero when inactive); per-client power-of-two beta puts max |U'| at ~2^14
+  // U' rows j = s*B + b (zero when inactive); per-client power-of-two beta puts max |U'| at ~2^14.
+  // The thread's values stay in registers between the max pass and the split (all loads of
+  // the thread in flight together instead of one L2 round trip per element and pass).
+  constexpr int UQ = (FC_RMAX * HID + FMT_THREADS - 1) / FMT_THREADS;
+  float uv[UQ];
   float m = 0.f;
-  for (int i = t; i < FC_RMAX * HID; i += FMT_THREADS) {
-    const int j = i / HID, h = i - j * HID, sp = j / B, bp = j - sp * B;
-    if (j < J && sp < Sc && bp < hs.nbh[sp * hs.cstride + c]) {
-      const int64_t slot = (int64_t)c * B + bp;
-      const float v = hist_coef(lr, mu, Sc, sp) * hs.dz3h[sp * hs.dstride + slot * HID + h] /
-                      pscale_hist[(int64_t)sp * N + slot];
-      m = fmaxf(m, fabsf(v));
-    }
-  }
-  const float beta = block_scale(m, red);
-  for (int i = t; i < FC_RMAX * HID; i += FMT_THREADS) {
+#pragma unroll
+  for (int u = 0; u < UQ; ++u) {
+    const int i = t + u * FMT_THREADS;
     const int j = i / HID, h = i - j * HID, sp = j / B, bp = j - sp * B;
     float v = 0.f;
-    if (j < J && sp < Sc && bp < hs.nbh[sp * hs.cstride + c]) {
+    if (i < FC_RMAX * HID && j < J && sp < Sc && bp < hs.nbh[sp * hs.cstride + c]) {
       const int64_t slot = (int64_t)c * B + bp;
-      v = hist_coef(lr, mu, Sc, sp) * hs.dz3h[sp * hs.dstride + slot * HID + h] / pscale_hist[(int64_t)sp * N + slot] *
-          beta;
+      v = hist_coef(lr, mu, Sc, sp) * hs.dz3h[sp * hs.dstride + slot * HID + h] / pscale_hist[(int64_t)sp * N + slot];
     }
+    uv[u] = v;
+    m = fmaxf(m, fabsf(v));
+  }
+  const float beta = block_scale(m, red);
+#pragma unroll
+  for (int u = 0; u < UQ; ++u) {
+    const int i = t + u * FMT_THREADS;
+    if (i >= FC_RMAX * HID) break;
+    const int j = i / HID, h = i - j * HID;
     __half hi, lo;
-    split_f16(v, hi, lo);
+    split_f16(uv[u] * beta, hi, lo);
     const uint32_t off = (h >> 6) * FMT_BLK + sw128_off16(j, h & 63);
     *reinterpret_cast<__half*>(sB + off) = hi;
     *reinterpret_cast<__half*>(sB + 2 * FMT_BLK + off) = lo;
