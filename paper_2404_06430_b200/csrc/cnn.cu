@@ -2993,19 +2993,25 @@ __global__ void __launch_bounds__(C1F_THREADS, C1F_MINB) conv1_fwd_tc_kernel(
   }
   const float* dc = delta ? delta + (int64_t)(n0 / B) * ld : nullptr;
   const uint32_t sB0 = tc::smem_u32(sB), sA0 = tc::smem_u32(sA), simg = tc::smem_u32(img);
-  // B: rows o (hi) and 32 + o (lo), k = 0..26 weights, 27 bias, 28..31 zero
-  for (int i = t; i < C1 * 32; i += C1F_THREADS) {
-    const int o = i >> 5, k = i & 31;
-    const float v = k < 27 ? wt(theta, dc, O_W1 + o * 27 + k) : (k == 27 ? wt(theta, dc, O_B1 + o) : 0.f);
+  // B: rows o (hi) and 32 + o (lo), k = 0..26 weights, 27 bias, 28..31 zero.  A warp holds
+  // one output channel's 32 k per trip (lane = k), so sum_k |W[o, k]| (the a1 bound) is a
+  // warp reduction of the values already loaded (the loads of all trips in flight together)
+  static_assert(C1F_THREADS % 32 == 0 && (C1 * 32) % C1F_THREADS == 0, "conv1 fwd weight staging");
+  float wv[C1 * 32 / C1F_THREADS];
+#pragma unroll
+  for (int u = 0; u < C1 * 32 / C1F_THREADS; ++u) {
+    const int i = t + u * C1F_THREADS, o = i >> 5, k = i & 31;
+    wv[u] = k < 27 ? wt(theta, dc, O_W1 + o * 27 + k) : (k == 27 ? wt(theta, dc, O_B1 + o) : 0.f);
+  }
+#pragma unroll
+  for (int u = 0; u < C1 * 32 / C1F_THREADS; ++u) {
+    const int i = t + u * C1F_THREADS, o = i >> 5, k = i & 31;
     float hi, lo;
-    tc::split_tf32(v, hi, lo);
+    tc::split_tf32(wv[u], hi, lo);
     tc::sts_f32(sB0 + tc::sw128_offset(o, k), hi);
     tc::sts_f32(sB0 + tc::sw128_offset(C1 + o, k), lo);
-  }
-  if (t < C1) {
-    float sw = 0.f;
-    for (int k = 0; k < 27; ++k) sw += fabsf(wt(theta, dc, O_W1 + t * 27 + k));
-    wsum[t] = sw;
+    const float sw = warp_sum(k < 27 ? fabsf(wv[u]) : 0.f);
+    if (lane == 0) wsum[o] = sw;
   }
   if (warp == 0) {  // active slots of the group, compacted in order (ballot + popc; G <= 32)
     const bool a = lane < G && n0 + lane < N && slot_row[n0 + lane] >= 0;
