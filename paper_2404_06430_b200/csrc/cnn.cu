@@ -3195,7 +3195,7 @@ static_assert(W1_NLD * W1_THREADS == W1_CH * 8 && W1_KPER * (W1_THREADS / W1_CH)
 #ifndef W1_MINB
 #define W1_MINB 2
 #endif
-constexpr int W1_SMEM = 1024 + W1_ASTAGES * W1_STAGE + IMG * 4 + 32 * 33 * 4 + 64;
+constexpr int W1_SMEM = 1024 + W1_ASTAGES * W1_STAGE + 2 * IMG * 4 + 32 * 33 * 4 + 64;
 constexpr uint32_t W1_IDESC = tc::idesc_tf32(128, 64);
 
 template <bool SPLIT>
@@ -3207,10 +3207,11 @@ __global__ void __launch_bounds__(W1_THREADS, W1_MINB) conv1_bwd_w_tc_kernel(con
                                                                       int split, float* __restrict__ wpart) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  float* img = reinterpret_cast<float*>(sm + W1_ASTAGES * W1_STAGE);  // [3][32][32]
-  float* red = img + IMG;                                    // [32][33]: warp 1's sums
+  float* img = reinterpret_cast<float*>(sm + W1_ASTAGES * W1_STAGE);  // [2][3][32][32] (next sample prefetched)
+  float* red = img + 2 * IMG;                                // [32][33]: warp 1's sums
   uint64_t* done = reinterpret_cast<uint64_t*>(red + 32 * 33);  // [2] MMA completion per stage
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 2);
+  uint64_t* imfull = done + 2;                                   // [2] image arrival
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(imfull + 2);
   // split > 1 (few active clients): CTA (c, part) takes samples [b0, b1) and writes a
   // partial [28][32] gradient; conv1_bwd_w_reduce_kernel applies the update
   // (SPLIT = false: the plain one-CTA-per-client kernel, compiled separately)
@@ -3235,6 +3236,8 @@ __global__ void __launch_bounds__(W1_THREADS, W1_MINB) conv1_bwd_w_tc_kernel(con
   if (t == 0) {
     tc::mbar_init(&done[0], 1);
     tc::mbar_init(&done[1], 1);
+    tc::mbar_init(&imfull[0], 1);
+    tc::mbar_init(&imfull[1], 1);
     tc::fence_mbar_init();
   }
   if (warp == 0) tc::tmem_alloc<128>(tmem_slot);
@@ -3294,10 +3297,21 @@ __global__ void __launch_bounds__(W1_THREADS, W1_MINB) conv1_bwd_w_tc_kernel(con
     if (i >= W1_ASTAGES)  // chunk i - W1_ASTAGES's MMAs done reading this stage
       tc::mbar_wait(&done[(i - W1_ASTAGES) & 1], ((i - W1_ASTAGES) >> 1) & 1);
     if (ch == 0) {
-      __syncthreads();  // previous sample's im2col reads finished
-      const float4* src = reinterpret_cast<const float4*>(X + slot_row[n] * IMG);
-      for (int q = t; q < IMG / 4; q += W1_THREADS) reinterpret_cast<float4*>(img)[q] = __ldg(src + q);
+      // the previous sample's im2col reads are finished: its buffer takes sample b + 1 (bulk
+      // async copy, overlapping this sample); sample b's image was fetched one sample ago
       __syncthreads();
+      if (t == 0) {
+        tc::fence_proxy_async();  // (the generic-proxy reads of that buffer precede the async write)
+        if (b == 0) {
+          tc::mbar_arrive_expect_tx(&imfull[0], IMG * 4);
+          tc::bulk_load(img, X + slot_row[n] * IMG, IMG * 4, &imfull[0]);
+        }
+        if (b + 1 < b1 - b0) {
+          tc::mbar_arrive_expect_tx(&imfull[(b + 1) & 1], IMG * 4);
+          tc::bulk_load(img + ((b + 1) & 1) * IMG, X + slot_row[n + 1] * IMG, IMG * 4, &imfull[(b + 1) & 1]);
+        }
+      }
+      tc::mbar_wait(&imfull[b & 1], (b >> 1) & 1);
     }
 #pragma unroll
     for (int j = 0; j < W1_NLD; ++j) {
@@ -3319,7 +3333,7 @@ __global__ void __launch_bounds__(W1_THREADS, W1_MINB) conv1_bwd_w_tc_kernel(con
       const int p = p0 + pl, y = p / S1, x = p - y * S1;
       const bool valid = p < S1 * S1;
       const uint32_t atom = stg + (pl >> 5) * W1_ATOM + 8192;
-      const uint32_t ib = simg + 4 * (y * S0 + x);
+      const uint32_t ib = simg + (b & 1) * IMG * 4 + 4 * (y * S0 + x);
 #pragma unroll
       for (int kk = 0; kk < 7; ++kk) {
         const int k = kq * 7 + kk;
