@@ -309,6 +309,8 @@ class GpuSimulationEngine:
         self._pf_pending = None
         self._plans: dict = {}      # host plans computed ahead (key: population, seed, cohort size, epochs)
         self._planned: set = set()
+        # per population: this rank's queue and its per-client eval / norm / clip results of the last context
+        self.last_client_results: dict = {}
 
     @property
     def num_workers(self) -> int:
@@ -686,6 +688,9 @@ class GpuSimulationEngine:
         h_norm = host_res[8 * Cp: 16 * Cp].view(torch.float64).numpy()[:C]
         h_ints = host_res[16 * Cp:].view(torch.int32).numpy()
         h_correct, h_clipped, h_bad = h_ints[:C], h_ints[Cp:Cp + C], h_ints[2 * Cp:2 * Cp + C]
+        self.last_client_results[pop_key.value] = dict(queue=tuple(queue), loss=h_loss.copy(),
+                                                       correct=h_correct.copy(), norm=h_norm.copy(),
+                                                       clipped=h_clipped.copy())
 
         if train and C and h_bad.any():
             uid = queue[int(np.flatnonzero(h_bad)[0])]
