@@ -227,6 +227,30 @@ int fb_weighted_sum_f32(const float* delta, int64_t ld_delta, int num_clients, i
                         const float* coef, float* agg, int accumulate,
                         void* workspace, int64_t workspace_bytes, void* stream);
 
+/* ------------------------------------------------ a9 (worker_reduce)
+ * Per-context sums over the C clients of this rank, fp64 in a fixed order,
+ * written as fp32 (hi, lo) pairs: tail[2f] + tail[2f+1] == sum f (hi alone
+ * exact for integer-valued sums < 2^24).  The tail sits behind the payload in
+ * one flat fp32 buffer so a single all-reduce replaces the reference's
+ * worker_reduce of payload + bookkeeping (fedsim/engine/aggregator.py:55-62)
+ * and the metric merge (fedsim/engine/runtime.py:148-153).  Fields:        */
+#define FB_SUM_LOSS 0      /* sum eval loss            (fedsim/algorithms/fedavg.py:127-139) */
+#define FB_SUM_CORRECT 1   /* sum correct predictions                                      */
+#define FB_SUM_POINTS 2    /* sum n_c                                                      */
+#define FB_SUM_USER_ACC 3  /* sum correct_c / n_c      (fedsim/core/metrics.py:52-53)      */
+#define FB_SUM_USERS 4     /* number of clients                                            */
+#define FB_SUM_CLIPPED 5   /* sum clip indicators      (fedsim/privacy/clipping.py:113-116)  */
+#define FB_SUM_COUNT 6     /* training clients                                             */
+#define FB_SUM_NORM 7      /* sum pre-clip norms                                           */
+#define FB_SUM_WEIGHT 8    /* sum w_c                  (fedsim/core/statistics.py:96-102)  */
+#define FB_SUM_NONFINITE 9 /* clients with a non-finite update (fedsim/engine/runtime.py:202-208) */
+#define FB_NUM_SUMS 10
+/* train = 0 (evaluation context): norm / clipped / nonfinite / w may be NULL and
+ * fields 5..9 are 0.  tail: 2 * FB_NUM_SUMS floats (OVERWRITTEN).           */
+int fb_context_sums(const double* loss, const int32_t* correct, const int32_t* num_rows, const double* norm,
+                    const int32_t* clipped, const int32_t* nonfinite, const float* w, int num_clients, int train,
+                    float* tail, void* stream);
+
 /* ------------------------------------------------- a10 helpers (K4 SNR)
  * out[0] = sum_i x[i]^2 in fp64 (OVERWRITTEN).  workspace >= 8 KiB.         */
 int fb_sumsq_f32(const float* x, int64_t n, double* out, void* workspace,

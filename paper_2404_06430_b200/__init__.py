@@ -1,13 +1,16 @@
 """B200-native central-iteration engine for private federated learning
 simulation (pfl-research, arXiv 2404.06430, as restated by fedsim).
 
-Public surface mirrors the reference's names (FedAvg, ClippingPostprocessor,
-GaussianCentralMechanism, SumAggregator, run_simulation, ...) and adds
-``GpuSimulationEngine``, the drop-in for fedsim's SimulationEngine whose
-cohort work runs in hand-written sm_100a kernels (libfedsim_b200.so).
+``GpuSimulationEngine`` is the drop-in for fedsim's SimulationEngine: fedsim's
+own ``run_simulation`` drives it with fedsim's own algorithm, postprocessor
+and aggregator objects (recognised by duck typing, see ``interop``), and the
+cohort work runs in hand-written sm_100a kernels (libfedsim_b200.so).  The
+package also keeps the reference's names (FedAvg, ClippingPostprocessor,
+GaussianCentralMechanism, SumAggregator, ...) in device-resident form, whose
+parameters and aggregates stay in HBM between iterations.
 """
 
-from .aggregator import Aggregator, SumAggregator, worker_reduce_sum
+from .aggregator import Aggregator, SumAggregator
 from .algorithms import (
     AdaFedProx,
     AlgorithmState,
@@ -48,6 +51,7 @@ from .core import (
 )
 from .device import ControlStore, DeviceParams, DevicePopulation, DeviceStatistics
 from .engine import GpuSimulationEngine, IterationResult, client_permutations
+from .interop import cohort_plan, native_model
 from .errors import (
     CohortTooLarge,
     DataError,
@@ -71,7 +75,6 @@ from .feddata import (
     sample_cohort,
     save_partition,
 )
-from .loop import MetricsRow, SimulationResult, run_simulation
 from .models import CNN, MLP, AdamOptimizer, LogisticRegression, Model, SGDOptimizer, central_step, count_local_steps
 from .privacy import (
     AdaptiveClipConfig,

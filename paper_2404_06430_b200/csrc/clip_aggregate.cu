@@ -188,6 +188,45 @@ __global__ void sumsq_final_kernel(const double* __restrict__ part, int nblk, do
   if (threadIdx.x == 0) *out = s;
 }
 
+
+// Per-context metric / bookkeeping sums (fp64, fixed order) written as fp32 hi + lo pairs
+// into the tail of the buffer the ranks all-reduce, so one collective carries payload and
+// sums (fedsim/engine/aggregator.py:55-62 reduces both in one worker_reduce).  Fields in
+// FB_SUM_* order; integer-valued sums are exact in the hi word (< 2^24).
+__global__ void __launch_bounds__(kThreads) context_sums_kernel(
+    const double* __restrict__ loss, const int32_t* __restrict__ correct, const int32_t* __restrict__ num_rows,
+    const double* __restrict__ norm, const int32_t* __restrict__ clipped, const int32_t* __restrict__ nonfinite,
+    const float* __restrict__ w, int C, int train, float* __restrict__ tail) {
+  __shared__ double red[32];
+  double a[FB_NUM_SUMS];
+#pragma unroll
+  for (int f = 0; f < FB_NUM_SUMS; ++f) a[f] = 0.0;
+  for (int c = threadIdx.x; c < C; c += kThreads) {
+    const double n = (double)num_rows[c], k = (double)correct[c];
+    a[FB_SUM_LOSS] += loss[c];
+    a[FB_SUM_CORRECT] += k;
+    a[FB_SUM_POINTS] += n;
+    a[FB_SUM_USER_ACC] += n > 0.0 ? k / n : 0.0;
+    a[FB_SUM_USERS] += 1.0;
+    if (train) {
+      a[FB_SUM_CLIPPED] += (double)clipped[c];
+      a[FB_SUM_COUNT] += 1.0;
+      a[FB_SUM_NORM] += nonfinite[c] ? 0.0 : norm[c];
+      a[FB_SUM_WEIGHT] += (double)w[c];
+      a[FB_SUM_NONFINITE] += (double)(nonfinite[c] != 0);
+    }
+  }
+#pragma unroll
+  for (int f = 0; f < FB_NUM_SUMS; ++f) {
+    const double s = block_sum(a[f], red);
+    if (threadIdx.x == 0) {
+      const float hi = (float)s;
+      tail[2 * f] = hi;
+      tail[2 * f + 1] = (float)(s - (double)hi);
+    }
+  }
+}
+
 int g_sms = 0;
 int sm_count() {
   if (!g_sms) {
@@ -332,6 +371,19 @@ int fb_sumsq_f32(const float* x, int64_t n, double* out, void* workspace, int64_
   if (st) return st;
   FB_LAUNCH("sumsq_final_kernel", s, fb::sumsq_final_kernel<<<1, 256, 0, s>>>(part, (int)nb, out));
   return fb::launch_status("sumsq_final_kernel");
+}
+
+int fb_context_sums(const double* loss, const int32_t* correct, const int32_t* num_rows, const double* norm,
+                    const int32_t* clipped, const int32_t* nonfinite, const float* w, int num_clients, int train,
+                    float* tail, void* stream) {
+  FB_REQUIRE(num_clients >= 0, "context_sums: negative client count");
+  FB_REQUIRE(tail != nullptr && num_rows != nullptr, "context_sums: null tail / num_rows");
+  FB_REQUIRE(num_clients == 0 || (loss && correct), "context_sums: null loss / correct");
+  FB_REQUIRE(!train || num_clients == 0 || (norm && clipped && nonfinite && w), "context_sums: null training arrays");
+  cudaStream_t s = fb::as_stream(stream);
+  FB_LAUNCH("context_sums_kernel", s, fb::context_sums_kernel<<<1, fb::kThreads, 0, s>>>(
+      loss, correct, num_rows, norm, clipped, nonfinite, w, num_clients, train, tail));
+  return fb::launch_status("context_sums_kernel");
 }
 
 }  // extern "C"

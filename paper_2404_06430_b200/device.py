@@ -119,6 +119,12 @@ class Comm:
     group: object | None = None
     epilogue: str = "rank0"   # "rank0": step on rank 0 + broadcast; "replicated"
 
+    def root(self) -> int:
+        """Global rank of the group's rank 0 (broadcast takes global ranks)."""
+        if self.group is None:
+            return 0
+        return _torch().distributed.get_global_rank(self.group, 0)
+
 
 @dataclass
 class DeviceStatistics:
@@ -206,7 +212,7 @@ class DeviceStatistics:
                 float(self.scale), float(lr), None, native.stream_handle(),
             )
         if comm.world_size > 1 and comm.epilogue == "rank0":
-            torch.distributed.broadcast(out, src=0, group=comm.group)
+            torch.distributed.broadcast(out, src=comm.root(), group=comm.group)
         return DeviceParams(out, params.dims)
 
     def apply_adam(self, params: DeviceParams, opt, lr: float) -> DeviceParams:
@@ -234,7 +240,7 @@ class DeviceStatistics:
                 int(opt.step_count), None, native.stream_handle(),
             )
         if comm.world_size > 1 and comm.epilogue == "rank0":
-            torch.distributed.broadcast(out, src=0, group=comm.group)
+            torch.distributed.broadcast(out, src=comm.root(), group=comm.group)
         return DeviceParams(out, params.dims)
 
     def split_payload(self, sizes: Sequence[int]) -> list["DeviceStatistics"]:
@@ -280,6 +286,19 @@ class DeviceStatistics:
         if self.scale != 1.0:
             x = (x.double() * self.scale).float()
         return x
+
+    @classmethod
+    def from_host(cls, stats, device, workspace: Workspace | None = None, comm: Comm | None = None) -> "DeviceStatistics":
+        """Host statistics (entries name -> vector, ``_``-prefixed bookkeeping
+        kept on the host) as a device aggregate with nothing pending."""
+        torch = _torch()
+        dims = {n: int(np.asarray(v).size) for n, v in stats.entries.items() if not n.startswith("_")}
+        book = {n: np.asarray(v, dtype=np.float64) for n, v in stats.entries.items() if n.startswith("_")}
+        host = (np.concatenate([np.asarray(stats.entries[n], dtype=np.float64).ravel() for n in dims])
+                if dims else np.zeros(0))
+        flat = torch.from_numpy(host.astype(np.float32)).to(device)
+        return cls(flat=flat, dims=dims, weight=float(stats.weight), bookkeeping=book, workspace=workspace,
+                   comm=comm if comm is not None else Comm())
 
     def to_host(self) -> Statistics:
         host = self.materialize().to("cpu", dtype=_torch().float64).numpy()
@@ -327,6 +346,7 @@ class DevicePopulation:
             self.y = torch.from_numpy(y).pin_memory()
         self.total_rows = total
         self.max_label = int(y.max()) if total else 0
+        self.min_label = int(y.min()) if total else 0
 
 
 class ControlStore:

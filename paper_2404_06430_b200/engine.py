@@ -25,22 +25,14 @@ from typing import Any, Mapping, Sequence
 
 import numpy as np
 
-from . import cnn, native
-from .aggregator import SumAggregator
+from . import cnn, interop, native
 from .core import CentralContext, MetricKind, MetricValue, Population, merge_metrics, user_seed
 from .algorithms import CONTROL_PREFIX, MODEL_PREFIX
 from .device import Comm, ControlStore, ControlUpdates, DeviceParams, DevicePopulation, DeviceStatistics, Workspace
 from .errors import EngineError
 from .feddata import FederatedDataset, sample_cohort
 from .models import CNN, MLP, LogisticRegression
-from .privacy import (
-    CLIPPED_KEY,
-    COUNT_KEY,
-    NORM_KEY,
-    ClippingPostprocessor,
-    GaussianCentralMechanism,
-    validate_pipeline,
-)
+from .privacy import CLIPPED_KEY, COUNT_KEY, NORM_KEY, validate_pipeline
 from .scheduling import compute_base_weight, schedule_users
 
 
@@ -96,23 +88,53 @@ PREFETCH_MAX_RUNS = 64
 # largest single memcpy of a run (measured e2e: one copy per run 18.7 it/s, 8 MB chunks 18.5)
 PREFETCH_CHUNK_BYTES = 1 << 30
 
-# layout of the per-context fp64 sums reduced across ranks
-SUM_FIELDS = ("loss", "correct", "points", "per_user_acc", "users", "clipped", "count", "norm", "weight")
+# per-context sums reduced across ranks (FB_SUM_* in include/fedsim_b200.h), carried as fp32
+# (hi, lo) pairs in the tail of the one buffer that is all-reduced
+SUM_FIELDS = ("loss", "correct", "points", "per_user_acc", "users", "clipped", "count", "norm", "weight",
+              "nonfinite")
+NUM_SUMS = len(SUM_FIELDS)
+TAIL = 2 * NUM_SUMS
 
 
-def reduce_across_ranks(sums: np.ndarray, agg_flat, group=None) -> np.ndarray:
-    """worker_reduce across ranks (fedsim/engine/aggregator.py:46-62): one
-    all-reduce(SUM) of the flat payload (NCCL over NVLink on GPUs) and one of
-    the fp64 metric / bookkeeping sums.  Returns the reduced sums."""
+def pack_sums(sums: np.ndarray) -> np.ndarray:
+    """fp64 sums -> the fp32 (hi, lo) tail fb_context_sums writes."""
+    s = np.asarray(sums, dtype=np.float64)
+    hi = s.astype(np.float32)
+    lo = (s - hi.astype(np.float64)).astype(np.float32)
+    return np.stack([hi, lo], axis=1).ravel()
+
+
+def unpack_sums(tail: np.ndarray) -> np.ndarray:
+    t = np.asarray(tail, dtype=np.float32).astype(np.float64).reshape(-1, 2)
+    return t[:, 0] + t[:, 1]
+
+
+def reduce_across_ranks(buf, group=None) -> None:
+    """worker_reduce across ranks (fedsim/engine/aggregator.py:46-62): ONE
+    all-reduce(SUM) of the flat fp32 buffer [payload | sums tail] (NCCL over
+    NVLink on GPUs), in place.  No host synchronisation before it: the tail
+    is written on the device by fb_context_sums."""
+    _torch().distributed.all_reduce(buf, group=group)
+
+
+def first_bad_user(local_pos: int, rank: int, world_size: int, group=None) -> tuple[int, int]:
+    """(rank, queue position) of the first client with a non-finite update in
+    rank-then-queue order -- the error the reference raises first (its worker
+    futures are read in worker-index order, fedsim/engine/runtime.py:139-147).
+    Collective over the group (error path only); local_pos < 0 = none here."""
     torch = _torch()
-    dist = torch.distributed
-    dev = agg_flat.device if agg_flat is not None else (
-        torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else torch.device("cpu"))
-    t = torch.from_numpy(np.ascontiguousarray(sums, dtype=np.float64)).to(dev)
-    dist.all_reduce(t, group=group)
-    if agg_flat is not None:
-        dist.all_reduce(agg_flat, group=group)
-    return t.cpu().numpy()
+    big = (1 << 62)
+    key = big if local_pos < 0 else (rank << 32) + local_pos
+    if world_size > 1:
+        dist = torch.distributed
+        dev = (torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl"
+               else torch.device("cpu"))
+        t = torch.tensor([key], dtype=torch.int64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+        key = int(t.item())
+    if key >= big:
+        return -1, -1
+    return key >> 32, key & 0xFFFFFFFF
 
 
 def native_permutations(ctx_seed: int, user_ids: Sequence[str], num_rows: np.ndarray, epochs: int,
@@ -189,6 +211,8 @@ class _ModelRunner:
         elif isinstance(model, LogisticRegression):
             self.kind, self.dims = "linear", (model.dim, model.num_classes)
         elif isinstance(model, CNN):
+            if model != CNN():  # csrc/cnn.cu is compiled for exactly this geometry
+                raise ValueError(f"GpuSimulationEngine: the CNN kernels are compiled for {CNN()}, got {model}")
             self.kind, self.dims = "cnn", ()
         else:
             raise ValueError(f"GpuSimulationEngine: unsupported model {type(model).__name__}")
@@ -252,19 +276,8 @@ class GpuSimulationEngine:
         if num_workers < 1:
             raise ValueError("num_workers must be >= 1")
         validate_pipeline(postprocessors)
-        for p in postprocessors:
-            if isinstance(p, ClippingPostprocessor):
-                if p.norm_order != 2.0:
-                    raise ValueError("GpuSimulationEngine supports L2 clipping only")
-            elif isinstance(p, GaussianCentralMechanism):
-                if p.privatize_bookkeeping:
-                    raise ValueError("privatize_bookkeeping is not supported on the GPU path")
-            else:
-                raise ValueError(f"GpuSimulationEngine: unsupported postprocessor {type(p).__name__}")
-        if sum(isinstance(p, ClippingPostprocessor) for p in postprocessors) > 1:
-            raise ValueError("GpuSimulationEngine supports at most one clipping postprocessor")
-        if aggregator is not None and not isinstance(aggregator, SumAggregator):
-            raise ValueError(f"GpuSimulationEngine: unsupported aggregator {type(aggregator).__name__}")
+        interop.check_postprocessors(postprocessors)   # the reference's own objects or this package's
+        interop.check_aggregator(aggregator)
         if central_epilogue not in ("rank0", "replicated"):
             raise ValueError("central_epilogue must be 'rank0' or 'replicated'")
         if data_residency not in ("device", "host"):
@@ -284,8 +297,8 @@ class GpuSimulationEngine:
         self._datasets = dict(datasets)
         self._num_workers = int(num_workers)
         self._postprocessors = tuple(postprocessors)
-        self._clip = next((p for p in postprocessors if isinstance(p, ClippingPostprocessor)), None)
-        self._aggregator = aggregator if aggregator is not None else SumAggregator()
+        self._clip = next((p for p in postprocessors if interop.is_clipping(p)), None)
+        self._aggregator = aggregator  # None or a SumAggregator: run as K3 + the rank all-reduce
         self._base_policy = base_policy
         self._base_value = float(base_value)
         self._cohort_mode = cohort_mode
@@ -309,8 +322,11 @@ class GpuSimulationEngine:
         self._pf_pending = None
         self._plans: dict = {}      # host plans computed ahead (key: population, seed, cohort size, epochs)
         self._planned: set = set()
-        # per population: this rank's queue and its per-client eval / norm / clip results of the last context
+        # record_clients: keep this rank's queue and its per-client eval / norm / clip results of
+        # the last context of each population (one extra D2H copy; tests and diagnostics)
+        self.record_clients = False
         self.last_client_results: dict = {}
+        self._theta_cache = None  # (host params object, its DeviceParams) for the reference's host params
 
     @property
     def num_workers(self) -> int:
@@ -326,16 +342,17 @@ class GpuSimulationEngine:
         return self._pops[pop]
 
     def _runner(self, model) -> _ModelRunner:
-        key = id(model)
+        key = model  # frozen dataclass layouts: equal layouts share a runner
         if key not in self._runners:
             self._runners[key] = _ModelRunner(model, self.ws)
         return self._runners[key]
 
     # ------------------------------------------------------------------ API
     def run_iteration(self, algorithm, state, contexts: Sequence[CentralContext]) -> IterationResult:
-        if not hasattr(algorithm, "cohort_plan"):
+        own = interop.is_own(algorithm)
+        if not own and "FedAvg" not in interop.class_names(algorithm):
             raise ValueError(f"GpuSimulationEngine: unsupported algorithm {type(algorithm).__name__}")
-        if not isinstance(state.params, DeviceParams):
+        if own and not isinstance(state.params, DeviceParams):
             state.params = DeviceParams.from_host(state.params, self.device)
         aggregates, metrics, cohorts, updates = [], {}, [], []
         if self._prefetch and contexts:
@@ -507,6 +524,48 @@ class GpuSimulationEngine:
                 hp["perms"] = native_permutations(ctx.seed, hp["queue"], num_rows, epochs, perm_off,
                                                   self._repr_cache)
 
+    def _theta(self, state) -> DeviceParams:
+        """theta_t on the device.  This package's algorithms keep it there; the
+        reference's keep host float64 ModelParams (fedsim/models/params.py:17),
+        uploaded once per new params object (one per iteration)."""
+        if isinstance(state.params, DeviceParams):
+            return state.params
+        cached = self._theta_cache
+        if cached is None or cached[0] is not state.params:
+            cached = self._theta_cache = (state.params, DeviceParams.from_host(state.params, self.device))
+        return cached[1]
+
+    def _clip_bound(self) -> float:
+        return float(self._clip.current_bound) if self._clip is not None else 0.0
+
+    def _host_controls(self, state, queue, D: int):
+        """The reference's Scaffold keeps controls on the host (fedsim/algorithms/
+        scaffold.py:34-57): server control and the queue's user controls are
+        uploaded into a transient device store for the correction / payload kernels."""
+        torch = _torch()
+        names = list(state.params)
+        server_h = state.extra["server_control"]
+        server = torch.from_numpy(np.concatenate([np.asarray(server_h[n], dtype=np.float64).ravel()
+                                                  for n in names]).astype(np.float32)).to(self.device)
+        store = ControlStore(D, self.device)
+        users = state.extra["user_controls"]
+        known = [u for u in queue if u in users]
+        if known:
+            mat = np.stack([np.concatenate([np.asarray(users[u][n], dtype=np.float64).ravel() for n in names])
+                            for u in known]).astype(np.float32)
+            store.set_rows(known, torch.from_numpy(mat).to(self.device))
+        return server, store
+
+    def _host_updates(self, updates, state):
+        """ControlUpdates -> the reference's user_updates: (uid, {name: float64 vector})."""
+        if updates is None:
+            return []
+        names = list(state.params)
+        offs = np.cumsum([0] + [int(np.asarray(state.params[n]).size) for n in names])
+        mat = updates.matrix[:, : offs[-1]].double().cpu().numpy() if len(updates.uids) else None
+        return [(u, {n: mat[c, offs[i]:offs[i + 1]].copy() for i, n in enumerate(names)})
+                for c, u in enumerate(updates.uids)]
+
     def _controls(self, state, D: int):
         """SCAFFOLD server control (flat fp32) and per-user control store,
         created on the device on first use (zero, as the reference)."""
@@ -528,13 +587,17 @@ class GpuSimulationEngine:
         if not cohort:
             return None, {}, cohort, None
 
-        plan = algorithm.cohort_plan(state, ctx)
+        plan = interop.cohort_plan(algorithm, state, ctx)
+        own = interop.is_own(algorithm)
         runner = self._runner(plan.model)
         scaffold = bool(getattr(plan, "scaffold", False)) and plan.train is not None
         pop = self.population(pop_key)
         if pop.dim != plan.model.input_dim:
             raise ValueError(f"dataset dim {pop.dim} != model input dim {plan.model.input_dim}")
-        theta: DeviceParams = state.params
+        if pop.total_rows and (pop.min_label < 0 or pop.max_label >= plan.model.num_classes):
+            raise ValueError(f"labels of population {pop_key.value!r} lie in [{pop.min_label}, {pop.max_label}], "
+                             f"outside the model's {plan.model.num_classes} classes")
+        theta = self._theta(state)
         C = len(queue)
         stream = native.stream_handle(self.stream)
         idx = np.fromiter((pop.index[u] for u in queue), dtype=np.int64, count=C)
@@ -613,16 +676,21 @@ class GpuSimulationEngine:
 
         agg_flat = None
         updates = None
+        d_w = None
         if train:
             d_perms, d_perm_off, d_w = dev[2], dev[3], dev[4]
             # SCAFFOLD: the payload is [model delta | control delta] (fedsim/algorithms/scaffold.py:63-79)
             Dp = 2 * runner.D if scaffold else runner.D
-            agg_flat = torch.empty(Dp, dtype=torch.float32, device=self.device)
+            # one flat buffer [payload | sums tail]: the only thing the ranks all-reduce
+            red = torch.empty(Dp + TAIL, dtype=torch.float32, device=self.device)
+            agg_flat = red[:Dp]
+            if scaffold:  # every rank owns a store, also with an empty shard (its queue may be empty)
+                server, store = (self._controls(state, runner.D) if own
+                                 else self._host_controls(state, queue, runner.D))
             if C:
                 delta = self.ws.tensor("delta", (C, runner.ld), torch.float32)
                 control = None
                 if scaffold:
-                    server, store = self._controls(state, runner.D)
                     d_rows = torch.from_numpy(store.rows_of(queue)).to(self.device, non_blocking=True)
                     control = self.ws.tensor("scaffold_correction", (C, runner.ld), torch.float32)
                     native.call("fb_scaffold_correction_f32", native.ptr(server), native.ptr(store.matrix()),
@@ -642,7 +710,7 @@ class GpuSimulationEngine:
                                 runner.D, native.ptr(payload), ldp, native.ptr(new_control), runner.ld, stream)
                     updates = ControlUpdates(queue, new_control)
                 coef = self.ws.tensor("coef", (Cp,), torch.float32)
-                bound = self._clip.current_bound if self._clip is not None else 0.0
+                bound = self._clip_bound()
                 wsb = native.call("fb_clip_workspace_bytes", C, Dp) + 16 * C  # (+ the two-range K2 variant)
                 kws = self.ws.get("clip_ws", wsb)
                 nf2 = self.ws.tensor("nonfinite2", (Cp,), torch.int32)
@@ -676,37 +744,39 @@ class GpuSimulationEngine:
                 agg_flat.zero_()
             if scaffold and self.world_size > 1:  # every rank's store takes the whole cohort's controls
                 updates = self._gather_controls(hp["queues"], updates, runner.ld)
+        else:
+            red = torch.empty(TAIL, dtype=torch.float32, device=self.device)
+        native.call("fb_context_sums", native.ptr(loss), native.ptr(correct), native.ptr(d_num_rows),
+                    native.ptr(norm), native.ptr(clipped), native.ptr(nonfinite), native.ptr(d_w), C, int(train),
+                    native.ptr(red) + 4 * (red.numel() - TAIL), stream)
+        if self.world_size > 1:
+            reduce_across_ranks(red, self.group)
 
         # the host half of the next iteration (sampling, LPT shard, permutations) runs here,
         # while the GPU works through this context, instead of between iterations
         if train:
             self._plan_ahead(algorithm, state, ctx.iteration + 1)
-        # one D2H copy of the per-client results
-        host_res = res[: 16 * Cp + 12 * Cp].to("cpu", non_blocking=False)
-        self.io_bytes["d2h"] += int(host_res.numel())
-        h_loss = host_res[: 8 * Cp].view(torch.float64).numpy()[:C]
-        h_norm = host_res[8 * Cp: 16 * Cp].view(torch.float64).numpy()[:C]
-        h_ints = host_res[16 * Cp:].view(torch.int32).numpy()
-        h_correct, h_clipped, h_bad = h_ints[:C], h_ints[Cp:Cp + C], h_ints[2 * Cp:2 * Cp + C]
-        self.last_client_results[pop_key.value] = dict(queue=tuple(queue), loss=h_loss.copy(),
-                                                       correct=h_correct.copy(), norm=h_norm.copy(),
-                                                       clipped=h_clipped.copy())
-
-        if train and C and h_bad.any():
-            uid = queue[int(np.flatnonzero(h_bad)[0])]
-            raise EngineError(
-                f"iteration {ctx.iteration}, population {pop_key.value!r}, user {uid!r}: "
-                "entry contains non-finite values"
-            )
-        n_f = num_rows.astype(np.float64)
-        sums = np.array([
-            h_loss.sum(), float(h_correct.sum()), n_f.sum(), (h_correct / n_f).sum() if C else 0.0, float(C),
-            float(h_clipped.sum()) if train else 0.0, float(C) if train else 0.0,
-            float(h_norm.sum()) if train else 0.0,
-            float((n_f if plan.weighting == "datapoints" else np.ones(C)).sum()) if train else 0.0,
-        ], dtype=np.float64)
-        if self.world_size > 1:
-            sums = reduce_across_ranks(sums, agg_flat, self.group)
+        # one small D2H copy: the reduced sums (waits for this context's kernels and the reduce)
+        sums = unpack_sums(red[-TAIL:].to("cpu").numpy())
+        self.io_bytes["d2h"] += 4 * TAIL
+        if self.record_clients or (train and sums[9] > 0):
+            host_res = res[: 16 * Cp + 12 * Cp].to("cpu")
+            self.io_bytes["d2h"] += int(host_res.numel())
+            h_ints = host_res[16 * Cp:].view(torch.int32).numpy()
+            h_bad = h_ints[2 * Cp:2 * Cp + C]
+            if self.record_clients:
+                self.last_client_results[pop_key.value] = dict(
+                    queue=tuple(queue), loss=host_res[: 8 * Cp].view(torch.float64).numpy()[:C].copy(),
+                    norm=host_res[8 * Cp: 16 * Cp].view(torch.float64).numpy()[:C].copy(),
+                    correct=h_ints[:C].copy(), clipped=h_ints[Cp:Cp + C].copy())
+            if train and sums[9] > 0:  # raised on EVERY rank (the count came through the all-reduce)
+                bad = np.flatnonzero(h_bad)
+                r, pos = first_bad_user(int(bad[0]) if len(bad) else -1, self.rank, self.world_size, self.group)
+                uid = hp.get("queues", (queue,))[r][pos]
+                raise EngineError(
+                    f"iteration {ctx.iteration}, population {pop_key.value!r}, user {uid!r}: "
+                    "entry contains non-finite values"
+                )
         metrics: dict[str, MetricValue] = {}
         if sums[4] > 0:
             metrics = {
@@ -728,6 +798,8 @@ class GpuSimulationEngine:
                                      bookkeeping=book, workspace=self.ws, comm=self._comm)
         for proc in reversed(self._postprocessors):
             try:
+                if not interop.is_own(proc) and isinstance(aggregate, DeviceStatistics):
+                    aggregate = aggregate.to_host()  # the reference's own server half runs on host Statistics
                 aggregate, server_metrics = proc.postprocess_server(aggregate, ctx)
             except Exception as exc:
                 raise EngineError(
@@ -735,4 +807,10 @@ class GpuSimulationEngine:
                     f"{type(proc).__name__} failed: {exc}"
                 ) from exc
             metrics = merge_metrics(metrics, server_metrics)
+        if not own:  # the reference's central step consumes host Statistics and host user_updates
+            if isinstance(aggregate, DeviceStatistics):
+                aggregate = aggregate.to_host()
+            updates = self._host_updates(updates, state) if scaffold else updates
+        elif not isinstance(aggregate, DeviceStatistics):
+            aggregate = DeviceStatistics.from_host(aggregate, self.device, workspace=self.ws, comm=self._comm)
         return aggregate, metrics, cohort, updates

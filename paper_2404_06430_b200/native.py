@@ -63,6 +63,7 @@ SIGNATURES: dict[str, tuple] = {
     "fb_weighted_sum_workspace_bytes": (_i64, [_i32, _i64]),
     "fb_weighted_sum_f32": (_i32, [_p, _i64, _i32, _i64, _p, _p, _i32, _p, _i64, _p]),
     "fb_sumsq_f32": (_i32, [_p, _i64, _p, _p, _i64, _p]),
+    "fb_context_sums": (_i32, [_p, _p, _p, _p, _p, _p, _p, _i32, _i32, _p, _p]),
     "fb_gaussian_f32": (_i32, [_p, _i64, _f64, _u64, _u64, _i32, _p]),
     "fb_noise_avg_sgd_f32": (_i32, [_p, _p, _i64, _f64, _u64, _p, _f64, _f64, _p, _p]),
     "fb_scaffold_correction_f32": (_i32, [_p, _p, _i64, _p, _i32, _i64, _p, _i64, _p]),

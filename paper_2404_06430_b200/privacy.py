@@ -173,8 +173,12 @@ class GaussianCentralMechanism:
         if std == 0.0 or not payload:
             return stats, metrics
         seed = noise_seed(self.noise_base_seed, context.iteration, context.population.value)
-        if not hasattr(stats, "with_noise"):
-            raise TypeError("GaussianCentralMechanism expects the GPU engine's DeviceStatistics")
+        if not hasattr(stats, "with_noise"):  # host Statistics (the reference's algorithms): numpy draws,
+            rng = make_rng(seed)              # entry by entry (fedsim/privacy/mechanisms.py:58-75)
+            entries = dict(stats.entries)
+            for n in payload:
+                entries[n] = np.asarray(entries[n], dtype=np.float64) + rng.normal(0.0, std, entries[n].size)
+            return Statistics(entries=entries, weight=stats.weight), metrics
         if self.noise_source == "numpy":
             import torch
 

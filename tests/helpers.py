@@ -95,5 +95,44 @@ def golden_rows(g):
             for t, p, n, v, w in zip(g["row_t"], g["row_pop"], g["row_name"], g["row_value"], g["row_weight"])]
 
 
-__all__ = ["CONFIGS", "product_datasets", "product_model", "product_algorithm", "oracle_model", "product_run_parts", "oracle_run",
+__all__ = ["run_sim", "CONFIGS", "product_datasets", "product_model", "product_algorithm", "oracle_model", "product_run_parts", "oracle_run",
            "golden_rows", "users_of", "noise_base"]
+
+
+def run_sim(algorithm, engine, callbacks=()):
+    """The outer loop for tests that do not use fedsim itself: contexts ->
+    engine.run_iteration -> algorithm fold -> metric rows sorted by
+    (population, name) -> callbacks (fedsim/engine/loop.py:62 semantics,
+    cohort digest over repr((t, population, cohort))).  Test infrastructure;
+    the product is driven by fedsim's own run_simulation."""
+    import hashlib
+    from types import SimpleNamespace
+
+    state = algorithm.initial_state()
+    rows, digest, t = [], hashlib.sha256(), 0
+    while True:
+        contexts = algorithm.get_next_central_contexts(state, t)
+        if not contexts:
+            break
+        res = engine.run_iteration(algorithm, state, contexts)
+        state = algorithm.process_aggregated_statistics_all_contexts(state, contexts, res.aggregates, res.metrics,
+                                                                     res.user_updates)
+        for pop, cohort in res.cohorts:
+            digest.update(repr((t, pop, cohort)).encode())
+        it_rows = [(t, pop, name, mv.value, mv.denominator) for (pop, name), mv in sorted(res.metrics.items())]
+        rows.extend(it_rows)
+        if any([bool(cb(state.params, tuple(it_rows), t)) for cb in callbacks]):
+            t += 1
+            break
+        t += 1
+    return SimulationResult(state=state, metrics_rows=rows, iterations_run=t, cohort_digest=digest.hexdigest())
+
+
+class SimulationResult:
+    def __init__(self, state, metrics_rows, iterations_run, cohort_digest):
+        self.state, self.metrics_rows, self.iterations_run, self.cohort_digest = (state, metrics_rows,
+                                                                                  iterations_run, cohort_digest)
+
+    @property
+    def params(self):
+        return self.state.params

@@ -102,6 +102,7 @@ def test_central_iteration_at_bench_shape_matches_oracle(bench_data, cohort):
     mech = fb.GaussianCentralMechanism(clip, sigma=WL["sigma"], r=r, noise_base_seed=noise_base,
                                        noise_source="numpy")
     eng = fb.GpuSimulationEngine(ds, postprocessors=[clip, mech])
+    eng.record_clients = True
     state = alg.initial_state()
     ctx = alg.get_next_central_contexts(state, 0)[0]
     res = eng.run_iteration(alg, state, (ctx,))
@@ -168,6 +169,7 @@ def _engine_round(ds, factored):
                     run_seed=0, init_seed=0)
     clip = fb.ClippingPostprocessor(WL["bound"])
     eng = fb.GpuSimulationEngine(ds, postprocessors=[clip], factored_aggregate=factored)
+    eng.record_clients = True
     state = alg.initial_state()
     ctx = alg.get_next_central_contexts(state, 0)[0]
     res = eng.run_iteration(alg, state, (ctx,))

@@ -9,7 +9,7 @@ import pytest
 import paper_2404_06430_b200 as fb
 from oracle import port
 from tests.conftest import assert_close_fp32
-from tests.helpers import CONFIGS, golden_rows, product_datasets, product_run_parts
+from tests.helpers import CONFIGS, golden_rows, product_datasets, product_run_parts, run_sim
 
 pytestmark = pytest.mark.gpu
 
@@ -90,7 +90,7 @@ def test_cnn_engine_matches_reference_fixture(name, golden):
     alg, post = product_run_parts(cfg, noise_source="numpy")
     eng = fb.GpuSimulationEngine(ds, postprocessors=post)
     thetas = []
-    res = fb.run_simulation(alg, eng, callbacks=[lambda p, rows, t: thetas.append(p.flat_host()) and False])
+    res = run_sim(alg, eng, callbacks=[lambda p, rows, t: thetas.append(p.flat_host()) and False])
     assert res.cohort_digest == str(g["digest"])
     keep = g["keep"]
     for t, th in enumerate(thetas):
@@ -163,7 +163,7 @@ def test_cnn_factored_aggregate_matches_materialised(monkeypatch):
         alg, post = product_run_parts(cfg, noise_source="numpy")
         eng = fb.GpuSimulationEngine(ds, postprocessors=post, factored_aggregate=fact)
         out = []
-        fb.run_simulation(alg, eng, callbacks=[lambda p, rows, t: out.append(p.flat_host()) and False])
+        run_sim(alg, eng, callbacks=[lambda p, rows, t: out.append(p.flat_host()) and False])
         thetas[key] = np.array(out)
     for t in range(len(thetas["fact"])):
         assert_close_fp32(thetas["fact"][t], thetas["mat"][t], what=f"theta after iteration {t}")

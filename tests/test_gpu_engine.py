@@ -12,7 +12,7 @@ import pytest
 
 import paper_2404_06430_b200 as fb
 from tests.conftest import assert_close_fp32
-from tests.helpers import CONFIGS, golden_rows, oracle_run, product_datasets, product_run_parts
+from tests.helpers import CONFIGS, golden_rows, oracle_run, product_datasets, product_run_parts, run_sim
 
 pytestmark = pytest.mark.gpu
 
@@ -22,7 +22,7 @@ def run_engine(cfg, noise_source="numpy", **engine_kw):
     alg, post = product_run_parts(cfg, noise_source=noise_source)
     eng = fb.GpuSimulationEngine(ds, postprocessors=post, **engine_kw)
     thetas = []
-    res = fb.run_simulation(alg, eng, callbacks=[lambda p, rows, t: thetas.append(p.flat_host()) and False])
+    res = run_sim(alg, eng, callbacks=[lambda p, rows, t: thetas.append(p.flat_host()) and False])
     return res, np.array(thetas)
 
 
@@ -121,7 +121,7 @@ def test_scaffold_controls_match_oracle():
     ds = product_datasets(cfg)
     alg, post = product_run_parts(cfg)
     eng = fb.GpuSimulationEngine(ds, postprocessors=post)
-    res = fb.run_simulation(alg, eng)
+    res = run_sim(alg, eng)
     store = res.state.extra["user_controls"]
     # replay the oracle and capture its controls
     model = oracle_model(cfg)
@@ -151,7 +151,7 @@ def test_scaffold_zero_local_steps_raises_with_provenance():
     alg, post = product_run_parts({**cfg, "lr": 0.0})
     eng = fb.GpuSimulationEngine(ds, postprocessors=post)
     with pytest.raises(fb.EngineError, match="control update divides by steps"):
-        fb.run_simulation(alg, eng)
+        run_sim(alg, eng)
 
 
 def test_engine_metrics_csv_and_checkpoint(golden, tmp_path):
@@ -165,7 +165,7 @@ def test_engine_metrics_csv_and_checkpoint(golden, tmp_path):
     ds = product_datasets(cfg)
     alg, post = product_run_parts(cfg)
     buf = io.StringIO()
-    res = fb.run_simulation(alg, fb.GpuSimulationEngine(ds, postprocessors=post), callbacks=[fb.CsvMetricsWriter(buf)])
+    res = run_sim(alg, fb.GpuSimulationEngine(ds, postprocessors=post), callbacks=[fb.CsvMetricsWriter(buf)])
     lines = buf.getvalue().splitlines()
     assert lines[0] == "iteration,population,metric,value,weight"
     got = [ln.split(",") for ln in lines[1:]]

@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 import paper_2404_06430_b200 as fb
-from tests.helpers import CONFIGS, product_datasets, product_run_parts
+from tests.helpers import CONFIGS, product_datasets, product_run_parts, run_sim
 
 pytestmark = pytest.mark.gpu
 
@@ -24,7 +24,7 @@ def _alg(cfg, **over):
 def _run(cfg, alg, post, callbacks=(), **engine_kw):
     eng = fb.GpuSimulationEngine(product_datasets(cfg), postprocessors=post, **engine_kw)
     thetas = []
-    res = fb.run_simulation(alg, eng, callbacks=[lambda p, rows, t: thetas.append(p.flat_host()) and False,
+    res = run_sim(alg, eng, callbacks=[lambda p, rows, t: thetas.append(p.flat_host()) and False,
                                                  *callbacks])
     return res, np.array(thetas)
 
@@ -56,16 +56,30 @@ def test_empty_poisson_cohort_produces_no_aggregate_and_keeps_theta():
     np.testing.assert_array_equal(state.params.flat_host(), theta0)
 
 
+def _run_fedsim_loop(cfg, alg, post, callbacks=()):
+    """fedsim's own run_simulation (fedsim/engine/loop.py:45-88) driving the engine."""
+    from tests.fedsim_ref import fedsim
+
+    fedsim()
+    from fedsim.engine import run_simulation
+
+    eng = fb.GpuSimulationEngine(product_datasets(cfg), postprocessors=post)
+    thetas = []
+    res = run_simulation(alg, eng, callbacks=[lambda p, rows, t: thetas.append(p.flat_host()) and False,
+                                              *callbacks])
+    return res, np.array(thetas)
+
+
 def test_zero_iterations_returns_initial_state():
     cfg, alg, post = _alg(CONFIGS["mlp_dp"], iterations=0)
-    res, thetas = _run(cfg, alg, post)
+    res, thetas = _run_fedsim_loop(cfg, alg, post)
     assert res.iterations_run == 0 and res.metrics_rows == [] and res.iteration_seconds == []
     assert len(thetas) == 0
 
 
 def test_early_stop_callback_runs_exactly_six_iterations():
     cfg, alg, post = _alg(CONFIGS["logistic_dp"], iterations=1500)
-    res, _ = _run(cfg, alg, post, callbacks=[lambda p, rows, t: t == 5])
+    res, _ = _run_fedsim_loop(cfg, alg, post, callbacks=[lambda p, rows, t: t == 5])
     assert res.iterations_run == 6 and len(res.iteration_seconds) == 6
     assert {row[0] for row in res.metrics_rows} == set(range(6))
 
@@ -128,7 +142,7 @@ def test_one_point_users_and_tail_batches_match_oracle(model):
                     local_num_epochs=2, local_batch_size=2, eval_frequency=10, eval_cohort_size=1,
                     weighting="datapoints", run_seed=3, init_seed=4)
     eng = fb.GpuSimulationEngine({fb.Population.TRAIN: ds, fb.Population.VAL: ds})
-    res = fb.run_simulation(alg, eng)
+    res = run_sim(alg, eng)
     theta0 = om.init(4)
     ref = port.run_context(om, theta0, {u.user_id: (u.features.astype(np.float32).astype(np.float64), u.labels)
                                         for u in ds.users.values()}, len(sizes),
