@@ -248,20 +248,42 @@ def kernel_work(wl: dict, counts: dict) -> dict:
         "fc1_fwd_kernel": ("hbm", steps * fc1_bytes + fwd * 12544 * 4, "bytes"),
         "fc1_bwd_kernel": ("hbm", steps * 2 * fc1_bytes + 2 * train * 12544 * 4, "bytes"),
         "row_sumsq_partial_kernel": ("hbm", counts["clients"] * counts["D_dense"] * 4, "bytes"),
-        "weighted_sum_kernel": ("hbm", counts["clients"] * counts["D"] * 4 + counts["D"] * 4 * counts["iters"], "bytes"),
+        # K3 reads the columns around the factored fc1 block (that block comes from fc1_agg_tc)
+        "weighted_sum_kernel": ("hbm", counts["clients"] * counts["D_dense"] * 4 + counts["D_dense"] * 4 * counts["iters"],
+                                "bytes"),
         "zero_delta_kernel": ("hbm", counts["clients"] * counts["D_dense"] * 4, "bytes"),
     }
+
+
+def _ncu_kernel(name: str) -> dict | None:
+    try:
+        return json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())["kernels"][name]
+    except (OSError, KeyError, ValueError):
+        return None
 
 
 def _ncu_traffic(name: str):
     """DRAM bytes (read + write) of one launch of `name` from the committed
     ncu --set full capture (profiles/ncu_traffic.json), with the launch size."""
-    try:
-        k = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())["kernels"][name]
-    except (OSError, KeyError, ValueError):
+    k = _ncu_kernel(name)
+    if k is None:
         return None
     return {"dram_bytes_per_launch": k["dram_bytes"], "slots_per_launch": k["slots"],
             "algorithmic_bytes_per_launch": k.get("algorithmic_bytes"), "source": "profiles/ncu_traffic.json"}
+
+
+def _tensor_evidence(name: str, frac: float) -> dict:
+    """ncu tensor-pipe utilisation and issued-MMA-op accounting of a tcgen05
+    kernel (profiles/ncu_traffic.json): the issued fraction counts every
+    product the hi/lo operand split and the M padding make the pipe execute."""
+    k = _ncu_kernel(name) or {}
+    out = {}
+    if "tensor_pipe_pct" in k:
+        out["tensor_pipe_active_pct"] = k["tensor_pipe_pct"]
+    if "mma_ops_per_algorithmic" in k:
+        out["issued_ops_per_algorithmic"] = k["mma_ops_per_algorithmic"]
+        out["issued_frac"] = round(frac * k["mma_ops_per_algorithmic"], 4)
+    return out
 
 
 def roofline(report: dict, wl: dict, counts: dict, peaks: dict) -> tuple[dict, dict]:
@@ -280,7 +302,8 @@ def roofline(report: dict, wl: dict, counts: dict, peaks: dict) -> tuple[dict, d
             ach = amount / (ms * 1e-3) / 1e12
             peak = peaks.get("bf16_tflops", 1590.0)
             per[name] = {"bound": "tensor", "achieved": round(ach, 2), "unit": "TFLOP/s", "frac": round(ach / peak, 4),
-                         "ms": round(ms, 2), "share": round(ms / total, 4), "math": note}
+                         "ms": round(ms, 2), "share": round(ms / total, 4), "math": note,
+                         **_tensor_evidence(name, ach / peak)}
         else:
             ach = amount / (ms * 1e-3) / 1e9
             peak = peaks.get("hbm_gbs", 6650.0)
@@ -293,6 +316,8 @@ def roofline(report: dict, wl: dict, counts: dict, peaks: dict) -> tuple[dict, d
         peak = peaks.get("bf16_tflops", 1590.0) if k["bound"] == "tensor" else peaks.get("hbm_gbs", 6650.0)
         out.update(bound=k["bound"], achieved=k["achieved"], peak=peak, unit=k["unit"], frac=k["frac"],
                    traffic=_ncu_traffic(name),
+                   **{key: k[key] for key in ("tensor_pipe_active_pct", "issued_ops_per_algorithmic", "issued_frac")
+                      if key in k},
                    peak_source=("MEASURED_PEAKS.json bf16_tflops (dense bf16 cuBLAS); the kernel's own math is "
                                 + k.get("math", "") + ": per algorithmic product one N=128 MMA (hi*[Whi;Wlo]) + one "
                                 "N=64 MMA (lo*Whi) -> at most 1/3 of the fp16/bf16 dense rate, and the N=64 half is "
@@ -325,27 +350,33 @@ def gpu_arm(args, wl):
 
     ds = build(wl)
     K, W = args.steps, args.warmup
-    alg, post = make_algorithm(wl, W + K + max(args.e2e_warmup, wl["eval_every"]) + args.e2e_steps + 1)
+    alg, post = make_algorithm(wl, W + K + args.profile_steps + max(args.e2e_warmup, wl["eval_every"]) +
+                               args.e2e_steps + 1)
     engine = fb.GpuSimulationEngine(ds, postprocessors=post)
     state = alg.initial_state()
     state = run_iterations(engine, alg, state, 0, W)
     n0 = native.lib().fb_launch_count()
-    native.lib().fb_timing_enable(1)
+    native.lib().fb_timing_enable(0)  # the headline carries no per-launch instrumentation
     with ClockSampler(local) as clk:
         state, ms, wall = timed(engine, alg, state, W, K, dist, world)
-    report = native.timing_report()
-    native.lib().fb_timing_enable(0)
     launches = native.lib().fb_launch_count() - n0
     clocks = clk.summary()
+    # second pass, per-kernel device times (every launch bracketed by CUDA events on its
+    # stream): the roofline's kernel durations, not the headline
+    KP = max(1, min(K, args.profile_steps))
+    native.lib().fb_timing_enable(1)
+    state, ms_prof, _ = timed(engine, alg, state, W + K, KP, dist, world)
+    report = native.timing_report()
+    native.lib().fb_timing_enable(0)
 
     # samples processed by the forward / training kernels in the timed window (this rank)
     C = wl["cohort"]
     per_rank = C / world
-    val_iters = sum(1 for t in range(W, W + K) if t % wl["eval_every"] == 0)
+    val_iters = sum(1 for t in range(W + K, W + K + KP) if t % wl["eval_every"] == 0)
     ppu = wl["ppu"] or float(np.mean([u.num_points for u in ds[fb.Population.TRAIN].users.values()]))
     steps = wl["epochs"] * -(-int(round(ppu)) // wl["batch"])  # (ragged: at the mean size; approximate)
-    train_samples = per_rank * ppu * wl["epochs"] * K
-    fwd_samples = train_samples + per_rank * ppu * K + val_iters * (wl["eval_cohort"] / world) * ppu
+    train_samples = per_rank * ppu * wl["epochs"] * KP
+    fwd_samples = train_samples + per_rank * ppu * KP + val_iters * (wl["eval_cohort"] / world) * ppu
     D = make_model(wl).num_params
     # columns the dense per-client passes (zero_delta, K2) touch: the factored CNN fc1
     # block is written by fc1_mat_tc and its squares come out of that kernel
@@ -353,17 +384,17 @@ def gpu_arm(args, wl):
     dense_D = (D + 3) & ~3
     if wl["model"] == "cnn" and cnn_mod.hist_steps(max(int(steps), 1), wl["batch"]):
         dense_D -= cnn_mod.FC1_HI - cnn_mod.FC1_LO
-    counts = {"train": train_samples, "fwd": fwd_samples, "client_steps": per_rank * steps * K,
-              "clients": per_rank * K, "D": (D + 3) & ~3, "D_dense": dense_D, "iters": K}
+    counts = {"train": train_samples, "fwd": fwd_samples, "client_steps": per_rank * steps * KP,
+              "clients": per_rank * KP, "D": (D + 3) & ~3, "D_dense": dense_D, "iters": KP}
 
     # end-to-end: dataset in pinned host memory, cohort rows moved every iteration
     e2e = None
     if args.e2e_steps > 0:
         eng2 = fb.GpuSimulationEngine(ds, postprocessors=post, data_residency="host")
-        t0 = W + K
         # warm-up covers a validation iteration too (every context kind has allocated its
         # prefetch buffers once before the timed window)
         e2e_warmup = max(args.e2e_warmup, wl["eval_every"])
+        t0 = W + K + KP
         state = run_iterations(eng2, alg, state, t0, e2e_warmup)
         eng2.io_bytes = {"h2d": 0, "d2h": 0}
         state, ms2, wall2 = timed(eng2, alg, state, t0 + e2e_warmup, args.e2e_steps, dist, world)
@@ -391,6 +422,9 @@ def gpu_arm(args, wl):
                        "eval_every": wl["eval_every"], "parallelism": f"cohort-dp{world}",
                        "l2": "inputs larger than L2 (dataset 614 MB + per-iteration working set of GBs)"},
             "wall_s": wall, "clocks": clocks, "gpu_launches": int(launches), "e2e": e2e,
+            "profile_pass": {"steps": KP, "ms_per_step": ms_prof / KP,
+                             "note": "per-kernel times come from this second pass (fb_timing_enable(1)); the "
+                                     "headline window above runs without instrumentation"},
             "roofline": rf,
             "kernels": per_kernel,
             "kernels_ms": {k: round(v[0], 3) for k, v in sorted(report.items(), key=lambda kv: -kv[1][0])},
@@ -450,10 +484,208 @@ def cpu_baseline(wl, ds, n_clients):
             "seconds_per_iteration": it}
 
 
+_REF: dict = {}  # fork-inherited by the reference arm's worker processes
+
+
+def _ref_queue_worker(span):
+    """One worker of the reference engine, in its own process: fedsim's own
+    SimulationEngine._run_queue (simulate_one_user -> postprocess_one_user ->
+    SumAggregator.accumulate over the queue; fedsim/engine/runtime.py:173-209)
+    on a slice of the cohort, one BLAS thread."""
+    from threadpoolctl import threadpool_limits
+
+    lo, hi = span
+    with threadpool_limits(1):
+        return _REF["engine"]._run_queue(_REF["alg"], _REF["state"], _REF["dataset"], _REF["ctx"],
+                                         _REF["queue"][lo:hi])
+
+
+def _reference_setup(wl):
+    """The reference's own objects (fedsim from baseline/_ref): datasets, the
+    oracle CNN in fedsim's generic Model contract (fedsim has no CNN; its own
+    fit_local loop drives it), a FedAvg factory (cohort size -> algorithm) and
+    ClippingPostprocessor + GaussianCentralMechanism at the bench's settings."""
+    REF = ROOT / "baseline" / "_ref"
+    if not (REF / "fedsim" / "__init__.py").exists():
+        raise ImportError("fedsim not installed in baseline/_ref")
+    os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join(tempfile.gettempdir(), "fedsim_numba_cache"))
+    sys.path.append(str(REF))
+    from fedsim.algorithms import FedAvg
+    from fedsim.core import Population, derive_seed
+    from fedsim.feddata import make_synthetic_classification, partition_iid
+    from fedsim.models import MLP, LogisticRegression, Model, SGDOptimizer
+    from fedsim.privacy import ClippingPostprocessor, GaussianCentralMechanism
+
+    from oracle.port import Cnn
+
+    class RefCNN(Model):
+        def __init__(self):
+            self.impl = Cnn()
+
+        @property
+        def param_dims(self):
+            return self.impl.dims
+
+        def init_params(self, seed):
+            return self.impl.init(seed)
+
+        def loss_and_grad(self, params, X, y):
+            return self.impl.loss_and_grad(params, X, y)
+
+        def eval_counts(self, params, X, y, backend=None):
+            return self.impl.eval_counts(params, X, y)
+
+    ppu = wl["ppu"]
+    ntr, nva = wl["users"] * ppu, wl["val_users"] * ppu
+    X, y = make_synthetic_classification(ntr + nva, dim=wl["dim"], num_classes=10, margin=6.0,
+                                         seed=derive_seed(0, "pool"))
+    X = X.astype(np.float32).astype(np.float64)  # the same fp32-representable features the GPU arm sees
+    ds = {Population.TRAIN: partition_iid(X[:ntr], y[:ntr], ppu, seed=derive_seed(0, "train", "split"),
+                                          population=Population.TRAIN, id_prefix="train"),
+          Population.VAL: partition_iid(X[ntr:], y[ntr:], ppu, seed=derive_seed(0, "val", "split"),
+                                        population=Population.VAL, id_prefix="val")}
+    model = {"cnn": RefCNN, "mlp": lambda: MLP(wl["dim"], wl["hidden"], 10),
+             "logistic": lambda: LogisticRegression(wl["dim"], 10)}[wl["model"]]()
+    def make_alg(cohort):
+        return FedAvg(model, SGDOptimizer(wl["clr"]), total_iterations=1 << 30, cohort_size=cohort,
+                      local_learning_rate=wl["lr"], local_num_epochs=wl["epochs"], local_batch_size=wl["batch"],
+                      eval_frequency=wl["eval_every"], eval_cohort_size=wl["eval_cohort"], weighting="uniform",
+                      run_seed=0, init_seed=0)
+
+    clip = ClippingPostprocessor(wl["bound"])
+    mech = GaussianCentralMechanism(clip, sigma=wl["sigma"], r=wl["cohort"] / wl["noise_cohort"],
+                                    noise_base_seed=derive_seed(0, "noise-stream", 0))
+    return ds, make_alg, [clip, mech]
+
+
+def _reference_iteration(setting, ds, alg, post, state, t, ncores):
+    """Seconds for one central iteration of the reference (train context only)
+    at ``alg.cohort_size`` users, in one of BASELINE.md section 2.3's settings:
+    "blas"    SimulationEngine(num_workers=1), BLAS threads = ncores;
+    "threads" SimulationEngine(num_workers=ncores), BLAS threads = 1;
+    "procs"   the engine's per-worker _run_queue in ncores forked processes
+              (BLAS 1 each) + its own worker_reduce / server postprocessors."""
+    import multiprocessing as mp
+
+    from fedsim.engine import SimulationEngine
+    from fedsim.engine.scheduling import compute_base_weight, schedule_users
+    from fedsim.feddata import sample_cohort
+    from threadpoolctl import threadpool_limits
+
+    ctx = alg.get_next_central_contexts(state, t)[0]
+    t0 = time.perf_counter()
+    if setting in ("blas", "threads"):
+        workers = 1 if setting == "blas" else ncores
+        with threadpool_limits(ncores if setting == "blas" else 1):
+            eng = SimulationEngine(ds, num_workers=workers, postprocessors=post)
+            res = eng.run_iteration(alg, state, (ctx,))
+            state = alg.process_aggregated_statistics_all_contexts(state, (ctx,), res.aggregates, res.metrics,
+                                                                   res.user_updates)
+        return time.perf_counter() - t0, state
+    eng = SimulationEngine(ds, num_workers=ncores, postprocessors=post)
+    dataset = ds[ctx.population]
+    cohort = sample_cohort(dataset, ctx.cohort_size, ctx.seed)
+    w = {u: float(dataset.users[u].weight) for u in cohort}
+    queues = schedule_users(w, ncores, compute_base_weight(list(w.values()), "median")).queues
+    flat = [u for q in queues for u in q]
+    bounds = np.cumsum([0] + [len(q) for q in queues])
+    _REF.update(engine=eng, alg=alg, state=state, dataset=dataset, ctx=ctx, queue=flat)
+    with mp.get_context("fork").Pool(ncores) as pool:
+        outs = pool.map(_ref_queue_worker, [(int(a), int(b)) for a, b in zip(bounds[:-1], bounds[1:])])
+    agg = eng._aggregator.worker_reduce([o[0] for o in outs])
+    for proc in reversed(post):
+        agg, _ = proc.postprocess_server(agg, ctx)
+    state = alg.process_aggregated_statistics_all_contexts(state, (ctx,), (agg,), {}, [])
+    return time.perf_counter() - t0, state
+
+
 def reference_arm(args, wl):
+    """The reference's own CPU implementation of the path on this box's host
+    cores: fedsim's SimulationEngine / FedAvg / ClippingPostprocessor /
+    GaussianCentralMechanism / SumAggregator from baseline/_ref, with the
+    oracle CNN as the model (the reference has none).  Each step is one
+    reference central iteration at a bounded cohort sample (3 x ncores users)
+    in the fastest of BASELINE.md section 2.3's settings; the per-iteration
+    cost at cohort C is a + C * b from a two-size fit (fixed cost a: noise
+    over D, the server step; b: per user), plus the validation context
+    amortised over eval_every.  Falls back to the oracle port's timing if
+    baseline/_ref is absent."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    ncores = len(os.sched_getaffinity(0))
+    C = wl["cohort"]
+    try:
+        ds, make_alg, post = _reference_setup(wl)
+    except ImportError as exc:
+        return _reference_arm_port(args, wl, str(exc))
+    small, big = ncores, 3 * ncores
+    alg_small, alg_big = make_alg(small), make_alg(big)
+    cpu = {"model": _cpu_model(), "affinity": ncores}
+    # settings on the small sample (one iteration each, after a warm-up of the fastest)
+    st = alg_small.initial_state()
+    settings = {}
+    for setting in ("procs", "threads", "blas"):
+        if setting == "blas" and args.steps > 0:
+            sec, st = _reference_iteration(setting, ds, alg_small, post, st, 1, ncores)
+        else:
+            _reference_iteration(setting, ds, alg_small, post, st, 1, ncores)
+            sec, st = _reference_iteration(setting, ds, alg_small, post, st, 2, ncores)
+        settings[setting] = sec
+    best = min(settings, key=settings.get)
+    st_big = alg_big.initial_state()
+    for k in range(args.warmup):
+        _, st_big = _reference_iteration(best, ds, alg_big, post, st_big, 1 + k, ncores)
+    t_small = settings[best]
+    times = []
+    for k in range(args.steps):
+        sec, st_big = _reference_iteration(best, ds, alg_big, post, st_big, 1 + args.warmup + k, ncores)
+        times.append(sec)
+    t_big = float(np.median(times))
+    b = max((t_big - t_small) / (big - small), 1e-9)
+    a = max(t_small - small * b, 0.0)
+    # validation context (eval of eval_cohort users at theta_t), amortised over eval_every
+    from fedsim.core import CentralContext, EvalParams
+    from fedsim.engine import SimulationEngine
+    from threadpoolctl import threadpool_limits
+
+    vctx = CentralContext(iteration=0, population=next(p for p in ds if p.value == "val"),
+                          cohort_size=wl["eval_cohort"], seed=0, do_training=False, eval_params=EvalParams())
+    t0 = time.perf_counter()
+    with threadpool_limits(1):
+        SimulationEngine(ds, num_workers=ncores, postprocessors=post).run_iteration(alg_big, st_big, (vctx,))
+    t_val = time.perf_counter() - t0
+    it = a + C * b + t_val / wl["eval_every"]
+    value = 1.0 / it
+    sample = (f"reference SimulationEngine iterations at cohort {small} and {big} (median of {args.steps}), "
+              f"setting '{best}'; fit a + C*b with a={a:.3f}s b={b:.4f}s/user -> cohort {C}, plus the "
+              f"{wl['eval_cohort']}-user validation context ({t_val:.2f}s) / {wl['eval_every']}")
+    line = {
+        "metric": METRIC, "impl": "reference", "value": value, "unit": "iterations/s", "clients_per_sec": value * C,
+        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * it, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": wl["name"], "model": wl["model"], "cohort": C, "parallelism": "host-cpu"},
+        "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": ncores,
+                         "kind": "reference", "sample": sample, "cpu": cpu,
+                         "settings_s_per_iteration_at_small_cohort": {k: round(v, 3) for k, v in settings.items()},
+                         "fastest": best},
+        "e2e": {"value": value, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _reference_arm_port(args, wl, why):
     ds = build(wl)
     cpu_iteration_seconds(wl, ds, 1)  # warm-up (BLAS thread pools, page-in)
     its = []
@@ -469,7 +701,7 @@ def reference_arm(args, wl):
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": wl["name"], "model": wl["model"], "cohort": C, "parallelism": "host-cpu"},
         "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": _cores(), "kind": "port",
-                         "sample": sample},
+                         "sample": sample + f" (oracle port: {why})"},
         "e2e": {"value": value, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -558,6 +790,7 @@ def main(argv=None):
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--e2e-warmup", type=int, default=2)
     ap.add_argument("--cpu-clients", type=int, default=16)
+    ap.add_argument("--profile-steps", type=int, default=5)
     ap.add_argument("--ref-clients", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args(argv)

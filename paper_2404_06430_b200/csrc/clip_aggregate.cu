@@ -377,8 +377,8 @@ int fb_context_sums(const double* loss, const int32_t* correct, const int32_t* n
                     const int32_t* clipped, const int32_t* nonfinite, const float* w, int num_clients, int train,
                     float* tail, void* stream) {
   FB_REQUIRE(num_clients >= 0, "context_sums: negative client count");
-  FB_REQUIRE(tail != nullptr && num_rows != nullptr, "context_sums: null tail / num_rows");
-  FB_REQUIRE(num_clients == 0 || (loss && correct), "context_sums: null loss / correct");
+  FB_REQUIRE(tail != nullptr, "context_sums: null tail");
+  FB_REQUIRE(num_clients == 0 || (loss && correct && num_rows), "context_sums: null loss / correct / num_rows");
   FB_REQUIRE(!train || num_clients == 0 || (norm && clipped && nonfinite && w), "context_sums: null training arrays");
   cudaStream_t s = fb::as_stream(stream);
   FB_LAUNCH("context_sums_kernel", s, fb::context_sums_kernel<<<1, fb::kThreads, 0, s>>>(
