@@ -227,6 +227,23 @@ int fb_weighted_sum_f32(const float* delta, int64_t ld_delta, int num_clients, i
                         const float* coef, float* agg, int accumulate,
                         void* workspace, int64_t workspace_bytes, void* stream);
 
+/* ------------------------------------------ a6 + a7 + a8 fused (K2 + K3)
+ * One HBM pass: the outputs of fb_delta_norm_clip_f32 (norm, coef, clipped,
+ * nonfinite) AND of fb_weighted_sum_f32 (agg (+)= sum_c coef[c] delta[c])
+ * from a single persistent cooperative kernel that keeps each SM's column
+ * slice of the aggregate on chip and re-reads client c-1 from L2 while it
+ * streams client c from HBM.  Same reference semantics as K2 and K3
+ * (fedsim/privacy/clipping.py:37-56, fedsim/engine/aggregator.py:39-44);
+ * fp32 accumulation in blocks of 64 clients, fp64 across blocks.
+ * Requires D <= fb_clip_aggregate_max_columns() (FB_ERR_UNSUPPORTED
+ * otherwise: use K2 + K3), ld_delta % 4 == 0 and a 16-byte aligned delta. */
+int64_t fb_clip_aggregate_max_columns(void);
+int64_t fb_clip_aggregate_workspace_bytes(int num_clients, int64_t D);
+int fb_clip_aggregate_f32(const float* delta, int64_t ld_delta, int num_clients, int64_t D,
+                          const float* w, double bound, double* norm, float* coef,
+                          int32_t* clipped, int32_t* nonfinite, float* agg, int accumulate,
+                          void* workspace, int64_t workspace_bytes, void* stream);
+
 /* ------------------------------------------------ a9 (worker_reduce)
  * Per-context sums over the C clients of this rank, fp64 in a fixed order,
  * written as fp32 (hi, lo) pairs: tail[2f] + tail[2f+1] == sum f (hi alone

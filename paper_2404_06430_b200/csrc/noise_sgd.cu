@@ -45,11 +45,14 @@ __device__ __forceinline__ float u01(uint32_t v) {
 __device__ __forceinline__ void normal4(uint64_t seed, uint64_t g, float out[4]) {
   const U4 r = philox4x32_10(U4{(uint32_t)g, (uint32_t)(g >> 32), 0x46656453u /*"FedS"*/, 0u},
                              (uint32_t)seed, (uint32_t)(seed >> 32));
+  // hardware MUFU approximations (log2 / sin / cos: ~2^-21 relative on these ranges): the
+  // noise is a statistical object (tested by its moments), and the full-precision libm
+  // paths made this HBM-bound kernel issue-bound
   float s0, c0, s1, c1;
-  const float rad0 = sqrtf(-2.0f * logf(u01(r.x)));
-  const float rad1 = sqrtf(-2.0f * logf(u01(r.z)));
-  sincospif(2.0f * u01(r.y), &s0, &c0);
-  sincospif(2.0f * u01(r.w), &s1, &c1);
+  const float rad0 = sqrtf(-2.0f * __logf(u01(r.x)));
+  const float rad1 = sqrtf(-2.0f * __logf(u01(r.z)));
+  __sincosf(6.28318530717958648f * u01(r.y), &s0, &c0);
+  __sincosf(6.28318530717958648f * u01(r.w), &s1, &c1);
   out[0] = rad0 * c0;
   out[1] = rad0 * s0;
   out[2] = rad1 * c1;
@@ -78,27 +81,32 @@ __global__ void __launch_bounds__(kThreads) noise_avg_sgd_kernel(
   const int64_t i0 = g << 2;
   if (i0 >= D) return;
   float z[4] = {0.f, 0.f, 0.f, 0.f};
-  if (!injected && noise_std != 0.0f) normal4(seed, g, z);
   const bool full = i0 + 3 < D;
   const bool vec = full && ((reinterpret_cast<uintptr_t>(theta) | reinterpret_cast<uintptr_t>(agg) |
                              (injected ? reinterpret_cast<uintptr_t>(injected) : 0) |
                              (agg_out ? reinterpret_cast<uintptr_t>(agg_out) : 0)) & 15u) == 0;
   if (vec) {
+    // loads first: the Philox rounds and the Box-Muller transform overlap their latency
     float4 t = *reinterpret_cast<float4*>(theta + i0);
     float4 a = __ldcs(reinterpret_cast<const float4*>(agg + i0));
     if (injected) {
       const float4 nz = __ldcs(reinterpret_cast<const float4*>(injected + i0));
       a.x += nz.x; a.y += nz.y; a.z += nz.z; a.w += nz.w;
-    } else {
+    } else if (noise_std != 0.0f) {
+      normal4(seed, g, z);
       a.x = fmaf(noise_std, z[0], a.x); a.y = fmaf(noise_std, z[1], a.y);
       a.z = fmaf(noise_std, z[2], a.z); a.w = fmaf(noise_std, z[3], a.w);
+    } else {
+      a.x = fmaf(noise_std, 0.f, a.x); a.y = fmaf(noise_std, 0.f, a.y);
+      a.z = fmaf(noise_std, 0.f, a.z); a.w = fmaf(noise_std, 0.f, a.w);
     }
-    if (agg_out) *reinterpret_cast<float4*>(agg_out + i0) = a;
+    if (agg_out) __stcs(reinterpret_cast<float4*>(agg_out + i0), a);
     t.x = fmaf(-step, a.x, t.x); t.y = fmaf(-step, a.y, t.y);
     t.z = fmaf(-step, a.z, t.z); t.w = fmaf(-step, a.w, t.w);
     *reinterpret_cast<float4*>(theta + i0) = t;
     return;
   }
+  if (!injected && noise_std != 0.0f) normal4(seed, g, z);
   for (int j = 0; j < 4 && i0 + j < D; ++j) {
     float a = agg[i0 + j];
     a = injected ? a + injected[i0 + j] : fmaf(noise_std, z[j], a);

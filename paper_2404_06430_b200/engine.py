@@ -109,6 +109,18 @@ def unpack_sums(tail: np.ndarray) -> np.ndarray:
     return t[:, 0] + t[:, 1]
 
 
+# Materialised payloads at least this wide go through the fused one-pass K2 + K3
+# (clip_aggregate_fused.cu); below it the per-client grid handshake costs more than the
+# second HBM pass it saves (aggregation microbench: fused 0.58 vs two-pass 0.49 of the
+# roofline at D = 4 M, 0.37 vs 0.44 at 2 M).
+FUSED_CLIP_AGGREGATE_MIN_D = 3_000_000
+
+
+def fused_clip_aggregate(D: int, ld: int, deferred: bool) -> bool:
+    return (not deferred and D >= FUSED_CLIP_AGGREGATE_MIN_D and ld % 4 == 0
+            and D <= native.call("fb_clip_aggregate_max_columns"))
+
+
 def reduce_across_ranks(buf, group=None) -> None:
     """worker_reduce across ranks (fedsim/engine/aggregator.py:46-62): ONE
     all-reduce(SUM) of the flat fp32 buffer [payload | sums tail] (NCCL over
@@ -719,6 +731,11 @@ class GpuSimulationEngine:
                                 cnn.FC1_HI, native.ptr(fc1_sq), native.ptr(d_w), float(bound), native.ptr(norm),
                                 native.ptr(coef), native.ptr(clipped), native.ptr(nf2), native.ptr(kws), kws.numel(),
                                 stream)
+                elif fused_clip_aggregate(Dp, ldp, deferred):  # K2 + K3 in one HBM pass
+                    fws = self.ws.get("fused_ws", native.call("fb_clip_aggregate_workspace_bytes", C, Dp))
+                    native.call("fb_clip_aggregate_f32", native.ptr(payload), ldp, C, Dp, native.ptr(d_w),
+                                float(bound), native.ptr(norm), native.ptr(coef), native.ptr(clipped),
+                                native.ptr(nf2), native.ptr(agg_flat), 0, native.ptr(fws), fws.numel(), stream)
                 else:
                     native.call("fb_delta_norm_clip_f32", native.ptr(payload), ldp, C, Dp, native.ptr(d_w),
                                 float(bound), native.ptr(norm), native.ptr(coef), native.ptr(clipped),
@@ -737,7 +754,7 @@ class GpuSimulationEngine:
                                 native.ptr(coef), native.ptr(agg_flat) + 4 * hi, 0, native.ptr(sws), sws.numel(),
                                 stream)
                     cnn.fc1_aggregate(runner, coef, agg_flat[lo:hi], stream)
-                else:
+                elif not fused_clip_aggregate(Dp, ldp, deferred):
                     native.call("fb_weighted_sum_f32", native.ptr(payload), ldp, C, Dp, native.ptr(coef),
                                 native.ptr(agg_flat), 0, native.ptr(sws), sws.numel(), stream)
             else:
