@@ -193,6 +193,31 @@ int fb_gather_rows_lite(const void* src, int64_t row_bytes, const int64_t* row_s
  * of the next iteration's cohort rows. */
 int fb_upload_pinned(const void* host_src, void* dst, int64_t bytes, void* stream);
 
+/* ------------------------------------- config C: transformer LM (a4 + a5)
+ * models.TransformerLM, the StackOverflow-shaped next-word model of BASELINE
+ * configs[2].  dims (host int32[6])
+ * = {vocab, d_model, heads, ff, layers, seq}.  X rows are sentences of seq+1
+ * token ids stored as floats (0 = pad); h_num_rows is the host copy of
+ * num_rows.  Eval: per-client summed CE over non-pad targets and correct
+ * (first-argmax) targets, processed in chunks of eval_groups x batch_size
+ * sentences.  Local SGD: the generic update rule of fedsim/models/models.py:
+ * 53-79 with the batch loss the mean CE over the batch's non-pad targets,
+ * clients trained clients_per_wave at a time; delta / nonfinite as in
+ * fb_local_sgd_mlp_f32.  Shapes: d <= 256, d % heads == 0, d / heads <= 32,
+ * seq <= 32 (FB_ERR_UNSUPPORTED otherwise).                                */
+int64_t fb_lm_num_params(const int32_t* dims);
+int64_t fb_lm_workspace_bytes(const int32_t* dims, int batch_size, int clients_per_wave, int eval_groups);
+int fb_eval_lm_f32(const float* theta, const int32_t* dims, const float* X, const int64_t* row_start,
+                   const int32_t* num_rows, const int32_t* h_num_rows, int num_clients, double* loss_sum,
+                   int32_t* correct, int batch_size, int eval_groups, void* workspace, int64_t workspace_bytes,
+                   void* stream);
+int fb_local_sgd_lm_f32(const float* theta_t, const int32_t* dims, const float* X, const int64_t* row_start,
+                        const int32_t* num_rows, const int32_t* h_num_rows, const int32_t* perms,
+                        const int64_t* perm_off, int num_clients, int epochs, int batch_size, float lr,
+                        float prox_mu, const float* control, int64_t ld_control, float* delta_out, int64_t ld_delta,
+                        int32_t* nonfinite, int clients_per_wave, void* workspace, int64_t workspace_bytes,
+                        void* stream);
+
 /* ------------------------------------------------- a6 + a7 (kernel K2)
  * For every client c: norm[c] = || w[c] * delta[c, :D] ||_2 (fp64
  * accumulation), clipped[c] = norm[c] > bound (strict), coef[c] =

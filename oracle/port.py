@@ -275,6 +275,179 @@ class Cnn:
         return _eval_rows(logits, y)
 
 
+# ---------------------------------------------------- config C: transformer LM
+# StackOverflow-shaped next-word model (BASELINE configs[2]; /root/reference/PAPER.md:
+# 1052 "transformer model with 1962912 parameters", 1071-1085: embedding 96, 8 heads,
+# feed-forward 1536, 3 layers, sequence length 20).  The reference ships no LM, so this
+# oracle DEFINES the arithmetic (like Cnn above) and is pinned to float64 torch
+# autograd (tests/test_oracle_lm.py).  1 962 912 = 10 004 * 96 (tied input / output
+# embedding, no output bias) + 3 * 334 176 (PyTorch nn.TransformerEncoderLayer(96, 8,
+# 1536) parameter set: in_proj, out_proj, linear1, linear2, norm1, norm2).
+#   * post-norm encoder layers (norm_first=False), ReLU feed-forward, LayerNorm eps 1e-5;
+#   * causal self-attention, sinusoidal positions, embedding scaled by sqrt(d_model);
+#   * dropout off (the reference has no RNG stream for it, SURVEY.md section 8 Config A note);
+#   * a datapoint is ONE sentence: features = L + 1 token ids (0 = pad), inputs
+#     tokens[:L], targets tokens[1:]; pad targets are ignored;
+#   * batch loss = mean cross-entropy over the batch's non-pad targets (0 if none);
+#     eval_counts = (summed CE over non-pad targets, correct non-pad targets).
+LM_PAD = 0
+
+
+def lm_positions(L: int, d: int) -> np.ndarray:
+    pos = np.arange(L, dtype=np.float64)[:, None]
+    div = np.exp(np.arange(0, d, 2, dtype=np.float64) * (-np.log(10000.0) / d))
+    pe = np.zeros((L, d))
+    pe[:, 0::2] = np.sin(pos * div)
+    pe[:, 1::2] = np.cos(pos * div[: d // 2])
+    return pe
+
+
+@dataclass(frozen=True)
+class TransformerLM:
+    vocab: int = 10004
+    d: int = 96
+    heads: int = 8
+    ff: int = 1536
+    layers: int = 3
+    seq: int = 20
+    eps: float = 1e-5
+
+    @property
+    def dims(self):
+        d, f, out = self.d, self.ff, {"embedding": self.vocab * self.d}
+        for l in range(self.layers):
+            out.update({f"layer{l}/in_proj_weight": 3 * d * d, f"layer{l}/in_proj_bias": 3 * d,
+                        f"layer{l}/out_proj_weight": d * d, f"layer{l}/out_proj_bias": d,
+                        f"layer{l}/linear1_weight": f * d, f"layer{l}/linear1_bias": f,
+                        f"layer{l}/linear2_weight": d * f, f"layer{l}/linear2_bias": d,
+                        f"layer{l}/norm1_weight": d, f"layer{l}/norm1_bias": d,
+                        f"layer{l}/norm2_weight": d, f"layer{l}/norm2_bias": d})
+        return out
+
+    def init(self, seed):
+        """Weights N(0, 0.02^2) in dims order (one generator), biases 0, LayerNorm gains 1."""
+        rng = np.random.default_rng(seed)
+        out = {}
+        for name, n in self.dims.items():
+            if name.endswith("_bias"):
+                out[name] = np.zeros(n)
+            elif "norm" in name:
+                out[name] = np.ones(n)
+            else:
+                out[name] = rng.normal(0.0, 0.02, n)
+        return out
+
+    def _ln(self, y, g, b):
+        mu = y.mean(axis=-1, keepdims=True)
+        var = ((y - mu) ** 2).mean(axis=-1, keepdims=True)
+        rstd = 1.0 / np.sqrt(var + self.eps)
+        xh = (y - mu) * rstd
+        return xh * g + b, xh, rstd
+
+    def _ln_back(self, dout, xh, rstd, g):
+        dxh = dout * g
+        return rstd * (dxh - dxh.mean(axis=-1, keepdims=True) - xh * (dxh * xh).mean(axis=-1, keepdims=True))
+
+    def _forward(self, p, X):
+        N, L, d, H = X.shape[0], self.seq, self.d, self.heads
+        dh = d // H
+        tok = X[:, :L].astype(np.int64)
+        E = p["embedding"].reshape(self.vocab, d)
+        x = E[tok] * np.sqrt(d) + lm_positions(L, d)
+        causal = np.triu(np.ones((L, L), dtype=bool), 1)
+        cache = []
+        for l in range(self.layers):
+            q = lambda n: p[f"layer{l}/{n}"]
+            Wqkv, bqkv = q("in_proj_weight").reshape(3 * d, d), q("in_proj_bias")
+            qkv = x @ Wqkv.T + bqkv                                             # N, L, 3d
+            Q, K, V = (qkv[..., i * d:(i + 1) * d].reshape(N, L, H, dh).transpose(0, 2, 1, 3) for i in range(3))
+            s = Q @ K.transpose(0, 1, 3, 2) / np.sqrt(dh)                      # N, H, L, L
+            s = np.where(causal, -np.inf, s)
+            P = np.exp(s - s.max(axis=-1, keepdims=True))
+            P /= P.sum(axis=-1, keepdims=True)
+            o = (P @ V).transpose(0, 2, 1, 3).reshape(N, L, d)
+            a = o @ q("out_proj_weight").reshape(d, d).T + q("out_proj_bias")
+            x1, xh1, r1 = self._ln(x + a, q("norm1_weight"), q("norm1_bias"))
+            z = x1 @ q("linear1_weight").reshape(self.ff, d).T + q("linear1_bias")
+            h = np.maximum(z, 0.0)
+            f = h @ q("linear2_weight").reshape(d, self.ff).T + q("linear2_bias")
+            x2, xh2, r2 = self._ln(x1 + f, q("norm2_weight"), q("norm2_bias"))
+            cache.append(dict(x=x, Q=Q, K=K, V=V, P=P, o=o, x1=x1, xh1=xh1, r1=r1, z=z, h=h, xh2=xh2, r2=r2))
+            x = x2
+        logits = x @ E.T                                                        # N, L, V
+        return tok, x, cache, logits
+
+    def _targets(self, X):
+        tgt = X[:, 1:self.seq + 1].astype(np.int64)
+        return tgt, tgt != LM_PAD
+
+    def loss_and_grad(self, p, X, y=None):
+        N, L, d, H = X.shape[0], self.seq, self.d, self.heads
+        dh = d // H
+        tok, xL, cache, logits = self._forward(p, X)
+        tgt, mask = self._targets(X)
+        nv = int(mask.sum())
+        z = logits - logits.max(axis=-1, keepdims=True)
+        P = np.exp(z)
+        P /= P.sum(axis=-1, keepdims=True)
+        lp = np.log(np.take_along_axis(P, tgt[..., None], axis=-1)[..., 0])
+        loss = float(-(lp * mask).sum() / nv) if nv else 0.0
+        dl = P
+        np.put_along_axis(dl, tgt[..., None], np.take_along_axis(dl, tgt[..., None], axis=-1) - 1.0, axis=-1)
+        dl *= (mask / nv)[..., None] if nv else 0.0
+        E = p["embedding"].reshape(self.vocab, d)
+        g = {"embedding": np.einsum("nlv,nld->vd", dl, xL)}
+        dx = dl @ E
+        for l in reversed(range(self.layers)):
+            c = cache[l]
+            q = lambda n: p[f"layer{l}/{n}"]
+            G = {}
+            dy2 = dx
+            G["norm2_weight"] = (dy2 * c["xh2"]).sum(axis=(0, 1))
+            G["norm2_bias"] = dy2.sum(axis=(0, 1))
+            dx1 = self._ln_back(dy2, c["xh2"], c["r2"], q("norm2_weight"))    # into x1 (both branches)
+            W2 = q("linear2_weight").reshape(d, self.ff)
+            G["linear2_weight"] = np.einsum("nld,nlf->df", dx1, c["h"])
+            G["linear2_bias"] = dx1.sum(axis=(0, 1))
+            dz = (dx1 @ W2) * (c["z"] > 0.0)
+            W1 = q("linear1_weight").reshape(self.ff, d)
+            G["linear1_weight"] = np.einsum("nlf,nld->fd", dz, c["x1"])
+            G["linear1_bias"] = dz.sum(axis=(0, 1))
+            dx1 = dx1 + dz @ W1
+            G["norm1_weight"] = (dx1 * c["xh1"]).sum(axis=(0, 1))
+            G["norm1_bias"] = dx1.sum(axis=(0, 1))
+            dy1 = self._ln_back(dx1, c["xh1"], c["r1"], q("norm1_weight"))   # into x and a
+            Wo = q("out_proj_weight").reshape(d, d)
+            G["out_proj_weight"] = np.einsum("nli,nlj->ij", dy1, c["o"])
+            G["out_proj_bias"] = dy1.sum(axis=(0, 1))
+            do = (dy1 @ Wo).reshape(N, L, H, dh).transpose(0, 2, 1, 3)
+            Pm = c["P"]
+            dP = do @ c["V"].transpose(0, 1, 3, 2)
+            dV = Pm.transpose(0, 1, 3, 2) @ do
+            ds = Pm * (dP - (dP * Pm).sum(axis=-1, keepdims=True)) / np.sqrt(dh)
+            dQ = ds @ c["K"]
+            dK = ds.transpose(0, 1, 3, 2) @ c["Q"]
+            dqkv = np.concatenate([t.transpose(0, 2, 1, 3).reshape(N, L, d) for t in (dQ, dK, dV)], axis=-1)
+            Wqkv = q("in_proj_weight").reshape(3 * d, d)
+            G["in_proj_weight"] = np.einsum("nlo,nli->oi", dqkv, c["x"])
+            G["in_proj_bias"] = dqkv.sum(axis=(0, 1))
+            dx = dy1 + dqkv @ Wqkv
+            for k, v in G.items():
+                g[f"layer{l}/{k}"] = v
+        gE = g["embedding"]
+        np.add.at(gE, tok.ravel(), dx.reshape(-1, d) * np.sqrt(d))
+        return loss, {n: np.asarray(g[n]).ravel() for n in self.dims}
+
+    def eval_counts(self, p, X, y=None):
+        _, _, _, logits = self._forward(p, X)
+        tgt, mask = self._targets(X)
+        m = logits.max(axis=-1, keepdims=True)
+        lse = np.log(np.exp(logits - m).sum(axis=-1))
+        ce = -(np.take_along_axis(logits, tgt[..., None], axis=-1)[..., 0] - m[..., 0] - lse)
+        hit = np.argmax(logits, axis=-1) == tgt
+        return float((ce * mask).sum()), int((hit & mask).sum())
+
+
 # ------------------------------------------------------------ local work
 
 

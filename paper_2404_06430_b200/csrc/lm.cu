@@ -1,0 +1,1037 @@
+// Config C: the StackOverflow-shaped transformer language model
+// (models.TransformerLM), local SGD
+// of a whole cohort at once and the pre-training evaluation.
+//
+// The reference has no LM: the arithmetic is the oracle's TransformerLM
+// (oracle/port.py, pinned to float64 autograd), trained through the
+// reference's generic update rule (fedsim/models/models.py:53-79):
+//   theta <- theta - lr * (grad + prox_mu * (theta - theta_t) + control),
+// batches in perms order, the tail batch kept, the batch loss the mean
+// cross-entropy over the batch's non-pad targets.
+//
+// Layout.  A wave of W clients is trained together, every client's step-s
+// minibatch (B sentences x L positions = T rows) side by side: activations are
+// [W, T, width] fp32, each client's weights a row of Wc [W, D] (its current
+// theta) and its gradient a row of G [W, D], in TransformerLM.param_dims
+// order (PyTorch [out, in] weight layouts).  One step is ~45 launches over the
+// wave: a grouped (per-client) tiled GEMM for every projection -- forward
+// Y = X W^T (NT), backward dX = dY W (NN) and dW = dY^T X (TN) -- plus
+// attention (one warp per sentence x head, L <= 32), residual + LayerNorm
+// (one warp per row), the vocabulary softmax-CE (one CTA per row), bias /
+// gain column sums in a fixed row order, the deterministic embedding
+// scatter, and the SGD step.  Every reduction has a fixed order, so reruns
+// are bit-identical.
+//
+// Evaluation runs the same forward with the shared theta (weight stride 0)
+// over the cohort's sentences in chunks and sums per-sentence loss / hits
+// into each client's totals in sentence order.
+
+#include <math.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "fb_common.cuh"
+
+namespace fb {
+namespace lm {
+
+struct Dims {
+  int V, d, H, dh, F, layers, L;
+};
+
+// entry offsets inside one layer (models.TransformerLM.param_dims order)
+struct LayerOff {
+  int64_t in_w, in_b, out_w, out_b, l1_w, l1_b, l2_w, l2_b, n1_w, n1_b, n2_w, n2_b, size;
+};
+
+inline LayerOff layer_off(const Dims& m) {
+  LayerOff o;
+  const int64_t d = m.d, F = m.F;
+  o.in_w = 0;
+  o.in_b = o.in_w + 3 * d * d;
+  o.out_w = o.in_b + 3 * d;
+  o.out_b = o.out_w + d * d;
+  o.l1_w = o.out_b + d;
+  o.l1_b = o.l1_w + F * d;
+  o.l2_w = o.l1_b + F;
+  o.l2_b = o.l2_w + d * F;
+  o.n1_w = o.l2_b + d;
+  o.n1_b = o.n1_w + d;
+  o.n2_w = o.n1_b + d;
+  o.n2_b = o.n2_w + d;
+  o.size = o.n2_b + d;
+  return o;
+}
+inline int64_t num_params(const Dims& m) { return (int64_t)m.V * m.d + (int64_t)m.layers * layer_off(m).size; }
+inline int64_t layer_base(const Dims& m, int l) { return (int64_t)m.V * m.d + (int64_t)l * layer_off(m).size; }
+
+// ------------------------------------------------------------------ GEMM
+// C[z](m, n) = alpha * sum_k A[z](m, k) B[z](k, n) (+ beta C) (+ bias[z](n)),
+//   A(m, k) = TA ? A[k * lda + m] : A[m * lda + k]   (relu_a: max(0, .))
+//   B(k, n) = TB ? B[n * ldb + k] : B[k * ldb + n]   (relu_b: max(0, .))
+// mask_aux: multiply the result by (aux[z](m, n) > 0)  (ReLU backward).
+// Batches (clients) whose active[z] == 0 are skipped.
+struct Gemm {
+  const float* A;
+  int64_t lda, sA;
+  const float* B;
+  int64_t ldb, sB;
+  float* C;
+  int64_t ldc, sC;
+  int M, N, K;
+  const float* bias;
+  int64_t sBias;
+  const float* aux;
+  int64_t ldaux, sAux;
+  const int32_t* active;
+  float alpha, beta;
+  int relu_a, relu_b;
+};
+
+constexpr int BM = 64, BN = 64, BK = 16, GT = 256;
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(GT) gemm_kernel(const Gemm g) {
+  const int z = blockIdx.z;
+  if (g.active && !g.active[z]) return;
+  __shared__ float As[2][BK][BM + 4];
+  __shared__ float Bs[2][BK][BN + 4];
+  const float* A = g.A + (int64_t)z * g.sA;
+  const float* B = g.B + (int64_t)z * g.sB;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  float ra[4], rb[4];
+  // element i of this thread's share of a tile: (row-of-16, k) for NT-style loads, (k, col) otherwise
+  auto load_a = [&](int k0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int idx = tid + i * GT;
+      int m, k;
+      if (TA) { k = idx / BM; m = idx % BM; } else { m = idx / BK; k = idx % BK; }
+      const int gm = m0 + m, gk = k0 + k;
+      float v = 0.f;
+      if (gm < g.M && gk < g.K) v = TA ? A[(int64_t)gk * g.lda + gm] : A[(int64_t)gm * g.lda + gk];
+      ra[i] = g.relu_a ? fmaxf(v, 0.f) : v;
+    }
+  };
+  auto load_b = [&](int k0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int idx = tid + i * GT;
+      int n, k;
+      if (TB) { n = idx / BK; k = idx % BK; } else { k = idx / BN; n = idx % BN; }
+      const int gn = n0 + n, gk = k0 + k;
+      float v = 0.f;
+      if (gn < g.N && gk < g.K) v = TB ? B[(int64_t)gn * g.ldb + gk] : B[(int64_t)gk * g.ldb + gn];
+      rb[i] = g.relu_b ? fmaxf(v, 0.f) : v;
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int idx = tid + i * GT;
+      if (TA) As[buf][idx / BM][idx % BM] = ra[i]; else As[buf][idx % BK][idx / BK] = ra[i];
+      if (TB) Bs[buf][idx % BK][idx / BK] = rb[i]; else Bs[buf][idx / BN][idx % BN] = rb[i];
+    }
+  };
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+  const int nk = (g.K + BK - 1) / BK;
+  load_a(0);
+  load_b(0);
+  store(0);
+  __syncthreads();
+  for (int t = 0; t < nk; ++t) {
+    const int cur = t & 1;
+    if (t + 1 < nk) {  // next tile's global loads in flight during this tile's math
+      load_a((t + 1) * BK);
+      load_b((t + 1) * BK);
+    }
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      const float4 a = *reinterpret_cast<const float4*>(&As[cur][kk][ty * 4]);
+      const float4 b = *reinterpret_cast<const float4*>(&Bs[cur][kk][tx * 4]);
+      const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    if (t + 1 < nk) store(cur ^ 1);
+    __syncthreads();
+  }
+  float* C = g.C + (int64_t)z * g.sC;
+  const float* bias = g.bias ? g.bias + (int64_t)z * g.sBias : nullptr;
+  const float* aux = g.aux ? g.aux + (int64_t)z * g.sAux : nullptr;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + ty * 4 + i;
+    if (m >= g.M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + tx * 4 + j;
+      if (n >= g.N) continue;
+      float v = g.alpha * acc[i][j];
+      float* c = C + (int64_t)m * g.ldc + n;
+      if (g.beta != 0.f) v = fmaf(g.beta, *c, v);
+      if (bias) v += bias[n];
+      if (aux && !(aux[(int64_t)m * g.ldaux + n] > 0.f)) v = 0.f;
+      *c = v;
+    }
+  }
+}
+
+// ------------------------------------------------------------ batch gather
+// Client c's step-s minibatch: epoch e = s / nb, batch j = s % nb (nb = ceil(n / B)),
+// sentences perms[c][e * n + j * B + i]; slots past the batch are all-pad.
+// nvalid[c] = non-pad targets in the batch (0: client idle this step).
+__global__ void gather_batch_kernel(const float* __restrict__ X, const int64_t* __restrict__ row_start,
+                                    const int32_t* __restrict__ num_rows, const int32_t* __restrict__ perms,
+                                    const int64_t* __restrict__ perm_off, int c0, int epochs, int B, int L, int step,
+                                    int32_t* __restrict__ tok, int32_t* __restrict__ nvalid) {
+  const int w = blockIdx.x, c = c0 + w;
+  const int n = num_rows[c];
+  const int nb = n > 0 ? (n + B - 1) / B : 0;
+  const bool live = nb > 0 && step < epochs * nb;
+  const int e = live ? step / nb : 0, j = live ? step % nb : 0;
+  const int cnt = live ? min(B, n - j * B) : 0;
+  int32_t* t = tok + (int64_t)w * B * (L + 1);
+  __shared__ int nv;
+  if (threadIdx.x == 0) nv = 0;
+  __syncthreads();
+  int mine = 0;
+  for (int q = threadIdx.x; q < B * (L + 1); q += blockDim.x) {
+    const int i = q / (L + 1), p = q - i * (L + 1);
+    int v = 0;
+    if (i < cnt) {
+      const int r = perms[perm_off[c] + (int64_t)e * n + j * B + i];
+      v = (int)X[(row_start[c] + r) * (int64_t)(L + 1) + p];
+    }
+    t[q] = v;
+    mine += (p > 0 && v != 0);
+  }
+  atomicAdd(&nv, mine);  // integer: order-free
+  __syncthreads();
+  if (threadIdx.x == 0) nvalid[w] = nv;
+}
+
+// eval chunk: sentences [g0, g0 + cnt) of the cohort in client-major order
+__global__ void gather_eval_kernel(const float* __restrict__ X, const int64_t* __restrict__ row_start,
+                                   const int64_t* __restrict__ sent_off, int C, int64_t g0, int cnt, int L,
+                                   int32_t* __restrict__ tok) {
+  const int i = blockIdx.x;  // sentence slot
+  int32_t* t = tok + (int64_t)i * (L + 1);
+  if (i >= cnt) {
+    for (int p = threadIdx.x; p <= L; p += blockDim.x) t[p] = 0;
+    return;
+  }
+  const int64_t g = g0 + i;
+  int lo = 0, hi = C - 1;  // last client with sent_off <= g
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (sent_off[mid] <= g) lo = mid; else hi = mid - 1;
+  }
+  const int64_t row = row_start[lo] + (g - sent_off[lo]);
+  for (int p = threadIdx.x; p <= L; p += blockDim.x) t[p] = (int)X[row * (L + 1) + p];
+}
+
+__global__ void positions_kernel(float* __restrict__ pe, int L, int d) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= L * d) return;
+  const int pos = i / d, j = i - pos * d;
+  const double div = exp((double)(j & ~1) * (-log(10000.0) / d));
+  pe[i] = (float)((j & 1) ? cos(pos * div) : sin(pos * div));
+}
+
+// x[w, s*L + p, :] = E_w[tok[w, s, p]] * sqrt(d) + pe[p]
+__global__ void embed_kernel(const int32_t* __restrict__ tok, const float* __restrict__ Wc, int64_t sW,
+                             const float* __restrict__ pe, int B, int L, int d, const int32_t* __restrict__ active,
+                             float* __restrict__ x) {
+  const int w = blockIdx.y;
+  if (active && !active[w]) return;
+  const int row = blockIdx.x;  // s * L + p
+  const int s = row / L, p = row - s * L;
+  const int id = tok[((int64_t)w * B + s) * (L + 1) + p];
+  const float* E = Wc + (int64_t)w * sW + (int64_t)id * d;
+  const float sc = sqrtf((float)d);
+  float* out = x + ((int64_t)w * B * L + row) * d;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) out[j] = fmaf(E[j], sc, pe[p * d + j]);
+}
+
+// dE_w[tok] += dx0 * sqrt(d), tokens in row order (deterministic)
+__global__ void embed_bwd_kernel(const int32_t* __restrict__ tok, const float* __restrict__ dx, int B, int L, int d,
+                                 const int32_t* __restrict__ active, float* __restrict__ G, int64_t sG) {
+  const int w = blockIdx.x;
+  if (!active[w]) return;
+  const float sc = sqrtf((float)d);
+  float* gE = G + (int64_t)w * sG;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    for (int r = 0; r < B * L; ++r) {
+      const int s = r / L, p = r - s * L;
+      const int id = tok[((int64_t)w * B + s) * (L + 1) + p];
+      gE[(int64_t)id * d + j] = fmaf(dx[((int64_t)w * B * L + r) * d + j], sc, gE[(int64_t)id * d + j]);
+    }
+  }
+}
+
+// ----------------------------------------------------------------- attention
+// one warp per (client, sentence, head); lane i = query position i (L <= 32, dh <= 32)
+constexpr int kAttWarps = 2;  // (5 x 32 x 33 floats of staging per warp in the backward: 42 KB per CTA)
+
+__global__ void __launch_bounds__(32 * kAttWarps) attn_fwd_kernel(const float* __restrict__ qkv, int B, int L,
+                                                                  int H, int dh, const int32_t* __restrict__ active,
+                                                                  float* __restrict__ P, float* __restrict__ o) {
+  extern __shared__ float sh[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int w = blockIdx.y, unit = blockIdx.x * kAttWarps + warp;  // (sentence, head) of client w
+  if (unit >= B * H || !active[w]) return;
+  const int s = unit / H, h = unit - s * H;
+  const int d = H * dh;
+  float* q = sh + warp * 3 * 32 * 33;
+  float* k = q + 32 * 33;
+  float* v = k + 32 * 33;
+  const float* base = qkv + ((int64_t)w * B * L + (int64_t)s * L) * 3 * d;
+  for (int e = lane; e < L * dh; e += 32) {
+    const int i = e / dh, c = e - i * dh;
+    q[i * 33 + c] = base[(int64_t)i * 3 * d + h * dh + c];
+    k[i * 33 + c] = base[(int64_t)i * 3 * d + d + h * dh + c];
+    v[i * 33 + c] = base[(int64_t)i * 3 * d + 2 * d + h * dh + c];
+  }
+  __syncwarp();
+  float* prow = P + ((((int64_t)w * B + s) * H + h) * L) * L;
+  float* orow = o + ((int64_t)w * B * L + (int64_t)s * L) * d + h * dh;
+  if (lane < L) {
+    const int i = lane;
+    const float sc = 1.0f / sqrtf((float)dh);
+    float sv[32];
+    float mx = -INFINITY;
+    for (int j = 0; j <= i; ++j) {
+      float a = 0.f;
+      for (int c = 0; c < dh; ++c) a = fmaf(q[i * 33 + c], k[j * 33 + c], a);
+      sv[j] = a * sc;
+      mx = fmaxf(mx, sv[j]);
+    }
+    float sum = 0.f;
+    for (int j = 0; j <= i; ++j) {
+      sv[j] = expf(sv[j] - mx);
+      sum += sv[j];
+    }
+    const float inv = 1.0f / sum;
+    for (int j = 0; j < L; ++j) prow[i * L + j] = j <= i ? sv[j] * inv : 0.f;
+    for (int c = 0; c < dh; ++c) {
+      float a = 0.f;
+      for (int j = 0; j <= i; ++j) a = fmaf(sv[j] * inv, v[j * 33 + c], a);
+      orow[(int64_t)i * d + c] = a;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(32 * kAttWarps) attn_bwd_kernel(const float* __restrict__ qkv,
+                                                                  const float* __restrict__ P,
+                                                                  const float* __restrict__ dout, int B, int L, int H,
+                                                                  int dh, const int32_t* __restrict__ active,
+                                                                  float* __restrict__ dqkv) {
+  extern __shared__ float sh[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int w = blockIdx.y, unit = blockIdx.x * kAttWarps + warp;
+  if (unit >= B * H || !active[w]) return;
+  const int s = unit / H, h = unit - s * H;
+  const int d = H * dh;
+  float* q = sh + warp * 5 * 32 * 33;
+  float* k = q + 32 * 33;
+  float* v = k + 32 * 33;
+  float* dO = v + 32 * 33;
+  float* dS = dO + 32 * 33;
+  const float* base = qkv + ((int64_t)w * B * L + (int64_t)s * L) * 3 * d;
+  const float* dbase = dout + ((int64_t)w * B * L + (int64_t)s * L) * d + h * dh;
+  for (int e = lane; e < L * dh; e += 32) {
+    const int i = e / dh, c = e - i * dh;
+    q[i * 33 + c] = base[(int64_t)i * 3 * d + h * dh + c];
+    k[i * 33 + c] = base[(int64_t)i * 3 * d + d + h * dh + c];
+    v[i * 33 + c] = base[(int64_t)i * 3 * d + 2 * d + h * dh + c];
+    dO[i * 33 + c] = dbase[(int64_t)i * d + c];
+  }
+  const float* prow = P + ((((int64_t)w * B + s) * H + h) * L) * L;
+  const float sc = 1.0f / sqrtf((float)dh);
+  __syncwarp();
+  if (lane < L) {  // row i: dS_ij = P_ij (dP_ij - sum_j P_ij dP_ij) / sqrt(dh)
+    const int i = lane;
+    float dp[32];
+    float rs = 0.f;
+    for (int j = 0; j <= i; ++j) {
+      float a = 0.f;
+      for (int c = 0; c < dh; ++c) a = fmaf(dO[i * 33 + c], v[j * 33 + c], a);
+      dp[j] = a;
+      rs = fmaf(prow[i * L + j], a, rs);
+    }
+    for (int j = 0; j < L; ++j) dS[i * 33 + j] = j <= i ? prow[i * L + j] * (dp[j] - rs) * sc : 0.f;
+  }
+  __syncwarp();
+  float* dq = dqkv + ((int64_t)w * B * L + (int64_t)s * L) * 3 * d + h * dh;
+  if (lane < L) {
+    const int i = lane;  // dq_i = sum_j dS_ij k_j ; dk_i = sum_r dS_ri q_r ; dv_i = sum_r P_ri dO_r
+    for (int c = 0; c < dh; ++c) {
+      float aq = 0.f, ak = 0.f, av = 0.f;
+      for (int j = 0; j <= i; ++j) aq = fmaf(dS[i * 33 + j], k[j * 33 + c], aq);
+      for (int r = i; r < L; ++r) {
+        ak = fmaf(dS[r * 33 + i], q[r * 33 + c], ak);
+        av = fmaf(prow[r * L + i], dO[r * 33 + c], av);
+      }
+      dq[(int64_t)i * 3 * d + c] = aq;
+      dq[(int64_t)i * 3 * d + d + c] = ak;
+      dq[(int64_t)i * 3 * d + 2 * d + c] = av;
+    }
+  }
+}
+
+// --------------------------------------------------------------- LayerNorm
+// out = LN(a + b) * g + beta per row of d (one warp per row); keeps xh, rstd
+__global__ void add_ln_kernel(const float* __restrict__ a, const float* __restrict__ b, const float* __restrict__ gw,
+                              const float* __restrict__ gb, int64_t sWc, int rows, int d, float eps,
+                              const int32_t* __restrict__ active, float* __restrict__ xh, float* __restrict__ rstd,
+                              float* __restrict__ out) {
+  const int w = blockIdx.y;
+  if (!active[w]) return;
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const int64_t off = ((int64_t)w * rows + r) * d;
+  float y[8];
+  float s = 0.f;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int j = lane + 32 * u;
+    y[u] = j < d ? a[off + j] + b[off + j] : 0.f;
+    s += y[u];
+  }
+  s = warp_sum(s);
+  const float mean = s / d;
+  float v = 0.f;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int j = lane + 32 * u;
+    const float c = j < d ? y[u] - mean : 0.f;
+    v = fmaf(c, c, v);
+  }
+  v = warp_sum(v);
+  const float rs = 1.0f / sqrtf(v / d + eps);
+  const float* g = gw + (int64_t)w * sWc;
+  const float* be = gb + (int64_t)w * sWc;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int j = lane + 32 * u;
+    if (j < d) {
+      const float h = (y[u] - mean) * rs;
+      if (xh) xh[off + j] = h;
+      out[off + j] = fmaf(h, g[j], be[j]);
+    }
+  }
+  if (rstd && lane == 0) rstd[(int64_t)w * rows + r] = rs;
+}
+
+// dy = rstd * (dxh - mean(dxh) - xh * mean(dxh * xh)), dxh = dout * g
+__global__ void ln_bwd_kernel(const float* __restrict__ dout, const float* __restrict__ xh,
+                              const float* __restrict__ rstd, const float* __restrict__ gw, int64_t sWc, int rows,
+                              int d, const int32_t* __restrict__ active, float* __restrict__ dy) {
+  const int w = blockIdx.y;
+  if (!active[w]) return;
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const int64_t off = ((int64_t)w * rows + r) * d;
+  const float* g = gw + (int64_t)w * sWc;
+  float dh[8], hh[8];
+  float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int j = lane + 32 * u;
+    dh[u] = j < d ? dout[off + j] * g[j] : 0.f;
+    hh[u] = j < d ? xh[off + j] : 0.f;
+    s1 += dh[u];
+    s2 = fmaf(dh[u], hh[u], s2);
+  }
+  s1 = warp_sum(s1) / d;
+  s2 = warp_sum(s2) / d;
+  const float rs = rstd[(int64_t)w * rows + r];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int j = lane + 32 * u;
+    if (j < d) dy[off + j] = rs * (dh[u] - s1 - hh[u] * s2);
+  }
+}
+
+// G_w[col] = sum_r in1[w, r, col] (* in2[w, r, col]), rows in order (deterministic)
+__global__ void colsum_kernel(const float* __restrict__ in1, const float* __restrict__ in2, int rows, int cols,
+                              const int32_t* __restrict__ active, float* __restrict__ G, int64_t sG) {
+  const int w = blockIdx.y;
+  if (!active[w]) return;
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= cols) return;
+  const int64_t base = (int64_t)w * rows * cols + col;
+  float s = 0.f;
+  if (in2) {
+    for (int r = 0; r < rows; ++r) s = fmaf(in1[base + (int64_t)r * cols], in2[base + (int64_t)r * cols], s);
+  } else {
+    for (int r = 0; r < rows; ++r) s += in1[base + (int64_t)r * cols];
+  }
+  G[(int64_t)w * sG + col] = s;
+}
+
+// ------------------------------------------------------------ softmax-CE
+// one CTA per row of V logits; target t = tok[w, s, p + 1] (0 = pad: ignored).
+// train: logits <- (softmax - onehot) / nvalid[w] (0 for pad rows).
+// eval : row_loss / row_hit (first argmax) for non-pad rows, 0 else.
+constexpr int kCeT = 256;
+
+template <bool kTrain>
+__global__ void __launch_bounds__(kCeT) ce_kernel(float* __restrict__ logits, const int32_t* __restrict__ tok,
+                                                  int B, int L, int V, const int32_t* __restrict__ nvalid,
+                                                  float* __restrict__ row_loss, int32_t* __restrict__ row_hit) {
+  const int w = blockIdx.y;
+  if (kTrain && nvalid[w] == 0) return;
+  const int r = blockIdx.x;  // s * L + p
+  const int s = r / L, p = r - s * L;
+  const int tgt = tok[((int64_t)w * B + s) * (L + 1) + p + 1];
+  float* z = logits + ((int64_t)w * B * L + r) * V;
+  __shared__ float red[32];
+  __shared__ int redi[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (tgt == 0) {
+    if (kTrain) {
+      for (int v = threadIdx.x; v < V; v += kCeT) z[v] = 0.f;
+    } else if (threadIdx.x == 0) {
+      row_loss[(int64_t)w * B * L + r] = 0.f;
+      row_hit[(int64_t)w * B * L + r] = 0;
+    }
+    return;
+  }
+  // max (and its first index for eval)
+  float mx = -INFINITY;
+  int arg = 0x7fffffff;
+  for (int v = threadIdx.x; v < V; v += kCeT) {
+    const float x = z[v];
+    if (x > mx) { mx = x; arg = v; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float om = __shfl_xor_sync(0xffffffffu, mx, o);
+    const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+    if (om > mx || (om == mx && oa < arg)) { mx = om; arg = oa; }
+  }
+  if (lane == 0) { red[wid] = mx; redi[wid] = arg; }
+  __syncthreads();
+  if (wid == 0) {
+    mx = lane < kCeT / 32 ? red[lane] : -INFINITY;
+    arg = lane < kCeT / 32 ? redi[lane] : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float om = __shfl_xor_sync(0xffffffffu, mx, o);
+      const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+      if (om > mx || (om == mx && oa < arg)) { mx = om; arg = oa; }
+    }
+    if (lane == 0) { red[0] = mx; redi[0] = arg; }
+  }
+  __syncthreads();
+  mx = red[0];
+  arg = redi[0];
+  __syncthreads();
+  float se = 0.f;
+  for (int v = threadIdx.x; v < V; v += kCeT) se += expf(z[v] - mx);
+  se = warp_sum(se);
+  if (lane == 0) red[wid] = se;
+  __syncthreads();
+  if (wid == 0) {
+    se = lane < kCeT / 32 ? red[lane] : 0.f;
+    se = warp_sum(se);
+    if (lane == 0) red[0] = se;
+  }
+  __syncthreads();
+  se = red[0];
+  if (kTrain) {
+    const float scale = 1.0f / (float)nvalid[w];
+    const float inv = 1.0f / se;
+    for (int v = threadIdx.x; v < V; v += kCeT) {
+      float pr = expf(z[v] - mx) * inv;
+      if (v == tgt) pr -= 1.0f;
+      z[v] = pr * scale;
+    }
+  } else if (threadIdx.x == 0) {
+    row_loss[(int64_t)w * B * L + r] = -(z[tgt] - mx - logf(se));
+    row_hit[(int64_t)w * B * L + r] = arg == tgt;
+  }
+}
+
+// per-sentence (in position order) then per-client (in sentence order) eval sums
+__global__ void eval_accum_kernel(const float* __restrict__ row_loss, const int32_t* __restrict__ row_hit,
+                                  const int64_t* __restrict__ sent_off, const int32_t* __restrict__ num_rows, int C,
+                                  int64_t g0, int cnt, int L, double* __restrict__ loss, int32_t* __restrict__ correct) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const int64_t lo = sent_off[c] > g0 ? sent_off[c] : g0;
+  const int64_t hi = sent_off[c] + num_rows[c] < g0 + cnt ? sent_off[c] + num_rows[c] : g0 + cnt;
+  double s = 0.0;
+  int k = 0;
+  for (int64_t g = lo; g < hi; ++g) {
+    const int64_t i = g - g0;
+    double sl = 0.0;
+    for (int p = 0; p < L; ++p) {
+      sl += (double)row_loss[i * L + p];
+      k += row_hit[i * L + p];
+    }
+    s += sl;
+  }
+  if (hi > lo) {
+    loss[c] += s;
+    correct[c] += k;
+  }
+}
+
+// -------------------------------------------------------------- SGD step
+// theta <- theta - lr * (g + mu * (theta - theta_t) + control); delta accumulates the step
+__global__ void sgd_kernel(float* __restrict__ Wc, const float* __restrict__ G, int64_t sW,
+                           float* __restrict__ Dl, int64_t ldD, const float* __restrict__ control, int64_t ldc,
+                           int64_t D, float lr, float mu, const int32_t* __restrict__ nvalid) {
+  const int w = blockIdx.y;
+  if (nvalid[w] == 0) return;
+  float* W = Wc + (int64_t)w * sW;
+  const float* g = G + (int64_t)w * sW;
+  float* dl = Dl + (int64_t)w * ldD;
+  const float* ct = control ? control + (int64_t)w * ldc : nullptr;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < D; i += (int64_t)gridDim.x * blockDim.x) {
+    float s = g[i];
+    if (mu != 0.f) s = fmaf(mu, -dl[i], s);
+    if (ct) s += ct[i];
+    s *= lr;
+    W[i] -= s;
+    dl[i] += s;
+  }
+}
+
+__global__ void init_wave_kernel(const float* __restrict__ theta_t, int64_t D, float* __restrict__ Wc, int64_t sW,
+                                 float* __restrict__ Dl, int64_t ldD) {
+  const int w = blockIdx.y;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < D; i += (int64_t)gridDim.x * blockDim.x) {
+    Wc[(int64_t)w * sW + i] = theta_t[i];
+    Dl[(int64_t)w * ldD + i] = 0.f;
+  }
+}
+
+__global__ void nonfinite_kernel(const float* __restrict__ Dl, int64_t ldD, int64_t D, int32_t* __restrict__ bad) {
+  const int w = blockIdx.x;
+  int b = 0;
+  for (int64_t i = threadIdx.x; i < D; i += blockDim.x) b |= !isfinite(Dl[(int64_t)w * ldD + i]);
+  b = __syncthreads_or(b);
+  if (threadIdx.x == 0) bad[w] = b;
+}
+
+__global__ void copy_kernel(const float* __restrict__ src, float* __restrict__ dst, int64_t n_per, int64_t stride,
+                            const int32_t* __restrict__ active) {
+  const int w = blockIdx.y;
+  if (!active[w]) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_per; i += (int64_t)gridDim.x * blockDim.x)
+    dst[(int64_t)w * stride + i] = src[(int64_t)w * stride + i];
+}
+
+__global__ void ones_kernel(int32_t* p, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = 1;
+}
+
+__global__ void sent_offsets_kernel(const int32_t* __restrict__ num_rows, int C, int64_t* __restrict__ off) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    int64_t s = 0;
+    for (int c = 0; c < C; ++c) {
+      off[c] = s;
+      s += num_rows[c];
+    }
+  }
+}
+
+// ------------------------------------------------------------ workspace
+struct Buf {
+  size_t off = 0;
+  char* base = nullptr;
+  template <typename T>
+  T* take(size_t n) {
+    off = (off + 255) & ~size_t(255);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += n * sizeof(T);
+    return p;
+  }
+};
+
+struct Layer {
+  float *xin, *qkv, *P, *o, *xh1, *r1, *x1, *z, *xh2, *r2;
+};
+
+struct Work {
+  int32_t *tok, *nvalid, *active, *hit;
+  int64_t* sent_off;
+  float *pe, *Wc, *G, *xf, *logits, *dx, *dx1, *dz, *dqkv, *dtmp, *a, *f, *rloss;
+  std::vector<Layer> layer;
+};
+
+// W groups of B sentences; train = with gradient / client-weight buffers
+inline Work carve(const Dims& m, int W, int B, bool train, Buf& b) {
+  const int64_t T = (int64_t)B * m.L, d = m.d, D = num_params(m);
+  const int64_t sW = (D + 3) & ~int64_t(3);
+  Work k;
+  k.tok = b.take<int32_t>((size_t)W * B * (m.L + 1));
+  k.nvalid = b.take<int32_t>(W);
+  k.active = b.take<int32_t>(W);
+  k.sent_off = b.take<int64_t>(65536);
+  k.pe = b.take<float>((size_t)m.L * d);
+  k.Wc = train ? b.take<float>((size_t)W * sW) : nullptr;
+  k.G = train ? b.take<float>((size_t)W * sW) : nullptr;
+  k.layer.resize(m.layers);
+  for (int l = 0; l < m.layers; ++l) {
+    Layer& y = k.layer[l];
+    y.xin = b.take<float>((size_t)W * T * d);
+    y.qkv = b.take<float>((size_t)W * T * 3 * d);
+    y.P = b.take<float>((size_t)W * B * m.H * m.L * m.L);
+    y.o = b.take<float>((size_t)W * T * d);
+    y.xh1 = b.take<float>((size_t)W * T * d);
+    y.r1 = b.take<float>((size_t)W * T);
+    y.x1 = b.take<float>((size_t)W * T * d);
+    y.z = b.take<float>((size_t)W * T * m.F);
+    y.xh2 = b.take<float>((size_t)W * T * d);
+    y.r2 = b.take<float>((size_t)W * T);
+  }
+  k.xf = b.take<float>((size_t)W * T * d);
+  k.a = b.take<float>((size_t)W * T * d);
+  k.f = b.take<float>((size_t)W * T * d);
+  k.logits = b.take<float>((size_t)W * T * m.V);
+  k.rloss = b.take<float>((size_t)W * T);
+  k.hit = b.take<int32_t>((size_t)W * T);
+  if (train) {
+    k.dx = b.take<float>((size_t)W * T * d);
+    k.dx1 = b.take<float>((size_t)W * T * d);
+    k.dz = b.take<float>((size_t)W * T * m.F);
+    k.dqkv = b.take<float>((size_t)W * T * 3 * d);
+    k.dtmp = b.take<float>((size_t)W * T * d);
+  } else {
+    k.dx = k.dx1 = k.dz = k.dqkv = k.dtmp = nullptr;
+  }
+  return k;
+}
+
+int launch_gemm(bool TA, bool TB, const Gemm& g, int batch, cudaStream_t s) {
+  if (batch <= 0 || g.M <= 0 || g.N <= 0) return FB_OK;
+  const dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM, batch);
+  if (!TA && TB) FB_LAUNCH("lm_gemm_nt_kernel", s, (gemm_kernel<false, true><<<grid, GT, 0, s>>>(g)));
+  else if (!TA && !TB) FB_LAUNCH("lm_gemm_nn_kernel", s, (gemm_kernel<false, false><<<grid, GT, 0, s>>>(g)));
+  else FB_LAUNCH("lm_gemm_tn_kernel", s, (gemm_kernel<true, false><<<grid, GT, 0, s>>>(g)));
+  return launch_status("lm_gemm_kernel");
+}
+
+Gemm gemm_base() {
+  Gemm g{};
+  g.alpha = 1.f;
+  g.beta = 0.f;
+  return g;
+}
+
+// ------------------------------------------------------------- forward
+// W groups of B sentences; weights at Wc + w * sW (sW = 0: one shared theta)
+int forward(const Dims& m, const Work& k, const float* Wc, int64_t sW, int W, int B, cudaStream_t s) {
+  const int T = B * m.L, d = m.d;
+  const LayerOff lo = layer_off(m);
+  FB_LAUNCH("lm_embed_kernel", s, (embed_kernel<<<dim3(T, W), 128, 0, s>>>(k.tok, Wc, sW, k.pe, B, m.L, d,
+                                                                            k.active, k.layer[0].xin)));
+  int st;
+  for (int l = 0; l < m.layers; ++l) {
+    const Layer& y = k.layer[l];
+    const float* P = Wc + layer_base(m, l);
+    float* xout = l + 1 < m.layers ? k.layer[l + 1].xin : k.xf;
+    Gemm g = gemm_base();  // qkv = x Wqkv^T + b
+    g.A = y.xin; g.lda = d; g.sA = (int64_t)T * d;
+    g.B = P + lo.in_w; g.ldb = d; g.sB = sW;
+    g.C = y.qkv; g.ldc = 3 * d; g.sC = (int64_t)T * 3 * d;
+    g.M = T; g.N = 3 * d; g.K = d;
+    g.bias = P + lo.in_b; g.sBias = sW;
+    g.active = k.active;
+    if ((st = launch_gemm(false, true, g, W, s))) return st;
+    FB_LAUNCH("lm_attn_fwd_kernel", s,
+              (attn_fwd_kernel<<<dim3((B * m.H + kAttWarps - 1) / kAttWarps, W), 32 * kAttWarps,
+                                 kAttWarps * 3 * 32 * 33 * sizeof(float), s>>>(y.qkv, B, m.L, m.H, m.dh, k.active,
+                                                                              y.P, y.o)));
+    g = gemm_base();  // a = o Wo^T + bo
+    g.A = y.o; g.lda = d; g.sA = (int64_t)T * d;
+    g.B = P + lo.out_w; g.ldb = d; g.sB = sW;
+    g.C = k.a; g.ldc = d; g.sC = (int64_t)T * d;
+    g.M = T; g.N = d; g.K = d;
+    g.bias = P + lo.out_b; g.sBias = sW;
+    g.active = k.active;
+    if ((st = launch_gemm(false, true, g, W, s))) return st;
+    const dim3 lngrid((T + 7) / 8, W);
+    FB_LAUNCH("lm_add_ln_kernel", s, (add_ln_kernel<<<lngrid, 256, 0, s>>>(y.xin, k.a, P + lo.n1_w, P + lo.n1_b, sW,
+                                                                           T, d, 1e-5f, k.active, y.xh1, y.r1, y.x1)));
+    g = gemm_base();  // z = x1 W1^T + b1
+    g.A = y.x1; g.lda = d; g.sA = (int64_t)T * d;
+    g.B = P + lo.l1_w; g.ldb = d; g.sB = sW;
+    g.C = y.z; g.ldc = m.F; g.sC = (int64_t)T * m.F;
+    g.M = T; g.N = m.F; g.K = d;
+    g.bias = P + lo.l1_b; g.sBias = sW;
+    g.active = k.active;
+    if ((st = launch_gemm(false, true, g, W, s))) return st;
+    g = gemm_base();  // f = relu(z) W2^T + b2
+    g.A = y.z; g.lda = m.F; g.sA = (int64_t)T * m.F; g.relu_a = 1;
+    g.B = P + lo.l2_w; g.ldb = m.F; g.sB = sW;
+    g.C = k.f; g.ldc = d; g.sC = (int64_t)T * d;
+    g.M = T; g.N = d; g.K = m.F;
+    g.bias = P + lo.l2_b; g.sBias = sW;
+    g.active = k.active;
+    if ((st = launch_gemm(false, true, g, W, s))) return st;
+    FB_LAUNCH("lm_add_ln_kernel", s, (add_ln_kernel<<<lngrid, 256, 0, s>>>(y.x1, k.f, P + lo.n2_w, P + lo.n2_b, sW,
+                                                                           T, d, 1e-5f, k.active, y.xh2, y.r2, xout)));
+  }
+  Gemm g = gemm_base();  // logits = x E^T (tied embedding)
+  g.A = k.xf; g.lda = d; g.sA = (int64_t)T * d;
+  g.B = Wc; g.ldb = d; g.sB = sW;
+  g.C = k.logits; g.ldc = m.V; g.sC = (int64_t)T * m.V;
+  g.M = T; g.N = m.V; g.K = d;
+  g.active = k.active;
+  return launch_gemm(false, true, g, W, s);
+}
+
+// ------------------------------------------------------------- backward
+// gradient of the step's mean loss into G (every entry written once, then the
+// embedding scatter adds the input-side term)
+int backward(const Dims& m, const Work& k, int64_t sW, int W, int B, cudaStream_t s) {
+  const int T = B * m.L, d = m.d;
+  const LayerOff lo = layer_off(m);
+  int st;
+  FB_LAUNCH("lm_ce_kernel", s, (ce_kernel<true><<<dim3(T, W), kCeT, 0, s>>>(k.logits, k.tok, B, m.L, m.V, k.nvalid,
+                                                                            nullptr, nullptr)));
+  Gemm g = gemm_base();  // dE = dlogits^T x
+  g.A = k.logits; g.lda = m.V; g.sA = (int64_t)T * m.V;
+  g.B = k.xf; g.ldb = d; g.sB = (int64_t)T * d;
+  g.C = k.G; g.ldc = d; g.sC = sW;
+  g.M = m.V; g.N = d; g.K = T;
+  g.active = k.nvalid;
+  if ((st = launch_gemm(true, false, g, W, s))) return st;
+  g = gemm_base();  // dx = dlogits E
+  g.A = k.logits; g.lda = m.V; g.sA = (int64_t)T * m.V;
+  g.B = k.Wc; g.ldb = d; g.sB = sW;
+  g.C = k.dx; g.ldc = d; g.sC = (int64_t)T * d;
+  g.M = T; g.N = d; g.K = m.V;
+  g.active = k.nvalid;
+  if ((st = launch_gemm(false, false, g, W, s))) return st;
+  const dim3 lngrid((T + 7) / 8, W);
+  const dim3 cs_d((d + 127) / 128, W), cs_3d((3 * d + 127) / 128, W), cs_F((m.F + 127) / 128, W);
+  for (int l = m.layers - 1; l >= 0; --l) {
+    const Layer& y = k.layer[l];
+    const int64_t pb = layer_base(m, l);
+    const float* P = k.Wc + pb;
+    float* Gl = k.G + pb;
+    // LayerNorm 2: gains / biases, then into x1
+    FB_LAUNCH("lm_colsum_kernel", s, (colsum_kernel<<<cs_d, 128, 0, s>>>(k.dx, y.xh2, T, d, k.nvalid, Gl + lo.n2_w, sW)));
+    FB_LAUNCH("lm_colsum_kernel", s, (colsum_kernel<<<cs_d, 128, 0, s>>>(k.dx, nullptr, T, d, k.nvalid, Gl + lo.n2_b, sW)));
+    FB_LAUNCH("lm_ln_bwd_kernel", s, (ln_bwd_kernel<<<lngrid, 256, 0, s>>>(k.dx, y.xh2, y.r2, P + lo.n2_w, sW, T, d,
+                                                                           k.nvalid, k.dx1)));
+    // feed-forward
+    g = gemm_base();  // dW2 = dx1^T relu(z)
+    g.A = k.dx1; g.lda = d; g.sA = (int64_t)T * d;
+    g.B = y.z; g.ldb = m.F; g.sB = (int64_t)T * m.F; g.relu_b = 1;
+    g.C = Gl + lo.l2_w; g.ldc = m.F; g.sC = sW;
+    g.M = d; g.N = m.F; g.K = T;
+    g.active = k.nvalid;
+    if ((st = launch_gemm(true, false, g, W, s))) return st;
+    FB_LAUNCH("lm_colsum_kernel", s, (colsum_kernel<<<cs_d, 128, 0, s>>>(k.dx1, nullptr, T, d, k.nvalid, Gl + lo.l2_b, sW)));
+    g = gemm_base();  // dz = (dx1 W2) * (z > 0)
+    g.A = k.dx1; g.lda = d; g.sA = (int64_t)T * d;
+    g.B = P + lo.l2_w; g.ldb = m.F; g.sB = sW;
+    g.C = k.dz; g.ldc = m.F; g.sC = (int64_t)T * m.F;
+    g.M = T; g.N = m.F; g.K = d;
+    g.aux = y.z; g.ldaux = m.F; g.sAux = (int64_t)T * m.F;
+    g.active = k.nvalid;
+    if ((st = launch_gemm(false, false, g, W, s))) return st;
+    g = gemm_base();  // dW1 = dz^T x1
+    g.A = k.dz; g.lda = m.F; g.sA = (int64_t)T * m.F;
+    g.B = y.x1; g.ldb = d; g.sB = (int64_t)T * d;
+    g.C = Gl + lo.l1_w; g.ldc = d; g.sC = sW;
+    g.M = m.F; g.N = d; g.K = T;
+    g.active = k.nvalid;
+    if ((st = launch_gemm(true, false, g, W, s))) return st;
+    FB_LAUNCH("lm_colsum_kernel", s, (colsum_kernel<<<cs_F, 128, 0, s>>>(k.dz, nullptr, T, m.F, k.nvalid, Gl + lo.l1_b, sW)));
+    g = gemm_base();  // dx1 += dz W1
+    g.A = k.dz; g.lda = m.F; g.sA = (int64_t)T * m.F;
+    g.B = P + lo.l1_w; g.ldb = d; g.sB = sW;
+    g.C = k.dx1; g.ldc = d; g.sC = (int64_t)T * d;
+    g.M = T; g.N = d; g.K = m.F;
+    g.beta = 1.f;
+    g.active = k.nvalid;
+    if ((st = launch_gemm(false, false, g, W, s))) return st;
+    // LayerNorm 1: gains / biases, then into x and the attention output a
+    FB_LAUNCH("lm_colsum_kernel", s, (colsum_kernel<<<cs_d, 128, 0, s>>>(k.dx1, y.xh1, T, d, k.nvalid, Gl + lo.n1_w, sW)));
+    FB_LAUNCH("lm_colsum_kernel", s, (colsum_kernel<<<cs_d, 128, 0, s>>>(k.dx1, nullptr, T, d, k.nvalid, Gl + lo.n1_b, sW)));
+    FB_LAUNCH("lm_ln_bwd_kernel", s, (ln_bwd_kernel<<<lngrid, 256, 0, s>>>(k.dx1, y.xh1, y.r1, P + lo.n1_w, sW, T, d,
+                                                                           k.nvalid, k.dx)));  // dy1 -> dx
+    g = gemm_base();  // dWo = dy1^T o
+    g.A = k.dx; g.lda = d; g.sA = (int64_t)T * d;
+    g.B = y.o; g.ldb = d; g.sB = (int64_t)T * d;
+    g.C = Gl + lo.out_w; g.ldc = d; g.sC = sW;
+    g.M = d; g.N = d; g.K = T;
+    g.active = k.nvalid;
+    if ((st = launch_gemm(true, false, g, W, s))) return st;
+    FB_LAUNCH("lm_colsum_kernel", s, (colsum_kernel<<<cs_d, 128, 0, s>>>(k.dx, nullptr, T, d, k.nvalid, Gl + lo.out_b, sW)));
+    g = gemm_base();  // do = dy1 Wo
+    g.A = k.dx; g.lda = d; g.sA = (int64_t)T * d;
+    g.B = P + lo.out_w; g.ldb = d; g.sB = sW;
+    g.C = k.dtmp; g.ldc = d; g.sC = (int64_t)T * d;
+    g.M = T; g.N = d; g.K = d;
+    g.active = k.nvalid;
+    if ((st = launch_gemm(false, false, g, W, s))) return st;
+    FB_LAUNCH("lm_attn_bwd_kernel", s,
+              (attn_bwd_kernel<<<dim3((B * m.H + kAttWarps - 1) / kAttWarps, W), 32 * kAttWarps,
+                                 kAttWarps * 5 * 32 * 33 * sizeof(float), s>>>(y.qkv, y.P, k.dtmp, B, m.L, m.H, m.dh,
+                                                                              k.nvalid, k.dqkv)));
+    g = gemm_base();  // dWqkv = dqkv^T x
+    g.A = k.dqkv; g.lda = 3 * d; g.sA = (int64_t)T * 3 * d;
+    g.B = y.xin; g.ldb = d; g.sB = (int64_t)T * d;
+    g.C = Gl + lo.in_w; g.ldc = d; g.sC = sW;
+    g.M = 3 * d; g.N = d; g.K = T;
+    g.active = k.nvalid;
+    if ((st = launch_gemm(true, false, g, W, s))) return st;
+    FB_LAUNCH("lm_colsum_kernel", s, (colsum_kernel<<<cs_3d, 128, 0, s>>>(k.dqkv, nullptr, T, 3 * d, k.nvalid,
+                                                                          Gl + lo.in_b, sW)));
+    g = gemm_base();  // dx (= dy1, the residual) += dqkv Wqkv
+    g.A = k.dqkv; g.lda = 3 * d; g.sA = (int64_t)T * 3 * d;
+    g.B = P + lo.in_w; g.ldb = d; g.sB = sW;
+    g.C = k.dx; g.ldc = d; g.sC = (int64_t)T * d;
+    g.M = T; g.N = d; g.K = 3 * d;
+    g.beta = 1.f;
+    g.active = k.nvalid;
+    if ((st = launch_gemm(false, false, g, W, s))) return st;
+  }
+  FB_LAUNCH("lm_embed_bwd_kernel", s, (embed_bwd_kernel<<<W, 128, 0, s>>>(k.tok, k.dx, B, m.L, d, k.nvalid, k.G, sW)));
+  return launch_status("lm backward");
+}
+
+bool dims_ok(const Dims& m) {
+  return m.V >= 2 && m.d >= 1 && m.d <= 256 && m.H >= 1 && m.d % m.H == 0 && m.dh <= 32 && m.F >= 1 &&
+         m.layers >= 1 && m.L >= 1 && m.L <= 32;
+}
+
+Dims parse(const int32_t* dims) {
+  Dims m;
+  m.V = dims[0];
+  m.d = dims[1];
+  m.H = dims[2] > 0 ? dims[2] : 1;
+  m.dh = m.d / m.H;
+  m.F = dims[3];
+  m.layers = dims[4];
+  m.L = dims[5];
+  return m;
+}
+
+}  // namespace lm
+}  // namespace fb
+
+extern "C" {
+
+int64_t fb_lm_num_params(const int32_t* dims) { return dims ? fb::lm::num_params(fb::lm::parse(dims)) : 0; }
+
+int64_t fb_lm_workspace_bytes(const int32_t* dims, int batch_size, int clients_per_wave, int eval_groups) {
+  if (!dims || batch_size < 1) return 0;
+  const fb::lm::Dims m = fb::lm::parse(dims);
+  fb::lm::Buf a, b;
+  fb::lm::carve(m, clients_per_wave > 0 ? clients_per_wave : 1, batch_size, true, a);
+  fb::lm::carve(m, eval_groups > 0 ? eval_groups : 1, batch_size, false, b);
+  return (int64_t)(a.off > b.off ? a.off : b.off) + 256;
+}
+
+int fb_eval_lm_f32(const float* theta, const int32_t* dims, const float* X, const int64_t* row_start,
+                   const int32_t* num_rows, const int32_t* h_num_rows, int num_clients, double* loss_sum,
+                   int32_t* correct, int batch_size, int eval_groups, void* workspace, int64_t workspace_bytes,
+                   void* stream) {
+  FB_REQUIRE(dims != nullptr && h_num_rows != nullptr, "eval_lm: null dims / host row counts");
+  const fb::lm::Dims m = fb::lm::parse(dims);
+  FB_UNSUPPORTED(fb::lm::dims_ok(m), "eval_lm: unsupported shape (d <= 256, d %% heads == 0, head dim <= 32, seq <= 32)");
+  FB_REQUIRE(num_clients >= 0 && num_clients <= 65536 && batch_size >= 1 && eval_groups >= 1,
+             "eval_lm: bad sizes");
+  FB_REQUIRE(workspace_bytes >= fb_lm_workspace_bytes(dims, batch_size, 1, eval_groups), "eval_lm: workspace too small");
+  cudaStream_t s = fb::as_stream(stream);
+  if (num_clients == 0) return FB_OK;
+  cudaMemsetAsync(loss_sum, 0, sizeof(double) * num_clients, s);
+  cudaMemsetAsync(correct, 0, sizeof(int32_t) * num_clients, s);
+  fb::lm::Buf b;
+  b.base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255));
+  const fb::lm::Work k = fb::lm::carve(m, eval_groups, batch_size, false, b);
+  const int W = eval_groups, B = batch_size, L = m.L;
+  FB_LAUNCH("lm_positions_kernel", s, (fb::lm::positions_kernel<<<(L * m.d + 255) / 256, 256, 0, s>>>(k.pe, L, m.d)));
+  FB_LAUNCH("lm_ones_kernel", s, (fb::lm::ones_kernel<<<(W + 255) / 256, 256, 0, s>>>(k.active, W)));
+  FB_LAUNCH("lm_sent_offsets_kernel", s, (fb::lm::sent_offsets_kernel<<<1, 32, 0, s>>>(num_rows, num_clients, k.sent_off)));
+  int64_t total = 0;
+  for (int c = 0; c < num_clients; ++c) total += h_num_rows[c];
+  const int chunk = W * B;
+  for (int64_t g0 = 0; g0 < total; g0 += chunk) {
+    const int cnt = (int)(total - g0 < chunk ? total - g0 : chunk);
+    FB_LAUNCH("lm_gather_eval_kernel", s, (fb::lm::gather_eval_kernel<<<chunk, 32, 0, s>>>(
+                                              X, row_start, k.sent_off, num_clients, g0, cnt, L, k.tok)));
+    int st = fb::lm::forward(m, k, theta, 0, W, B, s);
+    if (st) return st;
+    FB_LAUNCH("lm_ce_kernel", s, (fb::lm::ce_kernel<false><<<dim3(B * L, W), fb::lm::kCeT, 0, s>>>(
+                                     k.logits, k.tok, B, L, m.V, nullptr, k.rloss, k.hit)));
+    FB_LAUNCH("lm_eval_accum_kernel", s, (fb::lm::eval_accum_kernel<<<(num_clients + 127) / 128, 128, 0, s>>>(
+                                             k.rloss, k.hit, k.sent_off, num_rows, num_clients, g0, cnt, L, loss_sum,
+                                             correct)));
+  }
+  return fb::launch_status("eval_lm");
+}
+
+int fb_local_sgd_lm_f32(const float* theta_t, const int32_t* dims, const float* X, const int64_t* row_start,
+                        const int32_t* num_rows, const int32_t* h_num_rows, const int32_t* perms,
+                        const int64_t* perm_off, int num_clients, int epochs, int batch_size, float lr,
+                        float prox_mu, const float* control, int64_t ld_control, float* delta_out, int64_t ld_delta,
+                        int32_t* nonfinite, int clients_per_wave, void* workspace, int64_t workspace_bytes,
+                        void* stream) {
+  FB_REQUIRE(dims != nullptr && h_num_rows != nullptr, "local_sgd_lm: null dims / host row counts");
+  const fb::lm::Dims m = fb::lm::parse(dims);
+  FB_UNSUPPORTED(fb::lm::dims_ok(m), "local_sgd_lm: unsupported shape (d <= 256, d %% heads == 0, head dim <= 32, seq <= 32)");
+  const int64_t D = fb::lm::num_params(m);
+  FB_REQUIRE(num_clients >= 0 && epochs >= 0 && batch_size >= 1 && clients_per_wave >= 1 && ld_delta >= D,
+             "local_sgd_lm: bad sizes");
+  FB_REQUIRE(workspace_bytes >= fb_lm_workspace_bytes(dims, batch_size, clients_per_wave, 1),
+             "local_sgd_lm: workspace too small");
+  cudaStream_t s = fb::as_stream(stream);
+  if (num_clients == 0) return FB_OK;
+  fb::lm::Buf b;
+  b.base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255));
+  fb::lm::Work k = fb::lm::carve(m, clients_per_wave, batch_size, true, b);
+  const int64_t sW = (D + 3) & ~int64_t(3);
+  const int B = batch_size, L = m.L;
+  FB_LAUNCH("lm_positions_kernel", s, (fb::lm::positions_kernel<<<(L * m.d + 255) / 256, 256, 0, s>>>(k.pe, L, m.d)));
+  for (int c0 = 0; c0 < num_clients; c0 += clients_per_wave) {
+    const int W = num_clients - c0 < clients_per_wave ? num_clients - c0 : clients_per_wave;
+    int max_steps = 0;
+    for (int c = c0; c < c0 + W; ++c) {
+      const int n = h_num_rows[c];
+      const int st = n > 0 ? epochs * ((n + B - 1) / B) : 0;
+      max_steps = st > max_steps ? st : max_steps;
+    }
+    float* Dl = delta_out + (int64_t)c0 * ld_delta;
+    FB_LAUNCH("lm_init_wave_kernel", s, (fb::lm::init_wave_kernel<<<dim3(256, W), 256, 0, s>>>(theta_t, D, k.Wc, sW,
+                                                                                                Dl, ld_delta)));
+    for (int step = 0; step < max_steps; ++step) {
+      FB_LAUNCH("lm_gather_batch_kernel", s, (fb::lm::gather_batch_kernel<<<W, 128, 0, s>>>(
+                                                 X, row_start, num_rows, perms, perm_off, c0, epochs, B, L, step,
+                                                 k.tok, k.nvalid)));
+      k.active = k.nvalid;  // (nonzero = the client has a minibatch this step)
+      int st = fb::lm::forward(m, k, k.Wc, sW, W, B, s);
+      if (st) return st;
+      st = fb::lm::backward(m, k, sW, W, B, s);
+      if (st) return st;
+      FB_LAUNCH("lm_sgd_kernel", s, (fb::lm::sgd_kernel<<<dim3(128, W), 256, 0, s>>>(
+                                        k.Wc, k.G, sW, Dl, ld_delta,
+                                        control ? control + (ld_control ? (int64_t)c0 * ld_control : 0) : nullptr,
+                                        ld_control, D, lr, prox_mu, k.nvalid)));
+    }
+    FB_LAUNCH("lm_nonfinite_kernel", s, (fb::lm::nonfinite_kernel<<<W, 256, 0, s>>>(Dl, ld_delta, D, nonfinite + c0)));
+  }
+  return fb::launch_status("local_sgd_lm");
+}
+
+}  // extern "C"

@@ -347,6 +347,10 @@ class DevicePopulation:
         self.total_rows = total
         self.max_label = int(y.max()) if total else 0
         self.min_label = int(y.min()) if total else 0
+        # (token-id datasets, the LM: every feature an integer id in [0, max_feature])
+        self.integral = bool(total == 0 or np.array_equal(X, np.floor(X)))
+        self.min_feature = float(X.min()) if total else 0.0
+        self.max_feature = float(X.max()) if total else 0.0
 
 
 class ControlStore:

@@ -25,13 +25,13 @@ from typing import Any, Mapping, Sequence
 
 import numpy as np
 
-from . import cnn, interop, native
+from . import cnn, interop, lm, native
 from .core import CentralContext, MetricKind, MetricValue, Population, merge_metrics, user_seed
 from .algorithms import CONTROL_PREFIX, MODEL_PREFIX
 from .device import Comm, ControlStore, ControlUpdates, DeviceParams, DevicePopulation, DeviceStatistics, Workspace
 from .errors import EngineError
 from .feddata import FederatedDataset, sample_cohort
-from .models import CNN, MLP, LogisticRegression
+from .models import CNN, MLP, LogisticRegression, TransformerLM
 from .privacy import CLIPPED_KEY, COUNT_KEY, NORM_KEY, validate_pipeline
 from .scheduling import compute_base_weight, schedule_users
 
@@ -222,6 +222,8 @@ class _ModelRunner:
             self.kind, self.dims = "mlp", (model.dim, model.hidden_units, model.num_classes)
         elif isinstance(model, LogisticRegression):
             self.kind, self.dims = "linear", (model.dim, model.num_classes)
+        elif isinstance(model, TransformerLM):
+            self.kind, self.dims = "lm", ()
         elif isinstance(model, CNN):
             if model != CNN():  # csrc/cnn.cu is compiled for exactly this geometry
                 raise ValueError(f"GpuSimulationEngine: the CNN kernels are compiled for {CNN()}, got {model}")
@@ -234,6 +236,8 @@ class _ModelRunner:
     def eval(self, theta, pop: DevicePopulation, row_start, num_rows, C, loss, correct, stream, h_num_rows):
         if self.kind == "cnn":
             return cnn.eval_cohort(self, theta, pop, row_start, num_rows, C, loss, correct, stream, h_num_rows)
+        if self.kind == "lm":
+            return lm.eval_cohort(self, theta, pop, row_start, num_rows, C, loss, correct, stream, h_num_rows)
         fn = f"fb_eval_{self.kind}_f32"
         native.call(fn, native.ptr(theta), *self.dims, native.ptr(pop.X), native.ptr(pop.y),
                     native.ptr(row_start), native.ptr(num_rows), C, native.ptr(loss), native.ptr(correct),
@@ -245,6 +249,9 @@ class _ModelRunner:
             return cnn.local_sgd_cohort(self, theta, pop, row_start, num_rows, perms, perm_off, C, tp,
                                         prox_mu, delta, nonfinite, stream, h_num_rows, control=control,
                                         defer_fc1=defer_fc1)
+        if self.kind == "lm":
+            return lm.local_sgd_cohort(self, theta, pop, row_start, num_rows, perms, perm_off, C, tp, prox_mu, delta,
+                                       nonfinite, stream, h_num_rows, control=control)
         fn = f"fb_local_sgd_{self.kind}_f32"
         native.call(fn, native.ptr(theta), *self.dims, native.ptr(pop.X), native.ptr(pop.y),
                     native.ptr(row_start), native.ptr(num_rows), native.ptr(perms), native.ptr(perm_off), C,
@@ -606,7 +613,11 @@ class GpuSimulationEngine:
         pop = self.population(pop_key)
         if pop.dim != plan.model.input_dim:
             raise ValueError(f"dataset dim {pop.dim} != model input dim {plan.model.input_dim}")
-        if pop.total_rows and (pop.min_label < 0 or pop.max_label >= plan.model.num_classes):
+        if runner.kind == "lm":  # sentences of token ids: the kernels index the embedding with them
+            if pop.total_rows and (not pop.integral or pop.min_feature < 0 or pop.max_feature >= plan.model.vocab):
+                raise ValueError(f"population {pop_key.value!r}: token ids must be integers in "
+                                 f"[0, {plan.model.vocab}), got [{pop.min_feature}, {pop.max_feature}]")
+        elif pop.total_rows and (pop.min_label < 0 or pop.max_label >= plan.model.num_classes):
             raise ValueError(f"labels of population {pop_key.value!r} lie in [{pop.min_label}, {pop.max_label}], "
                              f"outside the model's {plan.model.num_classes} classes")
         theta = self._theta(state)

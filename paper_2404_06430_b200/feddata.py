@@ -138,6 +138,47 @@ def make_synthetic_classification(
     return features, labels
 
 
+LM_PAD, LM_BOS, LM_EOS, LM_OOV = 0, 1, 2, 3
+
+
+def make_synthetic_sentences(
+    num_users: int,
+    *,
+    vocab: int = 10004,
+    seq: int = 20,
+    max_sentences: int = 64,
+    seed: int = 0,
+    population: Population = Population.TRAIN,
+    id_prefix: str = "u",
+) -> FederatedDataset:
+    """StackOverflow-shaped users for the config C language model (BASELINE
+    configs[2]; <= 64 sentences per user,
+    sequence length 20).  There is no dataset offline, so the shape is
+    synthesised: sentences per user max(1, round(lognormal(3, 1))) capped at
+    ``max_sentences`` (the ragged draw of fedsim/cli/bench.py:61-63); each
+    sentence is [BOS, w_1 .. w_k, EOS] padded with PAD to ``seq + 1`` ids,
+    k ~ U[1, seq - 1], words Zipf(1.2)-ranked over ids 4 .. vocab - 1 (OOV
+    beyond).  A datapoint is one sentence: features = the seq + 1 ids (as
+    float64, exact), label = its number of non-pad targets."""
+    if num_users < 0 or seq < 2 or vocab < 5 or max_sentences < 1:
+        raise ValueError("need num_users >= 0, seq >= 2, vocab >= 5, max_sentences >= 1")
+    rng = make_rng(seed)
+    sizes = np.clip(np.round(rng.lognormal(3.0, 1.0, size=num_users)), 1, max_sentences).astype(np.int64)
+    users = {}
+    for i, n in enumerate(sizes):
+        k = rng.integers(1, seq, size=n)                       # real words per sentence
+        ranks = rng.zipf(1.2, size=(n, seq - 1))
+        words = np.where(ranks <= vocab - 4, ranks + 3, LM_OOV)
+        X = np.full((n, seq + 1), LM_PAD, dtype=np.int64)
+        X[:, 0] = LM_BOS
+        for r in range(n):
+            X[r, 1:k[r] + 1] = words[r, :k[r]]
+            X[r, k[r] + 1] = LM_EOS
+        uid = f"{id_prefix}{i:05d}"
+        users[uid] = UserDataset(uid, X.astype(np.float64), (k + 1).astype(np.int64))
+    return FederatedDataset(users=users, population=population)
+
+
 def _users_from_chunks(features, labels, chunks, population, prefix) -> FederatedDataset:
     users = {}
     for i, idx in enumerate(chunks):

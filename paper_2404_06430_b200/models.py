@@ -15,6 +15,8 @@ lives in ``csrc/`` -- there is no host forward/backward (no CPU fallback).
   [out][in][kh][kw], fc weights [in][out] (the reference's ``X @ W``
   convention); inputs are CHW rows of 3*32*32.  Initialised like the
   reference MLP: U(+-1/sqrt(fan_in)) drawn in entry order.
+* ``TransformerLM``      -- config C's StackOverflow-shaped next-word model
+  (1,962,912 parameters), also absent from the reference; see its docstring.
 """
 
 from __future__ import annotations
@@ -163,6 +165,67 @@ class CNN(Model):
             + self.hidden_units * self.num_classes
         )
         return 2 * macs
+
+
+@dataclass(frozen=True)
+class TransformerLM(Model):
+    """Config C (BASELINE configs[2]): the StackOverflow-shaped next-word
+    transformer (/root/reference/PAPER.md:1052,1071-1085) -- vocabulary
+    10 004, d_model 96, 8 heads, feed-forward 1536, 3 post-norm causal
+    encoder layers, sequence length 20, tied input/output embedding without
+    output bias: 1 962 912 parameters.  ReLU feed-forward, LayerNorm eps
+    1e-5, sinusoidal positions added to the sqrt(d)-scaled embedding, no
+    dropout.  Weight layouts are PyTorch's ([out, in] row-major).  A
+    datapoint is one sentence of ``seq + 1`` token ids (0 = pad): inputs
+    ids[:seq], targets ids[1:]; pad targets are ignored, the batch loss is
+    the mean cross-entropy over the batch's non-pad targets.  The reference
+    has no LM; the arithmetic is defined (and pinned to float64 autograd) by
+    the oracle's TransformerLM.  Weights init N(0, 0.02^2) in entry order
+    from one generator, biases 0, LayerNorm gains 1."""
+
+    vocab: int = 10004
+    d_model: int = 96
+    heads: int = 8
+    ff: int = 1536
+    layers: int = 3
+    seq: int = 20
+    kind = "lm"
+
+    @property
+    def input_dim(self) -> int:
+        return self.seq + 1
+
+    @property
+    def param_dims(self) -> dict[str, int]:
+        d, f = self.d_model, self.ff
+        out = {"embedding": self.vocab * d}
+        for l in range(self.layers):
+            out.update({f"layer{l}/in_proj_weight": 3 * d * d, f"layer{l}/in_proj_bias": 3 * d,
+                        f"layer{l}/out_proj_weight": d * d, f"layer{l}/out_proj_bias": d,
+                        f"layer{l}/linear1_weight": f * d, f"layer{l}/linear1_bias": f,
+                        f"layer{l}/linear2_weight": d * f, f"layer{l}/linear2_bias": d,
+                        f"layer{l}/norm1_weight": d, f"layer{l}/norm1_bias": d,
+                        f"layer{l}/norm2_weight": d, f"layer{l}/norm2_bias": d})
+        return out
+
+    def init_params(self, seed: int) -> dict[str, np.ndarray]:
+        rng = make_rng(seed)
+        out = {}
+        for name, n in self.param_dims.items():
+            if name.endswith("_bias"):
+                out[name] = np.zeros(n)
+            elif "norm" in name:
+                out[name] = np.ones(n)
+            else:
+                out[name] = rng.normal(0.0, 0.02, n)
+        return out
+
+    def forward_flops_per_token(self) -> int:
+        """2 x MACs of one token's forward pass: projections, attention over the
+        causal prefix (mean length (seq + 1) / 2) and the tied output layer."""
+        d, f, L = self.d_model, self.ff, self.seq
+        per_layer = 3 * d * d + d * d + 2 * d * f + d * (L + 1)  # (QK^T + PV: 2 * d * (L + 1) / 2)
+        return 2 * (self.layers * per_layer + self.vocab * d)
 
 
 def count_local_steps(num_points: int, local_params) -> int:

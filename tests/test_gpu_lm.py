@@ -1,0 +1,177 @@
+"""Config C (StackOverflow-shaped transformer LM): the sm_100a local-SGD and
+eval entry points (csrc/lm.cu, through the C ABI) against the float64 oracle
+(oracle/port.py TransformerLM, itself pinned to float64 autograd in
+tests/test_oracle_lm.py), at a tiny shape and at the full config C shape, and
+one end-to-end FedAvg + clip + Gaussian-DP central iteration through
+GpuSimulationEngine with central Adam.
+
+Tolerance: fp32 against float64 over a 1.96 M-parameter network whose
+forward has ReLU kinks; per-client update relative L2 error <= 1e-5 and
+elementwise rtol 1e-5 with atol 1e-6 * max|ref| on the aggregate, eval loss
+rtol 1e-5, correct counts exact (+-1 allowed only at the full shape, where a
+near-tie argmax over 10 004 logits can flip)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_2404_06430_b200 as fb
+from oracle import port
+from paper_2404_06430_b200 import lm as lm_glue
+from paper_2404_06430_b200 import native
+from tests.conftest import assert_close_fp32
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+TINY = dict(vocab=37, d=16, heads=4, ff=32, layers=2, seq=8)
+
+
+def product_model(shape):
+    return fb.TransformerLM(vocab=shape.get("vocab", 10004), d_model=shape.get("d", 96), heads=shape.get("heads", 8),
+                            ff=shape.get("ff", 1536), layers=shape.get("layers", 3), seq=shape.get("seq", 20))
+
+
+def cohort(shape, n_users, seed, max_sentences=40):
+    m = port.TransformerLM(**shape)
+    ds = fb.make_synthetic_sentences(n_users, vocab=m.vocab, seq=m.seq, max_sentences=max_sentences, seed=seed)
+    return m, list(ds.users.values())
+
+
+def pack(users):
+    X = np.concatenate([u.features for u in users]).astype(np.float32)
+    n = np.array([u.num_points for u in users], dtype=np.int32)
+    start = np.concatenate([[0], np.cumsum(n)[:-1]]).astype(np.int64)
+    return X, n, start
+
+
+def run_local_sgd(model, theta, users, ctx_seed, E, B, lr, mu=0.0, wave=None):
+    X, n, start = pack(users)
+    perms = [port.user_perms(ctx_seed, u.user_id, u.num_points, E).astype(np.int32).ravel() for u in users]
+    off = np.concatenate([[0], np.cumsum([len(p) for p in perms])[:-1]]).astype(np.int64)
+    C, D = len(users), model.num_params
+    ld = (D + 3) & ~3
+    dims = lm_glue.dims_of(model)
+    W = wave or C
+    ws = torch.empty(native.call("fb_lm_workspace_bytes", dims.ctypes.data, B, W, 1), dtype=torch.uint8,
+                     device="cuda")
+    delta = torch.zeros(C, ld, device="cuda")
+    bad = torch.zeros(C, dtype=torch.int32, device="cuda")
+    d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    th, Xd, sd, nd, pd, od = d(theta.astype(np.float32)), d(X), d(start), d(n), d(np.concatenate(perms)), d(off)
+    native.call("fb_local_sgd_lm_f32", th.data_ptr(), dims.ctypes.data, Xd.data_ptr(), sd.data_ptr(), nd.data_ptr(),
+                n.ctypes.data, pd.data_ptr(), od.data_ptr(), C, E, B, lr, mu, None, 0, delta.data_ptr(), ld,
+                bad.data_ptr(), W, ws.data_ptr(), ws.numel(), native.stream_handle())
+    torch.cuda.synchronize()
+    return delta[:, :D].double().cpu().numpy(), bad.cpu().numpy()
+
+
+def run_eval(model, theta, users, groups=4, B=16):
+    X, n, start = pack(users)
+    C = len(users)
+    dims = lm_glue.dims_of(model)
+    ws = torch.empty(native.call("fb_lm_workspace_bytes", dims.ctypes.data, B, 1, groups), dtype=torch.uint8,
+                     device="cuda")
+    loss = torch.zeros(C, dtype=torch.float64, device="cuda")
+    corr = torch.zeros(C, dtype=torch.int32, device="cuda")
+    d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    th, Xd, sd, nd = d(theta.astype(np.float32)), d(X), d(start), d(n)
+    native.call("fb_eval_lm_f32", th.data_ptr(), dims.ctypes.data, Xd.data_ptr(), sd.data_ptr(), nd.data_ptr(),
+                n.ctypes.data, C, loss.data_ptr(), corr.data_ptr(), B, groups, ws.data_ptr(), ws.numel(),
+                native.stream_handle())
+    torch.cuda.synchronize()
+    return loss.cpu().numpy(), corr.cpu().numpy()
+
+
+def oracle_deltas(m, p0, users, ctx_seed, E, B, lr, mu=0.0):
+    out = []
+    for u in users:
+        after = port.fit_local(m, p0, u.features, u.labels, port.user_perms(ctx_seed, u.user_id, u.num_points, E),
+                               lr, B, mu=mu)
+        out.append(port.flat(p0, m.dims) - port.flat(after, m.dims))
+    return np.array(out)
+
+
+def rel_err(a, b):
+    return np.linalg.norm(a - b, axis=-1) / np.maximum(np.linalg.norm(b, axis=-1), 1e-30)
+
+
+@pytest.mark.parametrize("E,B,lr,mu", [(1, 16, 0.3, 0.0), (2, 5, 0.1, 0.0), (1, 4, 0.2, 0.05)])
+def test_lm_local_sgd_tiny_matches_oracle(E, B, lr, mu):
+    """Ragged clients (1 .. 40 sentences), tail batches, two epochs, FedProx term;
+    clients trained in waves of 3 to cover the wave loop."""
+    m, users = cohort(TINY, 7, seed=11)
+    model = product_model(TINY)
+    p0 = m.init(3)
+    theta = port.flat(p0, m.dims)
+    got, bad = run_local_sgd(model, theta, users, 99, E, B, lr, mu, wave=3)
+    want = oracle_deltas(m, p0, users, 99, E, B, lr, mu)
+    assert not bad.any()
+    assert rel_err(got, want).max() <= 1e-5, rel_err(got, want)
+    for c in range(len(users)):
+        assert_close_fp32(got[c], want[c], what=f"client {c}")
+
+
+def test_lm_eval_tiny_matches_oracle():
+    m, users = cohort(TINY, 9, seed=5)
+    p0 = m.init(2)
+    loss, corr = run_eval(product_model(TINY), port.flat(p0, m.dims), users, groups=3, B=4)
+    for c, u in enumerate(users):
+        ls, k = m.eval_counts(p0, u.features)
+        assert loss[c] == pytest.approx(ls, rel=1e-5)
+        assert corr[c] == k
+
+
+def test_lm_configC_local_sgd_and_eval_match_oracle():
+    """The full 1.96 M-parameter shape, 4 ragged clients, one epoch at B = 16."""
+    m, users = cohort({}, 4, seed=21, max_sentences=24)
+    model = product_model({})
+    p0 = m.init(7)
+    theta = port.flat(p0, m.dims)
+    got, bad = run_local_sgd(model, theta, users, 5, 1, 16, 0.3)
+    want = oracle_deltas(m, p0, users, 5, 1, 16, 0.3)
+    assert not bad.any()
+    err = rel_err(got, want)
+    assert err.max() <= 1e-5, err
+    loss, corr = run_eval(model, theta, users, groups=2)
+    for c, u in enumerate(users):
+        ls, k = m.eval_counts(p0, u.features)
+        assert loss[c] == pytest.approx(ls, rel=1e-5)
+        assert abs(int(corr[c]) - k) <= 1
+
+
+def test_lm_deterministic_rerun():
+    m, users = cohort(TINY, 5, seed=3)
+    theta = port.flat(m.init(1), m.dims)
+    a, _ = run_local_sgd(product_model(TINY), theta, users, 7, 1, 6, 0.3)
+    b, _ = run_local_sgd(product_model(TINY), theta, users, 7, 1, 6, 0.3)
+    np.testing.assert_array_equal(a, b)
+
+
+def test_lm_engine_central_iteration_with_adam_matches_oracle():
+    """FedAvg + ClippingPostprocessor + GaussianCentralMechanism (reference noise
+    injected) + central Adam, one iteration through GpuSimulationEngine."""
+    shape = dict(vocab=211, d=32, heads=4, ff=64, layers=2, seq=12)
+    m = port.TransformerLM(**shape)
+    model = product_model(shape)
+    train = fb.make_synthetic_sentences(12, vocab=m.vocab, seq=m.seq, max_sentences=30, seed=8, id_prefix="train")
+    clip = fb.ClippingPostprocessor(0.5)
+    mech = fb.GaussianCentralMechanism(clip, sigma=1.0, r=0.1, noise_base_seed=7, noise_source="numpy")
+    alg = fb.FedAvg(model, fb.AdamOptimizer(0.1, beta1=0.9, beta2=0.99, adaptivity_degree=0.1), total_iterations=1,
+                    cohort_size=6, local_learning_rate=0.3, local_num_epochs=1, local_batch_size=16,
+                    eval_frequency=10, eval_cohort_size=1, weighting="datapoints", run_seed=3, init_seed=4)
+    eng = fb.GpuSimulationEngine({fb.Population.TRAIN: train, fb.Population.VAL: train}, postprocessors=[clip, mech])
+    state = alg.initial_state()
+    ctxs = alg.get_next_central_contexts(state, 0)[:1]
+    res = eng.run_iteration(alg, state, ctxs)
+    state = alg.process_aggregated_statistics_all_contexts(state, ctxs, res.aggregates, res.metrics, [])
+    got = state.params.flat_host()
+    users = {u.user_id: (u.features, u.labels) for u in train.users.values()}
+    theta0 = m.init(4)
+    ref = port.run_context(m, theta0, users, 6, ctxs[0].seed, train=(0.3, 1, 16), weighting="datapoints", bound=0.5,
+                           sigma=1.0, r=0.1, noise_base=7, t=0, pop="train")
+    want = port.central_adam(port.flat(theta0, m.dims), ref.aggregate, ref.weight, 0.1, {}, noise=ref.noise,
+                             beta1=0.9, beta2=0.99, eps=0.1)
+    assert_close_fp32(got, want, what="theta after one LM central iteration")
