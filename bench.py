@@ -60,7 +60,17 @@ WORKLOADS = {
                        eval_cohort=100, epochs=1, batch=10, lr=0.1, clr=1.0, bound=1.0, sigma=SIGMA_T1500,
                        noise_cohort=1000, eval_every=10,
                        name="cifar10-cnn fedavg+gaussian-dp cohort200, ragged users 1-500 (FLAIR-shaped sizes)"),
+    # BASELINE configs[2] / SURVEY.md 8(f) row 3: StackOverflow-shaped next-word transformer
+    # (/root/reference/PAPER.md:1052,1071-1085): cohort 400, 1 epoch, B=16, local lr 0.3,
+    # central Adam (lr 0.1, betas 0.9/0.99, adaptivity 0.1), clip 1.0, noise cohort 5000,
+    # evaluation every 20; <= 64 sentences of 20 tokens per user (synthetic, ragged)
+    "lm": dict(model="lm", users=4000, val_users=200, ppu=None, sentences=True, cohort=400, eval_cohort=100,
+               epochs=1, batch=16, lr=0.3, clr=0.1, adam=(0.9, 0.99, 0.1), bound=1.0, sigma=1.0, noise_cohort=5000,
+               eval_every=20, name="stackoverflow-transformer-lm fedavg+gaussian-dp+adam cohort400 (BASELINE configs[2])"),
 }
+
+# FP32 FFMA peak: 148 SMs x 128 lanes x 2 x 1.965 GHz
+FP32_FFMA_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
 
 # algorithmic FLOPs per processed sample for the CNN kernels (2 x MACs of the
 # dense operation the kernel implements)
@@ -105,6 +115,11 @@ def build_ragged(wl: dict):
 def build(wl: dict):
     import paper_2404_06430_b200 as fb
 
+    if wl.get("sentences"):
+        return {fb.Population.TRAIN: fb.make_synthetic_sentences(wl["users"], seed=fb.derive_seed(0, "train", "lm"),
+                                                                 population=fb.Population.TRAIN, id_prefix="train"),
+                fb.Population.VAL: fb.make_synthetic_sentences(wl["val_users"], seed=fb.derive_seed(0, "val", "lm"),
+                                                               population=fb.Population.VAL, id_prefix="val")}
     if wl.get("ragged"):
         return build_ragged(wl)
     ppu = wl["ppu"]
@@ -124,6 +139,8 @@ def make_model(wl):
 
     if wl["model"] == "cnn":
         return fb.CNN()
+    if wl["model"] == "lm":
+        return fb.TransformerLM()
     if wl["model"] == "mlp":
         return fb.MLP(wl["dim"], wl["hidden"], 10)
     return fb.LogisticRegression(wl["dim"], 10)
@@ -132,7 +149,9 @@ def make_model(wl):
 def make_algorithm(wl, iterations):
     import paper_2404_06430_b200 as fb
 
-    alg = fb.FedAvg(make_model(wl), fb.SGDOptimizer(wl["clr"]), total_iterations=iterations,
+    opt = (fb.AdamOptimizer(wl["clr"], beta1=wl["adam"][0], beta2=wl["adam"][1], adaptivity_degree=wl["adam"][2])
+           if wl.get("adam") else fb.SGDOptimizer(wl["clr"]))
+    alg = fb.FedAvg(make_model(wl), opt, total_iterations=iterations,
                     cohort_size=wl["cohort"], local_learning_rate=wl["lr"], local_num_epochs=wl["epochs"],
                     local_batch_size=wl["batch"], eval_frequency=wl["eval_every"],
                     eval_cohort_size=wl["eval_cohort"], weighting="uniform", run_seed=0, init_seed=0)
@@ -255,6 +274,22 @@ def kernel_work(wl: dict, counts: dict) -> dict:
     }
 
 
+def lm_kernel_work(counts: dict) -> dict:
+    """Config C: every grouped GEMM flavour does the same dense work per processed
+    token row -- 2 x (3d^2 + d^2 + 2 d F) x layers + 2 V d FLOPs (3.91 MFLOP at the
+    config C shape): forward Y = X W^T (NT), backward dX = dY W (NN), dW = dY^T X (TN).
+    Rows = slot rows processed (B x seq per active client step, eval chunks of
+    256 x 16 sentences), padding included."""
+    import paper_2404_06430_b200 as fb
+
+    m = fb.TransformerLM()
+    per_row = 2 * ((3 * m.d_model**2 + m.d_model**2 + 2 * m.d_model * m.ff) * m.layers + m.vocab * m.d_model)
+    note = "FP32 FFMA (SIMT tiled GEMM)"
+    return {"lm_gemm_nt_kernel": ("fp32", per_row * counts["fwd_rows"], note),
+            "lm_gemm_nn_kernel": ("fp32", per_row * counts["train_rows"], note),
+            "lm_gemm_tn_kernel": ("fp32", per_row * counts["train_rows"], note)}
+
+
 def _ncu_kernel(name: str) -> dict | None:
     try:
         return json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())["kernels"][name]
@@ -291,14 +326,20 @@ def roofline(report: dict, wl: dict, counts: dict, peaks: dict) -> tuple[dict, d
     same figure for every kernel with a defined algorithmic work."""
     if not report:
         return {}, {}
-    work = kernel_work(wl, counts) if wl["model"] == "cnn" else {}
+    work = (kernel_work(wl, counts) if wl["model"] == "cnn" else
+            lm_kernel_work(counts) if wl["model"] == "lm" else {})
     total = sum(v[0] for v in report.values())
     per = {}
     for name, (ms, launches) in report.items():
         if name not in work:
             continue
         bound, amount, note = work[name]
-        if bound == "tensor":
+        if bound == "fp32":
+            ach = amount / (ms * 1e-3) / 1e12
+            per[name] = {"bound": "tensor", "achieved": round(ach, 2), "unit": "TFLOP/s",
+                         "frac": round(ach / FP32_FFMA_TFLOPS, 4), "ms": round(ms, 2), "share": round(ms / total, 4),
+                         "math": note, "peak": round(FP32_FFMA_TFLOPS, 1)}
+        elif bound == "tensor":
             ach = amount / (ms * 1e-3) / 1e12
             peak = peaks.get("bf16_tflops", 1590.0)
             per[name] = {"bound": "tensor", "achieved": round(ach, 2), "unit": "TFLOP/s", "frac": round(ach / peak, 4),
@@ -311,7 +352,13 @@ def roofline(report: dict, wl: dict, counts: dict, peaks: dict) -> tuple[dict, d
                          "ms": round(ms, 2), "share": round(ms / total, 4)}
     name, (ms, launches) = max(report.items(), key=lambda kv: kv[1][0])
     out = {"kernel": name, "share_of_gpu_time": ms / total if total else None}
-    if name in per:
+    if name in per and "peak" in per[name]:  # FP32 SIMT kernels: against the FFMA peak
+        k = per[name]
+        out.update(bound="tensor", achieved=k["achieved"], peak=k["peak"], unit="TFLOP/s", frac=k["frac"],
+                   traffic=None, peak_source="FP32 FFMA peak 148 SMs x 128 lanes x 2 x 1.965 GHz (SURVEY.md 8(d)); "
+                   "the kernel is a SIMT FP32 tiled GEMM, not tcgen05",
+                   algorithmic=f"{work[name][1]:.4g} FLOP over {launches} launches")
+    elif name in per:
         k = per[name]
         peak = peaks.get("bf16_tflops", 1590.0) if k["bound"] == "tensor" else peaks.get("hbm_gbs", 6650.0)
         out.update(bound=k["bound"], achieved=k["achieved"], peak=peak, unit=k["unit"], frac=k["frac"],
@@ -386,6 +433,17 @@ def gpu_arm(args, wl):
         dense_D -= cnn_mod.FC1_HI - cnn_mod.FC1_LO
     counts = {"train": train_samples, "fwd": fwd_samples, "client_steps": per_rank * steps * KP,
               "clients": per_rank * KP, "D": (D + 3) & ~3, "D_dense": dense_D, "iters": KP}
+    if wl["model"] == "lm":  # slot rows the GEMMs process (B x seq per client step; eval chunks padded)
+        from paper_2404_06430_b200 import lm as lm_mod
+        seq, B = 20, wl["batch"]
+        sizes = np.array([u.num_points for u in ds[fb.Population.TRAIN].users.values()], dtype=np.float64)
+        mean_steps = float(np.mean(wl["epochs"] * np.ceil(sizes / B)))
+        chunk = lm_mod.EVAL_GROUPS * B
+        ev_rows = lambda nsent: np.ceil(nsent / chunk) * chunk * seq
+        counts["train_rows"] = per_rank * mean_steps * B * seq * KP
+        counts["fwd_rows"] = (counts["train_rows"] + ev_rows(per_rank * float(sizes.mean())) * KP
+                              + val_iters * ev_rows((wl["eval_cohort"] / world) * float(sizes.mean())))
+        steps = mean_steps
 
     # end-to-end: dataset in pinned host memory, cohort rows moved every iteration
     e2e = None
@@ -416,7 +474,9 @@ def gpu_arm(args, wl):
             "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": wl["name"], "model": wl["model"], "cohort": C, "users": wl["users"],
-                       "points_per_user": wl["ppu"] or f"ragged lognormal(3,1) in [1,500], mean {ppu:.1f}",
+                       "points_per_user": wl["ppu"] or (f"ragged lognormal(3,1) in [1,64] sentences of 20 tokens, "
+                                                        f"mean {ppu:.1f}" if wl["model"] == "lm" else
+                                                        f"ragged lognormal(3,1) in [1,500], mean {ppu:.1f}"),
                        "local_epochs": wl["epochs"], "batch": wl["batch"],
                        "local_steps_per_client": steps, "sigma": wl["sigma"], "clip_bound": wl["bound"],
                        "eval_every": wl["eval_every"], "parallelism": f"cohort-dp{world}",
@@ -455,7 +515,8 @@ def cpu_iteration_seconds(wl, ds, n_clients: int, t: int = 0) -> tuple[float, st
     import paper_2404_06430_b200 as fb
     from oracle import port
 
-    model = {"cnn": lambda: port.Cnn(), "mlp": lambda: port.Mlp(wl["dim"], wl["hidden"], 10),
+    model = {"cnn": lambda: port.Cnn(), "lm": lambda: port.TransformerLM(),
+             "mlp": lambda: port.Mlp(wl["dim"], wl["hidden"], 10),
              "logistic": lambda: port.Linear(wl["dim"], 10)}[wl["model"]]()
     theta = model.init(0)
     train = ds[fb.Population.TRAIN]
