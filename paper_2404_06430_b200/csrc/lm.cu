@@ -185,6 +185,128 @@ __global__ void __launch_bounds__(GT) gemm_kernel(const Gemm g) {
   }
 }
 
+// 128 x 128 tiles, 8 x 8 outputs per thread (two 4 x 4 blocks 64 apart in each
+// dimension), BK = 8, double-buffered shared memory: 4 LDS.128 feed 64 FFMA, so the
+// FMA pipe, not shared-memory bandwidth, bounds it (the 64 x 64 / 4 x 4 kernel above
+// spends 2 LDS.128 per 16 FFMA).  kVec: 128-bit global loads along the contiguous
+// dimension (every row 16-byte aligned, extent % 4 == 0); else scalar.
+constexpr int BM2 = 128, BN2 = 128, BK2 = 8;
+
+template <bool TA, bool TB, bool kVec>
+__global__ void __launch_bounds__(GT) gemm_big_kernel(const Gemm g) {
+  const int z = blockIdx.z;
+  if (g.active && !g.active[z]) return;
+  __shared__ __align__(16) float As[2][BK2][BM2];
+  __shared__ __align__(16) float Bs[2][BK2][BN2];
+  const float* A = g.A + (int64_t)z * g.sA;
+  const float* B = g.B + (int64_t)z * g.sB;
+  const int m0 = blockIdx.y * BM2, n0 = blockIdx.x * BN2;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  float4 ra, rb;
+  // each thread moves 4 consecutive elements along the contiguous dimension of A and of B
+  auto fetch4 = [&](const float* base, int64_t ld, bool trans, int rows, int kdim, int r0, int k0, bool relu) {
+    // trans: element (r, k) at base[k * ld + r] (r contiguous); else base[r * ld + k] (k contiguous)
+    int r, k;
+    if (trans) { k = tid >> 5; r = (tid & 31) * 4; } else { r = tid >> 1; k = (tid & 1) * 4; }
+    const int gr = r0 + r, gk = k0 + k;
+    float v[4];
+    if (kVec) {
+      if (trans) {
+        if (gk < kdim && gr < rows) {
+          const float4 x = *reinterpret_cast<const float4*>(base + (int64_t)gk * ld + gr);
+          v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+        } else {
+          v[0] = v[1] = v[2] = v[3] = 0.f;
+        }
+      } else {
+        if (gr < rows && gk < kdim) {
+          const float4 x = *reinterpret_cast<const float4*>(base + (int64_t)gr * ld + gk);
+          v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+        } else {
+          v[0] = v[1] = v[2] = v[3] = 0.f;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int rr = trans ? gr + q : gr, kk = trans ? gk : gk + q;
+        v[q] = (rr < rows && kk < kdim) ? (trans ? base[(int64_t)kk * ld + rr] : base[(int64_t)rr * ld + kk]) : 0.f;
+      }
+    }
+    if (relu) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[q] = fmaxf(v[q], 0.f);
+    }
+    return make_float4(v[0], v[1], v[2], v[3]);
+  };
+  auto store = [&](int buf) {
+    // A: As[k][m]; B: Bs[k][n]
+    if (TA) {
+      *reinterpret_cast<float4*>(&As[buf][tid >> 5][(tid & 31) * 4]) = ra;
+    } else {
+      const int r = tid >> 1, k = (tid & 1) * 4;
+      As[buf][k + 0][r] = ra.x; As[buf][k + 1][r] = ra.y; As[buf][k + 2][r] = ra.z; As[buf][k + 3][r] = ra.w;
+    }
+    if (!TB) {
+      *reinterpret_cast<float4*>(&Bs[buf][tid >> 5][(tid & 31) * 4]) = rb;
+    } else {
+      const int r = tid >> 1, k = (tid & 1) * 4;
+      Bs[buf][k + 0][r] = rb.x; Bs[buf][k + 1][r] = rb.y; Bs[buf][k + 2][r] = rb.z; Bs[buf][k + 3][r] = rb.w;
+    }
+  };
+  auto fetch = [&](int k0) {
+    ra = fetch4(A, g.lda, TA, g.M, g.K, m0, k0, g.relu_a);
+    rb = fetch4(B, g.ldb, !TB, g.N, g.K, n0, k0, g.relu_b);
+  };
+  float acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+  const int nk = (g.K + BK2 - 1) / BK2;
+  fetch(0);
+  store(0);
+  __syncthreads();
+  for (int t = 0; t < nk; ++t) {
+    const int cur = t & 1;
+    if (t + 1 < nk) fetch((t + 1) * BK2);
+#pragma unroll
+    for (int kk = 0; kk < BK2; ++kk) {
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[cur][kk][ty * 4]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[cur][kk][64 + ty * 4]);
+      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[cur][kk][tx * 4]);
+      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[cur][kk][64 + tx * 4]);
+      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    if (t + 1 < nk) store(cur ^ 1);
+    __syncthreads();
+  }
+  float* C = g.C + (int64_t)z * g.sC;
+  const float* bias = g.bias ? g.bias + (int64_t)z * g.sBias : nullptr;
+  const float* aux = g.aux ? g.aux + (int64_t)z * g.sAux : nullptr;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int m = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
+    if (m >= g.M) continue;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int n = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
+      if (n >= g.N) continue;
+      float v = g.alpha * acc[i][j];
+      float* c = C + (int64_t)m * g.ldc + n;
+      if (g.beta != 0.f) v = fmaf(g.beta, *c, v);
+      if (bias) v += bias[n];
+      if (aux && !(aux[(int64_t)m * g.ldaux + n] > 0.f)) v = 0.f;
+      *c = v;
+    }
+  }
+}
+
 // ------------------------------------------------------------ batch gather
 // Client c's step-s minibatch: epoch e = s / nb, batch j = s % nb (nb = ceil(n / B)),
 // sentences perms[c][e * n + j * B + i]; slots past the batch are all-pad.
@@ -717,13 +839,34 @@ inline Work carve(const Dims& m, int W, int B, bool train, Buf& b) {
   return k;
 }
 
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
 int launch_gemm(bool TA, bool TB, const Gemm& g, int batch, cudaStream_t s) {
   if (batch <= 0 || g.M <= 0 || g.N <= 0) return FB_OK;
-  const dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM, batch);
-  if (!TA && TB) FB_LAUNCH("lm_gemm_nt_kernel", s, (gemm_kernel<false, true><<<grid, GT, 0, s>>>(g)));
-  else if (!TA && !TB) FB_LAUNCH("lm_gemm_nn_kernel", s, (gemm_kernel<false, false><<<grid, GT, 0, s>>>(g)));
-  else FB_LAUNCH("lm_gemm_tn_kernel", s, (gemm_kernel<true, false><<<grid, GT, 0, s>>>(g)));
-  return launch_status("lm_gemm_kernel");
+  // 128 x 128 tiles once both output sides fill at least ~3/4 of a tile
+  const bool big = g.M >= 96 && g.N >= 96;
+  if (!big) {
+    const dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM, batch);
+    if (!TA && TB) FB_LAUNCH("lm_gemm_nt_kernel", s, (gemm_kernel<false, true><<<grid, GT, 0, s>>>(g)));
+    else if (!TA && !TB) FB_LAUNCH("lm_gemm_nn_kernel", s, (gemm_kernel<false, false><<<grid, GT, 0, s>>>(g)));
+    else FB_LAUNCH("lm_gemm_tn_kernel", s, (gemm_kernel<true, false><<<grid, GT, 0, s>>>(g)));
+    return launch_status("lm_gemm_kernel");
+  }
+  // contiguous extents: A along K (NT/NN) or M (TN); B along K (NT) or N (NN/TN)
+  const int ea = TA ? g.M : g.K, eb = TB ? g.K : g.N;
+  const bool vec = aligned16(g.A) && aligned16(g.B) && g.lda % 4 == 0 && g.ldb % 4 == 0 && g.sA % 4 == 0 &&
+                   g.sB % 4 == 0 && ea % 4 == 0 && eb % 4 == 0;
+  const dim3 grid((g.N + BN2 - 1) / BN2, (g.M + BM2 - 1) / BM2, batch);
+#define FB_LM_BIG(TA_, TB_, NAME)                                                                   \
+  do {                                                                                              \
+    if (vec) FB_LAUNCH(NAME, s, (gemm_big_kernel<TA_, TB_, true><<<grid, GT, 0, s>>>(g)));           \
+    else FB_LAUNCH(NAME, s, (gemm_big_kernel<TA_, TB_, false><<<grid, GT, 0, s>>>(g)));              \
+  } while (0)
+  if (!TA && TB) FB_LM_BIG(false, true, "lm_gemm_nt_kernel");
+  else if (!TA && !TB) FB_LM_BIG(false, false, "lm_gemm_nn_kernel");
+  else FB_LM_BIG(true, false, "lm_gemm_tn_kernel");
+#undef FB_LM_BIG
+  return launch_status("lm_gemm_big_kernel");
 }
 
 Gemm gemm_base() {
