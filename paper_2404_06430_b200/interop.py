@@ -13,8 +13,8 @@ product never imports fedsim -- and maps each onto what the GPU path runs:
   algorithm's public attributes (``model``, ``weighting``) and the context
   (``local_params``, ``algo_params["mu"]``, ``eval_params``);
 * models: a layout whose ``param_dims`` equal one of the compiled models'
-  (LogisticRegression / MLP of fedsim/models/models.py:85-228, or the
-  BASELINE CNN);
+  (LogisticRegression / MLP of fedsim/models/models.py:85-228, the BASELINE
+  CNN, or config C's TransformerLM);
 * postprocessors: a clipping stage (``is_clipping``, fedsim/privacy/
   clipping.py:75-103) whose per-user half runs as the fused K2 kernel from
   ``current_bound``, and ``GaussianCentralMechanism`` (fedsim/privacy/
@@ -78,7 +78,7 @@ def check_aggregator(aggregator) -> None:
 def native_model(model):
     """This package's compiled model with the same parameter layout as ``model``
     (entry names, order and sizes), or ValueError."""
-    from .models import CNN, MLP, LogisticRegression, Model
+    from .models import CNN, MLP, LogisticRegression, Model, TransformerLM
 
     if isinstance(model, Model):
         return model
@@ -91,6 +91,11 @@ def native_model(model):
         else:
             candidates.append(LogisticRegression(int(model.dim), int(model.num_classes)))
     candidates.append(CNN())
+    if hasattr(model, "vocab") and hasattr(model, "heads"):  # a config C transformer LM layout
+        d = int(getattr(model, "d_model", getattr(model, "d", 96)))
+        candidates.append(TransformerLM(int(model.vocab), d, int(model.heads), int(getattr(model, "ff", 1536)),
+                                        int(getattr(model, "layers", 3)), int(getattr(model, "seq", 20))))
+    candidates.append(TransformerLM())
     for cand in candidates:
         if list(cand.param_dims.items()) == [(n, int(k)) for n, k in dims.items()]:
             return cand

@@ -23,6 +23,17 @@ def test_reference_models_map_to_compiled_layouts():
     assert interop.native_model(alg.model) == fb.CNN()
 
 
+def test_lm_layouts_map_to_transformer():
+    """A fedsim Model wrapping the config C oracle LM (any vocab / width) maps onto
+    the compiled TransformerLM of the same layout."""
+    from oracle import port
+
+    for shape in (dict(), dict(vocab=37, d=16, heads=4, ff=32, layers=2, seq=8)):
+        m = port.TransformerLM(**shape)
+        got = interop.native_model(m)
+        assert isinstance(got, fb.TransformerLM) and got.param_dims == m.dims
+
+
 @pytest.mark.parametrize("name,mu,scaffold", [("logistic_dp", 0.0, False), ("logistic_fedprox", 0.3, False),
                                               ("mlp_adafedprox", 0.1, False), ("mlp_scaffold_dp", 0.0, True)])
 def test_reference_algorithms_become_cohort_plans(name, mu, scaffold):
