@@ -866,7 +866,7 @@ def main(argv=None):
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS) + ["aggmicro"], default="cnn")
     ap.add_argument("--micro-dim", type=int, default=10_000_000)
-    ap.add_argument("--micro-pool", type=int, default=256)
+    ap.add_argument("--micro-pool", type=int, default=64)
     ap.add_argument("--micro-impl", choices=["fused", "twopass"], default="fused")
     ap.add_argument("--cohort", type=int, default=None)
     ap.add_argument("--e2e-steps", type=int, default=10)
