@@ -57,6 +57,7 @@ SIGNATURES: dict[str, tuple] = {
          _i64, _p, _i32, _p],
     ),
     "fb_cnn_fc1_aggregate_f32": (_i32, [_p, _i32, _i32, _i32, _f32, _f32, _i32, _i32, _p, _i64, _p, _p]),
+    "fb_lm_set_gemm_impl": (_i32, [_i32]),
     "fb_lm_num_params": (_i64, [_p]),
     "fb_lm_workspace_bytes": (_i64, [_p, _i32, _i32, _i32]),
     "fb_eval_lm_f32": (_i32, [_p, _p, _p, _p, _p, _p, _i32, _p, _p, _i32, _i32, _p, _i64, _p]),
