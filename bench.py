@@ -794,18 +794,23 @@ def aggregation_microbench(args):
     s = native.stream_handle()
 
     fused = args.micro_impl == "fused"
-    if fused:
-        fws = torch.empty(max(native.call("fb_clip_aggregate_workspace_bytes", P, D), 16), dtype=torch.uint8,
+    if fused:  # all C clients in ONE launch, client c reading pool row c % P
+        fws = torch.empty(max(native.call("fb_clip_aggregate_workspace_bytes", C, D), 16), dtype=torch.uint8,
                           device="cuda")
+        rows = torch.arange(C, device="cuda", dtype=torch.int32) % P
+        wC = torch.ones(C, device="cuda")
+        normC = torch.empty(C, dtype=torch.float64, device="cuda")
+        coefC = torch.empty(C, device="cuda")
+        clipC = torch.empty(C, dtype=torch.int32, device="cuda")
+        badC = torch.empty(C, dtype=torch.int32, device="cuda")
 
     def step():
-        for c0 in range(0, C, P):
+        if fused:  # K2 + K3 in one HBM pass (clip_aggregate_fused.cu)
+            native.call("fb_clip_aggregate_rows_f32", pool.data_ptr(), rows.data_ptr(), ld, C, D, wC.data_ptr(), 1.0,
+                        normC.data_ptr(), coefC.data_ptr(), clipC.data_ptr(), badC.data_ptr(), agg.data_ptr(), 0,
+                        fws.data_ptr(), fws.numel(), s)
+        for c0 in range(0, C if not fused else 0, P):
             n = min(P, C - c0)
-            if fused:  # K2 + K3 in one HBM pass (clip_aggregate_fused.cu)
-                native.call("fb_clip_aggregate_f32", pool.data_ptr(), ld, n, D, w.data_ptr(), 1.0, norm.data_ptr(),
-                            coef.data_ptr(), clipped.data_ptr(), bad.data_ptr(), agg.data_ptr(), int(c0 > 0),
-                            fws.data_ptr(), fws.numel(), s)
-                continue
             native.call("fb_delta_norm_clip_f32", pool.data_ptr(), ld, n, D, w.data_ptr(), 1.0, norm.data_ptr(),
                         coef.data_ptr(), clipped.data_ptr(), bad.data_ptr(), cws.data_ptr(), cws.numel(), s)
             native.call("fb_weighted_sum_f32", pool.data_ptr(), ld, n, D, coef.data_ptr(), agg.data_ptr(),
@@ -837,8 +842,8 @@ def aggregation_microbench(args):
     chunks = -(-C // P)
     for name, bytes_per_step in (("row_sumsq_partial_kernel", 4.0 * D * C),
                                  ("weighted_sum_kernel", 4.0 * D * C + 4.0 * D * chunks),
-                                 # one read per client + the aggregate written (and re-read after the first chunk)
-                                 ("clip_aggregate_fused_kernel", 4.0 * D * C + 4.0 * D * (2 * chunks - 1)),
+                                 # one read per client + the aggregate written once (one launch)
+                                 ("clip_aggregate_fused_kernel", 4.0 * D * C + 4.0 * D),
                                  ("noise_avg_sgd_kernel", 12.0 * D)):
         if name in rep:
             t = rep[name][0] / args.steps

@@ -272,6 +272,13 @@ int fb_clip_aggregate_f32(const float* delta, int64_t ld_delta, int num_clients,
                           const float* w, double bound, double* norm, float* coef,
                           int32_t* clipped, int32_t* nonfinite, float* agg, int accumulate,
                           void* workspace, int64_t workspace_bytes, void* stream);
+/* The same with client c's update at delta row rows[c] (int32 device array): a
+ * queue order that differs from the storage order, or one pool of rows reused
+ * (the configs[4] microbench) -- all C clients in one launch.               */
+int fb_clip_aggregate_rows_f32(const float* delta, const int32_t* rows, int64_t ld_delta, int num_clients,
+                               int64_t D, const float* w, double bound, double* norm, float* coef,
+                               int32_t* clipped, int32_t* nonfinite, float* agg, int accumulate,
+                               void* workspace, int64_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------ a9 (worker_reduce)
  * Per-context sums over the C clients of this rank, fp64 in a fixed order,

@@ -151,6 +151,7 @@ __device__ __forceinline__ float4 mask_tail(float4 v, int64_t col, int64_t D) {
 
 struct Args {
   const float* delta;
+  const int32_t* rows;  // nullable: client k's update is delta row rows[k] (else row k)
   int64_t ld;
   int C;
   int64_t D;
@@ -231,7 +232,8 @@ __global__ void __launch_bounds__(kT, 1) clip_aggregate_fused_kernel(const Args 
           const int slot = i % stages;
           if (i >= stages) mbar_wait_spin(&empty[slot], ((i / stages) - 1) & 1);
           tc::mbar_arrive_expect_tx(&full[slot], bytes);
-          bulk_load_hint(tc::smem_u32(ring + slot * kStageBytes), a.delta + (int64_t)k * a.ld + c0, bytes,
+          const int64_t row = a.rows ? (int64_t)__ldg(a.rows + k) : (int64_t)k;
+          bulk_load_hint(tc::smem_u32(ring + slot * kStageBytes), a.delta + row * a.ld + c0, bytes,
                          tc::smem_u32(&full[slot]), pol);
         }
       }
@@ -468,7 +470,7 @@ int64_t fb_clip_aggregate_workspace_bytes(int num_clients, int64_t D) {
   return fb::workspace_bytes(num_clients, D);
 }
 
-int fb_clip_aggregate_f32(const float* delta, int64_t ld_delta, int num_clients, int64_t D, const float* w,
+static int clip_aggregate(const float* delta, const int32_t* rows, int64_t ld_delta, int num_clients, int64_t D, const float* w,
                           double bound, double* norm, float* coef, int32_t* clipped, int32_t* nonfinite,
                           float* agg, int accumulate, void* workspace, int64_t workspace_bytes, void* stream) {
   FB_REQUIRE(num_clients >= 0 && D >= 0 && ld_delta >= D, "clip_aggregate: bad shape (C=%d D=%lld ld=%lld)",
@@ -489,6 +491,7 @@ int fb_clip_aggregate_f32(const float* delta, int64_t ld_delta, int num_clients,
   char* ws = static_cast<char*>(workspace);
   fb::Args a;
   a.delta = delta;
+  a.rows = rows;
   a.ld = ld_delta;
   a.C = num_clients;
   a.D = D;
@@ -526,6 +529,22 @@ int fb_clip_aggregate_f32(const float* delta, int64_t ld_delta, int num_clients,
     return FB_ERR_CUDA;
   }
   return fb::launch_status("clip_aggregate_fused_kernel");
+}
+
+int fb_clip_aggregate_f32(const float* delta, int64_t ld_delta, int num_clients, int64_t D, const float* w,
+                          double bound, double* norm, float* coef, int32_t* clipped, int32_t* nonfinite,
+                          float* agg, int accumulate, void* workspace, int64_t workspace_bytes, void* stream) {
+  return clip_aggregate(delta, nullptr, ld_delta, num_clients, D, w, bound, norm, coef, clipped, nonfinite, agg,
+                        accumulate, workspace, workspace_bytes, stream);
+}
+
+int fb_clip_aggregate_rows_f32(const float* delta, const int32_t* rows, int64_t ld_delta, int num_clients, int64_t D,
+                               const float* w, double bound, double* norm, float* coef, int32_t* clipped,
+                               int32_t* nonfinite, float* agg, int accumulate, void* workspace,
+                               int64_t workspace_bytes, void* stream) {
+  FB_REQUIRE(rows != nullptr || num_clients == 0, "clip_aggregate_rows: null rows");
+  return clip_aggregate(delta, rows, ld_delta, num_clients, D, w, bound, norm, coef, clipped, nonfinite, agg,
+                        accumulate, workspace, workspace_bytes, stream);
 }
 
 }  // extern "C"

@@ -73,6 +73,7 @@ SIGNATURES: dict[str, tuple] = {
     "fb_clip_aggregate_max_columns": (_i64, []),
     "fb_clip_aggregate_workspace_bytes": (_i64, [_i32, _i64]),
     "fb_clip_aggregate_f32": (_i32, [_p, _i64, _i32, _i64, _p, _f64, _p, _p, _p, _p, _p, _i32, _p, _i64, _p]),
+    "fb_clip_aggregate_rows_f32": (_i32, [_p, _p, _i64, _i32, _i64, _p, _f64, _p, _p, _p, _p, _p, _i32, _p, _i64, _p]),
     "fb_sumsq_f32": (_i32, [_p, _i64, _p, _p, _i64, _p]),
     "fb_context_sums": (_i32, [_p, _p, _p, _p, _p, _p, _p, _i32, _i32, _p, _p]),
     "fb_gaussian_f32": (_i32, [_p, _i64, _f64, _u64, _u64, _i32, _p]),

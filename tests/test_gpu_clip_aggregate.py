@@ -171,3 +171,28 @@ def test_engine_through_fused_path_matches_reference_run(name, golden, monkeypat
     got, ref = res.metrics_rows, golden_rows(g)
     assert [r[:3] for r in got] == [r[:3] for r in ref]
     np.testing.assert_allclose([r[3] for r in got], [r[3] for r in ref], rtol=2e-5)
+
+
+def test_fused_rows_gather_matches_two_pass():
+    """fb_clip_aggregate_rows_f32: client c reads delta row rows[c] -- a permuted queue with
+    repeats (a pool of 5 rows for 150 clients, crossing two fp32 blocks) equals the
+    two-kernel path over the materialised gathered matrix."""
+    P, C, D = 5, 150, 70_001
+    buf, ld, _ = make(P, D, seed=9)
+    rows = torch.tensor(np.random.default_rng(1).integers(0, P, C), dtype=torch.int32, device="cuda")
+    w = torch.rand(C, device="cuda") + 0.5
+    norm = torch.zeros(C, dtype=torch.float64, device="cuda")
+    coef = torch.zeros(C, device="cuda")
+    clipped = torch.zeros(C, dtype=torch.int32, device="cuda")
+    bad = torch.zeros(C, dtype=torch.int32, device="cuda")
+    agg = torch.zeros(D, device="cuda")
+    ws = torch.empty(native.call("fb_clip_aggregate_workspace_bytes", C, D), dtype=torch.uint8, device="cuda")
+    native.call("fb_clip_aggregate_rows_f32", buf.data_ptr(), rows.data_ptr(), ld, C, D, w.data_ptr(), 0.9,
+                norm.data_ptr(), coef.data_ptr(), clipped.data_ptr(), bad.data_ptr(), agg.data_ptr(), 0,
+                ws.data_ptr(), ws.numel(), S())
+    torch.cuda.synchronize()
+    gathered = buf[rows.long()].contiguous()
+    agg2, norm2, coef2, clipped2 = two_pass(gathered, ld, C, D, w, 0.9)
+    np.testing.assert_allclose(norm.cpu().numpy(), norm2, rtol=1e-14)
+    np.testing.assert_array_equal(clipped.cpu().numpy(), clipped2)
+    assert_close_fp32(agg.double().cpu().numpy(), agg2, what="gathered fused vs two-pass")
