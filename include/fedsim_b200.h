@@ -206,9 +206,10 @@ int fb_upload_pinned(const void* host_src, void* dst, int64_t bytes, void* strea
  * fb_local_sgd_mlp_f32.  Shapes: d <= 256, d % heads == 0, d / heads <= 32,
  * seq <= 32 (FB_ERR_UNSUPPORTED otherwise).                                */
 int64_t fb_lm_num_params(const int32_t* dims);
-/* [host] GEMM implementation of the LM entry points (process-wide): 0 = the
- * SIMT FP32 tiled GEMM (default), 1 = tcgen05 3xTF32 (split products on the
- * tensor cores, TMEM accumulation in 2-slice windows folded into fp32).     */
+/* [host] GEMM implementation of the LM entry points (process-wide): 1 =
+ * tcgen05 3xTF32 (default: TMA-fed persistent kernel, split products on the
+ * tensor cores, TMEM accumulation in 2-slice windows folded into fp32), 0 =
+ * the SIMT FP32 tiled GEMM (validation).                                    */
 int fb_lm_set_gemm_impl(int impl);
 int64_t fb_lm_workspace_bytes(const int32_t* dims, int batch_size, int clients_per_wave, int eval_groups);
 int fb_eval_lm_f32(const float* theta, const int32_t* dims, const float* X, const int64_t* row_start,

@@ -34,6 +34,8 @@
 #include "fb_common.cuh"
 #include "tc_common.cuh"
 
+#include <cudaTypedefs.h>
+
 namespace fb {
 namespace lm {
 
@@ -311,125 +313,118 @@ __global__ void __launch_bounds__(GT) gemm_big_kernel(const Gemm g) {
 // ------------------------------------------------------- tcgen05 3xTF32 GEMM
 // The same grouped C = op(A) op(B) on the 5th-gen tensor cores.  kind::tf32 reads
 // K-major operands only, and an fp32-accurate product needs the 3xTF32 split
-// (hi*hi + hi*lo + lo*hi, ~2^-22 relative, fp32 exponent range: no scaling), so
-// the operands cannot go global -> smem untouched; instead 4 converter warps load
-// the CTA's A (128 x 32) and B (BN x 32) K-slices with 128-bit loads in whatever
-// layout they have in memory (K- or M/N-contiguous), split every value and store
-// the hi / lo parts K-major SWIZZLE_128B into a 3-stage ring.  One warp issues
-// the MMAs (M = 128, N = BN, K = 8: three per K step, fp32 accumulators in TMEM);
-// 4 epilogue warps drain TMEM (warp w reads lanes 32 (w % 4) ..) and apply
-// alpha / beta / bias / ReLU-mask.  One output tile per CTA; grid = tiles x clients.
+// (hi*hi + hi*lo + lo*hi, hi = rna_tf32(x), lo = rna_tf32(x - hi): ~2^-22 of the
+// summands, fp32 exponent range, no scaling).  Per 32-wide K slice:
+//   * a producer warp TMA-loads the raw fp32 A (128 rows) and B (BN rows) tiles
+//     -- K-major operands as SWIZZLE_128B boxes {32 k, rows}, M/N-contiguous ones
+//     as plain boxes {rows, 32 k} -- into a ring (3-D tensor maps, the client as
+//     the outer coordinate), completion counted on an mbarrier;
+//   * 4 converter warps split in shared memory: a K-major tile's hi is rounded in
+//     place and its lo written at the same swizzled offset (one 16-byte chunk per
+//     step); an M/N-contiguous tile is transposed into K-major SW128 hi / lo tiles;
+//   * one warp issues the MMAs (M = 128, N = BN, K = 8: three per K step) into a
+//     TMEM window; every 2 K slices (24 MMAs -- one long chain drifted 1.5e-4 at
+//     K = 10 004) the window is handed to
+//   * 4 epilogue warps that fold it into fp32 registers and finally apply alpha /
+//     beta / bias / ReLU-mask with 128-bit stores.
+// One output tile per CTA; grid = tiles x clients.
 constexpr int TCM = 128;                 // M tile (UMMA M)
 constexpr int TCK = 32;                  // K slice per stage = one 128-byte swizzle row
-constexpr int TC_STAGES = 3;
 constexpr int TC_CONV = 4;               // converter warps
-constexpr int TC_THREADS = 32 * (TC_CONV + 1 + 4);
-template <int BNT>
+constexpr int TC_THREADS = 32 * (2 + TC_CONV + 4);
+constexpr int TC_WIN = 2;                // K slices per TMEM window
+
+template <bool TA, bool TB, int BNT>
 struct TcCfg {
-  static constexpr int A_BYTES = TCM * 128;            // one part of the A slice
-  static constexpr int B_BYTES = BNT * 128;
-  static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;  // A hi | A lo | B hi | B lo
-  static constexpr int SMEM = 1024 + TC_STAGES * STAGE + 256;  // (+ barriers and the TMEM slot)
+  static constexpr bool AK = !TA, BK_ = TB;          // operand already K-major in memory
+  static constexpr int A_T = TCM * 128, B_T = BNT * 128;  // one K-major tile (hi or lo)
+  static constexpr int A_RAW = TCM * TCK * 4, B_RAW = BNT * TCK * 4;
+  // stage: [A raw (= hi when K-major)] [A hi (M-contiguous only)] [A lo] [B raw] [B hi] [B lo]
+  static constexpr int A_HI = AK ? 0 : A_RAW, A_LO = AK ? A_RAW : A_RAW + A_T;
+  static constexpr int B0 = A_LO + A_T;
+  static constexpr int B_HI = BK_ ? B0 : B0 + B_RAW, B_LO = BK_ ? B0 + B_RAW : B0 + B_RAW + B_T;
+  static constexpr int STAGE = B_LO + B_T;
+  static constexpr int STAGES = STAGE <= 64 * 1024 ? 3 : 2;
+  static constexpr int SMEM = 1024 + STAGES * STAGE + 256;
   static constexpr uint32_t IDESC = tc::idesc_tf32(TCM, BNT);
+  static constexpr uint32_t TX = A_RAW + B_RAW;
 };
 
-// 3xTF32 split with BOTH parts rounded to nearest tf32 (the tensor core would truncate
-// lo's low 13 bits): |x - hi - lo| <= 2^-23 |x|
+// 3xTF32 split with BOTH parts rounded to nearest tf32: |x - hi - lo| <= 2^-23 |x|
 __device__ __forceinline__ void split_rn(float x, float& hi, float& lo) {
   hi = __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
   uint32_t l;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(x - hi));
   lo = __uint_as_float(l);
 }
+__device__ __forceinline__ float4 lds4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts4(uint32_t a, float x, float y, float z, float w) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(x), "f"(y), "f"(z), "f"(w) : "memory");
+}
 
-// converter: rows [r0, r0 + nrows) x k [k0, k0 + 32) of an operand into (hi, lo)
-// K-major SW128 tiles; trans = the operand's row index is contiguous in memory.  All of
-// a thread's (<= 8) 128-bit loads are issued before any is split and stored.
-__device__ __forceinline__ void tc_convert(const float* base, int64_t ld, bool trans, int rows, int kdim, int r0,
-                                           int k0, int nrows, bool relu, uint32_t hi, uint32_t lo, int ct) {
+// K-major raw tile of `rows` x 32 k (SW128): hi in place, lo at the same offset
+__device__ __forceinline__ void conv_kmajor(uint32_t raw, uint32_t lo, int rows, bool relu, int ct) {
   constexpr int NT = 32 * TC_CONV;
-  const bool vec = ((ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(base) & 15) == 0);
-  const int rq = (nrows + 3) >> 2;
-  const int total = trans ? TCK * rq : nrows * 8;  // float4 units of the tile
-  float4 v[8];
-#pragma unroll
-  for (int u = 0; u < 8; ++u) {
-    const int i = ct + u * NT;
-    v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (i >= total) continue;
-    int gr, gk;
-    if (trans) { const int k = i / rq; gr = r0 + (i - k * rq) * 4; gk = k0 + k; }
-    else { gr = r0 + (i >> 3); gk = k0 + (i & 7) * 4; }
-    float x[4];
-    if (!trans) {
-      if (vec && gr < rows && gk + 3 < kdim) {
-        v[u] = *reinterpret_cast<const float4*>(base + (int64_t)gr * ld + gk);
-        continue;
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) x[q] = (gr < rows && gk + q < kdim) ? base[(int64_t)gr * ld + gk + q] : 0.f;
-    } else {
-      if (vec && gk < kdim && gr + 3 < rows) {
-        v[u] = *reinterpret_cast<const float4*>(base + (int64_t)gk * ld + gr);
-        continue;
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) x[q] = (gk < kdim && gr + q < rows) ? base[(int64_t)gk * ld + gr + q] : 0.f;
-    }
-    v[u] = make_float4(x[0], x[1], x[2], x[3]);
-  }
-#pragma unroll
-  for (int u = 0; u < 8; ++u) {
-    const int i = ct + u * NT;
-    if (i >= total) continue;
-    float x[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+  for (int i = ct; i < rows * 8; i += NT) {
+    const uint32_t off = (uint32_t)i * 16;
+    const float4 v = lds4(raw + off);
+    const float x[4] = {v.x, v.y, v.z, v.w};
     float h[4], l[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) split_rn(relu ? fmaxf(x[q], 0.f) : x[q], h[q], l[q]);
-    if (!trans) {
-      const uint32_t off = tc::sw128_offset(i >> 3, (i & 7) * 4);  // one 16-byte chunk
-      asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(hi + off), "f"(h[0]), "f"(h[1]), "f"(h[2]),
-                   "f"(h[3]) : "memory");
-      asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(lo + off), "f"(l[0]), "f"(l[1]), "f"(l[2]),
-                   "f"(l[3]) : "memory");
-    } else {
-      const int k = i / rq, r = (i - k * rq) * 4;
+    sts4(raw + off, h[0], h[1], h[2], h[3]);
+    sts4(lo + off, l[0], l[1], l[2], l[3]);
+  }
+}
+// M/N-contiguous raw tile [32 k][rows] -> K-major SW128 hi / lo tiles
+__device__ __forceinline__ void conv_mnmajor(uint32_t raw, uint32_t hi, uint32_t lo, int rows, bool relu, int ct) {
+  constexpr int NT = 32 * TC_CONV;
+  for (int i = ct; i < rows * 8; i += NT) {
+    const int r = i % rows, kc = (i / rows) * 4;  // consecutive threads: consecutive rows (banks)
+    float h[4], l[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        if (r + q < nrows) {
-          const uint32_t off = tc::sw128_offset(r + q, k);
-          tc::sts_f32(hi + off, h[q]);
-          tc::sts_f32(lo + off, l[q]);
-        }
-      }
+    for (int q = 0; q < 4; ++q) {
+      const float x = tc::lds_f32(raw + (uint32_t)((kc + q) * rows + r) * 4);
+      split_rn(relu ? fmaxf(x, 0.f) : x, h[q], l[q]);
     }
+    const uint32_t off = tc::sw128_offset(r, kc);
+    sts4(hi + off, h[0], h[1], h[2], h[3]);
+    sts4(lo + off, l[0], l[1], l[2], l[3]);
   }
 }
 
-// K-slices accumulated per TMEM window before the epilogue folds the window into its fp32
-// registers: the tensor core's fp32 accumulation drifts over long MMA chains (measured:
-// 1.5e-4 relative at K = 10 004 in one chain), 2 slices = 24 MMAs stays at fp32 accuracy
-constexpr int TC_WIN = 2;
-
+// Persistent: CTA b takes tiles b, b + grid, ... of the (client, m-tile, n-tile) space
+// (idle clients' tiles skipped by every role alike); the stage ring and the two TMEM
+// windows run on across tile boundaries, so one tile's epilogue overlaps the next
+// tile's loads, conversion and MMAs.
 template <bool TA, bool TB, int BNT>
-__global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const Gemm g) {
-  using Cfg = TcCfg<BNT>;
-  const int z = blockIdx.z;
-  if (g.active && !g.active[z]) return;
+__global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap ma,
+                                                                const __grid_constant__ CUtensorMap mb,
+                                                                const Gemm g, int a_batched, int b_batched,
+                                                                int batch) {
+  using Cfg = TcCfg<TA, TB, BNT>;
+  constexpr int S = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(sm + TC_STAGES * Cfg::STAGE);
-  uint64_t* empty = full + TC_STAGES;
-  uint64_t* tfull = empty + TC_STAGES;  // [2] window accumulated
-  uint64_t* tempty = tfull + 2;         // [2] window drained by the epilogue
+  uint64_t* rfull = reinterpret_cast<uint64_t*>(sm + S * Cfg::STAGE);  // raw tiles landed
+  uint64_t* cfull = rfull + S;                                         // split tiles ready
+  uint64_t* empty = cfull + S;                                         // MMAs of the stage done
+  uint64_t* tfull = empty + S;                                         // [2] window accumulated
+  uint64_t* tempty = tfull + 2;                                        // [2] window drained
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * TCM, n0 = blockIdx.x * BNT;
+  const int tn = (g.N + BNT - 1) / BNT, tm = (g.M + TCM - 1) / TCM;
+  const int tiles = tn * tm * batch;
   const int nk = (g.K + TCK - 1) / TCK;
-  const int nwin = (nk + TC_WIN - 1) / TC_WIN;
+  const int nwin = (nk + TC_WIN - 1) / TC_WIN;  // windows per tile
   if (threadIdx.x == 0) {
-    for (int i = 0; i < TC_STAGES; ++i) {
-      tc::mbar_init(&full[i], TC_CONV);
+    for (int i = 0; i < S; ++i) {
+      tc::mbar_init(&rfull[i], 1);
+      tc::mbar_init(&cfull[i], TC_CONV);
       tc::mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -438,108 +433,153 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const Gemm g) {
     }
     tc::fence_mbar_init();
   }
-  constexpr uint32_t kCols = BNT <= 128 ? 256 : 512;  // two accumulator windows
-  if (warp == TC_CONV) tc::tmem_alloc<kCols>(tmem_slot);
+  constexpr uint32_t kCols = 2 * BNT <= 256 ? 256 : 512;  // two accumulator windows
+  if (warp == 1) tc::tmem_alloc<kCols>(tmem_slot);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t s0 = tc::smem_u32(sm);
-  const float* A = g.A + (int64_t)z * g.sA;
-  const float* B = g.B + (int64_t)z * g.sB;
+  // tile -> (client z, m0, n0); n fastest so consecutive tiles of a CTA share the A rows
+  auto geom = [&](int tile, int& z, int& m0, int& n0) -> bool {
+    z = tile / (tn * tm);
+    const int r = tile - z * tn * tm, mt = r / tn;
+    m0 = mt * TCM;
+    n0 = (r - mt * tn) * BNT;
+    return !g.active || g.active[z];
+  };
 
-  if (warp < TC_CONV) {
-    // ------------------------------------------------------------ converters
-    const int ct = threadIdx.x;
-    for (int t = 0; t < nk; ++t) {
-      const int st = t % TC_STAGES;
-      if (t >= TC_STAGES) tc::mbar_wait(&empty[st], ((t / TC_STAGES) - 1) & 1);
-      const uint32_t base = s0 + st * Cfg::STAGE;
-      // A(m, k): TA -> A[k * lda + m] (m contiguous); B(n, k) as a K-major operand:
-      // TB -> B[n * ldb + k] (k contiguous), else B[k * ldb + n] (n contiguous)
-      tc_convert(A, g.lda, TA, g.M, g.K, m0, t * TCK, TCM, g.relu_a, base, base + Cfg::A_BYTES, ct);
-      tc_convert(B, g.ldb, !TB, g.N, g.K, n0, t * TCK, BNT, g.relu_b, base + 2 * Cfg::A_BYTES,
-                 base + 2 * Cfg::A_BYTES + Cfg::B_BYTES, ct);
-      tc::fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&full[st]);
-    }
-  } else if (warp == TC_CONV) {
-    // ------------------------------------------------------------- MMA issuer
-    for (int t = 0; t < nk; ++t) {
-      const int st = t % TC_STAGES, w = t / TC_WIN, buf = w & 1;
-      if (t % TC_WIN == 0 && w >= 2) {  // this window's TMEM buffer drained (window w - 2)?
-        tc::mbar_wait(&tempty[buf], ((w >> 1) - 1) & 1);
-        tc::tc_fence_after();
-      }
-      tc::mbar_wait(&full[st], (t / TC_STAGES) & 1);
-      tc::tc_fence_after();
-      if (tc::elect_one()) {
-        const uint32_t d = tmem + buf * BNT;
-        const uint32_t ah = s0 + st * Cfg::STAGE, al = ah + Cfg::A_BYTES;
-        const uint32_t bh = ah + 2 * Cfg::A_BYTES, bl = bh + Cfg::B_BYTES;
-#pragma unroll
-        for (int k8 = 0; k8 < TCK / 8; ++k8) {
-          const uint32_t kb = k8 * 32;  // 8 tf32 = 32 bytes along the swizzled row
-          const uint32_t acc0 = (t % TC_WIN > 0 || k8 > 0) ? 1u : 0u;
-          tc::mma_tf32(d, tc::sdesc_k128(ah + kb), tc::sdesc_k128(bh + kb), Cfg::IDESC, acc0);
-          tc::mma_tf32(d, tc::sdesc_k128(ah + kb), tc::sdesc_k128(bl + kb), Cfg::IDESC, 1u);
-          tc::mma_tf32(d, tc::sdesc_k128(al + kb), tc::sdesc_k128(bh + kb), Cfg::IDESC, 1u);
+  if (warp == 0) {
+    // -------------------------------------------------------------- producer
+    if (lane == 0) {
+      tc::tma_prefetch(&ma);
+      tc::tma_prefetch(&mb);
+      int t = 0;  // global stage counter
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        int z, m0, n0;
+        if (!geom(tile, z, m0, n0)) continue;
+        const int za = a_batched ? z : 0, zb = b_batched ? z : 0;
+        for (int kk = 0; kk < nk; ++kk, ++t) {
+          const int st = t % S;
+          if (t >= S) tc::mbar_wait(&empty[st], ((t / S) - 1) & 1);
+          tc::mbar_arrive_expect_tx(&rfull[st], Cfg::TX);
+          uint8_t* base = sm + st * Cfg::STAGE;
+          const int k0 = kk * TCK;
+          if (Cfg::AK) tc::tma_load_3d(base, &ma, k0, m0, za, &rfull[st]);
+          else tc::tma_load_3d(base, &ma, m0, k0, za, &rfull[st]);
+          if (Cfg::BK_) tc::tma_load_3d(base + Cfg::B0, &mb, k0, n0, zb, &rfull[st]);
+          else tc::tma_load_3d(base + Cfg::B0, &mb, n0, k0, zb, &rfull[st]);
         }
-        tc::mma_commit(&empty[st]);
-        if (t % TC_WIN == TC_WIN - 1 || t == nk - 1) tc::mma_commit(&tfull[buf]);
       }
-      __syncwarp();
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------- MMA issuer
+    int t = 0, w = 0;  // global stage / window counters
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      int z, m0, n0;
+      if (!geom(tile, z, m0, n0)) continue;
+      for (int kk = 0; kk < nk; ++kk, ++t) {
+        const int st = t % S, buf = w & 1;
+        if (kk % TC_WIN == 0 && w >= 2) {  // this window's buffer drained (window w - 2)?
+          tc::mbar_wait(&tempty[buf], ((w >> 1) - 1) & 1);
+          tc::tc_fence_after();
+        }
+        tc::mbar_wait(&cfull[st], (t / S) & 1);
+        tc::tc_fence_after();
+        if (tc::elect_one()) {
+          const uint32_t d = tmem + buf * BNT;
+          const uint32_t base = s0 + st * Cfg::STAGE;
+          const uint32_t ah = base + Cfg::A_HI, al = base + Cfg::A_LO;
+          const uint32_t bh = base + Cfg::B_HI, bl = base + Cfg::B_LO;
+#pragma unroll
+          for (int k8 = 0; k8 < TCK / 8; ++k8) {
+            const uint32_t kb = k8 * 32;  // 8 tf32 = 32 bytes along the swizzled row
+            const uint32_t acc0 = (kk % TC_WIN > 0 || k8 > 0) ? 1u : 0u;
+            tc::mma_tf32(d, tc::sdesc_k128(ah + kb), tc::sdesc_k128(bh + kb), Cfg::IDESC, acc0);
+            tc::mma_tf32(d, tc::sdesc_k128(ah + kb), tc::sdesc_k128(bl + kb), Cfg::IDESC, 1u);
+            tc::mma_tf32(d, tc::sdesc_k128(al + kb), tc::sdesc_k128(bh + kb), Cfg::IDESC, 1u);
+          }
+          tc::mma_commit(&empty[st]);
+          if (kk % TC_WIN == TC_WIN - 1 || kk == nk - 1) tc::mma_commit(&tfull[buf]);
+        }
+        __syncwarp();
+        if (kk % TC_WIN == TC_WIN - 1 || kk == nk - 1) ++w;
+      }
+    }
+  } else if (warp < 2 + TC_CONV) {
+    // ------------------------------------------------------------ converters
+    const int ct = threadIdx.x - 64;
+    int t = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      int z, m0, n0;
+      if (!geom(tile, z, m0, n0)) continue;
+      for (int kk = 0; kk < nk; ++kk, ++t) {
+        const int st = t % S;
+        tc::mbar_wait(&rfull[st], (t / S) & 1);
+        const uint32_t base = s0 + st * Cfg::STAGE;
+        if (Cfg::AK) conv_kmajor(base, base + Cfg::A_LO, TCM, g.relu_a, ct);
+        else conv_mnmajor(base, base + Cfg::A_HI, base + Cfg::A_LO, TCM, g.relu_a, ct);
+        if (Cfg::BK_) conv_kmajor(base + Cfg::B0, base + Cfg::B_LO, BNT, g.relu_b, ct);
+        else conv_mnmajor(base + Cfg::B0, base + Cfg::B_HI, base + Cfg::B_LO, BNT, g.relu_b, ct);
+        tc::fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&cfull[st]);
+      }
     }
   } else {
     // --------------------------------------------------------------- epilogue
     const int q = warp & 3;
-    const int m = m0 + q * 32 + lane;
-    float sum[BNT];
+    int w = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      int z, m0, n0;
+      if (!geom(tile, z, m0, n0)) continue;
+      const int m = m0 + q * 32 + lane;
+      float sum[BNT];
 #pragma unroll
-    for (int j = 0; j < BNT; ++j) sum[j] = 0.f;
-    for (int w = 0; w < nwin; ++w) {
-      const int buf = w & 1;
-      tc::mbar_wait(&tfull[buf], (w >> 1) & 1);
-      tc::tc_fence_after();
+      for (int j = 0; j < BNT; ++j) sum[j] = 0.f;
+      for (int wi = 0; wi < nwin; ++wi, ++w) {
+        const int buf = w & 1;
+        tc::mbar_wait(&tfull[buf], (w >> 1) & 1);
+        tc::tc_fence_after();
 #pragma unroll
-      for (int c0 = 0; c0 < BNT; c0 += 32) {
-        uint32_t v[32];
-        tc::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + buf * BNT + c0, v);
-        tc::tmem_ld_wait();
+        for (int c0 = 0; c0 < BNT; c0 += 32) {
+          uint32_t v[32];
+          tc::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + buf * BNT + c0, v);
+          tc::tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) sum[c0 + j] += __uint_as_float(v[j]);
-      }
-      tc::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&tempty[buf]);
-    }
-    if (m < g.M) {
-      float* crow = g.C + (int64_t)z * g.sC + (int64_t)m * g.ldc;
-      const float* bias = g.bias ? g.bias + (int64_t)z * g.sBias : nullptr;
-      const float* arow = g.aux ? g.aux + (int64_t)z * g.sAux + (int64_t)m * g.ldaux : nullptr;
-      const bool v4 = ((g.ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(crow) & 15) == 0);
-#pragma unroll
-      for (int j0 = 0; j0 < BNT; j0 += 4) {
-        const int n = n0 + j0;
-        float x[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int nn = n + u;
-          float val = g.alpha * sum[j0 + u];
-          if (nn < g.N) {
-            if (g.beta != 0.f) val = fmaf(g.beta, crow[nn], val);
-            if (bias) val += bias[nn];
-            if (arow && !(arow[nn] > 0.f)) val = 0.f;
-          }
-          x[u] = val;
+          for (int j = 0; j < 32; ++j) sum[c0 + j] += __uint_as_float(v[j]);
         }
-        if (v4 && n + 3 < g.N) {
-          *reinterpret_cast<float4*>(crow + n) = make_float4(x[0], x[1], x[2], x[3]);
-        } else {
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&tempty[buf]);
+      }
+      if (m < g.M) {
+        float* crow = g.C + (int64_t)z * g.sC + (int64_t)m * g.ldc;
+        const float* bias = g.bias ? g.bias + (int64_t)z * g.sBias : nullptr;
+        const float* arow = g.aux ? g.aux + (int64_t)z * g.sAux + (int64_t)m * g.ldaux : nullptr;
+        const bool v4 = ((g.ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(crow) & 15) == 0);
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (n + u < g.N) crow[n + u] = x[u];
+        for (int j0 = 0; j0 < BNT; j0 += 4) {
+          const int n = n0 + j0;
+          float x[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int nn = n + u;
+            float val = g.alpha * sum[j0 + u];
+            if (nn < g.N) {
+              if (g.beta != 0.f) val = fmaf(g.beta, crow[nn], val);
+              if (bias) val += bias[nn];
+              if (arow && !(arow[nn] > 0.f)) val = 0.f;
+            }
+            x[u] = val;
+          }
+          if (v4 && n + 3 < g.N) {
+            *reinterpret_cast<float4*>(crow + n) = make_float4(x[0], x[1], x[2], x[3]);
+          } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (n + u < g.N) crow[n + u] = x[u];
+          }
         }
       }
     }
@@ -547,7 +587,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const Gemm g) {
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
-  if (warp == TC_CONV) tc::tmem_dealloc<kCols>(tmem);
+  if (warp == 1) tc::tmem_dealloc<kCols>(tmem);
 }
 
 // ------------------------------------------------------------ batch gather
@@ -1084,27 +1124,76 @@ inline Work carve(const Dims& m, int W, int B, bool train, Buf& b) {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-// 0 = SIMT FP32 tiled GEMM (default: measured faster here -- 196 vs 232 ms per config C
-// iteration -- because the tcgen05 path's per-stage operand conversion (split into tf32
-// hi / lo, K-major swizzle) runs at one CTA per SM), 1 = tcgen05 3xTF32
-int g_gemm_impl = 0;
+// 1 = tcgen05 3xTF32 (default: config C 140.6 ms per iteration vs 196 ms with the SIMT
+// GEMM, profiles/r02x_lm_bench_tc.log), 0 = SIMT FP32 tiled GEMM (validation)
+int g_gemm_impl = 1;
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 3-D fp32 map {inner, rows, batch} (batch stride 0 -> one batch), box {bi, br, 1}
+bool map3d(CUtensorMap* map, const float* base, int64_t inner, int64_t rows, int64_t ld, int64_t batch,
+           int64_t sbatch, int bi, int br, bool swz) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)rows, (cuuint64_t)(sbatch ? batch : 1)};
+  const cuuint64_t strides[2] = {(cuuint64_t)ld * 4, (cuuint64_t)(sbatch ? sbatch : ld * rows) * 4};
+  const cuuint32_t box[3] = {(cuuint32_t)bi, (cuuint32_t)br, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, swz ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// tensor-map constraints: 16-byte aligned base and strides
+bool tma_ok(const float* p, int64_t ld, int64_t sb) {
+  return aligned16(p) && (ld & 3) == 0 && (sb & 3) == 0;
+}
 
 template <bool TA, bool TB, int BNT>
 int launch_tc(const Gemm& g, int batch, cudaStream_t s, const char* name) {
-  using Cfg = TcCfg<BNT>;
+  using Cfg = TcCfg<TA, TB, BNT>;
+  CUtensorMap ma, mb;
+  // A(m, k): K-major [M rows][K] (ld lda) or M-contiguous [K rows][M]; B(k, n) likewise
+  const bool okA = TA ? map3d(&ma, g.A, g.M, g.K, g.lda, batch, g.sA, TCM, TCK, false)
+                      : map3d(&ma, g.A, g.K, g.M, g.lda, batch, g.sA, TCK, TCM, true);
+  const bool okB = TB ? map3d(&mb, g.B, g.K, g.N, g.ldb, batch, g.sB, TCK, BNT, true)
+                      : map3d(&mb, g.B, g.N, g.K, g.ldb, batch, g.sB, BNT, TCK, false);
+  if (!okA || !okB) {
+    set_error("lm tcgen05 GEMM: cuTensorMapEncodeTiled failed");
+    return FB_ERR_CUDA;
+  }
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(gemm_tc_kernel<TA, TB, BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     attr = true;
   }
-  const dim3 grid((g.N + BNT - 1) / BNT, (g.M + TCM - 1) / TCM, batch);
-  FB_LAUNCH(name, s, (gemm_tc_kernel<TA, TB, BNT><<<grid, TC_THREADS, Cfg::SMEM, s>>>(g)));
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const int64_t tiles = (int64_t)((g.N + BNT - 1) / BNT) * ((g.M + TCM - 1) / TCM) * batch;
+  const int grid = (int)(tiles < sms ? tiles : sms);  // persistent: one CTA per SM
+  FB_LAUNCH(name, s, (gemm_tc_kernel<TA, TB, BNT><<<grid, TC_THREADS, Cfg::SMEM, s>>>(ma, mb, g, g.sA != 0,
+                                                                                        g.sB != 0, batch)));
   return launch_status(name);
 }
 
 int launch_gemm(bool TA, bool TB, const Gemm& g, int batch, cudaStream_t s) {
   if (batch <= 0 || g.M <= 0 || g.N <= 0) return FB_OK;
-  if (g_gemm_impl == 1 && g.M >= 64 && g.N >= 64) {
+  if (g_gemm_impl == 1 && g.M >= 64 && g.N >= 64 && tma_ok(g.A, g.lda, g.sA) && tma_ok(g.B, g.ldb, g.sB)) {
     // N tile 96 when it divides N (d_model-wide outputs), else 128
     const bool n96 = g.N % 96 == 0 && g.N <= 192;
     if (!TA && TB) return n96 ? launch_tc<false, true, 96>(g, batch, s, "lm_gemm_tc_nt_kernel")
@@ -1347,7 +1436,7 @@ Dims parse(const int32_t* dims) {
 extern "C" {
 
 int fb_lm_set_gemm_impl(int impl) {
-  FB_REQUIRE(impl == 0 || impl == 1, "lm_set_gemm_impl: 0 (SIMT FP32, default) or 1 (tcgen05 3xTF32)");
+  FB_REQUIRE(impl == 0 || impl == 1, "lm_set_gemm_impl: 0 (SIMT FP32) or 1 (tcgen05 3xTF32, default)");
   fb::lm::g_gemm_impl = impl;
   return FB_OK;
 }
