@@ -285,9 +285,13 @@ def lm_kernel_work(counts: dict) -> dict:
     m = fb.TransformerLM()
     per_row = 2 * ((3 * m.d_model**2 + m.d_model**2 + 2 * m.d_model * m.ff) * m.layers + m.vocab * m.d_model)
     note = "FP32 FFMA (SIMT tiled GEMM)"
+    tc = "3xTF32 tcgen05 (grouped persistent GEMM)"
     return {"lm_gemm_nt_kernel": ("fp32", per_row * counts["fwd_rows"], note),
             "lm_gemm_nn_kernel": ("fp32", per_row * counts["train_rows"], note),
-            "lm_gemm_tn_kernel": ("fp32", per_row * counts["train_rows"], note)}
+            "lm_gemm_tn_kernel": ("fp32", per_row * counts["train_rows"], note),
+            "lm_gemm_tc_nt_kernel": ("tensor", per_row * counts["fwd_rows"], tc),
+            "lm_gemm_tc_nn_kernel": ("tensor", per_row * counts["train_rows"], tc),
+            "lm_gemm_tc_tn_kernel": ("tensor", per_row * counts["train_rows"], tc)}
 
 
 def _ncu_kernel(name: str) -> dict | None:
@@ -365,10 +369,14 @@ def roofline(report: dict, wl: dict, counts: dict, peaks: dict) -> tuple[dict, d
                    traffic=_ncu_traffic(name),
                    **{key: k[key] for key in ("tensor_pipe_active_pct", "issued_ops_per_algorithmic", "issued_frac")
                       if key in k},
-                   peak_source=("MEASURED_PEAKS.json bf16_tflops (dense bf16 cuBLAS); the kernel's own math is "
+                   peak_source=(("MEASURED_PEAKS.json bf16_tflops (dense bf16 cuBLAS); the kernel's own math is "
+                                 + k.get("math", "") + ": three kind::tf32 MMAs per algorithmic product at half the "
+                                 "bf16 rate -> at most 1/6 of this peak") if "TF32" in k.get("math", "") and
+                                wl["model"] == "lm" else
+                                ("MEASURED_PEAKS.json bf16_tflops (dense bf16 cuBLAS); the kernel's own math is "
                                 + k.get("math", "") + ": per algorithmic product one N=128 MMA (hi*[Whi;Wlo]) + one "
                                 "N=64 MMA (lo*Whi) -> at most 1/3 of the fp16/bf16 dense rate, and the N=64 half is "
-                                "bound by shared-memory operand reads (tools/microbench/README.md)")
+                                "bound by shared-memory operand reads (tools/microbench/README.md)"))
                    if k["bound"] == "tensor" else "MEASURED_PEAKS.json hbm_gbs",
                    algorithmic=f"{work[name][1]:.4g} {'FLOP' if k['bound'] == 'tensor' else 'bytes'} over {launches} launches")
     else:
