@@ -684,112 +684,119 @@ __global__ void embed_bwd_kernel(const int32_t* __restrict__ tok, const float* _
 }
 
 // ----------------------------------------------------------------- attention
-// one warp per (client, sentence, head); lane i = query position i (L <= 32, dh <= 32)
-constexpr int kAttWarps = 2;  // (5 x 32 x 33 floats of staging per warp in the backward: 42 KB per CTA)
-
-__global__ void __launch_bounds__(32 * kAttWarps) attn_fwd_kernel(const float* __restrict__ qkv, int B, int L,
-                                                                  int H, int dh, const int32_t* __restrict__ active,
-                                                                  float* __restrict__ P, float* __restrict__ o) {
-  extern __shared__ float sh[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int w = blockIdx.y, unit = blockIdx.x * kAttWarps + warp;  // (sentence, head) of client w
-  if (unit >= B * H || !active[w]) return;
-  const int s = unit / H, h = unit - s * H;
-  const int d = H * dh;
-  float* q = sh + warp * 3 * 32 * 33;
-  float* k = q + 32 * 33;
-  float* v = k + 32 * 33;
-  const float* base = qkv + ((int64_t)w * B * L + (int64_t)s * L) * 3 * d;
-  for (int e = lane; e < L * dh; e += 32) {
-    const int i = e / dh, c = e - i * dh;
-    q[i * 33 + c] = base[(int64_t)i * 3 * d + h * dh + c];
-    k[i * 33 + c] = base[(int64_t)i * 3 * d + d + h * dh + c];
-    v[i * 33 + c] = base[(int64_t)i * 3 * d + 2 * d + h * dh + c];
-  }
-  __syncwarp();
-  float* prow = P + ((((int64_t)w * B + s) * H + h) * L) * L;
-  float* orow = o + ((int64_t)w * B * L + (int64_t)s * L) * d + h * dh;
-  if (lane < L) {
-    const int i = lane;
-    const float sc = 1.0f / sqrtf((float)dh);
-    float sv[32];
-    float mx = -INFINITY;
-    for (int j = 0; j <= i; ++j) {
-      float a = 0.f;
-      for (int c = 0; c < dh; ++c) a = fmaf(q[i * 33 + c], k[j * 33 + c], a);
-      sv[j] = a * sc;
-      mx = fmaxf(mx, sv[j]);
-    }
-    float sum = 0.f;
-    for (int j = 0; j <= i; ++j) {
-      sv[j] = expf(sv[j] - mx);
-      sum += sv[j];
-    }
-    const float inv = 1.0f / sum;
-    for (int j = 0; j < L; ++j) prow[i * L + j] = j <= i ? sv[j] * inv : 0.f;
-    for (int c = 0; c < dh; ++c) {
-      float a = 0.f;
-      for (int j = 0; j <= i; ++j) a = fmaf(sv[j] * inv, v[j * 33 + c], a);
-      orow[(int64_t)i * d + c] = a;
-    }
+// one CTA per (client, sentence), one warp per head, lane i = query position i
+// (L <= 32, dh <= 32, H <= 16): the sentence's [L, 3d] qkv block is staged in shared
+// memory with coalesced loads (row stride 3d + 1: conflict-free per-lane rows); the
+// per-row score / probability vectors live in registers (fully unrolled over 32
+// positions, predicated by the causal bound)
+__device__ __forceinline__ void stage_rows(float* dst, int ldd, const float* src, int64_t lds, int rows, int cols) {
+  for (int e = threadIdx.x; e < rows * cols; e += blockDim.x) {
+    const int r = e / cols, c = e - r * cols;
+    dst[r * ldd + c] = src[(int64_t)r * lds + c];
   }
 }
 
-__global__ void __launch_bounds__(32 * kAttWarps) attn_bwd_kernel(const float* __restrict__ qkv,
-                                                                  const float* __restrict__ P,
-                                                                  const float* __restrict__ dout, int B, int L, int H,
-                                                                  int dh, const int32_t* __restrict__ active,
-                                                                  float* __restrict__ dqkv) {
-  extern __shared__ float sh[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int w = blockIdx.y, unit = blockIdx.x * kAttWarps + warp;
-  if (unit >= B * H || !active[w]) return;
-  const int s = unit / H, h = unit - s * H;
-  const int d = H * dh;
-  float* q = sh + warp * 5 * 32 * 33;
-  float* k = q + 32 * 33;
-  float* v = k + 32 * 33;
-  float* dO = v + 32 * 33;
-  float* dS = dO + 32 * 33;
-  const float* base = qkv + ((int64_t)w * B * L + (int64_t)s * L) * 3 * d;
-  const float* dbase = dout + ((int64_t)w * B * L + (int64_t)s * L) * d + h * dh;
-  for (int e = lane; e < L * dh; e += 32) {
-    const int i = e / dh, c = e - i * dh;
-    q[i * 33 + c] = base[(int64_t)i * 3 * d + h * dh + c];
-    k[i * 33 + c] = base[(int64_t)i * 3 * d + d + h * dh + c];
-    v[i * 33 + c] = base[(int64_t)i * 3 * d + 2 * d + h * dh + c];
-    dO[i * 33 + c] = dbase[(int64_t)i * d + c];
-  }
-  const float* prow = P + ((((int64_t)w * B + s) * H + h) * L) * L;
+__global__ void __launch_bounds__(512) attn_fwd_kernel(const float* __restrict__ qkv, int B, int L, int H, int dh,
+                                                       const int32_t* __restrict__ active, float* __restrict__ P,
+                                                       float* __restrict__ o) {
+  extern __shared__ float sh[];  // [L][3d + 1]
+  const int w = blockIdx.y, s = blockIdx.x;
+  if (!active[w]) return;
+  const int d = H * dh, ld = 3 * d + 1;
+  stage_rows(sh, ld, qkv + ((int64_t)w * B * L + (int64_t)s * L) * 3 * d, 3 * d, L, 3 * d);
+  __syncthreads();
+  const int h = threadIdx.x >> 5, i = threadIdx.x & 31;
+  if (h >= H || i >= L) return;
+  const float* q = sh + i * ld + h * dh;
   const float sc = 1.0f / sqrtf((float)dh);
-  __syncwarp();
-  if (lane < L) {  // row i: dS_ij = P_ij (dP_ij - sum_j P_ij dP_ij) / sqrt(dh)
-    const int i = lane;
-    float dp[32];
-    float rs = 0.f;
-    for (int j = 0; j <= i; ++j) {
+  float sv[32];
+  float mx = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    sv[j] = -INFINITY;
+    if (j <= i) {
+      const float* kj = sh + j * ld + d + h * dh;
       float a = 0.f;
-      for (int c = 0; c < dh; ++c) a = fmaf(dO[i * 33 + c], v[j * 33 + c], a);
-      dp[j] = a;
-      rs = fmaf(prow[i * L + j], a, rs);
+      for (int c = 0; c < dh; ++c) a = fmaf(q[c], kj[c], a);
+      sv[j] = a * sc;
+      mx = fmaxf(mx, sv[j]);
     }
-    for (int j = 0; j < L; ++j) dS[i * 33 + j] = j <= i ? prow[i * L + j] * (dp[j] - rs) * sc : 0.f;
+  }
+  float sum = 0.f;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    sv[j] = j <= i ? expf(sv[j] - mx) : 0.f;
+    sum += sv[j];
+  }
+  const float inv = 1.0f / sum;
+  float* prow = P + ((((int64_t)w * B + s) * H + h) * L + i) * L;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    sv[j] *= inv;
+    if (j < L) prow[j] = sv[j];
+  }
+  float* orow = o + ((int64_t)w * B * L + (int64_t)s * L + i) * d + h * dh;
+  for (int c = 0; c < dh; ++c) {
+    float a = 0.f;
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j <= i) a = fmaf(sv[j], sh[j * ld + 2 * d + h * dh + c], a);
+    orow[c] = a;
+  }
+}
+
+__global__ void __launch_bounds__(512) attn_bwd_kernel(const float* __restrict__ qkv, const float* __restrict__ P,
+                                                       const float* __restrict__ dout, int B, int L, int H, int dh,
+                                                       const int32_t* __restrict__ active, float* __restrict__ dqkv) {
+  extern __shared__ float sh[];  // qkv [L][3d + 1] | dO [L][d + 1] | dS [H][L][33]
+  const int w = blockIdx.y, s = blockIdx.x;
+  if (!active[w]) return;
+  const int d = H * dh, ld = 3 * d + 1, ldo = d + 1;
+  float* dO = sh + L * ld;
+  float* dSall = dO + L * ldo;
+  const int64_t row0 = (int64_t)w * B * L + (int64_t)s * L;
+  stage_rows(sh, ld, qkv + row0 * 3 * d, 3 * d, L, 3 * d);
+  stage_rows(dO, ldo, dout + row0 * d, d, L, d);
+  __syncthreads();
+  const int h = threadIdx.x >> 5, i = threadIdx.x & 31;
+  if (h >= H) return;
+  float* dS = dSall + h * L * 33;
+  const float* pbase = P + (((int64_t)w * B + s) * H + h) * L * L;
+  const float sc = 1.0f / sqrtf((float)dh);
+  if (i < L) {  // row i: dS_ij = P_ij (dP_ij - sum_j P_ij dP_ij) / sqrt(dh)
+    const float* doi = dO + i * ldo + h * dh;
+    float dp[32], pr[32];
+    float rs = 0.f;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      dp[j] = 0.f;
+      pr[j] = 0.f;
+      if (j <= i) {
+        const float* vj = sh + j * ld + 2 * d + h * dh;
+        float a = 0.f;
+        for (int c = 0; c < dh; ++c) a = fmaf(doi[c], vj[c], a);
+        dp[j] = a;
+        pr[j] = pbase[i * L + j];
+        rs = fmaf(pr[j], a, rs);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < L) dS[i * 33 + j] = j <= i ? pr[j] * (dp[j] - rs) * sc : 0.f;
   }
   __syncwarp();
-  float* dq = dqkv + ((int64_t)w * B * L + (int64_t)s * L) * 3 * d + h * dh;
-  if (lane < L) {
-    const int i = lane;  // dq_i = sum_j dS_ij k_j ; dk_i = sum_r dS_ri q_r ; dv_i = sum_r P_ri dO_r
-    for (int c = 0; c < dh; ++c) {
-      float aq = 0.f, ak = 0.f, av = 0.f;
-      for (int j = 0; j <= i; ++j) aq = fmaf(dS[i * 33 + j], k[j * 33 + c], aq);
-      for (int r = i; r < L; ++r) {
-        ak = fmaf(dS[r * 33 + i], q[r * 33 + c], ak);
-        av = fmaf(prow[r * L + i], dO[r * 33 + c], av);
-      }
-      dq[(int64_t)i * 3 * d + c] = aq;
-      dq[(int64_t)i * 3 * d + d + c] = ak;
-      dq[(int64_t)i * 3 * d + 2 * d + c] = av;
+  if (i >= L) return;
+  float* dq = dqkv + (row0 + i) * 3 * d + h * dh;
+  for (int c = 0; c < dh; ++c) {  // dq_i = sum_j dS_ij k_j ; dk_i = sum_r dS_ri q_r ; dv_i = sum_r P_ri dO_r
+    float aq = 0.f, ak = 0.f, av = 0.f;
+    for (int j = 0; j <= i; ++j) aq = fmaf(dS[i * 33 + j], sh[j * ld + d + h * dh + c], aq);
+    for (int r = i; r < L; ++r) {
+      ak = fmaf(dS[r * 33 + i], sh[r * ld + h * dh + c], ak);
+      av = fmaf(pbase[r * L + i], dO[r * ldo + h * dh + c], av);
     }
+    dq[c] = aq;
+    dq[d + c] = ak;
+    dq[2 * d + c] = av;
   }
 }
 
@@ -1257,9 +1264,8 @@ int forward(const Dims& m, const Work& k, const float* Wc, int64_t sW, int W, in
     g.active = k.active;
     if ((st = launch_gemm(false, true, g, W, s))) return st;
     FB_LAUNCH("lm_attn_fwd_kernel", s,
-              (attn_fwd_kernel<<<dim3((B * m.H + kAttWarps - 1) / kAttWarps, W), 32 * kAttWarps,
-                                 kAttWarps * 3 * 32 * 33 * sizeof(float), s>>>(y.qkv, B, m.L, m.H, m.dh, k.active,
-                                                                              y.P, y.o)));
+              (attn_fwd_kernel<<<dim3(B, W), 32 * m.H, m.L * (3 * d + 1) * sizeof(float), s>>>(
+                  y.qkv, B, m.L, m.H, m.dh, k.active, y.P, y.o)));
     g = gemm_base();  // a = o Wo^T + bo
     g.A = y.o; g.lda = d; g.sA = (int64_t)T * d;
     g.B = P + lo.out_w; g.ldb = d; g.sB = sW;
@@ -1387,10 +1393,16 @@ int backward(const Dims& m, const Work& k, int64_t sW, int W, int B, cudaStream_
     g.M = T; g.N = d; g.K = d;
     g.active = k.nvalid;
     if ((st = launch_gemm(false, false, g, W, s))) return st;
+    static bool att_attr = false;
+    if (!att_attr) {  // (the backward stages qkv, dO and per-head dS: > 48 KB at config C)
+      cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      att_attr = true;
+    }
     FB_LAUNCH("lm_attn_bwd_kernel", s,
-              (attn_bwd_kernel<<<dim3((B * m.H + kAttWarps - 1) / kAttWarps, W), 32 * kAttWarps,
-                                 kAttWarps * 5 * 32 * 33 * sizeof(float), s>>>(y.qkv, y.P, k.dtmp, B, m.L, m.H, m.dh,
-                                                                              k.nvalid, k.dqkv)));
+              (attn_bwd_kernel<<<dim3(B, W), 32 * m.H,
+                                 (m.L * (3 * d + 1) + m.L * (d + 1) + m.H * m.L * 33) * sizeof(float), s>>>(
+                  y.qkv, y.P, k.dtmp, B, m.L, m.H, m.dh, k.nvalid, k.dqkv)));
     g = gemm_base();  // dWqkv = dqkv^T x
     g.A = k.dqkv; g.lda = 3 * d; g.sA = (int64_t)T * 3 * d;
     g.B = y.xin; g.ldb = d; g.sB = (int64_t)T * d;
@@ -1414,8 +1426,9 @@ int backward(const Dims& m, const Work& k, int64_t sW, int W, int B, cudaStream_
 }
 
 bool dims_ok(const Dims& m) {
-  return m.V >= 2 && m.d >= 1 && m.d <= 256 && m.H >= 1 && m.d % m.H == 0 && m.dh <= 32 && m.F >= 1 &&
-         m.layers >= 1 && m.L >= 1 && m.L <= 32;
+  const size_t att = (size_t)(m.L * (3 * m.d + 1) + m.L * (m.d + 1) + m.H * m.L * 33) * sizeof(float);
+  return m.V >= 2 && m.d >= 1 && m.d <= 256 && m.H >= 1 && m.H <= 16 && m.d % m.H == 0 && m.dh <= 32 &&
+         m.F >= 1 && m.layers >= 1 && m.L >= 1 && m.L <= 32 && att <= 200 * 1024;
 }
 
 Dims parse(const int32_t* dims) {
