@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(kT, 1) clip_aggregate_fused_kernel(const Args 
   __shared__ uint32_t tmem_base;
   __shared__ double red[2][kGroup / 32];  // norm partials per warp, double-buffered by client parity
   __shared__ float s_cf;
-  __shared__ volatile int acc_done;        // clients fully accumulated by this CTA
+  __shared__ int acc_done;                 // clients fully accumulated by this CTA (atomic access)
 
   const int G = gridDim.x, b = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(kT, 1) clip_aggregate_fused_kernel(const Args 
       tc::mbar_init(&acc_empty[s], kGroup / 32);
     }
     tc::fence_mbar_init();
-    acc_done = 0;
+    atomicExch(&acc_done, 0);
   }
   if (warp == 0) tc::tmem_alloc<512>(&tmem_base);
   tc::tc_fence_before();
@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(kT, 1) clip_aggregate_fused_kernel(const Args 
     for (int k = 0; k < a.C; ++k) {
       if (k > a.lead) {
         const long long t0 = clock64();
-        while (acc_done < k - a.lead) {
+        while (atomicAdd(&acc_done, 0) < k - a.lead) {
           __nanosleep(32);
           if (clock64() - t0 > kSpinLimit) __trap();  // a lost peer must fail loudly, never hang
         }
@@ -268,6 +268,7 @@ __global__ void __launch_bounds__(kT, 1) clip_aggregate_fused_kernel(const Args 
             ss1 += sq4(mask_tail(st[r * (kRowF / 4) + kGroup + gt], colB + ro, a.D));
           }
         }
+        tc::fence_proxy_async();  // (generic reads of the slot ordered before the next bulk write)
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&norm_empty[slot]);
       }
@@ -418,6 +419,7 @@ __global__ void __launch_bounds__(kT, 1) clip_aggregate_fused_kernel(const Args 
             }
           }
         }
+        tc::fence_proxy_async();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&acc_empty[slot]);
       }
@@ -425,7 +427,7 @@ __global__ void __launch_bounds__(kT, 1) clip_aggregate_fused_kernel(const Args 
       // clients 0..k accumulated: flush a full fp32 block into the fp64 accumulator
       if (((k + 1) % kFlush) == 0 && k + 1 < a.C) flush_or_emit(false, k + 1 == kFlush);
       bar_group(2);  // (all of this group is done with client k and with s_cf)
-      if (gt == 0) acc_done = k + 1;
+      if (gt == 0) atomicExch(&acc_done, k + 1);
     }
     // epilogue: agg (+)= fp64 block sum + the open fp32 block
     flush_or_emit(true, false);
