@@ -874,21 +874,36 @@ __global__ void ln_bwd_kernel(const float* __restrict__ dout, const float* __res
   }
 }
 
-// G_w[col] = sum_r in1[w, r, col] (* in2[w, r, col]), rows in order (deterministic)
-__global__ void colsum_kernel(const float* __restrict__ in1, const float* __restrict__ in2, int rows, int cols,
-                              const int32_t* __restrict__ active, float* __restrict__ G, int64_t sG) {
+// G_w[col] = sum_r in1[w, r, col] (* in2[w, r, col]): CTA = 32 columns x 8 warps, warp u
+// sums rows u, u + 8, ... in order and the 8 partials are added in warp order (fixed, so
+// deterministic; 8 independent load streams per column instead of one serial one)
+constexpr int kCsWarps = 8;
+__global__ void __launch_bounds__(32 * kCsWarps) colsum_kernel(const float* __restrict__ in1,
+                                                               const float* __restrict__ in2, int rows, int cols,
+                                                               const int32_t* __restrict__ active,
+                                                               float* __restrict__ G, int64_t sG) {
+  __shared__ float part[kCsWarps][33];
   const int w = blockIdx.y;
   if (!active[w]) return;
-  const int col = blockIdx.x * blockDim.x + threadIdx.x;
-  if (col >= cols) return;
-  const int64_t base = (int64_t)w * rows * cols + col;
+  const int lane = threadIdx.x & 31, u = threadIdx.x >> 5;
+  const int col = blockIdx.x * 32 + lane;
   float s = 0.f;
-  if (in2) {
-    for (int r = 0; r < rows; ++r) s = fmaf(in1[base + (int64_t)r * cols], in2[base + (int64_t)r * cols], s);
-  } else {
-    for (int r = 0; r < rows; ++r) s += in1[base + (int64_t)r * cols];
+  if (col < cols) {
+    const int64_t base = (int64_t)w * rows * cols + col;
+    if (in2) {
+      for (int r = u; r < rows; r += kCsWarps) s = fmaf(in1[base + (int64_t)r * cols], in2[base + (int64_t)r * cols], s);
+    } else {
+      for (int r = u; r < rows; r += kCsWarps) s += in1[base + (int64_t)r * cols];
+    }
   }
-  G[(int64_t)w * sG + col] = s;
+  part[u][lane] = s;
+  __syncthreads();
+  if (u == 0 && col < cols) {
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < kCsWarps; ++i) t += part[i][lane];
+    G[(int64_t)w * sG + col] = t;
+  }
 }
 
 // ------------------------------------------------------------ softmax-CE
@@ -1329,15 +1344,16 @@ int backward(const Dims& m, const Work& k, int64_t sW, int W, int B, cudaStream_
   g.active = k.nvalid;
   if ((st = launch_gemm(false, false, g, W, s))) return st;
   const dim3 lngrid((T + 7) / 8, W);
-  const dim3 cs_d((d + 127) / 128, W), cs_3d((3 * d + 127) / 128, W), cs_F((m.F + 127) / 128, W);
+  const dim3 cs_d((d + 31) / 32, W), cs_3d((3 * d + 31) / 32, W), cs_F((m.F + 31) / 32, W);
+  constexpr int CS = 32 * kCsWarps;
   for (int l = m.layers - 1; l >= 0; --l) {
     const Layer& y = k.layer[l];
     const int64_t pb = layer_base(m, l);
     const float* P = k.Wc + pb;
     float* Gl = k.G + pb;
     // LayerNorm 2: gains / biases, then into x1
-    FB_LAUNCH("lm_colsum_kernel", s, (colsum_kernel<<<cs_d, 128, 0, s>>>(k.dx, y.xh2, T, d, k.nvalid, Gl + lo.n2_w, sW)));
-    FB_LAUNCH("lm_colsum_kernel", s, (colsum_kernel<<<cs_d, 128, 0, s>>>(k.dx, nullptr, T, d, k.nvalid, Gl + lo.n2_b, sW)));
+    FB_LAUNCH("lm_colsum_kernel", s, (colsum_kernel<<<cs_d, CS, 0, s>>>(k.dx, y.xh2, T, d, k.nvalid, Gl + lo.n2_w, sW)));
+    FB_LAUNCH("lm_colsum_kernel", s, (colsum_kernel<<<cs_d, CS, 0, s>>>(k.dx, nullptr, T, d, k.nvalid, Gl + lo.n2_b, sW)));
     FB_LAUNCH("lm_ln_bwd_kernel", s, (ln_bwd_kernel<<<lngrid, 256, 0, s>>>(k.dx, y.xh2, y.r2, P + lo.n2_w, sW, T, d,
                                                                            k.nvalid, k.dx1)));
     // feed-forward
@@ -1348,7 +1364,7 @@ int backward(const Dims& m, const Work& k, int64_t sW, int W, int B, cudaStream_
     g.M = d; g.N = m.F; g.K = T;
     g.active = k.nvalid;
     if ((st = launch_gemm(true, false, g, W, s))) return st;
-    FB_LAUNCH("lm_colsum_kernel", s, (colsum_kernel<<<cs_d, 128, 0, s>>>(k.dx1, nullptr, T, d, k.nvalid, Gl + lo.l2_b, sW)));
+    FB_LAUNCH("lm_colsum_kernel", s, (colsum_kernel<<<cs_d, CS, 0, s>>>(k.dx1, nullptr, T, d, k.nvalid, Gl + lo.l2_b, sW)));
     g = gemm_base();  // dz = (dx1 W2) * (z > 0)
     g.A = k.dx1; g.lda = d; g.sA = (int64_t)T * d;
     g.B = P + lo.l2_w; g.ldb = m.F; g.sB = sW;
@@ -1364,7 +1380,7 @@ int backward(const Dims& m, const Work& k, int64_t sW, int W, int B, cudaStream_
     g.M = m.F; g.N = d; g.K = T;
     g.active = k.nvalid;
     if ((st = launch_gemm(true, false, g, W, s))) return st;
-    FB_LAUNCH("lm_colsum_kernel", s, (colsum_kernel<<<cs_F, 128, 0, s>>>(k.dz, nullptr, T, m.F, k.nvalid, Gl + lo.l1_b, sW)));
+    FB_LAUNCH("lm_colsum_kernel", s, (colsum_kernel<<<cs_F, CS, 0, s>>>(k.dz, nullptr, T, m.F, k.nvalid, Gl + lo.l1_b, sW)));
     g = gemm_base();  // dx1 += dz W1
     g.A = k.dz; g.lda = m.F; g.sA = (int64_t)T * m.F;
     g.B = P + lo.l1_w; g.ldb = d; g.sB = sW;
@@ -1374,8 +1390,8 @@ int backward(const Dims& m, const Work& k, int64_t sW, int W, int B, cudaStream_
     g.active = k.nvalid;
     if ((st = launch_gemm(false, false, g, W, s))) return st;
     // LayerNorm 1: gains / biases, then into x and the attention output a
-    FB_LAUNCH("lm_colsum_kernel", s, (colsum_kernel<<<cs_d, 128, 0, s>>>(k.dx1, y.xh1, T, d, k.nvalid, Gl + lo.n1_w, sW)));
-    FB_LAUNCH("lm_colsum_kernel", s, (colsum_kernel<<<cs_d, 128, 0, s>>>(k.dx1, nullptr, T, d, k.nvalid, Gl + lo.n1_b, sW)));
+    FB_LAUNCH("lm_colsum_kernel", s, (colsum_kernel<<<cs_d, CS, 0, s>>>(k.dx1, y.xh1, T, d, k.nvalid, Gl + lo.n1_w, sW)));
+    FB_LAUNCH("lm_colsum_kernel", s, (colsum_kernel<<<cs_d, CS, 0, s>>>(k.dx1, nullptr, T, d, k.nvalid, Gl + lo.n1_b, sW)));
     FB_LAUNCH("lm_ln_bwd_kernel", s, (ln_bwd_kernel<<<lngrid, 256, 0, s>>>(k.dx1, y.xh1, y.r1, P + lo.n1_w, sW, T, d,
                                                                            k.nvalid, k.dx)));  // dy1 -> dx
     g = gemm_base();  // dWo = dy1^T o
@@ -1385,7 +1401,7 @@ int backward(const Dims& m, const Work& k, int64_t sW, int W, int B, cudaStream_
     g.M = d; g.N = d; g.K = T;
     g.active = k.nvalid;
     if ((st = launch_gemm(true, false, g, W, s))) return st;
-    FB_LAUNCH("lm_colsum_kernel", s, (colsum_kernel<<<cs_d, 128, 0, s>>>(k.dx, nullptr, T, d, k.nvalid, Gl + lo.out_b, sW)));
+    FB_LAUNCH("lm_colsum_kernel", s, (colsum_kernel<<<cs_d, CS, 0, s>>>(k.dx, nullptr, T, d, k.nvalid, Gl + lo.out_b, sW)));
     g = gemm_base();  // do = dy1 Wo
     g.A = k.dx; g.lda = d; g.sA = (int64_t)T * d;
     g.B = P + lo.out_w; g.ldb = d; g.sB = sW;
@@ -1410,7 +1426,7 @@ int backward(const Dims& m, const Work& k, int64_t sW, int W, int B, cudaStream_
     g.M = 3 * d; g.N = d; g.K = T;
     g.active = k.nvalid;
     if ((st = launch_gemm(true, false, g, W, s))) return st;
-    FB_LAUNCH("lm_colsum_kernel", s, (colsum_kernel<<<cs_3d, 128, 0, s>>>(k.dqkv, nullptr, T, 3 * d, k.nvalid,
+    FB_LAUNCH("lm_colsum_kernel", s, (colsum_kernel<<<cs_3d, CS, 0, s>>>(k.dqkv, nullptr, T, 3 * d, k.nvalid,
                                                                           Gl + lo.in_b, sW)));
     g = gemm_base();  // dx (= dy1, the residual) += dqkv Wqkv
     g.A = k.dqkv; g.lda = 3 * d; g.sA = (int64_t)T * 3 * d;
