@@ -331,7 +331,8 @@ __global__ void __launch_bounds__(GT) gemm_big_kernel(const Gemm g) {
 constexpr int TCM = 128;                 // M tile (UMMA M)
 constexpr int TCK = 32;                  // K slice per stage = one 128-byte swizzle row
 constexpr int TC_CONV = 4;               // converter warps
-constexpr int TC_THREADS = 32 * (2 + TC_CONV + 4);
+constexpr int TC_EPI = 8;                // epilogue warps: 2 per TMEM lane quarter, half the columns each
+constexpr int TC_THREADS = 32 * (2 + TC_CONV + TC_EPI);
 constexpr int TC_WIN = 2;                // K slices per TMEM window
 
 template <bool TA, bool TB, int BNT>
@@ -429,7 +430,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
     }
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&tfull[i], 1);
-      tc::mbar_init(&tempty[i], 4);
+      tc::mbar_init(&tempty[i], TC_EPI);
     }
     tc::fence_mbar_init();
   }
@@ -528,26 +529,29 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
     }
   } else {
     // --------------------------------------------------------------- epilogue
-    const int q = warp & 3;
+    // warp e = warp - 6: TMEM lane quarter warp % 4, column half e / 4
+    constexpr int EH = BNT / 2;
+    const int q = warp & 3, half = (warp - 2 - TC_CONV) >> 2;
     int w = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
       int z, m0, n0;
       if (!geom(tile, z, m0, n0)) continue;
       const int m = m0 + q * 32 + lane;
-      float sum[BNT];
+      n0 += half * EH;  // this warp's columns
+      float sum[EH];
 #pragma unroll
-      for (int j = 0; j < BNT; ++j) sum[j] = 0.f;
+      for (int j = 0; j < EH; ++j) sum[j] = 0.f;
       for (int wi = 0; wi < nwin; ++wi, ++w) {
         const int buf = w & 1;
         tc::mbar_wait(&tfull[buf], (w >> 1) & 1);
         tc::tc_fence_after();
 #pragma unroll
-        for (int c0 = 0; c0 < BNT; c0 += 32) {
-          uint32_t v[32];
-          tc::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + buf * BNT + c0, v);
+        for (int c0 = 0; c0 < EH; c0 += 16) {
+          uint32_t v[16];
+          tc::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + buf * BNT + half * EH + c0, v);
           tc::tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) sum[c0 + j] += __uint_as_float(v[j]);
+          for (int j = 0; j < 16; ++j) sum[c0 + j] += __uint_as_float(v[j]);
         }
         tc::tc_fence_before();
         __syncwarp();
@@ -559,7 +563,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         const float* arow = g.aux ? g.aux + (int64_t)z * g.sAux + (int64_t)m * g.ldaux : nullptr;
         const bool v4 = ((g.ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(crow) & 15) == 0);
 #pragma unroll
-        for (int j0 = 0; j0 < BNT; j0 += 4) {
+        for (int j0 = 0; j0 < EH; j0 += 4) {
           const int n = n0 + j0;
           float x[4];
 #pragma unroll
