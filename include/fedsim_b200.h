@@ -143,10 +143,15 @@ int64_t fb_cnn_workspace_bytes(int max_slots, int max_clients, int hist_steps);
  * measured slower); 0 = the FP32 CUDA-core kernels kept as an independent
  * check.                                                                    */
 int fb_cnn_set_conv_impl(int impl);
+/* perms / perm_off nullable: when given, client c's evaluated rows are epoch 0's
+ * perms[perm_off[c] + min(skip, n_c) ..] (the rows past the first local batch, whose
+ * theta_t loss / hits fb_local_sgd_cnn_f32 adds through eval_loss / eval_correct) and
+ * total_rows counts only those.                                                   */
 int fb_eval_cnn_f32(const float* theta, const float* X, const int32_t* y,
                     const int64_t* row_start, const int32_t* num_rows, int num_clients,
                     int64_t total_rows, double* loss_sum, int32_t* correct,
-                    int max_slots, void* workspace, int64_t workspace_bytes, void* stream);
+                    int max_slots, void* workspace, int64_t workspace_bytes,
+                    const int32_t* perms, const int64_t* perm_off, int skip, void* stream);
 int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
                          const int64_t* row_start, const int32_t* num_rows,
                          const int32_t* perms, const int64_t* perm_off, int num_clients,
@@ -156,7 +161,9 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
                          double* fc1_sumsq, const float* control /* nullable [C, ld_control]: c - c_i */,
                          int64_t ld_control,
                          const int32_t* h_client_steps /* nullable HOST [C]: local steps per client */,
-                         int fc1_store, void* stream);
+                         int fc1_store,
+                         double* eval_loss /* nullable [C]: += the first batch's theta_t loss */,
+                         int32_t* eval_correct /* nullable [C]: += its first-argmax hits */, void* stream);
 /* fc1_store = 0 (factored tcgen05 form, one wave of clients, fc1_sumsq set):
  * the clients' fc1 weight-delta blocks [O_F1, O_BF1) are NOT materialised --
  * fc1_sumsq still receives their sums of squares (for the clip norms) and

@@ -35,14 +35,23 @@ def _eval_slots(total_rows: int) -> int:
     return (n + EVAL_GROUP - 1) // EVAL_GROUP * EVAL_GROUP
 
 
-def eval_cohort(runner, theta, pop, row_start, num_rows, C, loss, correct, stream, h_num_rows):
-    total = int(np.asarray(h_num_rows, dtype=np.int64).sum())
-    slots = _eval_slots(total)
+def eval_cohort(runner, theta, pop, row_start, num_rows, C, loss, correct, stream, h_num_rows, skip_first=None):
+    """``skip_first=(perms, perm_off, B)``: evaluate only epoch 0's rows past each client's
+    first batch of B -- the local-SGD call that follows evaluates that batch at theta_t in its
+    first step (its forward IS the evaluation) and adds it to ``loss`` / ``correct``."""
+    n = np.asarray(h_num_rows, dtype=np.int64)
+    if skip_first is not None:
+        perms, perm_off, B = skip_first
+        total = int((n - np.minimum(n, B)).sum())
+    else:
+        perms, perm_off, B = None, None, 0
+        total = int(n.sum())
+    slots = _eval_slots(max(total, 1))
     nbytes = native.call("fb_cnn_workspace_bytes", slots, C, 0)
     ws = runner.ws.get("cnn_ws", nbytes)
     native.call("fb_eval_cnn_f32", native.ptr(theta), native.ptr(pop.X), native.ptr(pop.y), native.ptr(row_start),
                 native.ptr(num_rows), C, total, native.ptr(loss), native.ptr(correct), slots, native.ptr(ws),
-                ws.numel(), stream)
+                ws.numel(), native.ptr(perms), native.ptr(perm_off), int(B), stream)
 
 
 # (row range of the fc1 weight block in the flat parameter vector: models.CNN.param_dims order)
@@ -50,7 +59,7 @@ FC1_LO, FC1_HI = 19392, 19392 + 12544 * 128
 
 
 def local_sgd_cohort(runner, theta, pop, row_start, num_rows, perms, perm_off, C, tp, prox_mu, delta, nonfinite,
-                     stream, h_num_rows, control=None, defer_fc1=False):
+                     stream, h_num_rows, control=None, defer_fc1=False, eval_out=None):
     """Returns the per-client fc1-block sum of squares (fp64 device [C]) when the
     factored tcgen05 path produced it, else None (K2 then scans the whole row).
     ``control`` ([C, ld] device, c - c_i per client; SCAFFOLD) selects the dense
@@ -80,7 +89,9 @@ def local_sgd_cohort(runner, theta, pop, row_start, num_rows, perms, perm_off, C
                 runner.ld, native.ptr(nonfinite), slots, hist, native.ptr(ws), ws.numel(),
                 native.ptr(sq) if sq is not None else None,
                 native.ptr(control) if control is not None else None,
-                control.stride(0) if control is not None else 0, steps.ctypes.data, 0 if defer else 1, stream)
+                control.stride(0) if control is not None else 0, steps.ctypes.data, 0 if defer else 1,
+                native.ptr(eval_out[0]) if eval_out is not None else None,
+                native.ptr(eval_out[1]) if eval_out is not None else None, stream)
     return sq
 
 

@@ -126,9 +126,14 @@ __global__ void train_slots_kernel(int step, const int64_t* __restrict__ row_sta
 }
 
 // evaluation chunk: cohort rows [r0, r0+N) -> (dataset row, client)
+// (perms != nullptr: client c's evaluated rows are perms[perm_off[c] + skip_c + j],
+//  skip_c = min(skip, n_c) -- epoch 0's order past the first batch, whose rows the first
+//  local-SGD step evaluates at theta_t)
 __global__ void eval_slots_kernel(int64_t r0, int N, int64_t total, const int64_t* __restrict__ prefix, int C,
                                   const int64_t* __restrict__ row_start, int64_t* __restrict__ slot_row,
-                                  int32_t* __restrict__ slot_client) {
+                                  int32_t* __restrict__ slot_client, const int32_t* __restrict__ perms,
+                                  const int64_t* __restrict__ perm_off, const int32_t* __restrict__ num_rows,
+                                  int skip) {
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= N) return;
   const int64_t r = r0 + n;
@@ -142,19 +147,37 @@ __global__ void eval_slots_kernel(int64_t r0, int N, int64_t total, const int64_
     const int mid = (lo + hi) >> 1;
     if (prefix[mid] <= r) lo = mid; else hi = mid;
   }
-  slot_row[n] = row_start[lo] + (r - prefix[lo]);
+  const int64_t j = r - prefix[lo];
+  slot_row[n] = perms ? row_start[lo] + perms[perm_off[lo] + min(skip, num_rows[lo]) + j] : row_start[lo] + j;
   slot_client[n] = lo;
 }
 
-__global__ void prefix_kernel(const int32_t* __restrict__ num_rows, int C, int64_t* __restrict__ prefix) {
+__global__ void prefix_kernel(const int32_t* __restrict__ num_rows, int C, int64_t* __restrict__ prefix, int skip) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     int64_t s = 0;
     for (int c = 0; c < C; ++c) {
       prefix[c] = s;
-      s += num_rows[c];
+      s += num_rows[c] - min(skip, num_rows[c]);
     }
     prefix[C] = s;
   }
+}
+
+// the first local step's batch slots (client c: slots c * B + b, b < nb[c]) add their
+// theta_t loss / hits to the client's evaluation sums (in slot order)
+__global__ void step0_eval_kernel(const double* __restrict__ slot_loss, const int32_t* __restrict__ slot_hit,
+                                  const int32_t* __restrict__ client_nb, int B, int Cw, double* __restrict__ loss,
+                                  int32_t* __restrict__ correct) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= Cw) return;
+  double sl = 0.0;
+  int h = 0;
+  for (int b = 0; b < client_nb[c]; ++b) {
+    sl += slot_loss[c * B + b];
+    h += slot_hit[c * B + b];
+  }
+  loss[c] += sl;
+  correct[c] += h;
 }
 
 // ------------------------------------------------------------ conv1 fwd
@@ -500,10 +523,11 @@ __global__ void __launch_bounds__(HID) head_kernel(const float* __restrict__ par
       if (row[q] > mx) { mx = row[q]; arg = q; }
     float s = 0.f;
     for (int q = 0; q < NCLS; ++q) s += expf(row[q] - mx);
-    if (!train) {
+    if (slot_loss) {  // evaluation, or the first local step (its forward is the eval at theta_t)
       slot_loss[n0 + j] = -((double)row[lab[j]] - (double)mx - (double)logf(s));
       slot_hit[n0 + j] = arg == lab[j];
-    } else {
+    }
+    if (train) {
       for (int q = 0; q < NCLS; ++q) {
         float p = expf(row[q] - mx) / s;
         if (q == lab[j]) p -= 1.f;
@@ -3942,7 +3966,8 @@ int64_t fb_cnn_workspace_bytes(int max_slots, int max_clients, int hist_steps) {
 
 int fb_eval_cnn_f32(const float* theta, const float* X, const int32_t* y, const int64_t* row_start,
                     const int32_t* num_rows, int num_clients, int64_t total_rows, double* loss_sum,
-                    int32_t* correct, int max_slots, void* workspace, int64_t workspace_bytes, void* stream) {
+                    int32_t* correct, int max_slots, void* workspace, int64_t workspace_bytes,
+                    const int32_t* perms, const int64_t* perm_off, int skip, void* stream) {
   FB_REQUIRE(num_clients >= 0 && total_rows >= 0 && max_slots >= GMAX, "eval_cnn: bad arguments");
   FB_REQUIRE(workspace_bytes >= carve(nullptr, max_slots, num_clients, 0, nullptr), "eval_cnn: workspace too small");
   if (num_clients == 0) return FB_OK;
@@ -3954,7 +3979,8 @@ int fb_eval_cnn_f32(const float* theta, const float* X, const int32_t* y, const 
   const int N = (max_slots / GMAX) * GMAX;
   cudaMemsetAsync(loss_sum, 0, sizeof(double) * num_clients, s);
   cudaMemsetAsync(correct, 0, sizeof(int32_t) * num_clients, s);
-  FB_LAUNCH("prefix_kernel", s, prefix_kernel<<<1, 1, 0, s>>>(num_rows, num_clients, w.prefix));
+  FB_REQUIRE(!perms || (perm_off && skip >= 0), "eval_cnn: perms need perm_off and skip >= 0");
+  FB_LAUNCH("prefix_kernel", s, prefix_kernel<<<1, 1, 0, s>>>(num_rows, num_clients, w.prefix, perms ? skip : 0));
   const bool tcf = fc1_tc(nullptr, false);
   if (tcf) {
     st = prep_theta_images(theta, w, s);
@@ -3962,7 +3988,7 @@ int fb_eval_cnn_f32(const float* theta, const float* X, const int32_t* y, const 
   }
   for (int64_t r0 = 0; r0 < total_rows; r0 += N) {
     FB_LAUNCH("eval_slots_kernel", s, eval_slots_kernel<<<(N + 255) / 256, 256, 0, s>>>(r0, N, total_rows, w.prefix, num_clients, row_start,
-                                                      w.slot_row, w.slot_client));
+                                                      w.slot_row, w.slot_client, perms, perm_off, num_rows, skip));
     st = forward(X, theta, nullptr, 0, 1, N, GMAX, w, s, nullptr);
     if (st) return st;
     FB_LAUNCH("head_kernel", s, head_kernel<<<N / GMAX, HID, 0, s>>>(w.part, w.slot_row, N, GMAX, y, theta, nullptr, 0, nullptr, Step{0, 0},
@@ -4003,7 +4029,8 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
                          int epochs, int batch_size, int max_steps, float lr, float prox_mu, float* delta_out,
                          int64_t ld_delta, int32_t* nonfinite, int max_slots, int hist_steps, void* workspace,
                          int64_t workspace_bytes, double* fc1_sumsq, const float* control, int64_t ld_control,
-                         const int32_t* h_client_steps, int fc1_store, void* stream) {
+                         const int32_t* h_client_steps, int fc1_store, double* eval_loss, int32_t* eval_correct,
+                         void* stream) {
   FB_REQUIRE(num_clients >= 0 && epochs >= 0 && batch_size >= 1 && max_steps >= 0 && hist_steps >= 0,
              "local_sgd_cnn: bad arguments");
   FB_REQUIRE(fc1_store || (hist_steps > 0 && fc1_sumsq && g_conv_impl == 1 && num_clients <= max_slots / batch_size),
@@ -4095,9 +4122,16 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
                                                     hs, B, w.gram_part));
         FB_LAUNCH("fc1_gram_reduce_kernel", s, fc1_gram_reduce_kernel<<<Cw, 256, 0, s>>>(hs, B, gks, w.gram_part));
       }
+      // step 0 runs at theta_t: its batch's loss / hits are those rows' evaluation (the caller
+      // evaluated only the rest, fb_eval_cnn_f32 with skip = batch_size)
+      const bool ev0 = step == 0 && eval_loss != nullptr;
       FB_LAUNCH("head_kernel", s, head_kernel<<<Cw, HID, 0, s>>>(ws.part, ws.slot_row, N, B, y, theta_t, dlt, ld_delta, ws.client_nb, sp, ws.dz3,
-                                     nullptr, nullptr, hs, tcf ? FT_FSPLIT : KSPLIT, tcf ? ws.dz3fh : nullptr,
-                                     ws.dz3fl, ws.dz3scale));
+                                     ev0 ? ws.slot_loss : nullptr, ev0 ? ws.slot_hit : nullptr, hs,
+                                     tcf ? FT_FSPLIT : KSPLIT, tcf ? ws.dz3fh : nullptr, ws.dz3fl, ws.dz3scale));
+      if (ev0)
+        FB_LAUNCH("step0_eval_kernel", s, step0_eval_kernel<<<(Cw + 127) / 128, 128, 0, s>>>(
+                                              ws.slot_loss, ws.slot_hit, ws.client_nb, B, Cw, eval_loss + c0,
+                                              eval_correct + c0));
       if (tcf) {
         CUtensorMap ah, al, bh, bl;
         st = tensor_map_2d_f16(&ah, ws.dz3fh, HID, N, FT_KS, 128);

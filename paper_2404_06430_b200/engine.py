@@ -115,6 +115,10 @@ def unpack_sums(tail: np.ndarray) -> np.ndarray:
 # roofline at D = 4 M, 0.37 vs 0.44 at 2 M).
 FUSED_CLIP_AGGREGATE_MIN_D = 3_000_000
 
+# CNN: evaluate each client's first local batch inside the first local-SGD step (same
+# forward at theta_t) instead of a second time in the evaluation pass
+SHARE_FIRST_BATCH_EVAL = True
+
 
 def fused_clip_aggregate(D: int, ld: int, deferred: bool) -> bool:
     return (not deferred and D >= FUSED_CLIP_AGGREGATE_MIN_D and ld % 4 == 0
@@ -233,9 +237,11 @@ class _ModelRunner:
         self.D = model.num_params
         self.ld = (self.D + 3) & ~3  # 16-byte aligned client rows
 
-    def eval(self, theta, pop: DevicePopulation, row_start, num_rows, C, loss, correct, stream, h_num_rows):
+    def eval(self, theta, pop: DevicePopulation, row_start, num_rows, C, loss, correct, stream, h_num_rows,
+             skip_first=None):
         if self.kind == "cnn":
-            return cnn.eval_cohort(self, theta, pop, row_start, num_rows, C, loss, correct, stream, h_num_rows)
+            return cnn.eval_cohort(self, theta, pop, row_start, num_rows, C, loss, correct, stream, h_num_rows,
+                                   skip_first=skip_first)
         if self.kind == "lm":
             return lm.eval_cohort(self, theta, pop, row_start, num_rows, C, loss, correct, stream, h_num_rows)
         fn = f"fb_eval_{self.kind}_f32"
@@ -244,11 +250,11 @@ class _ModelRunner:
                     stream)
 
     def local_sgd(self, theta, pop, row_start, num_rows, perms, perm_off, C, tp, prox_mu, delta, nonfinite, stream,
-                  h_num_rows, control=None, defer_fc1=False):
+                  h_num_rows, control=None, defer_fc1=False, eval_out=None):
         if self.kind == "cnn":  # returns the fc1-block sum of squares when the factored path made it
             return cnn.local_sgd_cohort(self, theta, pop, row_start, num_rows, perms, perm_off, C, tp,
                                         prox_mu, delta, nonfinite, stream, h_num_rows, control=control,
-                                        defer_fc1=defer_fc1)
+                                        defer_fc1=defer_fc1, eval_out=eval_out)
         if self.kind == "lm":
             return lm.local_sgd_cohort(self, theta, pop, row_start, num_rows, perms, perm_off, C, tp, prox_mu, delta,
                                        nonfinite, stream, h_num_rows, control=control)
@@ -693,8 +699,15 @@ class GpuSimulationEngine:
         norm = res[8 * Cp: 16 * Cp].view(torch.float64)
         ints = res[16 * Cp: 16 * Cp + 12 * Cp].view(torch.int32)
         correct, clipped, nonfinite = ints[:Cp], ints[Cp:2 * Cp], ints[2 * Cp:3 * Cp]
+        # CNN training contexts: the first local step runs at theta_t, so its forward IS the
+        # evaluation of the first batch (fedsim/algorithms/fedavg.py:165 evaluates every row at
+        # theta_t before training): evaluate only epoch 0's remaining rows here and let the
+        # local-SGD call add the first batch's loss / hits
+        share0 = bool(train and C and runner.kind == "cnn" and plan.train is not None
+                      and plan.train.num_epochs >= 1 and SHARE_FIRST_BATCH_EVAL)
         if C:
-            runner.eval(theta.flat, pop, d_row_start, d_num_rows, C, loss, correct, stream, num_rows)
+            runner.eval(theta.flat, pop, d_row_start, d_num_rows, C, loss, correct, stream, num_rows,
+                        skip_first=(dev[2], dev[3], plan.train.batch_size) if share0 else None)
         self._issue_prefetch()  # next iteration's rows: host work now overlaps the queued kernels
 
         agg_flat = None
@@ -720,7 +733,8 @@ class GpuSimulationEngine:
                                 store.ld, native.ptr(d_rows), C, runner.D, native.ptr(control), runner.ld, stream)
                 fc1_sq = runner.local_sgd(theta.flat, pop, d_row_start, d_num_rows, d_perms, d_perm_off, C,
                                           plan.train, plan.prox_mu, delta, nonfinite, stream, num_rows,
-                                          control=control, defer_fc1=self._factored_aggregate and not scaffold)
+                                          control=control, defer_fc1=self._factored_aggregate and not scaffold,
+                                          eval_out=(loss, correct) if share0 else None)
                 deferred = getattr(runner, "fc1_pending", None) is not None
                 payload, ldp = delta, runner.ld
                 if scaffold:

@@ -50,11 +50,11 @@ SIGNATURES: dict[str, tuple] = {
     "fb_upload_pinned": (_i32, [_p, _p, _i64, _p]),
     "fb_cnn_workspace_bytes": (_i64, [_i32, _i32, _i32]),
     "fb_cnn_set_conv_impl": (_i32, [_i32]),
-    "fb_eval_cnn_f32": (_i32, [_p, _p, _p, _p, _p, _i32, _i64, _p, _p, _i32, _p, _i64, _p]),
+    "fb_eval_cnn_f32": (_i32, [_p, _p, _p, _p, _p, _i32, _i64, _p, _p, _i32, _p, _i64, _p, _p, _i32, _p]),
     "fb_local_sgd_cnn_f32": (
         _i32,
         [_p, _p, _p, _p, _p, _p, _p, _i32, _i32, _i32, _i32, _f32, _f32, _p, _i64, _p, _i32, _i32, _p, _i64, _p, _p,
-         _i64, _p, _i32, _p],
+         _i64, _p, _i32, _p, _p, _p],
     ),
     "fb_cnn_fc1_aggregate_f32": (_i32, [_p, _i32, _i32, _i32, _f32, _f32, _i32, _i32, _p, _i64, _p, _p]),
     "fb_lm_set_gemm_impl": (_i32, [_i32]),
