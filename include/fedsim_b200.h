@@ -219,16 +219,20 @@ int64_t fb_lm_num_params(const int32_t* dims);
  * the SIMT FP32 tiled GEMM (validation).                                    */
 int fb_lm_set_gemm_impl(int impl);
 int64_t fb_lm_workspace_bytes(const int32_t* dims, int batch_size, int clients_per_wave, int eval_groups);
+/* perms / perm_off nullable, as in fb_eval_cnn_f32: when given, client c's evaluated
+ * sentences are epoch 0's perms[perm_off[c] + min(skip, n_c) ..], the first batch's
+ * theta_t loss / hits being added by fb_local_sgd_lm_f32 through eval_loss / eval_correct. */
 int fb_eval_lm_f32(const float* theta, const int32_t* dims, const float* X, const int64_t* row_start,
                    const int32_t* num_rows, const int32_t* h_num_rows, int num_clients, double* loss_sum,
                    int32_t* correct, int batch_size, int eval_groups, void* workspace, int64_t workspace_bytes,
-                   void* stream);
+                   const int32_t* perms, const int64_t* perm_off, int skip, void* stream);
 int fb_local_sgd_lm_f32(const float* theta_t, const int32_t* dims, const float* X, const int64_t* row_start,
                         const int32_t* num_rows, const int32_t* h_num_rows, const int32_t* perms,
                         const int64_t* perm_off, int num_clients, int epochs, int batch_size, float lr,
                         float prox_mu, const float* control, int64_t ld_control, float* delta_out, int64_t ld_delta,
                         int32_t* nonfinite, int clients_per_wave, void* workspace, int64_t workspace_bytes,
-                        void* stream);
+                        double* eval_loss /* nullable [C]: += the first batch's theta_t loss */,
+                        int32_t* eval_correct /* nullable [C] */, void* stream);
 
 /* ------------------------------------------------- a6 + a7 (kernel K2)
  * For every client c: norm[c] = || w[c] * delta[c, :D] ||_2 (fp64

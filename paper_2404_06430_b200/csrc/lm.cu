@@ -629,9 +629,13 @@ __global__ void gather_batch_kernel(const float* __restrict__ X, const int64_t* 
 }
 
 // eval chunk: sentences [g0, g0 + cnt) of the cohort in client-major order
+// (perms != nullptr: client c's evaluated sentences are epoch 0's perms[perm_off[c] + skip_c ..],
+//  skip_c = min(skip, n_c): the first local step evaluates the first batch)
 __global__ void gather_eval_kernel(const float* __restrict__ X, const int64_t* __restrict__ row_start,
                                    const int64_t* __restrict__ sent_off, int C, int64_t g0, int cnt, int L,
-                                   int32_t* __restrict__ tok) {
+                                   int32_t* __restrict__ tok, const int32_t* __restrict__ perms,
+                                   const int64_t* __restrict__ perm_off, const int32_t* __restrict__ num_rows,
+                                   int skip) {
   const int i = blockIdx.x;  // sentence slot
   int32_t* t = tok + (int64_t)i * (L + 1);
   if (i >= cnt) {
@@ -644,7 +648,8 @@ __global__ void gather_eval_kernel(const float* __restrict__ X, const int64_t* _
     const int mid = (lo + hi + 1) >> 1;
     if (sent_off[mid] <= g) lo = mid; else hi = mid - 1;
   }
-  const int64_t row = row_start[lo] + (g - sent_off[lo]);
+  const int64_t j = g - sent_off[lo];
+  const int64_t row = row_start[lo] + (perms ? perms[perm_off[lo] + min(skip, num_rows[lo]) + j] : j);
   for (int p = threadIdx.x; p <= L; p += blockDim.x) t[p] = (int)X[row * (L + 1) + p];
 }
 
@@ -932,7 +937,8 @@ __global__ void __launch_bounds__(kCeT) ce_kernel(float* __restrict__ logits, co
   if (tgt == 0) {
     if (kTrain) {
       for (int v = threadIdx.x; v < V; v += kCeT) z[v] = 0.f;
-    } else if (threadIdx.x == 0) {
+    }
+    if (row_loss && threadIdx.x == 0) {
       row_loss[(int64_t)w * B * L + r] = 0.f;
       row_hit[(int64_t)w * B * L + r] = 0;
     }
@@ -981,6 +987,13 @@ __global__ void __launch_bounds__(kCeT) ce_kernel(float* __restrict__ logits, co
   __syncthreads();
   se = red[0];
   if (kTrain) {
+    if (row_loss) {  // the first local step: its logits are the theta_t evaluation of the batch
+      if (threadIdx.x == 0) {
+        row_loss[(int64_t)w * B * L + r] = -(z[tgt] - mx - logf(se));
+        row_hit[(int64_t)w * B * L + r] = arg == tgt;
+      }
+      __syncthreads();  // (z[tgt] read before it is overwritten below)
+    }
     const float scale = 1.0f / (float)nvalid[w];
     const float inv = 1.0f / se;
     for (int v = threadIdx.x; v < V; v += kCeT) {
@@ -997,11 +1010,13 @@ __global__ void __launch_bounds__(kCeT) ce_kernel(float* __restrict__ logits, co
 // per-sentence (in position order) then per-client (in sentence order) eval sums
 __global__ void eval_accum_kernel(const float* __restrict__ row_loss, const int32_t* __restrict__ row_hit,
                                   const int64_t* __restrict__ sent_off, const int32_t* __restrict__ num_rows, int C,
-                                  int64_t g0, int cnt, int L, double* __restrict__ loss, int32_t* __restrict__ correct) {
+                                  int64_t g0, int cnt, int L, double* __restrict__ loss, int32_t* __restrict__ correct,
+                                  int skip) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= C) return;
+  const int64_t nc = num_rows[c] - min(skip, num_rows[c]);
   const int64_t lo = sent_off[c] > g0 ? sent_off[c] : g0;
-  const int64_t hi = sent_off[c] + num_rows[c] < g0 + cnt ? sent_off[c] + num_rows[c] : g0 + cnt;
+  const int64_t hi = sent_off[c] + nc < g0 + cnt ? sent_off[c] + nc : g0 + cnt;
   double s = 0.0;
   int k = 0;
   for (int64_t g = lo; g < hi; ++g) {
@@ -1017,6 +1032,27 @@ __global__ void eval_accum_kernel(const float* __restrict__ row_loss, const int3
     loss[c] += s;
     correct[c] += k;
   }
+}
+
+// the first local step's batch rows (client w of the wave: sentences s < B, in order) added
+// to the client's evaluation sums the same way eval_accum_kernel adds a chunk's
+__global__ void step0_eval_kernel(const float* __restrict__ row_loss, const int32_t* __restrict__ row_hit,
+                                  const int32_t* __restrict__ nvalid, int W, int B, int L,
+                                  double* __restrict__ loss, int32_t* __restrict__ correct) {
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= W || nvalid[w] == 0) return;
+  double sacc = 0.0;
+  int k = 0;
+  for (int s = 0; s < B; ++s) {
+    double sl = 0.0;
+    for (int p = 0; p < L; ++p) {
+      sl += (double)row_loss[((int64_t)w * B + s) * L + p];
+      k += row_hit[((int64_t)w * B + s) * L + p];
+    }
+    sacc += sl;
+  }
+  loss[w] += sacc;
+  correct[w] += k;
 }
 
 // -------------------------------------------------------------- SGD step
@@ -1070,12 +1106,12 @@ __global__ void ones_kernel(int32_t* p, int n) {
   if (i < n) p[i] = 1;
 }
 
-__global__ void sent_offsets_kernel(const int32_t* __restrict__ num_rows, int C, int64_t* __restrict__ off) {
+__global__ void sent_offsets_kernel(const int32_t* __restrict__ num_rows, int C, int64_t* __restrict__ off, int skip) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     int64_t s = 0;
     for (int c = 0; c < C; ++c) {
       off[c] = s;
-      s += num_rows[c];
+      s += num_rows[c] - min(skip, num_rows[c]);
     }
   }
 }
@@ -1327,12 +1363,13 @@ int forward(const Dims& m, const Work& k, const float* Wc, int64_t sW, int W, in
 // ------------------------------------------------------------- backward
 // gradient of the step's mean loss into G (every entry written once, then the
 // embedding scatter adds the input-side term)
-int backward(const Dims& m, const Work& k, int64_t sW, int W, int B, cudaStream_t s) {
+int backward(const Dims& m, const Work& k, int64_t sW, int W, int B, cudaStream_t s, bool eval_rows = false) {
   const int T = B * m.L, d = m.d;
   const LayerOff lo = layer_off(m);
   int st;
   FB_LAUNCH("lm_ce_kernel", s, (ce_kernel<true><<<dim3(T, W), kCeT, 0, s>>>(k.logits, k.tok, B, m.L, m.V, k.nvalid,
-                                                                            nullptr, nullptr)));
+                                                                            eval_rows ? k.rloss : nullptr,
+                                                                            eval_rows ? k.hit : nullptr)));
   Gemm g = gemm_base();  // dE = dlogits^T x
   g.A = k.logits; g.lda = m.V; g.sA = (int64_t)T * m.V;
   g.B = k.xf; g.ldb = d; g.sB = (int64_t)T * d;
@@ -1488,7 +1525,7 @@ int64_t fb_lm_workspace_bytes(const int32_t* dims, int batch_size, int clients_p
 int fb_eval_lm_f32(const float* theta, const int32_t* dims, const float* X, const int64_t* row_start,
                    const int32_t* num_rows, const int32_t* h_num_rows, int num_clients, double* loss_sum,
                    int32_t* correct, int batch_size, int eval_groups, void* workspace, int64_t workspace_bytes,
-                   void* stream) {
+                   const int32_t* perms, const int64_t* perm_off, int skip, void* stream) {
   FB_REQUIRE(dims != nullptr && h_num_rows != nullptr, "eval_lm: null dims / host row counts");
   const fb::lm::Dims m = fb::lm::parse(dims);
   FB_UNSUPPORTED(fb::lm::dims_ok(m), "eval_lm: unsupported shape (d <= 256, d %% heads == 0, head dim <= 32, seq <= 32)");
@@ -1505,21 +1542,24 @@ int fb_eval_lm_f32(const float* theta, const int32_t* dims, const float* X, cons
   const int W = eval_groups, B = batch_size, L = m.L;
   FB_LAUNCH("lm_positions_kernel", s, (fb::lm::positions_kernel<<<(L * m.d + 255) / 256, 256, 0, s>>>(k.pe, L, m.d)));
   FB_LAUNCH("lm_ones_kernel", s, (fb::lm::ones_kernel<<<(W + 255) / 256, 256, 0, s>>>(k.active, W)));
-  FB_LAUNCH("lm_sent_offsets_kernel", s, (fb::lm::sent_offsets_kernel<<<1, 32, 0, s>>>(num_rows, num_clients, k.sent_off)));
+  FB_REQUIRE(!perms || (perm_off && skip >= 0), "eval_lm: perms need perm_off and skip >= 0");
+  const int sk = perms ? skip : 0;
+  FB_LAUNCH("lm_sent_offsets_kernel", s, (fb::lm::sent_offsets_kernel<<<1, 32, 0, s>>>(num_rows, num_clients, k.sent_off, sk)));
   int64_t total = 0;
-  for (int c = 0; c < num_clients; ++c) total += h_num_rows[c];
+  for (int c = 0; c < num_clients; ++c) total += h_num_rows[c] - (sk < h_num_rows[c] ? sk : h_num_rows[c]);
   const int chunk = W * B;
   for (int64_t g0 = 0; g0 < total; g0 += chunk) {
     const int cnt = (int)(total - g0 < chunk ? total - g0 : chunk);
     FB_LAUNCH("lm_gather_eval_kernel", s, (fb::lm::gather_eval_kernel<<<chunk, 32, 0, s>>>(
-                                              X, row_start, k.sent_off, num_clients, g0, cnt, L, k.tok)));
+                                              X, row_start, k.sent_off, num_clients, g0, cnt, L, k.tok, perms,
+                                              perm_off, num_rows, sk)));
     int st = fb::lm::forward(m, k, theta, 0, W, B, s);
     if (st) return st;
     FB_LAUNCH("lm_ce_kernel", s, (fb::lm::ce_kernel<false><<<dim3(B * L, W), fb::lm::kCeT, 0, s>>>(
                                      k.logits, k.tok, B, L, m.V, nullptr, k.rloss, k.hit)));
     FB_LAUNCH("lm_eval_accum_kernel", s, (fb::lm::eval_accum_kernel<<<(num_clients + 127) / 128, 128, 0, s>>>(
                                              k.rloss, k.hit, k.sent_off, num_rows, num_clients, g0, cnt, L, loss_sum,
-                                             correct)));
+                                             correct, sk)));
   }
   return fb::launch_status("eval_lm");
 }
@@ -1529,7 +1569,7 @@ int fb_local_sgd_lm_f32(const float* theta_t, const int32_t* dims, const float* 
                         const int64_t* perm_off, int num_clients, int epochs, int batch_size, float lr,
                         float prox_mu, const float* control, int64_t ld_control, float* delta_out, int64_t ld_delta,
                         int32_t* nonfinite, int clients_per_wave, void* workspace, int64_t workspace_bytes,
-                        void* stream) {
+                        double* eval_loss, int32_t* eval_correct, void* stream) {
   FB_REQUIRE(dims != nullptr && h_num_rows != nullptr, "local_sgd_lm: null dims / host row counts");
   const fb::lm::Dims m = fb::lm::parse(dims);
   FB_UNSUPPORTED(fb::lm::dims_ok(m), "local_sgd_lm: unsupported shape (d <= 256, d %% heads == 0, head dim <= 32, seq <= 32)");
@@ -1564,8 +1604,12 @@ int fb_local_sgd_lm_f32(const float* theta_t, const int32_t* dims, const float* 
       k.active = k.nvalid;  // (nonzero = the client has a minibatch this step)
       int st = fb::lm::forward(m, k, k.Wc, sW, W, B, s);
       if (st) return st;
-      st = fb::lm::backward(m, k, sW, W, B, s);
+      const bool ev0 = step == 0 && eval_loss != nullptr;  // step 0 runs at theta_t: the batch's evaluation
+      st = fb::lm::backward(m, k, sW, W, B, s, ev0);
       if (st) return st;
+      if (ev0)
+        FB_LAUNCH("lm_step0_eval_kernel", s, (fb::lm::step0_eval_kernel<<<(W + 127) / 128, 128, 0, s>>>(
+                                                 k.rloss, k.hit, k.nvalid, W, B, L, eval_loss + c0, eval_correct + c0)));
       FB_LAUNCH("lm_sgd_kernel", s, (fb::lm::sgd_kernel<<<dim3(128, W), 256, 0, s>>>(
                                         k.Wc, k.G, sW, Dl, ld_delta,
                                         control ? control + (ld_control ? (int64_t)c0 * ld_control : 0) : nullptr,

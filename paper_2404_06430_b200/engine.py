@@ -243,7 +243,8 @@ class _ModelRunner:
             return cnn.eval_cohort(self, theta, pop, row_start, num_rows, C, loss, correct, stream, h_num_rows,
                                    skip_first=skip_first)
         if self.kind == "lm":
-            return lm.eval_cohort(self, theta, pop, row_start, num_rows, C, loss, correct, stream, h_num_rows)
+            return lm.eval_cohort(self, theta, pop, row_start, num_rows, C, loss, correct, stream, h_num_rows,
+                                  skip_first=skip_first)
         fn = f"fb_eval_{self.kind}_f32"
         native.call(fn, native.ptr(theta), *self.dims, native.ptr(pop.X), native.ptr(pop.y),
                     native.ptr(row_start), native.ptr(num_rows), C, native.ptr(loss), native.ptr(correct),
@@ -257,7 +258,7 @@ class _ModelRunner:
                                         defer_fc1=defer_fc1, eval_out=eval_out)
         if self.kind == "lm":
             return lm.local_sgd_cohort(self, theta, pop, row_start, num_rows, perms, perm_off, C, tp, prox_mu, delta,
-                                       nonfinite, stream, h_num_rows, control=control)
+                                       nonfinite, stream, h_num_rows, control=control, eval_out=eval_out)
         fn = f"fb_local_sgd_{self.kind}_f32"
         native.call(fn, native.ptr(theta), *self.dims, native.ptr(pop.X), native.ptr(pop.y),
                     native.ptr(row_start), native.ptr(num_rows), native.ptr(perms), native.ptr(perm_off), C,
@@ -699,11 +700,11 @@ class GpuSimulationEngine:
         norm = res[8 * Cp: 16 * Cp].view(torch.float64)
         ints = res[16 * Cp: 16 * Cp + 12 * Cp].view(torch.int32)
         correct, clipped, nonfinite = ints[:Cp], ints[Cp:2 * Cp], ints[2 * Cp:3 * Cp]
-        # CNN training contexts: the first local step runs at theta_t, so its forward IS the
+        # CNN / LM training contexts: the first local step runs at theta_t, so its forward IS the
         # evaluation of the first batch (fedsim/algorithms/fedavg.py:165 evaluates every row at
         # theta_t before training): evaluate only epoch 0's remaining rows here and let the
         # local-SGD call add the first batch's loss / hits
-        share0 = bool(train and C and runner.kind == "cnn" and plan.train is not None
+        share0 = bool(train and C and runner.kind in ("cnn", "lm") and plan.train is not None
                       and plan.train.num_epochs >= 1 and SHARE_FIRST_BATCH_EVAL)
         if C:
             runner.eval(theta.flat, pop, d_row_start, d_num_rows, C, loss, correct, stream, num_rows,

@@ -60,10 +60,11 @@ SIGNATURES: dict[str, tuple] = {
     "fb_lm_set_gemm_impl": (_i32, [_i32]),
     "fb_lm_num_params": (_i64, [_p]),
     "fb_lm_workspace_bytes": (_i64, [_p, _i32, _i32, _i32]),
-    "fb_eval_lm_f32": (_i32, [_p, _p, _p, _p, _p, _p, _i32, _p, _p, _i32, _i32, _p, _i64, _p]),
+    "fb_eval_lm_f32": (_i32, [_p, _p, _p, _p, _p, _p, _i32, _p, _p, _i32, _i32, _p, _i64, _p, _p, _i32, _p]),
     "fb_local_sgd_lm_f32": (
         _i32,
-        [_p, _p, _p, _p, _p, _p, _p, _p, _i32, _i32, _i32, _f32, _f32, _p, _i64, _p, _i64, _p, _i32, _p, _i64, _p],
+        [_p, _p, _p, _p, _p, _p, _p, _p, _i32, _i32, _i32, _f32, _f32, _p, _i64, _p, _i64, _p, _i32, _p, _i64, _p, _p,
+         _p],
     ),
     "fb_clip_workspace_bytes": (_i64, [_i32, _i64]),
     "fb_delta_norm_clip_f32": (_i32, [_p, _i64, _i32, _i64, _p, _f64, _p, _p, _p, _p, _p, _i64, _p]),

@@ -59,7 +59,7 @@ def pack(users):
     return X, n, start
 
 
-def run_local_sgd(model, theta, users, ctx_seed, E, B, lr, mu=0.0, wave=None):
+def run_local_sgd(model, theta, users, ctx_seed, E, B, lr, mu=0.0, wave=None, eval_out=None):
     X, n, start = pack(users)
     perms = [port.user_perms(ctx_seed, u.user_id, u.num_points, E).astype(np.int32).ravel() for u in users]
     off = np.concatenate([[0], np.cumsum([len(p) for p in perms])[:-1]]).astype(np.int64)
@@ -75,12 +75,14 @@ def run_local_sgd(model, theta, users, ctx_seed, E, B, lr, mu=0.0, wave=None):
     th, Xd, sd, nd, pd, od = d(theta.astype(np.float32)), d(X), d(start), d(n), d(np.concatenate(perms)), d(off)
     native.call("fb_local_sgd_lm_f32", th.data_ptr(), dims.ctypes.data, Xd.data_ptr(), sd.data_ptr(), nd.data_ptr(),
                 n.ctypes.data, pd.data_ptr(), od.data_ptr(), C, E, B, lr, mu, None, 0, delta.data_ptr(), ld,
-                bad.data_ptr(), W, ws.data_ptr(), ws.numel(), native.stream_handle())
+                bad.data_ptr(), W, ws.data_ptr(), ws.numel(), native.ptr(eval_out[0]) if eval_out else None,
+                native.ptr(eval_out[1]) if eval_out else None, native.stream_handle())
     torch.cuda.synchronize()
     return delta[:, :D].double().cpu().numpy(), bad.cpu().numpy()
 
 
-def run_eval(model, theta, users, groups=4, B=16):
+def run_eval(model, theta, users, groups=4, B=16, skip_first=None):
+    """skip_first=(ctx_seed, E, skip): evaluate only epoch 0's sentences past the first skip."""
     X, n, start = pack(users)
     C = len(users)
     dims = lm_glue.dims_of(model)
@@ -90,9 +92,16 @@ def run_eval(model, theta, users, groups=4, B=16):
     corr = torch.zeros(C, dtype=torch.int32, device="cuda")
     d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
     th, Xd, sd, nd = d(theta.astype(np.float32)), d(X), d(start), d(n)
+    pd = od = None
+    skip = 0
+    if skip_first is not None:
+        seed, E, skip = skip_first
+        perms = [port.user_perms(seed, u.user_id, u.num_points, E).astype(np.int32).ravel() for u in users]
+        pd = d(np.concatenate(perms))
+        od = d(np.concatenate([[0], np.cumsum([len(p) for p in perms])[:-1]]).astype(np.int64))
     native.call("fb_eval_lm_f32", th.data_ptr(), dims.ctypes.data, Xd.data_ptr(), sd.data_ptr(), nd.data_ptr(),
                 n.ctypes.data, C, loss.data_ptr(), corr.data_ptr(), B, groups, ws.data_ptr(), ws.numel(),
-                native.stream_handle())
+                native.ptr(pd), native.ptr(od), skip, native.stream_handle())
     torch.cuda.synchronize()
     return loss.cpu().numpy(), corr.cpu().numpy()
 
@@ -158,6 +167,30 @@ def test_lm_configC_local_sgd_and_eval_match_oracle():
         ls, k = m.eval_counts(p0, u.features)
         assert loss[c] == pytest.approx(ls, rel=1e-5)
         assert abs(int(corr[c]) - k) <= 1
+
+
+@pytest.mark.parametrize("shape,B,E", [("tiny", 5, 2), ("mid", 16, 1)])
+def test_lm_first_batch_eval_shared_with_local_sgd(shape, B, E):
+    """The engine's split evaluation: eval of epoch 0's sentences past the first batch
+    (fb_eval_lm_f32 perms/skip) plus the first local step's theta_t loss / hits
+    (fb_local_sgd_lm_f32 eval_loss / eval_correct) equals the full evaluation and the
+    oracle's -- ragged clients, some with fewer sentences than a batch."""
+    shp = TINY if shape == "tiny" else MID
+    m, users = cohort(shp, 7, seed=17)
+    model = product_model(shp)
+    p0 = m.init(6)
+    theta = port.flat(p0, m.dims)
+    full_loss, full_corr = run_eval(model, theta, users, groups=3)
+    loss, corr = run_eval(model, theta, users, groups=3, skip_first=(41, E, B))
+    lt = torch.from_numpy(loss).cuda()
+    ct = torch.from_numpy(corr).cuda()
+    run_local_sgd(model, theta, users, 41, E, B, 0.2, wave=3, eval_out=(lt, ct))
+    loss, corr = lt.cpu().numpy(), ct.cpu().numpy()
+    for c, u in enumerate(users):
+        ls, k = m.eval_counts(p0, u.features)
+        assert loss[c] == pytest.approx(ls, rel=1e-5), c
+        assert loss[c] == pytest.approx(full_loss[c], rel=1e-5), c
+        assert abs(int(corr[c]) - k) <= 1 and abs(int(corr[c]) - int(full_corr[c])) <= 1, c
 
 
 def test_lm_deterministic_rerun():
