@@ -67,6 +67,14 @@ WORKLOADS = {
     "lm": dict(model="lm", users=4000, val_users=200, ppu=None, sentences=True, cohort=400, eval_cohort=100,
                epochs=1, batch=16, lr=0.3, clr=0.1, adam=(0.9, 0.99, 0.1), bound=1.0, sigma=1.0, noise_cohort=5000,
                eval_every=20, name="stackoverflow-transformer-lm fedavg+gaussian-dp+adam cohort400 (BASELINE configs[2])"),
+    # BASELINE configs[3] / SURVEY.md 8(f) row 3: FLAIR-shaped ResNet-18 (GroupNorm), 17-label
+    # multi-label BCE: cohort 200, 2 epochs, B=16, local lr
+    # 0.01, central Adam (lr 0.1, betas 0.9/0.99, adaptivity 0.1), clip 0.1, noise cohort 5000,
+    # evaluation every 20; 1 - 500 224 x 224 images per user (synthetic, ragged)
+    "resnet": dict(model="resnet", users=400, val_users=40, ppu=None, images=True, cohort=200, eval_cohort=40,
+                   epochs=2, batch=16, lr=0.01, clr=0.1, adam=(0.9, 0.99, 0.1), bound=0.1, sigma=1.0,
+                   noise_cohort=5000, eval_every=20,
+                   name="flair-resnet18-gn multilabel fedavg+gaussian-dp+adam cohort200 (BASELINE configs[3])"),
 }
 
 # FP32 FFMA peak: 148 SMs x 128 lanes x 2 x 1.965 GHz
@@ -115,6 +123,11 @@ def build_ragged(wl: dict):
 def build(wl: dict):
     import paper_2404_06430_b200 as fb
 
+    if wl.get("images"):
+        return {fb.Population.TRAIN: fb.make_synthetic_images(wl["users"], seed=fb.derive_seed(0, "train", "resnet"),
+                                                              id_prefix="train"),
+                fb.Population.VAL: fb.make_synthetic_images(wl["val_users"], seed=fb.derive_seed(0, "val", "resnet"),
+                                                            population=fb.Population.VAL, id_prefix="val")}
     if wl.get("sentences"):
         return {fb.Population.TRAIN: fb.make_synthetic_sentences(wl["users"], seed=fb.derive_seed(0, "train", "lm"),
                                                                  population=fb.Population.TRAIN, id_prefix="train"),
@@ -141,6 +154,8 @@ def make_model(wl):
         return fb.CNN()
     if wl["model"] == "lm":
         return fb.TransformerLM()
+    if wl["model"] == "resnet":
+        return fb.ResNet18()
     if wl["model"] == "mlp":
         return fb.MLP(wl["dim"], wl["hidden"], 10)
     return fb.LogisticRegression(wl["dim"], 10)
@@ -294,6 +309,27 @@ def lm_kernel_work(counts: dict) -> dict:
             "lm_gemm_tc_tn_kernel": ("tensor", per_row * counts["train_rows"], tc)}
 
 
+def resnet_kernel_work(counts: dict) -> dict:
+    """Config D: algorithmic conv + fc FLOPs per image (2 x MACs, models.ResNet18
+    .forward_flops_per_image: 3.63 GFLOP at 224 x 224) -- forward Y = col W^T (NT) for
+    every forward pass, dW = dY^T col (TN) and dcol = dY W (NN, no stem: its input needs
+    no gradient) per trained image.  Images = real images only: the zero slots of tail
+    batches are work the kernels do but the algorithm does not."""
+    import paper_2404_06430_b200 as fb
+
+    m = fb.ResNet18()
+    f = m.forward_flops_per_image()
+    h = (m.image + 6 - 7) // 2 + 1
+    stem = 2 * 3 * m.width * 49 * h * h
+    tc = "3xTF32 tcgen05 (grouped persistent GEMM over im2col)"
+    note = "FP32 FFMA (SIMT tiled GEMM)"
+    return {"rn_gemm_tc_nt_kernel": ("tensor", f * counts["fwd"], tc),
+            "rn_gemm_tc_tn_kernel": ("tensor", f * counts["train"], tc),
+            "rn_gemm_tc_nn_kernel": ("tensor", (f - stem) * counts["train"], tc),
+            "rn_gemm_nt_kernel": ("fp32", 0, note), "rn_gemm_nn_kernel": ("fp32", 0, note),
+            "rn_gemm_tn_kernel": ("fp32", 0, note)}
+
+
 def _ncu_kernel(name: str) -> dict | None:
     try:
         return json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())["kernels"][name]
@@ -331,7 +367,8 @@ def roofline(report: dict, wl: dict, counts: dict, peaks: dict) -> tuple[dict, d
     if not report:
         return {}, {}
     work = (kernel_work(wl, counts) if wl["model"] == "cnn" else
-            lm_kernel_work(counts) if wl["model"] == "lm" else {})
+            lm_kernel_work(counts) if wl["model"] == "lm" else
+            resnet_kernel_work(counts) if wl["model"] == "resnet" else {})
     total = sum(v[0] for v in report.values())
     per = {}
     for name, (ms, launches) in report.items():
@@ -372,7 +409,7 @@ def roofline(report: dict, wl: dict, counts: dict, peaks: dict) -> tuple[dict, d
                    peak_source=(("MEASURED_PEAKS.json bf16_tflops (dense bf16 cuBLAS); the kernel's own math is "
                                  + k.get("math", "") + ": three kind::tf32 MMAs per algorithmic product at half the "
                                  "bf16 rate -> at most 1/6 of this peak") if "TF32" in k.get("math", "") and
-                                wl["model"] == "lm" else
+                                wl["model"] in ("lm", "resnet") else
                                 ("MEASURED_PEAKS.json bf16_tflops (dense bf16 cuBLAS); the kernel's own math is "
                                 + k.get("math", "") + ": per algorithmic product one N=128 MMA (hi*[Whi;Wlo]) + one "
                                 "N=64 MMA (lo*Whi) -> at most 1/3 of the fp16/bf16 dense rate, and the N=64 half is "
@@ -452,6 +489,15 @@ def gpu_arm(args, wl):
         counts["fwd_rows"] = (counts["train_rows"] + ev_rows(per_rank * float(sizes.mean())) * KP
                               + val_iters * ev_rows((wl["eval_cohort"] / world) * float(sizes.mean())))
         steps = mean_steps
+    if wl["model"] == "resnet":  # real images through the forward / training passes (tail slots excluded)
+        sizes = np.array([u.num_points for u in ds[fb.Population.TRAIN].users.values()], dtype=np.float64)
+        B = wl["batch"]
+        mean_n = float(sizes.mean())
+        shared = float(np.mean(np.minimum(sizes, B)))  # the first batch's eval rides on local step 0
+        counts["train"] = per_rank * mean_n * wl["epochs"] * KP
+        counts["fwd"] = (counts["train"] + per_rank * (mean_n - shared) * KP
+                         + val_iters * (wl["eval_cohort"] / world) * mean_n)
+        steps = float(np.mean(wl["epochs"] * np.ceil(sizes / B)))
 
     # end-to-end: dataset in pinned host memory, cohort rows moved every iteration
     e2e = None
@@ -471,8 +517,8 @@ def gpu_arm(args, wl):
                "data": "dataset in pinned host memory; cohort rows gathered to HBM each iteration"}
 
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(wl, ds, args.cpu_clients)
+    if rank == 0 and not args.no_cpu_baseline:  # (config D: ~0.5 s per image pass on the host -> one client)
+        cpu = cpu_baseline(wl, ds, 1 if wl["model"] == "resnet" else args.cpu_clients)
 
     rf, per_kernel = roofline(report, wl, counts, peaks)
     if rank == 0:
@@ -484,6 +530,8 @@ def gpu_arm(args, wl):
             "config": {"workload": wl["name"], "model": wl["model"], "cohort": C, "users": wl["users"],
                        "points_per_user": wl["ppu"] or (f"ragged lognormal(3,1) in [1,64] sentences of 20 tokens, "
                                                         f"mean {ppu:.1f}" if wl["model"] == "lm" else
+                                                        f"ragged lognormal(3,1) in [1,500] 224x224 images, 17 "
+                                                        f"labels, mean {ppu:.1f}" if wl["model"] == "resnet" else
                                                         f"ragged lognormal(3,1) in [1,500], mean {ppu:.1f}"),
                        "local_epochs": wl["epochs"], "batch": wl["batch"],
                        "local_steps_per_client": steps, "sigma": wl["sigma"], "clip_bound": wl["bound"],
@@ -523,7 +571,7 @@ def cpu_iteration_seconds(wl, ds, n_clients: int, t: int = 0) -> tuple[float, st
     import paper_2404_06430_b200 as fb
     from oracle import port
 
-    model = {"cnn": lambda: port.Cnn(), "lm": lambda: port.TransformerLM(),
+    model = {"cnn": lambda: port.Cnn(), "lm": lambda: port.TransformerLM(), "resnet": lambda: port.ResNet18(),
              "mlp": lambda: port.Mlp(wl["dim"], wl["hidden"], 10),
              "logistic": lambda: port.Linear(wl["dim"], 10)}[wl["model"]]()
     theta = model.init(0)
@@ -575,6 +623,8 @@ def _reference_setup(wl):
     fit_local loop drives it), a FedAvg factory (cohort size -> algorithm) and
     ClippingPostprocessor + GaussianCentralMechanism at the bench's settings."""
     REF = ROOT / "baseline" / "_ref"
+    if wl.get("ppu") is None:  # ragged / sentence / image populations: the port's own data path
+        raise ValueError(f"the reference arm's fedsim datasets cover fixed-size users only ({wl['model']})")
     if not (REF / "fedsim" / "__init__.py").exists():
         raise ImportError("fedsim not installed in baseline/_ref")
     os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join(tempfile.gettempdir(), "fedsim_numba_cache"))
@@ -686,7 +736,7 @@ def reference_arm(args, wl):
     C = wl["cohort"]
     try:
         ds, make_alg, post = _reference_setup(wl)
-    except ImportError as exc:
+    except (ImportError, ValueError) as exc:
         return _reference_arm_port(args, wl, str(exc))
     small, big = ncores, 3 * ncores
     alg_small, alg_big = make_alg(small), make_alg(big)

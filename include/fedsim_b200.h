@@ -234,6 +234,33 @@ int fb_local_sgd_lm_f32(const float* theta_t, const int32_t* dims, const float* 
                         double* eval_loss /* nullable [C]: += the first batch's theta_t loss */,
                         int32_t* eval_correct /* nullable [C] */, void* stream);
 
+/* ------------------------------- config D: ResNet-18, multi-label (a4 + a5)
+ * models.ResNet18, the FLAIR-shaped image model of BASELINE configs[3]
+ * (/root/reference/PAPER.md:1104-1138): torchvision's ResNet-18 layout with
+ * GroupNorm, dims (host int32[4]) = {num_classes, width, groups, image side}.
+ * X rows (ldx floats, >= 3 S^2 + K) hold an image's CHW pixels followed by its K
+ * label indicators; h_num_rows is the host copy of num_rows.  Loss per image: the
+ * mean sigmoid BCE over its K labels; eval: per-client summed per-image loss and
+ * exact-match images, in chunks of groups x batch_size images.  Local SGD: the
+ * generic update rule of fedsim/models/models.py:53-79 (batch loss = mean over
+ * the batch's images), clients trained clients_per_wave at a time, largest
+ * first; delta / nonfinite / perms / eval_loss as in fb_local_sgd_lm_f32.
+ * Shapes: width a power of two in [4, 64], groups dividing it, S in [32, 1024],
+ * K <= 256 (FB_ERR_UNSUPPORTED otherwise).                                  */
+int64_t fb_resnet_num_params(const int32_t* dims);
+int64_t fb_resnet_workspace_bytes(const int32_t* dims, int batch_size, int clients_per_wave);
+int fb_eval_resnet_f32(const float* theta, const int32_t* dims, const float* X, int64_t ldx, const int64_t* row_start,
+                       const int32_t* num_rows, const int32_t* h_num_rows, int num_clients, double* loss_sum,
+                       int32_t* correct, int batch_size, int groups, void* workspace, int64_t workspace_bytes,
+                       const int32_t* perms, const int64_t* perm_off, int skip, void* stream);
+int fb_local_sgd_resnet_f32(const float* theta_t, const int32_t* dims, const float* X, int64_t ldx,
+                            const int64_t* row_start, const int32_t* num_rows, const int32_t* h_num_rows,
+                            const int32_t* perms, const int64_t* perm_off, int num_clients, int epochs,
+                            int batch_size, float lr, float prox_mu, const float* control, int64_t ld_control,
+                            float* delta_out, int64_t ld_delta, int32_t* nonfinite, int clients_per_wave,
+                            void* workspace, int64_t workspace_bytes, double* eval_loss, int32_t* eval_correct,
+                            void* stream);
+
 /* ------------------------------------------------- a6 + a7 (kernel K2)
  * For every client c: norm[c] = || w[c] * delta[c, :D] ||_2 (fp64
  * accumulation), clipped[c] = norm[c] > bound (strict), coef[c] =

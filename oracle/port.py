@@ -448,6 +448,228 @@ class TransformerLM:
         return float((ce * mask).sum()), int((hit & mask).sum())
 
 
+# ------------------------------------------------ config D: ResNet-18, multi-label
+# FLAIR-shaped image model (BASELINE configs[3]; /root/reference/PAPER.md:1104-1138:
+# ResNet-18, 17 coarse multi-label classes, cohort 200, E = 2, B = 16, central Adam).
+# The reference ships no ResNet, so this oracle DEFINES the arithmetic and is pinned
+# to float64 torch autograd (tests/test_oracle_resnet.py):
+#   * torchvision's ResNet-18 layout (He et al. 2016): conv7x7/2 (pad 3) -> norm -> ReLU
+#     -> maxpool 3x3/2 (pad 1) -> 4 stages x 2 BasicBlocks (widths w, 2w, 4w, 8w; stage
+#     strides 1, 2, 2, 2; 1x1/stride conv + norm shortcut where the shape changes) ->
+#     global average pool -> fc (8w -> K, with bias); convs without bias;
+#   * GroupNorm(groups, C), eps 1e-5, in place of BatchNorm (the FLAIR benchmark's
+#     choice for federated training: no cross-client batch statistics);
+#   * maxpool ties go to the first maximum in row-major window order (PyTorch's);
+#   * a datapoint is ONE image: features = 3 x S x S pixels in CHW order followed by K
+#     label indicators (0 / 1);
+#   * loss = sigmoid binary cross-entropy, per image the mean over its K labels, the
+#     batch loss the mean over the batch's images (BCEWithLogits, reduction "mean");
+#     eval_counts = (summed per-image loss, images whose K thresholded logits (z > 0)
+#     all equal their labels -- exact-match accuracy).
+def _conv_cols(x: np.ndarray, k: int, stride: int, pad: int):
+    """NCHW x -> im2col [N*Ho*Wo, C*k*k] in (c, ky, kx) column order (OIHW flattening)."""
+    N, C, H, W = x.shape
+    xp = np.pad(x, ((0, 0), (0, 0), (pad, pad), (pad, pad))) if pad else x
+    win = np.lib.stride_tricks.sliding_window_view(xp, (k, k), axis=(2, 3))[:, :, ::stride, ::stride]
+    Ho, Wo = win.shape[2], win.shape[3]
+    return win.transpose(0, 2, 3, 1, 4, 5).reshape(N * Ho * Wo, C * k * k), Ho, Wo
+
+
+def _conv_back_input(dcols: np.ndarray, shape, k: int, stride: int, pad: int, Ho: int, Wo: int):
+    N, C, H, W = shape
+    d = dcols.reshape(N, Ho, Wo, C, k, k)
+    dxp = np.zeros((N, C, H + 2 * pad, W + 2 * pad))
+    for i in range(k):
+        for j in range(k):
+            dxp[:, :, i:i + stride * (Ho - 1) + 1:stride, j:j + stride * (Wo - 1) + 1:stride] += \
+                d[:, :, :, :, i, j].transpose(0, 3, 1, 2)
+    return dxp[:, :, pad:pad + H, pad:pad + W]
+
+
+@dataclass(frozen=True)
+class ResNet18:
+    num_classes: int = 17
+    width: int = 64
+    groups: int = 32
+    image: int = 224
+    eps: float = 1e-5
+
+    def blocks(self):
+        """(name, c_in, c_out, stride, has_downsample) per BasicBlock."""
+        out, cin = [], self.width
+        for s in range(4):
+            cout = self.width << s
+            for b in range(2):
+                stride = 2 if (s > 0 and b == 0) else 1
+                out.append((f"layer{s + 1}.{b}", cin, cout, stride, stride != 1 or cin != cout))
+                cin = cout
+        return out
+
+    @property
+    def dims(self):
+        w = self.width
+        out = {"conv1.weight": w * 3 * 49, "gn1.weight": w, "gn1.bias": w}
+        for name, ci, co, _, ds in self.blocks():
+            out.update({f"{name}.conv1.weight": co * ci * 9, f"{name}.gn1.weight": co, f"{name}.gn1.bias": co,
+                        f"{name}.conv2.weight": co * co * 9, f"{name}.gn2.weight": co, f"{name}.gn2.bias": co})
+            if ds:
+                out.update({f"{name}.downsample.0.weight": co * ci, f"{name}.downsample.1.weight": co,
+                            f"{name}.downsample.1.bias": co})
+        out.update({"fc.weight": self.num_classes * 8 * w, "fc.bias": self.num_classes})
+        return out
+
+    def init(self, seed):
+        """Convs N(0, 2 / (c_out k^2)) (kaiming fan-out, torchvision), fc N(0, 1 / fan_in),
+        norm gains 1, biases 0; one generator in dims order."""
+        rng = np.random.default_rng(seed)
+        out = {}
+        for name, n in self.dims.items():
+            if name.endswith("bias"):
+                out[name] = np.zeros(n)
+            elif ".gn" in name or name.startswith("gn") or "downsample.1" in name:
+                out[name] = np.ones(n)
+            elif name == "fc.weight":
+                out[name] = rng.normal(0.0, 1.0 / np.sqrt(8 * self.width), n)
+            else:
+                k2 = 49 if name == "conv1.weight" else (1 if "downsample" in name else 9)
+                out[name] = rng.normal(0.0, np.sqrt(2.0 / (self._cout(name) * k2)), n)
+        return out
+
+    def _cout(self, name):
+        if name == "conv1.weight":
+            return self.width
+        blk = name.split(".conv")[0].split(".downsample")[0]
+        return {b[0]: b[2] for b in self.blocks()}[blk]
+
+    def _gn(self, x, g, b):
+        N, C, H, W = x.shape
+        G = self.groups
+        xg = x.reshape(N, G, -1)
+        mu = xg.mean(axis=-1, keepdims=True)
+        var = ((xg - mu) ** 2).mean(axis=-1, keepdims=True)
+        rstd = 1.0 / np.sqrt(var + self.eps)
+        xh = ((xg - mu) * rstd).reshape(N, C, H, W)
+        return xh * g[None, :, None, None] + b[None, :, None, None], xh, rstd
+
+    def _gn_back(self, dy, xh, rstd, g):
+        N, C, H, W = dy.shape
+        G = self.groups
+        dxh = (dy * g[None, :, None, None]).reshape(N, G, -1)
+        xg = xh.reshape(N, G, -1)
+        dx = rstd * (dxh - dxh.mean(axis=-1, keepdims=True) - xg * (dxh * xg).mean(axis=-1, keepdims=True))
+        return dx.reshape(N, C, H, W), (dy * xh).sum(axis=(0, 2, 3)), dy.sum(axis=(0, 2, 3))
+
+    def _conv(self, x, w, k, stride, pad):
+        cols, Ho, Wo = _conv_cols(x, k, stride, pad)
+        co = w.size // cols.shape[1]
+        y = (cols @ w.reshape(co, -1).T).reshape(x.shape[0], Ho, Wo, co).transpose(0, 3, 1, 2)
+        return y, cols
+
+    def _conv_back(self, dy, cols, x_shape, w, k, stride, pad, need_dx=True):
+        N, co, Ho, Wo = dy.shape
+        d2 = dy.transpose(0, 2, 3, 1).reshape(-1, co)
+        gw = (d2.T @ cols).ravel()
+        if not need_dx:
+            return None, gw
+        return _conv_back_input(d2 @ w.reshape(co, -1), x_shape, k, stride, pad, Ho, Wo), gw
+
+    def _split(self, X):
+        S, K = self.image, self.num_classes
+        return X[:, :3 * S * S].reshape(-1, 3, S, S), X[:, 3 * S * S:3 * S * S + K]
+
+    def _forward(self, p, X):
+        x, _ = self._split(X)
+        N = x.shape[0]
+        cache = {}
+        c1, cols = self._conv(x, p["conv1.weight"], 7, 2, 3)
+        a, xh, r = self._gn(c1, p["gn1.weight"], p["gn1.bias"])
+        a = np.maximum(a, 0.0)
+        cache["stem"] = (x.shape, cols, xh, r, a)
+        # maxpool 3x3/2 pad 1: first maximum in row-major window order
+        ap = np.pad(a, ((0, 0), (0, 0), (1, 1), (1, 1)), constant_values=-np.inf)
+        win = np.lib.stride_tricks.sliding_window_view(ap, (3, 3), axis=(2, 3))[:, :, ::2, ::2]
+        Ho, Wo = win.shape[2], win.shape[3]
+        win = win.reshape(N, a.shape[1], Ho, Wo, 9)
+        arg = win.argmax(axis=-1)
+        x = np.take_along_axis(win, arg[..., None], axis=-1)[..., 0]
+        cache["pool"] = (a.shape, arg, Ho, Wo)
+        for name, ci, co, st, ds in self.blocks():
+            q = lambda n: p[f"{name}.{n}"]
+            t1, cols1 = self._conv(x, q("conv1.weight"), 3, st, 1)
+            u1, xh1, r1 = self._gn(t1, q("gn1.weight"), q("gn1.bias"))
+            u1 = np.maximum(u1, 0.0)
+            t2, cols2 = self._conv(u1, q("conv2.weight"), 3, 1, 1)
+            v2, xh2, r2 = self._gn(t2, q("gn2.weight"), q("gn2.bias"))
+            if ds:
+                td, colsd = self._conv(x, q("downsample.0.weight"), 1, st, 0)
+                sc, xhd, rd = self._gn(td, q("downsample.1.weight"), q("downsample.1.bias"))
+            else:
+                sc, colsd, xhd, rd = x, None, None, None
+            out = np.maximum(v2 + sc, 0.0)
+            cache[name] = (x.shape, cols1, xh1, r1, u1, cols2, xh2, r2, colsd, xhd, rd, out)
+            x = out
+        feat = x.mean(axis=(2, 3))
+        logits = feat @ p["fc.weight"].reshape(self.num_classes, -1).T + p["fc.bias"]
+        cache["head"] = (x.shape, feat)
+        return cache, logits
+
+    @staticmethod
+    def _bce(z, y):
+        """per-element BCE with logits, stable form."""
+        return np.maximum(z, 0.0) - z * y + np.log1p(np.exp(-np.abs(z)))
+
+    def loss_and_grad(self, p, X, y=None):
+        cache, z = self._forward(p, X)
+        _, lab = self._split(X)
+        N, K = z.shape
+        loss = float(self._bce(z, lab).mean())
+        dz = (1.0 / (1.0 + np.exp(-z)) - lab) / (N * K)
+        g = {}
+        shape4, feat = cache["head"]
+        g["fc.weight"] = (dz.T @ feat).ravel()
+        g["fc.bias"] = dz.sum(axis=0)
+        dx = np.broadcast_to((dz @ p["fc.weight"].reshape(K, -1))[:, :, None, None], shape4) / (shape4[2] * shape4[3])
+        for name, ci, co, st, ds in reversed(self.blocks()):
+            q = lambda n: p[f"{name}.{n}"]
+            xs, cols1, xh1, r1, u1, cols2, xh2, r2, colsd, xhd, rd, out = cache[name]
+            dv = dx * (out > 0.0)
+            dt2, g[f"{name}.gn2.weight"], g[f"{name}.gn2.bias"] = self._gn_back(dv, xh2, r2, q("gn2.weight"))
+            if ds:
+                dtd, g[f"{name}.downsample.1.weight"], g[f"{name}.downsample.1.bias"] = \
+                    self._gn_back(dv, xhd, rd, q("downsample.1.weight"))
+                dsc, g[f"{name}.downsample.0.weight"] = self._conv_back(dtd, colsd, xs, q("downsample.0.weight"),
+                                                                       1, st, 0)
+            else:
+                dsc = dv
+            du1, g[f"{name}.conv2.weight"] = self._conv_back(dt2, cols2, u1.shape, q("conv2.weight"), 3, 1, 1)
+            du1 = du1 * (u1 > 0.0)
+            dt1, g[f"{name}.gn1.weight"], g[f"{name}.gn1.bias"] = self._gn_back(du1, xh1, r1, q("gn1.weight"))
+            dxin, g[f"{name}.conv1.weight"] = self._conv_back(dt1, cols1, xs, q("conv1.weight"), 3, st, 1)
+            dx = dxin + dsc
+        ashape, arg, Ho, Wo = cache["pool"]
+        Nn, C, H, W = ashape
+        dwin = np.zeros((Nn, C, Ho, Wo, 9))
+        np.put_along_axis(dwin, arg[..., None], dx[..., None], axis=-1)
+        dap = np.zeros((Nn, C, H + 2, W + 2))
+        dwin = dwin.reshape(Nn, C, Ho, Wo, 3, 3)
+        for i in range(3):
+            for j in range(3):
+                dap[:, :, i:i + 2 * (Ho - 1) + 1:2, j:j + 2 * (Wo - 1) + 1:2] += dwin[..., i, j]
+        da = dap[:, :, 1:1 + H, 1:1 + W]
+        xshape, cols, xh, r, a = cache["stem"]
+        da = da * (a > 0.0)
+        dc1, g["gn1.weight"], g["gn1.bias"] = self._gn_back(da, xh, r, p["gn1.weight"])
+        _, g["conv1.weight"] = self._conv_back(dc1, cols, xshape, p["conv1.weight"], 7, 2, 3, need_dx=False)
+        return loss, {n: np.asarray(g[n]).ravel() for n in self.dims}
+
+    def eval_counts(self, p, X, y=None):
+        _, z = self._forward(p, X)
+        _, lab = self._split(X)
+        per = self._bce(z, lab).mean(axis=1)
+        hit = ((z > 0.0) == (lab > 0.5)).all(axis=1)
+        return float(per.sum()), int(hit.sum())
+
+
 # ------------------------------------------------------------ local work
 
 

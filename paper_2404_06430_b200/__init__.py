@@ -71,13 +71,14 @@ from .feddata import (
     UserDataset,
     load_partition,
     make_synthetic_classification,
+    make_synthetic_images,
     make_synthetic_sentences,
     partition_iid,
     sample_cohort,
     save_partition,
 )
-from .models import (CNN, MLP, AdamOptimizer, LogisticRegression, Model, SGDOptimizer, TransformerLM, central_step,
-                     count_local_steps)
+from .models import (CNN, MLP, AdamOptimizer, LogisticRegression, Model, ResNet18, SGDOptimizer, TransformerLM,
+                     central_step, count_local_steps)
 from .privacy import (
     AdaptiveClipConfig,
     ClippingPostprocessor,

@@ -32,6 +32,7 @@
 #include <vector>
 
 #include "fb_common.cuh"
+#include "grouped_gemm.cuh"
 #include "tc_common.cuh"
 
 #include <cudaTypedefs.h>
@@ -70,28 +71,7 @@ inline int64_t num_params(const Dims& m) { return (int64_t)m.V * m.d + (int64_t)
 inline int64_t layer_base(const Dims& m, int l) { return (int64_t)m.V * m.d + (int64_t)l * layer_off(m).size; }
 
 // ------------------------------------------------------------------ GEMM
-// C[z](m, n) = alpha * sum_k A[z](m, k) B[z](k, n) (+ beta C) (+ bias[z](n)),
-//   A(m, k) = TA ? A[k * lda + m] : A[m * lda + k]   (relu_a: max(0, .))
-//   B(k, n) = TB ? B[n * ldb + k] : B[k * ldb + n]   (relu_b: max(0, .))
-// mask_aux: multiply the result by (aux[z](m, n) > 0)  (ReLU backward).
-// Batches (clients) whose active[z] == 0 are skipped.
-struct Gemm {
-  const float* A;
-  int64_t lda, sA;
-  const float* B;
-  int64_t ldb, sB;
-  float* C;
-  int64_t ldc, sC;
-  int M, N, K;
-  const float* bias;
-  int64_t sBias;
-  const float* aux;
-  int64_t ldaux, sAux;
-  const int32_t* active;
-  float alpha, beta;
-  int relu_a, relu_b;
-};
-
+// (struct Gemm: grouped_gemm.cuh)
 constexpr int BM = 64, BN = 64, BK = 16, GT = 256;
 
 template <bool TA, bool TB>
@@ -1253,25 +1233,36 @@ int launch_tc(const Gemm& g, int batch, cudaStream_t s, const char* name) {
   return launch_status(name);
 }
 
-int launch_gemm(bool TA, bool TB, const Gemm& g, int batch, cudaStream_t s) {
+// launch labels per caller family (0 = the LM, 1 = the ResNet): {tc nt, tc nn, tc tn, nt, nn, tn}
+static const char* const kGemmNames[2][6] = {
+    {"lm_gemm_tc_nt_kernel", "lm_gemm_tc_nn_kernel", "lm_gemm_tc_tn_kernel", "lm_gemm_nt_kernel", "lm_gemm_nn_kernel",
+     "lm_gemm_tn_kernel"},
+    {"rn_gemm_tc_nt_kernel", "rn_gemm_tc_nn_kernel", "rn_gemm_tc_tn_kernel", "rn_gemm_nt_kernel", "rn_gemm_nn_kernel",
+     "rn_gemm_tn_kernel"}};
+
+int launch_gemm(bool TA, bool TB, const Gemm& g, int batch, cudaStream_t s, int family) {
+  const char* const* nm = kGemmNames[family == 1 ? 1 : 0];
   if (batch <= 0 || g.M <= 0 || g.N <= 0) return FB_OK;
   if (g_gemm_impl == 1 && g.M >= 64 && g.N >= 64 && tma_ok(g.A, g.lda, g.sA) && tma_ok(g.B, g.ldb, g.sB)) {
-    // N tile 96 when it divides N (d_model-wide outputs), else 128
-    const bool n96 = g.N % 96 == 0 && g.N <= 192;
-    if (!TA && TB) return n96 ? launch_tc<false, true, 96>(g, batch, s, "lm_gemm_tc_nt_kernel")
-                              : launch_tc<false, true, 128>(g, batch, s, "lm_gemm_tc_nt_kernel");
-    if (!TA && !TB) return n96 ? launch_tc<false, false, 96>(g, batch, s, "lm_gemm_tc_nn_kernel")
-                               : launch_tc<false, false, 128>(g, batch, s, "lm_gemm_tc_nn_kernel");
-    return n96 ? launch_tc<true, false, 96>(g, batch, s, "lm_gemm_tc_tn_kernel")
-               : launch_tc<true, false, 128>(g, batch, s, "lm_gemm_tc_tn_kernel");
+    // N tile 96 when it divides N (d_model-wide outputs), 64 for 64-wide outputs, else 128
+    const bool n96 = g.N % 96 == 0 && g.N <= 192, n64 = g.N == 64;
+    if (!TA && TB) return n96 ? launch_tc<false, true, 96>(g, batch, s, nm[0])
+                          : n64 ? launch_tc<false, true, 64>(g, batch, s, nm[0])
+                                : launch_tc<false, true, 128>(g, batch, s, nm[0]);
+    if (!TA && !TB) return n96 ? launch_tc<false, false, 96>(g, batch, s, nm[1])
+                           : n64 ? launch_tc<false, false, 64>(g, batch, s, nm[1])
+                                 : launch_tc<false, false, 128>(g, batch, s, nm[1]);
+    return n96 ? launch_tc<true, false, 96>(g, batch, s, nm[2])
+           : n64 ? launch_tc<true, false, 64>(g, batch, s, nm[2])
+                 : launch_tc<true, false, 128>(g, batch, s, nm[2]);
   }
   // 128 x 128 tiles once both output sides fill at least ~3/4 of a tile
   const bool big = g.M >= 96 && g.N >= 96;
   if (!big) {
     const dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM, batch);
-    if (!TA && TB) FB_LAUNCH("lm_gemm_nt_kernel", s, (gemm_kernel<false, true><<<grid, GT, 0, s>>>(g)));
-    else if (!TA && !TB) FB_LAUNCH("lm_gemm_nn_kernel", s, (gemm_kernel<false, false><<<grid, GT, 0, s>>>(g)));
-    else FB_LAUNCH("lm_gemm_tn_kernel", s, (gemm_kernel<true, false><<<grid, GT, 0, s>>>(g)));
+    if (!TA && TB) FB_LAUNCH(nm[3], s, (gemm_kernel<false, true><<<grid, GT, 0, s>>>(g)));
+    else if (!TA && !TB) FB_LAUNCH(nm[4], s, (gemm_kernel<false, false><<<grid, GT, 0, s>>>(g)));
+    else FB_LAUNCH(nm[5], s, (gemm_kernel<true, false><<<grid, GT, 0, s>>>(g)));
     return launch_status("lm_gemm_kernel");
   }
   // contiguous extents: A along K (NT/NN) or M (TN); B along K (NT) or N (NN/TN)
@@ -1284,9 +1275,9 @@ int launch_gemm(bool TA, bool TB, const Gemm& g, int batch, cudaStream_t s) {
     if (vec) FB_LAUNCH(NAME, s, (gemm_big_kernel<TA_, TB_, true><<<grid, GT, 0, s>>>(g)));           \
     else FB_LAUNCH(NAME, s, (gemm_big_kernel<TA_, TB_, false><<<grid, GT, 0, s>>>(g)));              \
   } while (0)
-  if (!TA && TB) FB_LM_BIG(false, true, "lm_gemm_nt_kernel");
-  else if (!TA && !TB) FB_LM_BIG(false, false, "lm_gemm_nn_kernel");
-  else FB_LM_BIG(true, false, "lm_gemm_tn_kernel");
+  if (!TA && TB) FB_LM_BIG(false, true, nm[3]);
+  else if (!TA && !TB) FB_LM_BIG(false, false, nm[4]);
+  else FB_LM_BIG(true, false, nm[5]);
 #undef FB_LM_BIG
   return launch_status("lm_gemm_big_kernel");
 }

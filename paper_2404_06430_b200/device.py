@@ -347,10 +347,30 @@ class DevicePopulation:
         self.total_rows = total
         self.max_label = int(y.max()) if total else 0
         self.min_label = int(y.min()) if total else 0
-        # (token-id datasets, the LM: every feature an integer id in [0, max_feature])
-        self.integral = bool(total == 0 or np.array_equal(X, np.floor(X)))
-        self.min_feature = float(X.min()) if total else 0.0
-        self.max_feature = float(X.max()) if total else 0.0
+        self._feature_range = None
+
+    def _features(self):
+        """(integral, min, max) of the features -- token-id datasets (the LM) index the
+        embedding with them; computed once, on first use, where the rows live."""
+        if self._feature_range is None:
+            if self.total_rows == 0:
+                self._feature_range = (True, 0.0, 0.0)
+            else:
+                X = self.X
+                self._feature_range = (bool(_torch().equal(X, X.floor())), float(X.min()), float(X.max()))
+        return self._feature_range
+
+    @property
+    def integral(self) -> bool:
+        return self._features()[0]
+
+    @property
+    def min_feature(self) -> float:
+        return self._features()[1]
+
+    @property
+    def max_feature(self) -> float:
+        return self._features()[2]
 
 
 class ControlStore:

@@ -25,13 +25,13 @@ from typing import Any, Mapping, Sequence
 
 import numpy as np
 
-from . import cnn, interop, lm, native
+from . import cnn, interop, lm, native, resnet
 from .core import CentralContext, MetricKind, MetricValue, Population, merge_metrics, user_seed
 from .algorithms import CONTROL_PREFIX, MODEL_PREFIX
 from .device import Comm, ControlStore, ControlUpdates, DeviceParams, DevicePopulation, DeviceStatistics, Workspace
 from .errors import EngineError
 from .feddata import FederatedDataset, sample_cohort
-from .models import CNN, MLP, LogisticRegression, TransformerLM
+from .models import CNN, MLP, LogisticRegression, ResNet18, TransformerLM
 from .privacy import CLIPPED_KEY, COUNT_KEY, NORM_KEY, validate_pipeline
 from .scheduling import compute_base_weight, schedule_users
 
@@ -228,6 +228,11 @@ class _ModelRunner:
             self.kind, self.dims = "linear", (model.dim, model.num_classes)
         elif isinstance(model, TransformerLM):
             self.kind, self.dims = "lm", ()
+        elif isinstance(model, ResNet18):
+            self.kind, self.dims = "resnet", ()
+            if native.call("fb_resnet_num_params", resnet.dims_of(model).ctypes.data) != model.num_params:
+                raise ValueError(f"GpuSimulationEngine: unsupported ResNet18 shape {model} (width a power of two "
+                                 "in [4, 64], groups dividing it, image side in [32, 1024], classes <= 256)")
         elif isinstance(model, CNN):
             if model != CNN():  # csrc/cnn.cu is compiled for exactly this geometry
                 raise ValueError(f"GpuSimulationEngine: the CNN kernels are compiled for {CNN()}, got {model}")
@@ -245,6 +250,9 @@ class _ModelRunner:
         if self.kind == "lm":
             return lm.eval_cohort(self, theta, pop, row_start, num_rows, C, loss, correct, stream, h_num_rows,
                                   skip_first=skip_first)
+        if self.kind == "resnet":
+            return resnet.eval_cohort(self, theta, pop, row_start, num_rows, C, loss, correct, stream, h_num_rows,
+                                      skip_first=skip_first)
         fn = f"fb_eval_{self.kind}_f32"
         native.call(fn, native.ptr(theta), *self.dims, native.ptr(pop.X), native.ptr(pop.y),
                     native.ptr(row_start), native.ptr(num_rows), C, native.ptr(loss), native.ptr(correct),
@@ -259,6 +267,9 @@ class _ModelRunner:
         if self.kind == "lm":
             return lm.local_sgd_cohort(self, theta, pop, row_start, num_rows, perms, perm_off, C, tp, prox_mu, delta,
                                        nonfinite, stream, h_num_rows, control=control, eval_out=eval_out)
+        if self.kind == "resnet":
+            return resnet.local_sgd_cohort(self, theta, pop, row_start, num_rows, perms, perm_off, C, tp, prox_mu,
+                                           delta, nonfinite, stream, h_num_rows, control=control, eval_out=eval_out)
         fn = f"fb_local_sgd_{self.kind}_f32"
         native.call(fn, native.ptr(theta), *self.dims, native.ptr(pop.X), native.ptr(pop.y),
                     native.ptr(row_start), native.ptr(num_rows), native.ptr(perms), native.ptr(perm_off), C,
@@ -624,6 +635,8 @@ class GpuSimulationEngine:
             if pop.total_rows and (not pop.integral or pop.min_feature < 0 or pop.max_feature >= plan.model.vocab):
                 raise ValueError(f"population {pop_key.value!r}: token ids must be integers in "
                                  f"[0, {plan.model.vocab}), got [{pop.min_feature}, {pop.max_feature}]")
+        elif runner.kind == "resnet":  # (multi-label: the K label indicators ride at the end of each row)
+            pass
         elif pop.total_rows and (pop.min_label < 0 or pop.max_label >= plan.model.num_classes):
             raise ValueError(f"labels of population {pop_key.value!r} lie in [{pop.min_label}, {pop.max_label}], "
                              f"outside the model's {plan.model.num_classes} classes")
@@ -704,7 +717,7 @@ class GpuSimulationEngine:
         # evaluation of the first batch (fedsim/algorithms/fedavg.py:165 evaluates every row at
         # theta_t before training): evaluate only epoch 0's remaining rows here and let the
         # local-SGD call add the first batch's loss / hits
-        share0 = bool(train and C and runner.kind in ("cnn", "lm") and plan.train is not None
+        share0 = bool(train and C and runner.kind in ("cnn", "lm", "resnet") and plan.train is not None
                       and plan.train.num_epochs >= 1 and SHARE_FIRST_BATCH_EVAL)
         if C:
             runner.eval(theta.flat, pop, d_row_start, d_num_rows, C, loss, correct, stream, num_rows,

@@ -179,6 +179,40 @@ def make_synthetic_sentences(
     return FederatedDataset(users=users, population=population)
 
 
+def make_synthetic_images(
+    num_users: int,
+    *,
+    image: int = 224,
+    num_classes: int = 17,
+    max_images: int = 500,
+    seed: int = 0,
+    population: Population = Population.TRAIN,
+    id_prefix: str = "u",
+) -> FederatedDataset:
+    """FLAIR-shaped users for the config D ResNet-18 (BASELINE configs[3];
+    /root/reference/PAPER.md:1104-1138: 1 - 500 (max 512) images per user, 17
+    coarse multi-label classes).  There is no dataset offline, so the shape is
+    synthesised: images per user max(1, round(lognormal(3, 1))) capped at
+    ``max_images`` (the ragged draw of fedsim/cli/bench.py:61-63), pixels N(0, 1)
+    (already normalised), each label present with probability 2 / K.  A datapoint
+    is one image: features = its 3 x S x S CHW pixels followed by the K label
+    indicators (float32), label = its number of positive labels."""
+    if num_users < 0 or image < 32 or num_classes < 1 or max_images < 1:
+        raise ValueError("need num_users >= 0, image >= 32, num_classes >= 1, max_images >= 1")
+    rng = make_rng(seed)
+    sizes = np.clip(np.round(rng.lognormal(3.0, 1.0, size=num_users)), 1, max_images).astype(np.int64)
+    npx = 3 * image * image
+    users = {}
+    for i, n in enumerate(sizes):
+        X = np.empty((n, npx + num_classes), dtype=np.float32)
+        X[:, :npx] = rng.standard_normal((n, npx), dtype=np.float32)
+        lab = rng.random((n, num_classes)) < 2.0 / num_classes
+        X[:, npx:] = lab
+        uid = f"{id_prefix}{i:05d}"
+        users[uid] = UserDataset(uid, X, lab.sum(axis=1).astype(np.int64))
+    return FederatedDataset(users=users, population=population)
+
+
 def _users_from_chunks(features, labels, chunks, population, prefix) -> FederatedDataset:
     users = {}
     for i, idx in enumerate(chunks):

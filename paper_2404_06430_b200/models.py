@@ -17,6 +17,8 @@ lives in ``csrc/`` -- there is no host forward/backward (no CPU fallback).
   reference MLP: U(+-1/sqrt(fan_in)) drawn in entry order.
 * ``TransformerLM``      -- config C's StackOverflow-shaped next-word model
   (1,962,912 parameters), also absent from the reference; see its docstring.
+* ``ResNet18``           -- config D's FLAIR-shaped multi-label image model
+  (11,185,233 parameters), also absent from the reference; see its docstring.
 """
 
 from __future__ import annotations
@@ -226,6 +228,89 @@ class TransformerLM(Model):
         d, f, L = self.d_model, self.ff, self.seq
         per_layer = 3 * d * d + d * d + 2 * d * f + d * (L + 1)  # (QK^T + PV: 2 * d * (L + 1) / 2)
         return 2 * (self.layers * per_layer + self.vocab * d)
+
+
+@dataclass(frozen=True)
+class ResNet18(Model):
+    """Config D (BASELINE configs[3]): the FLAIR-shaped multi-label image model
+    (ResNet-18, 17 coarse labels).
+    torchvision's ResNet-18 layout -- conv7x7/2 -> norm -> ReLU -> maxpool
+    3x3/2 -> 4 stages x 2 BasicBlocks (widths w, 2w, 4w, 8w) -> global average
+    pool -> fc(8w -> K) -- with GroupNorm(``groups``, eps 1e-5) for BatchNorm
+    (no cross-client batch statistics in federated training), no conv biases.
+    Weight layouts are PyTorch's (OIHW convs, [out, in] fc).  A datapoint is
+    one image: features = 3 x S x S CHW pixels then the K label indicators;
+    the loss is the sigmoid BCE, per image the mean over its K labels, the batch
+    loss the mean over its images; accuracy is exact-match.  The reference has
+    no ResNet; the arithmetic is defined (and pinned to float64 autograd) by the
+    oracle's ResNet18.  Init: convs N(0, 2 / (c_out k^2)) (kaiming fan-out), fc
+    N(0, 1 / fan_in), norm gains 1, biases 0, one generator in entry order."""
+
+    num_classes: int = 17
+    width: int = 64
+    groups: int = 32
+    image: int = 224
+    kind = "resnet"
+
+    @property
+    def input_dim(self) -> int:
+        return 3 * self.image * self.image + self.num_classes
+
+    def blocks(self):
+        """(name, c_in, c_out, stride, has_downsample) per BasicBlock."""
+        out, cin = [], self.width
+        for s in range(4):
+            cout = self.width << s
+            for b in range(2):
+                stride = 2 if (s > 0 and b == 0) else 1
+                out.append((f"layer{s + 1}.{b}", cin, cout, stride, stride != 1 or cin != cout))
+                cin = cout
+        return out
+
+    @property
+    def param_dims(self) -> dict[str, int]:
+        w = self.width
+        out = {"conv1.weight": w * 3 * 49, "gn1.weight": w, "gn1.bias": w}
+        for name, ci, co, _, ds in self.blocks():
+            out.update({f"{name}.conv1.weight": co * ci * 9, f"{name}.gn1.weight": co, f"{name}.gn1.bias": co,
+                        f"{name}.conv2.weight": co * co * 9, f"{name}.gn2.weight": co, f"{name}.gn2.bias": co})
+            if ds:
+                out.update({f"{name}.downsample.0.weight": co * ci, f"{name}.downsample.1.weight": co,
+                            f"{name}.downsample.1.bias": co})
+        out.update({"fc.weight": self.num_classes * 8 * w, "fc.bias": self.num_classes})
+        return out
+
+    def init_params(self, seed: int) -> dict[str, np.ndarray]:
+        rng = make_rng(seed)
+        cout = {b[0]: b[2] for b in self.blocks()}
+        out = {}
+        for name, n in self.param_dims.items():
+            if name.endswith("bias"):
+                out[name] = np.zeros(n)
+            elif ".gn" in name or name.startswith("gn") or "downsample.1" in name:
+                out[name] = np.ones(n)
+            elif name == "fc.weight":
+                out[name] = rng.normal(0.0, 1.0 / np.sqrt(8 * self.width), n)
+            else:
+                k2 = 49 if name == "conv1.weight" else (1 if "downsample" in name else 9)
+                co = self.width if name == "conv1.weight" else cout[name.split(".conv")[0].split(".downsample")[0]]
+                out[name] = rng.normal(0.0, np.sqrt(2.0 / (co * k2)), n)
+        return out
+
+    def forward_flops_per_image(self) -> int:
+        """2 x MACs of one image's forward pass (convolutions and fc; norms,
+        pooling and activations not counted)."""
+        def conv(ci, co, k, hout):
+            return ci * co * k * k * hout * hout
+        S = self.image
+        h = (S + 6 - 7) // 2 + 1
+        macs = conv(3, self.width, 7, h)
+        h = (h + 2 - 3) // 2 + 1
+        for _, ci, co, st, ds in self.blocks():
+            ho = (h + 2 - 3) // st + 1
+            macs += conv(ci, co, 3, ho) + conv(co, co, 3, ho) + (conv(ci, co, 1, ho) if ds else 0)
+            h = ho
+        return 2 * (macs + 8 * self.width * self.num_classes)
 
 
 def count_local_steps(num_points: int, local_params) -> int:

@@ -66,6 +66,14 @@ SIGNATURES: dict[str, tuple] = {
         [_p, _p, _p, _p, _p, _p, _p, _p, _i32, _i32, _i32, _f32, _f32, _p, _i64, _p, _i64, _p, _i32, _p, _i64, _p, _p,
          _p],
     ),
+    "fb_resnet_num_params": (_i64, [_p]),
+    "fb_resnet_workspace_bytes": (_i64, [_p, _i32, _i32]),
+    "fb_eval_resnet_f32": (_i32, [_p, _p, _p, _i64, _p, _p, _p, _i32, _p, _p, _i32, _i32, _p, _i64, _p, _p, _i32, _p]),
+    "fb_local_sgd_resnet_f32": (
+        _i32,
+        [_p, _p, _p, _i64, _p, _p, _p, _p, _p, _i32, _i32, _i32, _f32, _f32, _p, _i64, _p, _i64, _p, _i32, _p, _i64,
+         _p, _p, _p],
+    ),
     "fb_clip_workspace_bytes": (_i64, [_i32, _i64]),
     "fb_delta_norm_clip_f32": (_i32, [_p, _i64, _i32, _i64, _p, _f64, _p, _p, _p, _p, _p, _i64, _p]),
     "fb_delta_norm_clip_ex_f32": (_i32, [_p, _i64, _i32, _i64, _i64, _i64, _p, _p, _f64, _p, _p, _p, _p, _p, _i64, _p]),
