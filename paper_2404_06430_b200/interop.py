@@ -14,7 +14,7 @@ product never imports fedsim -- and maps each onto what the GPU path runs:
   (``local_params``, ``algo_params["mu"]``, ``eval_params``);
 * models: a layout whose ``param_dims`` equal one of the compiled models'
   (LogisticRegression / MLP of fedsim/models/models.py:85-228, the BASELINE
-  CNN, or config C's TransformerLM);
+  CNN, config C's TransformerLM or config D's ResNet18);
 * postprocessors: a clipping stage (``is_clipping``, fedsim/privacy/
   clipping.py:75-103) whose per-user half runs as the fused K2 kernel from
   ``current_bound``, and ``GaussianCentralMechanism`` (fedsim/privacy/
@@ -78,7 +78,7 @@ def check_aggregator(aggregator) -> None:
 def native_model(model):
     """This package's compiled model with the same parameter layout as ``model``
     (entry names, order and sizes), or ValueError."""
-    from .models import CNN, MLP, LogisticRegression, Model, TransformerLM
+    from .models import CNN, MLP, LogisticRegression, Model, ResNet18, TransformerLM
 
     if isinstance(model, Model):
         return model
@@ -96,6 +96,10 @@ def native_model(model):
         candidates.append(TransformerLM(int(model.vocab), d, int(model.heads), int(getattr(model, "ff", 1536)),
                                         int(getattr(model, "layers", 3)), int(getattr(model, "seq", 20))))
     candidates.append(TransformerLM())
+    if hasattr(model, "width") and hasattr(model, "groups"):  # a config D ResNet-18 layout
+        candidates.append(ResNet18(int(getattr(model, "num_classes", 17)), int(model.width), int(model.groups),
+                                   int(getattr(model, "image", 224))))
+    candidates.append(ResNet18())
     for cand in candidates:
         if list(cand.param_dims.items()) == [(n, int(k)) for n, k in dims.items()]:
             return cand
