@@ -150,6 +150,14 @@ inline bool dims_ok(const Dims& m) {
 
 inline Dims parse(const int32_t* d) { return Dims{d[0], d[1], d[2], d[3]}; }
 
+// weight-gradient K split: the GEMM's K is B * P_out rows; long ones (the stem, layer 1)
+// are cut into S power-of-two chunks of >= 2048 rows so (client, chunk) tiles fill the SMs
+inline int ksplit(int rows) {
+  int S = 1;
+  while (S < 16 && rows % (2 * S) == 0 && rows / (2 * S) >= 2048) S *= 2;
+  return S;
+}
+
 inline int nchunks(int P, int C) {
   const int per = std::max(1, kChunkElems / C);  // pixels per chunk
   return (P + per - 1) / per;
@@ -382,14 +390,13 @@ struct ConvTable {
 
 __global__ void permute_kernel(ConvTable tb, int64_t P, const float* __restrict__ W, int64_t sW,
                                float* __restrict__ Wp, int64_t sP, const int32_t* __restrict__ active, int to_perm) {
-  const int w = blockIdx.y;
+  const int w = blockIdx.y, j = blockIdx.z;  // client slot, conv
   if (active && !active[w]) return;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
-    int j = 0;
-    while (j + 1 < tb.n && tb.p_off[j + 1] <= i) ++j;
-    const int64_t e = i - tb.p_off[j];
-    const int kp = tb.kp[j], ci = tb.ci[j], kk = tb.kk[j];
-    const int o = (int)(e / kp), q = (int)(e - (int64_t)o * kp);
+  const int kp = tb.kp[j], ci = tb.ci[j], kk = tb.kk[j];
+  const int n = tb.co[j] * kp;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    const int64_t i = tb.p_off[j] + e;
+    const int o = e / kp, q = e - o * kp;
     if (q >= ci * kk) {
       if (to_perm) Wp[(int64_t)w * sP + i] = 0.f;
       continue;
@@ -478,7 +485,8 @@ __global__ void gn_finalize_kernel(const double2* __restrict__ part, int B, int 
   }
 }
 
-// y = (x - mean) rstd gamma + beta (+ res) (ReLU)
+// y = (x - mean) rstd gamma + beta (+ res) (ReLU); 4 channels per thread (C is a power of
+// two >= 4), 32-bit indices within the image
 __global__ void __launch_bounds__(kT) gn_apply_kernel(const float* __restrict__ x, int64_t s_x, int P, int C, int G,
                                                       const float2* __restrict__ stats, const float* __restrict__ Wc,
                                                       int64_t sW, int64_t g_off, int64_t b_off,
@@ -493,14 +501,24 @@ __global__ void __launch_bounds__(kT) gn_apply_kernel(const float* __restrict__ 
   const float* bet = Wc + (int64_t)w * sW + b_off;
   const int64_t base = (int64_t)w * s_x + (int64_t)b * P * C;
   const float2* st = stats + ((int64_t)w * B + b) * G;
-  const int64_t n = (int64_t)P * C;
-  for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kT) {
-    const int c = (int)(i % C);
-    const float2 ms = st[c / Cg];
-    float v = (x[base + i] - ms.x) * ms.y * gam[c] + bet[c];
-    if (res) v += res[base + i];
-    if (relu) v = fmaxf(v, 0.f);
-    y[base + i] = v;
+  const float4* xv = reinterpret_cast<const float4*>(x + base);
+  const float4* rv = res ? reinterpret_cast<const float4*>(res + base) : nullptr;
+  float4* yv = reinterpret_cast<float4*>(y + base);
+  const int n4 = P * C / 4;
+  for (int i = blockIdx.x * kT + threadIdx.x; i < n4; i += gridDim.x * kT) {
+    const int c = (4 * i) & (C - 1);
+    const float4 v = xv[i];
+    float o[4] = {v.x, v.y, v.z, v.w};
+    float4 r = rv ? rv[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float rr[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 ms = st[(c + e) / Cg];
+      float q = (o[e] - ms.x) * ms.y * gam[c + e] + bet[c + e];
+      if (rv) q += rr[e];
+      o[e] = relu ? fmaxf(q, 0.f) : q;
+    }
+    yv[i] = make_float4(o[0], o[1], o[2], o[3]);
   }
 }
 
@@ -575,7 +593,7 @@ __global__ void gn_bwd_finalize_kernel(const double2* __restrict__ part, int B, 
   if (lane == 0) coef[((int64_t)w * B + b) * G + g] = make_float2((float)(a / n), (float)(q / n));
 }
 
-// dx = rstd (gamma dv - A - xhat Bq)
+// dx = rstd (gamma dv - A - xhat Bq); 4 channels per thread, 32-bit indices in the image
 __global__ void __launch_bounds__(kT) gn_bwd_apply_kernel(const float* __restrict__ dout,
                                                           const float* __restrict__ mask,
                                                           const float* __restrict__ x, int64_t s_x, int P, int C,
@@ -591,14 +609,27 @@ __global__ void __launch_bounds__(kT) gn_bwd_apply_kernel(const float* __restric
   const int64_t base = (int64_t)w * s_x + (int64_t)b * P * C;
   const float2* st = stats + ((int64_t)w * B + b) * G;
   const float2* cf = coef + ((int64_t)w * B + b) * G;
-  const int64_t n = (int64_t)P * C;
-  for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kT) {
-    const int c = (int)(i % C), g = c / Cg;
-    float dv = dout[base + i];
-    if (mask && !(mask[base + i] > 0.f)) dv = 0.f;
-    const float2 ms = st[g], ab = cf[g];
-    const float xh = (x[base + i] - ms.x) * ms.y;
-    dx[base + i] = ms.y * (gam[c] * dv - ab.x - xh * ab.y);
+  const float4* dv4 = reinterpret_cast<const float4*>(dout + base);
+  const float4* mk4 = mask ? reinterpret_cast<const float4*>(mask + base) : nullptr;
+  const float4* x4 = reinterpret_cast<const float4*>(x + base);
+  float4* o4 = reinterpret_cast<float4*>(dx + base);
+  const int n4 = P * C / 4;
+  for (int i = blockIdx.x * kT + threadIdx.x; i < n4; i += gridDim.x * kT) {
+    const int c = (4 * i) & (C - 1);
+    const float4 dd = dv4[i], xx = x4[i];
+    const float4 mm = mk4 ? mk4[i] : make_float4(1.f, 1.f, 1.f, 1.f);
+    const float dva[4] = {dd.x, dd.y, dd.z, dd.w}, xa[4] = {xx.x, xx.y, xx.z, xx.w};
+    const float ma[4] = {mm.x, mm.y, mm.z, mm.w};
+    float o[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int g = (c + e) / Cg;
+      const float dv = ma[e] > 0.f ? dva[e] : 0.f;
+      const float2 ms = st[g], ab = cf[g];
+      const float xh = (xa[e] - ms.x) * ms.y;
+      o[e] = ms.y * (gam[c + e] * dv - ab.x - xh * ab.y);
+    }
+    o4[i] = make_float4(o[0], o[1], o[2], o[3]);
   }
 }
 
@@ -838,6 +869,24 @@ __global__ void nonfinite_kernel(const float* __restrict__ Dl, int64_t ldD, int6
   if (threadIdx.x == 0 && b) atomicOr(&bad[c], 1);
 }
 
+// per (slot, chunk) activity of a split-K launch
+__global__ void expand_active_kernel(const int32_t* __restrict__ active, int W, int S, int32_t* __restrict__ out) {
+  const int z = blockIdx.x * blockDim.x + threadIdx.x;
+  if (z < W * S) out[z] = active ? (active[z / S] != 0) : 1;
+}
+
+// the S chunk partials of a split-K weight gradient summed in chunk order
+__global__ void ksplit_reduce_kernel(const float* __restrict__ part, int S, int64_t n,
+                                     const int32_t* __restrict__ active, float* __restrict__ out, int64_t s_out) {
+  const int w = blockIdx.y;
+  if (active && !active[w]) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float a = 0.f;
+    for (int q = 0; q < S; ++q) a += part[((int64_t)w * S + q) * n + i];
+    out[(int64_t)w * s_out + i] = a;
+  }
+}
+
 // ord[rank] = client, ranks by num_rows descending, ties by client index (a stable sort)
 __global__ void order_kernel(const int32_t* __restrict__ num_rows, int C, int32_t* __restrict__ ord) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -887,7 +936,8 @@ struct Work {
   float2* st0;
   BlockAct blk[8];
   float *feat, *logits, *dz, *dfeat, *rloss;
-  float *col, *dcol, *gA, *gB, *gT, *gTd, *sc;
+  float *col, *dcol, *gA, *gB, *gT, *gTd, *sc, *kpart;
+  int32_t* act_split;
   double2* part;
   float2* coef;
 };
@@ -955,6 +1005,14 @@ inline Work carve(const Net& n, int W, int B, bool train, Buf& b) {
   k.dfeat = b.take<float>((size_t)W * B * F);
   k.rloss = b.take<float>((size_t)W * B);
   k.col = b.take<float>((size_t)W * k.s_col);
+  int64_t kp_max = 0;  // split-K partials per slot
+  for (int j = 0; j < n.nconv; ++j) {
+    const Conv& v = n.convs[j];
+    const int S = ksplit(B * v.pout());
+    if (S > 1) kp_max = std::max(kp_max, (int64_t)S * v.kp() * v.co);
+  }
+  k.kpart = train && kp_max ? b.take<float>((size_t)W * kp_max) : nullptr;
+  k.act_split = b.take<int32_t>((size_t)W * 16);
   k.sc = b.take<float>((size_t)W * k.s_pool);  // downsample-branch output (<= a pooled map)
   k.part = b.take<double2>((size_t)W * B * max_part(n));
   k.coef = b.take<float2>((size_t)W * B * m.G);
@@ -988,6 +1046,10 @@ struct Ctx {
   cudaStream_t s;
 };
 
+// per-slot stride of conv cv's im2col rows: compact (B * P_out * kp), so the rows of all
+// slots form one uniformly strided array (the split-K weight gradient below relies on it)
+inline int64_t col_stride(const Ctx& c, const Conv& cv) { return (int64_t)c.B * cv.pout() * cv.kp(); }
+
 // im2col of conv cv over the NHWC source src (per-slot stride s_src)
 int im2col(const Ctx& c, const Conv& cv, const float* src, int64_t s_src) {
   const Work& k = *c.k;
@@ -996,10 +1058,10 @@ int im2col(const Ctx& c, const Conv& cv, const float* src, int64_t s_src) {
   const dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>((rows + kRows - 1) / kRows, 8192)), c.W);
   if (vec) FB_LAUNCH("rn_im2col_kernel", c.s, (im2col_kernel<true><<<grid, 256, 0, c.s>>>(
                                                   src, s_src, c.B, cv.ci, cv.hin, cv.k, cv.stride, cv.pad, cv.hout,
-                                                  cv.kp(), c.active, k.col, k.s_col)));
+                                                  cv.kp(), c.active, k.col, col_stride(c, cv))));
   else FB_LAUNCH("rn_im2col_kernel", c.s, (im2col_kernel<false><<<grid, 256, 0, c.s>>>(
                                               src, s_src, c.B, cv.ci, cv.hin, cv.k, cv.stride, cv.pad, cv.hout,
-                                              cv.kp(), c.active, k.col, k.s_col)));
+                                              cv.kp(), c.active, k.col, col_stride(c, cv))));
   return launch_status("rn im2col");
 }
 
@@ -1022,7 +1084,7 @@ inline ConvTable table(const Net& n) {
 int permute_weights(const Ctx& c) {
   const Work& k = *c.k;
   const int slots = c.sW ? c.W : 1;
-  FB_LAUNCH("rn_permute_kernel", c.s, (permute_kernel<<<dim3(grid_for(c.n->P), slots), 256, 0, c.s>>>(
+  FB_LAUNCH("rn_permute_kernel", c.s, (permute_kernel<<<dim3(64, slots, c.n->nconv), 256, 0, c.s>>>(
                                           table(*c.n), c.n->P, c.Wc, c.sW, k.wperm, c.n->P,
                                           c.sW ? c.active : nullptr, 1)));
   return launch_status("rn permute");
@@ -1034,7 +1096,7 @@ int conv_fwd(const Ctx& c, const Conv& cv, const float* src, int64_t s_src, floa
   if (st) return st;
   const Work& k = *c.k;
   Gemm g = gemm_base();
-  g.A = k.col; g.lda = cv.kp(); g.sA = k.s_col;
+  g.A = k.col; g.lda = cv.kp(); g.sA = col_stride(c, cv);
   g.B = k.wperm + cv.p_off; g.ldb = cv.kp(); g.sB = c.sW ? c.n->P : 0;
   g.C = y; g.ldc = cv.co; g.sC = s_y;
   g.M = c.B * cv.pout(); g.N = cv.co; g.K = cv.kp();
@@ -1060,8 +1122,8 @@ int gn_stats(const Ctx& c, const float* x, int64_t s_x, int P, int C, float2* st
 
 int gn_apply(const Ctx& c, const float* x, int64_t s_x, int P, int C, const float2* stats, const Norm& nm,
              const float* res, bool relu, float* y) {
-  const int64_t n = (int64_t)P * C;
-  const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + kT * 16 - 1) / (kT * 16), 1024));
+  const int64_t n = (int64_t)P * C / 4;
+  const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + kT * 4 - 1) / (kT * 4), 1024));
   FB_LAUNCH("rn_gn_apply_kernel", c.s, (gn_apply_kernel<<<dim3(gx, c.W, c.B), kT, 0, c.s>>>(
                                            x, s_x, P, C, c.n->m.G, stats, c.Wc, c.sW, nm.g_off, nm.b_off, res,
                                            relu ? 1 : 0, c.active, y)));
@@ -1138,8 +1200,8 @@ int gn_backward(const Ctx& c, const float* dy, const float* mask, const float* x
   FB_LAUNCH("rn_gn_param_grad_kernel", c.s,
             (gn_param_grad_kernel<<<dim3((C + warps - 1) / warps, c.W), 32 * warps, 0, c.s>>>(
                 k.part, c.B, C, nch, c.active, k.G, c.sW, nm.g_off, nm.b_off)));
-  const int64_t n = (int64_t)P * C;
-  const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + kT * 16 - 1) / (kT * 16), 1024));
+  const int64_t n = (int64_t)P * C / 4;
+  const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + kT * 4 - 1) / (kT * 4), 1024));
   FB_LAUNCH("rn_gn_bwd_apply_kernel", c.s, (gn_bwd_apply_kernel<<<dim3(gx, c.W, c.B), kT, 0, c.s>>>(
                                                dy, mask, x, s_x, P, C, G, stats, k.coef, c.Wc, c.sW, nm.g_off,
                                                c.active, dx)));
@@ -1154,17 +1216,29 @@ int conv_backward(const Ctx& c, const Conv& cv, const float* src, int64_t s_src,
   int st = im2col(c, cv, src, s_src);
   if (st) return st;
   Gemm g = gemm_base();  // dWp^T = col^T dT ([kp][co]: M = kp fills the 128-row tiles)
-  g.A = k.col; g.lda = cv.kp(); g.sA = k.s_col;
-  g.B = dT; g.ldb = cv.co; g.sB = s_T;
-  g.C = k.gperm + cv.p_off; g.ldc = cv.co; g.sC = c.n->P;
-  g.M = cv.kp(); g.N = cv.co; g.K = c.B * cv.pout();
-  g.active = c.active;
-  if ((st = rn_gemm(true, false, g, c.W, c.s))) return st;
+  const int rows = c.B * cv.pout(), S = ksplit(rows), Kc = rows / S;
+  g.A = k.col; g.lda = cv.kp(); g.sA = (int64_t)Kc * cv.kp();  // batch z = slot * S + chunk
+  g.B = dT; g.ldb = cv.co; g.sB = (int64_t)Kc * cv.co;
+  g.M = cv.kp(); g.N = cv.co; g.K = Kc;
+  if (S == 1) {
+    g.C = k.gperm + cv.p_off; g.ldc = cv.co; g.sC = c.n->P;
+    g.active = c.active;
+    if ((st = rn_gemm(true, false, g, c.W, c.s))) return st;
+  } else {
+    FB_LAUNCH("rn_expand_active_kernel", c.s, (expand_active_kernel<<<(c.W * S + 255) / 256, 256, 0, c.s>>>(
+                                                  c.active, c.W, S, k.act_split)));
+    g.C = k.kpart; g.ldc = cv.co; g.sC = (int64_t)cv.kp() * cv.co;
+    g.active = k.act_split;
+    if ((st = rn_gemm(true, false, g, c.W * S, c.s))) return st;
+    const int64_t n = (int64_t)cv.kp() * cv.co;
+    FB_LAUNCH("rn_ksplit_reduce_kernel", c.s, (ksplit_reduce_kernel<<<dim3(grid_for(n), c.W), 256, 0, c.s>>>(
+                                                  k.kpart, S, n, c.active, k.gperm + cv.p_off, c.n->P)));
+  }
   if (!dx) return FB_OK;
   g = gemm_base();  // dcol = dT Wp
   g.A = dT; g.lda = cv.co; g.sA = s_T;
   g.B = k.wperm + cv.p_off; g.ldb = cv.kp(); g.sB = c.n->P;
-  g.C = k.dcol; g.ldc = cv.kp(); g.sC = k.s_col;
+  g.C = k.dcol; g.ldc = cv.kp(); g.sC = col_stride(c, cv);
   g.M = c.B * cv.pout(); g.N = cv.kk(); g.K = cv.co;
   g.active = c.active;
   if ((st = rn_gemm(false, false, g, c.W, c.s))) return st;
@@ -1172,7 +1246,8 @@ int conv_backward(const Ctx& c, const Conv& cv, const float* src, int64_t s_src,
   const dim3 grid(grid_for(total), c.W);
 #define FB_RN_COL2IM(K_, S_)                                                                                     \
   FB_LAUNCH("rn_col2im_kernel", c.s, (col2im_kernel<K_, S_><<<grid, 256, 0, c.s>>>(                              \
-                                         k.dcol, k.s_col, cv.kp(), c.B, cv.ci, cv.hin, cv.pad, cv.hout, c.active, \
+                                         k.dcol, col_stride(c, cv), cv.kp(), c.B, cv.ci, cv.hin, cv.pad, cv.hout, \
+                                         c.active,                                                              \
                                          add, mask, accumulate ? 1 : 0, dx, s_dx)))
   if (cv.k == 3 && cv.stride == 1) FB_RN_COL2IM(3, 1);
   else if (cv.k == 3 && cv.stride == 2) FB_RN_COL2IM(3, 2);
@@ -1250,7 +1325,7 @@ int backward(const Ctx& c, bool eval_rows) {
                           nullptr, nullptr, false)))
     return st;
   // the conv gradients back into G's OIHW rows
-  FB_LAUNCH("rn_permute_kernel", c.s, (permute_kernel<<<dim3(grid_for(n.P), c.W), 256, 0, c.s>>>(
+  FB_LAUNCH("rn_permute_kernel", c.s, (permute_kernel<<<dim3(64, c.W, n.nconv), 256, 0, c.s>>>(
                                           table(n), n.P, k.gperm, c.sW, k.G, n.P, c.active, 0)));
   return launch_status("rn backward");
 }

@@ -162,17 +162,19 @@ def test_resnet_narrow_local_sgd_matches_oracle(E, B, lr, mu, gemm_impl):
     assert_updates(got, want, margins, f"narrow E={E} B={B} mu={mu}")
 
 
-def test_resnet_wide32_local_sgd_and_eval_match_oracle(gemm_impl):
-    """The full 64-wide ResNet-18 (every conv GEMM on the tcgen05 tiles) on 32 x 32 images."""
-    m, users = cohort(WIDE32, 4, seed=21, max_images=10)
+@pytest.mark.parametrize("B,max_images", [(4, 10), (16, 40)], ids=["B4", "B16-splitK"])
+def test_resnet_wide32_local_sgd_and_eval_match_oracle(gemm_impl, B, max_images):
+    """The full 64-wide ResNet-18 (every conv GEMM on the tcgen05 tiles) on 32 x 32 images;
+    at B = 16 the stem's weight gradient (K = 16 x 256 rows) runs split-K in 2 chunks."""
+    m, users = cohort(WIDE32, 4, seed=21, max_images=max_images)
     model = product_model(WIDE32)
     p0 = m.init(7)
     theta = port.flat(p0, m.dims)
-    got, bad = run_local_sgd(model, theta, users, 5, 1, 4, 0.05)
+    got, bad = run_local_sgd(model, theta, users, 5, 1, B, 0.05)
     margins = []
-    want = oracle_deltas(m, p0, users, 5, 1, 4, 0.05, margins=margins)
+    want = oracle_deltas(m, p0, users, 5, 1, B, 0.05, margins=margins)
     assert not bad.any()
-    assert_updates(got, want, margins, "wide32")
+    assert_updates(got, want, margins, f"wide32 B={B}")
     loss, corr = run_eval(model, theta, users, groups=2, B=4)
     for c, u in enumerate(users):
         ls, k = m.eval_counts(p0, u.features.astype(np.float64))
