@@ -298,3 +298,53 @@ def test_resnet_engine_central_iteration_with_adam_matches_oracle():
     assert_close_fp32(got, want, what="theta after one ResNet central iteration")
     mt = res.metrics[0] if isinstance(res.metrics, list) else res.metrics
     assert mt is not None
+
+
+def test_resnet_bench_shape_cohort_matches_oracle():
+    """Parity at the benchmarked configuration (bench.py --workload resnet): the bench's own
+    synthetic population, cohort 200 drawn by the engine's sampler, E = 2, B = 16, local lr
+    0.01, every client trained in the bench's largest-first waves; the float64 oracle
+    replays a sample of three clients (~0.5 s per image step on the host).
+
+    Over several local steps at 224 px, fp32 decision flips (see
+    test_resnet_configD_matches_oracle) also perturb every later step, so the reference
+    point is PyTorch's own fp32 training of the same clients (same batches, same update
+    rule): the gate is max(1e-3, 3 x that fp32 error) per client (both printed)."""
+    import bench
+
+    wl = bench.WORKLOADS["resnet"]
+    ds = bench.build(wl)[fb.Population.TRAIN]
+    m = port.ResNet18()
+    model = product_model({})
+    cohort_ids = port.sample_cohort(ds.user_ids, wl["cohort"], port.cohort_seed(0, 0, "train"))
+    users = [ds.users[u] for u in cohort_ids]
+    p0 = m.init(0)
+    theta = port.flat(p0, m.dims)
+    got, bad = run_local_sgd(model, theta, users, 17, wl["epochs"], wl["batch"], wl["lr"],
+                             wave=rn_glue.wave_size(model, wl["batch"], len(users)))
+    assert not bad.any()
+    sizes = np.array([u.num_points for u in users])
+    order = np.argsort(sizes)
+    sample = [int(order[0]), int(order[len(order) // 2]), int(order[int(0.8 * len(order))])]  # small / median / large
+    want = oracle_deltas(m, p0, [users[i] for i in sample], 17, wl["epochs"], wl["batch"], wl["lr"])
+    err = rel_err(got[sample], want)
+    floor = rel_err(np.array([torch_fp32_deltas(m, p0, users[i], 17, wl["epochs"], wl["batch"], wl["lr"])
+                              for i in sample]), want)
+    print(f"bench-shape ResNet parity: clients {sample} with {sizes[sample].tolist()} images: GPU errors "
+          f"{np.array2string(err, precision=2)}, torch fp32 {np.array2string(floor, precision=2)}")
+    assert (err <= np.maximum(1e-3, 3 * floor)).all(), (err, floor)
+
+
+def torch_fp32_deltas(m, p0, u, ctx_seed, E, B, lr):
+    """PyTorch fp32 (CPU) local training with the reference's update rule and batches."""
+    from tests.test_oracle_resnet import torch_resnet_loss
+
+    X = u.features.astype(np.float64)
+    perms = port.user_perms(ctx_seed, u.user_id, u.num_points, E)
+    p = {k: v.astype(np.float32) for k, v in p0.items()}
+    for e in range(E):
+        for s0 in range(0, u.num_points, B):
+            loss, t = torch_resnet_loss(m, p, X[perms[e, s0:s0 + B]], dtype=torch.float32)
+            loss.backward()
+            p = {k: (torch.from_numpy(p[k]) - lr * t[k].grad.reshape(-1)).numpy() for k in p}
+    return port.flat(p0, m.dims) - port.flat({k: v.astype(np.float64) for k, v in p.items()}, m.dims)
