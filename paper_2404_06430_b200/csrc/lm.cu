@@ -326,7 +326,9 @@ struct TcCfg {
   static constexpr int B_HI = BK_ ? B0 : B0 + B_RAW, B_LO = BK_ ? B0 + B_RAW : B0 + B_RAW + B_T;
   static constexpr int STAGE = B_LO + B_T;
   static constexpr int STAGES = STAGE <= 64 * 1024 ? 3 : 2;
-  static constexpr int SMEM = 1024 + STAGES * STAGE + 256;
+  static constexpr int EPI_BYTES = TC_EPI * 32 * 33 * 4;  // per-warp 32 x 32 transpose tiles (plain stores)
+  static constexpr int SMEM = 1024 + STAGES * STAGE + 256 + EPI_BYTES;
+  static_assert(SMEM <= 232448, "tcgen05 GEMM shared memory");
   static constexpr uint32_t IDESC = tc::idesc_tf32(TCM, BNT);
   static constexpr uint32_t TX = A_RAW + B_RAW;
 };
@@ -397,6 +399,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
   uint64_t* tfull = empty + S;                                         // [2] window accumulated
   uint64_t* tempty = tfull + 2;                                        // [2] window drained
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* epi_tile = reinterpret_cast<float*>(sm + S * Cfg::STAGE + 256);  // [TC_EPI][32][33]
+  const bool plain = g.beta == 0.f && !g.bias && !g.aux;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tn = (g.N + BNT - 1) / BNT, tm = (g.M + TCM - 1) / TCM;
   const int tiles = tn * tm * batch;
@@ -537,7 +541,29 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&tempty[buf]);
       }
-      if (m < g.M) {
+      if (plain) {
+        // alpha * acc only: each 32 x 32 sub-tile goes through the warp's private smem tile
+        // (row-per-lane in, column-per-lane out, 33-float pitch: conflict-free both ways), so
+        // every store instruction writes 128 contiguous bytes of one output row (the
+        // row-per-lane float4 stores touched 32 rows each -- the dcol / logits outputs)
+        float* tile = epi_tile + (warp - 2 - TC_CONV) * (32 * 33);
+        const int mrow0 = m0 + q * 32;
+#pragma unroll
+        for (int c0 = 0; c0 < EH; c0 += 32) {
+          // (EH = 48 for the 96-wide tiles: the second sub-tile is 16 columns wide)
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (c0 + j < EH) tile[lane * 33 + j] = g.alpha * sum[c0 + j];
+          __syncwarp();
+          const int col = n0 + c0 + lane;
+          const bool live = c0 + lane < EH && col < g.N;
+          for (int r = 0; r < 32; ++r) {
+            const int mr = mrow0 + r;
+            if (live && mr < g.M) g.C[(int64_t)z * g.sC + (int64_t)mr * g.ldc + col] = tile[r * 33 + lane];
+          }
+          __syncwarp();
+        }
+      } else if (m < g.M) {
         float* crow = g.C + (int64_t)z * g.sC + (int64_t)m * g.ldc;
         const float* bias = g.bias ? g.bias + (int64_t)z * g.sBias : nullptr;
         const float* arow = g.aux ? g.aux + (int64_t)z * g.sAux + (int64_t)m * g.ldaux : nullptr;
