@@ -355,6 +355,8 @@ def _tensor_evidence(name: str, frac: float) -> dict:
     out = {}
     if "tensor_pipe_pct" in k:
         out["tensor_pipe_active_pct"] = k["tensor_pipe_pct"]
+    if "tensor_ops_pct_of_peak" in k:
+        out["tensor_ops_pct_of_tf32_or_f16_peak"] = k["tensor_ops_pct_of_peak"]
     if "mma_ops_per_algorithmic" in k:
         out["issued_ops_per_algorithmic"] = k["mma_ops_per_algorithmic"]
         out["issued_frac"] = round(frac * k["mma_ops_per_algorithmic"], 4)
