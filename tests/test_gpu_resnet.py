@@ -348,3 +348,57 @@ def torch_fp32_deltas(m, p0, u, ctx_seed, E, B, lr):
             loss.backward()
             p = {k: (torch.from_numpy(p[k]) - lr * t[k].grad.reshape(-1)).numpy() for k in p}
     return port.flat(p0, m.dims) - port.flat({k: v.astype(np.float64) for k, v in p.items()}, m.dims)
+
+
+@pytest.mark.parametrize("algo", [dict(kind="scaffold", num_train_users=10), dict(kind="fedprox", mu=0.1)],
+                         ids=["scaffold", "fedprox"])
+def test_resnet_engine_algorithms_match_oracle(algo):
+    """SCAFFOLD and FedProx on config D's model through
+    GpuSimulationEngine, 3 central iterations with clip + injected noise + central Adam and
+    evaluation, against the oracle's run_fedavg (fedsim/algorithms/scaffold.py:28-120,
+    fedsim/algorithms/fedavg.py:201-296).  Per-iteration theta at rtol 1e-5 (atol 1e-6
+    max|ref|) unless the oracle's trajectory passed a decision within FLIP_MARGIN of its
+    threshold (then relative L2 <= 1e-2; printed)."""
+    from tests.conftest import assert_close_fp32
+    from tests.helpers import run_sim
+
+    m = port.ResNet18(**NARROW)
+    model = product_model(NARROW)
+    train = fb.make_synthetic_images(10, image=m.image, num_classes=m.num_classes, max_images=14, seed=8,
+                                     id_prefix="train")
+    val = fb.make_synthetic_images(4, image=m.image, num_classes=m.num_classes, max_images=6, seed=9,
+                                   population=fb.Population.VAL, id_prefix="val")
+    clip = fb.ClippingPostprocessor(0.1)
+    noise_base = 7
+    mech = fb.GaussianCentralMechanism(clip, sigma=1.0, r=0.2, noise_base_seed=noise_base, noise_source="numpy")
+    opt = fb.AdamOptimizer(0.05, beta1=0.9, beta2=0.99, adaptivity_degree=0.1)
+    weighting = "uniform" if algo["kind"] == "scaffold" else "datapoints"  # (SCAFFOLD averages uniformly)
+    kw = dict(total_iterations=3, cohort_size=5, local_learning_rate=0.01, local_num_epochs=2, local_batch_size=4,
+              eval_frequency=2, eval_cohort_size=3, weighting=weighting, run_seed=3, init_seed=4)
+    alg = (fb.Scaffold(model, opt, num_train_users=algo["num_train_users"], **kw) if algo["kind"] == "scaffold"
+           else fb.FedProx(model, opt, mu=algo["mu"], **kw))
+    eng = fb.GpuSimulationEngine({fb.Population.TRAIN: train, fb.Population.VAL: val}, postprocessors=[clip, mech])
+    thetas = []
+    res = run_sim(alg, eng, callbacks=[lambda p, rows, t: thetas.append(p.flat_host()) and False])
+    users = lambda ds: {u.user_id: (u.features.astype(np.float64), u.labels) for u in ds.users.values()}
+    port.MARGINS.clear()
+    port.TRACK_MARGINS = True
+    try:
+        want, rows, digest = port.run_fedavg(
+            m, users(train), users(val), iterations=3, cohort=5, eval_cohort=3, eval_every=2, lr=0.01, epochs=2,
+            batch=4, clr=0.05, weighting=weighting, bound=0.1, sigma=1.0, r=0.2, noise_base=noise_base,
+            run_seed=3, init_seed=4, algorithm=algo,
+            optimizer=dict(kind="adam", lr=0.05, beta1=0.9, beta2=0.99, eps=0.1))
+    finally:
+        port.TRACK_MARGINS = False
+    margin = min(port.MARGINS, default=np.inf)
+    assert res.cohort_digest == digest
+    got = np.array(thetas)[:, :want.shape[1]]
+    errs = np.linalg.norm(got - want, axis=1) / np.linalg.norm(want, axis=1)
+    print(f"ResNet {algo['kind']}: theta errors per iteration {np.array2string(errs, precision=2)}, "
+          f"min decision margin {margin:.1e}")
+    if margin >= FLIP_MARGIN:
+        for t in range(len(want)):
+            assert_close_fp32(got[t], want[t], what=f"ResNet {algo['kind']} theta after iteration {t}")
+    else:
+        assert errs.max() <= 1e-2, errs
