@@ -341,8 +341,11 @@ def _ncu_traffic(name: str):
     """DRAM bytes (read + write) of one launch of `name` from the committed
     ncu --set full capture (profiles/ncu_traffic.json), with the launch size."""
     k = _ncu_kernel(name)
-    if k is None:
+    if k is None or "dram_bytes" not in k:
         return None
+    if "slots" not in k:  # (grouped-GEMM entries: bytes summed over the captured launches)
+        return {"dram_bytes_captured": k["dram_bytes"], "launches_captured": k.get("launches"),
+                "source": "profiles/ncu_traffic.json"}
     return {"dram_bytes_per_launch": k["dram_bytes"], "slots_per_launch": k["slots"],
             "algorithmic_bytes_per_launch": k.get("algorithmic_bytes"), "source": "profiles/ncu_traffic.json"}
 
@@ -406,8 +409,8 @@ def roofline(report: dict, wl: dict, counts: dict, peaks: dict) -> tuple[dict, d
         peak = peaks.get("bf16_tflops", 1590.0) if k["bound"] == "tensor" else peaks.get("hbm_gbs", 6650.0)
         out.update(bound=k["bound"], achieved=k["achieved"], peak=peak, unit=k["unit"], frac=k["frac"],
                    traffic=_ncu_traffic(name),
-                   **{key: k[key] for key in ("tensor_pipe_active_pct", "issued_ops_per_algorithmic", "issued_frac")
-                      if key in k},
+                   **{key: k[key] for key in ("tensor_pipe_active_pct", "issued_ops_per_algorithmic", "issued_frac",
+                                              "tensor_ops_pct_of_tf32_or_f16_peak") if key in k},
                    peak_source=(("MEASURED_PEAKS.json bf16_tflops (dense bf16 cuBLAS); the kernel's own math is "
                                  + k.get("math", "") + ": three kind::tf32 MMAs per algorithmic product at half the "
                                  "bf16 rate -> at most 1/6 of this peak") if "TF32" in k.get("math", "") and

@@ -656,52 +656,56 @@ __global__ void gn_param_grad_kernel(const double2* __restrict__ part, int B, in
 }
 
 // ----------------------------------------------------------------- maxpool
-// 3x3 / 2, pad 1; ties to the first maximum in row-major window order
-__global__ void maxpool_kernel(const float* __restrict__ a, int64_t s_a, int B, int C, int hin, int hout,
+// 3x3 / 2, pad 1; ties to the first maximum in row-major window order.  Grid (x, slot,
+// image); 4 channels per thread (C % 4 == 0), 32-bit indices within the image.
+__global__ void maxpool_kernel(const float* __restrict__ a, int64_t s_a, int C, int hin, int hout,
                                const int32_t* __restrict__ active, float* __restrict__ y, int64_t s_y,
                                uint8_t* __restrict__ arg) {
-  const int w = blockIdx.y;
+  const int w = blockIdx.y, b = blockIdx.z;
   if (active && !active[w]) return;
-  const int64_t total = (int64_t)B * hout * hout * C;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(i % C);
-    const int64_t pix = i / C;
-    const int b = (int)(pix / ((int64_t)hout * hout));
-    const int rem = (int)(pix - (int64_t)b * hout * hout);
-    const int oy = rem / hout, ox = rem - oy * hout;
-    float best = -INFINITY;
-    int bi = 0;
+  const int c4n = C / 4, n = hout * hout * c4n;
+  const float* ab = a + (int64_t)w * s_a + (int64_t)b * hin * hin * C;
+  float* yb = y + (int64_t)w * s_y + (int64_t)b * hout * hout * C;
+  uint8_t* gb = arg + (int64_t)w * s_y + (int64_t)b * hout * hout * C;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int c = (i % c4n) * 4, pix = i / c4n;
+    const int oy = pix / hout, ox = pix - oy * hout;
+    float best[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    int bi[4] = {0, 0, 0, 0};
     for (int ky = 0; ky < 3; ++ky) {
       const int iy = oy * 2 - 1 + ky;
       if (iy < 0 || iy >= hin) continue;
       for (int kx = 0; kx < 3; ++kx) {
         const int ix = ox * 2 - 1 + kx;
         if (ix < 0 || ix >= hin) continue;
-        const float v = a[(int64_t)w * s_a + (((int64_t)b * hin + iy) * hin + ix) * C + c];
-        if (v > best) {
-          best = v;
-          bi = ky * 3 + kx;
-        }
+        const float4 v = *reinterpret_cast<const float4*>(ab + (iy * hin + ix) * C + c);
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (vv[e] > best[e]) {
+            best[e] = vv[e];
+            bi[e] = ky * 3 + kx;
+          }
       }
     }
-    y[(int64_t)w * s_y + i] = best;
-    arg[(int64_t)w * s_y + i] = (uint8_t)bi;
+    *reinterpret_cast<float4*>(yb + pix * C + c) = make_float4(best[0], best[1], best[2], best[3]);
+    *reinterpret_cast<uchar4*>(gb + pix * C + c) = make_uchar4(bi[0], bi[1], bi[2], bi[3]);
   }
 }
 
-__global__ void maxpool_bwd_kernel(const float* __restrict__ dy, const uint8_t* __restrict__ arg, int64_t s_y, int B,
-                                   int C, int hin, int hout, const int32_t* __restrict__ active,
-                                   float* __restrict__ da, int64_t s_a) {
-  const int w = blockIdx.y;
+__global__ void maxpool_bwd_kernel(const float* __restrict__ dy, const uint8_t* __restrict__ arg, int64_t s_y, int C,
+                                   int hin, int hout, const int32_t* __restrict__ active, float* __restrict__ da,
+                                   int64_t s_a) {
+  const int w = blockIdx.y, b = blockIdx.z;
   if (active && !active[w]) return;
-  const int64_t total = (int64_t)B * hin * hin * C;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(i % C);
-    const int64_t pix = i / C;
-    const int b = (int)(pix / ((int64_t)hin * hin));
-    const int rem = (int)(pix - (int64_t)b * hin * hin);
-    const int y = rem / hin, x = rem - y * hin;
-    float s = 0.f;
+  const int c4n = C / 4, n = hin * hin * c4n;
+  const float* db = dy + (int64_t)w * s_y + (int64_t)b * hout * hout * C;
+  const uint8_t* gb = arg + (int64_t)w * s_y + (int64_t)b * hout * hout * C;
+  float* ob = da + (int64_t)w * s_a + (int64_t)b * hin * hin * C;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int c = (i % c4n) * 4, pix = i / c4n;
+    const int y = pix / hin, x = pix - y * hin;
+    float s[4] = {0.f, 0.f, 0.f, 0.f};
     // windows (oy, ox) with 2 oy - 1 <= y <= 2 oy + 1, in row-major order
     for (int oy = max(0, (y - 1) / 2); oy <= min(hout - 1, (y + 1) / 2); ++oy) {
       const int ky = y - (oy * 2 - 1);
@@ -709,11 +713,17 @@ __global__ void maxpool_bwd_kernel(const float* __restrict__ dy, const uint8_t* 
       for (int ox = max(0, (x - 1) / 2); ox <= min(hout - 1, (x + 1) / 2); ++ox) {
         const int kx = x - (ox * 2 - 1);
         if (kx < 0 || kx > 2) continue;
-        const int64_t o = (((int64_t)b * hout + oy) * hout + ox) * C + c;
-        if (arg[(int64_t)w * s_y + o] == ky * 3 + kx) s += dy[(int64_t)w * s_y + o];
+        const int o = (oy * hout + ox) * C + c;
+        const uchar4 g4 = *reinterpret_cast<const uchar4*>(gb + o);
+        const float4 d4 = *reinterpret_cast<const float4*>(db + o);
+        const int tap = ky * 3 + kx;
+        if (g4.x == tap) s[0] += d4.x;
+        if (g4.y == tap) s[1] += d4.y;
+        if (g4.z == tap) s[2] += d4.z;
+        if (g4.w == tap) s[3] += d4.w;
       }
     }
-    da[(int64_t)w * s_a + i] = s;
+    *reinterpret_cast<float4*>(ob + pix * C + c) = make_float4(s[0], s[1], s[2], s[3]);
   }
 }
 
@@ -1143,8 +1153,9 @@ int forward(const Ctx& c) {
   if ((st = conv_fwd(c, n.stem, k.stem_in, s_in0, k.c1, k.s_stem))) return st;
   if ((st = gn_stats(c, k.c1, k.s_stem, Ps, w, k.st0))) return st;
   if ((st = gn_apply(c, k.c1, k.s_stem, Ps, w, k.st0, n.n0, nullptr, true, k.a1))) return st;
-  FB_LAUNCH("rn_maxpool_kernel", c.s, (maxpool_kernel<<<dim3(grid_for(k.s_pool), c.W), 256, 0, c.s>>>(
-                                          k.a1, k.s_stem, c.B, w, n.hs, n.hp, c.active, k.m1, k.s_pool, k.arg)));
+  const unsigned gp = (unsigned)((n.hp * n.hp * (w / 4) + 255) / 256);
+  FB_LAUNCH("rn_maxpool_kernel", c.s, (maxpool_kernel<<<dim3(gp, c.W, c.B), 256, 0, c.s>>>(
+                                          k.a1, k.s_stem, w, n.hs, n.hp, c.active, k.m1, k.s_pool, k.arg)));
   const float* x = k.m1;
   int64_t s_x = k.s_pool;
   for (int i = 0; i < 8; ++i) {
@@ -1318,8 +1329,9 @@ int backward(const Ctx& c, bool eval_rows) {
     std::swap(dout, dnext);
   }
   // stem: dout = d(maxpool output) -> d a1 (into dnext, stem stride) -> GN (mask a1) -> conv dW
-  FB_LAUNCH("rn_maxpool_bwd_kernel", c.s, (maxpool_bwd_kernel<<<dim3(grid_for(k.s_stem), c.W), 256, 0, c.s>>>(
-                                              dout, k.arg, k.s_pool, c.B, w, n.hs, n.hp, c.active, dnext, k.s_stem)));
+  const unsigned gb = (unsigned)((n.hs * n.hs * (w / 4) + 255) / 256);
+  FB_LAUNCH("rn_maxpool_bwd_kernel", c.s, (maxpool_bwd_kernel<<<dim3(gb, c.W, c.B), 256, 0, c.s>>>(
+                                              dout, k.arg, k.s_pool, w, n.hs, n.hp, c.active, dnext, k.s_stem)));
   if ((st = gn_backward(c, dnext, k.a1, k.c1, k.s_stem, n.stem.pout(), w, k.st0, n.n0, k.gT))) return st;
   if ((st = conv_backward(c, n.stem, k.stem_in, (int64_t)c.B * n.m.S * n.m.S * 3, k.gT, k.s_stem, nullptr, 0,
                           nullptr, nullptr, false)))
