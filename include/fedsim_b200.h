@@ -140,8 +140,9 @@ int fb_local_sgd_mlp_f32(const float* theta_t, int dim, int hidden, int num_clas
 int64_t fb_cnn_workspace_bytes(int max_slots, int max_clients, int hist_steps);
 /* Validation knob: 1 (default) = the convolutions on tcgen05; 2 = tcgen05
  * with the conv2 forward on 2-CTA clusters (cta_group::2, M = 256; correct,
- * measured slower); 0 = the FP32 CUDA-core kernels kept as an independent
- * check.                                                                    */
+ * measured slower); 3 = tcgen05 with the conv1 forward on the im2col-staged
+ * kernel instead of the implicit GEMM; 0 = the FP32 CUDA-core kernels kept as
+ * an independent check.                                                     */
 int fb_cnn_set_conv_impl(int impl);
 /* perms / perm_off nullable: when given, client c's evaluated rows are epoch 0's
  * perms[perm_off[c] + min(skip, n_c) ..] (the rows past the first local batch, whose

@@ -3190,6 +3190,227 @@ __global__ void __launch_bounds__(C1F_THREADS, C1F_MINB) conv1_fwd_tc_kernel(
   if (warp == 0) tc::tmem_dealloc<128>(tmem);
 }
 
+// ------------------------------- conv1 forward as an implicit GEMM (tcgen05)
+// Same result as conv1_fwd_tc_kernel without the im2col staging.  Output rows
+// live on the image's 32-wide grid (row r = y * 32 + x, x >= 30 / y >= 30 rows
+// are computed and dropped), so tap (ky, kx) of a 128-row tile is the converted
+// image shifted by ky * 32 + kx rows: one smem descriptor per tap, nine
+// kind::tf32 M = 128, N = 64, K = 8 MMAs per tile.  The image is converted once
+// per sample into two K-major no-swizzle arrays of 16-byte rows (core-matrix
+// rows, SBO = 128 B, so a row shift is a 16-byte start-address shift):
+//   H[pos] = (x0 hi, x1 hi, x2 hi, 1)   L[pos] = (x0 lo, x1 lo, x2 lo, 0)
+// and the K = 8 step of tap t reads (H | L) at LBO = |H|.  B for tap t
+// (N = 64 rows x the same two 16-byte K chunks):
+//   rows o      : (W hi[o, :, t], b hi [t = 0]) | 0
+//   rows 32 + o : (W lo[o, :, t], b lo [t = 0]) | (W hi[o, :, t], 0)
+// so D[:, o] = xhi Whi + b hi and D[:, 32 + o] = xhi Wlo + xlo Whi + b lo -- the
+// 3xTF32 split of conv1_fwd_tc_kernel, the small cross terms summed apart from
+// the main products as there.  The per-sample image is prefetched
+// into registers one sample ahead (thread = 4 positions x 3 channels) and the
+// MMAs of tile i + 1 are issued before the epilogue of tile i (double-buffered
+// TMEM); one converted-image buffer (rewritten after the sample's last MMAs)
+// keeps the CTA at ~55 KB so that 4 CTAs share an SM.
+__device__ __forceinline__ void stg256(void* p, const uint32_t (&v)[8]) {
+  asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]),
+               "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]) : "memory");
+}
+constexpr int CIG_ROWS = 1096;                // >= 7 * 128 + 127 + 2 * 32 + 2 + 1, multiple of 8
+constexpr int CIG_ARR = CIG_ROWS * 16;        // one 16-byte-row array (H or L)
+constexpr int CIG_BUF = 2 * CIG_ARR;          // H | L of one sample
+constexpr int CIG_B = 9 * 2 * 64 * 16;        // per tap: 2 K chunks x 64 rows x 16 B
+#ifndef CIG_MINB
+#define CIG_MINB 4  // CTAs per SM (one converted-image buffer: ~55 KB of smem per CTA; 3 measured 2.82 vs 2.76 ms)
+#endif
+constexpr int CIG_SMEM = 1024 + CIG_B + CIG_BUF + 64;
+static_assert(CIG_ROWS >= (C1F_TILES - 1) * C1F_TILE + C1F_TILE + 2 * S0 + 2 && CIG_ROWS % 8 == 0, "conv1 ig rows");
+static_assert(C1F_TILES * C1F_TILE >= S1 * S0 - (S0 - S1), "conv1 ig tiles cover the 30 output rows");
+
+__global__ void __launch_bounds__(C1F_THREADS, CIG_MINB) conv1_fwd_ig_kernel(
+    const float* __restrict__ X, const int64_t* __restrict__ slot_row, const float* __restrict__ theta,
+    const float* __restrict__ delta, int64_t ld, int B, int N, int G, __half* __restrict__ a1fh,
+    __half* __restrict__ a1fl, float* __restrict__ a1scale) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sB = sm;
+  uint8_t* sC = sm + CIG_B;                                      // H | L of the current sample
+  uint64_t* done = reinterpret_cast<uint64_t*>(sC + CIG_BUF);  // [2] MMA completion per TMEM buffer
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 2);
+  __shared__ float wsum[C1];  // sum_k |W[o, k]| (a1 bound)
+  __shared__ float red[8];
+  __shared__ float s_scale[2];
+  __shared__ int s_slot[C1F_GMAX];
+  __shared__ int s_ns;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, t = threadIdx.x;
+  const int n0 = blockIdx.x * G;
+  {
+    const int b = threadIdx.x;
+    if (!__syncthreads_or(b < G && n0 + b < N && slot_row[n0 + b] >= 0)) return;
+  }
+  const float* dc = delta ? delta + (int64_t)(n0 / B) * ld : nullptr;
+  const uint32_t sB0 = tc::smem_u32(sB), sC0 = tc::smem_u32(sC);
+  // zero B and the pad rows of both converted buffers (never overwritten)
+  for (int i = t; i < CIG_B / 16; i += C1F_THREADS) reinterpret_cast<uint4*>(sB)[i] = make_uint4(0, 0, 0, 0);
+  for (int i = t; i < 2 * (CIG_ROWS - S0 * S0); i += C1F_THREADS) {
+    const int r = i % (CIG_ROWS - S0 * S0), a = i / (CIG_ROWS - S0 * S0);  // a = array (H, L)
+    reinterpret_cast<uint4*>(sC + a * CIG_ARR)[S0 * S0 + r] = make_uint4(0, 0, 0, 0);
+  }
+  static_assert(C1F_THREADS % 32 == 0 && (C1 * 32) % C1F_THREADS == 0, "conv1 ig weight staging");
+  float wv[C1 * 32 / C1F_THREADS];
+#pragma unroll
+  for (int u = 0; u < C1 * 32 / C1F_THREADS; ++u) {
+    const int i = t + u * C1F_THREADS, o = i >> 5, k = i & 31;
+    wv[u] = k < 27 ? wt(theta, dc, O_W1 + o * 27 + k) : (k == 27 ? wt(theta, dc, O_B1 + o) : 0.f);
+  }
+  __syncthreads();  // B zeroed before the scatter
+#pragma unroll
+  for (int u = 0; u < C1 * 32 / C1F_THREADS; ++u) {
+    const int i = t + u * C1F_THREADS, o = i >> 5, k = i & 31;
+    float hi, lo;
+    tc::split_tf32(wv[u], hi, lo);
+    if (k < 27) {
+      const int ci = k / 9, tap = k - ci * 9;
+      const uint32_t tb = sB0 + tap * 2048 + 4 * ci;
+      tc::sts_f32(tb + o * 16, hi);                // rows o, chunk 0 (x hi): W hi
+      tc::sts_f32(tb + (C1 + o) * 16, lo);         // rows 32 + o, chunk 0 (x hi): W lo
+      tc::sts_f32(tb + 1024 + (C1 + o) * 16, hi);  // rows 32 + o, chunk 1 (x lo): W hi
+    } else if (k == 27) {                          // bias against the constant-1 column of H (tap 0)
+      tc::sts_f32(sB0 + o * 16 + 12, hi);
+      tc::sts_f32(sB0 + (C1 + o) * 16 + 12, lo);
+    }
+    const float sw = warp_sum(k < 27 ? fabsf(wv[u]) : 0.f);
+    if (lane == 0) wsum[o] = sw;
+  }
+  if (warp == 0) {
+    const bool a = lane < G && n0 + lane < N && slot_row[n0 + lane] >= 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, a);
+    if (a) s_slot[__popc(bal & ((1u << lane) - 1u))] = n0 + lane;
+    if (lane == 0) s_ns = __popc(bal);
+  }
+  if (t == 0) {
+    tc::mbar_init(&done[0], 1);
+    tc::mbar_init(&done[1], 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc<128>(tmem_slot);
+  tc::fence_proxy_async();
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int ns = s_ns;
+  if (ns == 0) {
+    if (warp == 0) tc::tmem_dealloc<128>(tmem);
+    return;
+  }
+  // image prefetch: thread t holds positions t + 256 u (u < 4), channels 0..2
+  float xr[4][C0];
+  auto load_raw = [&](int j) {
+    const float* x = X + slot_row[s_slot[j]] * IMG;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int ci = 0; ci < C0; ++ci) xr[u][ci] = __ldg(x + ci * S0 * S0 + t + 256 * u);
+  };
+  // convert the prefetched image of sample j into the image buffer, then the CTA max |x|
+  // and (warp 0) the per-sample a1 scale of conv1_fwd_tc_kernel
+  auto convert = [&](int j) {
+    const uint32_t h = sC0, l = h + CIG_ARR;
+    float xm = 0.f;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      float hv[C0], lv[C0];
+#pragma unroll
+      for (int ci = 0; ci < C0; ++ci) {
+        xm = fmaxf(xm, fabsf(xr[u][ci]));
+        tc::split_tf32(xr[u][ci], hv[ci], lv[ci]);
+      }
+      const uint32_t off = 16 * (t + 256 * u);
+      asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(h + off), "f"(hv[0]), "f"(hv[1]), "f"(hv[2]),
+                   "f"(1.f) : "memory");
+      asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(l + off), "f"(lv[0]), "f"(lv[1]), "f"(lv[2]),
+                   "f"(0.f) : "memory");
+    }
+    xm = warp_max(xm);
+    if (lane == 0) red[warp] = xm;
+    __syncthreads();
+    if (warp == 0) {
+      float m = lane < C1F_THREADS / 32 ? red[lane] : 0.f;
+      m = warp_max(m);
+      const float bound = warp_max(fabsf(wt(theta, dc, O_B1 + lane)) + m * wsum[lane]);
+      if (lane == 0) {
+        const float scv = bound > 0.f ? exp2f(14.f - ceilf(log2f(bound))) : 1.f;
+        s_scale[j & 1] = scv;
+        a1scale[s_slot[j]] = scv;
+      }
+    }
+  };
+  auto issue = [&](int i) {  // warp 0: nine tap MMAs of tile i into TMEM buffer i & 1
+    if (warp != 0) return;
+    if (tc::elect_one()) {
+      const int j = i / C1F_TILES, tile = i - j * C1F_TILES;
+      const uint32_t a0 = sC0 + tile * C1F_TILE * 16, d = tmem + (i & 1) * 64;
+#pragma unroll
+      for (int tap = 0; tap < 9; ++tap) {
+        const uint32_t a = a0 + ((tap / 3) * S0 + tap % 3) * 16;
+        tc::mma_tf32(d, tc::sdesc(a, CIG_ARR, 128, 0), tc::sdesc(sB0 + tap * 2048, 1024, 128, 0), C1F_IDESC2,
+                     tap != 0);
+      }
+      tc::mma_commit(&done[i & 1]);
+    }
+    __syncwarp();
+  };
+  const int q = warp & 3, chh = warp >> 2;
+  const int T = ns * C1F_TILES;
+  load_raw(0);
+  convert(0);
+  if (ns > 1) load_raw(1);
+  tc::fence_proxy_async();
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  issue(0);
+  for (int i = 0; i < T; ++i) {
+    const int j = i / C1F_TILES, tile = i - j * C1F_TILES;
+    if (i + 1 < T && tile == C1F_TILES - 1) {  // tile i + 1 starts sample j + 1
+      tc::mbar_wait(&done[i & 1], (i >> 1) & 1);  // sample j's last MMAs (and all before) read the buffer
+      convert(j + 1);
+      if (j + 2 < ns) load_raw(j + 2);
+      tc::fence_proxy_async();
+    }
+    tc::tc_fence_before();
+    __syncthreads();  // every thread past the epilogue of tile i - 1 (TMEM buffer (i + 1) & 1 is free)
+    tc::tc_fence_after();
+    if (i + 1 < T) issue(i + 1);
+    // epilogue of tile i (overlaps tile i + 1's MMAs)
+    tc::mbar_wait(&done[i & 1], (i >> 1) & 1);
+    tc::tc_fence_after();
+    uint32_t v0[16], v1[16];
+    const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (i & 1) * 64 + chh * 16;
+    tc::tmem_ld16(base, v0);
+    tc::tmem_ld16(base + C1, v1);
+    tc::tmem_ld_wait();
+    const int r = tile * C1F_TILE + q * 32 + lane, y = r >> 5, x = r & 31;
+    if (x < S1 && y < S1) {
+      const float sc = s_scale[j & 1];
+      uint32_t hw[8], lw[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float z0 = fmaxf(__uint_as_float(v0[2 * e]) + __uint_as_float(v1[2 * e]), 0.f) * sc;
+        const float z1 = fmaxf(__uint_as_float(v0[2 * e + 1]) + __uint_as_float(v1[2 * e + 1]), 0.f) * sc;
+        split_f16x2(z0, z1, hw[e], lw[e]);
+      }
+      // one full 32-byte sector per lane and part (256-bit stores; the workspace is 256-byte aligned)
+      const int64_t off = (int64_t)s_slot[j] * A1 + (int64_t)(y * S1 + x) * C1 + chh * 16;
+      stg256(a1fh + off, hw);
+      stg256(a1fl + off, lw);
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  if (warp == 0) tc::tmem_dealloc<128>(tmem);
+}
+
 // ------------------------------------------ conv1 backward-weights (tcgen05)
 // dW1[o, k] = sum over the client's samples and positions p of dz1[p, o] * xcol[p, k],
 // k = (ci, ky, kx) (27) plus a constant-1 column k = 27 that yields the bias
@@ -3437,6 +3658,8 @@ int g_conv_impl = 1;  // 1 = tcgen05 (product path), 0 = FP32 CUDA-core kernels 
 // conv2 forward on CTA pairs (conv2_fwd_tc2_kernel): correct (tests) but measured slower
 // than the single-CTA kernel (10.7 vs 7.9 ms per iteration), so off by default
 bool g_conv2_pairs = false;
+// conv1 forward: 1 = implicit GEMM (conv1_fwd_ig_kernel, default), 0 = im2col staging (conv1_fwd_tc_kernel)
+int g_conv1_fwd_impl = 1;
 
 
 // ------------------------------------------------ conv2 backward-weights (tcgen05)
@@ -3787,6 +4010,7 @@ int set_smem_limits() {
   cudaFuncSetAttribute(conv1_bwd_w_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, W1_SMEM);
   cudaFuncSetAttribute(conv1_bwd_w_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, W1_SMEM);
   cudaFuncSetAttribute(conv1_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C1F_SMEM);
+  cudaFuncSetAttribute(conv1_fwd_ig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, CIG_SMEM);
   cudaFuncSetAttribute(fc1_mat_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FMT_SMEM);
   cudaFuncSetAttribute(conv2_wimg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, WIMG_BYTES);
   cudaFuncSetAttribute(conv2_wimgT_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, WIMGT_BYTES);
@@ -3831,8 +4055,12 @@ int forward(const float* X, const float* theta, const float* delta, int64_t ld, 
   if (tc) {
     // slots per CTA: (part of) one client's batch (its own weights), or 16 at theta_t
     const int g1 = delta ? B / client_split(active, B, 2) : C1F_GMAX;
-    FB_LAUNCH("conv1_fwd_tc_kernel", s, conv1_fwd_tc_kernel<<<(N + g1 - 1) / g1, C1F_THREADS, C1F_SMEM, s>>>(
-                                            X, w.slot_row, theta, delta, ld, B, N, g1, w.a1fh, w.a1fl, w.a1scale));
+    if (g_conv1_fwd_impl == 1)
+      FB_LAUNCH("conv1_fwd_ig_kernel", s, conv1_fwd_ig_kernel<<<(N + g1 - 1) / g1, C1F_THREADS, CIG_SMEM, s>>>(
+                                              X, w.slot_row, theta, delta, ld, B, N, g1, w.a1fh, w.a1fl, w.a1scale));
+    else
+      FB_LAUNCH("conv1_fwd_tc_kernel", s, conv1_fwd_tc_kernel<<<(N + g1 - 1) / g1, C1F_THREADS, C1F_SMEM, s>>>(
+                                              X, w.slot_row, theta, delta, ld, B, N, g1, w.a1fh, w.a1fl, w.a1scale));
   } else {
     FB_LAUNCH("conv1_fwd_kernel", s, conv1_fwd_kernel<<<N, 256, 0, s>>>(X, w.slot_row, theta, delta, ld, B, w.a1,
                                                                         nullptr, nullptr, w.a1scale));
@@ -3924,6 +4152,7 @@ int fb_cnn_fc1_aggregate_f32(const float* coef, int num_clients, int batch_size,
   if (st) return st;
   cudaStream_t s = fb::as_stream(stream);
   Work w;
+  FB_REQUIRE(reinterpret_cast<uintptr_t>(workspace) % 256 == 0, "cnn: workspace must be 256-byte aligned");
   carve(workspace, max_slots, per, hist_steps, &w);
   const int B = batch_size, C = num_clients, N = C * B;
   Hist hs{};
@@ -3952,10 +4181,12 @@ int fb_cnn_fc1_aggregate_f32(const float* coef, int num_clients, int batch_size,
 }
 
 int fb_cnn_set_conv_impl(int impl) {
-  FB_REQUIRE(impl >= 0 && impl <= 2,
-             "fb_cnn_set_conv_impl: 0 (FP32 CUDA cores), 1 (tcgen05) or 2 (tcgen05, CTA-pair conv2 forward)");
+  FB_REQUIRE(impl >= 0 && impl <= 3,
+             "fb_cnn_set_conv_impl: 0 (FP32 CUDA cores), 1 (tcgen05), 2 (tcgen05, CTA-pair conv2 forward) or 3 "
+             "(tcgen05, im2col-staged conv1 forward)");
   fb::cnn::g_conv_impl = impl == 0 ? 0 : 1;
   fb::cnn::g_conv2_pairs = impl == 2;
+  fb::cnn::g_conv1_fwd_impl = impl == 3 ? 0 : 1;
   return FB_OK;
 }
 
@@ -3975,6 +4206,7 @@ int fb_eval_cnn_f32(const float* theta, const float* X, const int32_t* y, const 
   if (st) return st;
   cudaStream_t s = fb::as_stream(stream);
   Work w;
+  FB_REQUIRE(reinterpret_cast<uintptr_t>(workspace) % 256 == 0, "cnn: workspace must be 256-byte aligned");
   carve(workspace, max_slots, num_clients, 0, &w);
   const int N = (max_slots / GMAX) * GMAX;
   cudaMemsetAsync(loss_sum, 0, sizeof(double) * num_clients, s);
@@ -4052,6 +4284,7 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
   if (st) return st;
   cudaStream_t s = fb::as_stream(stream);
   Work w;
+  FB_REQUIRE(reinterpret_cast<uintptr_t>(workspace) % 256 == 0, "cnn: workspace must be 256-byte aligned");
   carve(workspace, max_slots, per, hist_steps, &w);
   const bool fact = hist_steps > 0;
   const int64_t tot4 = (int64_t)num_clients * (ld_delta / 4);
