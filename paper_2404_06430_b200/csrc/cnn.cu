@@ -59,6 +59,12 @@ struct Step {
   float lr, mu;
 };
 
+// 256-bit global store (sm_100): one full 32-byte sector per lane; p 32-byte aligned
+__device__ __forceinline__ void stg256(void* p, const uint32_t (&v)[8]) {
+  asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]),
+               "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]) : "memory");
+}
+
 // Factored fc1 (see "fc1 in factored form" below): per-step history of the
 // pooled activations and fc1 output gradients of every slot, the per-step
 // batch sizes, and the per-client Gram matrix of the pooled rows.
@@ -989,7 +995,7 @@ __global__ void __launch_bounds__(128) fc1_gram_kernel(Hist hs, int B) {
   }
 }
 
-// Split-K Gram for the current step: grid (C, nks, 4), CTA = 2 warps, warp owns
+// Split-K Gram for the current step: grid (4, nks, C), CTA = 2 warps, warp owns
 // history rows j = 16 z + 8 w .. +7, lane = 4 consecutive k (float4, strided by 128
 // over the CTA's K range): per k-quad the lane loads the step's nb <= GM new rows and
 // its 8 history rows (coalesced 512-byte warp loads, 18 in flight per warp) and does
@@ -1004,10 +1010,13 @@ constexpr int GR_Z = FC_RMAX / (GR_JW * GR_WARPS);  // 4 row groups
 static_assert(FLAT % (GR_KS * 128) == 0 && FLAT % (7 * 128) == 0, "gram K split");
 template <int GM>
 __global__ void __launch_bounds__(GR_WARPS * 32) fc1_gram_split_kernel(Hist hs, int B, double* __restrict__ part) {
-  const int c = blockIdx.x, ks = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // grid (row groups, K splits, clients): the row-group CTAs of one (client, K split) read
+  // the same new rows and run back to back, so the rereads hit L2 (client-fastest order sent
+  // them to DRAM: a row group's pass over all clients is ~500 MB)
+  const int c = blockIdx.z, ks = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int s = hs.s, J = (s + 1) * B;
   const int nb = hs.nbh[s * hs.cstride + c];
-  const int j0 = (blockIdx.z * GR_WARPS + warp) * GR_JW;
+  const int j0 = (blockIdx.x * GR_WARPS + warp) * GR_JW;
   if (nb == 0 || j0 >= J) return;
   // new rows are consecutive slots of step s; history rows as 32-bit element offsets
   // (the host checks S * N * FLAT < 2^31)
@@ -2946,9 +2955,10 @@ __global__ void __launch_bounds__(BX_THREADS, 1) conv2_bwd_x_tc_kernel(
             o[j] = m0 ? z0 : 0.f;
             o[j + 1] = m1 ? z1 : 0.f;
           }
-          float4* o4 = reinterpret_cast<float4*>(dz1 + off);
-          o4[0] = make_float4(o[0], o[1], o[2], o[3]);
-          o4[1] = make_float4(o[4], o[5], o[6], o[7]);
+          uint32_t ov[8];  // one 32-byte sector per lane (256-bit store)
+#pragma unroll
+          for (int e = 0; e < 8; ++e) ov[e] = __float_as_uint(o[e]);
+          stg256(dz1 + off, ov);
         }
       }
     }
@@ -3210,10 +3220,6 @@ __global__ void __launch_bounds__(C1F_THREADS, C1F_MINB) conv1_fwd_tc_kernel(
 // MMAs of tile i + 1 are issued before the epilogue of tile i (double-buffered
 // TMEM); one converted-image buffer (rewritten after the sample's last MMAs)
 // keeps the CTA at ~55 KB so that 4 CTAs share an SM.
-__device__ __forceinline__ void stg256(void* p, const uint32_t (&v)[8]) {
-  asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]),
-               "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]) : "memory");
-}
 constexpr int CIG_ROWS = 1096;                // >= 7 * 128 + 127 + 2 * 32 + 2 + 1, multiple of 8
 constexpr int CIG_ARR = CIG_ROWS * 16;        // one 16-byte-row array (H or L)
 constexpr int CIG_BUF = 2 * CIG_ARR;          // H | L of one sample
@@ -4343,7 +4349,7 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
 #define GR_NKS 7
 #endif
         const int gks = Cw * GR_NKS >= 4 * g_num_sms ? GR_NKS : 14;  // more K splits for a small shard
-        const dim3 ggrid(Cw, gks, std::min(GR_Z, (int)((step + 1) * B + GR_JW * GR_WARPS - 1) / (GR_JW * GR_WARPS)));
+        const dim3 ggrid(std::min(GR_Z, (int)((step + 1) * B + GR_JW * GR_WARPS - 1) / (GR_JW * GR_WARPS)), gks, Cw);
         if (B <= 8)
           FB_LAUNCH("fc1_gram_split_kernel", s, fc1_gram_split_kernel<8><<<ggrid, GR_WARPS * 32, 0, s>>>(
                                                     hs, B, w.gram_part));
