@@ -274,6 +274,9 @@ def kernel_work(wl: dict, counts: dict) -> dict:
         "conv1_bwd_w_kernel": ("tensor", 2 * CNN_MACS["conv1"] * train, "FP32 FFMA"),
         "conv1_fwd_tc_kernel": ("tensor", 2 * CNN_MACS["conv1"] * fwd, "3xTF32 tcgen05 (hi/lo weights stacked along N)"),
         "conv1_bwd_w_tc_kernel": ("tensor", 2 * CNN_MACS["conv1"] * train, "3xTF32 tcgen05 (hi/lo in operand rows)"),
+        # implicit-GEMM conv1 forward: the tensor work is ~1% of the tcgen05 rate; the kernel is
+        # bound by writing a1 (fp16 hi + lo NHWC, 115,200 B per slot) after reading the image
+        "conv1_fwd_ig_kernel": ("hbm", fwd * (2 * 2 * 28800 + 4 * 3072), "bytes (a1 hi+lo written, image read)"),
         # factored fc1 (squares-only materialisation and the factored aggregate): each reads the
         # client's fp16 hi/lo pooled history once, 4 B per history row element (steps x batch rows)
         "fc1_mat_tc_kernel": ("hbm", counts["client_steps"] * wl["batch"] * 12544 * 4, "bytes"),

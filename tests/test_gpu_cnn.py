@@ -121,7 +121,9 @@ def test_cnn_tcgen05_conv_matches_cuda_core_kernels():
     args = (dev(pop.row_start), dev(pop.num_rows), dev(np.concatenate(perms).astype(np.int32)), dev(perm_off))
     out = {}
     try:
-        for impl in (0, 1, 2):  # FP32 CUDA cores / tcgen05 / tcgen05 with the CTA-pair conv2 forward
+        # FP32 CUDA cores / tcgen05 / tcgen05 with the CTA-pair conv2 forward / tcgen05 with the
+        # im2col-staged conv1 forward
+        for impl in (0, 1, 2, 3):
             native.call("fb_cnn_set_conv_impl", impl)
             runner = fb.engine._ModelRunner(m, fb.device.Workspace(theta.device))
             C = len(sizes)
@@ -140,6 +142,12 @@ def test_cnn_tcgen05_conv_matches_cuda_core_kernels():
     np.testing.assert_allclose(out[1][0], out[2][0], rtol=1e-5, atol=1e-7)
     np.testing.assert_allclose(out[1][1], out[0][1], rtol=1e-5)
     assert np.abs(out[1][2] - out[0][2]).max() <= 1
+    # implicit-GEMM conv1 forward vs the im2col-staged kernel: same 3xTF32 products, different
+    # summation order
+    np.testing.assert_allclose(out[3][1], out[1][1], rtol=1e-5)
+    for c in range(len(sizes)):
+        rel = np.linalg.norm(out[3][0][c] - out[1][0][c]) / np.linalg.norm(out[1][0][c])
+        assert rel < 1e-4, (c, rel)
     for c in range(len(sizes)):
         rel = np.linalg.norm(out[1][0][c] - out[0][0][c]) / np.linalg.norm(out[0][0][c])
         assert rel < 1e-2, (c, rel)
