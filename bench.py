@@ -274,6 +274,7 @@ def kernel_work(wl: dict, counts: dict) -> dict:
         "conv1_bwd_w_kernel": ("tensor", 2 * CNN_MACS["conv1"] * train, "FP32 FFMA"),
         "conv1_fwd_tc_kernel": ("tensor", 2 * CNN_MACS["conv1"] * fwd, "3xTF32 tcgen05 (hi/lo weights stacked along N)"),
         "conv1_bwd_w_tc_kernel": ("tensor", 2 * CNN_MACS["conv1"] * train, "3xTF32 tcgen05 (hi/lo in operand rows)"),
+        "conv1_bwd_w_ffma_kernel": ("fp32", 2 * CNN_MACS["conv1"] * train, "FP32 FFMA (register-blocked 8 x 7 tiles)"),
         # implicit-GEMM conv1 forward: the tensor work is ~1% of the tcgen05 rate; the kernel is
         # bound by writing a1 (fp16 hi + lo NHWC, 115,200 B per slot) after reading the image
         "conv1_fwd_ig_kernel": ("hbm", fwd * (2 * 2 * 28800 + 4 * 3072), "bytes (a1 hi+lo written, image read)"),
@@ -433,6 +434,8 @@ def gpu_arm(args, wl):
     torch = _torch()
     import paper_2404_06430_b200 as fb
     from paper_2404_06430_b200 import native
+    if os.environ.get("FB_CNN_CONV_IMPL"):  # experiments only: kernel variants (fb_cnn_set_conv_impl)
+        native.call("fb_cnn_set_conv_impl", int(os.environ["FB_CNN_CONV_IMPL"]))
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -3642,6 +3642,160 @@ __global__ void __launch_bounds__(W1_THREADS, W1_MINB) conv1_bwd_w_tc_kernel(con
   }
 }
 
+// conv1 weight gradient on the FP32 pipes, register-blocked: the GEMM is tiny
+// (M = 32 channels, N = 28 = 27 taps + bias, K = the client's positions) and its
+// tcgen05 form (conv1_bwd_w_tc_kernel) is bound by per-chunk operand staging
+// (two split + swizzled scalar stores per operand element), so here the only
+// staging is two 16-byte copies per thread per 128 positions and the math runs on
+// FFMA.  16 warps; warp w owns the output tile (8 channels og = w & 3) x (7 k,
+// kg = w >> 2; k = 27 is the bias column, x = 1) in 56 accumulators per lane;
+// lanes stride over the chunk's positions.  Per position a lane reads its 8 dz1
+// values (two 16-byte loads; chunks are stored with the 16-byte index XOR
+// (position & 7), so a quarter-warp's 8 positions hit 8 different bank groups)
+// and 7 image values (the k-group's taps are compile-time offsets: the tile loop
+// is instantiated per kg), then does 56 FMAs.  dz1 chunks are prefetched into
+// registers one chunk ahead (a TMA ring measured slower: 4.5 vs 3.95 ms per
+// iteration), images by bulk copy one sample ahead.  Lane partials (fp32 over the
+// lane's positions) are warp-reduced in fixed order; SPLIT writes [28][32]
+// partials for conv1_bwd_w_reduce_kernel as conv1_bwd_w_tc_kernel does.
+constexpr int WF_THREADS = 512;
+#ifndef WF_CH
+#define WF_CH 128                                            // positions per chunk
+#endif
+constexpr int WF_CPS = (S1 * S1 + WF_CH - 1) / WF_CH;        // chunks per sample (last: partial)
+constexpr int WF_NLD = WF_CH * C1 / 4 / WF_THREADS;          // dz1 float4 per thread per chunk
+constexpr int WF_SMEM = 2 * WF_CH * C1 * 4 + 2 * IMG * 4 + 16;
+static_assert(WF_NLD * WF_THREADS * 4 == WF_CH * C1, "conv1 bwd-w FFMA: whole float4 per thread per chunk");
+
+template <int KG>
+__device__ __forceinline__ void wf_chunk(const float* __restrict__ dzb, const float* __restrict__ im, int p0, int og,
+                                         int lane, float (&acc)[8][7]) {
+  constexpr int K0 = 7 * KG;
+#pragma unroll
+  for (int j = 0; j < WF_CH / 32; ++j) {
+    const int pl = 32 * j + lane, p = min(p0 + pl, S1 * S1 - 1);  // rows past 900: dz1 zero
+    const int y = p / S1, x = p - y * S1;
+    const float* ib = im + y * S0 + x;
+    const float4* dr = reinterpret_cast<const float4*>(dzb) + pl * 8;
+    const float4 d0 = dr[(2 * og) ^ (lane & 7)];
+    const float4 d1 = dr[(2 * og + 1) ^ (lane & 7)];
+    const float dv[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+    float xv[7];
+#pragma unroll
+    for (int e = 0; e < 7; ++e) {
+      const int k = K0 + e;
+      if (k < 27)
+        xv[e] = ib[(k / 9) * S0 * S0 + ((k % 9) / 3) * S0 + k % 3];
+      else
+        xv[e] = 1.f;
+    }
+#pragma unroll
+    for (int o = 0; o < 8; ++o)
+#pragma unroll
+      for (int e = 0; e < 7; ++e) acc[o][e] = fmaf(dv[o], xv[e], acc[o][e]);
+  }
+}
+
+template <bool SPLIT>
+__global__ void __launch_bounds__(WF_THREADS, 1) conv1_bwd_w_ffma_kernel(const float* __restrict__ X,
+                                                                        const int64_t* __restrict__ slot_row,
+                                                                        const float* __restrict__ dz1, int B,
+                                                                        const int32_t* __restrict__ client_nb,
+                                                                        float* __restrict__ delta, int64_t ld,
+                                                                        Step st, int split,
+                                                                        float* __restrict__ wpart) {
+  extern __shared__ __align__(16) uint8_t wf_smem[];
+  float* dzs = reinterpret_cast<float*>(wf_smem);                          // [2][WF_CH pos][32 ch], swizzled
+  float* imgs = dzs + 2 * WF_CH * C1;                                      // [2][IMG]
+  uint64_t* imfull = reinterpret_cast<uint64_t*>(imgs + 2 * IMG);          // [2]
+  int c = blockIdx.x, b0 = 0, b1;
+  if constexpr (SPLIT) {
+    c = blockIdx.x / split;
+    const int part = blockIdx.x - c * split, nbc = client_nb[c];
+    b0 = part * nbc / split;
+    b1 = (part + 1) * nbc / split;
+    if (b1 <= b0) return;
+  } else {
+    b1 = client_nb[c];
+    if (b1 == 0) return;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, t = threadIdx.x;
+  const int og = warp & 3, kg = warp >> 2;
+  const int ns = b1 - b0, nchunks = ns * WF_CPS;
+  const int64_t n0 = (int64_t)c * B + b0;
+  if (t == 0) {
+    tc::mbar_init(&imfull[0], 1);
+    tc::mbar_init(&imfull[1], 1);
+    tc::fence_mbar_init();
+  }
+  __syncthreads();
+  auto fetch_img = [&](int b) {  // thread 0
+    tc::mbar_arrive_expect_tx(&imfull[b & 1], IMG * 4);
+    tc::bulk_load(imgs + (b & 1) * IMG, X + slot_row[n0 + b] * IMG, IMG * 4, &imfull[b & 1]);
+  };
+  if (t == 0) fetch_img(0);
+  // dz1 chunk prefetch: float4 f = t + 512 u of the chunk's [WF_CH pos][8 quads] block
+  float4 pre[WF_NLD];
+  auto load_dz = [&](int i) {
+    const int b = i / WF_CPS, p0 = (i - b * WF_CPS) * WF_CH;
+    const float4* src = reinterpret_cast<const float4*>(dz1 + (n0 + b) * A1 + (int64_t)p0 * C1);
+#pragma unroll
+    for (int u = 0; u < WF_NLD; ++u) {
+      const int f = t + u * WF_THREADS;
+      pre[u] = p0 + (f >> 3) < S1 * S1 ? __ldg(src + f) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  float acc[8][7];
+#pragma unroll
+  for (int o = 0; o < 8; ++o)
+#pragma unroll
+    for (int e = 0; e < 7; ++e) acc[o][e] = 0.f;
+  load_dz(0);
+  for (int i = 0; i < nchunks; ++i) {
+    const int b = i / WF_CPS, ch = i - b * WF_CPS, p0 = ch * WF_CH;
+    float* dzb = dzs + (i & 1) * WF_CH * C1;
+#pragma unroll
+    for (int u = 0; u < WF_NLD; ++u) {
+      const int f = t + u * WF_THREADS, pl = f >> 3, q = f & 7;
+      reinterpret_cast<float4*>(dzb)[pl * 8 + (q ^ (pl & 7))] = pre[u];
+    }
+    if (i + 1 < nchunks) load_dz(i + 1);
+    __syncthreads();  // chunk i staged; every thread is past chunk i - 1 (sample b - 1's last image reads)
+    if (ch == 0) {
+      if (t == 0 && b + 1 < ns) {  // image buffer (b + 1) & 1 held sample b - 1
+        tc::fence_proxy_async();
+        fetch_img(b + 1);
+      }
+      tc::mbar_wait(&imfull[b & 1], (b >> 1) & 1);
+    }
+    const float* im = imgs + (b & 1) * IMG;
+    switch (kg) {  // warp-uniform
+      case 0: wf_chunk<0>(dzb, im, p0, og, lane, acc); break;
+      case 1: wf_chunk<1>(dzb, im, p0, og, lane, acc); break;
+      case 2: wf_chunk<2>(dzb, im, p0, og, lane, acc); break;
+      default: wf_chunk<3>(dzb, im, p0, og, lane, acc); break;
+    }
+  }
+  // lane partials -> warp sums (fixed order); lane 0 updates (or writes the split partial)
+  float* dc = delta + (int64_t)c * ld;
+  float* wp = SPLIT ? wpart + (int64_t)blockIdx.x * W1_PART : nullptr;
+#pragma unroll
+  for (int o = 0; o < 8; ++o)
+#pragma unroll
+    for (int e = 0; e < 7; ++e) {
+      const float g = warp_sum(acc[o][e]);
+      const int k = 7 * kg + e, oc = 8 * og + o;
+      if (lane == 0) {
+        if constexpr (SPLIT) {
+          wp[k * 32 + oc] = g;
+        } else {
+          float& dl = k < 27 ? dc[O_W1 + (int64_t)oc * (C0 * 9) + k] : dc[O_B1 + oc];
+          dl += st.lr * (g - st.mu * dl);
+        }
+      }
+    }
+}
+
 // split conv1 weight gradient: fixed-order sum of the client's CTA partials, then the update
 __global__ void conv1_bwd_w_reduce_kernel(const float* __restrict__ wpart, int split,
                                           const int32_t* __restrict__ client_nb, float* __restrict__ delta,
@@ -3666,6 +3820,9 @@ int g_conv_impl = 1;  // 1 = tcgen05 (product path), 0 = FP32 CUDA-core kernels 
 bool g_conv2_pairs = false;
 // conv1 forward: 1 = implicit GEMM (conv1_fwd_ig_kernel, default), 0 = im2col staging (conv1_fwd_tc_kernel)
 int g_conv1_fwd_impl = 1;
+// conv1 weight gradient: the register-blocked FP32 kernel (conv1_bwd_w_ffma_kernel, default:
+// 3.8 vs 4.35 ms per iteration) or, with impl 4, the tcgen05 kernel (conv1_bwd_w_tc_kernel)
+bool g_conv1_bwd_ffma = true;
 
 
 // ------------------------------------------------ conv2 backward-weights (tcgen05)
@@ -4015,6 +4172,8 @@ int set_smem_limits() {
   cudaFuncSetAttribute(conv2_bwd_w_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BW_SMEM);
   cudaFuncSetAttribute(conv1_bwd_w_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, W1_SMEM);
   cudaFuncSetAttribute(conv1_bwd_w_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, W1_SMEM);
+  cudaFuncSetAttribute(conv1_bwd_w_ffma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, WF_SMEM);
+  cudaFuncSetAttribute(conv1_bwd_w_ffma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, WF_SMEM);
   cudaFuncSetAttribute(conv1_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C1F_SMEM);
   cudaFuncSetAttribute(conv1_fwd_ig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, CIG_SMEM);
   cudaFuncSetAttribute(fc1_mat_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FMT_SMEM);
@@ -4187,12 +4346,13 @@ int fb_cnn_fc1_aggregate_f32(const float* coef, int num_clients, int batch_size,
 }
 
 int fb_cnn_set_conv_impl(int impl) {
-  FB_REQUIRE(impl >= 0 && impl <= 3,
-             "fb_cnn_set_conv_impl: 0 (FP32 CUDA cores), 1 (tcgen05), 2 (tcgen05, CTA-pair conv2 forward) or 3 "
-             "(tcgen05, im2col-staged conv1 forward)");
+  FB_REQUIRE(impl >= 0 && impl <= 4,
+             "fb_cnn_set_conv_impl: 0 (FP32 CUDA cores), 1 (tcgen05), 2 (tcgen05, CTA-pair conv2 forward), 3 "
+             "(tcgen05, im2col-staged conv1 forward) or 4 (tcgen05 also for the conv1 weight gradient)");
   fb::cnn::g_conv_impl = impl == 0 ? 0 : 1;
   fb::cnn::g_conv2_pairs = impl == 2;
   fb::cnn::g_conv1_fwd_impl = impl == 3 ? 0 : 1;
+  fb::cnn::g_conv1_bwd_ffma = impl != 4;
   return FB_OK;
 }
 
@@ -4349,6 +4509,7 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
 #define GR_NKS 7
 #endif
         const int gks = Cw * GR_NKS >= 4 * g_num_sms ? GR_NKS : 14;  // more K splits for a small shard
+        FB_REQUIRE(Cw <= 65535, "local_sgd_cnn: %d clients in one wave exceed the Gram grid's z extent", Cw);
         const dim3 ggrid(std::min(GR_Z, (int)((step + 1) * B + GR_JW * GR_WARPS - 1) / (GR_JW * GR_WARPS)), gks, Cw);
         if (B <= 8)
           FB_LAUNCH("fc1_gram_split_kernel", s, fc1_gram_split_kernel<8><<<ggrid, GR_WARPS * 32, 0, s>>>(
@@ -4446,7 +4607,21 @@ int fb_local_sgd_cnn_f32(const float* theta_t, const float* X, const int32_t* y,
         FB_LAUNCH("conv2_bwd_w_kernel", s, conv2_bwd_w_kernel<<<Cw, 256, C2W_SMEM, s>>>(ws.dp, ws.pooled, ws.code, ws.a1, nullptr, B, ws.client_nb, dlt, ld_delta,
                                                      sp));
       }
-      if (g_conv_impl == 1)
+      if (g_conv_impl == 1 && g_conv1_bwd_ffma) {
+        int split1 = 1;  // few active clients: split each client's samples over CTAs (1 CTA per SM)
+        while (split1 < B && active * (split1 + 1) <= g_num_sms) ++split1;
+        if (split1 > 1) {
+          FB_LAUNCH("conv1_bwd_w_ffma_kernel", s, conv1_bwd_w_ffma_kernel<true><<<Cw * split1, WF_THREADS, WF_SMEM, s>>>(
+                                                      X, ws.slot_row, ws.dz1, B, ws.client_nb, dlt, ld_delta, sp,
+                                                      split1, ws.dp));
+          FB_LAUNCH("conv1_bwd_w_reduce_kernel", s, conv1_bwd_w_reduce_kernel<<<Cw, 256, 0, s>>>(
+                                                        ws.dp, split1, ws.client_nb, dlt, ld_delta, sp));
+        } else {
+          FB_LAUNCH("conv1_bwd_w_ffma_kernel", s, conv1_bwd_w_ffma_kernel<false><<<Cw, WF_THREADS, WF_SMEM, s>>>(
+                                                      X, ws.slot_row, ws.dz1, B, ws.client_nb, dlt, ld_delta, sp,
+                                                      1, nullptr));
+        }
+      } else if (g_conv_impl == 1)
       {
         int split1 = 1;  // few active clients: split each client's samples over CTAs (2 CTAs per SM)
         while (split1 < B && active * (split1 + 1) <= 2 * g_num_sms) ++split1;

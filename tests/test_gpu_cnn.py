@@ -122,8 +122,9 @@ def test_cnn_tcgen05_conv_matches_cuda_core_kernels():
     out = {}
     try:
         # FP32 CUDA cores / tcgen05 / tcgen05 with the CTA-pair conv2 forward / tcgen05 with the
-        # im2col-staged conv1 forward
-        for impl in (0, 1, 2, 3):
+        # im2col-staged conv1 forward / tcgen05 also for the conv1 weight gradient (default: the
+        # register-blocked FP32 kernel)
+        for impl in (0, 1, 2, 3, 4):
             native.call("fb_cnn_set_conv_impl", impl)
             runner = fb.engine._ModelRunner(m, fb.device.Workspace(theta.device))
             C = len(sizes)
@@ -145,8 +146,11 @@ def test_cnn_tcgen05_conv_matches_cuda_core_kernels():
     # implicit-GEMM conv1 forward vs the im2col-staged kernel: same 3xTF32 products, different
     # summation order
     np.testing.assert_allclose(out[3][1], out[1][1], rtol=1e-5)
+    np.testing.assert_allclose(out[4][1], out[1][1], rtol=1e-6)
     for c in range(len(sizes)):
         rel = np.linalg.norm(out[3][0][c] - out[1][0][c]) / np.linalg.norm(out[1][0][c])
+        assert rel < 1e-4, (c, rel)
+        rel = np.linalg.norm(out[4][0][c] - out[1][0][c]) / np.linalg.norm(out[1][0][c])
         assert rel < 1e-4, (c, rel)
     for c in range(len(sizes)):
         rel = np.linalg.norm(out[1][0][c] - out[0][0][c]) / np.linalg.norm(out[0][0][c])
