@@ -3649,7 +3649,9 @@ __global__ void __launch_bounds__(W1_THREADS, W1_MINB) conv1_bwd_w_tc_kernel(con
 // staging is two 16-byte copies per thread per 128 positions and the math runs on
 // FFMA.  16 warps; warp w owns the output tile (8 channels og = w & 3) x (7 k,
 // kg = w >> 2; k = 27 is the bias column, x = 1) in 56 accumulators per lane;
-// lanes stride over the chunk's positions.  Per position a lane reads its 8 dz1
+// lane = output column x (30 of 32 live), one output row per trip, chunks of 3
+// rows (a per-position layout with a division per position and 2-way image-load
+// bank conflicts measured 3.67 ms).  Per position a lane reads its 8 dz1
 // values (two 16-byte loads; chunks are stored with the 16-byte index XOR
 // (position & 7), so a quarter-warp's 8 positions hit 8 different bank groups)
 // and 7 image values (the k-group's taps are compile-time offsets: the tile loop
@@ -3659,26 +3661,30 @@ __global__ void __launch_bounds__(W1_THREADS, W1_MINB) conv1_bwd_w_tc_kernel(con
 // lane's positions) are warp-reduced in fixed order; SPLIT writes [28][32]
 // partials for conv1_bwd_w_reduce_kernel as conv1_bwd_w_tc_kernel does.
 constexpr int WF_THREADS = 512;
-#ifndef WF_CH
-#define WF_CH 128                                            // positions per chunk
-#endif
-constexpr int WF_CPS = (S1 * S1 + WF_CH - 1) / WF_CH;        // chunks per sample (last: partial)
-constexpr int WF_NLD = WF_CH * C1 / 4 / WF_THREADS;          // dz1 float4 per thread per chunk
-constexpr int WF_SMEM = 2 * WF_CH * C1 * 4 + 2 * IMG * 4 + 16;
-static_assert(WF_NLD * WF_THREADS * 4 == WF_CH * C1, "conv1 bwd-w FFMA: whole float4 per thread per chunk");
+constexpr int WF_ROWS = 3;                                   // output rows per chunk (30 = 10 x 3)
+constexpr int WF_CH = WF_ROWS * S1;                          // 90 positions per chunk
+constexpr int WF_CPS = S1 / WF_ROWS;                         // 10 chunks per sample
+constexpr int WF_NF4 = WF_CH * C1 / 4;                       // 720 dz1 float4 per chunk
+constexpr int WF_NLD = (WF_NF4 + WF_THREADS - 1) / WF_THREADS;
+constexpr int WF_BUF = (WF_CH + 2) * C1;                     // floats per dz1 buffer (+2 rows: lanes 30, 31 of the last row)
+constexpr int WF_IMGS = IMG + 64;                            // image stride (zero pad: lanes 30, 31 read past the plane)
+constexpr int WF_SMEM = 2 * WF_BUF * 4 + 2 * WF_IMGS * 4 + 16;
+static_assert(S1 % WF_ROWS == 0, "conv1 bwd-w FFMA: whole rows per chunk");
 
+// lane = output column x (lanes 30, 31 idle: their dz1 is forced to 0), one output row per trip
 template <int KG>
-__device__ __forceinline__ void wf_chunk(const float* __restrict__ dzb, const float* __restrict__ im, int p0, int og,
+__device__ __forceinline__ void wf_chunk(const float* __restrict__ dzb, const float* __restrict__ im, int y0, int og,
                                          int lane, float (&acc)[8][7]) {
   constexpr int K0 = 7 * KG;
+  const bool live = lane < S1;
 #pragma unroll
-  for (int j = 0; j < WF_CH / 32; ++j) {
-    const int pl = 32 * j + lane, p = min(p0 + pl, S1 * S1 - 1);  // rows past 900: dz1 zero
-    const int y = p / S1, x = p - y * S1;
-    const float* ib = im + y * S0 + x;
+  for (int r = 0; r < WF_ROWS; ++r) {
+    const int pl = r * S1 + lane;
+    const float* ib = im + (y0 + r) * S0 + lane;
     const float4* dr = reinterpret_cast<const float4*>(dzb) + pl * 8;
-    const float4 d0 = dr[(2 * og) ^ (lane & 7)];
-    const float4 d1 = dr[(2 * og + 1) ^ (lane & 7)];
+    float4 d0 = dr[(2 * og) ^ (pl & 7)];
+    float4 d1 = dr[(2 * og + 1) ^ (pl & 7)];
+    if (!live) d0 = d1 = make_float4(0.f, 0.f, 0.f, 0.f);
     const float dv[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
     float xv[7];
 #pragma unroll
@@ -3705,9 +3711,9 @@ __global__ void __launch_bounds__(WF_THREADS, 1) conv1_bwd_w_ffma_kernel(const f
                                                                         Step st, int split,
                                                                         float* __restrict__ wpart) {
   extern __shared__ __align__(16) uint8_t wf_smem[];
-  float* dzs = reinterpret_cast<float*>(wf_smem);                          // [2][WF_CH pos][32 ch], swizzled
-  float* imgs = dzs + 2 * WF_CH * C1;                                      // [2][IMG]
-  uint64_t* imfull = reinterpret_cast<uint64_t*>(imgs + 2 * IMG);          // [2]
+  float* dzs = reinterpret_cast<float*>(wf_smem);                          // [2][WF_BUF], swizzled rows
+  float* imgs = dzs + 2 * WF_BUF;                                          // [2][WF_IMGS]
+  uint64_t* imfull = reinterpret_cast<uint64_t*>(imgs + 2 * WF_IMGS);      // [2]
   int c = blockIdx.x, b0 = 0, b1;
   if constexpr (SPLIT) {
     c = blockIdx.x / split;
@@ -3723,6 +3729,7 @@ __global__ void __launch_bounds__(WF_THREADS, 1) conv1_bwd_w_ffma_kernel(const f
   const int og = warp & 3, kg = warp >> 2;
   const int ns = b1 - b0, nchunks = ns * WF_CPS;
   const int64_t n0 = (int64_t)c * B + b0;
+  if (t < 128) imgs[(t >> 6) * WF_IMGS + IMG + (t & 63)] = 0.f;
   if (t == 0) {
     tc::mbar_init(&imfull[0], 1);
     tc::mbar_init(&imfull[1], 1);
@@ -3731,10 +3738,10 @@ __global__ void __launch_bounds__(WF_THREADS, 1) conv1_bwd_w_ffma_kernel(const f
   __syncthreads();
   auto fetch_img = [&](int b) {  // thread 0
     tc::mbar_arrive_expect_tx(&imfull[b & 1], IMG * 4);
-    tc::bulk_load(imgs + (b & 1) * IMG, X + slot_row[n0 + b] * IMG, IMG * 4, &imfull[b & 1]);
+    tc::bulk_load(imgs + (b & 1) * WF_IMGS, X + slot_row[n0 + b] * IMG, IMG * 4, &imfull[b & 1]);
   };
   if (t == 0) fetch_img(0);
-  // dz1 chunk prefetch: float4 f = t + 512 u of the chunk's [WF_CH pos][8 quads] block
+  // dz1 chunk prefetch: float4 f = t + 512 u of the chunk's [90 pos][8 quads] block
   float4 pre[WF_NLD];
   auto load_dz = [&](int i) {
     const int b = i / WF_CPS, p0 = (i - b * WF_CPS) * WF_CH;
@@ -3742,7 +3749,7 @@ __global__ void __launch_bounds__(WF_THREADS, 1) conv1_bwd_w_ffma_kernel(const f
 #pragma unroll
     for (int u = 0; u < WF_NLD; ++u) {
       const int f = t + u * WF_THREADS;
-      pre[u] = p0 + (f >> 3) < S1 * S1 ? __ldg(src + f) : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (f < WF_NF4) pre[u] = __ldg(src + f);
     }
   };
   float acc[8][7];
@@ -3753,11 +3760,11 @@ __global__ void __launch_bounds__(WF_THREADS, 1) conv1_bwd_w_ffma_kernel(const f
   load_dz(0);
   for (int i = 0; i < nchunks; ++i) {
     const int b = i / WF_CPS, ch = i - b * WF_CPS, p0 = ch * WF_CH;
-    float* dzb = dzs + (i & 1) * WF_CH * C1;
+    float* dzb = dzs + (i & 1) * WF_BUF;
 #pragma unroll
     for (int u = 0; u < WF_NLD; ++u) {
       const int f = t + u * WF_THREADS, pl = f >> 3, q = f & 7;
-      reinterpret_cast<float4*>(dzb)[pl * 8 + (q ^ (pl & 7))] = pre[u];
+      if (f < WF_NF4) reinterpret_cast<float4*>(dzb)[pl * 8 + (q ^ (pl & 7))] = pre[u];
     }
     if (i + 1 < nchunks) load_dz(i + 1);
     __syncthreads();  // chunk i staged; every thread is past chunk i - 1 (sample b - 1's last image reads)
@@ -3768,12 +3775,13 @@ __global__ void __launch_bounds__(WF_THREADS, 1) conv1_bwd_w_ffma_kernel(const f
       }
       tc::mbar_wait(&imfull[b & 1], (b >> 1) & 1);
     }
-    const float* im = imgs + (b & 1) * IMG;
+    const float* im = imgs + (b & 1) * WF_IMGS;
+    const int y0 = ch * WF_ROWS;
     switch (kg) {  // warp-uniform
-      case 0: wf_chunk<0>(dzb, im, p0, og, lane, acc); break;
-      case 1: wf_chunk<1>(dzb, im, p0, og, lane, acc); break;
-      case 2: wf_chunk<2>(dzb, im, p0, og, lane, acc); break;
-      default: wf_chunk<3>(dzb, im, p0, og, lane, acc); break;
+      case 0: wf_chunk<0>(dzb, im, y0, og, lane, acc); break;
+      case 1: wf_chunk<1>(dzb, im, y0, og, lane, acc); break;
+      case 2: wf_chunk<2>(dzb, im, y0, og, lane, acc); break;
+      default: wf_chunk<3>(dzb, im, y0, og, lane, acc); break;
     }
   }
   // lane partials -> warp sums (fixed order); lane 0 updates (or writes the split partial)
