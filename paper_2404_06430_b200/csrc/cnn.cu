@@ -2077,10 +2077,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) fc1_tc_kernel(const __grid_cons
         const float inv = 1.f / (fa.rscale[n] * ts);
         float* o = fa.mode == 0 ? fa.out + ((int64_t)x * fa.N + n) * HID
                                 : fa.out + (int64_t)n * FLAT + (int64_t)x * 128;
-        float4* o4 = reinterpret_cast<float4*>(o);
+        // 256-bit stores: the row-per-lane pattern writes one FULL 32-byte sector per lane and
+        // instruction (16-byte stores left every L2 write sector half-filled: 2x the write
+        // sectors, ncu r02cp)
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
-          o4[i] = make_float4(sum[4 * i] * inv, sum[4 * i + 1] * inv, sum[4 * i + 2] * inv, sum[4 * i + 3] * inv);
+        for (int i = 0; i < 16; ++i) {
+          uint32_t v[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[e] = __float_as_uint(sum[8 * i + e] * inv);
+          stg256(o + 8 * i, v);
+        }
       }
     }
   }
