@@ -2651,10 +2651,14 @@ __global__ void __launch_bounds__(FMT_THREADS, 1) fc1_agg_tc_kernel(
     }
     const float m = __uint_as_float(*umax);
     const float inv = m > 0.f ? 1.f / exp2f(14.f - ceilf(log2f(m))) : 1.f;  // exact: power of two
-    float4* o4 = reinterpret_cast<float4*>(out + (int64_t)(q * 32 + lane) * HID + hh * 64);
+    float* orow = out + (int64_t)(q * 32 + lane) * HID + hh * 64;
 #pragma unroll
-    for (int j = 0; j < 16; ++j)
-      o4[j] = make_float4(run[4 * j] * inv, run[4 * j + 1] * inv, run[4 * j + 2] * inv, run[4 * j + 3] * inv);
+    for (int j = 0; j < 8; ++j) {  // row per lane: 256-bit stores fill whole sectors
+      uint32_t v[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[e] = __float_as_uint(run[8 * j + e] * inv);
+      stg256(orow + 8 * j, v);
+    }
   }
   tc::tc_fence_before();
   __syncthreads();

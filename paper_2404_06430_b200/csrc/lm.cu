@@ -571,28 +571,50 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         float* crow = g.C + (int64_t)z * g.sC + (int64_t)m * g.ldc;
         const float* bias = g.bias ? g.bias + (int64_t)z * g.sBias : nullptr;
         const float* arow = g.aux ? g.aux + (int64_t)z * g.sAux + (int64_t)m * g.ldaux : nullptr;
-        const bool v4 = ((g.ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(crow) & 15) == 0);
+        // row per lane: 256-bit loads / stores (whole 32-byte sectors per lane) where the row,
+        // the bias and the mask rows are 32-byte aligned; same arithmetic order as the scalar path
+        const auto al32 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31) == 0; };
+        const bool v8 = (g.ldc & 7) == 0 && al32(crow) && (!bias || al32(bias)) &&
+                        (!arow || ((g.ldaux & 7) == 0 && al32(arow)));
 #pragma unroll
-        for (int j0 = 0; j0 < EH; j0 += 4) {
+        for (int j0 = 0; j0 < EH; j0 += 8) {
           const int n = n0 + j0;
-          float x[4];
+          float x[8];
+          if (v8 && n + 7 < g.N) {
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int nn = n + u;
-            float val = g.alpha * sum[j0 + u];
-            if (nn < g.N) {
-              if (g.beta != 0.f) val = fmaf(g.beta, crow[nn], val);
-              if (bias) val += bias[nn];
-              if (arow && !(arow[nn] > 0.f)) val = 0.f;
+            for (int u = 0; u < 8; ++u) x[u] = g.alpha * sum[j0 + u];
+            if (g.beta != 0.f) {
+              float cv[8];
+              tc::ldg256(crow + n, cv);
+#pragma unroll
+              for (int u = 0; u < 8; ++u) x[u] = fmaf(g.beta, cv[u], x[u]);
             }
-            x[u] = val;
-          }
-          if (v4 && n + 3 < g.N) {
-            *reinterpret_cast<float4*>(crow + n) = make_float4(x[0], x[1], x[2], x[3]);
+            if (bias) {
+              float bv[8];
+              tc::ldg256(bias + n, bv);
+#pragma unroll
+              for (int u = 0; u < 8; ++u) x[u] += bv[u];
+            }
+            if (arow) {
+              float av[8];
+              tc::ldg256(arow + n, av);
+#pragma unroll
+              for (int u = 0; u < 8; ++u)
+                if (!(av[u] > 0.f)) x[u] = 0.f;
+            }
+            tc::stg256f(crow + n, x);
           } else {
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-              if (n + u < g.N) crow[n + u] = x[u];
+            for (int u = 0; u < 8; ++u) {
+              const int nn = n + u;
+              if (nn < g.N) {
+                float val = g.alpha * sum[j0 + u];
+                if (g.beta != 0.f) val = fmaf(g.beta, crow[nn], val);
+                if (bias) val += bias[nn];
+                if (arow && !(arow[nn] > 0.f)) val = 0.f;
+                crow[nn] = val;
+              }
+            }
           }
         }
       }
