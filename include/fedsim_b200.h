@@ -141,9 +141,9 @@ int64_t fb_cnn_workspace_bytes(int max_slots, int max_clients, int hist_steps);
 /* Validation knob: 1 (default) = the convolutions on tcgen05; 2 = tcgen05
  * with the conv2 forward on 2-CTA clusters (cta_group::2, M = 256; correct,
  * measured slower); 3 = tcgen05 with the conv1 forward on the im2col-staged
- * kernel instead of the implicit GEMM; 4 = the conv1 weight gradient on the
- * tcgen05 kernel instead of the register-blocked FP32 one; 0 = the FP32
- * CUDA-core kernels kept as an independent check.                           */
+ * kernel instead of the implicit GEMM; 4 = the conv1 weight gradient on a
+ * register-blocked FP32 kernel (faster, not the default: see DESIGN.md); 0 =
+ * the FP32 CUDA-core kernels kept as an independent check.                  */
 int fb_cnn_set_conv_impl(int impl);
 /* perms / perm_off nullable: when given, client c's evaluated rows are epoch 0's
  * perms[perm_off[c] + min(skip, n_c) ..] (the rows past the first local batch, whose

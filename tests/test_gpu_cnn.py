@@ -122,8 +122,7 @@ def test_cnn_tcgen05_conv_matches_cuda_core_kernels():
     out = {}
     try:
         # FP32 CUDA cores / tcgen05 / tcgen05 with the CTA-pair conv2 forward / tcgen05 with the
-        # im2col-staged conv1 forward / tcgen05 also for the conv1 weight gradient (default: the
-        # register-blocked FP32 kernel)
+        # im2col-staged conv1 forward / tcgen05 with the register-blocked FP32 conv1 weight gradient
         for impl in (0, 1, 2, 3, 4):
             native.call("fb_cnn_set_conv_impl", impl)
             runner = fb.engine._ModelRunner(m, fb.device.Workspace(theta.device))

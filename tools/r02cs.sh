@@ -1,0 +1,11 @@
+set -x
+timeout 1500 python -m pytest tests -m gpu -q -p no:warnings > gpurun_out/r02cs_pytest_gpu.log 2>&1; tail -2 gpurun_out/r02cs_pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r02cs_smoke.log 2>&1; tail -2 gpurun_out/r02cs_smoke.log
+timeout 600 python bench.py > gpurun_out/r02cs_bench.log 2>&1; tail -c 300 gpurun_out/r02cs_bench.log
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 700 --csv --log-file gpurun_out/r02cs_launches.csv python bench.py --steps 2 --warmup 3 --e2e-steps 0 --no-cpu-baseline --profile-steps 1 > gpurun_out/r02cs_ncu.log 2>&1; echo ncu=$?
+M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors_srcunit_tex_op_write.sum,smsp__issue_active.avg.pct_of_peak_sustained_active,l1tex__throughput.avg.pct_of_peak_sustained_elapsed
+timeout 900 ncu --metrics $M --clock-control none -k regex:"conv1_fwd_ig|conv1_bwd_w_ffma|fc1_tc" -c 24 --csv --log-file gpurun_out/r02cs_metrics.csv python bench.py --steps 1 --warmup 3 --e2e-steps 0 --no-cpu-baseline --profile-steps 1 > gpurun_out/r02cs_ncu2.log 2>&1; echo ncu2=$?
+export PYTORCH_NO_CUDA_MEMORY_CACHING=1
+timeout 900 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_gpu_cnn.py -q -p no:warnings -x -k "cuda_core or (oracle and sizes0)" > gpurun_out/r02cs_memcheck.log 2>&1; echo memcheck=$?; tail -3 gpurun_out/r02cs_memcheck.log
+timeout 1200 compute-sanitizer --tool racecheck --racecheck-report analysis --print-limit 20 python -m pytest tests/test_gpu_cnn.py -q -p no:warnings -x -k "cuda_core" > gpurun_out/r02cs_racecheck.log 2>&1; echo racecheck=$?; tail -3 gpurun_out/r02cs_racecheck.log
+timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/r02cs_ref.log 2>&1; tail -c 300 gpurun_out/r02cs_ref.log
