@@ -1098,6 +1098,34 @@ __global__ void sgd_kernel(float* __restrict__ Wc, const float* __restrict__ G, 
   const float* g = G + (int64_t)w * sW;
   float* dl = Dl + (int64_t)w * ldD;
   const float* ct = control ? control + (int64_t)w * ldc : nullptr;
+  // 16-byte path when every row is 16-byte aligned (the workspace strides are): 5 float4
+  // accesses in flight per thread instead of 5 scalars; the same arithmetic per element
+  const auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if ((D & 3) == 0 && a16(W) && a16(g) && a16(dl) && (!ct || a16(ct))) {
+    const int64_t D4 = D >> 2;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < D4; i += (int64_t)gridDim.x * blockDim.x) {
+      const float4 gv = reinterpret_cast<const float4*>(g)[i];
+      float4 dv = reinterpret_cast<float4*>(dl)[i];
+      float4 wv = reinterpret_cast<float4*>(W)[i];
+      const float4 cv = ct ? reinterpret_cast<const float4*>(ct)[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+      float sv[4] = {gv.x, gv.y, gv.z, gv.w};
+      float* dp4 = &dv.x;
+      float* wp4 = &wv.x;
+      const float* cp4 = &cv.x;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float x = sv[e];
+        if (mu != 0.f) x = fmaf(mu, -dp4[e], x);
+        if (ct) x += cp4[e];
+        x *= lr;
+        wp4[e] -= x;
+        dp4[e] += x;
+      }
+      reinterpret_cast<float4*>(W)[i] = wv;
+      reinterpret_cast<float4*>(dl)[i] = dv;
+    }
+    return;
+  }
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < D; i += (int64_t)gridDim.x * blockDim.x) {
     float s = g[i];
     if (mu != 0.f) s = fmaf(mu, -dl[i], s);
@@ -1111,16 +1139,45 @@ __global__ void sgd_kernel(float* __restrict__ Wc, const float* __restrict__ G, 
 __global__ void init_wave_kernel(const float* __restrict__ theta_t, int64_t D, float* __restrict__ Wc, int64_t sW,
                                  float* __restrict__ Dl, int64_t ldD) {
   const int w = blockIdx.y;
+  float* wc = Wc + (int64_t)w * sW;
+  float* dl = Dl + (int64_t)w * ldD;
+  const auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if ((D & 3) == 0 && a16(theta_t) && a16(wc) && a16(dl)) {  // 16-byte path
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (D >> 2); i += (int64_t)gridDim.x * blockDim.x) {
+      reinterpret_cast<float4*>(wc)[i] = reinterpret_cast<const float4*>(theta_t)[i];
+      reinterpret_cast<float4*>(dl)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    return;
+  }
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < D; i += (int64_t)gridDim.x * blockDim.x) {
-    Wc[(int64_t)w * sW + i] = theta_t[i];
-    Dl[(int64_t)w * ldD + i] = 0.f;
+    wc[i] = theta_t[i];
+    dl[i] = 0.f;
   }
 }
 
 __global__ void nonfinite_kernel(const float* __restrict__ Dl, int64_t ldD, int64_t D, int32_t* __restrict__ bad) {
   const int w = blockIdx.x;
+  const float* dl = Dl + (int64_t)w * ldD;
   int b = 0;
-  for (int64_t i = threadIdx.x; i < D; i += blockDim.x) b |= !isfinite(Dl[(int64_t)w * ldD + i]);
+  int64_t i0 = 0;
+  if ((reinterpret_cast<uintptr_t>(dl) & 15) == 0) {  // 16-byte loads, 4 in flight per thread
+    const float4* d4 = reinterpret_cast<const float4*>(dl);
+    const int64_t n4 = D >> 2, step = 4 * (int64_t)blockDim.x;
+    int64_t i = threadIdx.x;
+    for (; i + 3 * blockDim.x < n4; i += step) {
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = d4[i + u * blockDim.x];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) b |= !isfinite(v[u].x) | !isfinite(v[u].y) | !isfinite(v[u].z) | !isfinite(v[u].w);
+    }
+    for (; i < n4; i += blockDim.x) {
+      const float4 v = d4[i];
+      b |= !isfinite(v.x) | !isfinite(v.y) | !isfinite(v.z) | !isfinite(v.w);
+    }
+    i0 = n4 << 2;
+  }
+  for (int64_t i = i0 + threadIdx.x; i < D; i += blockDim.x) b |= !isfinite(dl[i]);
   b = __syncthreads_or(b);
   if (threadIdx.x == 0) bad[w] = b;
 }
