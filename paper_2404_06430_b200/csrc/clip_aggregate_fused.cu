@@ -169,6 +169,18 @@ struct Args {
   int lead;           // clients the norm group may run ahead of the accumulate group
 };
 
+// CTA-scope acquire load / release store of a shared flag: race-free (unlike a volatile
+// access) and, unlike an atomic RMW spin, no serialised shared atomics from the 256 spinning
+// threads of the norm group (atomicAdd(&flag, 0) cost ~7% of the step: 0.675 -> 0.63 of B_alg)
+__device__ __forceinline__ int ld_acquire_cta(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(tc::smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta(int* p, int v) {
+  asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(tc::smem_u32(p)), "r"(v) : "memory");
+}
+
 template <int kNormStages, int kAccStages>
 __global__ void __launch_bounds__(kT, 1) clip_aggregate_fused_kernel(const Args a) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -182,7 +194,7 @@ __global__ void __launch_bounds__(kT, 1) clip_aggregate_fused_kernel(const Args 
   __shared__ uint32_t tmem_base;
   __shared__ double red[2][kGroup / 32];  // norm partials per warp, double-buffered by client parity
   __shared__ float s_cf;
-  __shared__ int acc_done;                 // clients fully accumulated by this CTA (atomic access)
+  __shared__ int acc_done;                 // clients fully accumulated by this CTA (acquire / release access)
 
   const int G = gridDim.x, b = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -249,7 +261,7 @@ __global__ void __launch_bounds__(kT, 1) clip_aggregate_fused_kernel(const Args 
     for (int k = 0; k < a.C; ++k) {
       if (k > a.lead) {
         const long long t0 = clock64();
-        while (atomicAdd(&acc_done, 0) < k - a.lead) {
+        while (ld_acquire_cta(&acc_done) < k - a.lead) {
           __nanosleep(32);
           if (clock64() - t0 > kSpinLimit) __trap();  // a lost peer must fail loudly, never hang
         }
@@ -268,7 +280,9 @@ __global__ void __launch_bounds__(kT, 1) clip_aggregate_fused_kernel(const Args 
             ss1 += sq4(mask_tail(st[r * (kRowF / 4) + kGroup + gt], colB + ro, a.D));
           }
         }
+#ifdef FB_RING_PROXY_FENCE
         tc::fence_proxy_async();  // (generic reads of the slot ordered before the next bulk write)
+#endif
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&norm_empty[slot]);
       }
@@ -419,7 +433,9 @@ __global__ void __launch_bounds__(kT, 1) clip_aggregate_fused_kernel(const Args 
             }
           }
         }
+#ifdef FB_RING_PROXY_FENCE
         tc::fence_proxy_async();
+#endif
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&acc_empty[slot]);
       }
@@ -427,7 +443,7 @@ __global__ void __launch_bounds__(kT, 1) clip_aggregate_fused_kernel(const Args 
       // clients 0..k accumulated: flush a full fp32 block into the fp64 accumulator
       if (((k + 1) % kFlush) == 0 && k + 1 < a.C) flush_or_emit(false, k + 1 == kFlush);
       bar_group(2);  // (all of this group is done with client k and with s_cf)
-      if (gt == 0) atomicExch(&acc_done, k + 1);
+      if (gt == 0) st_release_cta(&acc_done, k + 1);
     }
     // epilogue: agg (+)= fp64 block sum + the open fp32 block
     flush_or_emit(true, false);
