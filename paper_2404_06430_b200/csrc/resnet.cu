@@ -858,7 +858,34 @@ __global__ void sgd_kernel(float* __restrict__ Wc, const float* __restrict__ Gr,
   const float* g = Gr + (int64_t)w * sW;
   float* dl = Dl + (int64_t)c * ldD;
   const float* ct = control ? control + (int64_t)c * ldc : nullptr;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < D; i += (int64_t)gridDim.x * blockDim.x) {
+  // 16-byte path over the aligned prefix when every row is 16-byte aligned (scalar tail); the
+  // same arithmetic per element
+  const auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  int64_t i0 = 0;  // first element of the scalar tail
+  if (a16(W) && a16(g) && a16(dl) && (!ct || a16(ct))) {
+    i0 = D & ~(int64_t)3;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (D >> 2); i += (int64_t)gridDim.x * blockDim.x) {
+      const float4 gv = reinterpret_cast<const float4*>(g)[i];
+      float4 dv = reinterpret_cast<float4*>(dl)[i];
+      float4 wv = reinterpret_cast<float4*>(W)[i];
+      const float4 cv = ct ? reinterpret_cast<const float4*>(ct)[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float gs[4] = {gv.x, gv.y, gv.z, gv.w}, cs[4] = {cv.x, cv.y, cv.z, cv.w};
+      float* dp4 = &dv.x;
+      float* wp4 = &wv.x;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float x = gs[e];
+        if (mu != 0.f) x = fmaf(mu, -dp4[e], x);
+        if (ct) x += cs[e];
+        x *= lr;
+        wp4[e] -= x;
+        dp4[e] += x;
+      }
+      reinterpret_cast<float4*>(W)[i] = wv;
+      reinterpret_cast<float4*>(dl)[i] = dv;
+    }
+  }
+  for (int64_t i = i0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < D; i += (int64_t)gridDim.x * blockDim.x) {
     float s = g[i];
     if (mu != 0.f) s = fmaf(mu, -dl[i], s);
     if (ct) s += ct[i];
