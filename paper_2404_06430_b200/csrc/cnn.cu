@@ -3857,18 +3857,25 @@ bool g_conv1_bwd_ffma = false;
 // staged a1 tile {32 ci, 30 x, 10 y} serves all nine taps -- the M = 128
 // operand for row ky is four 32-channel blocks at LBO = one 64-byte row
 // (kx = 0..3, the kx = 3 block discarded) starting at row ky*30.  A K block
-// = 8 output rows = 240 positions = 15 MMAs of K = 16; each K block starts
+// = 7 output rows = 210 positions = 14 MMAs of K = 16 (the last 14 positions
+// against zero dz2 rows; 8-row blocks left 4 of 32 rows empty); each K block starts
 // fresh TMEM accumulators per ky (hi*hi and cross terms separately), drained
 // by eight epilogue warps into fp32 registers with the per-sample unscale.
 constexpr int BW_PART = 3 * 64 * 96;  // floats per split partial of conv2_bwd_w_tc ([ky][o][kx*32+ci])
-constexpr int BW_ROWS = 8;                        // output rows per K block
+#ifndef BW_ROWS
+#define BW_ROWS 7  // output rows per K block: 4 x 7 = the 28 rows exactly (8 rows left 4 of 32 empty)
+#endif
 constexpr int BW_NKB = (S2 + BW_ROWS - 1) / BW_ROWS;  // 4 K blocks per sample
 static_assert(BW_NKB % 2 == 0, "conv2 weight gradient drains pairs of K blocks of one sample");
-constexpr int BW_KPOS = BW_ROWS * S1;             // 240 positions
-constexpr int BW_A_ROWS = 304;                    // a1 tile rows (300 loaded + 4 zero)
-constexpr int BW_A_BYTES = BW_A_ROWS * 64;        // 19456
-constexpr int BW_A_TX = (BW_ROWS + 2) * S1 * 64;  // 19200
-constexpr int BW_B_BYTES = BW_KPOS * 128;         // 30720
+constexpr int BW_KPOS = BW_ROWS * S1;             // 210 positions loaded per K block
+constexpr int BW_KSTEPS = (BW_KPOS + 15) / 16;    // 14 MMAs of K = 16 (positions 210..223: zero dz2 rows)
+// a1 rows the taps read: ky * 30 + 16 * BW_KSTEPS + kx (kx <= 3), rounded to 16 rows (1 KB)
+constexpr int BW_A_ROWS = ((2 * S1 + 16 * BW_KSTEPS + 3) + 15) / 16 * 16;
+constexpr int BW_A_BYTES = BW_A_ROWS * 64;
+constexpr int BW_A_TX = (BW_ROWS + 2) * S1 * 64;  // a1 bytes the TMA writes (the rest stays zero)
+constexpr int BW_B_TX = BW_KPOS * 128;            // dz2 bytes the TMA writes per part
+constexpr int BW_B_BYTES = BW_KSTEPS * 16 * 128;  // dz2 tile per part (the rows past BW_KPOS stay zero)
+static_assert(BW_A_ROWS * 64 >= BW_A_TX && BW_B_BYTES % 1024 == 0 && BW_A_BYTES % 1024 == 0, "bwd-w tiles");
 constexpr int BW_STAGE = 2 * BW_A_BYTES + 2 * BW_B_BYTES;  // 100352
 constexpr int BW_STAGES = 2;
 constexpr int BW_EPI_WARPS = 16;                  // 4 lane quarters x 4 groups of 16 output channels
@@ -3902,11 +3909,17 @@ __global__ void __launch_bounds__(BW_THREADS, 1) conv2_bwd_w_tc_kernel(
   const int b0 = part * nbc / split, b1 = (part + 1) * nbc / split;
   if (b1 <= b0) return;
   const int nblocks = (b1 - b0) * BW_NKB;
-  for (int s = 0; s < BW_STAGES; ++s)  // a1 rows 300..303 are read against zero dz2 rows: keep them finite
+  for (int s = 0; s < BW_STAGES; ++s) {  // a1 rows past the TMA box are read against zero dz2: keep them finite
     for (int i = threadIdx.x; i < (BW_A_BYTES - BW_A_TX) / 4; i += blockDim.x) {
       reinterpret_cast<float*>(sm + s * BW_STAGE + BW_A_TX)[i] = 0.f;
       reinterpret_cast<float*>(sm + s * BW_STAGE + BW_A_BYTES + BW_A_TX)[i] = 0.f;
     }
+    // dz2 positions past the K block (the last MMA's tail) must be zero: they are never loaded
+    for (int i = threadIdx.x; i < (BW_B_BYTES - BW_B_TX) / 4; i += blockDim.x) {
+      reinterpret_cast<float*>(sm + s * BW_STAGE + 2 * BW_A_BYTES + BW_B_TX)[i] = 0.f;
+      reinterpret_cast<float*>(sm + s * BW_STAGE + 2 * BW_A_BYTES + BW_B_BYTES + BW_B_TX)[i] = 0.f;
+    }
+  }
   tc::fence_proxy_async();
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < BW_STAGES; ++i) {
@@ -3936,7 +3949,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1) conv2_bwd_w_tc_kernel(
       for (int blk = 0; blk < nblocks; ++blk) {
         const int n = c * B + b0 + blk / BW_NKB, y0 = BW_ROWS * (blk % BW_NKB);
         tc::mbar_wait(&empty[stage], phase ^ 1);
-        tc::mbar_arrive_expect_tx(&full[stage], 2 * BW_A_TX + 2 * BW_B_BYTES);
+        tc::mbar_arrive_expect_tx(&full[stage], 2 * BW_A_TX + 2 * BW_B_TX);
         uint8_t* st_ = sm + stage * BW_STAGE;
         tc::tma_load_4d(st_, &ta_hi, 0, 0, y0, n, &full[stage]);
         tc::tma_load_4d(st_ + BW_A_BYTES, &ta_lo, 0, 0, y0, n, &full[stage]);
@@ -3955,7 +3968,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1) conv2_bwd_w_tc_kernel(
       const uint32_t ah = s0 + stage * BW_STAGE, al = ah + BW_A_BYTES;
       const uint32_t bh = ah + 2 * BW_A_BYTES;  // dz2 lo follows at + BW_B_BYTES
       // accumulators are drained once per PAIR of blocks (same sample: BW_NKB is even), a
-      // 30-step main chain per drain (<= 36: as accurate as fp32, tools/microbench)
+      // 28-step main chain per drain (<= 36: as accurate as fp32, tools/microbench)
       const bool first = (blk & 1) == 0, last = (blk & 1) == 1;
       for (int ky = 0; ky < 3; ++ky) {
         if (first) {
@@ -3965,7 +3978,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1) conv2_bwd_w_tc_kernel(
         if (tc::elect_one()) {
           const uint32_t dm = tmem + ky * 2 * C2, dx = dm + C2;
 #pragma unroll 5
-          for (int ks = 0; ks < BW_KPOS / 16; ++ks) {
+          for (int ks = 0; ks < BW_KSTEPS; ++ks) {
             const uint32_t arow = ky * S1 + ks * 16;
             const uint64_t adh = tc::sdesc(ah + arow * 64, 64, 512, 4);
             const uint64_t adl = tc::sdesc(al + arow * 64, 64, 512, 4);
