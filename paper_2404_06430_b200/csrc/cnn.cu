@@ -489,25 +489,35 @@ __global__ void __launch_bounds__(HID) head_kernel(const float* __restrict__ par
       }
     }
   }
+  // the K-split partials of two rows at a time: 14 loads in flight, each row summed in split
+  // order (bf1 first) -- the same additions as one row at a time
 #pragma unroll
-  for (int b = 0; b < GMAX; ++b) {
+  for (int b = 0; b < GMAX; b += 2) {
     if (b >= G) break;
-    const int n = n0 + b;
-    float z = 0.f;
-    if (n < N && slot_row[n] >= 0) {
-      // the K-split partials: loads issued 7 at a time, summed in split order
-      z = bf1;
-      int s = 0;
-      for (; s + 7 <= nsplit; s += 7) {
-        float v[7];
+    const int na = n0 + b, nb2 = n0 + b + 1;
+    const bool va = na < N && slot_row[na] >= 0;
+    const bool vb = b + 1 < G && nb2 < N && slot_row[nb2] >= 0;
+    float za = va ? bf1 : 0.f, zb = vb ? bf1 : 0.f;
+    int s = 0;
+    for (; s + 7 <= nsplit; s += 7) {
+      float v[7], w[7];
 #pragma unroll
-        for (int u = 0; u < 7; ++u) v[u] = part[((int64_t)(s + u) * N + n) * HID + j];
-#pragma unroll
-        for (int u = 0; u < 7; ++u) z += v[u];
+      for (int u = 0; u < 7; ++u) {
+        v[u] = va ? part[((int64_t)(s + u) * N + na) * HID + j] : 0.f;
+        w[u] = vb ? part[((int64_t)(s + u) * N + nb2) * HID + j] : 0.f;
       }
-      for (; s < nsplit; ++s) z += part[((int64_t)s * N + n) * HID + j];
+#pragma unroll
+      for (int u = 0; u < 7; ++u) {
+        za += v[u];
+        zb += w[u];
+      }
     }
-    z3[b][j] = z - corr[b];
+    for (; s < nsplit; ++s) {
+      if (va) za += part[((int64_t)s * N + na) * HID + j];
+      if (vb) zb += part[((int64_t)s * N + nb2) * HID + j];
+    }
+    z3[b][j] = za - corr[b];
+    if (b + 1 < G) z3[b + 1][j] = zb - corr[b + 1];
   }
   if (j < G) {
     const int n = n0 + j;
